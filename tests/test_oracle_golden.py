@@ -1,0 +1,75 @@
+"""Pin the numpy oracle to vectors produced by the real reference package."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import load_cases
+
+
+def _bl(c):
+    return O.BoxLine(c["a"], c["d"], c["l"], c["u"])
+
+
+def test_projection_matches_reference():
+    for c in load_cases("projection.npz", "p"):
+        bl = _bl(c)
+        x, lam, free = O.project(c["v"], bl)
+        scale = 1.0 + np.abs(c["x"]).max()
+        assert np.abs(x - c["x"]).max() <= 1e-12 * scale
+        assert abs(lam - c["lam"]) <= 1e-12 * (1.0 + abs(c["lam"]))
+        np.testing.assert_array_equal(free.astype(np.uint8), c["free"])
+        np.testing.assert_array_equal(O.breakpoints(c["v"], bl), c["bp"])
+        assert O.grad_phi(0.0, c["v"], bl) == pytest.approx(c["gphi0"], rel=1e-12, abs=1e-12)
+
+
+def test_hs_jacobian_matches_reference():
+    for c in load_cases("hs_jacobian.npz", "h"):
+        py = O.hs_apply(c["free"].astype(bool), c["a"], c["y"])
+        np.testing.assert_allclose(py, c["py"], rtol=0, atol=1e-13)
+
+
+def test_newton_direction_matches_reference():
+    for c in load_cases("newton.npz", "n"):
+        q = c["G"].T @ c["G"]
+        op = O.DenseQ(q)
+        bl = _bl(c)
+        sigma = c["sigma"]
+        u = c["x"] - sigma * (q @ c["w"] + c["c"])
+        x, lam, free = O.project(u, bl)
+        np.testing.assert_array_equal(free.astype(np.uint8), c["free"])
+        s = c["w"] - x
+        d, qd, dqd = O.newton_direction(s, q @ s, free, sigma, op, bl.a, O.SsnOpts())
+        sc = 1.0 + np.linalg.norm(c["qdir"])
+        assert np.linalg.norm(qd - c["qdir"]) <= 1e-9 * sc
+        assert abs(dqd - c["dqd"]) <= 1e-9 * (1.0 + abs(c["dqd"]))
+
+
+def test_kkt_residual_matches_reference():
+    for c in load_cases("kkt.npz", "k"):
+        op = O.DenseQ(c["G"].T @ c["G"])
+        r = O.kkt_residual(c["x"], op, c["c"], _bl(c))
+        assert r == pytest.approx(c["kkt"], rel=1e-12)
+
+
+def _problem(c):
+    if c["kind"] == "dense":
+        return O.DenseQ(c["G"].T @ c["G"]), c["c"], _bl(c)
+    if c["kind"] == "csvc":
+        return O.csvc_problem(c["A"], c["y"], c["C"])
+    return O.svr_problem(c["A"], c["t"], c["C"], c["eps"])
+
+
+def test_alm_solve_matches_reference():
+    for c in load_cases("solve.npz", "s"):
+        op, cc, bl = _problem(c)
+        rep = O.alm_solve(op, cc, bl, O.AlmOpts(tol_kkt=c["tol"]))
+        assert rep["converged"] == bool(c["converged"])
+        if c["converged"]:
+            assert rep["kkt_residual"] < c["tol"]
+        assert rep["objective"] == pytest.approx(c["obj"], rel=1e-6, abs=1e-9)
+        if c["kind"] == "dense":  # same operator arithmetic => same iterates, bit for bit
+            assert rep["kkt_residual"] == c["kkt"]
+            assert (rep["outer_iters"], rep["total_inner_iters"]) == (c["outer"], c["inner"])
+        x_ref = c["x_opt"]
+        assert np.linalg.norm(rep["x_opt"] - x_ref) <= 1e-4 * (1 + np.linalg.norm(x_ref))
