@@ -1,0 +1,145 @@
+/*
+ * ssnal_b200.h -- C-ABI of the B200 (sm_100a) SSsNAL hot path.
+ *
+ * Drop-in boundary for the reference package ``ssnal`` (arXiv 1910.01312,
+ * /root/reference/pkg/src/ssnal).  Every entry point names the reference
+ * interface it replaces.  Conventions:
+ *   - all array arguments are DEVICE pointers (fp64 unless stated), sizes are
+ *     int64_t, `stream` is a cudaStream_t passed as void*;
+ *   - every call is asynchronous on `stream` and returns 0 on success or a
+ *     nonzero code (cudaError_t or SSNAL_E_*); ssnal_last_error() describes it;
+ *   - "logical rows": the data operator is X = S (diag(row_sign) A) with A the
+ *     row-major n_phys x q sample matrix (leading dimension lda), row_sign an
+ *     optional +-1 label vector (C-SVC: X = diag(y) A) and S = [I] or, with
+ *     svr_block = 1, S = [I; -I] (eps-SVR: X = [A; -A], 2 n_phys logical rows).
+ *     Q = X X^T is never formed (ref kernels.py:68-154 forms its columns).
+ *   - every reduction is a fixed-order tree: results are bit-reproducible.
+ * No entry point has a CPU fallback.
+ */
+#ifndef SSNAL_B200_H
+#define SSNAL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSNAL_OK 0
+#define SSNAL_E_ARG 1001      /* invalid argument */
+#define SSNAL_E_DEVICE 1002   /* no sm_100 device / wrong architecture */
+
+/* Device-resident record of one projection (one per batched trial). */
+typedef struct ssnal_proj_state_t {
+  double lo, hi, flo, fhi;        /* current bracket in lambda and phi' values there   */
+  double below_max, above_min;    /* nearest breakpoints outside the bracket           */
+  double in_min, in_max;          /* extreme breakpoints inside (lo, hi]               */
+  long long in_count;             /* breakpoints inside (lo, hi]                       */
+  double lam;                     /* equality multiplier lambda-hat (ref lambda_hat)   */
+  double tmin, tmax;              /* breakpoint range                                   */
+  double sum_v2;                  /* sum v_i^2                                          */
+  double sum_r2;                  /* sum (v_i - x_i)^2                                  */
+  double sum_dref2;               /* sum (x_i - ref_i)^2 (ref optional)                 */
+  double sum_a2_free;             /* a_J' a_J over the free set (a' Sigma a)            */
+  long long nfree;                /* p = |J|                                            */
+  int status;                     /* 3 applied, 2 lambda known, <0 infeasible, else searching */
+  int passes;                     /* K-ary bracketing passes used                       */
+  unsigned int ticket;            /* internal: last-block-done counter (keep zeroed)    */
+  unsigned int pad_;
+} ssnal_proj_state_t;
+
+/* ---- library / device ------------------------------------------------- */
+const char* ssnal_version(void);
+const char* ssnal_last_error(void);
+int ssnal_device_check(int device);                 /* SSNAL_E_DEVICE unless sm_100 */
+size_t ssnal_proj_state_bytes(void);
+size_t ssnal_project_ws_bytes(int64_t n, int T);
+size_t ssnal_reduce_ws_bytes(int64_t n, int k);
+size_t ssnal_dense_xt_ws_bytes(int64_t n_phys, int64_t q, int k);
+size_t ssnal_gram_ws_bytes(int64_t q);
+size_t ssnal_compact_ws_bytes(int64_t n);
+
+/* ---- projection onto {x : a'x = d, l <= x <= u} ------------------------
+ * Replaces ref projection.py:152-211 project_box_line (+ :134-149 _classify).
+ * Projects T <= 16 vectors v_t = A - coef[t] * B (B may be NULL; coef is a HOST
+ * array of T doubles, passed by value to the kernels), each trial t writing state[t] and, when non-NULL,
+ * x_out[t*n..] (projection), free_out[t*n..] (uint8 free-set mask Sigma) and
+ * the fused sums of ssnal_proj_state_t.  l or u NULL => the scalar l_const /
+ * u_const bound for every slot.  phases: bit0 range, bit1 exact, bit2 apply;
+ * `passes` K-ary bracketing passes are launched between range and exact (a
+ * pass after convergence is a no-op).  state[t].status == 3 on completion; 0/1
+ * means more passes are needed (call again with phases = 6). */
+int ssnal_project(const double* A, const double* B, const double* coef,
+                  const double* a, const double* l, const double* u,
+                  double l_const, double u_const, double d, int64_t n, int T,
+                  ssnal_proj_state_t* state, void* ws,
+                  double* x_out, uint8_t* free_out, const double* ref,
+                  int phases, int passes, void* stream);
+
+/* ---- HS-Jacobian -------------------------------------------------------
+ * Replaces ref projection.py:214-225 hs_jacobian_apply.
+ * out = alpha * add + beta * P y,  P = S (I - a a'/(a'Sa)) S (or S if a'Sa = 0),
+ * S = diag(free).  add may be NULL.  ws: ssnal_reduce_ws_bytes(n, 2). */
+int ssnal_hs_apply(const uint8_t* free_mask, const double* a, const double* y, int64_t n,
+                   double beta, const double* add, double alpha, double* out,
+                   void* ws, void* stream);
+
+/* ---- fused dot products ------------------------------------------------
+ * out[j] = sum_i m_i x_j[i] y_j[i], j < k <= 8 (y_j NULL => x_j^2; mask NULL =>
+ * all ones).  xs / ys are HOST arrays of k device pointers.  Used for the
+ * norms and inner products of ref solver.py:130-148, 303-309, 353-358. */
+int ssnal_dots(int k, const double* const* xs, const double* const* ys,
+               const uint8_t* mask, int64_t n, double* out, void* ws, void* stream);
+
+/* ---- elementwise vector ops (numpy rounding order) ----------------------
+ * op 0: out = x + alpha * (y + z)   (z may be NULL)  -- u(w) = x - sigma (Qw + c)
+ * op 1: out = (x - y) - z                            -- x - Qx - c (KKT map)
+ * op 2: out = x + alpha * y                          -- w + alpha d, Qw + alpha Qd
+ * op 3: out = x - y                                  -- s(w) = w - Pi(u(w))
+ * op 4: out = alpha * x                              */
+int ssnal_vec(int op, int64_t n, double alpha, const double* x, const double* y,
+              const double* z, double* out, void* stream);
+
+/* ---- dense data operator (Q = X X^T) -----------------------------------
+ * ssnal_dense_xt: out[:, j] = X^T v_j for the k <= 4 logical-length vectors
+ *   vs[j] (HOST array of device pointers); out is q x k column-major.
+ *   Replaces the X^T half of ref kernels.py:144-154 KernelOperator.matvec.
+ * ssnal_dense_x: out[:, j] = X d_j, d q x k column-major, out n_log x k.
+ *   The X half of the same matvec, and the Q-image products of
+ *   ref solver.py:260-262 (cols @ v).                                       */
+int ssnal_dense_xt(const double* A, int64_t n_phys, int64_t q, int64_t lda,
+                   const double* row_sign, int svr_block, int k, const double* const* vs,
+                   double* out, void* ws, void* stream);
+int ssnal_dense_x(const double* A, int64_t n_phys, int64_t q, int64_t lda,
+                  const double* row_sign, int svr_block, int k, const double* d,
+                  double* out, void* stream);
+
+/* ---- reduced Newton system (Prop. 3.5 in factor space) ------------------
+ * ssnal_compact: ascending indices of nonzero mask entries (the free set J)
+ *   into idx (int32), count into *count (DEVICE int64).  ref: np.flatnonzero
+ *   in projection.py:144-148.
+ * ssnal_dense_gram: M = I + sigma (G - m1 m1'/asa) (or I + sigma G when asa = 0)
+ *   with G = X_J^T X_J (fp64 tensor cores, DMMA) and m1 = X_J^T a_J over the
+ *   *p_dev (DEVICE count, <= p_max) logical rows J; *asa_dev is a'Sigma a (DEVICE
+ *   scalar, e.g. state.sum_a2_free).  No host synchronisation is needed.
+ *   This is the q x q matrix I_r + sigma L^T Sigma (I - aa'/(a'Sa)) Sigma L of
+ *   the paper's Prop. 3.5 proof, which replaces the p x p system assembled in
+ *   ref solver.py:232-258.  M is q x q row-major (symmetric).
+ * ssnal_chol_solve: in-place Cholesky of the SPD m x m matrix M (lower factor)
+ *   and x = scale * M^{-1} b; *info (DEVICE int) = 0 or the failing column+1. */
+int ssnal_compact(const uint8_t* mask, int64_t n, int32_t* idx, int64_t* count,
+                  void* ws, void* stream);
+int ssnal_dense_gram(const double* A, int64_t n_phys, int64_t q, int64_t lda,
+                     const double* row_sign, int svr_block,
+                     const int32_t* J, const int64_t* p_dev, int64_t p_max, const double* a,
+                     double sigma, const double* asa_dev, double* M, double* m1,
+                     void* ws, void* stream);
+int ssnal_chol_solve(double* M, int64_t m, const double* b, double scale, double* x,
+                     int* info, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SSNAL_B200_H */

@@ -1,0 +1,99 @@
+"""ctypes binding of the sm_100a C-ABI library (include/ssnal_b200.h).
+
+There is deliberately no fallback: a missing library or a non-sm_100 device
+raises CudaUnavailableError.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import CudaUnavailableError, InternalError
+
+LIB_NAME = "_ssnal_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+# numpy view of ssnal_proj_state_t (checked against ssnal_proj_state_bytes())
+PROJ_STATE_DTYPE = np.dtype([
+    ("lo", "f8"), ("hi", "f8"), ("flo", "f8"), ("fhi", "f8"),
+    ("below_max", "f8"), ("above_min", "f8"), ("in_min", "f8"), ("in_max", "f8"),
+    ("in_count", "i8"), ("lam", "f8"), ("tmin", "f8"), ("tmax", "f8"),
+    ("sum_v2", "f8"), ("sum_r2", "f8"), ("sum_dref2", "f8"), ("sum_a2_free", "f8"),
+    ("nfree", "i8"), ("status", "i4"), ("passes", "i4"), ("ticket", "u4"), ("pad_", "u4"),
+])
+
+PROJ_SEARCH, PROJ_BRACKETED, PROJ_DONE, PROJ_APPLIED = 0, 1, 2, 3
+PROJ_INFEASIBLE_LOW, PROJ_INFEASIBLE_HIGH = -1, -2
+PHASE_RANGE, PHASE_EXACT, PHASE_APPLY = 1, 2, 4
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+_D = ctypes.c_double
+_SZ = ctypes.c_size_t
+
+# name -> (restype, argtypes)
+_SIGNATURES = {
+    "ssnal_version": (ctypes.c_char_p, []),
+    "ssnal_last_error": (ctypes.c_char_p, []),
+    "ssnal_device_check": (_I, [_I]),
+    "ssnal_proj_state_bytes": (_SZ, []),
+    "ssnal_project_ws_bytes": (_SZ, [_I64, _I]),
+    "ssnal_reduce_ws_bytes": (_SZ, [_I64, _I]),
+    "ssnal_dense_xt_ws_bytes": (_SZ, [_I64, _I64, _I]),
+    "ssnal_gram_ws_bytes": (_SZ, [_I64]),
+    "ssnal_compact_ws_bytes": (_SZ, [_I64]),
+    "ssnal_project": (_I, [_P, _P, _P, _P, _P, _P, _D, _D, _D, _I64, _I, _P, _P, _P, _P, _P,
+                           _I, _I, _P]),
+    "ssnal_hs_apply": (_I, [_P, _P, _P, _I64, _D, _P, _D, _P, _P, _P]),
+    "ssnal_dots": (_I, [_I, _P, _P, _P, _I64, _P, _P, _P]),
+    "ssnal_vec": (_I, [_I, _I64, _D, _P, _P, _P, _P, _P]),
+    "ssnal_dense_xt": (_I, [_P, _I64, _I64, _I64, _P, _I, _I, _P, _P, _P, _P]),
+    "ssnal_dense_x": (_I, [_P, _I64, _I64, _I64, _P, _I, _I, _P, _P, _P]),
+    "ssnal_compact": (_I, [_P, _I64, _P, _P, _P, _P]),
+    "ssnal_dense_gram": (_I, [_P, _I64, _I64, _I64, _P, _I, _P, _P, _I64, _P, _D, _P, _P, _P,
+                              _P, _P]),
+    "ssnal_chol_solve": (_I, [_P, _I64, _P, _D, _P, _P, _P]),
+}
+
+_lib = None
+
+
+def exported_symbols():
+    return tuple(_SIGNATURES)
+
+
+def load():
+    """Load (once) and type the library; raises CudaUnavailableError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise CudaUnavailableError(
+            f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.ssnal_proj_state_bytes() != PROJ_STATE_DTYPE.itemsize:
+        raise InternalError("ssnal_proj_state_t layout mismatch between C and Python")
+    _lib = lib
+    return lib
+
+
+def call(name, *args):
+    """Invoke an entry point and raise on a nonzero status."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.ssnal_last_error().decode(errors="replace")
+        raise InternalError(f"{name} failed ({rc}): {msg}")
+
+
+def ptr_array(ptrs):
+    """HOST array of device pointers for the const double* const* arguments."""
+    arr = (ctypes.c_void_p * len(ptrs))(*[ctypes.c_void_p(p) if p else None for p in ptrs])
+    return ctypes.cast(arr, ctypes.c_void_p), arr

@@ -1,0 +1,175 @@
+"""CUDA backend: thin typed wrappers over the C-ABI, operating on torch tensors.
+
+torch supplies device memory and the current stream only; every arithmetic
+operation of the SSsNAL path runs in the sm_100a library.  All calls are
+asynchronous on torch's current stream; ``fetch_*`` helpers are the only
+host synchronisation points.
+"""
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import CudaUnavailableError, InputError
+
+F64 = torch.float64
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+class CudaBackend:
+    """One per device.  Owns no problem-sized buffers (see solver.Workspace)."""
+
+    name = "cuda"
+
+    def __init__(self, device=None):
+        if not torch.cuda.is_available():
+            raise CudaUnavailableError("no CUDA device visible (there is no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        self.lib = _lib.load()
+        _lib.call("ssnal_device_check", self.device.index)
+        self._ws = {}
+
+    # ---------------------------------------------------------------- memory
+    def empty(self, shape, dtype=F64):
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def zeros(self, shape, dtype=F64):
+        return torch.zeros(shape, dtype=dtype, device=self.device)
+
+    def ws(self, key, nbytes):
+        """Zero-initialised scratch (tickets inside must start at 0), grown on demand."""
+        buf = self._ws.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=self.device)
+            self._ws[key] = buf
+        return buf
+
+    def stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def synchronize(self):
+        torch.cuda.current_stream(self.device).synchronize()
+
+    @staticmethod
+    def host_buffer(shape, dtype):
+        return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+    def new_states(self, T):
+        return torch.zeros((T, _lib.PROJ_STATE_DTYPE.itemsize), dtype=torch.uint8,
+                           device=self.device)
+
+    @staticmethod
+    def read_states(states_host):
+        return states_host.numpy().view(_lib.PROJ_STATE_DTYPE).reshape(-1)
+
+    # ---------------------------------------------------------------- projection
+    def project(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
+                ref=None, phases=7, passes=6):
+        n = box.n
+        coef_arr = None
+        if B is not None:
+            coef_arr = (_lib.ctypes.c_double * T)(*[float(c) for c in coefs])
+        ws = self.ws("proj", self.lib.ssnal_project_ws_bytes(n, T))
+        _lib.call(
+            "ssnal_project", _ptr(A), _ptr(B),
+            _lib.ctypes.cast(coef_arr, _lib.ctypes.c_void_p) if coef_arr is not None else None,
+            _ptr(box.a_dev), _ptr(box.l_dev), _ptr(box.u_dev), box.l_const, box.u_const, box.d,
+            n, T, _ptr(states), _ptr(ws), _ptr(x_out), _ptr(free_out), _ptr(ref),
+            phases, passes, self.stream())
+
+    def project_sync(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
+                     ref=None):
+        """Project and return the host copy of the T state records (one sync,
+        plus a rare extra round if a trial needed more bracketing passes)."""
+        self.project(A, box, states, T, B, coefs, x_out, free_out, ref)
+        st = self.read_states(states[:T].cpu())
+        extra = 0
+        while np.any((st["status"] == _lib.PROJ_SEARCH) | (st["status"] == _lib.PROJ_BRACKETED)):
+            extra += 1
+            if extra > 20:
+                raise RuntimeError("projection failed to bracket the multiplier")
+            self.project(A, box, states, T, B, coefs, x_out, free_out, ref,
+                         phases=_lib.PHASE_EXACT | _lib.PHASE_APPLY, passes=8)
+            st = self.read_states(states[:T].cpu())
+        return st
+
+    # ---------------------------------------------------------------- vectors
+    def dots(self, pairs, out, mask=None):
+        """out[j] = sum m x_j y_j (y None => x^2); pairs <= 8; async."""
+        k = len(pairs)
+        n = pairs[0][0].numel()
+        xs, keep1 = _lib.ptr_array([_ptr(x) for x, _ in pairs])
+        ys, keep2 = _lib.ptr_array([_ptr(y) for _, y in pairs])
+        ws = self.ws("reduce", self.lib.ssnal_reduce_ws_bytes(n, k))
+        _lib.call("ssnal_dots", k, xs, ys, _ptr(mask), n, _ptr(out), _ptr(ws), self.stream())
+        del keep1, keep2
+
+    def vec(self, op, alpha, x, y, z, out):
+        _lib.call("ssnal_vec", op, x.numel(), float(alpha), _ptr(x), _ptr(y), _ptr(z),
+                  _ptr(out), self.stream())
+
+    def hs_apply(self, free, a, y, beta, add, alpha, out):
+        n = y.numel()
+        ws = self.ws("hs", self.lib.ssnal_reduce_ws_bytes(n, 2))
+        _lib.call("ssnal_hs_apply", _ptr(free), _ptr(a), _ptr(y), n, float(beta), _ptr(add),
+                  float(alpha), _ptr(out), _ptr(ws), self.stream())
+
+    def compact(self, mask, idx_out, count_out):
+        n = mask.numel()
+        ws = self.ws("compact", self.lib.ssnal_compact_ws_bytes(n))
+        _lib.call("ssnal_compact", _ptr(mask), n, _ptr(idx_out), _ptr(count_out), _ptr(ws),
+                  self.stream())
+
+    # ---------------------------------------------------------------- dense operator
+    def dense_xt(self, op, vs, out):
+        k = len(vs)
+        arr, keep = _lib.ptr_array([_ptr(v) for v in vs])
+        ws = self.ws("xt", self.lib.ssnal_dense_xt_ws_bytes(op.n_phys, op.q, k))
+        _lib.call("ssnal_dense_xt", _ptr(op.A), op.n_phys, op.q, op.lda, _ptr(op.row_sign),
+                  int(op.svr_block), k, arr, _ptr(out), _ptr(ws), self.stream())
+        del keep
+
+    def dense_x(self, op, d, out, k=1):
+        _lib.call("ssnal_dense_x", _ptr(op.A), op.n_phys, op.q, op.lda, _ptr(op.row_sign),
+                  int(op.svr_block), k, _ptr(d), _ptr(out), self.stream())
+
+    def dense_gram(self, op, J, p_dev, p_max, a, sigma, asa_dev, M, m1):
+        ws = self.ws("gram", self.lib.ssnal_gram_ws_bytes(op.q))
+        _lib.call("ssnal_dense_gram", _ptr(op.A), op.n_phys, op.q, op.lda, _ptr(op.row_sign),
+                  int(op.svr_block), _ptr(J), _ptr(p_dev), int(p_max), _ptr(a), float(sigma),
+                  _ptr(asa_dev), _ptr(M), _ptr(m1), _ptr(ws), self.stream())
+
+    def chol_solve(self, M, m, b, scale, x, info):
+        _lib.call("ssnal_chol_solve", _ptr(M), int(m), _ptr(b), float(scale), _ptr(x),
+                  _ptr(info), self.stream())
+
+
+_DEFAULT = {}
+
+
+def default_backend(device=None):
+    key = str(device)
+    if key not in _DEFAULT:
+        _DEFAULT[key] = CudaBackend(device)
+    return _DEFAULT[key]
+
+
+def as_device(x, backend, dtype=F64):
+    """Host (numpy / list / CPU tensor) or device tensor -> contiguous device tensor."""
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=backend.device, dtype=dtype)
+    else:
+        arr = np.asarray(x, dtype=np.float64 if dtype == F64 else None)
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(device=backend.device, dtype=dtype)
+    if not t.is_contiguous():
+        t = t.contiguous()
+    return t
+
+
+def check_vector(v, n, what):
+    if v.dim() != 1 or v.numel() != n:
+        raise InputError(f"{what}: expected a vector of length {n}, got shape {tuple(v.shape)}")

@@ -1,0 +1,163 @@
+// extern "C" entry points of include/ssnal_b200.h: argument checks, launch, error text.
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "ssnal_internal.h"
+
+namespace ssnal {
+int stream_blocks(long long n, int per_thread);
+size_t reduce_ws_bytes(long long n);
+size_t compact_ws_bytes(long long n);
+size_t dense_xt_ws_bytes(long long n_phys, long long q, int k);
+size_t gram_ws_bytes(long long q);
+cudaError_t launch_dots(int k, const double* const* xs, const double* const* ys,
+                        const uint8_t* mask, long long n, double* out, void* ws, cudaStream_t s);
+cudaError_t launch_vec(int op, long long n, double alpha, const double* x, const double* y,
+                       const double* z, double* out, cudaStream_t s);
+cudaError_t launch_hs_apply(const uint8_t* fm, const double* a, const double* y, long long n,
+                            double beta, const double* add, double alpha, double* out, void* ws,
+                            cudaStream_t s);
+cudaError_t launch_compact(const uint8_t* m, long long n, int32_t* idx, long long* count, void* ws,
+                           cudaStream_t s);
+cudaError_t launch_dense_xt(const double* A, long long n, long long q, long long lda,
+                            const double* rs, int svr, int k, const double* const* vs, double* out,
+                            void* ws, cudaStream_t s);
+cudaError_t launch_dense_x(const double* A, long long n, long long q, long long lda,
+                           const double* rs, int svr, int k, const double* d, double* out,
+                           cudaStream_t s);
+cudaError_t launch_dense_gram(const double* A, long long n, long long q, long long lda,
+                              const double* rs, int svr, const int32_t* J, const long long* p_dev,
+                              long long p_max, const double* a, double sigma, const double* asa_dev,
+                              double* M, double* m1, void* ws, cudaStream_t s);
+cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
+                              int* info, cudaStream_t s);
+}  // namespace ssnal
+
+using namespace ssnal;
+
+static thread_local char g_err[512] = "";
+
+static int fail_arg(const char* fn, const char* what) {
+  snprintf(g_err, sizeof g_err, "%s: invalid argument: %s", fn, what);
+  return SSNAL_E_ARG;
+}
+
+static int check(const char* fn, cudaError_t e) {
+  if (e == cudaSuccess) return SSNAL_OK;
+  snprintf(g_err, sizeof g_err, "%s: CUDA error %d (%s)", fn, (int)e, cudaGetErrorString(e));
+  return (int)e;
+}
+
+#define S(stream) ((cudaStream_t)(stream))
+
+extern "C" {
+
+const char* ssnal_version(void) { return "ssnal_b200 0.1.0 (sm_100a)"; }
+
+const char* ssnal_last_error(void) { return g_err; }
+
+int ssnal_device_check(int device) {
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return check("ssnal_device_check", e);
+  if (prop.major != 10 || prop.minor != 0) {
+    snprintf(g_err, sizeof g_err, "ssnal_device_check: device %d is sm_%d%d, library is sm_100a",
+             device, prop.major, prop.minor);
+    return SSNAL_E_DEVICE;
+  }
+  return SSNAL_OK;
+}
+
+size_t ssnal_proj_state_bytes(void) { return sizeof(ssnal_proj_state_t); }
+size_t ssnal_project_ws_bytes(int64_t n, int T) { return proj_ws_bytes(n, T); }
+size_t ssnal_reduce_ws_bytes(int64_t n, int k) { (void)k; return reduce_ws_bytes(n) + 64; }
+size_t ssnal_dense_xt_ws_bytes(int64_t n_phys, int64_t q, int k) {
+  return dense_xt_ws_bytes(n_phys, q, k);
+}
+size_t ssnal_gram_ws_bytes(int64_t q) { return gram_ws_bytes(q); }
+size_t ssnal_compact_ws_bytes(int64_t n) { return compact_ws_bytes(n); }
+
+int ssnal_project(const double* A, const double* B, const double* coef, const double* a,
+                  const double* l, const double* u, double l_const, double u_const, double d,
+                  int64_t n, int T, ssnal_proj_state_t* state, void* ws, double* x_out,
+                  uint8_t* free_out, const double* ref, int phases, int passes, void* stream) {
+  if (n < 1) return fail_arg("ssnal_project", "n < 1");
+  if (T < 1 || T > SSNAL_MAX_TRIALS) return fail_arg("ssnal_project", "T must be in [1, 16]");
+  if (!A || !a || !state || !ws) return fail_arg("ssnal_project", "null A/a/state/ws");
+  if (B && !coef) return fail_arg("ssnal_project", "B given without coef");
+  if (passes < 0) return fail_arg("ssnal_project", "passes < 0");
+  ProjLaunch L;
+  L.A = A; L.B = B; L.coef = coef; L.a = a; L.l = l; L.u = u;
+  L.lc = l_const; L.uc = u_const; L.d = d; L.n = n; L.T = T;
+  L.st = state; L.part = (double*)ws; L.x_out = x_out; L.free_out = free_out; L.ref = ref;
+  L.phases = phases; L.passes = passes;
+  return check("ssnal_project", launch_project(L, S(stream)));
+}
+
+int ssnal_hs_apply(const uint8_t* free_mask, const double* a, const double* y, int64_t n,
+                   double beta, const double* add, double alpha, double* out, void* ws,
+                   void* stream) {
+  if (n < 1 || !free_mask || !a || !y || !out || !ws) return fail_arg("ssnal_hs_apply", "null/size");
+  return check("ssnal_hs_apply",
+               launch_hs_apply(free_mask, a, y, n, beta, add, alpha, out, ws, S(stream)));
+}
+
+int ssnal_dots(int k, const double* const* xs, const double* const* ys, const uint8_t* mask,
+               int64_t n, double* out, void* ws, void* stream) {
+  if (k < 1 || k > 8) return fail_arg("ssnal_dots", "k must be in [1, 8]");
+  if (n < 1 || !xs || !out || !ws) return fail_arg("ssnal_dots", "null/size");
+  return check("ssnal_dots", launch_dots(k, xs, ys, mask, n, out, ws, S(stream)));
+}
+
+int ssnal_vec(int op, int64_t n, double alpha, const double* x, const double* y, const double* z,
+              double* out, void* stream) {
+  if (op < 0 || op > 4 || n < 1 || !x || !out) return fail_arg("ssnal_vec", "op/size/null");
+  if ((op == 1 || op == 2 || op == 3 || op == 0) && !y) return fail_arg("ssnal_vec", "y required");
+  if (op == 1 && !z) return fail_arg("ssnal_vec", "z required for op 1");
+  return check("ssnal_vec", launch_vec(op, n, alpha, x, y, z, out, S(stream)));
+}
+
+int ssnal_dense_xt(const double* A, int64_t n_phys, int64_t q, int64_t lda, const double* row_sign,
+                   int svr_block, int k, const double* const* vs, double* out, void* ws,
+                   void* stream) {
+  if (n_phys < 1 || q < 1 || lda < q || k < 1 || k > 4 || !A || !vs || !out || !ws)
+    return fail_arg("ssnal_dense_xt", "size/null");
+  return check("ssnal_dense_xt", launch_dense_xt(A, n_phys, q, lda, row_sign, svr_block, k, vs, out,
+                                                 ws, S(stream)));
+}
+
+int ssnal_dense_x(const double* A, int64_t n_phys, int64_t q, int64_t lda, const double* row_sign,
+                  int svr_block, int k, const double* d, double* out, void* stream) {
+  if (n_phys < 1 || q < 1 || lda < q || k < 1 || k > 4 || !A || !d || !out)
+    return fail_arg("ssnal_dense_x", "size/null");
+  if ((long long)2 * q * sizeof(double) > 200 * 1024) return fail_arg("ssnal_dense_x", "q too large");
+  return check("ssnal_dense_x", launch_dense_x(A, n_phys, q, lda, row_sign, svr_block, k, d, out,
+                                               S(stream)));
+}
+
+int ssnal_compact(const uint8_t* mask, int64_t n, int32_t* idx, int64_t* count, void* ws,
+                  void* stream) {
+  if (n < 1 || !mask || !idx || !count || !ws) return fail_arg("ssnal_compact", "size/null");
+  if (n > 0x7fffffffLL) return fail_arg("ssnal_compact", "n exceeds int32 index range");
+  return check("ssnal_compact", launch_compact(mask, n, idx, (long long*)count, ws, S(stream)));
+}
+
+int ssnal_dense_gram(const double* A, int64_t n_phys, int64_t q, int64_t lda,
+                     const double* row_sign, int svr_block, const int32_t* J,
+                     const int64_t* p_dev, int64_t p_max, const double* a, double sigma,
+                     const double* asa_dev, double* M, double* m1, void* ws, void* stream) {
+  if (n_phys < 1 || q < 1 || lda < q || !A || !J || !p_dev || !a || !asa_dev || !M || !m1 || !ws)
+    return fail_arg("ssnal_dense_gram", "size/null");
+  return check("ssnal_dense_gram",
+               launch_dense_gram(A, n_phys, q, lda, row_sign, svr_block, J, (const long long*)p_dev,
+                                 p_max, a, sigma, asa_dev, M, m1, ws, S(stream)));
+}
+
+int ssnal_chol_solve(double* M, int64_t m, const double* b, double scale, double* x, int* info,
+                     void* stream) {
+  if (m < 1 || !M || !b || !x || !info) return fail_arg("ssnal_chol_solve", "size/null");
+  return check("ssnal_chol_solve", launch_chol_solve(M, m, b, scale, x, info, S(stream)));
+}
+
+}  // extern "C"

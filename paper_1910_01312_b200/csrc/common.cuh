@@ -1,0 +1,78 @@
+// Shared device helpers for the SSsNAL sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define SSNAL_NT 256          // threads per block for streaming kernels
+#define SSNAL_MAX_BLOCKS 592  // 4 x 148 SMs: cap for grid-stride streaming grids
+#define SSNAL_MAX_TRIALS 16   // batched projections per launch (line-search step lengths)
+
+namespace ssnal {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide reduction of NV values per thread (sum / min / max selected per slot
+// by `ops`: 0 = sum, 1 = min, 2 = max).  Result valid in thread 0 (vals[]).
+// Deterministic: fixed shuffle tree, then warps combined in index order.
+template <int NV>
+__device__ __forceinline__ void block_reduce(double (&vals)[NV], const int (&ops)[NV],
+                                             double* smem /* >= NV * 32 */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double v = vals[k];
+    v = ops[k] == 0 ? warp_sum(v) : (ops[k] == 1 ? warp_min(v) : warp_max(v));
+    if (lane == 0) smem[k * 32 + warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double v = smem[k * 32];
+      for (int w = 1; w < nwarps; ++w) {
+        double x = smem[k * 32 + w];
+        v = ops[k] == 0 ? v + x : (ops[k] == 1 ? fmin(v, x) : fmax(v, x));
+      }
+      vals[k] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// "Last block done" ticket: returns true in exactly one block (the last to arrive),
+// after a device-scope fence so that every block's partials are visible to it.
+__device__ __forceinline__ bool last_block_arrive(unsigned int* ticket, unsigned int nblocks) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int prev = atomicAdd(ticket, 1u);
+    is_last = (prev == nblocks - 1);
+    if (is_last) *ticket = 0u;  // reset for the next launch
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+__host__ __device__ inline long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+
+}  // namespace ssnal

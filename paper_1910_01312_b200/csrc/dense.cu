@@ -1,0 +1,358 @@
+// Dense data-operator kernels for Q = X X^T, X = S diag(row_sign) A (row-major A).
+//
+//   X^T V : column panels x row splits; each warp streams whole rows (coalesced,
+//           lanes over columns), per-lane register accumulators, warps folded
+//           in fixed order, splits folded by a second deterministic pass.
+//   X D   : one warp per row, D staged in shared memory, shuffle-reduced dots.
+//   Gram  : G = X_J^T X_J on the fp64 tensor cores (DMMA 8x8x4) over gathered
+//           free rows J, split-K over J with fixed-order fold, then assembled
+//           into the Prop. 3.5 Newton matrix I + sigma (G - m1 m1^T / a'Sa).
+// ref: kernels.py:97-106,144-154 (column-wise Q), solver.py:224-262 (Q_JJ, cols@v).
+#include "common.cuh"
+#include "ssnal_internal.h"
+
+namespace ssnal {
+
+int stream_blocks(long long n, int per_thread);
+
+// ------------------------------------------------------------------ X^T V
+static constexpr int XT_MAXC = 10;  // scalar columns per lane per panel (320-wide panels)
+static constexpr int XT_PANEL = 32 * XT_MAXC;
+static constexpr int XT_WARPS = 8;
+
+struct XtArgs {
+  const double* A;
+  long long n, q, lda;
+  const double* rs;
+  int svr;
+  const double* v[4];
+  int k;
+  double* part;  // [nsplit][k][q]
+  double* out;   // [k][q]
+};
+
+template <int KV>
+__global__ void __launch_bounds__(XT_WARPS * 32) dense_xt_kernel(XtArgs p, int kofs) {
+  __shared__ double red[XT_WARPS][KV][XT_PANEL];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long col0 = (long long)blockIdx.y * XT_PANEL;
+  const long long nsplit = gridDim.x;
+  const long long rows_per = ceil_div(p.n, nsplit);
+  const long long r0 = blockIdx.x * rows_per;
+  const long long r1 = min(p.n, r0 + rows_per);
+  double acc[KV][XT_MAXC];
+#pragma unroll
+  for (int j = 0; j < KV; ++j)
+#pragma unroll
+    for (int c = 0; c < XT_MAXC; ++c) acc[j][c] = 0.0;
+  for (long long r = r0 + warp; r < r1; r += XT_WARPS) {
+    double coef[KV];
+    const double sg = p.rs ? p.rs[r] : 1.0;
+#pragma unroll
+    for (int j = 0; j < KV; ++j) {
+      const double* vj = p.v[kofs + j];
+      double cv = vj[r];
+      if (p.svr) cv = __dsub_rn(cv, vj[r + p.n]);
+      coef[j] = sg * cv;
+    }
+    const double* row = p.A + r * p.lda + col0;
+    double av[XT_MAXC];
+#pragma unroll
+    for (int c = 0; c < XT_MAXC; ++c) {
+      long long col = col0 + lane + 32 * c;
+      av[c] = col < p.q ? __ldg(row + lane + 32 * c) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < KV; ++j)
+#pragma unroll
+      for (int c = 0; c < XT_MAXC; ++c) acc[j][c] = fma(coef[j], av[c], acc[j][c]);
+  }
+#pragma unroll
+  for (int j = 0; j < KV; ++j)
+#pragma unroll
+    for (int c = 0; c < XT_MAXC; ++c) red[warp][j][lane + 32 * c] = acc[j][c];
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < KV * XT_PANEL; idx += blockDim.x) {
+    int j = idx / XT_PANEL, c = idx % XT_PANEL;
+    long long col = col0 + c;
+    if (col >= p.q) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < XT_WARPS; ++w) s += red[w][j][c];
+    p.part[((long long)blockIdx.x * p.k + kofs + j) * p.q + col] = s;
+  }
+}
+
+__global__ void dense_xt_fold_kernel(const double* __restrict__ part, long long nsplit, int k,
+                                     long long q, double* __restrict__ out) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)k * q) return;
+  double s = 0.0;
+  for (long long b = 0; b < nsplit; ++b) s += part[b * k * q + idx];
+  out[idx] = s;
+}
+
+static int xt_splits(long long n) {
+  long long s = ceil_div(n, 64);  // at least 64 rows per split
+  if (s > 296) s = 296;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
+size_t dense_xt_ws_bytes(long long n_phys, long long q, int k) {
+  return (size_t)xt_splits(n_phys) * k * q * sizeof(double);
+}
+
+cudaError_t launch_dense_xt(const double* A, long long n, long long q, long long lda,
+                            const double* rs, int svr, int k, const double* const* vs,
+                            double* out, void* ws, cudaStream_t stream) {
+  XtArgs p;
+  p.A = A; p.n = n; p.q = q; p.lda = lda; p.rs = rs; p.svr = svr; p.k = k;
+  for (int j = 0; j < 4; ++j) p.v[j] = j < k ? vs[j] : nullptr;
+  p.part = (double*)ws;
+  p.out = out;
+  int nsplit = xt_splits(n);
+  dim3 grid(nsplit, (unsigned)ceil_div(q, XT_PANEL));
+  for (int j = 0; j < k;) {
+    if (k - j >= 2) {
+      dense_xt_kernel<2><<<grid, XT_WARPS * 32, 0, stream>>>(p, j);
+      j += 2;
+    } else {
+      dense_xt_kernel<1><<<grid, XT_WARPS * 32, 0, stream>>>(p, j);
+      j += 1;
+    }
+  }
+  long long tot = (long long)k * q;
+  dense_xt_fold_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, stream>>>(p.part, nsplit, k, q, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ X D
+static constexpr int X_WARPS = 8;
+static constexpr int X_ROWS = 2;  // rows in flight per warp
+
+template <int KV>
+__global__ void __launch_bounds__(X_WARPS * 32) dense_x_kernel(const double* __restrict__ A,
+                                                               long long n, long long q,
+                                                               long long lda,
+                                                               const double* __restrict__ rs,
+                                                               int svr, const double* __restrict__ d,
+                                                               int k, int kofs,
+                                                               double* __restrict__ out,
+                                                               long long nlog) {
+  extern __shared__ double sd[];  // [KV][q]
+  for (long long i = threadIdx.x; i < (long long)KV * q; i += blockDim.x)
+    sd[i] = d[(long long)kofs * q + i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * X_WARPS + (threadIdx.x >> 5);
+  const long long nw = (long long)gridDim.x * X_WARPS;
+  for (long long r0 = gw * X_ROWS; r0 < n; r0 += nw * X_ROWS) {
+    double acc[X_ROWS][KV];
+#pragma unroll
+    for (int rr = 0; rr < X_ROWS; ++rr)
+#pragma unroll
+      for (int j = 0; j < KV; ++j) acc[rr][j] = 0.0;
+    for (long long c = lane; c < q; c += 32) {
+#pragma unroll
+      for (int rr = 0; rr < X_ROWS; ++rr) {
+        long long r = r0 + rr;
+        if (r < n) {
+          double a = __ldg(A + r * lda + c);
+#pragma unroll
+          for (int j = 0; j < KV; ++j) acc[rr][j] = fma(a, sd[j * q + c], acc[rr][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < X_ROWS; ++rr) {
+      long long r = r0 + rr;
+#pragma unroll
+      for (int j = 0; j < KV; ++j) {
+        double s = warp_sum(acc[rr][j]);
+        if (lane == 0 && r < n) {
+          double v = rs ? rs[r] * s : s;
+          out[(long long)(kofs + j) * nlog + r] = v;
+          if (svr) out[(long long)(kofs + j) * nlog + r + n] = -v;
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_dense_x(const double* A, long long n, long long q, long long lda,
+                           const double* rs, int svr, int k, const double* d, double* out,
+                           cudaStream_t stream) {
+  long long nlog = svr ? 2 * n : n;
+  long long blocks = ceil_div(n, (long long)X_WARPS * X_ROWS);
+  if (blocks > 4 * 148) blocks = 4 * 148;
+  if (blocks < 1) blocks = 1;
+  for (int j = 0; j < k;) {
+    int kv = (k - j >= 2) ? 2 : 1;
+    size_t smem = (size_t)kv * q * sizeof(double);
+    if (kv == 2) {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(dense_x_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      dense_x_kernel<2><<<(unsigned)blocks, X_WARPS * 32, smem, stream>>>(A, n, q, lda, rs, svr, d, k, j, out, nlog);
+    } else {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(dense_x_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      dense_x_kernel<1><<<(unsigned)blocks, X_WARPS * 32, smem, stream>>>(A, n, q, lda, rs, svr, d, k, j, out, nlog);
+    }
+    j += kv;
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ Gram (DMMA)
+static constexpr int GT = 64;        // output tile edge
+static constexpr int GK = 32;        // gathered rows staged per step
+static constexpr int GLD = GT + 4;   // padded smem row (conflict-free fragment loads)
+static constexpr int GSPLIT = 16;    // split-K over J (fixed => deterministic fold)
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+struct GramArgs {
+  const double* A;
+  long long n, q, lda;
+  const int32_t* J;
+  const long long* p_dev;
+  double* part;  // [GSPLIT][q][q] (upper tile pairs + full diagonal tiles)
+  int ntile;
+};
+
+// grid.x = tile pair index (ti <= tj), grid.y = split
+__global__ void __launch_bounds__(256) gram_kernel(GramArgs g) {
+  __shared__ double sA[GK][GLD];
+  __shared__ double sB[GK][GLD];
+  const long long p = *g.p_dev;
+  // decode (ti, tj) from the linear upper-triangle index
+  int pair = blockIdx.x, ti = 0;
+  while (pair >= g.ntile - ti) { pair -= g.ntile - ti; ++ti; }
+  const int tj = ti + pair;
+  const long long chunk = ceil_div(ceil_div(p, GSPLIT), 4) * 4;
+  const long long k0 = blockIdx.y * chunk;
+  const long long k1 = min(p, k0 + chunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[8][2];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const long long ci = (long long)ti * GT, cj = (long long)tj * GT;
+  for (long long kb = k0; kb < k1; kb += GK) {
+    // stage GK gathered rows x 64 columns of both tiles
+    for (int idx = threadIdx.x; idx < GK * GT; idx += blockDim.x) {
+      int kr = idx / GT, c = idx % GT;
+      long long r = kb + kr;
+      double va = 0.0, vb = 0.0;
+      if (r < k1) {
+        long long li = g.J[r];
+        long long pr = li >= g.n ? li - g.n : li;  // SVR block: row sign cancels in x x^T
+        const double* row = g.A + pr * g.lda;
+        if (ci + c < g.q) va = __ldg(row + ci + c);
+        if (cj + c < g.q) vb = __ldg(row + cj + c);
+      }
+      sA[kr][c] = va;
+      sB[kr][c] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GK; kk += 4) {
+      const double a = sA[kk + (lane & 3)][warp * 8 + (lane >> 2)];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const double b = sB[kk + (lane & 3)][t * 8 + (lane >> 2)];
+        dmma_8x8x4(acc[t][0], acc[t][1], a, b);
+      }
+    }
+    __syncthreads();
+  }
+  // C fragment: row = lane/4, cols = 2*(lane%4) + {0,1}
+  double* dst = g.part + (long long)blockIdx.y * g.q * g.q;
+  const long long row = ci + warp * 8 + (lane >> 2);
+  if (row < g.q) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      long long col = cj + t * 8 + 2 * (lane & 3);
+      if (col < g.q) dst[row * g.q + col] = acc[t][0];
+      if (col + 1 < g.q) dst[row * g.q + col + 1] = acc[t][1];
+    }
+  }
+}
+
+// m1 partials: part_m1[split][q] = sum_{r in split} w_r x_{J_r}
+__global__ void __launch_bounds__(256) gram_m1_kernel(GramArgs g, const double* __restrict__ a,
+                                                      const double* __restrict__ rs, int svr,
+                                                      double* __restrict__ part_m1) {
+  const long long p = *g.p_dev;
+  const long long chunk = ceil_div(ceil_div(p, GSPLIT), 4) * 4;
+  const long long k0 = blockIdx.y * chunk;
+  const long long k1 = min(p, k0 + chunk);
+  const long long col = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= g.q) return;
+  double s = 0.0;
+  for (long long r = k0; r < k1; ++r) {
+    long long li = g.J[r];
+    long long pr = li >= g.n ? li - g.n : li;
+    double w = a[li];
+    if (rs) w *= rs[pr];
+    if (svr && li >= g.n) w = -w;
+    s = fma(w, __ldg(g.A + pr * g.lda + col), s);
+  }
+  part_m1[blockIdx.y * g.q + col] = s;
+}
+
+__global__ void gram_m1_fold_kernel(const double* __restrict__ part_m1, long long q,
+                                    double* __restrict__ m1) {
+  long long col = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= q) return;
+  double s = 0.0;
+  for (int b = 0; b < GSPLIT; ++b) s += part_m1[b * q + col];
+  m1[col] = s;
+}
+
+// M = I + sigma (G - m1 m1^T / asa)   (asa == 0: I + sigma G)
+__global__ void gram_assemble_kernel(const double* __restrict__ part, long long q,
+                                     const double* __restrict__ m1, double sigma,
+                                     const double* __restrict__ asa_dev,
+                                     double* __restrict__ M) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= q * q) return;
+  long long i = idx / q, j = idx % q;
+  long long si = i, sj = j;
+  if (i / GT > j / GT) { si = j; sj = i; }  // lower tiles are stored transposed
+  double g = 0.0;
+  for (int b = 0; b < GSPLIT; ++b) g += part[(long long)b * q * q + si * q + sj];
+  const double asa = *asa_dev;
+  if (asa != 0.0) g = g - m1[i] * m1[j] / asa;
+  M[idx] = (i == j ? 1.0 : 0.0) + sigma * g;
+}
+
+size_t gram_ws_bytes(long long q) {
+  return (size_t)GSPLIT * q * q * sizeof(double) + (size_t)GSPLIT * q * sizeof(double);
+}
+
+cudaError_t launch_dense_gram(const double* A, long long n, long long q, long long lda,
+                              const double* rs, int svr, const int32_t* J, const long long* p_dev,
+                              long long p_max, const double* a, double sigma,
+                              const double* asa_dev, double* M, double* m1, void* ws,
+                              cudaStream_t stream) {
+  (void)p_max;
+  GramArgs g;
+  g.A = A; g.n = n; g.q = q; g.lda = lda; g.J = J; g.p_dev = p_dev;
+  g.part = (double*)ws;
+  g.ntile = (int)ceil_div(q, GT);
+  double* part_m1 = g.part + (long long)GSPLIT * q * q;
+  int npairs = g.ntile * (g.ntile + 1) / 2;
+  gram_kernel<<<dim3(npairs, GSPLIT), 256, 0, stream>>>(g);
+  gram_m1_kernel<<<dim3((unsigned)ceil_div(q, 256), GSPLIT), 256, 0, stream>>>(g, a, rs, svr, part_m1);
+  gram_m1_fold_kernel<<<(unsigned)ceil_div(q, 256), 256, 0, stream>>>(part_m1, q, m1);
+  gram_assemble_kernel<<<(unsigned)ceil_div(q * q, 256), 256, 0, stream>>>(g.part, q, m1, sigma,
+                                                                          asa_dev, M);
+  return cudaGetLastError();
+}
+
+}  // namespace ssnal

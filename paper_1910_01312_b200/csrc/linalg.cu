@@ -1,0 +1,153 @@
+// Dense SPD solve for the reduced Newton system: blocked right-looking Cholesky
+// (32-column panels; diagonal block by one warp with shuffles, panel TRSM one row
+// per thread, trailing SYRK update from a shared-memory copy of the panel),
+// followed by blocked forward / backward substitution -- all inside ONE CTA so
+// the factor never leaves L2 and no host round trip is needed.
+// Replaces scipy.linalg.solve(..., assume_a="sym") of ref solver.py:175-191.
+#include "common.cuh"
+#include "ssnal_internal.h"
+
+namespace ssnal {
+
+static constexpr int NB = 32;
+static constexpr int CH_NT = 1024;
+static constexpr int PANEL_ROWS = 768;  // panel rows kept in shared memory (stride NB+1)
+
+__global__ void __launch_bounds__(CH_NT, 1) chol_solve_kernel(double* __restrict__ M, long long m,
+                                                                const double* __restrict__ b,
+                                                                double scale, double* __restrict__ x,
+                                                                int* __restrict__ info) {
+  extern __shared__ double smem[];
+  double* D = smem;                       // NB x (NB+1) diagonal block
+  double* P = smem + NB * (NB + 1);       // panel rows x (NB+1)
+  __shared__ int fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  for (long long k0 = 0; k0 < m; k0 += NB) {
+    const int kb = (int)min((long long)NB, m - k0);
+    // 1. diagonal block -> D, factor with warp 0
+    for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+      int i = idx / kb, j = idx % kb;
+      D[i * (NB + 1) + j] = M[(k0 + i) * m + k0 + j];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int j = 0; j < kb; ++j) {
+        // lane i (>= j) owns row i of the current column
+        double dj = D[j * (NB + 1) + j];
+        if (dj <= 0.0 || !(dj == dj)) {
+          if (lane == 0 && fail == 0) fail = (int)(k0 + j + 1);
+          dj = 1.0;
+        }
+        double ljj = sqrt(dj);
+        __syncwarp();
+        if (lane == j) D[j * (NB + 1) + j] = ljj;
+        if (lane > j && lane < kb) D[lane * (NB + 1) + j] /= ljj;
+        __syncwarp();
+        // rank-1 update of the remaining lower block: rows lane, cols j+1..lane
+        if (lane > j && lane < kb) {
+          double lij = D[lane * (NB + 1) + j];
+          for (int c = j + 1; c <= lane; ++c) D[lane * (NB + 1) + c] -= lij * D[c * (NB + 1) + j];
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+      int i = idx / kb, j = idx % kb;
+      if (j <= i) M[(k0 + i) * m + k0 + j] = D[i * (NB + 1) + j];
+    }
+    // 2. panel solve: rows below, L21 = A21 L11^{-T}; one thread per row
+    const long long r0 = k0 + kb;
+    const long long nr = m - r0;
+    const bool in_smem = nr <= PANEL_ROWS;
+    for (long long i = tid; i < nr; i += blockDim.x) {
+      double row[NB];
+      const long long gi = r0 + i;
+      for (int j = 0; j < kb; ++j) row[j] = M[gi * m + k0 + j];
+      for (int j = 0; j < kb; ++j) {
+        double s = row[j];
+        for (int t = 0; t < j; ++t) s -= row[t] * D[j * (NB + 1) + t];
+        row[j] = s / D[j * (NB + 1) + j];
+      }
+      for (int j = 0; j < kb; ++j) {
+        M[gi * m + k0 + j] = row[j];
+        if (in_smem) P[i * (NB + 1) + j] = row[j];
+      }
+    }
+    __syncthreads();
+    // 3. trailing update (lower triangle): A22 -= L21 L21^T
+    const double* Lp = in_smem ? P : nullptr;
+    for (long long i = warp; i < nr; i += (CH_NT / 32)) {
+      for (long long j = lane; j <= i; j += 32) {
+        double s = 0.0;
+        if (in_smem) {
+          for (int t = 0; t < kb; ++t) s += Lp[i * (NB + 1) + t] * Lp[j * (NB + 1) + t];
+        } else {
+          for (int t = 0; t < kb; ++t) s += M[(r0 + i) * m + k0 + t] * M[(r0 + j) * m + k0 + t];
+        }
+        M[(r0 + i) * m + r0 + j] -= s;
+      }
+    }
+    __syncthreads();
+  }
+  // forward substitution  L y = scale * b   (y kept in x)
+  for (long long i = tid; i < m; i += blockDim.x) x[i] = scale * b[i];
+  __syncthreads();
+  for (long long k0 = 0; k0 < m; k0 += NB) {
+    const int kb = (int)min((long long)NB, m - k0);
+    if (warp == 0) {
+      double yv = lane < kb ? x[k0 + lane] : 0.0;
+      for (int j = 0; j < kb; ++j) {
+        double yj = __shfl_sync(0xffffffffu, yv, j);
+        if (lane == j) { yj = yv / M[(k0 + j) * m + k0 + j]; yv = yj; }
+        yj = __shfl_sync(0xffffffffu, yv, j);
+        if (lane > j && lane < kb) yv -= M[(k0 + lane) * m + k0 + j] * yj;
+      }
+      if (lane < kb) x[k0 + lane] = yv;
+    }
+    __syncthreads();
+    for (long long i = k0 + kb + tid; i < m; i += blockDim.x) {
+      double s = 0.0;
+      for (int t = 0; t < kb; ++t) s += M[i * m + k0 + t] * x[k0 + t];
+      x[i] -= s;
+    }
+    __syncthreads();
+  }
+  // backward substitution  L^T x = y
+  const long long nblk = ceil_div(m, NB);
+  for (long long bk = nblk - 1; bk >= 0; --bk) {
+    const long long k0 = bk * NB;
+    const int kb = (int)min((long long)NB, m - k0);
+    if (warp == 0) {
+      double xv = lane < kb ? x[k0 + lane] : 0.0;
+      for (int j = kb - 1; j >= 0; --j) {
+        if (lane == j) xv = xv / M[(k0 + j) * m + k0 + j];
+        double xj = __shfl_sync(0xffffffffu, xv, j);
+        if (lane < j) xv -= M[(k0 + j) * m + k0 + lane] * xj;
+      }
+      if (lane < kb) x[k0 + lane] = xv;
+    }
+    __syncthreads();
+    for (long long i = tid; i < k0; i += blockDim.x) {
+      double s = 0.0;
+      for (int t = 0; t < kb; ++t) s += M[(k0 + t) * m + i] * x[k0 + t];
+      x[i] -= s;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *info = fail;
+}
+
+cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
+                              int* info, cudaStream_t stream) {
+  size_t smem = (size_t)(NB * (NB + 1) + PANEL_ROWS * (NB + 1)) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  chol_solve_kernel<<<1, CH_NT, smem, stream>>>(M, m, b, scale, x, info);
+  return cudaGetLastError();
+}
+
+}  // namespace ssnal

@@ -1,0 +1,372 @@
+// Projection onto K cap L = {x : a'x = d, l <= x <= u} on sm_100a.
+//
+// Replaces ref projection.py:152-211 (project_box_line) and :134-149 (_classify).
+// The reference sorts all 2n breakpoints and binary-searches them with one
+// O(n) grad_phi evaluation per probe.  Here the root of the non-decreasing
+// piecewise-linear phi'(lambda) = d - a'clip(v - lambda a, l, u) is bracketed by
+// a K-ary search in lambda (K = 32 sub-intervals per pass, all 31 probes summed in
+// registers in ONE streaming pass), then the bracket is closed onto the two
+// ADJACENT breakpoints t_l < t_u of the reference's sorted array and lambda is
+// the reference's interpolation  t_l - f_l (t_u - t_l) / (f_u - f_l)  with f_l,
+// f_u direct deterministic sums.  No sort, no atomics on floating-point data;
+// every reduction is a fixed-order two-stage tree, so results are bit-
+// reproducible run to run.
+//
+// Batching: blockIdx.y = trial t evaluates v_t = A - coef[t] * B, which is how
+// the Armijo line search evaluates several step lengths in one launch sequence.
+//
+// Phases (one launch each, every phase closes with a last-block-done finalize):
+//   range  : tmin / tmax over breakpoints, f(-inf), f(+inf)          (status 0|2|<0)
+//   pass   : 31 probe sums + in-bracket breakpoint stats -> narrower bracket (x P)
+//   exact  : direct sums at <= 4 candidate breakpoints -> lambda      (status 2)
+//   apply  : x = clip(v - lambda a), free mask, fused reductions
+#include "common.cuh"
+#include "ssnal_internal.h"
+
+namespace ssnal {
+
+static constexpr int KSUB = 32;          // sub-intervals per pass
+static constexpr int NPROBE = KSUB - 1;  // interior probes per pass
+static constexpr int PSTRIDE = 40;       // doubles per block partial record
+
+struct ProjArgs {
+  const double* A;
+  const double* B;
+  double coef[SSNAL_MAX_TRIALS];
+  const double* a;
+  const double* l;
+  const double* u;
+  double lc, uc, d;
+  long long n;
+  ProjState* st;
+  double* part;  // [T][nblk][PSTRIDE]
+  double* x_out;             // [T][n] or null
+  unsigned char* free_out;   // [T][n] or null
+  const double* ref;         // reference vector for sum (x - ref)^2, or null
+};
+
+__device__ __forceinline__ void load_elem(const ProjArgs& p, int t, long long i, double& v,
+                                          double& a, double& l, double& u) {
+  v = p.A[i];
+  if (p.B) v = __dsub_rn(v, __dmul_rn(p.coef[t], p.B[i]));
+  a = p.a[i];
+  l = p.l ? p.l[i] : p.lc;
+  u = p.u ? p.u[i] : p.uc;
+}
+
+// a * clip(v - lam a, l, u) with numpy's rounding for v - lam*a (no fma contraction)
+__device__ __forceinline__ double contrib(double v, double a, double l, double u, double lam) {
+  double y = __dsub_rn(v, __dmul_rn(lam, a));
+  return a * fmin(fmax(y, l), u);
+}
+
+__device__ __forceinline__ double probe_at(const ProjState& s, int k) {
+  // k in [0, KSUB]; k = 0 -> lo, k = KSUB -> hi exactly
+  if (k <= 0) return s.lo;
+  if (k >= KSUB) return s.hi;
+  double h = (s.hi - s.lo) / KSUB;
+  return s.lo + (double)k * h;
+}
+
+// ------------------------------------------------------------------ range
+__global__ void __launch_bounds__(SSNAL_NT) proj_range_kernel(ProjArgs p) {
+  __shared__ double red[5 * 32];
+  const int t = blockIdx.y;
+  ProjState* st = p.st + t;
+  double tmin = INFINITY, tmax = -INFINITY, s_left = 0.0, s_right = 0.0, nnz = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v, a, l, u;
+    load_elem(p, t, i, v, a, l, u);
+    if (a != 0.0) {
+      double t1 = __ddiv_rn(__dsub_rn(v, u), a), t2 = __ddiv_rn(__dsub_rn(v, l), a);
+      tmin = fmin(tmin, fmin(t1, t2));
+      tmax = fmax(tmax, fmax(t1, t2));
+      nnz += 1.0;
+      // saturation values: lambda -> -inf puts a>0 slots at u, a<0 slots at l
+      s_left += a > 0.0 ? a * u : a * l;
+      s_right += a > 0.0 ? a * l : a * u;
+    }
+  }
+  double vals[5] = {tmin, tmax, s_left, s_right, nnz};
+  const int ops[5] = {1, 2, 0, 0, 0};
+  block_reduce<5>(vals, ops, red);
+  double* mine = p.part + ((long long)t * gridDim.x + blockIdx.x) * PSTRIDE;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 5; ++k) mine[k] = vals[k];
+  if (!last_block_arrive(&st->ticket, gridDim.x)) return;
+  if (threadIdx.x != 0) return;
+  const double* base = p.part + (long long)t * gridDim.x * PSTRIDE;
+  double r0 = INFINITY, r1 = -INFINITY, r2 = 0.0, r3 = 0.0, r4 = 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) {
+    const double* q = base + (long long)b * PSTRIDE;
+    r0 = fmin(r0, __ldcg(q + 0));
+    r1 = fmax(r1, __ldcg(q + 1));
+    r2 += __ldcg(q + 2);
+    r3 += __ldcg(q + 3);
+    r4 += __ldcg(q + 4);
+  }
+  st->tmin = r0;
+  st->tmax = r1;
+  st->passes = 0;
+  st->in_count = -1;
+  if (r4 == 0.0) {  // a == 0: equality constraint is 0 = d, project by clipping
+    st->lam = 0.0;
+    st->status = PROJ_DONE;
+    return;
+  }
+  double f_neg = p.d - r2, f_pos = p.d - r3;
+  if (f_neg >= 0.0) {  // ref projection.py:186-191
+    st->lam = r0;
+    st->status = f_neg > 1e-9 * (1.0 + fabs(p.d)) ? PROJ_INFEASIBLE_LOW : PROJ_DONE;
+    return;
+  }
+  if (f_pos < 0.0) {  // ref projection.py:192-193
+    st->status = PROJ_INFEASIBLE_HIGH;
+    return;
+  }
+  st->lo = r0;
+  st->hi = r1;
+  st->flo = f_neg;
+  st->fhi = f_pos;
+  st->below_max = r0;
+  st->above_min = INFINITY;
+  st->status = PROJ_SEARCH;
+}
+
+// ------------------------------------------------------------------ pass
+__global__ void __launch_bounds__(SSNAL_NT) proj_pass_kernel(ProjArgs p) {
+  __shared__ double red[(NPROBE + 8) * 32];
+  const int t = blockIdx.y;
+  ProjState* st = p.st + t;
+  if (st->status != PROJ_SEARCH) return;  // uniform across the grid
+  const ProjState s = *st;
+  const double lo = s.lo, hi = s.hi;
+  double acc[NPROBE];
+#pragma unroll
+  for (int k = 0; k < NPROBE; ++k) acc[k] = 0.0;
+  double s_const = 0.0, s_slope = 0.0;  // settled slots: sum of (alpha + beta lambda)
+  double bmax = -INFINITY, amin = INFINITY, imin = INFINITY, imax = -INFINITY, icnt = 0.0;
+  double probes[NPROBE];
+#pragma unroll
+  for (int k = 0; k < NPROBE; ++k) probes[k] = probe_at(s, k + 1);
+
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v, a, l, u;
+    load_elem(p, t, i, v, a, l, u);
+    if (a == 0.0) continue;
+    double t1 = __ddiv_rn(__dsub_rn(v, u), a), t2 = __ddiv_rn(__dsub_rn(v, l), a);
+    double ta = fmin(t1, t2), tb = fmax(t1, t2);
+    bool in_a = ta > lo && ta <= hi, in_b = tb > lo && tb <= hi;
+    if (ta <= lo) bmax = fmax(bmax, ta); else if (ta > hi) amin = fmin(amin, ta);
+    if (tb <= lo) bmax = fmax(bmax, tb); else if (tb > hi) amin = fmin(amin, tb);
+    if (in_a) { icnt += 1.0; imin = fmin(imin, ta); imax = fmax(imax, ta); }
+    if (in_b) { icnt += 1.0; imin = fmin(imin, tb); imax = fmax(imax, tb); }
+    if (in_a || in_b) {
+#pragma unroll
+      for (int k = 0; k < NPROBE; ++k) acc[k] += contrib(v, a, l, u, probes[k]);
+    } else if (tb <= lo) {  // saturated on the right side over the whole bracket
+      s_const += a > 0.0 ? a * l : a * u;
+    } else if (ta > hi) {   // saturated on the left side
+      s_const += a > 0.0 ? a * u : a * l;
+    } else {                // linear over the whole bracket: a v - a^2 lambda
+      s_const += a * v;
+      s_slope -= a * a;
+    }
+  }
+  // reduce: probes (sum), s_const, s_slope (sum), bmax (max), amin, imin (min), imax, icnt
+  double vals[NPROBE + 7];
+  int ops[NPROBE + 7];
+#pragma unroll
+  for (int k = 0; k < NPROBE; ++k) { vals[k] = acc[k]; ops[k] = 0; }
+  vals[NPROBE + 0] = s_const; ops[NPROBE + 0] = 0;
+  vals[NPROBE + 1] = s_slope; ops[NPROBE + 1] = 0;
+  vals[NPROBE + 2] = bmax;    ops[NPROBE + 2] = 2;
+  vals[NPROBE + 3] = amin;    ops[NPROBE + 3] = 1;
+  vals[NPROBE + 4] = imin;    ops[NPROBE + 4] = 1;
+  vals[NPROBE + 5] = imax;    ops[NPROBE + 5] = 2;
+  vals[NPROBE + 6] = icnt;    ops[NPROBE + 6] = 0;
+  block_reduce<NPROBE + 7>(vals, ops, red);
+  double* mine = p.part + ((long long)t * gridDim.x + blockIdx.x) * PSTRIDE;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NPROBE + 7; ++k) mine[k] = vals[k];
+  if (!last_block_arrive(&st->ticket, gridDim.x)) return;
+  if (threadIdx.x != 0) return;
+
+  const double* base = p.part + (long long)t * gridDim.x * PSTRIDE;
+  double tot[NPROBE + 7];
+  for (int k = 0; k < NPROBE + 7; ++k)
+    tot[k] = (k == NPROBE + 2) ? -INFINITY : (k == NPROBE + 3 || k == NPROBE + 4) ? INFINITY
+             : (k == NPROBE + 5) ? -INFINITY : 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) {
+    const double* q = base + (long long)b * PSTRIDE;
+    for (int k = 0; k < NPROBE + 7; ++k) {
+      double x = __ldcg(q + k);
+      int op = (k < NPROBE + 2 || k == NPROBE + 6) ? 0 : (k == NPROBE + 3 || k == NPROBE + 4) ? 1 : 2;
+      tot[k] = op == 0 ? tot[k] + x : (op == 1 ? fmin(tot[k], x) : fmax(tot[k], x));
+    }
+  }
+  const double below = fmax(s.below_max, tot[NPROBE + 2]);
+  const double above = fmin(s.above_min, tot[NPROBE + 3]);
+  const double in_min = tot[NPROBE + 4], in_max = tot[NPROBE + 5];
+  const long long in_cnt = (long long)tot[NPROBE + 6];
+  st->passes = s.passes + 1;
+  st->below_max = below;
+  st->above_min = above;
+  st->in_count = in_cnt;
+  st->in_min = in_min;
+  st->in_max = in_max;
+  const double width = hi - lo;
+  const bool tiny = !(width > 4.0 * 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi)));
+  if (in_cnt == 0 || in_min == in_max || tiny) {
+    st->status = PROJ_BRACKETED;  // the exact phase closes onto adjacent breakpoints
+    return;
+  }
+  // f(probe_k) = d - (sum over unsettled + s_const + s_slope * probe_k); pick the first
+  // sub-interval whose right end has f >= 0.
+  int k_hit = KSUB;
+  for (int k = 1; k < KSUB; ++k) {
+    double fk = p.d - (tot[k - 1] + tot[NPROBE] + tot[NPROBE + 1] * probe_at(s, k));
+    if (fk >= 0.0) { k_hit = k; break; }
+  }
+  double new_lo = probe_at(s, k_hit - 1), new_hi = probe_at(s, k_hit);
+  st->lo = new_lo;
+  st->hi = new_hi;
+}
+
+// ------------------------------------------------------------------ exact
+// Candidates are sorted breakpoint values; f is evaluated by direct sums.
+__global__ void __launch_bounds__(SSNAL_NT) proj_exact_kernel(ProjArgs p) {
+  __shared__ double red[4 * 32];
+  __shared__ double cand_s[4];
+  __shared__ int ncand_s;
+  const int t = blockIdx.y;
+  ProjState* st = p.st + t;
+  if (st->status != PROJ_BRACKETED) return;
+  if (threadIdx.x == 0) {
+    const ProjState s = *st;
+    int nc = 0;
+    cand_s[nc++] = s.below_max;
+    if (s.in_count > 0) {
+      cand_s[nc++] = s.in_min;
+      if (s.in_max != s.in_min) cand_s[nc++] = s.in_max;
+    }
+    if (s.above_min < INFINITY) cand_s[nc++] = s.above_min;
+    ncand_s = nc;
+  }
+  __syncthreads();
+  const int nc = ncand_s;
+  double cand[4];
+  for (int k = 0; k < 4; ++k) cand[k] = k < nc ? cand_s[k] : 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v, a, l, u;
+    load_elem(p, t, i, v, a, l, u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < nc) acc[k] += contrib(v, a, l, u, cand[k]);
+  }
+  const int ops[4] = {0, 0, 0, 0};
+  block_reduce<4>(acc, ops, red);
+  double* mine = p.part + ((long long)t * gridDim.x + blockIdx.x) * PSTRIDE;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 4; ++k) mine[k] = acc[k];
+  if (!last_block_arrive(&st->ticket, gridDim.x)) return;
+  if (threadIdx.x != 0) return;
+  const double* base = p.part + (long long)t * gridDim.x * PSTRIDE;
+  double f[4] = {0.0, 0.0, 0.0, 0.0};
+  for (unsigned b = 0; b < gridDim.x; ++b)
+    for (int k = 0; k < nc; ++k) f[k] += __ldcg(base + (long long)b * PSTRIDE + k);
+  for (int k = 0; k < nc; ++k) f[k] = p.d - f[k];
+  // first candidate with f >= 0 is t_u; its predecessor is t_l (ref projection.py:195-208)
+  int iu = nc - 1;
+  for (int k = 0; k < nc; ++k)
+    if (f[k] >= 0.0) { iu = k; break; }
+  double lam;
+  if (iu == 0) {
+    lam = cand[0];  // rounding put the root at/below t_l: flat zero segment
+  } else {
+    const double tl = cand[iu - 1], tu = cand[iu], fl = f[iu - 1], fu = f[iu];
+    if (fu == fl || tu == tl) lam = tl;
+    else lam = tl - fl * (tu - tl) / (fu - fl);
+  }
+  st->lam = lam;
+  st->status = PROJ_DONE;
+}
+
+// ------------------------------------------------------------------ apply
+__global__ void __launch_bounds__(SSNAL_NT) proj_apply_kernel(ProjArgs p) {
+  __shared__ double red[5 * 32];
+  const int t = blockIdx.y;
+  ProjState* st = p.st + t;
+  if (st->status != PROJ_DONE) return;
+  const double lam = st->lam;
+  double sv2 = 0.0, sr2 = 0.0, sd2 = 0.0, sa2 = 0.0, nfree = 0.0;
+  double* xo = p.x_out ? p.x_out + (long long)t * p.n : nullptr;
+  unsigned char* fo = p.free_out ? p.free_out + (long long)t * p.n : nullptr;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v, a, l, u;
+    load_elem(p, t, i, v, a, l, u);
+    double y = __dsub_rn(v, __dmul_rn(lam, a));
+    double x = fmin(fmax(y, l), u);
+    // ref projection.py:134-149: bound slots within 1e-12 (1 + |bound|)
+    bool lower = y <= __dadd_rn(l, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(l))));
+    bool upper = !lower && (y >= __dsub_rn(u, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(u)))));
+    bool fr = !(lower || upper);
+    if (xo) xo[i] = x;
+    if (fo) fo[i] = fr ? 1 : 0;
+    double r = v - x;
+    sv2 += v * v;
+    sr2 += r * r;
+    if (p.ref) { double dd = x - p.ref[i]; sd2 += dd * dd; }
+    if (fr) { sa2 += a * a; nfree += 1.0; }
+  }
+  double vals[5] = {sv2, sr2, sd2, sa2, nfree};
+  const int ops[5] = {0, 0, 0, 0, 0};
+  block_reduce<5>(vals, ops, red);
+  double* mine = p.part + ((long long)t * gridDim.x + blockIdx.x) * PSTRIDE;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 5; ++k) mine[k] = vals[k];
+  if (!last_block_arrive(&st->ticket, gridDim.x)) return;
+  if (threadIdx.x != 0) return;
+  const double* base = p.part + (long long)t * gridDim.x * PSTRIDE;
+  double r[5] = {0, 0, 0, 0, 0};
+  for (unsigned b = 0; b < gridDim.x; ++b)
+    for (int k = 0; k < 5; ++k) r[k] += __ldcg(base + (long long)b * PSTRIDE + k);
+  st->sum_v2 = r[0];
+  st->sum_r2 = r[1];
+  st->sum_dref2 = r[2];
+  st->sum_a2_free = r[3];
+  st->nfree = (long long)r[4];
+  st->status = PROJ_APPLIED;
+}
+
+int proj_blocks(long long n) {
+  long long b = ceil_div(n, (long long)SSNAL_NT * 4);
+  if (b < 1) b = 1;
+  if (b > SSNAL_MAX_BLOCKS / 2) b = SSNAL_MAX_BLOCKS / 2;
+  return (int)b;
+}
+
+size_t proj_ws_bytes(long long n, int T) {
+  return (size_t)T * proj_blocks(n) * PSTRIDE * sizeof(double);
+}
+
+cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
+  ProjArgs p;
+  p.A = L.A; p.B = L.B;
+  for (int t = 0; t < SSNAL_MAX_TRIALS; ++t) p.coef[t] = (L.coef && t < L.T) ? L.coef[t] : 0.0; p.a = L.a; p.l = L.l; p.u = L.u;
+  p.lc = L.lc; p.uc = L.uc; p.d = L.d; p.n = L.n; p.st = L.st; p.part = L.part;
+  p.x_out = L.x_out; p.free_out = L.free_out; p.ref = L.ref;
+  dim3 grid(proj_blocks(L.n), L.T);
+  if (L.phases & PHASE_RANGE) proj_range_kernel<<<grid, SSNAL_NT, 0, stream>>>(p);
+  for (int k = 0; k < L.passes; ++k) proj_pass_kernel<<<grid, SSNAL_NT, 0, stream>>>(p);
+  if (L.phases & PHASE_EXACT) proj_exact_kernel<<<grid, SSNAL_NT, 0, stream>>>(p);
+  if (L.phases & PHASE_APPLY) proj_apply_kernel<<<grid, SSNAL_NT, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace ssnal

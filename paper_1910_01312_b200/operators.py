@@ -1,0 +1,115 @@
+"""Implicit Q operators in factor form Q = X X^T (device resident).
+
+ref kernels.py builds Q_ij = y_i y_j K(x_i, x_j) column by column (KernelOperator
+:68-154), the SVR block [[K,-K],[-K,K]] (BlockKernelOperator :181-215) and an
+explicit matrix (DenseOperator :218-238).  For the linear kernel all three are
+Q = X X^T with
+
+    C-SVC  X = diag(y) A          (LinearKernelOperator(A, labels=y))
+    SVR    X = [A; -A]            (LinearKernelOperator(A, svr_block=True))
+    dense  X = V diag(sqrt(ev+))  (DenseOperator(Q): host eigendecomposition once)
+
+so the hot path only ever streams A (csrc/dense.cu) and never forms an n x n
+block.  ``matvec`` / ``columns`` / ``submatrix`` / ``diag`` keep the reference
+operator protocol for callers.
+"""
+
+import numpy as np
+import torch
+
+from .backend import F64, as_device, check_vector, default_backend
+from .errors import InputError
+
+
+class LinearKernelOperator:
+    """Q = X X^T, X = S diag(labels) A, A row-major n x q (fp64, on the device)."""
+
+    kind = "dense"
+
+    def __init__(self, samples, labels=None, svr_block=False, backend=None):
+        self.backend = be = backend or default_backend()
+        A = as_device(samples, be)
+        if A.dim() != 2:
+            raise InputError("samples must be an n x q matrix")
+        self.A = A
+        self.n_phys, self.q = A.shape
+        self.lda = A.stride(0)
+        self.svr_block = bool(svr_block)
+        self.n = 2 * self.n_phys if self.svr_block else self.n_phys
+        if labels is not None:
+            lab = as_device(labels, be)
+            check_vector(lab, self.n_phys, "labels")
+            if not bool(torch.all(lab.abs() == 1.0)):
+                raise InputError("labels must be +1/-1")
+            self.row_sign = lab
+        else:
+            self.row_sign = None
+
+    # -- factor products (device, async) -------------------------------------
+    def xt(self, vs, out=None):
+        """X^T [v_0 .. v_{k-1}] -> q x k column-major buffer (returned as (k, q))."""
+        out = out if out is not None else self.backend.empty((len(vs), self.q))
+        self.backend.dense_xt(self, vs, out)
+        return out
+
+    def x(self, d, out=None, k=1):
+        """X d for d a (k, q) buffer -> (k, n) buffer."""
+        out = out if out is not None else self.backend.empty((k, self.n))
+        self.backend.dense_x(self, d, out, k)
+        return out
+
+    # -- reference operator protocol -------------------------------------------
+    def matvec(self, v):
+        v = as_device(v, self.backend)
+        check_vector(v, self.n, "matvec")
+        return self.x(self.xt([v]))[0]
+
+    def _rows(self, idx):
+        idx = torch.as_tensor(idx, dtype=torch.long, device=self.A.device)
+        if idx.numel() and (int(idx.min()) < 0 or int(idx.max()) >= self.n):
+            raise InputError("column index out of range")
+        phys = idx % self.n_phys
+        rows = self.A[phys]
+        sgn = torch.ones(idx.numel(), dtype=F64, device=self.A.device)
+        if self.row_sign is not None:
+            sgn = sgn * self.row_sign[phys]
+        if self.svr_block:
+            sgn = torch.where(idx >= self.n_phys, -sgn, sgn)
+        return rows, sgn
+
+    def columns(self, idx):
+        """Dense n x p block Q[:, idx] (for callers; not on the hot path)."""
+        rows, sgn = self._rows(idx)
+        d = (rows * sgn[:, None]).contiguous()  # (p, q) == columns of X^T
+        out = self.backend.empty((d.shape[0], self.n))
+        for j in range(0, d.shape[0], 2):
+            k = min(2, d.shape[0] - j)
+            self.backend.dense_x(self, d[j:j + k], out[j:j + k], k)
+        return out.T
+
+    def submatrix(self, idx):
+        rows, sgn = self._rows(idx)
+        r = rows * sgn[:, None]
+        return r @ r.T
+
+    def diag(self):
+        d = (self.A * self.A).sum(dim=1)
+        return torch.cat([d, d]) if self.svr_block else d
+
+
+class DenseOperator(LinearKernelOperator):
+    """Explicit symmetric PSD Q (ref kernels.py:218-238), factored once on the host
+    as Q = X X^T with X = V diag(sqrt(max(ev, 0)))."""
+
+    def __init__(self, q, backend=None):
+        qh = np.asarray(q.detach().cpu().numpy() if isinstance(q, torch.Tensor) else q,
+                        dtype=np.float64)
+        if qh.ndim != 2 or qh.shape[0] != qh.shape[1]:
+            raise InputError("Q must be square")
+        ev, vec = np.linalg.eigh(0.5 * (qh + qh.T))
+        keep = ev > 1e-13 * max(float(ev.max()), 1.0)
+        factor = vec[:, keep] * np.sqrt(ev[keep])[None, :]
+        if factor.shape[1] == 0:
+            factor = np.zeros((qh.shape[0], 1))
+        super().__init__(np.ascontiguousarray(factor), backend=backend)
+        self.q_host = qh

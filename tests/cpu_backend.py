@@ -1,0 +1,168 @@
+"""TEST-ONLY CPU stand-in for CudaBackend (numpy / oracle arithmetic).
+
+It lets the host-side control flow of the solver (solver._Engine, the ALM /
+SsN loops, the line search batching, the sharded plumbing) run in the CPU test
+suite.  It is injected explicitly by tests; the product package never imports
+it and has no CPU path of its own.
+"""
+
+import numpy as np
+import torch
+
+import oracle as O
+from paper_1910_01312_b200 import _lib
+
+F64 = torch.float64
+
+
+class CpuTestBackend:
+    name = "cpu-test"
+
+    def __init__(self):
+        self.device = torch.device("cpu")
+        self.calls = {}
+
+    def _count(self, k):
+        self.calls[k] = self.calls.get(k, 0) + 1
+
+    # memory ------------------------------------------------------------------
+    def empty(self, shape, dtype=F64):
+        return torch.empty(shape, dtype=dtype)
+
+    def zeros(self, shape, dtype=F64):
+        return torch.zeros(shape, dtype=dtype)
+
+    def ws(self, key, nbytes):
+        return torch.zeros(max(int(nbytes), 256), dtype=torch.uint8)
+
+    def stream(self):
+        return None
+
+    def synchronize(self):
+        pass
+
+    @staticmethod
+    def host_buffer(shape, dtype):
+        return torch.empty(shape, dtype=dtype)
+
+    def new_states(self, T):
+        return torch.zeros((T, _lib.PROJ_STATE_DTYPE.itemsize), dtype=torch.uint8)
+
+    @staticmethod
+    def read_states(states_host):
+        return states_host.numpy().view(_lib.PROJ_STATE_DTYPE).reshape(-1)
+
+    # projection --------------------------------------------------------------
+    def project(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
+                ref=None, phases=7, passes=6):
+        self._count("project")
+        a = box.a_dev.numpy()
+        l = box.l.numpy()
+        u = box.u.numpy()
+        bl = O.BoxLine(a, box.d, l, u)
+        rec = self.read_states(states)
+        for t in range(T):
+            v = A.numpy().copy()
+            if B is not None:
+                v = v - float(coefs[t]) * B.numpy()
+            x, lam, free = O.project(v, bl)
+            r = v - x
+            rec[t]["lam"] = lam
+            rec[t]["sum_v2"] = float(v @ v)
+            rec[t]["sum_r2"] = float(r @ r)
+            rec[t]["sum_dref2"] = float(((x - ref.numpy()) ** 2).sum()) if ref is not None else 0.0
+            rec[t]["sum_a2_free"] = float((a[free] ** 2).sum())
+            rec[t]["nfree"] = int(free.sum())
+            rec[t]["status"] = _lib.PROJ_APPLIED
+            rec[t]["passes"] = 1
+            if x_out is not None:
+                x_out.view(-1, box.n)[t].copy_(torch.from_numpy(x))
+            if free_out is not None:
+                free_out.view(-1, box.n)[t].copy_(torch.from_numpy(free.astype(np.uint8)))
+
+    # vectors -----------------------------------------------------------------
+    def dots(self, pairs, out, mask=None):
+        self._count("dots")
+        m = None if mask is None else mask.numpy().astype(bool)
+        for j, (x, y) in enumerate(pairs):
+            xv = x.numpy()
+            yv = xv if y is None else y.numpy()
+            prod = xv * yv
+            out[j] = float(prod[m].sum() if m is not None else prod.sum())
+
+    def vec(self, op, alpha, x, y, z, out):
+        self._count("vec")
+        xv = x.numpy()
+        if op == 0:
+            r = xv + alpha * (y.numpy() + (z.numpy() if z is not None else 0.0))
+        elif op == 1:
+            r = (xv - y.numpy()) - z.numpy()
+        elif op == 2:
+            r = xv + alpha * y.numpy()
+        elif op == 3:
+            r = xv - y.numpy()
+        else:
+            r = alpha * xv
+        out.copy_(torch.from_numpy(np.ascontiguousarray(r)))
+
+    def hs_apply(self, free, a, y, beta, add, alpha, out):
+        self._count("hs_apply")
+        py = O.hs_apply(free.numpy().astype(bool), a.numpy(), y.numpy())
+        r = beta * py
+        if add is not None:
+            r = alpha * add.numpy() + r
+        out.copy_(torch.from_numpy(r))
+
+    def compact(self, mask, idx_out, count_out):
+        self._count("compact")
+        idx = np.flatnonzero(mask.numpy())
+        idx_out[: idx.size] = torch.from_numpy(idx.astype(np.int32))
+        count_out[0] = idx.size
+
+    # dense operator ------------------------------------------------------------
+    @staticmethod
+    def _x_rows(op):
+        A = op.A.numpy()
+        if op.row_sign is not None:
+            A = op.row_sign.numpy()[:, None] * A
+        return np.vstack([A, -A]) if op.svr_block else A
+
+    def dense_xt(self, op, vs, out):
+        self._count("dense_xt")
+        X = self._x_rows(op)
+        for j, v in enumerate(vs):
+            out[j] = torch.from_numpy(X.T @ v.numpy())
+
+    def dense_x(self, op, d, out, k=1):
+        self._count("dense_x")
+        X = self._x_rows(op)
+        dd = d.reshape(k, -1).numpy()
+        o = out.reshape(k, -1)
+        for j in range(k):
+            o[j] = torch.from_numpy(X @ dd[j])
+
+    def dense_gram(self, op, J, p_dev, p_max, a, sigma, asa_dev, M, m1):
+        self._count("dense_gram")
+        X = self._x_rows(op)
+        p = int(p_dev[0])
+        idx = J[:p].numpy().astype(np.int64)
+        Z = X[idx]
+        G = Z.T @ Z
+        m = Z.T @ a.numpy()[idx]
+        asa = float(asa_dev[0])
+        if asa != 0.0:
+            G = G - np.outer(m, m) / asa
+        M.copy_(torch.from_numpy(np.eye(G.shape[0]) + sigma * G))
+        m1.copy_(torch.from_numpy(m))
+
+    def chol_solve(self, M, m, b, scale, x, info):
+        self._count("chol_solve")
+        Mh = M.numpy()
+        try:
+            L = np.linalg.cholesky(Mh)
+        except np.linalg.LinAlgError:
+            info[0] = 1
+            return
+        y = np.linalg.solve(L, scale * b.numpy())
+        x.copy_(torch.from_numpy(np.linalg.solve(L.T, y)))
+        info[0] = 0

@@ -1,0 +1,177 @@
+"""Kernel-level parity of the sm_100a library against the oracle / golden vectors.
+
+Tolerances (BASELINE north_star): projection and operator products within
+1e-12 relative, free set J bit-exact given identical input vectors.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import load_cases
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import __graft_entry__ as g
+
+    g.build()
+    import paper_1910_01312_b200 as P
+
+    return P
+
+
+def _dev(x, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda")
+
+
+def test_projection_golden(pkg):
+    for c in load_cases("projection.npz", "p"):
+        box = pkg.BoxLineSet(c["a"], c["d"], c["l"], c["u"])
+        r = pkg.project_box_line(c["v"], box)
+        x = r.x.cpu().numpy()
+        scale = 1.0 + np.abs(c["x"]).max()
+        assert np.abs(x - c["x"]).max() <= 1e-12 * scale, (c["v"].size, np.abs(x - c["x"]).max())
+        assert abs(r.lambda_hat - c["lam"]) <= 1e-12 * (1.0 + abs(c["lam"]))
+        np.testing.assert_array_equal(r.active_mask.free_mask.cpu().numpy(), c["free"])
+
+
+def test_projection_random_vs_oracle(pkg):
+    rng = np.random.default_rng(11)
+    for trial in range(60):
+        n = int(rng.choice([1, 7, 100, 1000, 20000, 200000]))
+        a = rng.standard_normal(n)
+        a[rng.random(n) < 0.1] = 0.0
+        if trial % 3 == 0:  # SVM shape
+            a = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+            l, u = np.zeros(n), np.full(n, float(rng.choice([0.1, 1.0, 64.0])))
+        else:
+            l, u = -rng.random(n) - 0.1, rng.random(n) + 0.1
+        d = float(a @ (l + rng.random(n) * (u - l)))
+        v = rng.standard_normal(n) * rng.choice([0.5, 3.0, 100.0])
+        if trial % 5 == 0:  # heavy duplication of breakpoints
+            v = np.round(v, 1)
+        bl = O.BoxLine(a, d, l, u)
+        x_ref, lam_ref, free_ref = O.project(v, bl)
+        r = pkg.project_box_line(v, pkg.BoxLineSet(a, d, l, u))
+        x = r.x.cpu().numpy()
+        assert np.abs(x - x_ref).max() <= 1e-12 * (1.0 + np.abs(x_ref).max())
+        assert abs(r.lambda_hat - lam_ref) <= 1e-12 * (1.0 + abs(lam_ref))
+        np.testing.assert_array_equal(r.active_mask.free_mask.cpu().numpy().astype(bool), free_ref)
+        # feasibility at the reference's stated tolerances
+        assert abs(a @ x - d) <= 1e-9 * (1.0 + abs(d)) + 1e-12 * np.abs(a).sum() * np.abs(x).max()
+
+
+def test_projection_batched_trials(pkg):
+    from paper_1910_01312_b200 import backend as B
+
+    rng = np.random.default_rng(3)
+    n = 50000
+    y = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+    box = pkg.BoxLineSet(y, 0.0, np.zeros(n), np.ones(n))
+    be = box.backend
+    u = rng.standard_normal(n) * 2
+    qd = rng.standard_normal(n)
+    coefs = [3.0 * 0.5 ** j for j in range(4)]
+    states = be.new_states(4)
+    xo = be.empty((4, n))
+    fo = be.empty((4, n), torch.uint8)
+    st = be.project_sync(_dev(u), box, states, T=4, B=_dev(qd), coefs=coefs, x_out=xo, free_out=fo)
+    bl = O.BoxLine(y, 0.0, np.zeros(n), np.ones(n))
+    for t, cf in enumerate(coefs):
+        v = u - cf * qd
+        x_ref, lam_ref, free_ref = O.project(v, bl)
+        assert np.abs(xo[t].cpu().numpy() - x_ref).max() <= 1e-12
+        np.testing.assert_array_equal(fo[t].cpu().numpy().astype(bool), free_ref)
+        assert st["sum_v2"][t] == pytest.approx(v @ v, rel=1e-12)
+        assert st["sum_r2"][t] == pytest.approx(((v - x_ref) ** 2).sum(), rel=1e-10, abs=1e-14)
+        assert st["nfree"][t] == free_ref.sum()
+    del B
+
+
+def test_hs_jacobian_golden(pkg):
+    for c in load_cases("hs_jacobian.npz", "h"):
+        py = pkg.hs_jacobian_apply(_dev(c["free"], torch.uint8), c["a"], c["y"]).cpu().numpy()
+        np.testing.assert_allclose(py, c["py"], rtol=0, atol=1e-13)
+
+
+def test_dots_vec_compact(pkg):
+    be = pkg.default_backend()
+    rng = np.random.default_rng(5)
+    for n in (1, 33, 4097, 1_000_003):
+        xs = [rng.standard_normal(n) for _ in range(3)]
+        m = (rng.random(n) < 0.3).astype(np.uint8)
+        out = be.zeros(8)
+        be.dots([(_dev(xs[0]), _dev(xs[1])), (_dev(xs[2]), None)], out, mask=_dev(m, torch.uint8))
+        o = out.cpu().numpy()
+        mb = m.astype(bool)
+        assert o[0] == pytest.approx(float(xs[0][mb] @ xs[1][mb]), rel=1e-12, abs=1e-12)
+        assert o[1] == pytest.approx(float(xs[2][mb] @ xs[2][mb]), rel=1e-12, abs=1e-12)
+        # vec op 0: x + alpha (y + z), numpy rounding order -> bit exact
+        r = be.empty(n)
+        be.vec(0, -2.5, _dev(xs[0]), _dev(xs[1]), _dev(xs[2]), r)
+        np.testing.assert_array_equal(r.cpu().numpy(), xs[0] + (-2.5) * (xs[1] + xs[2]))
+        be.vec(1, 0.0, _dev(xs[0]), _dev(xs[1]), _dev(xs[2]), r)
+        np.testing.assert_array_equal(r.cpu().numpy(), (xs[0] - xs[1]) - xs[2])
+        idx = be.zeros(n, torch.int32)
+        cnt = be.zeros(1, torch.int64)
+        be.compact(_dev(m, torch.uint8), idx, cnt)
+        p = int(cnt.cpu()[0])
+        np.testing.assert_array_equal(idx[:p].cpu().numpy(), np.flatnonzero(m))
+
+
+@pytest.mark.parametrize("shape,svr,signed", [((1000, 50), False, True), ((3001, 300), False, True),
+                                              ((777, 500), True, False), ((20000, 333), False, False),
+                                              ((64, 7), True, False)])
+def test_dense_products(pkg, shape, svr, signed):
+    rng = np.random.default_rng(shape[0])
+    n, q = shape
+    A = rng.standard_normal((n, q))
+    y = np.where(rng.random(n) < 0.5, 1.0, -1.0) if signed else None
+    op = pkg.LinearKernelOperator(A, labels=y, svr_block=svr)
+    X = (y[:, None] * A) if signed else A
+    if svr:
+        X = np.vstack([A, -A])
+    v1, v2 = rng.standard_normal(X.shape[0]), rng.standard_normal(X.shape[0])
+    g = op.xt([_dev(v1), _dev(v2)]).cpu().numpy()
+    ref = X.T @ np.stack([v1, v2], axis=1)
+    assert np.abs(g.T - ref).max() <= 1e-12 * np.abs(X).sum(axis=0).max() * max(np.abs(v1).max(), 1)
+    d = rng.standard_normal((2, q))
+    out = op.x(_dev(d), k=2).cpu().numpy()
+    ref = X @ d.T
+    assert np.abs(out.T - ref).max() <= 1e-12 * np.abs(X).sum(axis=1).max() * np.abs(d).max()
+
+
+@pytest.mark.parametrize("n,q,p", [(500, 50, 37), (5000, 300, 300), (3000, 130, 1), (9000, 500, 2000)])
+def test_gram_and_cholesky(pkg, n, q, p):
+    rng = np.random.default_rng(q)
+    A = rng.standard_normal((n, q))
+    y = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+    op = pkg.LinearKernelOperator(A, labels=y)
+    be = op.backend
+    J = np.sort(rng.choice(n, size=p, replace=False)).astype(np.int32)
+    Jd = be.zeros(n, torch.int32)
+    Jd[:p] = _dev(J, torch.int32)
+    pdev = _dev(np.array([p]), torch.int64)
+    asa = float(p)  # a = y, a_J'a_J = p
+    asa_dev = _dev(np.array([asa]))
+    sigma = 7.5
+    M = be.empty((q, q))
+    m1 = be.empty(q)
+    be.dense_gram(op, Jd, pdev, n, _dev(y), sigma, asa_dev, M, m1)
+    X = y[:, None] * A
+    Z = X[J]
+    m1_ref = Z.T @ y[J]
+    M_ref = np.eye(q) + sigma * (Z.T @ Z - np.outer(m1_ref, m1_ref) / asa)
+    np.testing.assert_allclose(m1.cpu().numpy(), m1_ref, rtol=1e-12, atol=1e-10)
+    np.testing.assert_allclose(M.cpu().numpy(), M_ref, rtol=1e-12, atol=1e-9 * sigma * p)
+    b = rng.standard_normal(q)
+    xo = be.empty(q)
+    info = be.zeros(1, torch.int32)
+    be.chol_solve(M, q, _dev(b), -1.0, xo, info)
+    assert int(info.cpu()[0]) == 0
+    x_ref = -np.linalg.solve(M_ref, b)
+    assert np.linalg.norm(xo.cpu().numpy() - x_ref) <= 1e-10 * np.linalg.cond(M_ref) * np.linalg.norm(x_ref)

@@ -1,0 +1,88 @@
+"""End-to-end SSsNAL parity on the GPU against golden reference runs and the oracle.
+
+Bar (BASELINE north_star): dual objective within 1e-6 relative at KKT <= tol;
+iteration counts reported alongside.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import load_cases
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import __graft_entry__ as g
+
+    g.build()
+    import paper_1910_01312_b200 as P
+
+    return P
+
+
+def _problem(P, c):
+    if c["kind"] == "dense":
+        return P.QpProblem(P.DenseOperator(c["G"].T @ c["G"]), c["c"],
+                           P.BoxLineSet(c["a"], c["d"], c["l"], c["u"]))
+    if c["kind"] == "csvc":
+        return P.build_csvc_dual(c["A"], c["y"], c["C"])
+    return P.build_svr_dual(c["A"], c["t"], c["C"], c["eps"])
+
+
+def test_alm_solve_golden(pkg):
+    for c in load_cases("solve.npz", "s"):
+        rep = pkg.alm_solve(_problem(pkg, c), pkg.AlmOptions(tol_kkt=c["tol"]))
+        assert rep.converged or not c["converged"]
+        if rep.converged:
+            assert rep.kkt_residual < c["tol"]
+        assert rep.objective == pytest.approx(c["obj"], rel=1e-6, abs=1e-9)
+        if c["kind"] != "dense":  # SVM duals: same iteration counts as the reference
+            assert (rep.outer_iters, rep.total_inner_iters) == (c["outer"], c["inner"])
+            assert np.linalg.norm(rep.x_opt - c["x_opt"]) <= 1e-6 * (1 + np.linalg.norm(c["x_opt"]))
+
+
+def test_kkt_residual_golden(pkg):
+    for c in load_cases("kkt.npz", "k"):
+        pb = pkg.QpProblem(pkg.DenseOperator(c["G"].T @ c["G"]), c["c"],
+                           pkg.BoxLineSet(c["a"], c["d"], c["l"], c["u"]))
+        assert pkg.kkt_residual(c["x"], pb) == pytest.approx(c["kkt"], rel=1e-10)
+
+
+def test_tiny_instance(pkg):
+    pb = pkg.QpProblem(pkg.DenseOperator(np.eye(2)), -np.ones(2),
+                       pkg.BoxLineSet(np.ones(2), 1.0, np.zeros(2), np.ones(2)))
+    rep = pkg.alm_solve(pb, pkg.AlmOptions(tol_kkt=1e-10))
+    np.testing.assert_allclose(rep.x_opt, [0.5, 0.5], atol=1e-9)
+    assert rep.converged and rep.objective == pytest.approx(-0.75)
+
+
+@pytest.mark.parametrize("n,q,seed", [(8000, 120, 1), (20000, 300, 2)])
+def test_gaussian_mixture_vs_oracle(pkg, n, q, seed):
+    from paper_1910_01312_b200 import datagen
+
+    cfg = datagen.config1(seed=seed, n=n, q=q)
+    rep = pkg.alm_solve(pkg.build_csvc_dual(cfg["A"], cfg["y"], cfg["C"]),
+                        pkg.AlmOptions(tol_kkt=1e-6))
+    op, c, bl = O.csvc_problem(cfg["A"], cfg["y"], cfg["C"])
+    ref = O.alm_solve(op, c, bl, O.AlmOpts(tol_kkt=1e-6))
+    assert rep.converged and rep.kkt_residual < 1e-6
+    assert rep.objective == pytest.approx(ref["objective"], rel=1e-6)
+    # the returned x is the projection at the GPU iterate: feasibility to 1e-10
+    y = cfg["y"]
+    assert abs(float(y @ rep.x_opt)) <= 1e-9 * (1 + np.abs(rep.x_opt).sum())
+    assert rep.x_opt.min() >= 0.0 and rep.x_opt.max() <= cfg["C"]
+
+
+def test_svr_vs_oracle(pkg):
+    rng = np.random.default_rng(4)
+    n, q = 4000, 40
+    A = rng.standard_normal((n, q))
+    t = A @ (rng.standard_normal(q) / np.sqrt(q)) + 0.1 * rng.standard_normal(n)
+    rep = pkg.alm_solve(pkg.build_svr_dual(A, t, 1.0, 0.1), pkg.AlmOptions(tol_kkt=1e-6))
+    op, c, bl = O.svr_problem(A, t, 1.0, 0.1)
+    ref = O.alm_solve(op, c, bl, O.AlmOpts(tol_kkt=1e-6))
+    assert rep.converged
+    assert rep.objective == pytest.approx(ref["objective"], rel=1e-6)
