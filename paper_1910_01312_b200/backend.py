@@ -102,6 +102,8 @@ class CudaBackend:
         """out[j] = sum m x_j y_j (y None => x^2); pairs <= 8; async."""
         k = len(pairs)
         n = pairs[0][0].numel()
+        if any(x.numel() != n or (y is not None and y.numel() != n) for x, y in pairs):
+            raise InputError("dots: all vectors of one call must have the same length")
         xs, keep1 = _lib.ptr_array([_ptr(x) for x, _ in pairs])
         ys, keep2 = _lib.ptr_array([_ptr(y) for _, y in pairs])
         ws = self.ws("reduce", self.lib.ssnal_reduce_ws_bytes(n, k))

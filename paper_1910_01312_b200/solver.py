@@ -287,8 +287,8 @@ class _Engine:
         op.x(self.t, self.qdir.view(1, -1), k=1)
         # d = -s - sigma P(Qd)  (ref solver.py:269)
         be.hs_apply(self.free, self.box.a_dev, self.qdir, -sigma, self.s, -1.0, self.dir)
-        be.dots([(self.grad, self.dir), (self.w, self.qw), (self.w, self.qdir),
-                 (self.t[0], None)], self.scal)
+        be.dots([(self.grad, self.dir), (self.w, self.qw), (self.w, self.qdir)], self.scal)
+        be.dots([(self.t[0], None)], self.scal[3:4])  # length q, separate reduction
 
     def pb_direct_limit(self):
         return self._direct_limit

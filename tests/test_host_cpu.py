@@ -1,0 +1,69 @@
+"""Host-side solver logic on the CPU (no GPU): the device control flow of
+solver._Engine driven by the TEST-ONLY CpuTestBackend, checked against golden
+reference runs.  Verifies the factor-space Newton system reproduces the
+reference's iterates (same outer/inner counts on the SVM duals)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_cases
+from cpu_backend import CpuTestBackend
+
+
+@pytest.fixture(scope="module")
+def mods():
+    from paper_1910_01312_b200 import operators, projection, solver, svm
+
+    return operators, projection, solver, svm
+
+
+def _problem(mods, c, be):
+    operators, projection, solver, svm = mods
+    if c["kind"] == "dense":
+        return solver.QpProblem(operators.DenseOperator(c["G"].T @ c["G"], backend=be), c["c"],
+                                projection.BoxLineSet(c["a"], c["d"], c["l"], c["u"], backend=be))
+    if c["kind"] == "csvc":
+        return svm.build_csvc_dual(c["A"], c["y"], c["C"], backend=be)
+    return svm.build_svr_dual(c["A"], c["t"], c["C"], c["eps"], backend=be)
+
+
+def test_alm_solve_host_logic_matches_reference(mods):
+    solver = mods[2]
+    be = CpuTestBackend()
+    for c in load_cases("solve.npz", "s"):
+        rep = solver.alm_solve(_problem(mods, c, be), solver.AlmOptions(tol_kkt=c["tol"]))
+        assert rep.objective == pytest.approx(c["obj"], rel=1e-6, abs=1e-9)
+        if c["kind"] != "dense":
+            assert rep.converged and rep.kkt_residual < c["tol"]
+            assert (rep.outer_iters, rep.total_inner_iters) == (c["outer"], c["inner"])
+            np.testing.assert_allclose(rep.x_opt, c["x_opt"], atol=1e-8)
+
+
+def test_newton_direction_factor_space_matches_reference(mods):
+    operators, projection, solver, _ = mods
+    be = CpuTestBackend()
+    for c in load_cases("newton.npz", "n"):
+        q = c["G"].T @ c["G"]
+        pb = solver.QpProblem(operators.DenseOperator(q, backend=be), c["c"],
+                              projection.BoxLineSet(c["a"], c["d"], c["l"], c["u"], backend=be))
+        eng = pb.engine()
+        sc, cur = eng.start_inner(torch.from_numpy(c["x"]), torch.from_numpy(c["w"].copy()),
+                                  torch.from_numpy(q @ c["w"]), c["sigma"])
+        np.testing.assert_array_equal(eng.free.numpy(), c["free"])
+        eng.direction(int(cur["nfree"]), c["sigma"])
+        sc, _ = eng.fetch(info=True)
+        assert np.linalg.norm(eng.qdir.numpy() - c["qdir"]) <= 1e-10 * (1 + np.linalg.norm(c["qdir"]))
+        assert sc[3] == pytest.approx(c["dqd"], rel=1e-9, abs=1e-12)
+
+
+def test_batched_line_search_picks_reference_alpha(mods):
+    """Armijo with batched step lengths returns the same alpha as sequential halving."""
+    operators, projection, solver, svm = mods
+    be = CpuTestBackend()
+    c = load_cases("solve.npz", "s")[12]  # config 0
+    for batch in (1, 3, 4):
+        pb = svm.build_csvc_dual(c["A"], c["y"], c["C"], backend=be)
+        rep = solver.alm_solve(pb, solver.AlmOptions(tol_kkt=c["tol"]),
+                               solver.SsnOptions(line_search_batch=batch))
+        assert (rep.outer_iters, rep.total_inner_iters) == (c["outer"], c["inner"])
