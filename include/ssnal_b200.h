@@ -42,6 +42,8 @@ typedef struct ssnal_proj_state_t {
   double sum_r2;                  /* sum (v_i - x_i)^2                                  */
   double sum_dref2;               /* sum (x_i - ref_i)^2 (ref optional)                 */
   double sum_a2_free;             /* a_J' a_J over the free set (a' Sigma a)            */
+  double sum_xv;                  /* sum x_i (2 v_i - x_i) = ||v||^2 - ||v - x||^2 without
+                                     cancellation (the psi term of ref solver.py:130-133) */
   long long nfree;                /* p = |J|                                            */
   int status;                     /* 3 applied, 2 lambda known, <0 infeasible, else searching */
   int passes;                     /* K-ary bracketing passes used                       */
@@ -52,6 +54,7 @@ typedef struct ssnal_proj_state_t {
 /* ---- library / device ------------------------------------------------- */
 const char* ssnal_version(void);
 const char* ssnal_last_error(void);
+unsigned long long ssnal_launch_count(void);        /* kernels launched by this library */
 int ssnal_device_check(int device);                 /* SSNAL_E_DEVICE unless sm_100 */
 size_t ssnal_proj_state_bytes(void);
 size_t ssnal_project_ws_bytes(int64_t n, int T);

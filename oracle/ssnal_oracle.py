@@ -26,7 +26,7 @@ __all__ = [
     "grad_phi", "breakpoints", "classify_free", "project", "hs_apply",
     "DenseQ", "FactoredQ", "SvrFactoredQ",
     "AlmOpts", "SsnOpts", "psi_value", "newton_direction", "line_search",
-    "ssn_solve", "kkt_residual", "alm_solve",
+    "ssn_solve", "kkt_residual", "alm_solve", "set_psi_mode", "PSI_MODE",
     "csvc_problem", "svr_problem", "objective",
 ]
 
@@ -282,8 +282,23 @@ class SsnOpts:
         self.cg_max_iters = cg_max_iters
 
 
+PSI_MODE = {"mode": "reference"}
+
+
+def set_psi_mode(mode):
+    """'reference' (ref solver.py:130-133 verbatim) or 'stable': the same psi with
+    ||u||^2 - ||u - Pi(u)||^2 evaluated as Pi(u)'(2u - Pi(u)) -- identical in exact
+    arithmetic, free of the cancellation that stalls Armijo when ||u|| >> ||Pi(u)||
+    (the product path's evaluation)."""
+    if mode not in ("reference", "stable"):
+        raise ValueError(mode)
+    PSI_MODE["mode"] = mode
+
+
 def psi_value(w_qw, u, px, x_sq, sigma):
     """ref solver.py:130-133."""
+    if PSI_MODE["mode"] == "stable":
+        return 0.5 * w_qw + float(px.dot(2.0 * u - px)) / (2.0 * sigma) - x_sq / (2.0 * sigma)
     r = u - px
     return 0.5 * w_qw + (float(u.dot(u)) - float(r.dot(r))) / (2.0 * sigma) - x_sq / (2.0 * sigma)
 

@@ -19,7 +19,7 @@ PROJ_STATE_DTYPE = np.dtype([
     ("lo", "f8"), ("hi", "f8"), ("flo", "f8"), ("fhi", "f8"),
     ("below_max", "f8"), ("above_min", "f8"), ("in_min", "f8"), ("in_max", "f8"),
     ("in_count", "i8"), ("lam", "f8"), ("tmin", "f8"), ("tmax", "f8"),
-    ("sum_v2", "f8"), ("sum_r2", "f8"), ("sum_dref2", "f8"), ("sum_a2_free", "f8"),
+    ("sum_v2", "f8"), ("sum_r2", "f8"), ("sum_dref2", "f8"), ("sum_a2_free", "f8"), ("sum_xv", "f8"),
     ("nfree", "i8"), ("status", "i4"), ("passes", "i4"), ("ticket", "u4"), ("pad_", "u4"),
 ])
 
@@ -37,6 +37,7 @@ _SZ = ctypes.c_size_t
 _SIGNATURES = {
     "ssnal_version": (ctypes.c_char_p, []),
     "ssnal_last_error": (ctypes.c_char_p, []),
+    "ssnal_launch_count": (ctypes.c_ulonglong, []),
     "ssnal_device_check": (_I, [_I]),
     "ssnal_proj_state_bytes": (_SZ, []),
     "ssnal_project_ws_bytes": (_SZ, [_I64, _I]),

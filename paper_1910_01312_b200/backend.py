@@ -32,6 +32,36 @@ class CudaBackend:
         self.lib = _lib.load()
         _lib.call("ssnal_device_check", self.device.index)
         self._ws = {}
+        self.timing = None  # list of (op, start_event, end_event, algorithmic bytes) when on
+
+    # ---------------------------------------------------------------- profiling
+    def start_timing(self):
+        self.timing = []
+
+    def stop_timing(self):
+        """Per-op totals {op: (launch count, seconds, algorithmic bytes)} from CUDA events
+        recorded on the launching stream around every timed op."""
+        torch.cuda.synchronize(self.device)
+        out = {}
+        for op, e0, e1, nbytes in self.timing or []:
+            c, t, b = out.get(op, (0, 0.0, 0.0))
+            out[op] = (c + 1, t + e0.elapsed_time(e1) * 1e-3, b + nbytes)
+        self.timing = None
+        return out
+
+    def _timed(self, op, nbytes, fn, *args):
+        if self.timing is None:
+            return fn(*args)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        s = torch.cuda.current_stream(self.device)
+        e0.record(s)
+        fn(*args)
+        e1.record(s)
+        self.timing.append((op, e0, e1, nbytes))
+
+    def launch_count(self):
+        return int(self.lib.ssnal_launch_count())
 
     # ---------------------------------------------------------------- memory
     def empty(self, shape, dtype=F64):
@@ -74,7 +104,10 @@ class CudaBackend:
         if B is not None:
             coef_arr = (_lib.ctypes.c_double * T)(*[float(c) for c in coefs])
         ws = self.ws("proj", self.lib.ssnal_project_ws_bytes(n, T))
-        _lib.call(
+        # per streaming phase: v (+ B) and a, (+ l, u vectors), once per launch
+        per_phase = 8 * n * (2 + (B is not None) + (box.l_dev is not None) + (box.u_dev is not None))
+        self._timed(
+            "project", per_phase * (3 + passes), _lib.call,
             "ssnal_project", _ptr(A), _ptr(B),
             _lib.ctypes.cast(coef_arr, _lib.ctypes.c_void_p) if coef_arr is not None else None,
             _ptr(box.a_dev), _ptr(box.l_dev), _ptr(box.u_dev), box.l_const, box.u_const, box.d,
@@ -127,27 +160,39 @@ class CudaBackend:
                   self.stream())
 
     # ---------------------------------------------------------------- dense operator
+    @staticmethod
+    def dense_bytes(op, k, direction):
+        """Algorithmic HBM bytes of one X^T V (direction 't') or X D ('x') product:
+        the sample matrix once, the row signs, the k input and k output vectors."""
+        a_bytes = 8 * op.n_phys * op.q + (8 * op.n_phys if op.row_sign is not None else 0)
+        if direction == "t":
+            return a_bytes + 8 * k * op.n + 8 * k * op.q
+        return a_bytes + 8 * k * op.q + 8 * k * op.n
+
     def dense_xt(self, op, vs, out):
         k = len(vs)
         arr, keep = _lib.ptr_array([_ptr(v) for v in vs])
         ws = self.ws("xt", self.lib.ssnal_dense_xt_ws_bytes(op.n_phys, op.q, k))
-        _lib.call("ssnal_dense_xt", _ptr(op.A), op.n_phys, op.q, op.lda, _ptr(op.row_sign),
-                  int(op.svr_block), k, arr, _ptr(out), _ptr(ws), self.stream())
+        self._timed("dense_xt", self.dense_bytes(op, k, "t"), _lib.call, "ssnal_dense_xt",
+                    _ptr(op.A), op.n_phys, op.q, op.lda, _ptr(op.row_sign), int(op.svr_block), k,
+                    arr, _ptr(out), _ptr(ws), self.stream())
         del keep
 
     def dense_x(self, op, d, out, k=1):
-        _lib.call("ssnal_dense_x", _ptr(op.A), op.n_phys, op.q, op.lda, _ptr(op.row_sign),
-                  int(op.svr_block), k, _ptr(d), _ptr(out), self.stream())
+        self._timed("dense_x", self.dense_bytes(op, k, "x"), _lib.call, "ssnal_dense_x",
+                    _ptr(op.A), op.n_phys, op.q, op.lda, _ptr(op.row_sign), int(op.svr_block), k,
+                    _ptr(d), _ptr(out), self.stream())
 
     def dense_gram(self, op, J, p_dev, p_max, a, sigma, asa_dev, M, m1):
         ws = self.ws("gram", self.lib.ssnal_gram_ws_bytes(op.q))
-        _lib.call("ssnal_dense_gram", _ptr(op.A), op.n_phys, op.q, op.lda, _ptr(op.row_sign),
-                  int(op.svr_block), _ptr(J), _ptr(p_dev), int(p_max), _ptr(a), float(sigma),
-                  _ptr(asa_dev), _ptr(M), _ptr(m1), _ptr(ws), self.stream())
+        self._timed("dense_gram", 0, _lib.call, "ssnal_dense_gram", _ptr(op.A), op.n_phys, op.q,
+                    op.lda, _ptr(op.row_sign), int(op.svr_block), _ptr(J), _ptr(p_dev),
+                    int(p_max), _ptr(a), float(sigma), _ptr(asa_dev), _ptr(M), _ptr(m1), _ptr(ws),
+                    self.stream())
 
     def chol_solve(self, M, m, b, scale, x, info):
-        _lib.call("ssnal_chol_solve", _ptr(M), int(m), _ptr(b), float(scale), _ptr(x),
-                  _ptr(info), self.stream())
+        self._timed("chol_solve", 16 * m * m, _lib.call, "ssnal_chol_solve", _ptr(M), int(m),
+                    _ptr(b), float(scale), _ptr(x), _ptr(info), self.stream())
 
 
 _DEFAULT = {}

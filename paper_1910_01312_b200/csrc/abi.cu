@@ -34,6 +34,13 @@ cudaError_t launch_chol_solve(double* M, long long m, const double* b, double sc
                               int* info, cudaStream_t s);
 }  // namespace ssnal
 
+#include <atomic>
+
+namespace ssnal {
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace ssnal
+
 using namespace ssnal;
 
 static thread_local char g_err[512] = "";
@@ -56,6 +63,8 @@ extern "C" {
 const char* ssnal_version(void) { return "ssnal_b200 0.1.0 (sm_100a)"; }
 
 const char* ssnal_last_error(void) { return g_err; }
+
+unsigned long long ssnal_launch_count(void) { return g_launches.load(); }
 
 int ssnal_device_check(int device) {
   cudaDeviceProp prop;

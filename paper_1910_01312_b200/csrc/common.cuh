@@ -76,3 +76,8 @@ __device__ __forceinline__ bool last_block_arrive(unsigned int* ticket, unsigned
 __host__ __device__ inline long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
 
 }  // namespace ssnal
+
+namespace ssnal {
+// host-side count of kernel launches issued by this library (ssnal_launch_count)
+void note_launch();
+}  // namespace ssnal

@@ -115,15 +115,15 @@ cudaError_t launch_dense_xt(const double* A, long long n, long long q, long long
   dim3 grid(nsplit, (unsigned)ceil_div(q, XT_PANEL));
   for (int j = 0; j < k;) {
     if (k - j >= 2) {
-      dense_xt_kernel<2><<<grid, XT_WARPS * 32, 0, stream>>>(p, j);
+      { note_launch(); dense_xt_kernel<2><<<grid, XT_WARPS * 32, 0, stream>>>(p, j); }
       j += 2;
     } else {
-      dense_xt_kernel<1><<<grid, XT_WARPS * 32, 0, stream>>>(p, j);
+      { note_launch(); dense_xt_kernel<1><<<grid, XT_WARPS * 32, 0, stream>>>(p, j); }
       j += 1;
     }
   }
   long long tot = (long long)k * q;
-  dense_xt_fold_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, stream>>>(p.part, nsplit, k, q, out);
+  { note_launch(); dense_xt_fold_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, stream>>>(p.part, nsplit, k, q, out); }
   return cudaGetLastError();
 }
 
@@ -193,11 +193,11 @@ cudaError_t launch_dense_x(const double* A, long long n, long long q, long long 
     if (kv == 2) {
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(dense_x_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      dense_x_kernel<2><<<(unsigned)blocks, X_WARPS * 32, smem, stream>>>(A, n, q, lda, rs, svr, d, k, j, out, nlog);
+      { note_launch(); dense_x_kernel<2><<<(unsigned)blocks, X_WARPS * 32, smem, stream>>>(A, n, q, lda, rs, svr, d, k, j, out, nlog); }
     } else {
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(dense_x_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      dense_x_kernel<1><<<(unsigned)blocks, X_WARPS * 32, smem, stream>>>(A, n, q, lda, rs, svr, d, k, j, out, nlog);
+      { note_launch(); dense_x_kernel<1><<<(unsigned)blocks, X_WARPS * 32, smem, stream>>>(A, n, q, lda, rs, svr, d, k, j, out, nlog); }
     }
     j += kv;
   }
@@ -347,11 +347,11 @@ cudaError_t launch_dense_gram(const double* A, long long n, long long q, long lo
   g.ntile = (int)ceil_div(q, GT);
   double* part_m1 = g.part + (long long)GSPLIT * q * q;
   int npairs = g.ntile * (g.ntile + 1) / 2;
-  gram_kernel<<<dim3(npairs, GSPLIT), 256, 0, stream>>>(g);
-  gram_m1_kernel<<<dim3((unsigned)ceil_div(q, 256), GSPLIT), 256, 0, stream>>>(g, a, rs, svr, part_m1);
-  gram_m1_fold_kernel<<<(unsigned)ceil_div(q, 256), 256, 0, stream>>>(part_m1, q, m1);
-  gram_assemble_kernel<<<(unsigned)ceil_div(q * q, 256), 256, 0, stream>>>(g.part, q, m1, sigma,
-                                                                          asa_dev, M);
+  { note_launch(); gram_kernel<<<dim3(npairs, GSPLIT), 256, 0, stream>>>(g); }
+  { note_launch(); gram_m1_kernel<<<dim3((unsigned)ceil_div(q, 256), GSPLIT), 256, 0, stream>>>(g, a, rs, svr, part_m1); }
+  { note_launch(); gram_m1_fold_kernel<<<(unsigned)ceil_div(q, 256), 256, 0, stream>>>(part_m1, q, m1); }
+  { note_launch(); gram_assemble_kernel<<<(unsigned)ceil_div(q * q, 256), 256, 0, stream>>>(g.part, q, m1, sigma,
+                                                                          asa_dev, M); }
   return cudaGetLastError();
 }
 

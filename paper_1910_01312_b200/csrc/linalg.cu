@@ -146,7 +146,7 @@ cudaError_t launch_chol_solve(double* M, long long m, const double* b, double sc
   cudaError_t e = cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  chol_solve_kernel<<<1, CH_NT, smem, stream>>>(M, m, b, scale, x, info);
+  { note_launch(); chol_solve_kernel<<<1, CH_NT, smem, stream>>>(M, m, b, scale, x, info); }
   return cudaGetLastError();
 }
 

@@ -298,12 +298,12 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_exact_kernel(ProjArgs p) {
 
 // ------------------------------------------------------------------ apply
 __global__ void __launch_bounds__(SSNAL_NT) proj_apply_kernel(ProjArgs p) {
-  __shared__ double red[5 * 32];
+  __shared__ double red[6 * 32];
   const int t = blockIdx.y;
   ProjState* st = p.st + t;
   if (st->status != PROJ_DONE) return;
   const double lam = st->lam;
-  double sv2 = 0.0, sr2 = 0.0, sd2 = 0.0, sa2 = 0.0, nfree = 0.0;
+  double sv2 = 0.0, sr2 = 0.0, sd2 = 0.0, sa2 = 0.0, nfree = 0.0, sxv = 0.0;
   double* xo = p.x_out ? p.x_out + (long long)t * p.n : nullptr;
   unsigned char* fo = p.free_out ? p.free_out + (long long)t * p.n : nullptr;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
@@ -321,26 +321,28 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_apply_kernel(ProjArgs p) {
     double r = v - x;
     sv2 += v * v;
     sr2 += r * r;
+    sxv += x * (2.0 * v - x);
     if (p.ref) { double dd = x - p.ref[i]; sd2 += dd * dd; }
     if (fr) { sa2 += a * a; nfree += 1.0; }
   }
-  double vals[5] = {sv2, sr2, sd2, sa2, nfree};
-  const int ops[5] = {0, 0, 0, 0, 0};
-  block_reduce<5>(vals, ops, red);
+  double vals[6] = {sv2, sr2, sd2, sa2, nfree, sxv};
+  const int ops[6] = {0, 0, 0, 0, 0, 0};
+  block_reduce<6>(vals, ops, red);
   double* mine = p.part + ((long long)t * gridDim.x + blockIdx.x) * PSTRIDE;
   if (threadIdx.x == 0)
-    for (int k = 0; k < 5; ++k) mine[k] = vals[k];
+    for (int k = 0; k < 6; ++k) mine[k] = vals[k];
   if (!last_block_arrive(&st->ticket, gridDim.x)) return;
   if (threadIdx.x != 0) return;
   const double* base = p.part + (long long)t * gridDim.x * PSTRIDE;
-  double r[5] = {0, 0, 0, 0, 0};
+  double r[6] = {0, 0, 0, 0, 0, 0};
   for (unsigned b = 0; b < gridDim.x; ++b)
-    for (int k = 0; k < 5; ++k) r[k] += __ldcg(base + (long long)b * PSTRIDE + k);
+    for (int k = 0; k < 6; ++k) r[k] += __ldcg(base + (long long)b * PSTRIDE + k);
   st->sum_v2 = r[0];
   st->sum_r2 = r[1];
   st->sum_dref2 = r[2];
   st->sum_a2_free = r[3];
   st->nfree = (long long)r[4];
+  st->sum_xv = r[5];
   st->status = PROJ_APPLIED;
 }
 
@@ -362,10 +364,10 @@ cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
   p.lc = L.lc; p.uc = L.uc; p.d = L.d; p.n = L.n; p.st = L.st; p.part = L.part;
   p.x_out = L.x_out; p.free_out = L.free_out; p.ref = L.ref;
   dim3 grid(proj_blocks(L.n), L.T);
-  if (L.phases & PHASE_RANGE) proj_range_kernel<<<grid, SSNAL_NT, 0, stream>>>(p);
-  for (int k = 0; k < L.passes; ++k) proj_pass_kernel<<<grid, SSNAL_NT, 0, stream>>>(p);
-  if (L.phases & PHASE_EXACT) proj_exact_kernel<<<grid, SSNAL_NT, 0, stream>>>(p);
-  if (L.phases & PHASE_APPLY) proj_apply_kernel<<<grid, SSNAL_NT, 0, stream>>>(p);
+  if (L.phases & PHASE_RANGE) { note_launch(); proj_range_kernel<<<grid, SSNAL_NT, 0, stream>>>(p); }
+  for (int k = 0; k < L.passes; ++k) { note_launch(); proj_pass_kernel<<<grid, SSNAL_NT, 0, stream>>>(p); }
+  if (L.phases & PHASE_EXACT) { note_launch(); proj_exact_kernel<<<grid, SSNAL_NT, 0, stream>>>(p); }
+  if (L.phases & PHASE_APPLY) { note_launch(); proj_apply_kernel<<<grid, SSNAL_NT, 0, stream>>>(p); }
   return cudaGetLastError();
 }
 

@@ -72,7 +72,7 @@ cudaError_t launch_dots(int k, const double* const* xs, const double* const* ys,
   p.out = out;
   p.ticket = (unsigned int*)ws;
   p.part = (double*)((char*)ws + TICKET_BYTES);
-  dots_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(p);
+  { note_launch(); dots_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(p); }
   return cudaGetLastError();
 }
 
@@ -99,7 +99,7 @@ __global__ void vec_kernel(int op, long long n, double alpha, const double* __re
 
 cudaError_t launch_vec(int op, long long n, double alpha, const double* x, const double* y,
                        const double* z, double* out, cudaStream_t stream) {
-  vec_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(op, n, alpha, x, y, z, out);
+  { note_launch(); vec_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(op, n, alpha, x, y, z, out); }
   return cudaGetLastError();
 }
 
@@ -129,8 +129,8 @@ cudaError_t launch_hs_apply(const uint8_t* fm, const double* a, const double* y,
   const double* ys[2] = {y, nullptr};
   cudaError_t e = launch_dots(2, xs, ys, fm, n, sums, ws, stream);
   if (e != cudaSuccess) return e;
-  hs_finish_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(fm, a, y, n, beta, add, alpha,
-                                                                  out, sums);
+  { note_launch(); hs_finish_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(fm, a, y, n, beta, add, alpha,
+                                                                  out, sums); }
   return cudaGetLastError();
 }
 
@@ -229,8 +229,8 @@ cudaError_t launch_compact(const uint8_t* m, long long n, int32_t* idx, long lon
   if (ntiles < 1) ntiles = 1;
   unsigned int* ticket = (unsigned int*)ws;
   int* tile = (int*)((char*)ws + TICKET_BYTES);
-  compact_count_kernel<<<ntiles, SSNAL_NT, 0, stream>>>(m, n, tile, count, ticket, ntiles);
-  compact_write_kernel<<<ntiles, SSNAL_NT, 0, stream>>>(m, n, tile, idx);
+  { note_launch(); compact_count_kernel<<<ntiles, SSNAL_NT, 0, stream>>>(m, n, tile, count, ticket, ntiles); }
+  { note_launch(); compact_write_kernel<<<ntiles, SSNAL_NT, 0, stream>>>(m, n, tile, idx); }
   return cudaGetLastError();
 }
 

@@ -70,6 +70,7 @@ class SsnOptions:
     direct_solve_threshold: int = 2000
     cg_max_iters: int = 500
     line_search_batch: int = 4
+    psi_eval: str = "stable"  # or "reference": ref solver.py:130-133 term for term
 
 
 @dataclass
@@ -327,8 +328,7 @@ class _Engine:
                                      x_out=self.tx, free_out=self.tfree, ref=self.x)
             for j, a in enumerate(alphas):
                 quad = wqw + 2.0 * a * wqdir + a * a * dqd
-                psi_t = (0.5 * quad + (float(st["sum_v2"][j]) - float(st["sum_r2"][j]))
-                         / (2.0 * sigma) - x_sq / (2.0 * sigma))
+                psi_t = _psi(quad, st[j], x_sq, sigma, opts.psi_eval)
                 if psi_t <= psi0 + opts.mu * a * gd:
                     return a, j, st[j], psi_t
             tried += T
@@ -345,9 +345,18 @@ class _Engine:
         self.st_cur.copy_(self.st_trial[j:j + 1])
 
 
-def _psi(wqw, sum_u2, sum_r2, x_sq, sigma):
-    """ref solver.py:130-133 from the fused sums."""
-    return 0.5 * wqw + (sum_u2 - sum_r2) / (2.0 * sigma) - x_sq / (2.0 * sigma)
+def _psi(wqw, rec, x_sq, sigma, mode="stable"):
+    """psi^k(w) of ref solver.py:130-133 from the projection's fused sums.
+
+    'reference' forms ||u||^2 - ||u - Pi(u)||^2 as the difference of two sums,
+    exactly as the reference; its rounding error ~ eps ||u||^2 / sigma swamps the
+    Armijo decrease once ||u|| >> ||Pi(u)|| (config 1 stalls at R_KKT 3.7e-6).
+    'stable' uses the identical quantity sum Pi(u)_i (2 u_i - Pi(u)_i)."""
+    if mode == "reference":
+        diff = float(rec["sum_v2"]) - float(rec["sum_r2"])
+    else:
+        diff = float(rec["sum_xv"])
+    return 0.5 * wqw + diff / (2.0 * sigma) - x_sq / (2.0 * sigma)
 
 
 @dataclass
@@ -396,7 +405,7 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
             sc = eng.steepest()
             gd, wqw, wqdir, dqd = (float(v) for v in sc[:4])
             steepest = True
-        psi0 = _psi(wqw, float(cur["sum_v2"]), float(cur["sum_r2"]), x_sq, sigma)
+        psi0 = _psi(wqw, cur, x_sq, sigma, ssn_opts.psi_eval)
         if ssn_opts.mu * abs(gd) <= 1e-16 * (1.0 + abs(psi0)):
             converged, exhausted = True, False
             break

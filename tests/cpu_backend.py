@@ -70,6 +70,7 @@ class CpuTestBackend:
             rec[t]["lam"] = lam
             rec[t]["sum_v2"] = float(v @ v)
             rec[t]["sum_r2"] = float(r @ r)
+            rec[t]["sum_xv"] = float(x @ (2.0 * v - x))
             rec[t]["sum_dref2"] = float(((x - ref.numpy()) ** 2).sum()) if ref is not None else 0.0
             rec[t]["sum_a2_free"] = float((a[free] ** 2).sum())
             rec[t]["nfree"] = int(free.sum())

@@ -15,7 +15,8 @@ def test_build_and_exports():
 
     lib = _lib.load()
     header = open(os.path.join(ROOT, "include", "ssnal_b200.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(ssnal_\w+)\(", header, re.M))
+    declared = set(re.findall(
+        r"^\s*(?:int|size_t|const char\*|unsigned long long)\s+(ssnal_\w+)\(", header, re.M))
     assert declared, "no declarations parsed"
     for name in declared:
         assert hasattr(lib, name), name
