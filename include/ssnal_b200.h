@@ -141,6 +141,19 @@ int ssnal_dense_gram(const double* A, int64_t n_phys, int64_t q, int64_t lda,
 int ssnal_chol_solve(double* M, int64_t m, const double* b, double scale, double* x,
                      int* info, void* stream);
 
+/* ssnal_dense_newton_pspace: the same Newton image through the p x p SPD system
+ *   (I_p + sigma P_J Q_JJ P_J) y = P_J grad_J,   t = -g_r + sigma X_J^T (P_J y),
+ * (Woodbury dual of ssnal_dense_gram's q x q system; chosen when p < q).  J holds
+ * the p logical free rows (host-known p), grad = Q s (n_log), g_r = X^T s (q),
+ * asa = a_J'a_J (host scalar).  Writes t (q) and *info (DEVICE int).  This is the
+ * p x p route of ref solver.py:224-258 (Q_JJ + rank-one term, dense symmetric
+ * solve).  ws: ssnal_pspace_ws_bytes(p, q). */
+size_t ssnal_pspace_ws_bytes(int64_t p, int64_t q);
+int ssnal_dense_newton_pspace(const double* A, int64_t n_phys, int64_t q, int64_t lda,
+                              const double* row_sign, int svr_block, const int32_t* J, int64_t p,
+                              const double* grad, const double* a, double sigma, double asa,
+                              const double* g_r, double* t, int* info, void* ws, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,6 +56,9 @@ _SIGNATURES = {
     "ssnal_dense_gram": (_I, [_P, _I64, _I64, _I64, _P, _I, _P, _P, _I64, _P, _D, _P, _P, _P,
                               _P, _P]),
     "ssnal_chol_solve": (_I, [_P, _I64, _P, _D, _P, _P, _P]),
+    "ssnal_pspace_ws_bytes": (_SZ, [_I64, _I64]),
+    "ssnal_dense_newton_pspace": (_I, [_P, _I64, _I64, _I64, _P, _I, _P, _I64, _P, _P, _D, _D,
+                                       _P, _P, _P, _P, _P]),
 }
 
 _lib = None

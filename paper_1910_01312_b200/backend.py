@@ -190,6 +190,13 @@ class CudaBackend:
                     int(p_max), _ptr(a), float(sigma), _ptr(asa_dev), _ptr(M), _ptr(m1), _ptr(ws),
                     self.stream())
 
+    def newton_pspace(self, op, J, p, grad, a, sigma, asa, g_r, t, info):
+        ws = self.ws("pspace", self.lib.ssnal_pspace_ws_bytes(p, op.q))
+        self._timed("newton_pspace", 0, _lib.call, "ssnal_dense_newton_pspace", _ptr(op.A),
+                    op.n_phys, op.q, op.lda, _ptr(op.row_sign), int(op.svr_block), _ptr(J), int(p),
+                    _ptr(grad), _ptr(a), float(sigma), float(asa), _ptr(g_r), _ptr(t), _ptr(info),
+                    _ptr(ws), self.stream())
+
     def chol_solve(self, M, m, b, scale, x, info):
         self._timed("chol_solve", 16 * m * m, _lib.call, "ssnal_chol_solve", _ptr(M), int(m),
                     _ptr(b), float(scale), _ptr(x), _ptr(info), self.stream())

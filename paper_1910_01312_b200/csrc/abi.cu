@@ -32,6 +32,12 @@ cudaError_t launch_dense_gram(const double* A, long long n, long long q, long lo
                               double* M, double* m1, void* ws, cudaStream_t s);
 cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
                               int* info, cudaStream_t s);
+size_t pspace_ws_bytes(long long p, long long q);
+cudaError_t launch_pspace_direction(const double* A, long long n, long long q, long long lda,
+                                    const double* rs, int svr, const int32_t* J, long long p,
+                                    const double* grad, const double* a, double sigma, double asa,
+                                    const double* g_r, double* t, int* info, void* ws,
+                                    cudaStream_t stream);
 }  // namespace ssnal
 
 #include <atomic>
@@ -161,6 +167,20 @@ int ssnal_dense_gram(const double* A, int64_t n_phys, int64_t q, int64_t lda,
   return check("ssnal_dense_gram",
                launch_dense_gram(A, n_phys, q, lda, row_sign, svr_block, J, (const long long*)p_dev,
                                  p_max, a, sigma, asa_dev, M, m1, ws, S(stream)));
+}
+
+size_t ssnal_pspace_ws_bytes(int64_t p, int64_t q) { return pspace_ws_bytes(p, q); }
+
+int ssnal_dense_newton_pspace(const double* A, int64_t n_phys, int64_t q, int64_t lda,
+                              const double* row_sign, int svr_block, const int32_t* J, int64_t p,
+                              const double* grad, const double* a, double sigma, double asa,
+                              const double* g_r, double* t, int* info, void* ws, void* stream) {
+  if (n_phys < 1 || q < 1 || lda < q || p < 1 || !A || !J || !grad || !a || !g_r || !t || !info ||
+      !ws)
+    return fail_arg("ssnal_dense_newton_pspace", "size/null");
+  return check("ssnal_dense_newton_pspace",
+               launch_pspace_direction(A, n_phys, q, lda, row_sign, svr_block, J, p, grad, a, sigma,
+                                       asa, g_r, t, info, ws, S(stream)));
 }
 
 int ssnal_chol_solve(double* M, int64_t m, const double* b, double scale, double* x, int* info,

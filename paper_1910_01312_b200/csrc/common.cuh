@@ -57,6 +57,27 @@ __device__ __forceinline__ void block_reduce(double (&vals)[NV], const int (&ops
   __syncthreads();
 }
 
+// Fold the per-block partial records of a grid (record b at base + b*stride, NV
+// values each) inside ONE block: thread t folds records t, t+blockDim, ... in
+// order, then a fixed shuffle/warp tree combines threads.  Result in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_fold_partials(const double* base, unsigned nrec,
+                                                    long long stride, const int (&ops)[NV],
+                                                    double (&vals)[NV], double* smem) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    vals[k] = ops[k] == 0 ? 0.0 : (ops[k] == 1 ? INFINITY : -INFINITY);
+  for (unsigned b = threadIdx.x; b < nrec; b += blockDim.x) {
+    const double* q = base + (long long)b * stride;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double x = __ldcg(q + k);
+      vals[k] = ops[k] == 0 ? vals[k] + x : (ops[k] == 1 ? fmin(vals[k], x) : fmax(vals[k], x));
+    }
+  }
+  block_reduce<NV>(vals, ops, smem);
+}
+
 // "Last block done" ticket: returns true in exactly one block (the last to arrive),
 // after a device-scope fence so that every block's partials are visible to it.
 __device__ __forceinline__ bool last_block_arrive(unsigned int* ticket, unsigned int nblocks) {

@@ -45,14 +45,16 @@ __global__ void __launch_bounds__(XT_WARPS * 32) dense_xt_kernel(XtArgs p, int k
   for (int j = 0; j < KV; ++j)
 #pragma unroll
     for (int c = 0; c < XT_MAXC; ++c) acc[j][c] = 0.0;
+  const double* vp[KV];
+#pragma unroll
+  for (int j = 0; j < KV; ++j) vp[j] = kofs == 0 ? p.v[j] : p.v[j + 2];  // kofs in {0, 2}
   for (long long r = r0 + warp; r < r1; r += XT_WARPS) {
     double coef[KV];
     const double sg = p.rs ? p.rs[r] : 1.0;
 #pragma unroll
     for (int j = 0; j < KV; ++j) {
-      const double* vj = p.v[kofs + j];
-      double cv = vj[r];
-      if (p.svr) cv = __dsub_rn(cv, vj[r + p.n]);
+      double cv = vp[j][r];
+      if (p.svr) cv = __dsub_rn(cv, vp[j][r + p.n]);
       coef[j] = sg * cv;
     }
     const double* row = p.A + r * p.lda + col0;
@@ -83,13 +85,17 @@ __global__ void __launch_bounds__(XT_WARPS * 32) dense_xt_kernel(XtArgs p, int k
   }
 }
 
+// one warp per output entry: lanes fold splits lane, lane+32, ..., then a fixed
+// shuffle tree -- deterministic and ~32x shorter dependency chains than a thread fold
 __global__ void dense_xt_fold_kernel(const double* __restrict__ part, long long nsplit, int k,
                                      long long q, double* __restrict__ out) {
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (idx >= (long long)k * q) return;
   double s = 0.0;
-  for (long long b = 0; b < nsplit; ++b) s += part[b * k * q + idx];
-  out[idx] = s;
+  for (long long b = lane; b < nsplit; b += 32) s += __ldcg(part + b * k * q + idx);
+  s = warp_sum(s);
+  if (lane == 0) out[idx] = s;
 }
 
 static int xt_splits(long long n) {
@@ -123,7 +129,7 @@ cudaError_t launch_dense_xt(const double* A, long long n, long long q, long long
     }
   }
   long long tot = (long long)k * q;
-  { note_launch(); dense_xt_fold_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, stream>>>(p.part, nsplit, k, q, out); }
+  { note_launch(); dense_xt_fold_kernel<<<(unsigned)ceil_div(tot * 32, 256), 256, 0, stream>>>(p.part, nsplit, k, q, out); }
   return cudaGetLastError();
 }
 

@@ -95,17 +95,10 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_range_kernel(ProjArgs p) {
   if (threadIdx.x == 0)
     for (int k = 0; k < 5; ++k) mine[k] = vals[k];
   if (!last_block_arrive(&st->ticket, gridDim.x)) return;
+  block_fold_partials<5>(p.part + (long long)t * gridDim.x * PSTRIDE, gridDim.x, PSTRIDE, ops,
+                         vals, red);
   if (threadIdx.x != 0) return;
-  const double* base = p.part + (long long)t * gridDim.x * PSTRIDE;
-  double r0 = INFINITY, r1 = -INFINITY, r2 = 0.0, r3 = 0.0, r4 = 0.0;
-  for (unsigned b = 0; b < gridDim.x; ++b) {
-    const double* q = base + (long long)b * PSTRIDE;
-    r0 = fmin(r0, __ldcg(q + 0));
-    r1 = fmax(r1, __ldcg(q + 1));
-    r2 += __ldcg(q + 2);
-    r3 += __ldcg(q + 3);
-    r4 += __ldcg(q + 4);
-  }
+  const double r0 = vals[0], r1 = vals[1], r2 = vals[2], r3 = vals[3], r4 = vals[4];
   st->tmin = r0;
   st->tmax = r1;
   st->passes = 0;
@@ -192,21 +185,10 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_pass_kernel(ProjArgs p) {
   if (threadIdx.x == 0)
     for (int k = 0; k < NPROBE + 7; ++k) mine[k] = vals[k];
   if (!last_block_arrive(&st->ticket, gridDim.x)) return;
-  if (threadIdx.x != 0) return;
-
-  const double* base = p.part + (long long)t * gridDim.x * PSTRIDE;
   double tot[NPROBE + 7];
-  for (int k = 0; k < NPROBE + 7; ++k)
-    tot[k] = (k == NPROBE + 2) ? -INFINITY : (k == NPROBE + 3 || k == NPROBE + 4) ? INFINITY
-             : (k == NPROBE + 5) ? -INFINITY : 0.0;
-  for (unsigned b = 0; b < gridDim.x; ++b) {
-    const double* q = base + (long long)b * PSTRIDE;
-    for (int k = 0; k < NPROBE + 7; ++k) {
-      double x = __ldcg(q + k);
-      int op = (k < NPROBE + 2 || k == NPROBE + 6) ? 0 : (k == NPROBE + 3 || k == NPROBE + 4) ? 1 : 2;
-      tot[k] = op == 0 ? tot[k] + x : (op == 1 ? fmin(tot[k], x) : fmax(tot[k], x));
-    }
-  }
+  block_fold_partials<NPROBE + 7>(p.part + (long long)t * gridDim.x * PSTRIDE, gridDim.x,
+                                  PSTRIDE, ops, tot, red);
+  if (threadIdx.x != 0) return;
   const double below = fmax(s.below_max, tot[NPROBE + 2]);
   const double above = fmin(s.above_min, tot[NPROBE + 3]);
   const double in_min = tot[NPROBE + 4], in_max = tot[NPROBE + 5];
@@ -274,11 +256,10 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_exact_kernel(ProjArgs p) {
   if (threadIdx.x == 0)
     for (int k = 0; k < 4; ++k) mine[k] = acc[k];
   if (!last_block_arrive(&st->ticket, gridDim.x)) return;
+  double f[4];
+  block_fold_partials<4>(p.part + (long long)t * gridDim.x * PSTRIDE, gridDim.x, PSTRIDE, ops, f,
+                         red);
   if (threadIdx.x != 0) return;
-  const double* base = p.part + (long long)t * gridDim.x * PSTRIDE;
-  double f[4] = {0.0, 0.0, 0.0, 0.0};
-  for (unsigned b = 0; b < gridDim.x; ++b)
-    for (int k = 0; k < nc; ++k) f[k] += __ldcg(base + (long long)b * PSTRIDE + k);
   for (int k = 0; k < nc; ++k) f[k] = p.d - f[k];
   // first candidate with f >= 0 is t_u; its predecessor is t_l (ref projection.py:195-208)
   int iu = nc - 1;
@@ -332,11 +313,10 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_apply_kernel(ProjArgs p) {
   if (threadIdx.x == 0)
     for (int k = 0; k < 6; ++k) mine[k] = vals[k];
   if (!last_block_arrive(&st->ticket, gridDim.x)) return;
+  double r[6];
+  block_fold_partials<6>(p.part + (long long)t * gridDim.x * PSTRIDE, gridDim.x, PSTRIDE, ops, r,
+                         red);
   if (threadIdx.x != 0) return;
-  const double* base = p.part + (long long)t * gridDim.x * PSTRIDE;
-  double r[6] = {0, 0, 0, 0, 0, 0};
-  for (unsigned b = 0; b < gridDim.x; ++b)
-    for (int k = 0; k < 6; ++k) r[k] += __ldcg(base + (long long)b * PSTRIDE + k);
   st->sum_v2 = r[0];
   st->sum_r2 = r[1];
   st->sum_dref2 = r[2];

@@ -47,11 +47,9 @@ __global__ void __launch_bounds__(SSNAL_NT) dots_kernel(DotArgs p) {
   if (threadIdx.x == 0)
     for (int j = 0; j < MAXDOT; ++j) p.part[blockIdx.x * MAXDOT + j] = acc[j];
   if (!last_block_arrive(p.ticket, gridDim.x)) return;
-  if (threadIdx.x < p.k) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(p.part + b * MAXDOT + threadIdx.x);
-    p.out[threadIdx.x] = s;
-  }
+  block_fold_partials<MAXDOT>(p.part, gridDim.x, MAXDOT, ops, acc, red);
+  if (threadIdx.x == 0)
+    for (int j = 0; j < p.k; ++j) p.out[j] = acc[j];
 }
 
 size_t reduce_ws_bytes(long long n) {

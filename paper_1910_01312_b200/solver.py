@@ -268,7 +268,7 @@ class _Engine:
                                  ref=x)
         return sc, st[0]
 
-    def direction(self, p, sigma):
+    def direction(self, p, sigma, asa=0.0):
         """Newton direction in factor space.  Fills self.dir, self.qdir and queues
         the dots [g'd, w'Qw, w'Qd, d'Qd]; returns nothing (caller fetches)."""
         be, op = self.be, self.op
@@ -278,13 +278,20 @@ class _Engine:
             be.dots([(self.grad, self.dir), (self.w, self.qw), (self.w, self.qdir),
                      (self.s, self.grad)], self.scal)
             return
-        if self.q > self.pb_direct_limit():
-            raise InternalError("factor-space system larger than direct_solve_threshold; "
-                                "the CG path is not built for dense operators")
         be.compact(self.free, self.J, self.pcount)
-        be.dense_gram(op, self.J, self.pcount, self.n, self.box.a_dev, sigma, self.asa_dev,
-                      self.M, self.m1)
-        be.chol_solve(self.M, self.q, self.gr[0], -1.0, self.t[0], self.info)
+        if p < self.q:  # sample-space p x p system (Woodbury dual), cheaper when p < q
+            if p > self.pb_direct_limit():
+                raise InternalError("p x p system larger than direct_solve_threshold; "
+                                    "the CG path is not built for dense operators")
+            be.newton_pspace(op, self.J, p, self.grad, self.box.a_dev, sigma, asa,
+                             self.gr[0], self.t[0], self.info)
+        else:           # factor-space q x q system
+            if self.q > self.pb_direct_limit():
+                raise InternalError("q x q system larger than direct_solve_threshold; "
+                                    "the CG path is not built for dense operators")
+            be.dense_gram(op, self.J, self.pcount, self.n, self.box.a_dev, sigma, self.asa_dev,
+                          self.M, self.m1)
+            be.chol_solve(self.M, self.q, self.gr[0], -1.0, self.t[0], self.info)
         op.x(self.t, self.qdir.view(1, -1), k=1)
         # d = -s - sigma P(Qd)  (ref solver.py:269)
         be.hs_apply(self.free, self.box.a_dev, self.qdir, -sigma, self.s, -1.0, self.dir)
@@ -394,7 +401,7 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
             converged, exhausted = True, False
             break
         p = int(cur["nfree"])
-        eng.direction(p, sigma)
+        eng.direction(p, sigma, float(cur["sum_a2_free"]))
         sc, _ = eng.fetch(info=(p > 0))
         if p > 0 and int(eng.h_info[0]) != 0:
             raise InternalError(f"factor-space Newton matrix not SPD (column {int(eng.h_info[0])})")

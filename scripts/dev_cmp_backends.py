@@ -25,7 +25,7 @@ for trial in range(3):
         print('  ', name, np.abs(a - b).max(), np.abs(b).max())
     print('  free diff', (eg.free.cpu().numpy() != ec.free.numpy()).sum(), 'gr', np.abs(eg.gr[0].cpu().numpy() - ec.gr[0].numpy()).max())
     p = int(curg['nfree'])
-    eg.direction(p, sigma); ec.direction(p, sigma)
+    asa = float(curg['sum_a2_free']); eg.direction(p, sigma, asa); ec.direction(p, sigma, asa)
     sg, _ = eg.fetch(info=True); sc_, _ = ec.fetch(info=True)
     print('  dir dots', sg[:4], sc_[:4], 'info', int(eg.h_info[0]))
     for name in ['M', 'm1', 't', 'qdir', 'dir']:

@@ -156,6 +156,18 @@ class CpuTestBackend:
         M.copy_(torch.from_numpy(np.eye(G.shape[0]) + sigma * G))
         m1.copy_(torch.from_numpy(m))
 
+    def newton_pspace(self, op, J, p, grad, a, sigma, asa, g_r, t, info):
+        self._count("newton_pspace")
+        X = self._x_rows(op)
+        idx = J[:p].numpy().astype(np.int64)
+        Z = X[idx]
+        aJ = a.numpy()[idx]
+        P = np.eye(p) - (np.outer(aJ, aJ) / asa if asa != 0.0 else 0.0)
+        M = np.eye(p) + sigma * P @ (Z @ Z.T) @ P
+        y = np.linalg.solve(M, P @ grad.numpy()[idx])
+        t.copy_(torch.from_numpy(-g_r.numpy() + sigma * Z.T @ (P @ y)))
+        info[0] = 0
+
     def chol_solve(self, M, m, b, scale, x, info):
         self._count("chol_solve")
         Mh = M.numpy()

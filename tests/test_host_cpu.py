@@ -51,7 +51,7 @@ def test_newton_direction_factor_space_matches_reference(mods):
         sc, cur = eng.start_inner(torch.from_numpy(c["x"]), torch.from_numpy(c["w"].copy()),
                                   torch.from_numpy(q @ c["w"]), c["sigma"])
         np.testing.assert_array_equal(eng.free.numpy(), c["free"])
-        eng.direction(int(cur["nfree"]), c["sigma"])
+        eng.direction(int(cur["nfree"]), c["sigma"], float(cur["sum_a2_free"]))
         sc, _ = eng.fetch(info=True)
         assert np.linalg.norm(eng.qdir.numpy() - c["qdir"]) <= 1e-10 * (1 + np.linalg.norm(c["qdir"]))
         assert sc[3] == pytest.approx(c["dqd"], rel=1e-9, abs=1e-12)
