@@ -66,19 +66,24 @@ size_t ssnal_compact_ws_bytes(int64_t n);
 /* ---- projection onto {x : a'x = d, l <= x <= u} ------------------------
  * Replaces ref projection.py:152-211 project_box_line (+ :134-149 _classify).
  * Projects T <= 16 vectors v_t = A - coef[t] * B (B may be NULL; coef is a HOST
- * array of T doubles, passed by value to the kernels), each trial t writing state[t] and, when non-NULL,
- * x_out[t*n..] (projection), free_out[t*n..] (uint8 free-set mask Sigma) and
- * the fused sums of ssnal_proj_state_t.  l or u NULL => the scalar l_const /
- * u_const bound for every slot.  phases: bit0 range, bit1 exact, bit2 apply;
- * `passes` K-ary bracketing passes are launched between range and exact (a
- * pass after convergence is a no-op).  state[t].status == 3 on completion; 0/1
- * means more passes are needed (call again with phases = 6). */
+ * array of T doubles, passed by value to the kernels), each trial t writing
+ * state[t] and, when non-NULL, x_out[t*n..] (projection), free_out[t*n..] (uint8
+ * free-set mask Sigma) and the fused sums of ssnal_proj_state_t.  l or u NULL =>
+ * the scalar l_const / u_const bound for every slot.
+ * Root search for lambda: `newton_passes` > 0 runs that many safeguarded Newton
+ * passes warm-started at lam_hint (O(1) work per slot per pass, exact on the
+ * final affine piece); otherwise phases bit0 starts a K-ary search over the full
+ * breakpoint range.  `passes` K-ary passes follow (they take over any unfinished
+ * Newton search), then bit1 exact (closes a K-ary bracket onto adjacent
+ * breakpoints) and bit2 apply.  Passes after convergence are no-ops.
+ * state[t].status == 3 on completion; 0, 1 or 4 means more passes are needed
+ * (call again with newton_passes = 0, phases = 6). */
 int ssnal_project(const double* A, const double* B, const double* coef,
                   const double* a, const double* l, const double* u,
                   double l_const, double u_const, double d, int64_t n, int T,
                   ssnal_proj_state_t* state, void* ws,
                   double* x_out, uint8_t* free_out, const double* ref,
-                  int phases, int passes, void* stream);
+                  double lam_hint, int newton_passes, int phases, int passes, void* stream);
 
 /* ---- HS-Jacobian -------------------------------------------------------
  * Replaces ref projection.py:214-225 hs_jacobian_apply.

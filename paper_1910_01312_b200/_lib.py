@@ -23,7 +23,7 @@ PROJ_STATE_DTYPE = np.dtype([
     ("nfree", "i8"), ("status", "i4"), ("passes", "i4"), ("ticket", "u4"), ("pad_", "u4"),
 ])
 
-PROJ_SEARCH, PROJ_BRACKETED, PROJ_DONE, PROJ_APPLIED = 0, 1, 2, 3
+PROJ_SEARCH, PROJ_BRACKETED, PROJ_DONE, PROJ_APPLIED, PROJ_NEWTON = 0, 1, 2, 3, 4
 PROJ_INFEASIBLE_LOW, PROJ_INFEASIBLE_HIGH = -1, -2
 PHASE_RANGE, PHASE_EXACT, PHASE_APPLY = 1, 2, 4
 
@@ -46,7 +46,7 @@ _SIGNATURES = {
     "ssnal_gram_ws_bytes": (_SZ, [_I64]),
     "ssnal_compact_ws_bytes": (_SZ, [_I64]),
     "ssnal_project": (_I, [_P, _P, _P, _P, _P, _P, _D, _D, _D, _I64, _I, _P, _P, _P, _P, _P,
-                           _I, _I, _P]),
+                           _D, _I, _I, _I, _P]),
     "ssnal_hs_apply": (_I, [_P, _P, _P, _I64, _D, _P, _D, _P, _P, _P]),
     "ssnal_dots": (_I, [_I, _P, _P, _P, _I64, _P, _P, _P]),
     "ssnal_vec": (_I, [_I, _I64, _D, _P, _P, _P, _P, _P]),

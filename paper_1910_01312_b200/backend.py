@@ -97,36 +97,44 @@ class CudaBackend:
         return states_host.numpy().view(_lib.PROJ_STATE_DTYPE).reshape(-1)
 
     # ---------------------------------------------------------------- projection
+    # default search: this many warm-started Newton passes, then K-ary passes take over
+    NEWTON_PASSES = 3
+    KARY_PASSES = 2
+
     def project(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
-                ref=None, phases=7, passes=6):
+                ref=None, phases=7, passes=None, hint=0.0, newton=None):
         n = box.n
+        if newton is None:
+            newton = self.NEWTON_PASSES
+        if passes is None:
+            passes = self.KARY_PASSES
         coef_arr = None
         if B is not None:
             coef_arr = (_lib.ctypes.c_double * T)(*[float(c) for c in coefs])
         ws = self.ws("proj", self.lib.ssnal_project_ws_bytes(n, T))
-        # per streaming phase: v (+ B) and a, (+ l, u vectors), once per launch
+        # per streaming launch: v (+ B) and a, (+ l, u vectors)
         per_phase = 8 * n * (2 + (B is not None) + (box.l_dev is not None) + (box.u_dev is not None))
         self._timed(
-            "project", per_phase * (3 + passes), _lib.call,
+            "project", per_phase * (newton + 1), _lib.call,
             "ssnal_project", _ptr(A), _ptr(B),
             _lib.ctypes.cast(coef_arr, _lib.ctypes.c_void_p) if coef_arr is not None else None,
             _ptr(box.a_dev), _ptr(box.l_dev), _ptr(box.u_dev), box.l_const, box.u_const, box.d,
             n, T, _ptr(states), _ptr(ws), _ptr(x_out), _ptr(free_out), _ptr(ref),
-            phases, passes, self.stream())
+            float(hint), int(newton), phases, passes, self.stream())
 
     def project_sync(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
-                     ref=None):
+                     ref=None, hint=0.0):
         """Project and return the host copy of the T state records (one sync,
         plus a rare extra round if a trial needed more bracketing passes)."""
-        self.project(A, box, states, T, B, coefs, x_out, free_out, ref)
+        self.project(A, box, states, T, B, coefs, x_out, free_out, ref, hint=hint)
         st = self.read_states(states[:T].cpu())
         extra = 0
-        while np.any((st["status"] == _lib.PROJ_SEARCH) | (st["status"] == _lib.PROJ_BRACKETED)):
+        while np.any((st["status"] >= 0) & (st["status"] != _lib.PROJ_APPLIED)):
             extra += 1
             if extra > 20:
                 raise RuntimeError("projection failed to bracket the multiplier")
             self.project(A, box, states, T, B, coefs, x_out, free_out, ref,
-                         phases=_lib.PHASE_EXACT | _lib.PHASE_APPLY, passes=8)
+                         phases=_lib.PHASE_EXACT | _lib.PHASE_APPLY, passes=8, newton=0)
             st = self.read_states(states[:T].cpu())
         return st
 

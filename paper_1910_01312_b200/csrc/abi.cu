@@ -96,7 +96,8 @@ size_t ssnal_compact_ws_bytes(int64_t n) { return compact_ws_bytes(n); }
 int ssnal_project(const double* A, const double* B, const double* coef, const double* a,
                   const double* l, const double* u, double l_const, double u_const, double d,
                   int64_t n, int T, ssnal_proj_state_t* state, void* ws, double* x_out,
-                  uint8_t* free_out, const double* ref, int phases, int passes, void* stream) {
+                  uint8_t* free_out, const double* ref, double lam_hint, int newton_passes,
+                  int phases, int passes, void* stream) {
   if (n < 1) return fail_arg("ssnal_project", "n < 1");
   if (T < 1 || T > SSNAL_MAX_TRIALS) return fail_arg("ssnal_project", "T must be in [1, 16]");
   if (!A || !a || !state || !ws) return fail_arg("ssnal_project", "null A/a/state/ws");
@@ -107,6 +108,7 @@ int ssnal_project(const double* A, const double* B, const double* coef, const do
   L.lc = l_const; L.uc = u_const; L.d = d; L.n = n; L.T = T;
   L.st = state; L.part = (double*)ws; L.x_out = x_out; L.free_out = free_out; L.ref = ref;
   L.phases = phases; L.passes = passes;
+  L.hint = lam_hint; L.newton = newton_passes < 0 ? 0 : newton_passes;
   return check("ssnal_project", launch_project(L, S(stream)));
 }
 

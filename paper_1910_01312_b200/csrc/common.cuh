@@ -43,16 +43,19 @@ __device__ __forceinline__ void block_reduce(double (&vals)[NV], const int (&ops
     if (lane == 0) smem[k * 32 + warp] = v;
   }
   __syncthreads();
+  // slot k is combined across warps by thread k (fixed order), then broadcast to thread 0
+  for (int k = threadIdx.x; k < NV; k += blockDim.x) {
+    double v = smem[k * 32];
+    for (int w = 1; w < nwarps; ++w) {
+      double x = smem[k * 32 + w];
+      v = ops[k] == 0 ? v + x : (ops[k] == 1 ? fmin(v, x) : fmax(v, x));
+    }
+    smem[k * 32] = v;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      double v = smem[k * 32];
-      for (int w = 1; w < nwarps; ++w) {
-        double x = smem[k * 32 + w];
-        v = ops[k] == 0 ? v + x : (ops[k] == 1 ? fmin(v, x) : fmax(v, x));
-      }
-      vals[k] = v;
-    }
+    for (int k = 0; k < NV; ++k) vals[k] = smem[k * 32];
   }
   __syncthreads();
 }

@@ -132,8 +132,14 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_pass_kernel(ProjArgs p) {
   __shared__ double red[(NPROBE + 8) * 32];
   const int t = blockIdx.y;
   ProjState* st = p.st + t;
-  if (st->status != PROJ_SEARCH) return;  // uniform across the grid
-  const ProjState s = *st;
+  if (st->status != PROJ_SEARCH && st->status != PROJ_NEWTON) return;  // uniform across grid
+  ProjState s = *st;
+  if (s.status == PROJ_NEWTON) {  // fallback after the Newton passes: finite bracket
+    if (!(s.lo > -INFINITY)) s.lo = s.tmin;
+    if (!(s.hi < INFINITY)) s.hi = s.tmax;
+    s.below_max = -INFINITY;
+    s.above_min = INFINITY;
+  }
   const double lo = s.lo, hi = s.hi;
   double acc[NPROBE];
 #pragma unroll
@@ -194,6 +200,7 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_pass_kernel(ProjArgs p) {
   const double in_min = tot[NPROBE + 4], in_max = tot[NPROBE + 5];
   const long long in_cnt = (long long)tot[NPROBE + 6];
   st->passes = s.passes + 1;
+  st->status = PROJ_SEARCH;
   st->below_max = below;
   st->above_min = above;
   st->in_count = in_cnt;
@@ -215,6 +222,134 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_pass_kernel(ProjArgs p) {
   double new_lo = probe_at(s, k_hit - 1), new_hi = probe_at(s, k_hit);
   st->lo = new_lo;
   st->hi = new_hi;
+}
+
+// ------------------------------------------------------------------ newton
+// Safeguarded Newton on the piecewise-affine phi'(lambda), O(1) work per slot per
+// pass: at the current point c one pass sums f(c), the slopes of the segments left
+// and right of c (sum of a_i^2 over slots free there) and the nearest breakpoints
+// on either side.  If the affine root of the segment the sign of f(c) points into
+// lies inside that segment it IS the multiplier (same affine piece the reference
+// interpolates on, ref projection.py:204-208); otherwise c moves to the Newton
+// point (or the next breakpoint on a flat piece, or the bracket midpoint) and the
+// bracket [lo, hi] with f(lo) < 0 <= f(hi) shrinks.  Warm-started from the
+// previous multiplier, one or two passes suffice in the line search.
+__global__ void __launch_bounds__(SSNAL_NT) proj_newton_kernel(ProjArgs p, int fresh,
+                                                               double hint) {
+  __shared__ double red[8 * 32];
+  const int t = blockIdx.y;
+  ProjState* st = p.st + t;
+  if (!fresh && st->status != PROJ_NEWTON) return;
+  const double c = fresh ? hint : st->lam;
+  double fsum = 0.0, sp = 0.0, sm = 0.0, amin = INFINITY, bmax = -INFINITY;
+  double tmin = INFINITY, tmax = -INFINITY, nnz = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v, a, l, u;
+    load_elem(p, t, i, v, a, l, u);
+    if (a == 0.0) continue;
+    double t1 = __ddiv_rn(__dsub_rn(v, u), a), t2 = __ddiv_rn(__dsub_rn(v, l), a);
+    double ta = fmin(t1, t2), tb = fmax(t1, t2);
+    fsum += contrib(v, a, l, u, c);
+    const double a2 = a * a;
+    if (ta <= c && c < tb) sp += a2;  // free just right of c
+    if (ta < c && c <= tb) sm += a2;  // free just left of c
+    if (ta > c) amin = fmin(amin, ta); else if (ta < c) bmax = fmax(bmax, ta);
+    if (tb > c) amin = fmin(amin, tb); else if (tb < c) bmax = fmax(bmax, tb);
+    tmin = fmin(tmin, ta);
+    tmax = fmax(tmax, tb);
+    nnz += 1.0;
+  }
+  double vals[8] = {fsum, sp, sm, amin, bmax, tmin, tmax, nnz};
+  const int ops[8] = {0, 0, 0, 1, 2, 1, 2, 0};
+  block_reduce<8>(vals, ops, red);
+  double* mine = p.part + ((long long)t * gridDim.x + blockIdx.x) * PSTRIDE;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 8; ++k) mine[k] = vals[k];
+  if (!last_block_arrive(&st->ticket, gridDim.x)) return;
+  block_fold_partials<8>(p.part + (long long)t * gridDim.x * PSTRIDE, gridDim.x, PSTRIDE, ops,
+                         vals, red);
+  if (threadIdx.x != 0) return;
+  const double f = p.d - vals[0], slope_r = vals[1], slope_l = vals[2];
+  const double above = vals[3], below = vals[4];
+  double lo, hi;
+  int passes;
+  if (fresh) {
+    lo = -INFINITY;
+    hi = INFINITY;
+    passes = 0;
+    st->tmin = vals[5];
+    st->tmax = vals[6];
+    st->in_count = -1;
+    if (vals[7] == 0.0) {  // a == 0: constraint 0 = d, project by clipping
+      st->lam = 0.0;
+      st->status = PROJ_DONE;
+      st->passes = 1;
+      return;
+    }
+  } else {
+    lo = st->lo;
+    hi = st->hi;
+    passes = st->passes;
+  }
+  ++passes;
+  st->passes = passes;
+  double next;
+  if (f == 0.0) {
+    st->lam = c;
+    st->status = PROJ_DONE;
+    return;
+  }
+  if (f < 0.0) {
+    lo = c;
+    if (!(above < INFINITY)) {  // right of every breakpoint: phi'(+inf) < 0
+      st->status = PROJ_INFEASIBLE_HIGH;
+      return;
+    }
+    if (slope_r > 0.0) {
+      const double r = c - f / slope_r;
+      if (r <= above) {
+        st->lam = r;
+        st->status = PROJ_DONE;
+        return;
+      }
+      lo = above;  // phi'(above) = f + slope (above - c) < 0
+      next = r;
+    } else {
+      next = above;  // flat piece: step to the next breakpoint
+    }
+  } else {
+    hi = c;
+    if (!(below > -INFINITY)) {  // left of every breakpoint: phi'(-inf) >= 0
+      // ref projection.py:186-191: lambda = smallest breakpoint (or infeasible)
+      st->lam = st->tmin;
+      st->status = f > 1e-9 * (1.0 + fabs(p.d)) ? PROJ_INFEASIBLE_LOW : PROJ_DONE;
+      return;
+    }
+    if (slope_l > 0.0) {
+      const double r = c - f / slope_l;
+      if (r >= below) {
+        st->lam = r;
+        st->status = PROJ_DONE;
+        return;
+      }
+      hi = below;  // phi'(below) = f - slope (c - below) > 0
+      next = r;
+    } else {
+      next = below;
+    }
+  }
+  // safeguard: stay strictly inside the bracket, bisect when Newton leaves it
+  const bool flat_step = (f < 0.0 && !(slope_r > 0.0)) || (f > 0.0 && !(slope_l > 0.0));
+  if (!flat_step && !(next > lo && next < hi)) {
+    if (lo > -INFINITY && hi < INFINITY) next = 0.5 * (lo + hi);
+    else if (lo > -INFINITY) next = f < 0.0 ? above : lo + 2.0 * (c - lo) + 1.0;
+    else next = below;
+  }
+  st->lo = lo;
+  st->hi = hi;
+  st->lam = next;
+  st->status = PROJ_NEWTON;
 }
 
 // ------------------------------------------------------------------ exact
@@ -344,7 +479,15 @@ cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
   p.lc = L.lc; p.uc = L.uc; p.d = L.d; p.n = L.n; p.st = L.st; p.part = L.part;
   p.x_out = L.x_out; p.free_out = L.free_out; p.ref = L.ref;
   dim3 grid(proj_blocks(L.n), L.T);
-  if (L.phases & PHASE_RANGE) { note_launch(); proj_range_kernel<<<grid, SSNAL_NT, 0, stream>>>(p); }
+  if (L.newton > 0) {
+    for (int k = 0; k < L.newton; ++k) {
+      note_launch();
+      proj_newton_kernel<<<grid, SSNAL_NT, 0, stream>>>(p, k == 0 ? 1 : 0, L.hint);
+    }
+  } else if (L.phases & PHASE_RANGE) {
+    note_launch();
+    proj_range_kernel<<<grid, SSNAL_NT, 0, stream>>>(p);
+  }
   for (int k = 0; k < L.passes; ++k) { note_launch(); proj_pass_kernel<<<grid, SSNAL_NT, 0, stream>>>(p); }
   if (L.phases & PHASE_EXACT) { note_launch(); proj_exact_kernel<<<grid, SSNAL_NT, 0, stream>>>(p); }
   if (L.phases & PHASE_APPLY) { note_launch(); proj_apply_kernel<<<grid, SSNAL_NT, 0, stream>>>(p); }

@@ -13,6 +13,7 @@ enum ProjStatus {
   PROJ_BRACKETED = 1,
   PROJ_DONE = 2,
   PROJ_APPLIED = 3,
+  PROJ_NEWTON = 4,
   PROJ_INFEASIBLE_LOW = -1,
   PROJ_INFEASIBLE_HIGH = -2,
 };
@@ -34,6 +35,8 @@ struct ProjLaunch {
   const double* ref;
   int phases;
   int passes;
+  double hint;  // warm-start multiplier for the Newton passes
+  int newton;   // Newton passes (0: start from the full breakpoint range instead)
 };
 
 int proj_blocks(long long n);

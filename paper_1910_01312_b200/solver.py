@@ -188,6 +188,8 @@ class _Engine:
         self.asa_dev = self.st_cur[0, _OFF["sum_a2_free"]:_OFF["sum_a2_free"] + 8].view(F64)
         self.counters = {"projections": 0, "proj_trials": 0, "newton": 0, "syncs": 0}
         self._direct_limit = 2000
+        self.lam_kkt = 0.0  # warm starts for the multiplier search
+        self.lam_cur = 0.0
 
     # ------------------------------------------------------------ host reads
     def fetch(self, states=None, T=1, info=False):
@@ -203,8 +205,9 @@ class _Engine:
         st = self.be.read_states(self.h_st[:T]).copy() if states is not None else None
         return sc, st
 
-    def _project(self, A, states, T=1, B=None, coefs=None, x_out=None, free_out=None, ref=None):
-        self.be.project(A, self.box, states, T, B, coefs, x_out, free_out, ref)
+    def _project(self, A, states, T=1, B=None, coefs=None, x_out=None, free_out=None, ref=None,
+                 hint=0.0):
+        self.be.project(A, self.box, states, T, B, coefs, x_out, free_out, ref, hint=hint)
         self.counters["projections"] += 1
         self.counters["proj_trials"] += T
 
@@ -212,12 +215,13 @@ class _Engine:
                        ref=None):
         """Rarely a trial needs more bracketing passes than the default launch."""
         rounds = 0
-        while np.any(st["status"] < _lib.PROJ_DONE) and np.all(st["status"] >= 0):
+        while np.all(st["status"] >= 0) and np.any(st["status"] != _lib.PROJ_APPLIED):
             rounds += 1
+            self.counters["extra_rounds"] = self.counters.get("extra_rounds", 0) + 1
             if rounds > 20:
                 raise InternalError("projection failed to bracket the multiplier")
             self.be.project(A, self.box, states, T, B, coefs, x_out, free_out, ref,
-                            phases=_lib.PHASE_EXACT | _lib.PHASE_APPLY, passes=8)
+                            phases=_lib.PHASE_EXACT | _lib.PHASE_APPLY, passes=8, newton=0)
             _, st = self.fetch(states, T)
         for s in st["status"]:
             raise_on_status(int(s))
@@ -238,10 +242,11 @@ class _Engine:
             g = op.xt([x], self.gr[:1])
             op.x(g, self.qx.view(1, -1), k=1)
         be.vec(1, 0.0, x, self.qx, self.pb.c, self.tmp)  # x - Qx - c
-        self._project(self.tmp, self.st_kkt, ref=x)
+        self._project(self.tmp, self.st_kkt, ref=x, hint=self.lam_kkt)
         be.dots([(x, None), (x, self.qx), (self.pb.c, x)], self.scal)
         sc, st = self.fetch(self.st_kkt)
         st = self._finish_states(st, self.st_kkt, 1, self.tmp, ref=x)
+        self.lam_kkt = float(st["lam"][0])
         res = math.sqrt(float(st["sum_dref2"][0])) / (1.0 + math.sqrt(sc[0]))
         obj = 0.5 * sc[1] + sc[2]
         return res, int(st["nfree"][0]), obj
@@ -260,12 +265,18 @@ class _Engine:
         self.sigma = sigma
         be = self.be
         be.vec(0, -sigma, x, qw, self.pb.c, self.u)
-        self._project(self.u, self.st_cur, x_out=self.xp, free_out=self.free, ref=x)
+        self._project(self.u, self.st_cur, x_out=self.xp, free_out=self.free, ref=x,
+                      hint=self.lam_cur)
         self.gradient()
         be.dots([(self.grad, None), (x, None)], self.scal)
         sc, st = self.fetch(self.st_cur)
-        st = self._finish_states(st, self.st_cur, 1, self.u, x_out=self.xp, free_out=self.free,
-                                 ref=x)
+        if st["status"][0] != _lib.PROJ_APPLIED:  # needed extra passes: redo what used xp
+            st = self._finish_states(st, self.st_cur, 1, self.u, x_out=self.xp,
+                                     free_out=self.free, ref=x)
+            self.gradient()
+            be.dots([(self.grad, None), (x, None)], self.scal)
+            sc, _ = self.fetch()
+        self.lam_cur = float(st["lam"][0])
         return sc, st[0]
 
     def direction(self, p, sigma, asa=0.0):
@@ -329,7 +340,7 @@ class _Engine:
                 alpha *= opts.backtrack
             coefs = [sigma * a for a in alphas]
             self._project(self.u, self.st_trial, T, B=self.qdir, coefs=coefs, x_out=self.tx,
-                          free_out=self.tfree, ref=self.x)
+                          free_out=self.tfree, ref=self.x, hint=self.lam_cur)
             _, st = self.fetch(self.st_trial, T)
             st = self._finish_states(st, self.st_trial, T, self.u, B=self.qdir, coefs=coefs,
                                      x_out=self.tx, free_out=self.tfree, ref=self.x)
@@ -337,6 +348,7 @@ class _Engine:
                 quad = wqw + 2.0 * a * wqdir + a * a * dqd
                 psi_t = _psi(quad, st[j], x_sq, sigma, opts.psi_eval)
                 if psi_t <= psi0 + opts.mu * a * gd:
+                    self.lam_cur = float(st["lam"][j])
                     return a, j, st[j], psi_t
             tried += T
         raise LineSearchError("Armijo backtracking exceeded 60 halvings")

@@ -54,7 +54,7 @@ class CpuTestBackend:
 
     # projection --------------------------------------------------------------
     def project(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
-                ref=None, phases=7, passes=6):
+                ref=None, phases=7, passes=6, hint=0.0, newton=3):
         self._count("project")
         a = box.a_dev.numpy()
         l = box.l.numpy()
