@@ -99,15 +99,17 @@ class CudaBackend:
     # ---------------------------------------------------------------- projection
     # default search: this many warm-started Newton passes, then K-ary passes take over
     NEWTON_PASSES = 3
-    KARY_PASSES = 2
+    KARY_PASSES = 0
 
     def project(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
-                ref=None, phases=7, passes=None, hint=0.0, newton=None):
+                ref=None, phases=None, passes=None, hint=0.0, newton=None):
         n = box.n
         if newton is None:
             newton = self.NEWTON_PASSES
         if passes is None:
             passes = self.KARY_PASSES
+        if phases is None:  # Newton ends exactly; the K-ary exact phase only in fallbacks
+            phases = _lib.PHASE_APPLY if newton > 0 else 7
         coef_arr = None
         if B is not None:
             coef_arr = (_lib.ctypes.c_double * T)(*[float(c) for c in coefs])

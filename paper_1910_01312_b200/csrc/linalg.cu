@@ -97,13 +97,19 @@ __global__ void __launch_bounds__(CH_NT, 1) chol_solve_kernel(double* __restrict
   __syncthreads();
   for (long long k0 = 0; k0 < m; k0 += NB) {
     const int kb = (int)min((long long)NB, m - k0);
+    // stage the diagonal block of L in shared memory: the warp-serial solve below
+    // then waits on smem (~30 cycles) instead of L2 (~600) per step
+    for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+      int i = idx / kb, j = idx % kb;
+      D[i * (NB + 1) + j] = j <= i ? M[(k0 + i) * m + k0 + j] : 0.0;
+    }
+    __syncthreads();
     if (warp == 0) {
       double yv = lane < kb ? x[k0 + lane] : 0.0;
       for (int j = 0; j < kb; ++j) {
-        double yj = __shfl_sync(0xffffffffu, yv, j);
-        if (lane == j) { yj = yv / M[(k0 + j) * m + k0 + j]; yv = yj; }
-        yj = __shfl_sync(0xffffffffu, yv, j);
-        if (lane > j && lane < kb) yv -= M[(k0 + lane) * m + k0 + j] * yj;
+        if (lane == j) yv = yv / D[j * (NB + 1) + j];
+        const double yj = __shfl_sync(0xffffffffu, yv, j);
+        if (lane > j && lane < kb) yv -= D[lane * (NB + 1) + j] * yj;
       }
       if (lane < kb) x[k0 + lane] = yv;
     }
@@ -120,12 +126,17 @@ __global__ void __launch_bounds__(CH_NT, 1) chol_solve_kernel(double* __restrict
   for (long long bk = nblk - 1; bk >= 0; --bk) {
     const long long k0 = bk * NB;
     const int kb = (int)min((long long)NB, m - k0);
+    for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+      int i = idx / kb, j = idx % kb;
+      D[i * (NB + 1) + j] = j <= i ? M[(k0 + i) * m + k0 + j] : 0.0;
+    }
+    __syncthreads();
     if (warp == 0) {
       double xv = lane < kb ? x[k0 + lane] : 0.0;
       for (int j = kb - 1; j >= 0; --j) {
-        if (lane == j) xv = xv / M[(k0 + j) * m + k0 + j];
-        double xj = __shfl_sync(0xffffffffu, xv, j);
-        if (lane < j) xv -= M[(k0 + j) * m + k0 + lane] * xj;
+        if (lane == j) xv = xv / D[j * (NB + 1) + j];
+        const double xj = __shfl_sync(0xffffffffu, xv, j);
+        if (lane < j) xv -= D[j * (NB + 1) + lane] * xj;
       }
       if (lane < kb) x[k0 + lane] = xv;
     }

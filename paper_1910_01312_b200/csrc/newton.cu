@@ -54,15 +54,19 @@ __global__ void __launch_bounds__(256) rows_gram_kernel(RowsArgs g, double* __re
   const int tj = ti + pair;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long ri = (long long)ti * RT, rj = (long long)tj * RT;
+  // split-K over the feature dimension (blockIdx.y), partial tiles folded later
+  const long long kchunk = ceil_div(ceil_div(g.q, (long long)gridDim.y), RK) * RK;
+  const long long kbeg = blockIdx.y * kchunk, kend = min(g.q, kbeg + kchunk);
+  Qjj += (long long)blockIdx.y * g.p * g.p;
   double acc[8][2];
 #pragma unroll
   for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
-  for (long long k0 = 0; k0 < g.q; k0 += RK) {
+  for (long long k0 = kbeg; k0 < kend; k0 += RK) {
     for (int idx = threadIdx.x; idx < RT * RK; idx += blockDim.x) {
       int r = idx / RK, kk = idx % RK;
       long long col = k0 + kk;
       double va = 0.0, vb = 0.0;
-      if (col < g.q) {
+      if (col < kend) {
         if (ri + r < g.p) {
           double sg;
           const double* row = logical_row(g, g.J[ri + r], sg);
@@ -99,10 +103,20 @@ __global__ void __launch_bounds__(256) rows_gram_kernel(RowsArgs g, double* __re
       long long col = rj + t * 8 + 2 * (lane & 3) + h;
       if (row < g.p && col < g.p) {
         Qjj[row * g.p + col] = acc[t][h];
-        Qjj[col * g.p + row] = acc[t][h];
+        if (ti != tj) Qjj[col * g.p + row] = acc[t][h];  // diagonal tiles hold both halves
       }
     }
   }
+}
+
+// Q = sum over the split-K partial Grams (fixed order)
+__global__ void rows_gram_fold_kernel(const double* __restrict__ part, long long pp, int nsplit,
+                                      double* __restrict__ Q) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= pp) return;
+  double s = part[idx];
+  for (int b = 1; b < nsplit; ++b) s += part[(long long)b * pp + idx];
+  Q[idx] = s;
 }
 
 // Single-CTA O(p^2) assembly: gJ, aJ gathered; qa = Q a; scalars; M = I + sigma P Q P,
@@ -190,8 +204,17 @@ __global__ void pspace_finish_kernel(const double* __restrict__ part, long long 
   t[col] = -g_r[col] + sigma * s;
 }
 
+static int gram_ksplit(long long p, long long q) {
+  const long long nt = ceil_div(p, RT);
+  const long long pairs = nt * (nt + 1) / 2;
+  long long s = ceil_div(2 * 148, pairs);
+  s = min(s, ceil_div(q, RK));
+  s = min(s, 16LL);
+  return (int)max(s, 1LL);
+}
+
 size_t pspace_ws_bytes(long long p, long long q) {
-  return (size_t)(p * p + 4 * p + GX_SPLIT * q + 64) * sizeof(double);
+  return (size_t)((gram_ksplit(p, q) + 1) * p * p + 4 * p + GX_SPLIT * q + 64) * sizeof(double);
 }
 
 cudaError_t launch_pspace_direction(const double* A, long long n, long long q, long long lda,
@@ -205,9 +228,12 @@ cudaError_t launch_pspace_direction(const double* A, long long n, long long q, l
   double* b = qa + p;
   double* y = b + p;
   double* part = y + p;
+  double* gpart = part + GX_SPLIT * q;
   RowsArgs g{A, n, q, lda, rs, svr, J, p};
   const int ntile = (int)ceil_div(p, RT);
-  { note_launch(); rows_gram_kernel<<<ntile * (ntile + 1) / 2, 256, 0, stream>>>(g, Q, ntile); }
+  const int ks = gram_ksplit(p, q);
+  { note_launch(); rows_gram_kernel<<<dim3(ntile * (ntile + 1) / 2, ks), 256, 0, stream>>>(g, gpart, ntile); }
+  { note_launch(); rows_gram_fold_kernel<<<(unsigned)ceil_div(p * p, 256), 256, 0, stream>>>(gpart, p * p, ks, Q); }
   { note_launch(); pspace_assemble_kernel<<<1, 1024, 0, stream>>>(J, p, grad, a, sigma, asa, Q, aJ, qa, b); }
   cudaError_t e = launch_chol_solve(Q, p, b, 1.0, y, info, stream);
   if (e != cudaSuccess) return e;

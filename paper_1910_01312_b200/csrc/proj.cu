@@ -295,11 +295,9 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_newton_kernel(ProjArgs p, int f
   ++passes;
   st->passes = passes;
   double next;
-  if (f == 0.0) {
-    st->lam = c;
-    st->status = PROJ_DONE;
-    return;
-  }
+  // f >= 0 branch also covers f == 0: the reference returns the LEFTMOST root (first
+  // sorted breakpoint with f >= 0, interpolated against its predecessor), so a zero
+  // on a flat piece keeps stepping left to where the flat zero piece starts.
   if (f < 0.0) {
     lo = c;
     if (!(above < INFINITY)) {  // right of every breakpoint: phi'(+inf) < 0
@@ -340,7 +338,7 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_newton_kernel(ProjArgs p, int f
     }
   }
   // safeguard: stay strictly inside the bracket, bisect when Newton leaves it
-  const bool flat_step = (f < 0.0 && !(slope_r > 0.0)) || (f > 0.0 && !(slope_l > 0.0));
+  const bool flat_step = (f < 0.0 && !(slope_r > 0.0)) || (f >= 0.0 && !(slope_l > 0.0));
   if (!flat_step && !(next > lo && next < hi)) {
     if (lo > -INFINITY && hi < INFINITY) next = 0.5 * (lo + hi);
     else if (lo > -INFINITY) next = f < 0.0 ? above : lo + 2.0 * (c - lo) + 1.0;

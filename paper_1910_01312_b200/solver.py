@@ -323,9 +323,33 @@ class _Engine:
         sc, _ = self.fetch()
         return sc
 
-    def line_search(self, gd, psi0, wqw, wqdir, dqd, x_sq, opts):
+    def enqueue_unit_trial(self):
+        """Projection of u - sigma*1*Qd (the alpha = 1 Armijo trial) into trial slot 0."""
+        self._project(self.u, self.st_trial, 1, B=self.qdir, coefs=[self.sigma],
+                      x_out=self.tx, free_out=self.tfree, ref=self.x, hint=self.lam_cur)
+
+    def advance(self, p, asa, sigma, with_gradient=True):
+        """Pipelined Newton step: [s, grad = Q s, ||grad||^2] + direction at the current
+        point + the alpha = 1 trial projection, all enqueued, then ONE host sync.
+        Returns (||grad||^2, [g'd, w'Qw, w'Qd, d'Qd], trial-0 record)."""
+        if with_gradient:
+            self.gradient()
+            self.be.dots([(self.grad, None)], self.scal[4:5])
+        self.direction(p, sigma, asa)
+        self.enqueue_unit_trial()
+        sc, st = self.fetch(self.st_trial, 1, info=(p > 0))
+        if p > 0 and int(self.h_info[0]) != 0:
+            raise InternalError(f"reduced Newton matrix not SPD (column {int(self.h_info[0])})")
+        if st["status"][0] != _lib.PROJ_APPLIED:
+            st = self._finish_states(st, self.st_trial, 1, self.u, B=self.qdir,
+                                     coefs=[self.sigma], x_out=self.tx, free_out=self.tfree,
+                                     ref=self.x)
+        return float(sc[4]), [float(v) for v in sc[:4]], st
+
+    def line_search(self, gd, psi0, wqw, wqdir, dqd, x_sq, opts, first=None):
         """Armijo backtracking (ref solver.py:292-319), step lengths evaluated in
-        batched projections: alpha = 1 first, then `line_search_batch` at a time.
+        batched projections: alpha = 1 first (``first``: its already computed
+        record), then `line_search_batch` at a time.
         Returns (alpha, trial index, state record)."""
         if gd >= 0.0:
             raise LineSearchError(f"not a descent direction (g'd = {gd:.3e})")
@@ -339,11 +363,15 @@ class _Engine:
                 alphas.append(alpha)
                 alpha *= opts.backtrack
             coefs = [sigma * a for a in alphas]
-            self._project(self.u, self.st_trial, T, B=self.qdir, coefs=coefs, x_out=self.tx,
-                          free_out=self.tfree, ref=self.x, hint=self.lam_cur)
-            _, st = self.fetch(self.st_trial, T)
-            st = self._finish_states(st, self.st_trial, T, self.u, B=self.qdir, coefs=coefs,
-                                     x_out=self.tx, free_out=self.tfree, ref=self.x)
+            if tried == 0 and first is not None:
+                st = first
+            else:
+                self._project(self.u, self.st_trial, T, B=self.qdir, coefs=coefs, x_out=self.tx,
+                              free_out=self.tfree, ref=self.x, hint=self.lam_cur)
+                _, st = self.fetch(self.st_trial, T)
+                st = self._finish_states(st, self.st_trial, T, self.u, B=self.qdir,
+                                         coefs=coefs, x_out=self.tx, free_out=self.tfree,
+                                         ref=self.x)
             for j, a in enumerate(alphas):
                 quad = wqw + 2.0 * a * wqdir + a * a * dqd
                 psi_t = _psi(quad, st[j], x_sq, sigma, opts.psi_eval)
@@ -401,6 +429,11 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
     converged = False
     exhausted = True
     iterations = 0
+    # pipelined: the Newton direction and the unit-step trial of the CURRENT point are
+    # computed speculatively together with its gradient (one host sync per step); at
+    # the step that meets the stopping test they are simply discarded.
+    _, dots, trial0 = eng.advance(int(cur["nfree"]), float(cur["sum_a2_free"]), sigma,
+                                  with_gradient=False)
     for _ in range(ssn_opts.max_inner):
         gnorm = math.sqrt(gnorm2)
         if trace is not None:
@@ -412,24 +445,22 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
         if gnorm <= grad_floor:
             converged, exhausted = True, False
             break
-        p = int(cur["nfree"])
-        eng.direction(p, sigma, float(cur["sum_a2_free"]))
-        sc, _ = eng.fetch(info=(p > 0))
-        if p > 0 and int(eng.h_info[0]) != 0:
-            raise InternalError(f"factor-space Newton matrix not SPD (column {int(eng.h_info[0])})")
-        gd, wqw, wqdir, dqd = (float(v) for v in sc[:4])
+        gd, wqw, wqdir, dqd = dots
         eng.counters["newton"] += 1
         steepest = False
+        first = trial0[0:1]
         if gd >= 0.0:
             sc = eng.steepest()
             gd, wqw, wqdir, dqd = (float(v) for v in sc[:4])
             steepest = True
+            first = None
         psi0 = _psi(wqw, cur, x_sq, sigma, ssn_opts.psi_eval)
         if ssn_opts.mu * abs(gd) <= 1e-16 * (1.0 + abs(psi0)):
             converged, exhausted = True, False
             break
         try:
-            alpha, j, cur, _ = eng.line_search(gd, psi0, wqw, wqdir, dqd, x_sq, ssn_opts)
+            alpha, j, cur, _ = eng.line_search(gd, psi0, wqw, wqdir, dqd, x_sq, ssn_opts,
+                                               first=first)
         except LineSearchError:
             if steepest:
                 exhausted = False
@@ -446,10 +477,7 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
                 break
         eng.accept(alpha, j)
         iterations += 1
-        eng.gradient()
-        eng.be.dots([(eng.grad, None)], eng.scal)
-        sc, _ = eng.fetch()
-        gnorm2 = float(sc[0])
+        gnorm2, dots, trial0 = eng.advance(int(cur["nfree"]), float(cur["sum_a2_free"]), sigma)
     if exhausted and trace is not None:
         trace.append(math.sqrt(gnorm2))
     state.inner_iter_total += iterations

@@ -65,6 +65,49 @@ def test_projection_random_vs_oracle(pkg):
         assert abs(a @ x - d) <= 1e-9 * (1.0 + abs(d)) + 1e-12 * np.abs(a).sum() * np.abs(x).max()
 
 
+@pytest.mark.parametrize("newton,hint_kind", [(0, "zero"), (1, "zero"), (3, "zero"),
+                                              (3, "near"), (8, "far"), (2, "near")])
+def test_projection_search_modes(pkg, newton, hint_kind):
+    """Every root-search route (pure K-ary, Newton then K-ary fallback, warm and cold
+    Newton) lands on the reference's multiplier and free set."""
+    from paper_1910_01312_b200 import _lib
+
+    rng = np.random.default_rng(100 + newton)
+    for trial in range(25):
+        n = int(rng.choice([3, 50, 5000, 60000]))
+        if trial % 2:
+            a = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+            l, u = np.zeros(n), np.full(n, 1.0)
+        else:
+            a = rng.standard_normal(n)
+            a[rng.random(n) < 0.1] = 0.0
+            l, u = -rng.random(n) - 0.1, rng.random(n) + 0.1
+        d = float(a @ (l + rng.random(n) * (u - l)))
+        v = rng.standard_normal(n) * rng.choice([0.5, 5.0, 1e3])
+        if trial % 5 == 0:
+            v = np.round(v, 1)
+        bl = O.BoxLine(a, d, l, u)
+        x_ref, lam_ref, free_ref = O.project(v, bl)
+        box = pkg.BoxLineSet(a, d, l, u)
+        be = box.backend
+        hint = {"zero": 0.0, "near": lam_ref * (1 + 1e-3) + 1e-6, "far": lam_ref + 1e3}[hint_kind]
+        states = be.new_states(1)
+        xo = be.empty(n)
+        fo = be.empty(n, torch.uint8)
+        be.project(_dev(v), box, states, x_out=xo, free_out=fo, hint=hint, newton=newton,
+                   passes=2, phases=7 if newton == 0 else 6)
+        st = be.read_states(states.cpu())
+        rounds = 0
+        while st["status"][0] != _lib.PROJ_APPLIED:
+            rounds += 1
+            assert rounds < 20
+            be.project(_dev(v), box, states, x_out=xo, free_out=fo, phases=6, passes=8, newton=0)
+            st = be.read_states(states.cpu())
+        assert np.abs(xo.cpu().numpy() - x_ref).max() <= 1e-12 * (1.0 + np.abs(x_ref).max())
+        assert abs(float(st["lam"][0]) - lam_ref) <= 1e-12 * (1.0 + abs(lam_ref))
+        np.testing.assert_array_equal(fo.cpu().numpy().astype(bool), free_ref)
+
+
 def test_projection_batched_trials(pkg):
     from paper_1910_01312_b200 import backend as B
 
