@@ -87,6 +87,59 @@ __global__ void __launch_bounds__(XT_WARPS * 32) dense_xt_kernel(XtArgs p, int k
 
 // one warp per output entry: lanes fold splits lane, lane+32, ..., then a fixed
 // shuffle tree -- deterministic and ~32x shorter dependency chains than a thread fold
+// Vectorised X^T V (even lda, 16B-aligned A): thread t owns the column pair
+// (2t, 2t+1) of a panel; the block streams its contiguous row range UNR rows at a
+// time, i.e. UNR independent 16-byte loads in flight per thread, with the row
+// coefficients (labels x vector entries) loaded alongside.  Partials per row split.
+template <int KV, int UNR>
+__global__ void __launch_bounds__(512) dense_xt2_kernel(XtArgs p, int kofs) {
+  const long long col = (long long)blockIdx.y * (2 * blockDim.x) + 2 * threadIdx.x;
+  const bool active = col < p.q;
+  const long long nsplit = gridDim.x;
+  const long long rows_per = ceil_div(p.n, nsplit);
+  const long long r0 = blockIdx.x * rows_per;
+  const long long r1 = min(p.n, r0 + rows_per);
+  const double* vp[KV];
+#pragma unroll
+  for (int j = 0; j < KV; ++j) vp[j] = kofs == 0 ? p.v[j] : p.v[j + 2];
+  double ax[KV], ay[KV];
+#pragma unroll
+  for (int j = 0; j < KV; ++j) ax[j] = ay[j] = 0.0;
+  const double* base = p.A + col;
+  for (long long r = r0; r < r1; r += UNR) {
+    double2 av[UNR];
+    double cf[UNR][KV];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const long long rr = r + u;
+      const bool ok = rr < r1;
+      av[u] = (ok && active) ? __ldg(reinterpret_cast<const double2*>(base + rr * p.lda))
+                             : make_double2(0.0, 0.0);
+      const double sg = (ok && p.rs) ? p.rs[rr] : 1.0;
+#pragma unroll
+      for (int j = 0; j < KV; ++j) {
+        double cv = ok ? vp[j][rr] : 0.0;
+        if (ok && p.svr) cv = __dsub_rn(cv, vp[j][rr + p.n]);
+        cf[u][j] = sg * cv;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+      for (int j = 0; j < KV; ++j) {
+        ax[j] = fma(cf[u][j], av[u].x, ax[j]);
+        ay[j] = fma(cf[u][j], av[u].y, ay[j]);
+      }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int j = 0; j < KV; ++j) {
+    double* dst = p.part + ((long long)blockIdx.x * p.k + kofs + j) * p.q + col;
+    dst[0] = ax[j];
+    dst[1] = ay[j];
+  }
+}
+
 __global__ void dense_xt_fold_kernel(const double* __restrict__ part, long long nsplit, int k,
                                      long long q, double* __restrict__ out) {
   const long long idx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -100,13 +153,17 @@ __global__ void dense_xt_fold_kernel(const double* __restrict__ part, long long 
 
 static int xt_splits(long long n) {
   long long s = ceil_div(n, 64);  // at least 64 rows per split
-  if (s > 296) s = 296;
+  if (s > 4 * 148) s = 4 * 148;
   if (s < 1) s = 1;
   return (int)s;
 }
 
 size_t dense_xt_ws_bytes(long long n_phys, long long q, int k) {
   return (size_t)xt_splits(n_phys) * k * q * sizeof(double);
+}
+
+static bool vec2_ok(const double* A, long long lda, long long q) {
+  return (lda % 2 == 0) && (q % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
 }
 
 cudaError_t launch_dense_xt(const double* A, long long n, long long q, long long lda,
@@ -118,6 +175,24 @@ cudaError_t launch_dense_xt(const double* A, long long n, long long q, long long
   p.part = (double*)ws;
   p.out = out;
   int nsplit = xt_splits(n);
+  if (vec2_ok(A, lda, q)) {
+    long long pairs = q / 2;
+    int threads = (int)min(512LL, ceil_div(pairs, 32) * 32);
+    dim3 grid2(nsplit, (unsigned)ceil_div(pairs, threads));
+    for (int j = 0; j < k;) {
+      if (k - j >= 2) {
+        { note_launch(); dense_xt2_kernel<2, 8><<<grid2, threads, 0, stream>>>(p, j); }
+        j += 2;
+      } else {
+        { note_launch(); dense_xt2_kernel<1, 8><<<grid2, threads, 0, stream>>>(p, j); }
+        j += 1;
+      }
+    }
+    long long tot = (long long)k * q;
+    { note_launch(); dense_xt_fold_kernel<<<(unsigned)ceil_div(tot * 32, 256), 256, 0, stream>>>(p.part, nsplit, k, q, out); }
+    return cudaGetLastError();
+  }
+  nsplit = min(nsplit, 296);
   dim3 grid(nsplit, (unsigned)ceil_div(q, XT_PANEL));
   for (int j = 0; j < k;) {
     if (k - j >= 2) {
@@ -186,10 +261,115 @@ __global__ void __launch_bounds__(X_WARPS * 32) dense_x_kernel(const double* __r
   }
 }
 
+// Vectorised X D: one warp per R rows, lanes stride the row in 16-byte column
+// pairs with all CP x R loads of a warp-task issued before the FMAs (D staged in
+// shared memory as double2), shuffle-tree dot products.
+template <int KV, int R, int CP>
+__global__ void __launch_bounds__(256, 2) dense_x2_kernel(const double* __restrict__ A, long long n,
+                                                      long long q, long long lda,
+                                                      const double* __restrict__ rs, int svr,
+                                                      const double* __restrict__ d, int kofs,
+                                                      double* __restrict__ out, long long nlog) {
+  extern __shared__ double2 sd2[];  // [KV][q/2]
+  const long long pairs = q / 2;
+  for (long long i = threadIdx.x; i < (long long)KV * pairs; i += blockDim.x) {
+    const long long j = i / pairs, c = i % pairs;
+    sd2[i] = make_double2(d[(kofs + j) * q + 2 * c], d[(kofs + j) * q + 2 * c + 1]);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long r0 = gw * R; r0 < n; r0 += nw * R) {
+    double2 av[R][CP];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int cp = 0; cp < CP; ++cp) {
+        const long long c = lane + 32 * cp, r = r0 + rr;
+        av[rr][cp] = (c < pairs && r < n)
+                         ? __ldg(reinterpret_cast<const double2*>(A + r * lda) + c)
+                         : make_double2(0.0, 0.0);
+      }
+    double acc[R][KV];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int j = 0; j < KV; ++j) acc[rr][j] = 0.0;
+#pragma unroll
+    for (int cp = 0; cp < CP; ++cp) {
+      const long long c = lane + 32 * cp;
+      if (c < pairs) {
+#pragma unroll
+        for (int j = 0; j < KV; ++j) {
+          const double2 dv = sd2[j * pairs + c];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+            acc[rr][j] = fma(av[rr][cp].y, dv.y, fma(av[rr][cp].x, dv.x, acc[rr][j]));
+        }
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const long long r = r0 + rr;
+#pragma unroll
+      for (int j = 0; j < KV; ++j) {
+        const double s = warp_sum(acc[rr][j]);
+        if (lane == 0 && r < n) {
+          const double v = rs ? rs[r] * s : s;
+          out[(long long)(kofs + j) * nlog + r] = v;
+          if (svr) out[(long long)(kofs + j) * nlog + r + n] = -v;
+        }
+      }
+    }
+  }
+}
+
+template <int KV, int CP>
+static void launch_x2(const double* A, long long n, long long q, long long lda, const double* rs,
+                      int svr, const double* d, int kofs, double* out, long long nlog,
+                      cudaStream_t stream) {
+  constexpr int R = 2;
+  const size_t smem = (size_t)KV * (q / 2) * sizeof(double2);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(dense_x2_kernel<KV, R, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  long long blocks = ceil_div(n, 8LL * R);
+  if (blocks > 8 * 148) blocks = 8 * 148;
+  note_launch();
+  dense_x2_kernel<KV, R, CP><<<(unsigned)blocks, 256, smem, stream>>>(A, n, q, lda, rs, svr, d, kofs,
+                                                                      out, nlog);
+}
+
+template <int KV>
+static bool dispatch_x2(const double* A, long long n, long long q, long long lda, const double* rs,
+                        int svr, const double* d, int kofs, double* out, long long nlog,
+                        cudaStream_t stream) {
+  const long long cps = ceil_div(q / 2, 32);
+  if (cps <= 1) launch_x2<KV, 1>(A, n, q, lda, rs, svr, d, kofs, out, nlog, stream);
+  else if (cps <= 2) launch_x2<KV, 2>(A, n, q, lda, rs, svr, d, kofs, out, nlog, stream);
+  else if (cps <= 4) launch_x2<KV, 4>(A, n, q, lda, rs, svr, d, kofs, out, nlog, stream);
+  else if (cps <= 8) launch_x2<KV, 8>(A, n, q, lda, rs, svr, d, kofs, out, nlog, stream);
+  else return false;
+  return true;
+}
+
 cudaError_t launch_dense_x(const double* A, long long n, long long q, long long lda,
                            const double* rs, int svr, int k, const double* d, double* out,
                            cudaStream_t stream) {
   long long nlog = svr ? 2 * n : n;
+  if (vec2_ok(A, lda, q) && q <= 512) {
+    for (int j = 0; j < k;) {
+      if (k - j >= 2) {
+        dispatch_x2<2>(A, n, q, lda, rs, svr, d, j, out, nlog, stream);
+        j += 2;
+      } else {
+        dispatch_x2<1>(A, n, q, lda, rs, svr, d, j, out, nlog, stream);
+        j += 1;
+      }
+    }
+    return cudaGetLastError();
+  }
   long long blocks = ceil_div(n, (long long)X_WARPS * X_ROWS);
   if (blocks > 4 * 148) blocks = 4 * 148;
   if (blocks < 1) blocks = 1;

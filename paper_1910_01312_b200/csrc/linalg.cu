@@ -151,8 +151,78 @@ __global__ void __launch_bounds__(CH_NT, 1) chol_solve_kernel(double* __restrict
   if (tid == 0) *info = fail;
 }
 
+// Small systems (m <= SMALL_M): the whole lower triangle lives in shared memory
+// (odd row stride: conflict-free column access), right-looking column Cholesky
+// with all 1024 threads on the trailing update, then column-sweep substitutions.
+static constexpr int SMALL_M = 160;
+
+__global__ void __launch_bounds__(CH_NT, 1) chol_small_kernel(const double* __restrict__ M, int m,
+                                                                const double* __restrict__ b,
+                                                                double scale,
+                                                                double* __restrict__ x,
+                                                                int* __restrict__ info) {
+  extern __shared__ double S[];
+  const int ld = m | 1;
+  double* y = S + (size_t)m * ld;
+  __shared__ int fail;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  if (tid == 0) fail = 0;
+  for (int idx = tid; idx < m * m; idx += blockDim.x) {
+    const int i = idx / m, j = idx % m;
+    if (j <= i) S[i * ld + j] = M[(long long)i * m + j];
+  }
+  for (int i = tid; i < m; i += blockDim.x) y[i] = scale * b[i];
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    if (tid == 0) {
+      double d = S[j * ld + j];
+      if (!(d > 0.0)) {
+        if (fail == 0) fail = j + 1;
+        d = 1.0;
+      }
+      S[j * ld + j] = sqrt(d);
+    }
+    __syncthreads();
+    const double ljj = S[j * ld + j];
+    for (int i = j + 1 + tid; i < m; i += blockDim.x) S[i * ld + j] /= ljj;
+    __syncthreads();
+    for (int i = j + 1 + ty; i < m; i += 32) {
+      const double lij = S[i * ld + j];
+      for (int k = j + 1 + tx; k <= i; k += 32) S[i * ld + k] -= lij * S[k * ld + j];
+    }
+    __syncthreads();
+  }
+  // forward: L z = y  (column sweep)
+  for (int j = 0; j < m; ++j) {
+    if (tid == 0) y[j] /= S[j * ld + j];
+    __syncthreads();
+    const double yj = y[j];
+    for (int i = j + 1 + tid; i < m; i += blockDim.x) y[i] -= S[i * ld + j] * yj;
+    __syncthreads();
+  }
+  // backward: L^T x = z  (row sweep on L^T = column sweep on L rows)
+  for (int j = m - 1; j >= 0; --j) {
+    if (tid == 0) y[j] /= S[j * ld + j];
+    __syncthreads();
+    const double yj = y[j];
+    for (int i = tid; i < j; i += blockDim.x) y[i] -= S[j * ld + i] * yj;
+    __syncthreads();
+  }
+  for (int i = tid; i < m; i += blockDim.x) x[i] = y[i];
+  if (tid == 0) *info = fail;
+}
+
 cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
                               int* info, cudaStream_t stream) {
+  if (m <= SMALL_M) {
+    const int mi = (int)m;
+    const size_t smem = ((size_t)mi * (mi | 1) + mi) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(chol_small_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    { note_launch(); chol_small_kernel<<<1, CH_NT, smem, stream>>>(M, mi, b, scale, x, info); }
+    return cudaGetLastError();
+  }
   size_t smem = (size_t)(NB * (NB + 1) + PANEL_ROWS * (NB + 1)) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

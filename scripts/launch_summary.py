@@ -1,0 +1,27 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list (per-kernel share)."""
+import collections
+import csv
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+hdr = None
+agg = collections.defaultdict(lambda: [0, 0.0])
+for r in rows:
+    if r and r[0] == "ID":
+        hdr = r
+        continue
+    if not hdr or len(r) != len(hdr):
+        continue
+    d = dict(zip(hdr, r))
+    if d.get("Metric Name") != "gpu__time_duration.sum":
+        continue
+    name = d["Kernel Name"].split("(")[0]
+    v = float(d["Metric Value"].replace(",", ""))
+    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(d["Metric Unit"], 1.0)
+    agg[name][0] += 1
+    agg[name][1] += v * scale
+tot = sum(v[1] for v in agg.values())
+print(f"{'kernel':44s} {'launches':>8s} {'total_us':>10s} {'us/launch':>10s} {'share':>6s}")
+for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f"{k:44s} {c:8d} {t:10.1f} {t / c:10.2f} {100 * t / tot:5.1f}%")
+print(f"total {tot:.1f} us over {sum(v[0] for v in agg.values())} launches")

@@ -188,6 +188,28 @@ def test_dense_products(pkg, shape, svr, signed):
     assert np.abs(out.T - ref).max() <= 1e-12 * np.abs(X).sum(axis=1).max() * np.abs(d).max()
 
 
+@pytest.mark.parametrize("m", [1, 7, 33, 115, 160, 161, 300, 517])
+def test_cholesky_solve_sizes(pkg, m):
+    """Both Cholesky routes (shared-memory resident m <= 160, blocked otherwise)."""
+    be = pkg.default_backend()
+    rng = np.random.default_rng(m)
+    G = rng.standard_normal((m, m + 3))
+    M = np.eye(m) + 3.0 * G @ G.T
+    b = rng.standard_normal(m)
+    Md = _dev(M)
+    xo = be.empty(m)
+    info = be.zeros(1, torch.int32)
+    be.chol_solve(Md, m, _dev(b), -2.0, xo, info)
+    assert int(info.cpu()[0]) == 0
+    x_ref = -2.0 * np.linalg.solve(M, b)
+    assert np.linalg.norm(xo.cpu().numpy() - x_ref) <= 1e-12 * np.linalg.cond(M) * np.linalg.norm(x_ref)
+    # not SPD -> info reports the failing column
+    Mbad = M.copy()
+    Mbad[m // 2, m // 2] = -1.0
+    be.chol_solve(_dev(Mbad), m, _dev(b), 1.0, xo, info)
+    assert int(info.cpu()[0]) > 0
+
+
 @pytest.mark.parametrize("n,q,p", [(500, 50, 37), (5000, 300, 300), (3000, 130, 1), (9000, 500, 2000)])
 def test_gram_and_cholesky(pkg, n, q, p):
     rng = np.random.default_rng(q)
