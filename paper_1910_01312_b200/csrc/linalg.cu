@@ -156,7 +156,9 @@ __global__ void __launch_bounds__(CH_NT, 1) chol_solve_kernel(double* __restrict
 // with all 1024 threads on the trailing update, then column-sweep substitutions.
 static constexpr int SMALL_M = 160;
 
-__global__ void __launch_bounds__(CH_NT, 1) chol_small_kernel(const double* __restrict__ M, int m,
+static constexpr int SM_NT = 512;  // 128 registers/thread: the 32-double row of warp 0 stays in RF
+
+__global__ void __launch_bounds__(SM_NT, 1) chol_small_kernel(const double* __restrict__ M, int m,
                                                                 const double* __restrict__ b,
                                                                 double scale,
                                                                 double* __restrict__ x,
@@ -173,39 +175,104 @@ __global__ void __launch_bounds__(CH_NT, 1) chol_small_kernel(const double* __re
   }
   for (int i = tid; i < m; i += blockDim.x) y[i] = scale * b[i];
   __syncthreads();
-  for (int j = 0; j < m; ++j) {
-    if (tid == 0) {
-      double d = S[j * ld + j];
-      if (!(d > 0.0)) {
-        if (fail == 0) fail = j + 1;
-        d = 1.0;
+  const int lane = tx, warp = ty;
+  __shared__ double rdiag[32];
+  for (int k0 = 0; k0 < m; k0 += 32) {
+    const int kb = min(32, m - k0);
+    // (1) diagonal block: warp 0, lane i holds row i in registers; right-looking
+    //     with shuffles -- no block barrier inside the 32 steps
+    if (warp == 0) {
+      double r[32];
+      double mydiag = 1.0;
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        r[c] = (lane < kb && c <= lane) ? S[(k0 + lane) * ld + k0 + c] : (c == lane ? 1.0 : 0.0);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        double d = __shfl_sync(0xffffffffu, r[j], j);
+        if (j < kb && !(d > 0.0)) {
+          if (lane == 0 && fail == 0) fail = k0 + j + 1;
+          d = 1.0;
+        }
+        const double ljj = sqrt(d);
+        if (lane == j) { r[j] = ljj; mydiag = ljj; }
+        if (lane > j) r[j] = r[j] / ljj;
+        const double lij = r[j];
+#pragma unroll
+        for (int c = j + 1; c < 32; ++c) {
+          const double lcj = __shfl_sync(0xffffffffu, r[j], c);
+          if (lane >= c) r[c] = fma(-lij, lcj, r[c]);
+        }
       }
-      S[j * ld + j] = sqrt(d);
+      if (lane < kb) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (c <= lane) S[(k0 + lane) * ld + k0 + c] = r[c];
+        rdiag[lane] = 1.0 / mydiag;
+      }
     }
     __syncthreads();
-    const double ljj = S[j * ld + j];
-    for (int i = j + 1 + tid; i < m; i += blockDim.x) S[i * ld + j] /= ljj;
+    // (2) panel: L21 = A21 L11^{-T}, one thread per row (reciprocal diagonal)
+    for (int i = k0 + kb + tid; i < m; i += blockDim.x) {
+      double* row = S + i * ld + k0;
+      for (int j = 0; j < kb; ++j) {
+        double s = row[j];
+        const double* lj = S + (k0 + j) * ld + k0;
+        for (int t = 0; t < j; ++t) s = fma(-row[t], lj[t], s);
+        row[j] = s * rdiag[j];
+      }
+    }
     __syncthreads();
-    for (int i = j + 1 + ty; i < m; i += 32) {
-      const double lij = S[i * ld + j];
-      for (int k = j + 1 + tx; k <= i; k += 32) S[i * ld + k] -= lij * S[k * ld + j];
+    // (3) trailing update A22 -= L21 L21^T (lower triangle)
+    for (int i = k0 + kb + ty; i < m; i += SM_NT / 32) {
+      const double* li = S + i * ld + k0;
+      for (int c = k0 + kb + tx; c <= i; c += 32) {
+        const double* lc = S + c * ld + k0;
+        double s = 0.0;
+        for (int t = 0; t < kb; ++t) s = fma(li[t], lc[t], s);
+        S[i * ld + c] -= s;
+      }
     }
     __syncthreads();
   }
-  // forward: L z = y  (column sweep)
-  for (int j = 0; j < m; ++j) {
-    if (tid == 0) y[j] /= S[j * ld + j];
+  // forward L z = y and backward L^T x = z: diagonal block by warp 0 with shuffles,
+  // off-diagonal updates by all threads
+  for (int k0 = 0; k0 < m; k0 += 32) {
+    const int kb = min(32, m - k0);
+    if (warp == 0) {
+      double yv = lane < kb ? y[k0 + lane] : 0.0;
+      for (int j = 0; j < kb; ++j) {
+        if (lane == j) yv = yv / S[(k0 + j) * ld + k0 + j];
+        const double yj = __shfl_sync(0xffffffffu, yv, j);
+        if (lane > j && lane < kb) yv = fma(-S[(k0 + lane) * ld + k0 + j], yj, yv);
+      }
+      if (lane < kb) y[k0 + lane] = yv;
+    }
     __syncthreads();
-    const double yj = y[j];
-    for (int i = j + 1 + tid; i < m; i += blockDim.x) y[i] -= S[i * ld + j] * yj;
+    for (int i = k0 + kb + tid; i < m; i += blockDim.x) {
+      double s = y[i];
+      for (int t = 0; t < kb; ++t) s = fma(-S[i * ld + k0 + t], y[k0 + t], s);
+      y[i] = s;
+    }
     __syncthreads();
   }
-  // backward: L^T x = z  (row sweep on L^T = column sweep on L rows)
-  for (int j = m - 1; j >= 0; --j) {
-    if (tid == 0) y[j] /= S[j * ld + j];
+  for (int k0 = ((m - 1) / 32) * 32; k0 >= 0; k0 -= 32) {
+    const int kb = min(32, m - k0);
+    if (warp == 0) {
+      double xv = lane < kb ? y[k0 + lane] : 0.0;
+      for (int j = kb - 1; j >= 0; --j) {
+        if (lane == j) xv = xv / S[(k0 + j) * ld + k0 + j];
+        const double xj = __shfl_sync(0xffffffffu, xv, j);
+        if (lane < j) xv = fma(-S[(k0 + j) * ld + k0 + lane], xj, xv);
+      }
+      if (lane < kb) y[k0 + lane] = xv;
+    }
     __syncthreads();
-    const double yj = y[j];
-    for (int i = tid; i < j; i += blockDim.x) y[i] -= S[j * ld + i] * yj;
+    for (int i = tid; i < k0; i += blockDim.x) {
+      double s = y[i];
+      for (int t = 0; t < kb; ++t) s = fma(-S[(k0 + t) * ld + i], y[k0 + t], s);
+      y[i] = s;
+    }
     __syncthreads();
   }
   for (int i = tid; i < m; i += blockDim.x) x[i] = y[i];
@@ -220,7 +287,7 @@ cudaError_t launch_chol_solve(double* M, long long m, const double* b, double sc
     cudaError_t e = cudaFuncSetAttribute(chol_small_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    { note_launch(); chol_small_kernel<<<1, CH_NT, smem, stream>>>(M, mi, b, scale, x, info); }
+    { note_launch(); chol_small_kernel<<<1, SM_NT, smem, stream>>>(M, mi, b, scale, x, info); }
     return cudaGetLastError();
   }
   size_t smem = (size_t)(NB * (NB + 1) + PANEL_ROWS * (NB + 1)) * sizeof(double);

@@ -17,7 +17,7 @@ for r in rows:
         continue
     name = d["Kernel Name"].split("(")[0]
     v = float(d["Metric Value"].replace(",", ""))
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(d["Metric Unit"], 1.0)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(d["Metric Unit"], 1.0)
     agg[name][0] += 1
     agg[name][1] += v * scale
 tot = sum(v[1] for v in agg.values())
