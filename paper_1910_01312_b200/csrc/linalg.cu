@@ -179,38 +179,34 @@ __global__ void __launch_bounds__(SM_NT, 1) chol_small_kernel(const double* __re
   __shared__ double rdiag[32];
   for (int k0 = 0; k0 < m; k0 += 32) {
     const int kb = min(32, m - k0);
-    // (1) diagonal block: warp 0, lane i holds row i in registers; right-looking
-    //     with shuffles -- no block barrier inside the 32 steps
-    if (warp == 0) {
-      double r[32];
-      double mydiag = 1.0;
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        r[c] = (lane < kb && c <= lane) ? S[(k0 + lane) * ld + k0 + c] : (c == lane ? 1.0 : 0.0);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        double d = __shfl_sync(0xffffffffu, r[j], j);
-        if (j < kb && !(d > 0.0)) {
-          if (lane == 0 && fail == 0) fail = k0 + j + 1;
-          d = 1.0;
-        }
-        const double ljj = sqrt(d);
-        if (lane == j) { r[j] = ljj; mydiag = ljj; }
-        if (lane > j) r[j] = r[j] / ljj;
-        const double lij = r[j];
-#pragma unroll
-        for (int c = j + 1; c < 32; ++c) {
-          const double lcj = __shfl_sync(0xffffffffu, r[j], c);
-          if (lane >= c) r[c] = fma(-lij, lcj, r[c]);
-        }
+    // (1) diagonal block, 2-D parallel over its (i, c) pairs: per column one barrier
+    //     for the scaled column, one for the rank-1 update (every thread recomputes
+    //     the pivot sqrt itself instead of waiting on a broadcast)
+    for (int j = 0; j < kb; ++j) {
+      double d = S[(k0 + j) * ld + k0 + j];
+      if (!(d > 0.0)) {
+        if (tid == 0 && fail == 0) fail = k0 + j + 1;
+        d = 1.0;
       }
-      if (lane < kb) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (c <= lane) S[(k0 + lane) * ld + k0 + c] = r[c];
-        rdiag[lane] = 1.0 / mydiag;
+      const double ljj = sqrt(d);
+      __syncthreads();  // everyone has read the pivot before it is overwritten
+      if (tid == 0) {
+        S[(k0 + j) * ld + k0 + j] = ljj;
+        rdiag[j] = 1.0 / ljj;
+      }
+      for (int i = k0 + j + 1 + tid; i < k0 + kb; i += blockDim.x) S[i * ld + k0 + j] /= ljj;
+      __syncthreads();
+      const int r = kb - j - 1;  // trailing rows inside the block
+      for (int idx = tid; idx < r * r; idx += blockDim.x) {
+        const int ii = idx / r, cc = idx % r;
+        if (cc <= ii) {
+          const int i = k0 + j + 1 + ii, c = k0 + j + 1 + cc;
+          S[i * ld + c] = fma(-S[i * ld + k0 + j], S[c * ld + k0 + j], S[i * ld + c]);
+        }
       }
     }
+    (void)lane;
+    (void)warp;
     __syncthreads();
     // (2) panel: L21 = A21 L11^{-T}, one thread per row (reciprocal diagonal)
     for (int i = k0 + kb + tid; i < m; i += blockDim.x) {
