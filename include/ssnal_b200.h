@@ -159,6 +159,52 @@ int ssnal_dense_newton_pspace(const double* A, int64_t n_phys, int64_t q, int64_
                               const double* grad, const double* a, double sigma, double asa,
                               const double* g_r, double* t, int* info, void* ws, void* stream);
 
+/* ---- native SSsNAL driver ------------------------------------------------
+ * The whole Algorithm 1 / Algorithm 3 loop of ref solver.py:331-530 (alm_solve,
+ * ssn_solve, line_search, newton_direction, kkt_residual) run from C++ on one
+ * stream: kernels are enqueued back to back and the host synchronises only at
+ * the reference's decision points (one pinned read per Newton step in the
+ * common case).  Same constants, criteria, safeguards and report fields as the
+ * reference; eps_k = delta_k = 0.5^k (the reference defaults). */
+typedef struct ssnal_dense_problem_t {
+  const double* A;          /* n_phys x q row-major samples (DEVICE)                 */
+  int64_t n_phys, q, lda;
+  const double* row_sign;   /* labels for C-SVC or NULL                              */
+  int svr_block;            /* 1: X = [A; -A] (eps-SVR)                              */
+  int64_t n;                /* logical variables (2 n_phys for SVR)                  */
+  const double* c;          /* linear term (DEVICE, n)                               */
+  const double* a;          /* equality row (DEVICE, n)                              */
+  const double* l;          /* lower bounds (DEVICE, n) or NULL => l_const           */
+  const double* u;          /* upper bounds (DEVICE, n) or NULL => u_const           */
+  double l_const, u_const, d;
+} ssnal_dense_problem_t;
+
+typedef struct ssnal_options_t {
+  double sigma0, sigma_growth, sigma_max, tol_kkt, lambda_min_surrogate;  /* AlmOptions */
+  int max_outer;
+  double mu, backtrack, tau, eta;                                         /* SsnOptions */
+  int max_inner, direct_solve_threshold, cg_max_iters, line_search_batch;
+  int psi_stable;           /* 1: psi via sum Pi(u)(2u - Pi(u)); 0: reference formula */
+} ssnal_options_t;
+
+typedef struct ssnal_report_t {
+  double kkt_residual, objective, wall_time;
+  int outer_iters, total_inner_iters, unbounded_support_count, converged;
+  int hit_max_inner_mask;   /* bit k: inner solver hit max_inner at outer k (k < 31)   */
+  int stagnated, max_outer_reached;
+  long long syncs, newton_steps, projections, launches;
+} ssnal_report_t;
+
+/* per outer iteration: (k, R_KKT, sigma, p, inner iterations) as ref solver.py:474-475 */
+typedef void (*ssnal_progress_fn)(int k, double kkt, double sigma, long long p, int inner,
+                                  void* ctx);
+
+size_t ssnal_alm_ws_bytes(int64_t n_phys, int64_t q, int svr_block);
+int ssnal_alm_solve_dense(const ssnal_dense_problem_t* problem, const ssnal_options_t* options,
+                          const double* x0, const double* w0, double* x_out,
+                          ssnal_report_t* report, void* ws, size_t ws_bytes,
+                          ssnal_progress_fn progress, void* progress_ctx, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -61,6 +61,40 @@ _SIGNATURES = {
                                        _P, _P, _P, _P, _P]),
 }
 
+class DenseProblem(ctypes.Structure):
+    """ssnal_dense_problem_t"""
+    _fields_ = [("A", _P), ("n_phys", ctypes.c_int64), ("q", ctypes.c_int64),
+                ("lda", ctypes.c_int64), ("row_sign", _P), ("svr_block", _I),
+                ("n", ctypes.c_int64), ("c", _P), ("a", _P), ("l", _P), ("u", _P),
+                ("l_const", _D), ("u_const", _D), ("d", _D)]
+
+
+class Options(ctypes.Structure):
+    """ssnal_options_t"""
+    _fields_ = [("sigma0", _D), ("sigma_growth", _D), ("sigma_max", _D), ("tol_kkt", _D),
+                ("lambda_min_surrogate", _D), ("max_outer", _I), ("mu", _D), ("backtrack", _D),
+                ("tau", _D), ("eta", _D), ("max_inner", _I), ("direct_solve_threshold", _I),
+                ("cg_max_iters", _I), ("line_search_batch", _I), ("psi_stable", _I)]
+
+
+class Report(ctypes.Structure):
+    """ssnal_report_t"""
+    _fields_ = [("kkt_residual", _D), ("objective", _D), ("wall_time", _D),
+                ("outer_iters", _I), ("total_inner_iters", _I),
+                ("unbounded_support_count", _I), ("converged", _I),
+                ("hit_max_inner_mask", _I), ("stagnated", _I), ("max_outer_reached", _I),
+                ("syncs", ctypes.c_longlong), ("newton_steps", ctypes.c_longlong),
+                ("projections", ctypes.c_longlong), ("launches", ctypes.c_longlong)]
+
+
+PROGRESS_FN = ctypes.CFUNCTYPE(None, _I, _D, _D, ctypes.c_longlong, _I, _P)
+
+_SIGNATURES.update({
+    "ssnal_alm_ws_bytes": (_SZ, [_I64, _I64, _I]),
+    "ssnal_alm_solve_dense": (_I, [ctypes.POINTER(DenseProblem), ctypes.POINTER(Options), _P, _P,
+                                   _P, ctypes.POINTER(Report), _P, _SZ, PROGRESS_FN, _P, _P]),
+})
+
 _lib = None
 
 

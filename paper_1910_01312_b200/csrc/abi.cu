@@ -33,6 +33,11 @@ cudaError_t launch_dense_gram(const double* A, long long n, long long q, long lo
 cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
                               int* info, cudaStream_t s);
 size_t pspace_ws_bytes(long long p, long long q);
+size_t alm_ws_bytes(long long n_phys, long long q, int svr);
+int alm_solve_dense(const ssnal_dense_problem_t* pb, const ssnal_options_t* opt, const double* x0,
+                    const double* w0, double* x_out, ssnal_report_t* rep, void* ws,
+                    size_t ws_bytes, ssnal_progress_fn cb, void* ctx, cudaStream_t stream,
+                    const char** err);
 cudaError_t launch_pspace_direction(const double* A, long long n, long long q, long long lda,
                                     const double* rs, int svr, const int32_t* J, long long p,
                                     const double* grad, const double* a, double sigma, double asa,
@@ -172,6 +177,28 @@ int ssnal_dense_gram(const double* A, int64_t n_phys, int64_t q, int64_t lda,
 }
 
 size_t ssnal_pspace_ws_bytes(int64_t p, int64_t q) { return pspace_ws_bytes(p, q); }
+
+size_t ssnal_alm_ws_bytes(int64_t n_phys, int64_t q, int svr_block) {
+  return alm_ws_bytes(n_phys, q, svr_block);
+}
+
+int ssnal_alm_solve_dense(const ssnal_dense_problem_t* problem, const ssnal_options_t* options,
+                          const double* x0, const double* w0, double* x_out,
+                          ssnal_report_t* report, void* ws, size_t ws_bytes,
+                          ssnal_progress_fn progress, void* progress_ctx, void* stream) {
+  if (!problem || !options || !x_out || !report || !ws)
+    return fail_arg("ssnal_alm_solve_dense", "null problem/options/x_out/report/ws");
+  const ssnal_dense_problem_t& p = *problem;
+  if (p.n_phys < 1 || p.q < 1 || p.lda < p.q || !p.A || !p.c || !p.a ||
+      p.n != (p.svr_block ? 2 * p.n_phys : p.n_phys))
+    return fail_arg("ssnal_alm_solve_dense", "inconsistent problem sizes");
+  const char* err = nullptr;
+  int rc = alm_solve_dense(problem, options, x0, w0, x_out, report, ws, ws_bytes, progress,
+                           progress_ctx, S(stream), &err);
+  if (rc != SSNAL_OK)
+    snprintf(g_err, sizeof g_err, "ssnal_alm_solve_dense: %s", err ? err : "failed");
+  return rc;
+}
 
 int ssnal_dense_newton_pspace(const double* A, int64_t n_phys, int64_t q, int64_t lda,
                               const double* row_sign, int svr_block, const int32_t* J, int64_t p,

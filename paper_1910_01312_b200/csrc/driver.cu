@@ -1,0 +1,576 @@
+// Native SSsNAL driver: Algorithm 1 (ALM outer loop) + Algorithm 3 (semismooth
+// Newton inner loop) for Q = X X^T on one CUDA stream.
+//
+// Control flow mirrors ref solver.py:331-530 branch for branch (and
+// paper_1910_01312_b200/solver.py, the Python mirror of the same loop): criteria
+// (A')/(B'), grad floor, steepest-descent rescue, Armijo batches, best-iterate
+// safeguard, sigma cap stagnation.  The host only synchronises at the
+// decision points: the KKT residual per outer step, the start of every inner
+// solve, and one pinned read per Newton step (gradient norm + Newton
+// direction inner products + the unit-step Armijo trial, enqueued together).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "ssnal_internal.h"
+
+namespace ssnal {
+
+int stream_blocks(long long n, int per_thread);
+size_t reduce_ws_bytes(long long n);
+size_t compact_ws_bytes(long long n);
+size_t dense_xt_ws_bytes(long long n_phys, long long q, int k);
+size_t gram_ws_bytes(long long q);
+size_t pspace_ws_bytes(long long p, long long q);
+cudaError_t launch_dots(int k, const double* const* xs, const double* const* ys,
+                        const uint8_t* mask, long long n, double* out, void* ws, cudaStream_t s);
+cudaError_t launch_vec(int op, long long n, double alpha, const double* x, const double* y,
+                       const double* z, double* out, cudaStream_t s);
+cudaError_t launch_hs_apply(const uint8_t* fm, const double* a, const double* y, long long n,
+                            double beta, const double* add, double alpha, double* out, void* ws,
+                            cudaStream_t s);
+cudaError_t launch_compact(const uint8_t* m, long long n, int32_t* idx, long long* count, void* ws,
+                           cudaStream_t s);
+cudaError_t launch_dense_xt(const double* A, long long n, long long q, long long lda,
+                            const double* rs, int svr, int k, const double* const* vs, double* out,
+                            void* ws, cudaStream_t s);
+cudaError_t launch_dense_x(const double* A, long long n, long long q, long long lda,
+                           const double* rs, int svr, int k, const double* d, double* out,
+                           cudaStream_t s);
+cudaError_t launch_dense_gram(const double* A, long long n, long long q, long long lda,
+                              const double* rs, int svr, const int32_t* J, const long long* p_dev,
+                              long long p_max, const double* a, double sigma, const double* asa_dev,
+                              double* M, double* m1, void* ws, cudaStream_t s);
+cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
+                              int* info, cudaStream_t s);
+cudaError_t launch_pspace_direction(const double* A, long long n, long long q, long long lda,
+                                    const double* rs, int svr, const int32_t* J, long long p,
+                                    const double* grad, const double* a, double sigma, double asa,
+                                    const double* g_r, double* t, int* info, void* ws,
+                                    cudaStream_t stream);
+
+namespace {
+
+constexpr int TMAX = 4;  // batched Armijo trials per launch
+constexpr int NSCAL = 16;
+
+struct DriverError {
+  int code;
+  const char* what;
+};
+
+// bump allocator over the caller's workspace (256-byte aligned slices)
+struct Carver {
+  char* base;
+  size_t off = 0, cap;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+struct Pinned {
+  double scal[NSCAL];
+  int info;
+  int pad;
+  ProjState st[TMAX];
+};
+
+Pinned* pinned_buffer() {
+  static thread_local Pinned* buf = nullptr;
+  if (!buf) {
+    if (cudaHostAlloc(&buf, sizeof(Pinned), cudaHostAllocDefault) != cudaSuccess) buf = nullptr;
+  }
+  return buf;
+}
+
+struct Layout {
+  double *x, *w, *qw, *u, *xp, *s, *grad, *qdir, *dir, *tmp, *qx, *qwx, *best_x, *tx;
+  double *gr, *t, *M, *m1, *scal;
+  uint8_t *fr, *tfree;
+  int32_t* J;
+  long long* pcount;
+  int* info;
+  ProjState *st_cur, *st_trial, *st_kkt;
+  void *ws_proj, *ws_red, *ws_xt, *ws_gram, *ws_cmp, *ws_ps;
+};
+
+Layout carve(char* base, long long n, long long n_phys, long long q, size_t* total) {
+  Carver cv{base, 0, 0};
+  Layout L;
+  L.x = cv.take<double>(n);
+  L.w = cv.take<double>(n);
+  L.qw = cv.take<double>(n);
+  L.u = cv.take<double>(n);
+  L.xp = cv.take<double>(n);
+  L.s = cv.take<double>(n);
+  L.grad = cv.take<double>(n);
+  L.qdir = cv.take<double>(n);
+  L.dir = cv.take<double>(n);
+  L.tmp = cv.take<double>(n);
+  L.qx = cv.take<double>(n);
+  L.qwx = cv.take<double>(2 * n);
+  L.best_x = cv.take<double>(n);
+  L.tx = cv.take<double>((size_t)TMAX * n);
+  L.gr = cv.take<double>(2 * q);
+  L.t = cv.take<double>(q);
+  L.M = cv.take<double>((size_t)q * q);
+  L.m1 = cv.take<double>(q);
+  L.scal = cv.take<double>(NSCAL);
+  L.fr = cv.take<uint8_t>(n);
+  L.tfree = cv.take<uint8_t>((size_t)TMAX * n);
+  L.J = cv.take<int32_t>(n);
+  L.pcount = cv.take<long long>(1);
+  L.info = cv.take<int>(1);
+  L.st_cur = cv.take<ProjState>(1);
+  L.st_trial = cv.take<ProjState>(TMAX);
+  L.st_kkt = cv.take<ProjState>(1);
+  L.ws_proj = cv.take<char>(proj_ws_bytes(n, TMAX));
+  L.ws_red = cv.take<char>(reduce_ws_bytes(n) + 64);
+  L.ws_xt = cv.take<char>(dense_xt_ws_bytes(n_phys, q, 2));
+  L.ws_gram = cv.take<char>(gram_ws_bytes(q));
+  L.ws_cmp = cv.take<char>(compact_ws_bytes(n));
+  L.ws_ps = cv.take<char>(pspace_ws_bytes(q, q));
+  *total = cv.off + 256;
+  return L;
+}
+
+void ck(cudaError_t e) {
+  if (e != cudaSuccess) throw DriverError{(int)e, cudaGetErrorString(e)};
+}
+
+struct Driver {
+  const ssnal_dense_problem_t& P;
+  const ssnal_options_t& O;
+  cudaStream_t S;
+  Layout L;
+  Pinned* H;
+  long long syncs = 0, newton = 0, projections = 0;
+  double lam_kkt = 0.0, lam_cur = 0.0;
+  double sigma = 1.0;
+  double c_norm = 0.0;
+
+  Driver(const ssnal_dense_problem_t& p, const ssnal_options_t& o, cudaStream_t s, Layout l,
+         Pinned* h)
+      : P(p), O(o), S(s), L(l), H(h) {}
+
+  // ---------------------------------------------------------------- plumbing
+  void fetch(const ProjState* states, int T, bool info) {
+    ck(cudaMemcpyAsync(H->scal, L.scal, sizeof(double) * NSCAL, cudaMemcpyDeviceToHost, S));
+    if (states) ck(cudaMemcpyAsync(H->st, states, sizeof(ProjState) * T, cudaMemcpyDeviceToHost, S));
+    if (info) ck(cudaMemcpyAsync(&H->info, L.info, sizeof(int), cudaMemcpyDeviceToHost, S));
+    ck(cudaStreamSynchronize(S));
+    ++syncs;
+  }
+
+  void project(const double* A, ProjState* st, int T, const double* B, const double* coefs,
+               double* xo, uint8_t* fo, const double* ref, double hint, int newton_passes = 3,
+               int passes = 0, int phases = 4) {
+    ProjLaunch pl;
+    pl.A = A; pl.B = B; pl.coef = coefs; pl.a = P.a; pl.l = P.l; pl.u = P.u;
+    pl.lc = P.l_const; pl.uc = P.u_const; pl.d = P.d; pl.n = P.n; pl.T = T;
+    pl.st = st; pl.part = (double*)L.ws_proj; pl.x_out = xo; pl.free_out = fo; pl.ref = ref;
+    pl.phases = phases; pl.passes = passes; pl.hint = hint; pl.newton = newton_passes;
+    ck(launch_project(pl, S));
+    ++projections;
+  }
+
+  static void raise_status(int s) {
+    if (s == PROJ_INFEASIBLE_LOW || s == PROJ_INFEASIBLE_HIGH)
+      throw DriverError{SSNAL_E_ARG, "projection bracket failed: constraint set infeasible"};
+  }
+
+  // rare: a trial needed more bracketing than the default launch
+  bool finish(ProjState* st_dev, int T, const double* A, const double* B, const double* coefs,
+              double* xo, uint8_t* fo, const double* ref) {
+    bool extra = false;
+    for (int round = 0;; ++round) {
+      bool pending = false;
+      for (int t = 0; t < T; ++t) {
+        raise_status(H->st[t].status);
+        if (H->st[t].status != PROJ_APPLIED) pending = true;
+      }
+      if (!pending) return extra;
+      if (round > 20) throw DriverError{SSNAL_E_ARG, "projection failed to bracket the multiplier"};
+      extra = true;
+      project(A, st_dev, T, B, coefs, xo, fo, ref, 0.0, 0, 8, PHASE_EXACT | PHASE_APPLY);
+      fetch(st_dev, T, false);
+    }
+  }
+
+  void dots(std::initializer_list<std::pair<const double*, const double*>> pairs, double* out,
+            long long len) {
+    const double* xs[8];
+    const double* ys[8];
+    int k = 0;
+    for (auto& pr : pairs) {
+      xs[k] = pr.first;
+      ys[k] = pr.second;
+      ++k;
+    }
+    ck(launch_dots(k, xs, ys, nullptr, len, out, L.ws_red, S));
+  }
+
+  void vec(int op, double alpha, const double* x, const double* y, const double* z, double* out) {
+    ck(launch_vec(op, P.n, alpha, x, y, z, out, S));
+  }
+
+  void xt(std::initializer_list<const double*> vs, double* out) {
+    const double* arr[4];
+    int k = 0;
+    for (auto v : vs) arr[k++] = v;
+    ck(launch_dense_xt(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, k, arr, out, L.ws_xt, S));
+  }
+
+  void xd(const double* d, double* out, int k) {
+    ck(launch_dense_x(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, k, d, out, S));
+  }
+
+  double psi(double wqw, const ProjState& r, double x_sq) const {
+    const double diff = O.psi_stable ? r.sum_xv : (r.sum_v2 - r.sum_r2);
+    return 0.5 * wqw + diff / (2.0 * sigma) - x_sq / (2.0 * sigma);
+  }
+
+  // ---------------------------------------------------------------- outer pieces
+  // returns residual; p and objective through refs; refreshes Qw when w given
+  double kkt_and_refresh(double* x, double* w, double* qw_out, long long& p, double& obj) {
+    if (w) {
+      xt({x, w}, L.gr);
+      xd(L.gr, L.qwx, 2);
+      ck(cudaMemcpyAsync(L.qx, L.qwx, sizeof(double) * P.n, cudaMemcpyDeviceToDevice, S));
+      ck(cudaMemcpyAsync(qw_out, L.qwx + P.n, sizeof(double) * P.n, cudaMemcpyDeviceToDevice, S));
+    } else {
+      xt({x}, L.gr);
+      xd(L.gr, L.qx, 1);
+    }
+    vec(1, 0.0, x, L.qx, P.c, L.tmp);
+    project(L.tmp, L.st_kkt, 1, nullptr, nullptr, nullptr, nullptr, x, lam_kkt);
+    dots({{x, nullptr}, {x, L.qx}, {P.c, x}}, L.scal, P.n);
+    fetch(L.st_kkt, 1, false);
+    const double xx = H->scal[0], xqx = H->scal[1], cx = H->scal[2];
+    finish(L.st_kkt, 1, L.tmp, nullptr, nullptr, nullptr, nullptr, x);
+    lam_kkt = H->st[0].lam;
+    p = H->st[0].nfree;
+    obj = 0.5 * xqx + cx;
+    return std::sqrt(H->st[0].sum_dref2) / (1.0 + std::sqrt(xx));
+  }
+
+  // ---------------------------------------------------------------- inner pieces
+  void gradient() {
+    vec(3, 0.0, L.w, L.xp, nullptr, L.s);
+    xt({L.s}, L.gr);
+    xd(L.gr, L.grad, 1);
+  }
+
+  void direction(long long p, double asa) {
+    if (p == 0) {  // Sigma = 0: d = -s, Qd = -grad (ref solver.py:221-222)
+      vec(4, -1.0, L.s, nullptr, nullptr, L.dir);
+      vec(4, -1.0, L.grad, nullptr, nullptr, L.qdir);
+      dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}, {L.s, L.grad}}, L.scal, P.n);
+      return;
+    }
+    ck(launch_compact(L.fr, P.n, L.J, L.pcount, L.ws_cmp, S));
+    if (p < P.q) {
+      if (p > O.direct_solve_threshold)
+        throw DriverError{SSNAL_E_ARG, "p x p system above direct_solve_threshold (no CG path)"};
+      ck(launch_pspace_direction(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, p,
+                                 L.grad, P.a, sigma, asa, L.gr, L.t, L.info, L.ws_ps, S));
+    } else {
+      if (P.q > O.direct_solve_threshold)
+        throw DriverError{SSNAL_E_ARG, "q x q system above direct_solve_threshold (no CG path)"};
+      const double* asa_dev = &L.st_cur->sum_a2_free;
+      ck(launch_dense_gram(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, L.pcount, P.n,
+                           P.a, sigma, asa_dev, L.M, L.m1, L.ws_gram, S));
+      ck(launch_chol_solve(L.M, P.q, L.gr, -1.0, L.t, L.info, S));
+    }
+    xd(L.t, L.qdir, 1);
+    ck(launch_hs_apply(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.ws_red, S));
+    dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}}, L.scal, P.n);
+    dots({{L.t, nullptr}}, L.scal + 3, P.q);
+  }
+
+  void steepest(double out[4]) {
+    vec(4, -1.0, L.grad, nullptr, nullptr, L.dir);
+    xt({L.dir}, L.gr + P.q);
+    xd(L.gr + P.q, L.qdir, 1);
+    dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}, {L.dir, L.qdir}}, L.scal, P.n);
+    fetch(nullptr, 0, false);
+    for (int k = 0; k < 4; ++k) out[k] = H->scal[k];
+  }
+
+  // [gradient, ||grad||^2] + direction + unit trial, one sync
+  void advance(long long p, double asa, bool with_gradient, double& gnorm2, double dotsv[4],
+               ProjState& trial0) {
+    if (with_gradient) {
+      gradient();
+      dots({{L.grad, nullptr}}, L.scal + 4, P.n);
+    }
+    direction(p, asa);
+    const double coef = sigma;
+    project(L.u, L.st_trial, 1, L.qdir, &coef, L.tx, L.tfree, L.x, lam_cur);
+    fetch(L.st_trial, 1, p > 0);
+    if (p > 0 && H->info != 0) throw DriverError{SSNAL_E_ARG, "reduced Newton matrix not SPD"};
+    gnorm2 = H->scal[4];
+    for (int k = 0; k < 4; ++k) dotsv[k] = H->scal[k];
+    if (H->st[0].status != PROJ_APPLIED)
+      finish(L.st_trial, 1, L.u, L.qdir, &coef, L.tx, L.tfree, L.x);
+    trial0 = H->st[0];
+  }
+
+  // Armijo (ref solver.py:292-319); returns false on failure (LineSearchError)
+  bool line_search(double gd, double psi0, double wqw, double wqdir, double dqd, double x_sq,
+                   const ProjState* first, double& alpha_out, int& j_out, ProjState& rec) {
+    if (gd >= 0.0) return false;
+    double alpha = 1.0;
+    int tried = 0;
+    while (tried < 61) {
+      const int T = tried == 0 ? 1
+                                : std::min(std::min(TMAX, std::max(1, O.line_search_batch)),
+                                           61 - tried);
+      double alphas[TMAX], coefs[TMAX];
+      for (int k = 0; k < T; ++k) {
+        alphas[k] = alpha;
+        coefs[k] = sigma * alpha;
+        alpha *= O.backtrack;
+      }
+      if (tried == 0 && first) {
+        H->st[0] = *first;
+      } else {
+        project(L.u, L.st_trial, T, L.qdir, coefs, L.tx, L.tfree, L.x, lam_cur);
+        fetch(L.st_trial, T, false);
+        finish(L.st_trial, T, L.u, L.qdir, coefs, L.tx, L.tfree, L.x);
+      }
+      for (int k = 0; k < T; ++k) {
+        const double a = alphas[k];
+        const double quad = wqw + 2.0 * a * wqdir + a * a * dqd;
+        const double pt = psi(quad, H->st[k], x_sq);
+        if (pt <= psi0 + O.mu * a * gd) {
+          lam_cur = H->st[k].lam;
+          alpha_out = a;
+          j_out = k;
+          rec = H->st[k];
+          return true;
+        }
+      }
+      tried += T;
+    }
+    return false;
+  }
+
+  void accept(double alpha, int j) {
+    vec(2, alpha, L.w, L.dir, nullptr, L.w);
+    vec(2, alpha, L.qw, L.qdir, nullptr, L.qw);
+    vec(2, -(sigma * alpha), L.u, L.qdir, nullptr, L.u);
+    ck(cudaMemcpyAsync(L.xp, L.tx + (size_t)j * P.n, sizeof(double) * P.n, cudaMemcpyDeviceToDevice, S));
+    ck(cudaMemcpyAsync(L.fr, L.tfree + (size_t)j * P.n, P.n, cudaMemcpyDeviceToDevice, S));
+    ck(cudaMemcpyAsync(L.st_cur, L.st_trial + j, sizeof(ProjState), cudaMemcpyDeviceToDevice, S));
+  }
+
+  // ---------------------------------------------------------------- ssn_solve
+  // returns inner iterations; sets flags; leaves Pi(u) in L.xp and its record in cur
+  int ssn_solve(double eps_k, double delta_k, bool& converged, bool& hit_max, ProjState& cur) {
+    const double coeff = std::sqrt(O.lambda_min_surrogate / sigma);
+    const double floor_ = 1e-12 * (1.0 + c_norm);
+    // start: u = x - sigma (Qw + c), Pi(u), s, grad
+    vec(0, -sigma, L.x, L.qw, P.c, L.u);
+    project(L.u, L.st_cur, 1, nullptr, nullptr, L.xp, L.fr, L.x, lam_cur);
+    gradient();
+    dots({{L.grad, nullptr}, {L.x, nullptr}}, L.scal, P.n);
+    fetch(L.st_cur, 1, false);
+    double gnorm2 = H->scal[0];
+    const double x_sq = H->scal[1];
+    if (H->st[0].status != PROJ_APPLIED) {
+      finish(L.st_cur, 1, L.u, nullptr, nullptr, L.xp, L.fr, L.x);
+      gradient();
+      dots({{L.grad, nullptr}, {L.x, nullptr}}, L.scal, P.n);
+      fetch(nullptr, 0, false);
+      gnorm2 = H->scal[0];
+    }
+    cur = H->st[0];
+    lam_cur = cur.lam;
+    double dv[4];
+    ProjState trial0;
+    double unused;
+    advance(cur.nfree, cur.sum_a2_free, false, unused, dv, trial0);
+    converged = false;
+    bool exhausted = true;
+    int its = 0;
+    for (int it = 0; it < O.max_inner; ++it) {
+      const double gnorm = std::sqrt(gnorm2);
+      const double dist = std::sqrt(cur.sum_dref2);
+      if (gnorm <= coeff * eps_k && gnorm <= coeff * delta_k * dist) {
+        converged = true;
+        exhausted = false;
+        break;
+      }
+      if (gnorm <= floor_) {
+        converged = true;
+        exhausted = false;
+        break;
+      }
+      double gd = dv[0], wqw = dv[1], wqdir = dv[2], dqd = dv[3];
+      ++newton;
+      bool steepest_dir = false;
+      const ProjState* first = &trial0;
+      if (gd >= 0.0) {
+        double sv[4];
+        steepest(sv);
+        gd = sv[0]; wqw = sv[1]; wqdir = sv[2]; dqd = sv[3];
+        steepest_dir = true;
+        first = nullptr;
+      }
+      const double psi0 = psi(wqw, cur, x_sq);
+      if (O.mu * std::fabs(gd) <= 1e-16 * (1.0 + std::fabs(psi0))) {
+        converged = true;
+        exhausted = false;
+        break;
+      }
+      double alpha;
+      int j;
+      ProjState rec;
+      if (!line_search(gd, psi0, wqw, wqdir, dqd, x_sq, first, alpha, j, rec)) {
+        if (steepest_dir) {
+          exhausted = false;
+          break;
+        }
+        double sv[4];
+        steepest(sv);
+        gd = sv[0]; wqw = sv[1]; wqdir = sv[2]; dqd = sv[3];
+        if (O.mu * (-gd) <= 1e-16 * (1.0 + std::fabs(psi0))) {
+          exhausted = false;
+          break;
+        }
+        if (!line_search(gd, psi0, wqw, wqdir, dqd, x_sq, nullptr, alpha, j, rec)) {
+          exhausted = false;
+          break;
+        }
+      }
+      accept(alpha, j);
+      cur = rec;
+      ++its;
+      advance(cur.nfree, cur.sum_a2_free, true, gnorm2, dv, trial0);
+    }
+    hit_max = exhausted;
+    return its;
+  }
+
+  // ---------------------------------------------------------------- alm_solve
+  void alm_solve(const double* x0, const double* w0, double* x_out, ssnal_report_t* rep,
+                 ssnal_progress_fn cb, void* ctx) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const size_t nb = sizeof(double) * P.n;
+    if (x0) ck(cudaMemcpyAsync(L.x, x0, nb, cudaMemcpyDeviceToDevice, S));
+    else ck(cudaMemsetAsync(L.x, 0, nb, S));
+    if (w0) ck(cudaMemcpyAsync(L.w, w0, nb, cudaMemcpyDeviceToDevice, S));
+    else ck(cudaMemsetAsync(L.w, 0, nb, S));
+    ck(cudaMemsetAsync(L.qw, 0, nb, S));
+    dots({{P.c, nullptr}}, L.scal, P.n);
+    fetch(nullptr, 0, false);
+    c_norm = std::sqrt(H->scal[0]);
+    sigma = O.sigma0;
+    lam_kkt = lam_cur = 0.0;
+    int outer = 0, inner_total = 0, inner_last = 0, stalled = 0;
+    long long p_last = -1;
+    bool converged = false, stagnated = false, max_outer = false;
+    int hit_mask = 0;
+    double res = INFINITY, obj_last = 0.0;
+    double best_res = INFINITY, best_obj = 0.0;
+    long long best_p = 0;
+    bool have_best = false;
+    for (int k = 0; k <= O.max_outer; ++k) {
+      long long p_kkt;
+      res = kkt_and_refresh(L.x, L.w, L.qw, p_kkt, obj_last);
+      if (p_last < 0) p_last = p_kkt;
+      if (cb) cb(k, res, sigma, p_last, inner_last, ctx);
+      if (!have_best || res < best_res) {
+        have_best = true;
+        best_res = res;
+        best_obj = obj_last;
+        best_p = p_last;
+        ck(cudaMemcpyAsync(L.best_x, L.x, nb, cudaMemcpyDeviceToDevice, S));
+        stalled = 0;
+      } else if (sigma >= O.sigma_max) {
+        if (++stalled >= 3) {
+          stagnated = true;
+          break;
+        }
+      }
+      if (res < O.tol_kkt) {
+        converged = true;
+        break;
+      }
+      if (k == O.max_outer) {
+        max_outer = true;
+        break;
+      }
+      bool conv_in, hit;
+      ProjState cur;
+      const double e = std::pow(0.5, k);
+      inner_last = ssn_solve(e, e, conv_in, hit, cur);
+      if (hit && k < 31) hit_mask |= 1 << k;
+      inner_total += inner_last;
+      ck(cudaMemcpyAsync(L.x, L.xp, nb, cudaMemcpyDeviceToDevice, S));
+      p_last = cur.nfree;
+      sigma = std::min(sigma * O.sigma_growth, O.sigma_max);
+      ++outer;
+    }
+    const bool use_best = have_best && best_res < res;
+    ck(cudaMemcpyAsync(x_out, use_best ? L.best_x : L.x, nb, cudaMemcpyDeviceToDevice, S));
+    ck(cudaStreamSynchronize(S));
+    rep->kkt_residual = use_best ? best_res : res;
+    rep->objective = use_best ? best_obj : obj_last;
+    rep->unbounded_support_count = (int)(use_best ? best_p : p_last);
+    rep->outer_iters = outer;
+    rep->total_inner_iters = inner_total;
+    rep->converged = converged ? 1 : 0;
+    rep->hit_max_inner_mask = hit_mask;
+    rep->stagnated = stagnated ? 1 : 0;
+    rep->max_outer_reached = max_outer ? 1 : 0;
+    rep->syncs = syncs;
+    rep->newton_steps = newton;
+    rep->projections = projections;
+    rep->wall_time =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+
+}  // namespace
+
+size_t alm_ws_bytes(long long n_phys, long long q, int svr) {
+  size_t total = 0;
+  const long long n = svr ? 2 * n_phys : n_phys;
+  carve(nullptr, n, n_phys, q, &total);
+  return total;
+}
+
+int alm_solve_dense(const ssnal_dense_problem_t* pb, const ssnal_options_t* opt, const double* x0,
+                    const double* w0, double* x_out, ssnal_report_t* rep, void* ws,
+                    size_t ws_bytes, ssnal_progress_fn cb, void* ctx, cudaStream_t stream,
+                    const char** err) {
+  size_t need = 0;
+  Layout L = carve((char*)ws, pb->n, pb->n_phys, pb->q, &need);
+  if (ws_bytes < need) {
+    *err = "workspace smaller than ssnal_alm_ws_bytes()";
+    return SSNAL_E_ARG;
+  }
+  Pinned* H = pinned_buffer();
+  if (!H) {
+    *err = "cudaHostAlloc of the pinned scalar buffer failed";
+    return SSNAL_E_DEVICE;
+  }
+  std::memset(rep, 0, sizeof(*rep));
+  Driver d(*pb, *opt, stream, L, H);
+  try {
+    d.alm_solve(x0, w0, x_out, rep, cb, ctx);
+  } catch (const DriverError& e) {
+    *err = e.what;
+    return e.code;
+  }
+  return SSNAL_OK;
+}
+
+}  // namespace ssnal

@@ -71,6 +71,7 @@ class SsnOptions:
     cg_max_iters: int = 500
     line_search_batch: int = 4
     psi_eval: str = "stable"  # or "reference": ref solver.py:130-133 term for term
+    engine: str = "native"    # "native": C++ driver (ssnal_alm_solve_dense); "python": _Engine
 
 
 @dataclass
@@ -494,12 +495,83 @@ def kkt_residual(x, problem):
     return problem.engine().kkt_and_refresh(x, None)[0]
 
 
+def _native_ok(problem, alm_opts, ssn_opts):
+    from .operators import LinearKernelOperator
+
+    return (ssn_opts.engine == "native" and getattr(problem.backend, "name", "") == "cuda"
+            and isinstance(problem.q_op, LinearKernelOperator)
+            and alm_opts.eps_seq is _half_powers and alm_opts.delta_seq is _half_powers)
+
+
+def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_device):
+    """The same loop through the C++ driver (csrc/driver.cu): one C-ABI call."""
+    import ctypes
+
+    be, op, box = problem.backend, problem.q_op, problem.constraint
+    n = problem.n
+    lib = _lib.load()
+    nbytes = lib.ssnal_alm_ws_bytes(op.n_phys, op.q, int(op.svr_block))
+    ws = getattr(problem, "_native_ws", None)
+    if ws is None or ws.numel() < nbytes:
+        ws = be.zeros(int(nbytes), torch.uint8)
+        problem._native_ws = ws
+    ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+    prob = _lib.DenseProblem(
+        A=ptr(op.A), n_phys=op.n_phys, q=op.q, lda=op.lda, row_sign=ptr(op.row_sign),
+        svr_block=int(op.svr_block), n=n, c=ptr(problem.c), a=ptr(box.a_dev),
+        l=ptr(box.l_dev), u=ptr(box.u_dev), l_const=box.l_const, u_const=box.u_const, d=box.d)
+    opts = _lib.Options(
+        sigma0=alm_opts.sigma0, sigma_growth=alm_opts.sigma_growth, sigma_max=alm_opts.sigma_max,
+        tol_kkt=alm_opts.tol_kkt, lambda_min_surrogate=alm_opts.lambda_min_surrogate,
+        max_outer=alm_opts.max_outer, mu=ssn_opts.mu, backtrack=ssn_opts.backtrack,
+        tau=ssn_opts.tau, eta=ssn_opts.eta, max_inner=ssn_opts.max_inner,
+        direct_solve_threshold=ssn_opts.direct_solve_threshold,
+        cg_max_iters=ssn_opts.cg_max_iters, line_search_batch=ssn_opts.line_search_batch,
+        psi_stable=int(ssn_opts.psi_eval != "reference"))
+    x0d = None if x0 is None else as_device(x0, be)
+    w0d = None if w0 is None else as_device(w0, be)
+    if x0d is not None:
+        check_vector(x0d, n, "x0")
+    if w0d is not None:
+        check_vector(w0d, n, "w0")
+    x_out = be.empty(n)
+    rep = _lib.Report()
+    if callback is not None:
+        cb = _lib.PROGRESS_FN(lambda k, r, s, p, inner, ctx: callback(k, r, s, int(p), inner))
+    else:
+        cb = _lib.PROGRESS_FN()
+    _lib.call("ssnal_alm_solve_dense", ctypes.byref(prob), ctypes.byref(opts), ptr(x0d), ptr(w0d),
+              ptr(x_out), ctypes.byref(rep), ptr(ws), ws.numel(), cb, None, be.stream())
+    notes = [f"inner solver hit max_inner at outer iteration {k}" for k in range(31)
+             if rep.hit_max_inner_mask >> k & 1]
+    if rep.stagnated:
+        notes.append("stagnated at the attainable accuracy for sigma_max; returning the best "
+                     "iterate")
+    if rep.max_outer_reached:
+        notes.append(f"max_outer={alm_opts.max_outer} reached")
+    problem.native_counters = {"syncs": rep.syncs, "newton": rep.newton_steps,
+                               "projections": rep.projections}
+    return SolveReport(
+        x_opt=x_out if return_device else x_out.cpu().numpy(),
+        kkt_residual=rep.kkt_residual, outer_iters=rep.outer_iters,
+        avg_inner_iters=rep.total_inner_iters / max(rep.outer_iters, 1),
+        total_inner_iters=rep.total_inner_iters,
+        unbounded_support_count=rep.unbounded_support_count, objective=rep.objective,
+        wall_time=rep.wall_time, converged=bool(rep.converged), solver="ssnal", warnings=notes)
+
+
 def alm_solve(problem, alm_opts=None, ssn_opts=None, x0=None, w0=None, callback=None,
               return_device=False):
     """SSsNAL (ref solver.py:429-530).  Inputs may be host arrays; ``x_opt`` is
-    returned as a numpy array (device tensor with ``return_device=True``)."""
+    returned as a numpy array (device tensor with ``return_device=True``).
+
+    Runs in the native C++ driver (one C-ABI call, csrc/driver.cu) when possible,
+    else in the Python mirror below (same control flow; used for custom tolerance
+    sequences, the test backends and the sharded path)."""
     alm_opts = alm_opts or AlmOptions()
     ssn_opts = ssn_opts or SsnOptions()
+    if _native_ok(problem, alm_opts, ssn_opts):
+        return _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_device)
     t_start = time.perf_counter()
     eng = problem.engine()
     eng._direct_limit = ssn_opts.direct_solve_threshold

@@ -32,11 +32,12 @@ def _problem(P, c):
     return P.build_svr_dual(c["A"], c["t"], c["C"], c["eps"])
 
 
+@pytest.mark.parametrize("engine", ["native", "python"])
 @pytest.mark.parametrize("psi_eval", ["reference", "stable"])
-def test_alm_solve_golden(pkg, psi_eval):
+def test_alm_solve_golden(pkg, psi_eval, engine):
     for c in load_cases("solve.npz", "s"):
         rep = pkg.alm_solve(_problem(pkg, c), pkg.AlmOptions(tol_kkt=c["tol"]),
-                            pkg.SsnOptions(psi_eval=psi_eval))
+                            pkg.SsnOptions(psi_eval=psi_eval, engine=engine))
         assert rep.converged or not c["converged"]
         if rep.converged:
             assert rep.kkt_residual < c["tol"]
@@ -64,6 +65,27 @@ def test_config1_full_size_vs_oracle(pkg):
     assert rep.converged and rep.kkt_residual <= 1e-6 and ref["converged"]
     assert rep.objective == pytest.approx(ref["objective"], rel=1e-6)
     assert (rep.outer_iters, rep.total_inner_iters) == (ref["outer_iters"], ref["total_inner_iters"])
+
+
+def test_native_driver_matches_python_engine(pkg):
+    """The C++ driver and the Python mirror run the same kernels in the same order:
+    identical iterates (bit for bit) on every golden SVM case, callbacks included."""
+    for c in load_cases("solve.npz", "s"):
+        if c["kind"] == "dense":
+            continue
+        rows = {}
+        reps = {}
+        for engine in ("native", "python"):
+            rows[engine] = []
+            reps[engine] = pkg.alm_solve(
+                _problem(pkg, c), pkg.AlmOptions(tol_kkt=c["tol"]), pkg.SsnOptions(engine=engine),
+                callback=lambda *a, e=engine: rows[e].append(a))
+        a, b = reps["native"], reps["python"]
+        assert (a.outer_iters, a.total_inner_iters, a.converged) == (
+            b.outer_iters, b.total_inner_iters, b.converged)
+        assert a.kkt_residual == b.kkt_residual and a.objective == b.objective
+        np.testing.assert_array_equal(a.x_opt, b.x_opt)
+        assert rows["native"] == rows["python"]
 
 
 def test_kkt_residual_golden(pkg):
