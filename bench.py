@@ -195,7 +195,8 @@ def run_ours(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)
     sampler.start()
     launches0 = be.launch_count()
-    be.start_timing()
+    prof_opts = P.SsnOptions(profile=True)  # CUDA events per op class, on the solver stream
+    kern = {}
     step_s = []
     reps = []
     for _ in range(args.steps):
@@ -203,12 +204,14 @@ def run_ours(args, rank, world, local_rank):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        rep = P.alm_solve(problem, opts, return_device=True)
+        rep = P.alm_solve(problem, opts, prof_opts, return_device=True)
         e1.record(stream)
         e1.synchronize()
         step_s.append(e0.elapsed_time(e1) * 1e-3)
         reps.append(rep)
-    kern = be.stop_timing()
+        for name, v in getattr(problem, "op_profile", {}).items():
+            c, s, b = kern.get(name, (0, 0.0, 0.0))
+            kern[name] = (c + v["calls"], s + v["seconds"], b + v["bytes"])
     launches = be.launch_count() - launches0
     clocks = sampler.stop()
     barrier()
@@ -246,22 +249,19 @@ def run_ours(args, rank, world, local_rank):
             dist.destroy_process_group()
         return
     peak, peak_kind = _peaks()
-    # dominant kernel by device time; roofline for the HBM-streaming operator products
-    dom = max(kern.items(), key=lambda kv: kv[1][1]) if kern else None
+    # dominant op class by device time; roofline = its algorithmic bytes / its time
     roof = None
     if kern:
-        name, (cnt, secs, nbytes) = dom
-        stream_ops = {k: v for k, v in kern.items() if k in ("dense_xt", "dense_x")}
-        per_launch_bytes = nbytes / max(cnt, 1)
+        name, (cnt, secs, nbytes) = max(kern.items(), key=lambda kv: kv[1][1])
         achieved = (nbytes / secs) / 1e9 if secs > 0 and nbytes > 0 else 0.0
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak if peak else None, "traffic": None,
                 "peak_kind": peak_kind, "launches": cnt, "mean_launch_us": secs / cnt * 1e6,
-                "algorithmic_bytes_per_launch": per_launch_bytes,
+                "algorithmic_bytes_per_launch": nbytes / max(cnt, 1),
                 "share_of_step": secs / total if total else None,
-                "streams": {k: {"launches": v[0], "s": v[1], "GBps": v[2] / v[1] / 1e9 if v[1] else None}
-                            for k, v in stream_ops.items()},
-                "all_ops_s": {k: v[1] for k, v in kern.items()}}
+                "ops": {k: {"calls": v[0], "s": v[1], "share": v[1] / total if total else None,
+                            "GBps": v[2] / v[1] / 1e9 if v[1] else None}
+                        for k, v in kern.items()}}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         secs, ref = cpu_oracle_solve(cfg)
@@ -287,7 +287,7 @@ def run_ours(args, rank, world, local_rank):
         "result": {"kkt": last.kkt_residual, "objective": last.objective,
                    "outer": last.outer_iters, "inner": last.total_inner_iters,
                    "p": last.unbounded_support_count, "converged": last.converged},
-        "counters": problem.engine().counters,
+        "counters": getattr(problem, "native_counters", None),
     }
     print(json.dumps(line), flush=True)
     if dist is not None:

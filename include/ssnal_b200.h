@@ -185,7 +185,16 @@ typedef struct ssnal_options_t {
   double mu, backtrack, tau, eta;                                         /* SsnOptions */
   int max_inner, direct_solve_threshold, cg_max_iters, line_search_batch;
   int psi_stable;           /* 1: psi via sum Pi(u)(2u - Pi(u)); 0: reference formula */
+  int profile;              /* 1: CUDA-event timing per op class into the report      */
 } ssnal_options_t;
+
+/* op classes of ssnal_report_t.op_seconds / op_calls */
+#define SSNAL_OP_XT 0       /* X^T V products (streams A)                             */
+#define SSNAL_OP_XD 1       /* X D products (streams A)                               */
+#define SSNAL_OP_PROJ 2     /* projections (Newton/K-ary passes + apply)              */
+#define SSNAL_OP_NEWTON 3   /* reduced Newton system: compaction, Gram, Cholesky      */
+#define SSNAL_OP_VEC 4      /* elementwise ops, fused dots, HS-Jacobian               */
+#define SSNAL_NOPS 5
 
 typedef struct ssnal_report_t {
   double kkt_residual, objective, wall_time;
@@ -193,6 +202,9 @@ typedef struct ssnal_report_t {
   int hit_max_inner_mask;   /* bit k: inner solver hit max_inner at outer k (k < 31)   */
   int stagnated, max_outer_reached;
   long long syncs, newton_steps, projections, launches;
+  double op_seconds[SSNAL_NOPS];   /* device time per op class (profile = 1)         */
+  long long op_calls[SSNAL_NOPS];
+  double op_bytes[SSNAL_NOPS];     /* algorithmic HBM bytes per op class             */
 } ssnal_report_t;
 
 /* per outer iteration: (k, R_KKT, sigma, p, inner iterations) as ref solver.py:474-475 */

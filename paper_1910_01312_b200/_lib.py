@@ -74,7 +74,12 @@ class Options(ctypes.Structure):
     _fields_ = [("sigma0", _D), ("sigma_growth", _D), ("sigma_max", _D), ("tol_kkt", _D),
                 ("lambda_min_surrogate", _D), ("max_outer", _I), ("mu", _D), ("backtrack", _D),
                 ("tau", _D), ("eta", _D), ("max_inner", _I), ("direct_solve_threshold", _I),
-                ("cg_max_iters", _I), ("line_search_batch", _I), ("psi_stable", _I)]
+                ("cg_max_iters", _I), ("line_search_batch", _I), ("psi_stable", _I),
+                ("profile", _I)]
+
+
+NOPS = 5
+OP_NAMES = ("dense_xt", "dense_x", "project", "newton_system", "vector")
 
 
 class Report(ctypes.Structure):
@@ -84,7 +89,9 @@ class Report(ctypes.Structure):
                 ("unbounded_support_count", _I), ("converged", _I),
                 ("hit_max_inner_mask", _I), ("stagnated", _I), ("max_outer_reached", _I),
                 ("syncs", ctypes.c_longlong), ("newton_steps", ctypes.c_longlong),
-                ("projections", ctypes.c_longlong), ("launches", ctypes.c_longlong)]
+                ("projections", ctypes.c_longlong), ("launches", ctypes.c_longlong),
+                ("op_seconds", _D * NOPS), ("op_calls", ctypes.c_longlong * NOPS),
+                ("op_bytes", _D * NOPS)]
 
 
 PROGRESS_FN = ctypes.CFUNCTYPE(None, _I, _D, _D, ctypes.c_longlong, _I, _P)

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "ssnal_internal.h"
@@ -143,6 +144,29 @@ void ck(cudaError_t e) {
   if (e != cudaSuccess) throw DriverError{(int)e, cudaGetErrorString(e)};
 }
 
+// CUDA-event timing per op class (ssnal_options_t.profile); events are pooled
+struct Prof {
+  struct Rec {
+    int op;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Rec> recs;
+  size_t used = 0;
+  static std::vector<cudaEvent_t>& pool() {
+    static thread_local std::vector<cudaEvent_t> p;
+    return p;
+  }
+  cudaEvent_t get() {
+    auto& p = pool();
+    if (used == p.size()) {
+      cudaEvent_t e;
+      ck(cudaEventCreate(&e));
+      p.push_back(e);
+    }
+    return p[used++];
+  }
+};
+
 struct Driver {
   const ssnal_dense_problem_t& P;
   const ssnal_options_t& O;
@@ -153,10 +177,32 @@ struct Driver {
   double lam_kkt = 0.0, lam_cur = 0.0;
   double sigma = 1.0;
   double c_norm = 0.0;
+  Prof prof;
+  double op_bytes[SSNAL_NOPS] = {0, 0, 0, 0, 0};
+  long long op_calls[SSNAL_NOPS] = {0, 0, 0, 0, 0};
 
   Driver(const ssnal_dense_problem_t& p, const ssnal_options_t& o, cudaStream_t s, Layout l,
          Pinned* h)
       : P(p), O(o), S(s), L(l), H(h) {}
+
+  template <class F>
+  void timed(int op, double bytes, F&& f) {
+    op_bytes[op] += bytes;
+    ++op_calls[op];
+    if (!O.profile) {
+      f();
+      return;
+    }
+    cudaEvent_t e0 = prof.get(), e1 = prof.get();
+    ck(cudaEventRecord(e0, S));
+    f();
+    ck(cudaEventRecord(e1, S));
+    prof.recs.push_back({op, e0, e1});
+  }
+
+  double a_bytes() const {
+    return 8.0 * P.n_phys * P.q + (P.row_sign ? 8.0 * P.n_phys : 0.0);
+  }
 
   // ---------------------------------------------------------------- plumbing
   void fetch(const ProjState* states, int T, bool info) {
@@ -175,7 +221,12 @@ struct Driver {
     pl.lc = P.l_const; pl.uc = P.u_const; pl.d = P.d; pl.n = P.n; pl.T = T;
     pl.st = st; pl.part = (double*)L.ws_proj; pl.x_out = xo; pl.free_out = fo; pl.ref = ref;
     pl.phases = phases; pl.passes = passes; pl.hint = hint; pl.newton = newton_passes;
-    ck(launch_project(pl, S));
+    // algorithmic bytes: each streaming launch reads v (+B), a (+l, u vectors); apply
+    // also writes x and the mask
+    const double per = 8.0 * P.n * (2 + (B != nullptr) + (P.l != nullptr) + (P.u != nullptr));
+    const double bytes = T * (per * (newton_passes + passes + 1) +
+                              (xo ? 8.0 * P.n : 0.0) + (fo ? 1.0 * P.n : 0.0));
+    timed(SSNAL_OP_PROJ, bytes, [&] { ck(launch_project(pl, S)); });
     ++projections;
   }
 
@@ -212,22 +263,30 @@ struct Driver {
       ys[k] = pr.second;
       ++k;
     }
-    ck(launch_dots(k, xs, ys, nullptr, len, out, L.ws_red, S));
+    timed(SSNAL_OP_VEC, 8.0 * len * 2 * k,
+          [&] { ck(launch_dots(k, xs, ys, nullptr, len, out, L.ws_red, S)); });
   }
 
   void vec(int op, double alpha, const double* x, const double* y, const double* z, double* out) {
-    ck(launch_vec(op, P.n, alpha, x, y, z, out, S));
+    const int nin = 1 + (y != nullptr) + (z != nullptr);
+    timed(SSNAL_OP_VEC, 8.0 * P.n * (nin + 1),
+          [&] { ck(launch_vec(op, P.n, alpha, x, y, z, out, S)); });
   }
 
   void xt(std::initializer_list<const double*> vs, double* out) {
     const double* arr[4];
     int k = 0;
     for (auto v : vs) arr[k++] = v;
-    ck(launch_dense_xt(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, k, arr, out, L.ws_xt, S));
+    timed(SSNAL_OP_XT, a_bytes() + 8.0 * k * (P.n + P.q), [&] {
+      ck(launch_dense_xt(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, k, arr, out,
+                         L.ws_xt, S));
+    });
   }
 
   void xd(const double* d, double* out, int k) {
-    ck(launch_dense_x(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, k, d, out, S));
+    timed(SSNAL_OP_XD, a_bytes() + 8.0 * k * (P.n + P.q), [&] {
+      ck(launch_dense_x(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, k, d, out, S));
+    });
   }
 
   double psi(double wqw, const ProjState& r, double x_sq) const {
@@ -273,22 +332,28 @@ struct Driver {
       dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}, {L.s, L.grad}}, L.scal, P.n);
       return;
     }
-    ck(launch_compact(L.fr, P.n, L.J, L.pcount, L.ws_cmp, S));
-    if (p < P.q) {
-      if (p > O.direct_solve_threshold)
-        throw DriverError{SSNAL_E_ARG, "p x p system above direct_solve_threshold (no CG path)"};
-      ck(launch_pspace_direction(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, p,
-                                 L.grad, P.a, sigma, asa, L.gr, L.t, L.info, L.ws_ps, S));
-    } else {
-      if (P.q > O.direct_solve_threshold)
-        throw DriverError{SSNAL_E_ARG, "q x q system above direct_solve_threshold (no CG path)"};
-      const double* asa_dev = &L.st_cur->sum_a2_free;
-      ck(launch_dense_gram(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, L.pcount, P.n,
-                           P.a, sigma, asa_dev, L.M, L.m1, L.ws_gram, S));
-      ck(launch_chol_solve(L.M, P.q, L.gr, -1.0, L.t, L.info, S));
-    }
+    if (p < P.q && p > O.direct_solve_threshold)
+      throw DriverError{SSNAL_E_ARG, "p x p system above direct_solve_threshold (no CG path)"};
+    if (p >= P.q && P.q > O.direct_solve_threshold)
+      throw DriverError{SSNAL_E_ARG, "q x q system above direct_solve_threshold (no CG path)"};
+    // gathered rows of A (p x q) once + the system matrix written and factored
+    const double m = (double)std::min<long long>(p, P.q);
+    timed(SSNAL_OP_NEWTON, 8.0 * p * P.q + 16.0 * m * m, [&] {
+      ck(launch_compact(L.fr, P.n, L.J, L.pcount, L.ws_cmp, S));
+      if (p < P.q) {
+        ck(launch_pspace_direction(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, p,
+                                   L.grad, P.a, sigma, asa, L.gr, L.t, L.info, L.ws_ps, S));
+      } else {
+        const double* asa_dev = &L.st_cur->sum_a2_free;
+        ck(launch_dense_gram(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, L.pcount,
+                             P.n, P.a, sigma, asa_dev, L.M, L.m1, L.ws_gram, S));
+        ck(launch_chol_solve(L.M, P.q, L.gr, -1.0, L.t, L.info, S));
+      }
+    });
     xd(L.t, L.qdir, 1);
-    ck(launch_hs_apply(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.ws_red, S));
+    timed(SSNAL_OP_VEC, 8.0 * P.n * 5, [&] {
+      ck(launch_hs_apply(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.ws_red, S));
+    });
     dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}}, L.scal, P.n);
     dots({{L.t, nullptr}}, L.scal + 3, P.q);
   }
@@ -533,6 +598,16 @@ struct Driver {
     rep->syncs = syncs;
     rep->newton_steps = newton;
     rep->projections = projections;
+    for (int k = 0; k < SSNAL_NOPS; ++k) {
+      rep->op_calls[k] = op_calls[k];
+      rep->op_bytes[k] = op_bytes[k];
+      rep->op_seconds[k] = 0.0;
+    }
+    for (auto& r : prof.recs) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, r.e0, r.e1));
+      rep->op_seconds[r.op] += 1e-3 * ms;
+    }
     rep->wall_time =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }

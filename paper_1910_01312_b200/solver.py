@@ -72,6 +72,7 @@ class SsnOptions:
     line_search_batch: int = 4
     psi_eval: str = "stable"  # or "reference": ref solver.py:130-133 term for term
     engine: str = "native"    # "native": C++ driver (ssnal_alm_solve_dense); "python": _Engine
+    profile: bool = False     # native: CUDA-event time per op class -> problem.op_profile
 
 
 @dataclass
@@ -527,7 +528,7 @@ def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_devi
         tau=ssn_opts.tau, eta=ssn_opts.eta, max_inner=ssn_opts.max_inner,
         direct_solve_threshold=ssn_opts.direct_solve_threshold,
         cg_max_iters=ssn_opts.cg_max_iters, line_search_batch=ssn_opts.line_search_batch,
-        psi_stable=int(ssn_opts.psi_eval != "reference"))
+        psi_stable=int(ssn_opts.psi_eval != "reference"), profile=int(bool(ssn_opts.profile)))
     x0d = None if x0 is None else as_device(x0, be)
     w0d = None if w0 is None else as_device(w0, be)
     if x0d is not None:
@@ -551,6 +552,9 @@ def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_devi
         notes.append(f"max_outer={alm_opts.max_outer} reached")
     problem.native_counters = {"syncs": rep.syncs, "newton": rep.newton_steps,
                                "projections": rep.projections}
+    problem.op_profile = {name: {"calls": int(rep.op_calls[k]), "seconds": float(rep.op_seconds[k]),
+                                 "bytes": float(rep.op_bytes[k])}
+                          for k, name in enumerate(_lib.OP_NAMES)}
     return SolveReport(
         x_opt=x_out if return_device else x_out.cpu().numpy(),
         kkt_residual=rep.kkt_residual, outer_iters=rep.outer_iters,
