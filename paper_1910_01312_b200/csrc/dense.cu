@@ -158,8 +158,18 @@ static int xt_splits(long long n) {
   return (int)s;
 }
 
+bool stream_ok(const double* A, long long lda, long long q);
+int stream_grid(long long n);
+cudaError_t launch_stream_xt(const double* A, long long n, long long q, long long lda,
+                             const double* rs, int svr, int k, const double* const* vs, int kofs,
+                             int ktot, double* part, cudaStream_t stream);
+cudaError_t launch_stream_xd(const double* A, long long n, long long q, long long lda,
+                             const double* rs, int svr, int k, const double* d, double* out,
+                             long long nlog, cudaStream_t stream);
+
 size_t dense_xt_ws_bytes(long long n_phys, long long q, int k) {
-  return (size_t)xt_splits(n_phys) * k * q * sizeof(double);
+  const long long splits = max((long long)xt_splits(n_phys), (long long)stream_grid(n_phys));
+  return (size_t)splits * k * q * sizeof(double);
 }
 
 static bool vec2_ok(const double* A, long long lda, long long q) {
@@ -175,6 +185,18 @@ cudaError_t launch_dense_xt(const double* A, long long n, long long q, long long
   p.part = (double*)ws;
   p.out = out;
   int nsplit = xt_splits(n);
+  if (stream_ok(A, lda, q)) {  // TMA-staged streaming (csrc/stream.cu)
+    const int grid = stream_grid(n);
+    for (int j = 0; j < k;) {
+      const int kk = (k - j >= 2) ? 2 : 1;
+      cudaError_t e = launch_stream_xt(A, n, q, lda, rs, svr, kk, vs, j, k, p.part, stream);
+      if (e != cudaSuccess) return e;
+      j += kk;
+    }
+    long long tot = (long long)k * q;
+    { note_launch(); dense_xt_fold_kernel<<<(unsigned)ceil_div(tot * 32, 256), 256, 0, stream>>>(p.part, grid, k, q, out); }
+    return cudaGetLastError();
+  }
   if (vec2_ok(A, lda, q)) {
     long long pairs = q / 2;
     int threads = (int)min(512LL, ceil_div(pairs, 32) * 32);
@@ -358,6 +380,16 @@ cudaError_t launch_dense_x(const double* A, long long n, long long q, long long 
                            const double* rs, int svr, int k, const double* d, double* out,
                            cudaStream_t stream) {
   long long nlog = svr ? 2 * n : n;
+  if (stream_ok(A, lda, q) && q <= 512) {  // TMA-staged streaming (csrc/stream.cu)
+    for (int j = 0; j < k;) {
+      const int kk = (k - j >= 2) ? 2 : 1;
+      cudaError_t e = launch_stream_xd(A, n, q, lda, rs, svr, kk, d + (long long)j * q,
+                                       out + (long long)j * nlog, nlog, stream);
+      if (e != cudaSuccess) return e;
+      j += kk;
+    }
+    return cudaGetLastError();
+  }
   if (vec2_ok(A, lda, q) && q <= 512) {
     for (int j = 0; j < k;) {
       if (k - j >= 2) {

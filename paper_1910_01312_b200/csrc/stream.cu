@@ -1,0 +1,328 @@
+// TMA-staged streaming of the sample matrix A for the two data-operator products.
+//
+// Every product of the SSsNAL step that touches A (X^T v for the gradient and the
+// KKT map, X d for Q-images) reads A exactly once, so it is HBM bound.  One CTA
+// per SM owns a contiguous slab of rows; a producer warp streams the slab into a
+// 4-stage shared-memory ring with 1-D bulk copies (cp.async.bulk, TMA engine,
+// mbarrier complete_tx), eight consumer warps compute from shared memory and
+// release stages through "empty" mbarriers.  192 KB in flight per SM keeps HBM
+// saturated without relying on occupancy.
+//   XT : consumers own column pairs, accumulate coef_r * A[r, :] in registers;
+//        per-CTA partials are folded deterministically afterwards.
+//   XD : each consumer warp takes whole rows of a stage, d is held in registers,
+//        shuffle-tree dot products.
+#include "common.cuh"
+#include "ssnal_internal.h"
+
+namespace ssnal {
+
+namespace {
+
+constexpr int NSTAGE = 4;
+constexpr int STAGE_BYTES = 48 * 1024;
+constexpr int NCONS = 8;                      // consumer warps
+constexpr int NTHREADS = (NCONS + 1) * 32;    // + one producer warp
+constexpr int ROWS_CTA = 512;                 // rows per CTA slab (coefficients fit in smem)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// try_wait suspends in hardware between probes; the bounded loop turns a protocol
+// bug into a trapped kernel (an error the host sees) instead of a hung GPU
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (long long spin = 0; spin < (1LL << 26); ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+  }
+  __trap();
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct StreamArgs {
+  const double* A;
+  long long n, q, lda;
+  const double* rs;
+  int svr;
+  int rows_per_stage;
+  // XT
+  const double* v[2];
+  int k;
+  double* part;  // [grid][k][q]
+  // XD
+  const double* d;  // [k][q]
+  double* out;      // [k][nlog]
+  long long nlog;
+};
+
+// Producer: stream rows [r0, r1) of A through the ring.  Returns after the last issue.
+__device__ __forceinline__ void produce(const StreamArgs& p, long long r0, long long r1,
+                                       char* ring, uint64_t* full, uint64_t* empty) {
+  const long long rows = r1 - r0;
+  const long long nchunk = ceil_div(rows, (long long)p.rows_per_stage);
+  for (long long c = 0; c < nchunk; ++c) {
+    const int s = (int)(c % NSTAGE);
+    if (c >= NSTAGE) mbar_wait(&empty[s], (uint32_t)(((c / NSTAGE) - 1) & 1));
+    const long long rb = r0 + c * p.rows_per_stage;
+    const long long nr = min((long long)p.rows_per_stage, r1 - rb);
+    const uint32_t bytes = (uint32_t)(nr * p.lda * sizeof(double));
+    mbar_expect_tx(&full[s], bytes);
+    bulk_g2s(ring + (size_t)s * STAGE_BYTES, p.A + rb * p.lda, bytes, &full[s]);
+  }
+}
+
+template <int KV, int CP>
+__global__ void __launch_bounds__(NTHREADS, 1) stream_xt_kernel(StreamArgs p) {
+  extern __shared__ __align__(128) char ring[];
+  __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
+  __shared__ double coef_s[ROWS_CTA][KV];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long rows_per = ceil_div(p.n, (long long)gridDim.x);
+  const long long r0 = blockIdx.x * rows_per, r1 = min(p.n, r0 + rows_per);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NCONS) {
+    if (lane == 0 && r1 > r0) produce(p, r0, r1, ring, full, empty);
+    return;
+  }
+  const int t = threadIdx.x;  // consumer thread 0..255, owns pairs t, t+256, ...
+  // row coefficients (labels x vector entries) of the whole slab, loaded once while the
+  // first stages are in flight
+  for (long long r = t; r < r1 - r0; r += NCONS * 32) {
+    const long long gr = r0 + r;
+    const double sg = p.rs ? p.rs[gr] : 1.0;
+#pragma unroll
+    for (int j = 0; j < KV; ++j) {
+      double cv = p.v[j][gr];
+      if (p.svr) cv = __dsub_rn(cv, p.v[j][gr + p.n]);
+      coef_s[r][j] = sg * cv;
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NCONS * 32) : "memory");
+  const long long pairs = p.q / 2;
+  double ax[KV][CP], ay[KV][CP];
+#pragma unroll
+  for (int j = 0; j < KV; ++j)
+#pragma unroll
+    for (int c = 0; c < CP; ++c) ax[j][c] = ay[j][c] = 0.0;
+  const long long rows = r1 - r0;
+  const long long nchunk = rows > 0 ? ceil_div(rows, (long long)p.rows_per_stage) : 0;
+  for (long long ch = 0; ch < nchunk; ++ch) {
+    const int s = (int)(ch % NSTAGE);
+    const long long rb = r0 + ch * p.rows_per_stage;
+    const int nr = (int)min((long long)p.rows_per_stage, r1 - rb);
+    mbar_wait(&full[s], (uint32_t)((ch / NSTAGE) & 1));
+    const double* st = reinterpret_cast<const double*>(ring + (size_t)s * STAGE_BYTES);
+    const int rl0 = (int)(rb - r0);
+    for (int r = 0; r < nr; ++r) {
+      double cf[KV];
+#pragma unroll
+      for (int j = 0; j < KV; ++j) cf[j] = coef_s[rl0 + r][j];
+      const double2* row = reinterpret_cast<const double2*>(st + (size_t)r * p.lda);
+#pragma unroll
+      for (int c = 0; c < CP; ++c) {
+        const long long pc = t + 256LL * c;
+        if (pc < pairs) {
+          const double2 a = row[pc];
+#pragma unroll
+          for (int j = 0; j < KV; ++j) {
+            ax[j][c] = fma(cf[j], a.x, ax[j][c]);
+            ay[j][c] = fma(cf[j], a.y, ay[j][c]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+#pragma unroll
+  for (int c = 0; c < CP; ++c) {
+    const long long pc = t + 256LL * c;
+    if (pc >= pairs) continue;
+#pragma unroll
+    for (int j = 0; j < KV; ++j) {
+      double* dst = p.part + ((long long)blockIdx.x * p.k + j) * p.q + 2 * pc;
+      dst[0] = ax[j][c];
+      dst[1] = ay[j][c];
+    }
+  }
+}
+
+template <int KV, int CP>
+__global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
+  extern __shared__ __align__(128) char ring[];
+  __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long rows_per = ceil_div(p.n, (long long)gridDim.x);
+  const long long r0 = blockIdx.x * rows_per, r1 = min(p.n, r0 + rows_per);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NCONS) {
+    if (lane == 0 && r1 > r0) produce(p, r0, r1, ring, full, empty);
+    return;
+  }
+  const long long pairs = p.q / 2;
+  // this lane's slice of d: pairs lane, lane+32, ... (CP*... <= 8 per lane for q <= 512)
+  double2 dv[KV][CP * 2];
+#pragma unroll
+  for (int j = 0; j < KV; ++j)
+#pragma unroll
+    for (int c = 0; c < CP * 2; ++c) {
+      const long long pc = lane + 32LL * c;
+      dv[j][c] = pc < pairs ? make_double2(p.d[j * p.q + 2 * pc], p.d[j * p.q + 2 * pc + 1])
+                            : make_double2(0.0, 0.0);
+    }
+  const long long rows = r1 - r0;
+  const long long nchunk = rows > 0 ? ceil_div(rows, (long long)p.rows_per_stage) : 0;
+  for (long long ch = 0; ch < nchunk; ++ch) {
+    const int s = (int)(ch % NSTAGE);
+    const long long rb = r0 + ch * p.rows_per_stage;
+    const int nr = (int)min((long long)p.rows_per_stage, r1 - rb);
+    mbar_wait(&full[s], (uint32_t)((ch / NSTAGE) & 1));
+    const double* st = reinterpret_cast<const double*>(ring + (size_t)s * STAGE_BYTES);
+    for (int r = warp; r < nr; r += NCONS) {
+      const double2* row = reinterpret_cast<const double2*>(st + (size_t)r * p.lda);
+      double acc[KV];
+#pragma unroll
+      for (int j = 0; j < KV; ++j) acc[j] = 0.0;
+#pragma unroll
+      for (int c = 0; c < CP * 2; ++c) {
+        const long long pc = lane + 32LL * c;
+        if (pc < pairs) {
+          const double2 a = row[pc];
+#pragma unroll
+          for (int j = 0; j < KV; ++j) acc[j] = fma(a.y, dv[j][c].y, fma(a.x, dv[j][c].x, acc[j]));
+        }
+      }
+      const long long gr = rb + r;
+#pragma unroll
+      for (int j = 0; j < KV; ++j) {
+        const double sum = warp_sum(acc[j]);
+        if (lane == 0) {
+          const double val = p.rs ? p.rs[gr] * sum : sum;
+          p.out[(long long)j * p.nlog + gr] = val;
+          if (p.svr) p.out[(long long)j * p.nlog + gr + p.n] = -val;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+int rows_per_stage(long long lda) {
+  long long r = STAGE_BYTES / (lda * (long long)sizeof(double));
+  return (int)(r < 1 ? 1 : r);
+}
+
+template <class K>
+cudaError_t launch_stream(K kernel, const StreamArgs& p, int grid, cudaStream_t stream) {
+  const int smem = NSTAGE * STAGE_BYTES;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  note_launch();
+  kernel<<<grid, NTHREADS, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool stream_ok(const double* A, long long lda, long long q) {
+  return (lda % 2 == 0) && (q % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+         lda * (long long)sizeof(double) <= STAGE_BYTES && q <= 2048;
+}
+
+int stream_grid(long long n) {
+  // one slab of <= ROWS_CTA rows per CTA, at least one CTA per SM when n allows
+  long long g = ceil_div(n, (long long)ROWS_CTA);
+  if (g < 148) g = min(148LL, ceil_div(n, 8LL));
+  return (int)(g < 1 ? 1 : g);
+}
+
+// X^T [v0 (, v1)] into part[grid][k][q]; caller folds.  k <= 2.
+cudaError_t launch_stream_xt(const double* A, long long n, long long q, long long lda,
+                             const double* rs, int svr, int k, const double* const* vs, int kofs,
+                             int ktot, double* part, cudaStream_t stream) {
+  StreamArgs p{};
+  p.A = A; p.n = n; p.q = q; p.lda = lda; p.rs = rs; p.svr = svr;
+  p.rows_per_stage = rows_per_stage(lda);
+  p.v[0] = vs[kofs];
+  p.v[1] = k > 1 ? vs[kofs + 1] : nullptr;
+  p.k = ktot;
+  p.part = part + (long long)kofs * q;  // slot kofs of each CTA record (record stride ktot*q)
+  const int grid = stream_grid(n);
+  const long long pairs = q / 2;
+  const int cp = (int)ceil_div(pairs, 256LL);
+  if (k == 2) {
+    if (cp <= 1) return launch_stream(stream_xt_kernel<2, 1>, p, grid, stream);
+    if (cp <= 2) return launch_stream(stream_xt_kernel<2, 2>, p, grid, stream);
+    return launch_stream(stream_xt_kernel<2, 4>, p, grid, stream);
+  }
+  if (cp <= 1) return launch_stream(stream_xt_kernel<1, 1>, p, grid, stream);
+  if (cp <= 2) return launch_stream(stream_xt_kernel<1, 2>, p, grid, stream);
+  return launch_stream(stream_xt_kernel<1, 4>, p, grid, stream);
+}
+
+cudaError_t launch_stream_xd(const double* A, long long n, long long q, long long lda,
+                             const double* rs, int svr, int k, const double* d, double* out,
+                             long long nlog, cudaStream_t stream) {
+  StreamArgs p{};
+  p.A = A; p.n = n; p.q = q; p.lda = lda; p.rs = rs; p.svr = svr;
+  p.rows_per_stage = rows_per_stage(lda);
+  p.d = d;
+  p.out = out;
+  p.nlog = nlog;
+  const int grid = stream_grid(n);
+  const long long pairs = q / 2;
+  const int cp = (int)ceil_div(pairs, 64LL);  // lanes hold 2*CP pairs each
+  if (k == 2) {
+    if (cp <= 1) return launch_stream(stream_xd_kernel<2, 1>, p, grid, stream);
+    if (cp <= 2) return launch_stream(stream_xd_kernel<2, 2>, p, grid, stream);
+    return launch_stream(stream_xd_kernel<2, 4>, p, grid, stream);
+  }
+  if (cp <= 1) return launch_stream(stream_xd_kernel<1, 1>, p, grid, stream);
+  if (cp <= 2) return launch_stream(stream_xd_kernel<1, 2>, p, grid, stream);
+  return launch_stream(stream_xd_kernel<1, 4>, p, grid, stream);
+}
+
+}  // namespace ssnal
