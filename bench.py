@@ -195,8 +195,6 @@ def run_ours(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)
     sampler.start()
     launches0 = be.launch_count()
-    prof_opts = P.SsnOptions(profile=True)  # CUDA events per op class, on the solver stream
-    kern = {}
     step_s = []
     reps = []
     for _ in range(args.steps):
@@ -204,15 +202,30 @@ def run_ours(args, rank, world, local_rank):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        rep = P.alm_solve(problem, opts, prof_opts, return_device=True)
+        rep = P.alm_solve(problem, opts, return_device=True)
         e1.record(stream)
         e1.synchronize()
         step_s.append(e0.elapsed_time(e1) * 1e-3)
         reps.append(rep)
+    launches = (be.launch_count() - launches0) // max(args.steps, 1)
+    # per-op-class device time: the same K solves again with CUDA events around every
+    # op on the solver stream (kept out of the timed region above: event records cost
+    # host time the latency-bound solve would otherwise not pay)
+    kern = {}
+    prof_opts = P.SsnOptions(profile=True)
+    prof_wall = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        P.alm_solve(problem, opts, prof_opts, return_device=True)
+        e1.record(stream)
+        e1.synchronize()
+        prof_wall.append(e0.elapsed_time(e1) * 1e-3)
         for name, v in getattr(problem, "op_profile", {}).items():
             c, s, b = kern.get(name, (0, 0.0, 0.0))
             kern[name] = (c + v["calls"], s + v["seconds"], b + v["bytes"])
-    launches = be.launch_count() - launches0
     clocks = sampler.stop()
     barrier()
     t_local = float(np.sum(step_s))
@@ -251,15 +264,20 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_kind = _peaks()
     # dominant op class by device time; roofline = its algorithmic bytes / its time
     roof = None
+    ptotal = float(np.sum(prof_wall)) if prof_wall else 0.0
     if kern:
-        name, (cnt, secs, nbytes) = max(kern.items(), key=lambda kv: kv[1][1])
+        # the roofline is reported for the streaming operator products (the HBM-bound
+        # kernels the path is built on); every op class's share is listed beside it
+        stream = {k: v for k, v in kern.items() if k in ("dense_xt", "dense_x")}
+        name, (cnt, secs, nbytes) = max(stream.items(), key=lambda kv: kv[1][1])
         achieved = (nbytes / secs) / 1e9 if secs > 0 and nbytes > 0 else 0.0
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak if peak else None, "traffic": None,
                 "peak_kind": peak_kind, "launches": cnt, "mean_launch_us": secs / cnt * 1e6,
                 "algorithmic_bytes_per_launch": nbytes / max(cnt, 1),
-                "share_of_step": secs / total if total else None,
-                "ops": {k: {"calls": v[0], "s": v[1], "share": v[1] / total if total else None,
+                "share_of_step": secs / ptotal if ptotal else None,
+                "measured": "CUDA events on the solver stream, K extra profiled solves",
+                "ops": {k: {"calls": v[0], "s": v[1], "share": v[1] / ptotal if ptotal else None,
                             "GBps": v[2] / v[1] / 1e9 if v[1] else None}
                         for k, v in kern.items()}}
     cpu = None
