@@ -20,8 +20,13 @@
 //   pass   : 31 probe sums + in-bracket breakpoint stats -> narrower bracket (x P)
 //   exact  : direct sums at <= 4 candidate breakpoints -> lambda      (status 2)
 //   apply  : x = clip(v - lambda a), free mask, fused reductions
+#include <algorithm>
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "ssnal_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace ssnal {
 
@@ -459,6 +464,186 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_apply_kernel(ProjArgs p) {
   st->status = PROJ_APPLIED;
 }
 
+// ------------------------------------------------------------------ fused
+// The whole default search (warm-started Newton passes, then apply) as ONE
+// cooperative launch: passes are separated by grid-wide barriers instead of
+// kernel boundaries, every block folds the (tiny) per-block partials of its
+// trial itself -- in the same fixed order, so all blocks hold bit-identical
+// state and branch uniformly -- and the apply pass follows without a return to
+// the host.  A trial still searching after max_newton passes is written back with
+// status NEWTON for the multi-launch K-ary fallback.
+__device__ __forceinline__ void newton_update(double f, double slope_r, double slope_l,
+                                              double above, double below, double tmin, double d,
+                                              double& c, double& lo, double& hi, double& lam,
+                                              int& status) {
+  double next;
+  if (f < 0.0) {
+    lo = c;
+    if (!(above < INFINITY)) { status = PROJ_INFEASIBLE_HIGH; return; }
+    if (slope_r > 0.0) {
+      const double r = c - f / slope_r;
+      if (r <= above) { lam = r; status = PROJ_DONE; return; }
+      lo = above;
+      next = r;
+    } else {
+      next = above;
+    }
+  } else {
+    hi = c;
+    if (!(below > -INFINITY)) {
+      lam = tmin;
+      status = f > 1e-9 * (1.0 + fabs(d)) ? PROJ_INFEASIBLE_LOW : PROJ_DONE;
+      return;
+    }
+    if (slope_l > 0.0) {
+      const double r = c - f / slope_l;
+      if (r >= below) { lam = r; status = PROJ_DONE; return; }
+      hi = below;
+      next = r;
+    } else {
+      next = below;
+    }
+  }
+  const bool flat_step = (f < 0.0 && !(slope_r > 0.0)) || (f >= 0.0 && !(slope_l > 0.0));
+  if (!flat_step && !(next > lo && next < hi)) {
+    if (lo > -INFINITY && hi < INFINITY) next = 0.5 * (lo + hi);
+    else if (lo > -INFINITY) next = f < 0.0 ? above : lo + 2.0 * (c - lo) + 1.0;
+    else next = below;
+  }
+  c = next;
+  status = PROJ_NEWTON;
+}
+
+__global__ void __launch_bounds__(SSNAL_NT) proj_fused_kernel(ProjArgs p, double hint,
+                                                              int max_newton, int* active) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[8 * 32];
+  __shared__ double sh[8];
+  __shared__ int sh_status;
+  const int t = blockIdx.y;
+  const unsigned nb = gridDim.x;
+  const long long region = (long long)gridDim.y * nb * PSTRIDE;
+  double c = hint, lo = -INFINITY, hi = INFINITY, lam = 0.0, tmin = INFINITY, tmax = -INFINITY;
+  int status = PROJ_NEWTON, passes = 0;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *active = (int)gridDim.y;
+  for (int pass = 0;; ++pass) {
+    double* part = p.part + (pass & 1) * region + (long long)t * nb * PSTRIDE;
+    const int ops[8] = {0, 0, 0, 1, 2, 1, 2, 0};
+    double vals[8] = {0.0, 0.0, 0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0.0};
+    if (status == PROJ_NEWTON) {
+      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+           i += (long long)nb * blockDim.x) {
+        double v, a, l, u;
+        load_elem(p, t, i, v, a, l, u);
+        if (a == 0.0) continue;
+        const double t1 = __ddiv_rn(__dsub_rn(v, u), a), t2 = __ddiv_rn(__dsub_rn(v, l), a);
+        const double ta = fmin(t1, t2), tb = fmax(t1, t2);
+        vals[0] += contrib(v, a, l, u, c);
+        const double a2 = a * a;
+        if (ta <= c && c < tb) vals[1] += a2;
+        if (ta < c && c <= tb) vals[2] += a2;
+        if (ta > c) vals[3] = fmin(vals[3], ta); else if (ta < c) vals[4] = fmax(vals[4], ta);
+        if (tb > c) vals[3] = fmin(vals[3], tb); else if (tb < c) vals[4] = fmax(vals[4], tb);
+        vals[5] = fmin(vals[5], ta);
+        vals[6] = fmax(vals[6], tb);
+        vals[7] += 1.0;
+      }
+      block_reduce<8>(vals, ops, red);
+      if (threadIdx.x == 0)
+        for (int k = 0; k < 8; ++k) part[(long long)blockIdx.x * PSTRIDE + k] = vals[k];
+    }
+    grid.sync();
+    bool finished_now = false;
+    if (status == PROJ_NEWTON) {
+      block_fold_partials<8>(part, nb, PSTRIDE, ops, vals, red);
+      if (threadIdx.x == 0) {
+        ++passes;
+        if (pass == 0) { tmin = vals[5]; tmax = vals[6]; }
+        if (vals[7] == 0.0) {
+          lam = 0.0;
+          status = PROJ_DONE;
+        } else {
+          newton_update(p.d - vals[0], vals[1], vals[2], vals[3], vals[4], tmin, p.d, c, lo, hi,
+                        lam, status);
+        }
+        sh[0] = c; sh[1] = lo; sh[2] = hi; sh[3] = lam; sh[4] = tmin; sh[5] = tmax;
+        sh[6] = (double)passes;
+        sh_status = status;
+      }
+      __syncthreads();
+      c = sh[0]; lo = sh[1]; hi = sh[2]; lam = sh[3]; tmin = sh[4]; tmax = sh[5];
+      passes = (int)sh[6];
+      status = sh_status;
+      finished_now = status != PROJ_NEWTON;
+      __syncthreads();
+    }
+    if (gridDim.y == 1) {  // single trial: every block knows the status
+      if (status != PROJ_NEWTON || pass + 1 >= max_newton) break;
+    } else {
+      if (finished_now && blockIdx.x == 0 && threadIdx.x == 0) atomicSub(active, 1);
+      grid.sync();
+      const int left = *(volatile int*)active;
+      if (left == 0 || pass + 1 >= max_newton) break;
+    }
+  }
+  // apply (region 2)
+  double* part = p.part + 2 * region + (long long)t * nb * PSTRIDE;
+  if (status == PROJ_DONE) {
+    double s6[6] = {0, 0, 0, 0, 0, 0};
+    double* xo = p.x_out ? p.x_out + (long long)t * p.n : nullptr;
+    unsigned char* fo = p.free_out ? p.free_out + (long long)t * p.n : nullptr;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+         i += (long long)nb * blockDim.x) {
+      double v, a, l, u;
+      load_elem(p, t, i, v, a, l, u);
+      const double y = __dsub_rn(v, __dmul_rn(lam, a));
+      const double x = fmin(fmax(y, l), u);
+      const bool lower = y <= __dadd_rn(l, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(l))));
+      const bool upper = !lower && (y >= __dsub_rn(u, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(u)))));
+      const bool fr = !(lower || upper);
+      if (xo) xo[i] = x;
+      if (fo) fo[i] = fr ? 1 : 0;
+      const double r = v - x;
+      s6[0] += v * v;
+      s6[1] += r * r;
+      if (p.ref) { const double dd = x - p.ref[i]; s6[2] += dd * dd; }
+      if (fr) { s6[3] += a * a; s6[4] += 1.0; }
+      s6[5] += x * (2.0 * v - x);
+    }
+    const int ops6[6] = {0, 0, 0, 0, 0, 0};
+    block_reduce<6>(s6, ops6, red);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < 6; ++k) part[(long long)blockIdx.x * PSTRIDE + k] = s6[k];
+  }
+  grid.sync();
+  if (blockIdx.x != 0) return;
+  ProjState* st = p.st + t;
+  if (status == PROJ_DONE) {
+    double r[6];
+    const int ops6[6] = {0, 0, 0, 0, 0, 0};
+    block_fold_partials<6>(part, nb, PSTRIDE, ops6, r, red);
+    if (threadIdx.x != 0) return;
+    st->sum_v2 = r[0];
+    st->sum_r2 = r[1];
+    st->sum_dref2 = r[2];
+    st->sum_a2_free = r[3];
+    st->nfree = (long long)r[4];
+    st->sum_xv = r[5];
+    st->lam = lam;
+    st->status = PROJ_APPLIED;
+  } else {
+    if (threadIdx.x != 0) return;
+    st->lam = c;  // Newton iterate for the fallback (or tmin for infeasible-low)
+    st->lo = lo;
+    st->hi = hi;
+    st->status = status;
+  }
+  st->tmin = tmin;
+  st->tmax = tmax;
+  st->passes = passes;
+  st->in_count = -1;
+}
+
 int proj_blocks(long long n) {
   long long b = ceil_div(n, (long long)SSNAL_NT * 4);
   if (b < 1) b = 1;
@@ -467,7 +652,20 @@ int proj_blocks(long long n) {
 }
 
 size_t proj_ws_bytes(long long n, int T) {
-  return (size_t)T * proj_blocks(n) * PSTRIDE * sizeof(double);
+  // 3 partial regions (two ping-pong search regions + apply) + the active-trial counter
+  return (size_t)3 * T * proj_blocks(n) * PSTRIDE * sizeof(double) + 64;
+}
+
+static int fused_capacity() {
+  static int cap = -1;
+  if (cap < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, proj_fused_kernel, SSNAL_NT, 0);
+    cap = sms * per;
+  }
+  return cap;
 }
 
 cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
@@ -476,7 +674,18 @@ cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
   for (int t = 0; t < SSNAL_MAX_TRIALS; ++t) p.coef[t] = (L.coef && t < L.T) ? L.coef[t] : 0.0; p.a = L.a; p.l = L.l; p.u = L.u;
   p.lc = L.lc; p.uc = L.uc; p.d = L.d; p.n = L.n; p.st = L.st; p.part = L.part;
   p.x_out = L.x_out; p.free_out = L.free_out; p.ref = L.ref;
-  dim3 grid(proj_blocks(L.n), L.T);
+  const int nblk = proj_blocks(L.n);
+  const int nbf = std::min(nblk, fused_capacity() / L.T);  // co-resident grid for grid.sync
+  if (L.newton > 0 && L.passes == 0 && L.phases == PHASE_APPLY && nbf >= 1) {
+    int* active = (int*)((char*)L.part + (size_t)3 * L.T * nblk * PSTRIDE * sizeof(double));
+    double hint = L.hint;
+    int maxn = L.newton;
+    void* args[] = {&p, &hint, &maxn, &active};
+    note_launch();
+    return cudaLaunchCooperativeKernel((void*)proj_fused_kernel, dim3(nbf, L.T), dim3(SSNAL_NT),
+                                       args, 0, stream);
+  }
+  dim3 grid(nblk, L.T);
   if (L.newton > 0) {
     for (int k = 0; k < L.newton; ++k) {
       note_launch();
