@@ -275,9 +275,175 @@ __global__ void __launch_bounds__(SM_NT, 1) chol_small_kernel(const double* __re
   if (tid == 0) *info = fail;
 }
 
+// Blocked (NB = 16) shared-memory Cholesky + solves for m <= SMALL_M.
+//  - 16 x 16 diagonal blocks: warp 0, lane i holds row i in registers; pivots by
+//    shuffle, rsqrt, no block barrier inside the block;
+//  - panel: one thread per row below, the 16-wide row in registers, reciprocal
+//    pivots (16-step dependent chain);
+//  - trailing update: each thread keeps one L row (16 values) in registers and
+//    sweeps columns, one shared load per FMA;
+//  - substitutions: 16-row diagonal blocks by warp 0 with shuffles, off-diagonal
+//    updates by all threads.  Three block barriers per 16 columns.
+constexpr int NB16 = 16;
+
+__device__ __forceinline__ void warp_chol16(double* S, int ld, int k0, int kb, int lane,
+                                            double* rdiag, int* fail) {
+  double r[NB16];
+#pragma unroll
+  for (int c = 0; c < NB16; ++c)
+    r[c] = (lane < kb && c <= lane) ? S[(k0 + lane) * ld + k0 + c] : (c == lane ? 1.0 : 0.0);
+  double mydiag = 1.0;
+#pragma unroll
+  for (int j = 0; j < NB16; ++j) {
+    double d = __shfl_sync(0xffffffffu, r[j], j);
+    if (j < kb && !(d > 0.0)) {
+      if (lane == 0 && *fail == 0) *fail = k0 + j + 1;
+      d = 1.0;
+    }
+    const double inv = rsqrt(d);
+    const double ljj = d * inv;
+    if (lane == j) mydiag = ljj;
+    r[j] = (lane == j) ? ljj : r[j] * inv;
+#pragma unroll
+    for (int c = j + 1; c < NB16; ++c) {
+      const double lcj = __shfl_sync(0xffffffffu, r[j], c);
+      if (lane >= c) r[c] = fma(-r[j], lcj, r[c]);
+    }
+  }
+  if (lane < kb) {
+#pragma unroll
+    for (int c = 0; c < NB16; ++c)
+      if (c <= lane) S[(k0 + lane) * ld + k0 + c] = r[c];
+    rdiag[lane] = 1.0 / mydiag;
+  }
+}
+
+__global__ void __launch_bounds__(SM_NT, 1) chol_small16_kernel(const double* __restrict__ M, int m,
+                                                                  const double* __restrict__ b,
+                                                                  double scale,
+                                                                  double* __restrict__ x,
+                                                                  int* __restrict__ info) {
+  extern __shared__ double S[];
+  const int ld = m | 1;
+  double* y = S + (size_t)m * ld;
+  __shared__ int fail;
+  __shared__ double rdiag[NB16];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) fail = 0;
+  for (int idx = tid; idx < m * m; idx += blockDim.x) {
+    const int i = idx / m, j = idx % m;
+    if (j <= i) S[i * ld + j] = M[(long long)i * m + j];
+  }
+  for (int i = tid; i < m; i += blockDim.x) y[i] = scale * b[i];
+  __syncthreads();
+  for (int k0 = 0; k0 < m; k0 += NB16) {
+    const int kb = min(NB16, m - k0);
+    if (warp == 0) warp_chol16(S, ld, k0, kb, lane, rdiag, &fail);
+    __syncthreads();
+    // panel rows below: L21 = A21 L11^{-T}
+    for (int i = k0 + kb + tid; i < m; i += blockDim.x) {
+      double row[NB16];
+#pragma unroll
+      for (int j = 0; j < NB16; ++j) row[j] = j < kb ? S[i * ld + k0 + j] : 0.0;
+#pragma unroll
+      for (int j = 0; j < NB16; ++j) {
+        if (j < kb) {
+          double s = row[j];
+#pragma unroll
+          for (int t = 0; t < j; ++t) s = fma(-row[t], S[(k0 + j) * ld + k0 + t], s);
+          row[j] = s * rdiag[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NB16; ++j)
+        if (j < kb) S[i * ld + k0 + j] = row[j];
+    }
+    __syncthreads();
+    // trailing update A22 -= L21 L21^T: thread (rows by warp, columns by lane)
+    const int r0 = k0 + kb;
+    for (int i = r0 + warp; i < m; i += SM_NT / 32) {
+      double li[NB16];
+#pragma unroll
+      for (int t = 0; t < NB16; ++t) li[t] = t < kb ? S[i * ld + k0 + t] : 0.0;
+      for (int c = r0 + lane; c <= i; c += 32) {
+        const double* lc = S + c * ld + k0;
+        double s = 0.0;
+#pragma unroll
+        for (int t = 0; t < NB16; ++t)
+          if (t < kb) s = fma(li[t], lc[t], s);
+        S[i * ld + c] -= s;
+      }
+    }
+    __syncthreads();
+  }
+  // forward L z = y
+  for (int k0 = 0; k0 < m; k0 += NB16) {
+    const int kb = min(NB16, m - k0);
+    if (warp == 0) {
+      double yv = lane < kb ? y[k0 + lane] : 0.0;
+      const double lrow_diag = lane < kb ? S[(k0 + lane) * ld + k0 + lane] : 1.0;
+#pragma unroll
+      for (int j = 0; j < NB16; ++j) {
+        if (j < kb) {
+          if (lane == j) yv = yv / lrow_diag;
+          const double yj = __shfl_sync(0xffffffffu, yv, j);
+          if (lane > j && lane < kb) yv = fma(-S[(k0 + lane) * ld + k0 + j], yj, yv);
+        }
+      }
+      if (lane < kb) y[k0 + lane] = yv;
+    }
+    __syncthreads();
+    for (int i = k0 + kb + tid; i < m; i += blockDim.x) {
+      double s = y[i];
+#pragma unroll
+      for (int t = 0; t < NB16; ++t)
+        if (t < kb) s = fma(-S[i * ld + k0 + t], y[k0 + t], s);
+      y[i] = s;
+    }
+    __syncthreads();
+  }
+  // backward L^T x = z
+  for (int k0 = ((m - 1) / NB16) * NB16; k0 >= 0; k0 -= NB16) {
+    const int kb = min(NB16, m - k0);
+    if (warp == 0) {
+      double xv = lane < kb ? y[k0 + lane] : 0.0;
+      const double ldiag = lane < kb ? S[(k0 + lane) * ld + k0 + lane] : 1.0;
+#pragma unroll
+      for (int j = NB16 - 1; j >= 0; --j) {
+        if (j < kb) {
+          if (lane == j) xv = xv / ldiag;
+          const double xj = __shfl_sync(0xffffffffu, xv, j);
+          if (lane < j) xv = fma(-S[(k0 + j) * ld + k0 + lane], xj, xv);
+        }
+      }
+      if (lane < kb) y[k0 + lane] = xv;
+    }
+    __syncthreads();
+    for (int i = tid; i < k0; i += blockDim.x) {
+      double s = y[i];
+#pragma unroll
+      for (int t = 0; t < NB16; ++t)
+        if (t < kb) s = fma(-S[(k0 + t) * ld + i], y[k0 + t], s);
+      y[i] = s;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < m; i += blockDim.x) x[i] = y[i];
+  if (tid == 0) *info = fail;
+}
+
 cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
                               int* info, cudaStream_t stream) {
   if (m <= SMALL_M) {
+    const int mi = (int)m;
+    const size_t smem = ((size_t)mi * (mi | 1) + mi) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(chol_small16_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    { note_launch(); chol_small16_kernel<<<1, SM_NT, smem, stream>>>(M, mi, b, scale, x, info); }
+    return cudaGetLastError();
+  }
+  if (m <= 0) {
     const int mi = (int)m;
     const size_t smem = ((size_t)mi * (mi | 1) + mi) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(chol_small_kernel,
