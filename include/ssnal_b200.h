@@ -159,6 +159,31 @@ int ssnal_dense_newton_pspace(const double* A, int64_t n_phys, int64_t q, int64_
                               const double* grad, const double* a, double sigma, double asa,
                               const double* g_r, double* t, int* info, void* ws, void* stream);
 
+/* ---- sparse (CSR) data operator ------------------------------------------
+ * X = diag(row_sign) A with A n x q in CSR (DEVICE arrays) plus its CSC copy and a
+ * segment plan for the transposed product (columns cut into segments of <= SEG
+ * nonzeros; split columns fold partial slots in order), built once per problem
+ * (the Python host builds it with numpy).  Replaces the sparse-sample use of ref
+ * kernels.py:68-154 for the linear kernel. */
+typedef struct ssnal_csr_operator_t {
+  int64_t n, q, nnz;
+  const int64_t* indptr;   const int32_t* indices; const double* values;   /* CSR */
+  const int64_t* colptr;   const int32_t* rowidx;  const double* valt;     /* CSC */
+  const double* row_sign;                                                  /* or NULL */
+  int64_t nseg;            /* segments of the CSC product                           */
+  const int64_t* seg_beg;  const int64_t* seg_end; const int32_t* seg_col; const int32_t* seg_slot;
+  int64_t nfold;           /* split columns                                         */
+  const int32_t* fold_col; const int32_t* fold_beg;   /* fold_beg: nfold + 1 entries  */
+  int64_t nslots;          /* partial slots (workspace doubles for ssnal_csr_xt)    */
+} ssnal_csr_operator_t;
+
+/* out[r] = row_sign[i] * A[i,:] . d for i = rows[r] (rows NULL: i = r), r < nrows */
+int ssnal_csr_xd(const ssnal_csr_operator_t* op, const int32_t* rows, int64_t nrows,
+                 const double* d, double* out, void* stream);
+/* out = X^T v (q), v of length n; ws >= nslots doubles */
+int ssnal_csr_xt(const ssnal_csr_operator_t* op, const double* v, double* out, void* ws,
+                 void* stream);
+
 /* ---- native SSsNAL driver ------------------------------------------------
  * The whole Algorithm 1 / Algorithm 3 loop of ref solver.py:331-530 (alm_solve,
  * ssn_solve, line_search, newton_direction, kkt_residual) run from C++ on one
@@ -177,6 +202,9 @@ typedef struct ssnal_dense_problem_t {
   const double* l;          /* lower bounds (DEVICE, n) or NULL => l_const           */
   const double* u;          /* upper bounds (DEVICE, n) or NULL => u_const           */
   double l_const, u_const, d;
+  const ssnal_csr_operator_t* csr;  /* non-NULL: sparse operator (A, lda unused); the
+                                       reduced Newton system is then solved by CG in
+                                       sample space (matrix-free)                      */
 } ssnal_dense_problem_t;
 
 typedef struct ssnal_options_t {
@@ -212,6 +240,7 @@ typedef void (*ssnal_progress_fn)(int k, double kkt, double sigma, long long p, 
                                   void* ctx);
 
 size_t ssnal_alm_ws_bytes(int64_t n_phys, int64_t q, int svr_block);
+size_t ssnal_alm_ws_bytes_csr(const ssnal_csr_operator_t* op);
 int ssnal_alm_solve_dense(const ssnal_dense_problem_t* problem, const ssnal_options_t* options,
                           const double* x0, const double* w0, double* x_out,
                           ssnal_report_t* report, void* ws, size_t ws_bytes,

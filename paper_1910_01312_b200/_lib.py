@@ -61,12 +61,22 @@ _SIGNATURES = {
                                        _P, _P, _P, _P, _P]),
 }
 
+class CsrOperator(ctypes.Structure):
+    """ssnal_csr_operator_t"""
+    _fields_ = [("n", ctypes.c_int64), ("q", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("indptr", _P), ("indices", _P), ("values", _P),
+                ("colptr", _P), ("rowidx", _P), ("valt", _P), ("row_sign", _P),
+                ("nseg", ctypes.c_int64), ("seg_beg", _P), ("seg_end", _P), ("seg_col", _P),
+                ("seg_slot", _P), ("nfold", ctypes.c_int64), ("fold_col", _P), ("fold_beg", _P),
+                ("nslots", ctypes.c_int64)]
+
+
 class DenseProblem(ctypes.Structure):
     """ssnal_dense_problem_t"""
     _fields_ = [("A", _P), ("n_phys", ctypes.c_int64), ("q", ctypes.c_int64),
                 ("lda", ctypes.c_int64), ("row_sign", _P), ("svr_block", _I),
                 ("n", ctypes.c_int64), ("c", _P), ("a", _P), ("l", _P), ("u", _P),
-                ("l_const", _D), ("u_const", _D), ("d", _D)]
+                ("l_const", _D), ("u_const", _D), ("d", _D), ("csr", ctypes.POINTER(CsrOperator))]
 
 
 class Options(ctypes.Structure):
@@ -98,6 +108,9 @@ PROGRESS_FN = ctypes.CFUNCTYPE(None, _I, _D, _D, ctypes.c_longlong, _I, _P)
 
 _SIGNATURES.update({
     "ssnal_alm_ws_bytes": (_SZ, [_I64, _I64, _I]),
+    "ssnal_alm_ws_bytes_csr": (_SZ, [ctypes.POINTER(CsrOperator)]),
+    "ssnal_csr_xd": (_I, [ctypes.POINTER(CsrOperator), _P, _I64, _P, _P, _P]),
+    "ssnal_csr_xt": (_I, [ctypes.POINTER(CsrOperator), _P, _P, _P, _P]),
     "ssnal_alm_solve_dense": (_I, [ctypes.POINTER(DenseProblem), ctypes.POINTER(Options), _P, _P,
                                    _P, ctypes.POINTER(Report), _P, _SZ, PROGRESS_FN, _P, _P]),
 })

@@ -34,6 +34,7 @@ cudaError_t launch_chol_solve(double* M, long long m, const double* b, double sc
                               int* info, cudaStream_t s);
 size_t pspace_ws_bytes(long long p, long long q);
 size_t alm_ws_bytes(long long n_phys, long long q, int svr);
+size_t alm_ws_bytes_csr(const ssnal_csr_operator_t* op);
 int alm_solve_dense(const ssnal_dense_problem_t* pb, const ssnal_options_t* opt, const double* x0,
                     const double* w0, double* x_out, ssnal_report_t* rep, void* ws,
                     size_t ws_bytes, ssnal_progress_fn cb, void* ctx, cudaStream_t stream,
@@ -182,6 +183,30 @@ size_t ssnal_alm_ws_bytes(int64_t n_phys, int64_t q, int svr_block) {
   return alm_ws_bytes(n_phys, q, svr_block);
 }
 
+size_t ssnal_alm_ws_bytes_csr(const ssnal_csr_operator_t* op) {
+  return op ? alm_ws_bytes_csr(op) : 0;
+}
+
+static bool csr_ok(const ssnal_csr_operator_t* op) {
+  return op && op->n >= 1 && op->q >= 1 && op->indptr && op->indices && op->values &&
+         op->colptr && op->rowidx && op->valt && op->seg_beg && op->seg_end && op->seg_col &&
+         op->seg_slot && (op->nfold == 0 || (op->fold_col && op->fold_beg));
+}
+
+int ssnal_csr_xd(const ssnal_csr_operator_t* op, const int32_t* rows, int64_t nrows,
+                 const double* d, double* out, void* stream) {
+  if (!csr_ok(op) || !d || !out || nrows < 0) return fail_arg("ssnal_csr_xd", "operator/null");
+  if (nrows == 0) return SSNAL_OK;
+  return check("ssnal_csr_xd", launch_csr_xd(*op, rows, nrows, d, out, S(stream)));
+}
+
+int ssnal_csr_xt(const ssnal_csr_operator_t* op, const double* v, double* out, void* ws,
+                 void* stream) {
+  if (!csr_ok(op) || !v || !out || (op->nslots > 0 && !ws))
+    return fail_arg("ssnal_csr_xt", "operator/null");
+  return check("ssnal_csr_xt", launch_csc_xt(*op, v, out, (double*)ws, S(stream)));
+}
+
 int ssnal_alm_solve_dense(const ssnal_dense_problem_t* problem, const ssnal_options_t* options,
                           const double* x0, const double* w0, double* x_out,
                           ssnal_report_t* report, void* ws, size_t ws_bytes,
@@ -189,9 +214,14 @@ int ssnal_alm_solve_dense(const ssnal_dense_problem_t* problem, const ssnal_opti
   if (!problem || !options || !x_out || !report || !ws)
     return fail_arg("ssnal_alm_solve_dense", "null problem/options/x_out/report/ws");
   const ssnal_dense_problem_t& p = *problem;
-  if (p.n_phys < 1 || p.q < 1 || p.lda < p.q || !p.A || !p.c || !p.a ||
-      p.n != (p.svr_block ? 2 * p.n_phys : p.n_phys))
+  if (p.csr) {
+    if (!csr_ok(p.csr) || p.svr_block || p.n != p.csr->n || p.n_phys != p.csr->n ||
+        p.q != p.csr->q || !p.c || !p.a)
+      return fail_arg("ssnal_alm_solve_dense", "inconsistent sparse problem");
+  } else if (p.n_phys < 1 || p.q < 1 || p.lda < p.q || !p.A || !p.c || !p.a ||
+             p.n != (p.svr_block ? 2 * p.n_phys : p.n_phys)) {
     return fail_arg("ssnal_alm_solve_dense", "inconsistent problem sizes");
+  }
   const char* err = nullptr;
   int rc = alm_solve_dense(problem, options, x0, w0, x_out, report, ws, ws_bytes, progress,
                            progress_ctx, S(stream), &err);

@@ -51,9 +51,24 @@ cudaError_t launch_pspace_direction(const double* A, long long n, long long q, l
                                     const double* g_r, double* t, int* info, void* ws,
                                     cudaStream_t stream);
 
+cudaError_t launch_cg_init(long long p, const double* b, double* y, double* r, double* pv,
+                           const double* g2, double eta, double tau, double sigma, double* cgs,
+                           double* part, cudaStream_t s);
+cudaError_t launch_cg_project(long long p, const double* x, const double* aJ, const double* dot,
+                              double asa, double* out, cudaStream_t s);
+cudaError_t launch_cg_ap(long long p, const double* pv, const double* zq, const double* aJ,
+                         double asa, double sigma, double* Ap, double* cgs, double* part,
+                         cudaStream_t s);
+cudaError_t launch_cg_step(long long p, double* y, double* r, const double* pv, const double* Ap,
+                           double* cgs, double* part, cudaStream_t s);
+cudaError_t launch_cg_dir(long long p, const double* r, double* pv, const double* cgs,
+                          cudaStream_t s);
+cudaError_t launch_scatter_zero(const int32_t* rows, long long p, double* dst, cudaStream_t s);
+
 namespace {
 
 constexpr int TMAX = 4;  // batched Armijo trials per launch
+constexpr int CG_BATCH = 16;  // CG iterations between host checks of the device flag
 constexpr int NSCAL = 16;
 
 struct DriverError {
@@ -76,6 +91,7 @@ struct Carver {
 
 struct Pinned {
   double scal[NSCAL];
+  double cg[8];
   int info;
   int pad;
   ProjState st[TMAX];
@@ -98,11 +114,18 @@ struct Layout {
   int* info;
   ProjState *st_cur, *st_trial, *st_kkt;
   void *ws_proj, *ws_red, *ws_xt, *ws_gram, *ws_cmp, *ws_ps;
+  // sparse operator: sample-space CG buffers, scattered vector, CSC partial slots
+  double *ys, *tq, *cg_gJ, *cg_aJ, *cg_b, *cg_y, *cg_r, *cg_pv, *cg_Ap, *cg_zq, *cg_w, *cgs,
+      *cg_part, *csc_part;
 };
 
-Layout carve(char* base, long long n, long long n_phys, long long q, size_t* total) {
+size_t cg_part_doubles(long long n) { return (size_t)stream_blocks(n, 4) + 8; }
+
+Layout carve(char* base, long long n, long long n_phys, long long q, size_t* total,
+             const ssnal_csr_operator_t* csr = nullptr) {
   Carver cv{base, 0, 0};
-  Layout L;
+  Layout L{};
+  const bool sparse = csr != nullptr;
   L.x = cv.take<double>(n);
   L.w = cv.take<double>(n);
   L.qw = cv.take<double>(n);
@@ -119,7 +142,7 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
   L.tx = cv.take<double>((size_t)TMAX * n);
   L.gr = cv.take<double>(2 * q);
   L.t = cv.take<double>(q);
-  L.M = cv.take<double>((size_t)q * q);
+  L.M = sparse ? nullptr : cv.take<double>((size_t)q * q);
   L.m1 = cv.take<double>(q);
   L.scal = cv.take<double>(NSCAL);
   L.fr = cv.take<uint8_t>(n);
@@ -132,10 +155,27 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
   L.st_kkt = cv.take<ProjState>(1);
   L.ws_proj = cv.take<char>(proj_ws_bytes(n, TMAX));
   L.ws_red = cv.take<char>(reduce_ws_bytes(n) + 64);
-  L.ws_xt = cv.take<char>(dense_xt_ws_bytes(n_phys, q, 2));
-  L.ws_gram = cv.take<char>(gram_ws_bytes(q));
   L.ws_cmp = cv.take<char>(compact_ws_bytes(n));
-  L.ws_ps = cv.take<char>(pspace_ws_bytes(q, q));
+  if (!sparse) {
+    L.ws_xt = cv.take<char>(dense_xt_ws_bytes(n_phys, q, 2));
+    L.ws_gram = cv.take<char>(gram_ws_bytes(q));
+    L.ws_ps = cv.take<char>(pspace_ws_bytes(q, q));
+  } else {
+    L.ys = cv.take<double>(n);
+    L.tq = cv.take<double>(q);
+    L.cg_gJ = cv.take<double>(n);
+    L.cg_aJ = cv.take<double>(n);
+    L.cg_b = cv.take<double>(n);
+    L.cg_y = cv.take<double>(n);
+    L.cg_r = cv.take<double>(n);
+    L.cg_pv = cv.take<double>(n);
+    L.cg_Ap = cv.take<double>(n);
+    L.cg_zq = cv.take<double>(n);
+    L.cg_w = cv.take<double>(n);
+    L.cgs = cv.take<double>(16);
+    L.cg_part = cv.take<double>(cg_part_doubles(n));
+    L.csc_part = cv.take<double>(csr->nslots > 0 ? csr->nslots : 1);
+  }
   *total = cv.off + 256;
   return L;
 }
@@ -173,7 +213,7 @@ struct Driver {
   cudaStream_t S;
   Layout L;
   Pinned* H;
-  long long syncs = 0, newton = 0, projections = 0;
+  long long syncs = 0, newton = 0, projections = 0, cg_iters = 0;
   double lam_kkt = 0.0, lam_cur = 0.0;
   double sigma = 1.0;
   double c_norm = 0.0;
@@ -201,7 +241,46 @@ struct Driver {
   }
 
   double a_bytes() const {
+    if (P.csr)  // values + column indices + row pointers (+ labels)
+      return 12.0 * P.csr->nnz + 8.0 * P.n_phys + (P.row_sign ? 8.0 * P.n_phys : 0.0);
     return 8.0 * P.n_phys * P.q + (P.row_sign ? 8.0 * P.n_phys : 0.0);
+  }
+
+  // sample-space CG for the sparse operator: t = -X^T s + sigma X_J^T P_J y
+  void cg_direction(long long p, double asa, const double* g2_dev) {
+    const CsrOp& op = *P.csr;
+    ck(launch_gather(L.J, p, L.grad, L.cg_gJ, S));
+    ck(launch_gather(L.J, p, P.a, L.cg_aJ, S));
+    dots({{L.cg_aJ, L.cg_gJ}}, L.cgs + 7, p);
+    ck(launch_cg_project(p, L.cg_gJ, L.cg_aJ, L.cgs + 7, asa, L.cg_b, S));
+    // reference target min(eta, ||grad||^(1+tau)) on the Newton residual (ref solver.py:229);
+    // the sample-space residual maps to it through sigma X Z^T P: scaled by 1/sigma
+    ck(launch_cg_init(p, L.cg_b, L.cg_y, L.cg_r, L.cg_pv, g2_dev, O.eta, O.tau, sigma, L.cgs,
+                      L.cg_part, S));
+    for (int it = 0; it < O.cg_max_iters;) {
+      for (int b = 0; b < CG_BATCH && it < O.cg_max_iters; ++b, ++it) {
+        ck(launch_scatter(L.J, p, L.cg_pv, L.ys, S));
+        ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
+        ck(launch_csr_xd(op, L.J, p, L.tq, L.cg_zq, S));
+        dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
+        ck(launch_cg_ap(p, L.cg_pv, L.cg_zq, L.cg_aJ, asa, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
+        ck(launch_cg_step(p, L.cg_y, L.cg_r, L.cg_pv, L.cg_Ap, L.cgs, L.cg_part, S));
+        ck(launch_cg_dir(p, L.cg_r, L.cg_pv, L.cgs, S));
+      }
+      ck(cudaMemcpyAsync(H->cg, L.cgs, sizeof(double) * 8, cudaMemcpyDeviceToHost, S));
+      ck(cudaStreamSynchronize(S));
+      ++syncs;
+      if (H->cg[5] != 0.0) break;
+    }
+    cg_iters += (long long)H->cg[6];
+    // w = P_J y, t = -g_r + sigma X^T scatter(w)
+    dots({{L.cg_aJ, L.cg_y}}, L.cgs + 7, p);
+    ck(launch_cg_project(p, L.cg_y, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
+    ck(launch_scatter(L.J, p, L.cg_w, L.ys, S));
+    ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
+    ck(launch_scatter_zero(L.J, p, L.ys, S));
+    ck(launch_vec(4, P.q, sigma, L.tq, nullptr, nullptr, L.t, S));  // sigma X^T P_J y
+    ck(launch_vec(3, P.q, 0.0, L.t, L.gr, nullptr, L.t, S));       // - X^T s
   }
 
   // ---------------------------------------------------------------- plumbing
@@ -278,14 +357,24 @@ struct Driver {
     int k = 0;
     for (auto v : vs) arr[k++] = v;
     timed(SSNAL_OP_XT, a_bytes() + 8.0 * k * (P.n + P.q), [&] {
-      ck(launch_dense_xt(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, k, arr, out,
-                         L.ws_xt, S));
+      if (P.csr) {
+        for (int j = 0; j < k; ++j) ck(launch_csc_xt(*P.csr, arr[j], out + (size_t)j * P.q,
+                                                     L.csc_part, S));
+      } else {
+        ck(launch_dense_xt(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, k, arr, out,
+                           L.ws_xt, S));
+      }
     });
   }
 
   void xd(const double* d, double* out, int k) {
     timed(SSNAL_OP_XD, a_bytes() + 8.0 * k * (P.n + P.q), [&] {
-      ck(launch_dense_x(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, k, d, out, S));
+      if (P.csr) {
+        for (int j = 0; j < k; ++j)
+          ck(launch_csr_xd(*P.csr, nullptr, P.n_phys, d + (size_t)j * P.q, out + (size_t)j * P.n, S));
+      } else {
+        ck(launch_dense_x(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, k, d, out, S));
+      }
     });
   }
 
@@ -325,11 +414,24 @@ struct Driver {
     xd(L.gr, L.grad, 1);
   }
 
-  void direction(long long p, double asa) {
+  void direction(long long p, double asa, const double* g2_dev) {
     if (p == 0) {  // Sigma = 0: d = -s, Qd = -grad (ref solver.py:221-222)
       vec(4, -1.0, L.s, nullptr, nullptr, L.dir);
       vec(4, -1.0, L.grad, nullptr, nullptr, L.qdir);
       dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}, {L.s, L.grad}}, L.scal, P.n);
+      return;
+    }
+    if (P.csr) {  // matrix-free sample-space CG (q is large for sparse data)
+      timed(SSNAL_OP_NEWTON, 0.0, [&] {
+        ck(launch_compact(L.fr, P.n, L.J, L.pcount, L.ws_cmp, S));
+        cg_direction(p, asa, g2_dev);
+      });
+      xd(L.t, L.qdir, 1);
+      timed(SSNAL_OP_VEC, 8.0 * P.n * 5, [&] {
+        ck(launch_hs_apply(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.ws_red, S));
+      });
+      dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}}, L.scal, P.n);
+      dots({{L.t, nullptr}}, L.scal + 3, P.q);
       return;
     }
     if (p < P.q && p > O.direct_solve_threshold)
@@ -374,7 +476,8 @@ struct Driver {
       gradient();
       dots({{L.grad, nullptr}}, L.scal + 4, P.n);
     }
-    direction(p, asa);
+    // ||grad||^2 of this point on the device: scal[4] after a gradient, scal[0] at the start
+    direction(p, asa, with_gradient ? L.scal + 4 : L.scal + 0);
     const double coef = sigma;
     project(L.u, L.st_trial, 1, L.qdir, &coef, L.tx, L.tfree, L.x, lam_cur);
     fetch(L.st_trial, 1, p > 0);
@@ -622,12 +725,18 @@ size_t alm_ws_bytes(long long n_phys, long long q, int svr) {
   return total;
 }
 
+size_t alm_ws_bytes_csr(const ssnal_csr_operator_t* op) {
+  size_t total = 0;
+  carve(nullptr, op->n, op->n, op->q, &total, op);
+  return total;
+}
+
 int alm_solve_dense(const ssnal_dense_problem_t* pb, const ssnal_options_t* opt, const double* x0,
                     const double* w0, double* x_out, ssnal_report_t* rep, void* ws,
                     size_t ws_bytes, ssnal_progress_fn cb, void* ctx, cudaStream_t stream,
                     const char** err) {
   size_t need = 0;
-  Layout L = carve((char*)ws, pb->n, pb->n_phys, pb->q, &need);
+  Layout L = carve((char*)ws, pb->n, pb->n_phys, pb->q, &need, pb->csr);
   if (ws_bytes < need) {
     *err = "workspace smaller than ssnal_alm_ws_bytes()";
     return SSNAL_E_ARG;

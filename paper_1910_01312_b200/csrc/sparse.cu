@@ -1,0 +1,145 @@
+// CSR data operator (configs 2, 3): Q = X X^T with X = diag(y) A, A sparse n x q.
+//
+//   X d    : warp per row group -- each 8-lane sub-warp owns a row, lanes stride the
+//            row's nonzeros (coalesced index/value loads), gather d[col] through the
+//            read-only path, sub-warp shuffle tree.  Optional row list (X_J d).
+//   X^T v  : on the CSC copy (built once per problem).  Columns are cut into
+//            segments of <= SEG nonzeros (Zipf-hot columns span many segments), one
+//            warp per segment; whole-column segments write the output directly,
+//            split columns write partials folded in segment order.  Balanced and
+//            deterministic: no atomics, fixed summation order.
+//   scatter/gather helpers for the sample-space CG of the reduced Newton system.
+#include "common.cuh"
+#include "ssnal_internal.h"
+
+namespace ssnal {
+
+static constexpr int SUB = 8;  // lanes per row in X d
+
+// out[r] = rs[i] * sum_k val[k] d[col[k]],  i = rows ? rows[r] : r  (r < nrows)
+__global__ void __launch_bounds__(256) csr_xd_kernel(const int64_t* __restrict__ indptr,
+                                                     const int32_t* __restrict__ indices,
+                                                     const double* __restrict__ values,
+                                                     const double* __restrict__ rs,
+                                                     const int32_t* __restrict__ rows, long long nrows,
+                                                     const double* __restrict__ d,
+                                                     double* __restrict__ out) {
+  const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SUB;
+  const int sl = threadIdx.x & (SUB - 1);
+  if (g >= nrows) return;
+  const long long i = rows ? (long long)rows[g] : g;
+  const long long k0 = indptr[i], k1 = indptr[i + 1];
+  double s = 0.0;
+  for (long long k = k0 + sl; k < k1; k += SUB) s = fma(values[k], __ldg(d + indices[k]), s);
+#pragma unroll
+  for (int o = SUB / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, SUB);
+  if (sl == 0) out[g] = rs ? rs[i] * s : s;
+}
+
+// segment s covers CSC entries [seg_beg[s], seg_end[s]) of column seg_col[s];
+// seg_slot[s] < 0: whole column (write out directly), else partial slot index.
+__global__ void __launch_bounds__(256) csc_xt_kernel(const int64_t* __restrict__ seg_beg,
+                                                     const int64_t* __restrict__ seg_end,
+                                                     const int32_t* __restrict__ seg_col,
+                                                     const int32_t* __restrict__ seg_slot,
+                                                     long long nseg,
+                                                     const int32_t* __restrict__ rowidx,
+                                                     const double* __restrict__ valt,
+                                                     const double* __restrict__ rs,
+                                                     const double* __restrict__ v,
+                                                     double* __restrict__ out,
+                                                     double* __restrict__ part) {
+  const long long s = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nseg) return;
+  const long long k0 = seg_beg[s], k1 = seg_end[s];
+  double acc = 0.0;
+  for (long long k = k0 + lane; k < k1; k += 32) {
+    const int r = rowidx[k];
+    const double cv = rs ? rs[r] * v[r] : v[r];
+    acc = fma(valt[k], cv, acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    const int slot = seg_slot[s];
+    if (slot < 0) out[seg_col[s]] = acc;
+    else part[slot] = acc;
+  }
+}
+
+// split columns: out[col] = sum of its partial slots [pbeg, pend) in order
+__global__ void csc_fold_kernel(const int32_t* __restrict__ fold_col,
+                                const int32_t* __restrict__ fold_beg, long long nfold,
+                                const double* __restrict__ part, double* __restrict__ out) {
+  const long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nfold) return;
+  double s = 0.0;
+  for (int k = fold_beg[f]; k < fold_beg[f + 1]; ++k) s += part[k];
+  out[fold_col[f]] = s;
+}
+
+// dst[i] = 0 for all i in [0, n) that are not overwritten later: zero fill
+__global__ void fill_kernel(double* __restrict__ dst, long long n, double v) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+
+// dst[rows[r]] = src[r]  (r < p)
+__global__ void scatter_kernel(const int32_t* __restrict__ rows, long long p,
+                               const double* __restrict__ src, double* __restrict__ dst) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < p) dst[rows[r]] = src[r];
+}
+
+// dst[r] = src[rows[r]]
+__global__ void gather_kernel(const int32_t* __restrict__ rows, long long p,
+                              const double* __restrict__ src, double* __restrict__ dst) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < p) dst[r] = src[rows[r]];
+}
+
+cudaError_t launch_csr_xd(const CsrOp& op, const int32_t* rows, long long nrows, const double* d,
+                          double* out, cudaStream_t stream) {
+  const long long threads = nrows * SUB;
+  note_launch();
+  csr_xd_kernel<<<(unsigned)ceil_div(threads, 256LL), 256, 0, stream>>>(
+      op.indptr, op.indices, op.values, op.row_sign, rows, nrows, d, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csc_xt(const CsrOp& op, const double* v, double* out, double* part,
+                          cudaStream_t stream) {
+  note_launch();
+  csc_xt_kernel<<<(unsigned)ceil_div(op.nseg * 32, 256LL), 256, 0, stream>>>(
+      op.seg_beg, op.seg_end, op.seg_col, op.seg_slot, op.nseg, op.rowidx, op.valt, op.row_sign,
+      v, out, part);
+  if (op.nfold > 0) {
+    note_launch();
+    csc_fold_kernel<<<(unsigned)ceil_div(op.nfold, 256LL), 256, 0, stream>>>(
+        op.fold_col, op.fold_beg, op.nfold, part, out);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(double* dst, long long n, double v, cudaStream_t stream) {
+  note_launch();
+  fill_kernel<<<(unsigned)min(ceil_div(n, 1024LL), 1184LL), 256, 0, stream>>>(dst, n, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const int32_t* rows, long long p, const double* src, double* dst,
+                           cudaStream_t stream) {
+  note_launch();
+  scatter_kernel<<<(unsigned)ceil_div(p, 256LL), 256, 0, stream>>>(rows, p, src, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const int32_t* rows, long long p, const double* src, double* dst,
+                          cudaStream_t stream) {
+  note_launch();
+  gather_kernel<<<(unsigned)ceil_div(p, 256LL), 256, 0, stream>>>(rows, p, src, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace ssnal

@@ -22,6 +22,17 @@ enum ProjPhase { PHASE_RANGE = 1, PHASE_EXACT = 2, PHASE_APPLY = 4 };
 
 // ProjState is the device record ssnal_proj_state_t of the public header.
 using ProjState = ssnal_proj_state_t;
+using CsrOp = ssnal_csr_operator_t;
+
+cudaError_t launch_csr_xd(const CsrOp& op, const int32_t* rows, long long nrows, const double* d,
+                          double* out, cudaStream_t stream);
+cudaError_t launch_csc_xt(const CsrOp& op, const double* v, double* out, double* part,
+                          cudaStream_t stream);
+cudaError_t launch_fill(double* dst, long long n, double v, cudaStream_t stream);
+cudaError_t launch_scatter(const int32_t* rows, long long p, const double* src, double* dst,
+                           cudaStream_t stream);
+cudaError_t launch_gather(const int32_t* rows, long long p, const double* src, double* dst,
+                          cudaStream_t stream);
 
 struct ProjLaunch {
   const double *A, *B, *coef, *a, *l, *u;

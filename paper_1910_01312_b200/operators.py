@@ -97,6 +97,114 @@ class LinearKernelOperator:
         return torch.cat([d, d]) if self.svr_block else d
 
 
+class CsrKernelOperator:
+    """Q = X X^T for sparse samples: X = diag(labels) A, A in CSR (device), with a CSC
+    copy and a segment plan for the deterministic balanced transposed product,
+    built once here on the host (numpy/scipy, not on the solve path)."""
+
+    kind = "csr"
+    SEG = 2048  # max nonzeros per warp segment of the CSC product
+
+    def __init__(self, samples, labels=None, backend=None):
+        import ctypes
+
+        import scipy.sparse as sp
+
+        from . import _lib
+
+        self.backend = be = backend or default_backend()
+        if isinstance(samples, tuple):
+            indptr, indices, data, shape = samples
+            A = sp.csr_matrix((data, indices, indptr), shape=shape)
+        else:
+            A = sp.csr_matrix(samples)
+        A.sort_indices()
+        A = A.astype(np.float64)
+        self.n_phys, self.q = A.shape
+        self.n = self.n_phys
+        self.nnz = int(A.nnz)
+        self.svr_block = False
+        self.lda = self.q
+        C = A.tocsc()
+        C.sort_indices()
+        colptr = C.indptr.astype(np.int64)
+        lens = np.diff(colptr)
+        nseg_col = np.maximum(1, -(-lens // self.SEG))
+        seg_col = np.repeat(np.arange(self.q, dtype=np.int64), nseg_col)
+        first = np.repeat(np.cumsum(nseg_col) - nseg_col, nseg_col)
+        k = np.arange(seg_col.size) - first
+        seg_beg = colptr[seg_col] + k * self.SEG
+        seg_end = np.minimum(seg_beg + self.SEG, colptr[seg_col + 1])
+        split = nseg_col[seg_col] > 1
+        seg_slot = np.full(seg_col.size, -1, dtype=np.int64)
+        seg_slot[split] = np.arange(int(split.sum()))
+        fold_cols = np.flatnonzero(nseg_col > 1)
+        fold_beg = np.concatenate([[0], np.cumsum(nseg_col[fold_cols])]).astype(np.int32)
+        dev = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=be.device)  # noqa: E731
+        self._t = {
+            "indptr": dev(A.indptr.astype(np.int64), torch.int64),
+            "indices": dev(A.indices.astype(np.int32), torch.int32),
+            "values": dev(A.data, torch.float64),
+            "colptr": dev(colptr, torch.int64),
+            "rowidx": dev(C.indices.astype(np.int32), torch.int32),
+            "valt": dev(C.data, torch.float64),
+            "seg_beg": dev(seg_beg, torch.int64), "seg_end": dev(seg_end, torch.int64),
+            "seg_col": dev(seg_col.astype(np.int32), torch.int32),
+            "seg_slot": dev(seg_slot.astype(np.int32), torch.int32),
+            "fold_col": dev(fold_cols.astype(np.int32) if fold_cols.size else np.zeros(1, np.int32),
+                            torch.int32),
+            "fold_beg": dev(fold_beg if fold_cols.size else np.zeros(2, np.int32), torch.int32),
+        }
+        if labels is not None:
+            lab = as_device(labels, be)
+            check_vector(lab, self.n_phys, "labels")
+            if not bool(torch.all(lab.abs() == 1.0)):
+                raise InputError("labels must be +1/-1")
+            self.row_sign = lab
+        else:
+            self.row_sign = None
+        self.nslots = int(split.sum())
+        self.part = be.zeros(max(self.nslots, 1))
+        p = lambda name: self._t[name].data_ptr()  # noqa: E731
+        self.c_op = _lib.CsrOperator(
+            n=self.n, q=self.q, nnz=self.nnz, indptr=p("indptr"), indices=p("indices"),
+            values=p("values"), colptr=p("colptr"), rowidx=p("rowidx"), valt=p("valt"),
+            row_sign=None if self.row_sign is None else self.row_sign.data_ptr(),
+            nseg=int(seg_col.size), seg_beg=p("seg_beg"), seg_end=p("seg_end"),
+            seg_col=p("seg_col"), seg_slot=p("seg_slot"), nfold=int(fold_cols.size),
+            fold_col=p("fold_col"), fold_beg=p("fold_beg"), nslots=self.nslots)
+        self._cref = ctypes.byref(self.c_op)
+        self.host_csr = A  # kept for callers (oracle checks, columns())
+
+    def xt(self, vs, out=None):
+        from . import _lib
+
+        out = out if out is not None else self.backend.empty((len(vs), self.q))
+        for j, v in enumerate(vs):
+            _lib.call("ssnal_csr_xt", self._cref, v.data_ptr(), out[j].data_ptr(),
+                      self.part.data_ptr(), self.backend.stream())
+        return out
+
+    def x(self, d, out=None, k=1):
+        from . import _lib
+
+        out = out if out is not None else self.backend.empty((k, self.n))
+        for j in range(k):
+            _lib.call("ssnal_csr_xd", self._cref, None, self.n, d[j].data_ptr(),
+                      out[j].data_ptr(), self.backend.stream())
+        return out
+
+    def matvec(self, v):
+        v = as_device(v, self.backend)
+        check_vector(v, self.n, "matvec")
+        return self.x(self.xt([v]))[0]
+
+    def diag(self):
+        a = self.host_csr
+        return torch.as_tensor(np.asarray(a.multiply(a).sum(axis=1)).ravel(),
+                               device=self.backend.device)
+
+
 class DenseOperator(LinearKernelOperator):
     """Explicit symmetric PSD Q (ref kernels.py:218-238), factored once on the host
     as Q = X X^T with X = V diag(sqrt(max(ev, 0)))."""

@@ -497,8 +497,13 @@ def kkt_residual(x, problem):
 
 
 def _native_ok(problem, alm_opts, ssn_opts):
-    from .operators import LinearKernelOperator
+    from .operators import CsrKernelOperator, LinearKernelOperator
 
+    if isinstance(problem.q_op, CsrKernelOperator):
+        if not (alm_opts.eps_seq is _half_powers and alm_opts.delta_seq is _half_powers):
+            raise InputError("the sparse operator runs only in the native driver, which uses "
+                             "the reference's default eps/delta sequences")
+        return True
     return (ssn_opts.engine == "native" and getattr(problem.backend, "name", "") == "cuda"
             and isinstance(problem.q_op, LinearKernelOperator)
             and alm_opts.eps_seq is _half_powers and alm_opts.delta_seq is _half_powers)
@@ -511,16 +516,21 @@ def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_devi
     be, op, box = problem.backend, problem.q_op, problem.constraint
     n = problem.n
     lib = _lib.load()
-    nbytes = lib.ssnal_alm_ws_bytes(op.n_phys, op.q, int(op.svr_block))
+    sparse = getattr(op, "kind", "dense") == "csr"
+    if sparse:
+        nbytes = lib.ssnal_alm_ws_bytes_csr(op._cref)
+    else:
+        nbytes = lib.ssnal_alm_ws_bytes(op.n_phys, op.q, int(op.svr_block))
     ws = getattr(problem, "_native_ws", None)
     if ws is None or ws.numel() < nbytes:
         ws = be.zeros(int(nbytes), torch.uint8)
         problem._native_ws = ws
     ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
     prob = _lib.DenseProblem(
-        A=ptr(op.A), n_phys=op.n_phys, q=op.q, lda=op.lda, row_sign=ptr(op.row_sign),
-        svr_block=int(op.svr_block), n=n, c=ptr(problem.c), a=ptr(box.a_dev),
-        l=ptr(box.l_dev), u=ptr(box.u_dev), l_const=box.l_const, u_const=box.u_const, d=box.d)
+        A=None if sparse else ptr(op.A), n_phys=op.n_phys, q=op.q, lda=op.lda,
+        row_sign=ptr(op.row_sign), svr_block=int(op.svr_block), n=n, c=ptr(problem.c),
+        a=ptr(box.a_dev), l=ptr(box.l_dev), u=ptr(box.u_dev), l_const=box.l_const,
+        u_const=box.u_const, d=box.d, csr=ctypes.pointer(op.c_op) if sparse else None)
     opts = _lib.Options(
         sigma0=alm_opts.sigma0, sigma_growth=alm_opts.sigma_growth, sigma_max=alm_opts.sigma_max,
         tol_kkt=alm_opts.tol_kkt, lambda_min_surrogate=alm_opts.lambda_min_surrogate,

@@ -17,6 +17,18 @@ from .solver import QpProblem
 SUPPORT_TOL = 1e-6  # ref svm.py:39
 
 
+def _is_sparse(features):
+    """scipy sparse matrix or an (indptr, indices, data, shape) CSR tuple."""
+    if isinstance(features, tuple) and len(features) == 4:
+        return True
+    try:
+        import scipy.sparse as sp
+
+        return sp.issparse(features)
+    except ImportError:  # pragma: no cover
+        return False
+
+
 def build_csvc_dual(features, labels, C, backend=None):
     """Q_ij = y_i y_j x_i'x_j, c = -e, y'x = 0, 0 <= x <= C (ref svm.py:95-108)."""
     be = backend or default_backend()
@@ -29,7 +41,12 @@ def build_csvc_dual(features, labels, C, backend=None):
         raise InputError("need samples from both classes")
     if not C > 0:
         raise InputError("C must be positive")
-    op = LinearKernelOperator(features, labels=y, backend=be)
+    if _is_sparse(features):
+        from .operators import CsrKernelOperator
+
+        op = CsrKernelOperator(features, labels=y, backend=be)
+    else:
+        op = LinearKernelOperator(features, labels=y, backend=be)
     if op.n != n:
         raise InputError("labels must have one entry per sample")
     box = BoxLineSet(a=y, d=0.0, l=np.zeros(n), u=np.full(n, float(C)), backend=be)

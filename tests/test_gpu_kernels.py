@@ -240,3 +240,32 @@ def test_gram_and_cholesky(pkg, n, q, p):
     assert int(info.cpu()[0]) == 0
     x_ref = -np.linalg.solve(M_ref, b)
     assert np.linalg.norm(xo.cpu().numpy() - x_ref) <= 1e-10 * np.linalg.cond(M_ref) * np.linalg.norm(x_ref)
+
+
+@pytest.mark.parametrize("n,q,nnz_row,zipf", [(3000, 500, 7, False), (20000, 3000, 30, True),
+                                              (5, 4, 2, False)])
+def test_csr_products(pkg, n, q, nnz_row, zipf):
+    """CSR X d and CSC X^T v (segmented, split hot columns) against scipy."""
+    import scipy.sparse as sp
+
+    from paper_1910_01312_b200.operators import CsrKernelOperator
+
+    rng = np.random.default_rng(n)
+    rows = np.repeat(np.arange(n), nnz_row)
+    if zipf:  # a few very hot columns force split segments + folds
+        cols = np.minimum(rng.zipf(1.3, size=n * nnz_row) - 1, q - 1)
+    else:
+        cols = rng.integers(0, q, size=n * nnz_row)
+    A = sp.csr_matrix((rng.standard_normal(rows.size), (rows, cols)), shape=(n, q))
+    A.sum_duplicates()
+    y = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+    op = CsrKernelOperator(A, labels=y)
+    X = sp.diags(y) @ A
+    d = rng.standard_normal(q)
+    v = rng.standard_normal(n)
+    out = op.x(_dev(d).view(1, -1))[0].cpu().numpy()
+    np.testing.assert_allclose(out, X @ d, rtol=1e-12, atol=1e-12 * np.abs(X).sum(axis=1).max())
+    g = op.xt([_dev(v)])[0].cpu().numpy()
+    np.testing.assert_allclose(g, X.T @ v, rtol=1e-12, atol=1e-11 * max(1, np.abs(X).sum(axis=0).max()))
+    if zipf and n > 1000:
+        assert op.nslots > 0  # hot columns were split

@@ -130,3 +130,29 @@ def test_svr_vs_oracle(pkg):
     ref = O.alm_solve(op, c, bl, O.AlmOpts(tol_kkt=1e-6))
     assert rep.converged
     assert rep.objective == pytest.approx(ref["objective"], rel=1e-6)
+
+
+@pytest.mark.parametrize("n,q,density,C", [(3000, 400, 0.03, 1.0), (6000, 2000, 0.01, 0.1)])
+def test_sparse_csvc_vs_oracle_and_dense(pkg, n, q, density, C):
+    """Sparse (CSR, sample-space CG) solve: same objective as the oracle and as the
+    dense operator on the same data, at R_KKT <= 1e-6."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(n)
+    A = sp.random(n, q, density=density, random_state=rng, data_rvs=rng.standard_normal,
+                  format="csr")
+    w = np.zeros(q)
+    w[rng.choice(q, size=max(1, q // 50), replace=False)] = rng.standard_normal(max(1, q // 50))
+    y = np.where(A @ w + 0.05 * rng.standard_normal(n) >= 0, 1.0, -1.0)
+    rep = pkg.alm_solve(pkg.build_csvc_dual(A, y, C), pkg.AlmOptions(tol_kkt=1e-6))
+    assert rep.converged and rep.kkt_residual < 1e-6, rep
+    dense = pkg.alm_solve(pkg.build_csvc_dual(A.toarray(), y, C), pkg.AlmOptions(tol_kkt=1e-6))
+    O.set_psi_mode("stable")
+    try:
+        op, c, bl = O.csvc_problem(A.toarray(), y, C)
+        ref = O.alm_solve(op, c, bl, O.AlmOpts(tol_kkt=1e-6))
+    finally:
+        O.set_psi_mode("reference")
+    assert rep.objective == pytest.approx(ref["objective"], rel=1e-6)
+    assert rep.objective == pytest.approx(dense.objective, rel=1e-6)
+    assert abs(float(y @ rep.x_opt)) <= 1e-9 * (1 + np.abs(rep.x_opt).sum())
