@@ -233,6 +233,8 @@ typedef struct ssnal_report_t {
   double op_seconds[SSNAL_NOPS];   /* device time per op class (profile = 1)         */
   long long op_calls[SSNAL_NOPS];
   double op_bytes[SSNAL_NOPS];     /* algorithmic HBM bytes per op class             */
+  long long cg_iters;              /* sparse operator: CG iterations, all Newton steps */
+  long long cg_fallbacks;          /* CG solves that fell back to the direct system     */
 } ssnal_report_t;
 
 /* per outer iteration: (k, R_KKT, sigma, p, inner iterations) as ref solver.py:474-475 */

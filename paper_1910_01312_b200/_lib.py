@@ -101,7 +101,8 @@ class Report(ctypes.Structure):
                 ("syncs", ctypes.c_longlong), ("newton_steps", ctypes.c_longlong),
                 ("projections", ctypes.c_longlong), ("launches", ctypes.c_longlong),
                 ("op_seconds", _D * NOPS), ("op_calls", ctypes.c_longlong * NOPS),
-                ("op_bytes", _D * NOPS)]
+                ("op_bytes", _D * NOPS), ("cg_iters", ctypes.c_longlong),
+                ("cg_fallbacks", ctypes.c_longlong)]
 
 
 PROGRESS_FN = ctypes.CFUNCTYPE(None, _I, _D, _D, ctypes.c_longlong, _I, _P)

@@ -52,40 +52,79 @@ __global__ void __launch_bounds__(SSNAL_NT) cg_ap_kernel(long long p,
   if (threadIdx.x == 0) cgs[CG_PAP] = acc[0];
 }
 
-// alpha = rz / pAp; y += alpha pv; r -= alpha Ap; rr = r.r; beta = rr / rz; rz = rr
+// alpha = rz / pAp; y += alpha pv; r -= alpha Ap; z = Dinv r (dinv NULL: z = r);
+// rz' = r.z; beta = rz' / rz; rz = rz'; rr = r.r
 __global__ void __launch_bounds__(SSNAL_NT) cg_step_kernel(long long p, double* __restrict__ y,
                                                            double* __restrict__ r,
                                                            const double* __restrict__ pv,
                                                            const double* __restrict__ Ap,
+                                                           const double* __restrict__ dinv,
+                                                           double* __restrict__ z,
                                                            double* cgs, double* part) {
-  __shared__ double red[32];
+  __shared__ double red[2 * 32];
   if (cgs[CG_DONE] != 0.0) return;
   const double pap = cgs[CG_PAP];
   const double alpha = pap > 0.0 ? cgs[CG_RZ] / pap : 0.0;
-  double acc[1] = {0.0};
+  double acc[2] = {0.0, 0.0};
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p;
        i += (long long)gridDim.x * blockDim.x) {
     y[i] = fma(alpha, pv[i], y[i]);
     const double ri = fma(-alpha, Ap[i], r[i]);
     r[i] = ri;
-    acc[0] = fma(ri, ri, acc[0]);
+    const double zi = dinv ? ri * dinv[i] : ri;
+    if (dinv) z[i] = zi;
+    acc[0] = fma(ri, zi, acc[0]);
+    acc[1] = fma(ri, ri, acc[1]);
   }
+  const int ops[2] = {0, 0};
+  block_reduce<2>(acc, ops, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = acc[0];
+    part[2 * blockIdx.x + 1] = acc[1];
+  }
+  if (!last_block_arrive(reinterpret_cast<unsigned int*>(cgs + CG_TICKET), gridDim.x)) return;
+  block_fold_partials<2>(part, gridDim.x, 2, ops, acc, red);
+  if (threadIdx.x == 0) {
+    const double rz = acc[0];
+    cgs[CG_BETA] = cgs[CG_RZ] > 0.0 ? rz / cgs[CG_RZ] : 0.0;
+    cgs[CG_RZ] = rz;
+    cgs[CG_RR] = acc[1];
+    cgs[CG_IT] += 1.0;
+    if (!(pap > 0.0) || !(rz > 0.0)) cgs[CG_DONE] = 1.0;  // exact solve / breakdown
+  }
+}
+
+// Stopping test of Algorithm 3 Step 1 on the TRUE Newton residual: with
+// t = -X^T s + sigma X_J^T P_J y and d = -s - sigma P~ X t, the residual is
+// (Q + sigma Q P~ Q) d + Q s = sigma^2 X X_J^T P Q_JJ P r_y; the caller passes
+// zn = X X_J^T P Q_JJ P r and scale = sigma^2: done when scale^2 ||zn||^2 <= cgs[TOL2].
+__global__ void __launch_bounds__(SSNAL_NT) cg_check_kernel(long long n, const double* __restrict__ zn,
+                                                            double sigma, double* cgs,
+                                                            double* part) {
+  __shared__ double red[32];
+  double acc[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    acc[0] = fma(zn[i], zn[i], acc[0]);
   const int ops[1] = {0};
   block_reduce<1>(acc, ops, red);
   if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
   if (!last_block_arrive(reinterpret_cast<unsigned int*>(cgs + CG_TICKET), gridDim.x)) return;
   block_fold_partials<1>(part, gridDim.x, 1, ops, acc, red);
   if (threadIdx.x == 0) {
-    const double rr = acc[0];
-    cgs[CG_BETA] = cgs[CG_RZ] > 0.0 ? rr / cgs[CG_RZ] : 0.0;
-    cgs[CG_RZ] = rr;
-    cgs[CG_RR] = rr;
-    cgs[CG_IT] += 1.0;
-    if (rr <= cgs[CG_TOL2] || !(pap > 0.0)) cgs[CG_DONE] = 1.0;
+    cgs[CG_RR] = sigma * sigma * acc[0];
+    if (cgs[CG_RR] <= cgs[CG_TOL2]) cgs[CG_DONE] = 1.0;
   }
 }
 
-// pv = r + beta pv (skipped once converged)
+cudaError_t launch_cg_check(long long n, const double* zn, double sigma, double* cgs, double* part,
+                            cudaStream_t s) {
+  note_launch();
+  cg_check_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, s>>>(n, zn, sigma, cgs, part);
+  return cudaGetLastError();
+}
+
+// pv = z + beta pv (z = r unpreconditioned; skipped once converged)
 __global__ void cg_dir_kernel(long long p, const double* __restrict__ r, double* __restrict__ pv,
                               const double* cgs) {
   if (cgs[CG_DONE] != 0.0) return;
@@ -95,38 +134,64 @@ __global__ void cg_dir_kernel(long long p, const double* __restrict__ r, double*
     pv[i] = fma(beta, pv[i], r[i]);
 }
 
-// y = 0, r = pv = b, rz = b.b, done = (rz <= tol^2) with the reference's CG target
-// tol = min(eta, ||grad||^(1+tau)) / sigma computed from the device ||grad||^2
+// y = 0, r = b, pv = z = Dinv b (dinv NULL: z = b), rz = b.z, done = (b == 0); the
+// target tol = min(eta, ||grad||^(1+tau)) is computed from the device ||grad||^2
 __global__ void __launch_bounds__(SSNAL_NT) cg_init_kernel(long long p, const double* __restrict__ b,
                                                            double* __restrict__ y,
                                                            double* __restrict__ r,
                                                            double* __restrict__ pv,
+                                                           const double* __restrict__ dinv,
                                                            const double* g2, double eta,
-                                                           double tau, double sigma,
-                                                           double* cgs, double* part) {
-  const double tol = fmin(eta, pow(sqrt(*g2), 1.0 + tau)) / sigma;
+                                                           double tau, double* cgs, double* part) {
+  const double tol = fmin(eta, pow(sqrt(*g2), 1.0 + tau));
   const double tol2 = tol * tol;
-  __shared__ double red[32];
-  double acc[1] = {0.0};
+  __shared__ double red[2 * 32];
+  double acc[2] = {0.0, 0.0};
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p;
        i += (long long)gridDim.x * blockDim.x) {
+    const double bi = b[i];
+    const double zi = dinv ? bi * dinv[i] : bi;
     y[i] = 0.0;
-    r[i] = b[i];
-    pv[i] = b[i];
-    acc[0] = fma(b[i], b[i], acc[0]);
+    r[i] = bi;
+    pv[i] = zi;
+    acc[0] = fma(bi, zi, acc[0]);
+    acc[1] = fma(bi, bi, acc[1]);
   }
-  const int ops[1] = {0};
-  block_reduce<1>(acc, ops, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  const int ops[2] = {0, 0};
+  block_reduce<2>(acc, ops, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = acc[0];
+    part[2 * blockIdx.x + 1] = acc[1];
+  }
   if (!last_block_arrive(reinterpret_cast<unsigned int*>(cgs + CG_TICKET), gridDim.x)) return;
-  block_fold_partials<1>(part, gridDim.x, 1, ops, acc, red);
+  block_fold_partials<2>(part, gridDim.x, 2, ops, acc, red);
   if (threadIdx.x == 0) {
     cgs[CG_RZ] = acc[0];
-    cgs[CG_RR] = acc[0];
+    cgs[CG_RR] = acc[1];
     cgs[CG_TOL2] = tol2;
     cgs[CG_IT] = 0.0;
-    cgs[CG_DONE] = acc[0] <= tol2 ? 1.0 : 0.0;
+    cgs[CG_DONE] = acc[1] > 0.0 ? 0.0 : 1.0;  // b = 0: y = 0 is exact
   }
+}
+
+// Jacobi preconditioner of the factor-space system I + sigma X_J^T P X_J:
+// dinv_k = 1 / (1 + sigma (sum_{i in J} x_ik^2 - u_k^2 / a'a)),  u = X_J^T a_J
+__global__ void cg_jacobi_kernel(long long q, const double* __restrict__ colsq,
+                                 const double* __restrict__ u, double asa, double sigma,
+                                 double* __restrict__ dinv) {
+  const double inv = asa != 0.0 ? 1.0 / asa : 0.0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < q;
+       k += (long long)gridDim.x * blockDim.x) {
+    const double d = 1.0 + sigma * fmax(colsq[k] - inv * u[k] * u[k], 0.0);
+    dinv[k] = 1.0 / d;
+  }
+}
+
+cudaError_t launch_cg_jacobi(long long q, const double* colsq, const double* u, double asa,
+                             double sigma, double* dinv, cudaStream_t s) {
+  note_launch();
+  cg_jacobi_kernel<<<stream_blocks(q, 4), SSNAL_NT, 0, s>>>(q, colsq, u, asa, sigma, dinv);
+  return cudaGetLastError();
 }
 
 __global__ void scatter_zero_kernel(const int32_t* __restrict__ rows, long long p,
@@ -138,10 +203,10 @@ __global__ void scatter_zero_kernel(const int32_t* __restrict__ rows, long long 
 static int cg_blocks(long long p) { return stream_blocks(p, 4); }
 
 cudaError_t launch_cg_init(long long p, const double* b, double* y, double* r, double* pv,
-                           const double* g2, double eta, double tau, double sigma, double* cgs,
-                           double* part, cudaStream_t s) {
+                           const double* dinv, const double* g2, double eta, double tau,
+                           double* cgs, double* part, cudaStream_t s) {
   note_launch();
-  cg_init_kernel<<<cg_blocks(p), SSNAL_NT, 0, s>>>(p, b, y, r, pv, g2, eta, tau, sigma, cgs, part);
+  cg_init_kernel<<<cg_blocks(p), SSNAL_NT, 0, s>>>(p, b, y, r, pv, dinv, g2, eta, tau, cgs, part);
   return cudaGetLastError();
 }
 
@@ -161,9 +226,10 @@ cudaError_t launch_cg_ap(long long p, const double* pv, const double* zq, const 
 }
 
 cudaError_t launch_cg_step(long long p, double* y, double* r, const double* pv, const double* Ap,
-                           double* cgs, double* part, cudaStream_t s) {
+                           const double* dinv, double* z, double* cgs, double* part,
+                           cudaStream_t s) {
   note_launch();
-  cg_step_kernel<<<cg_blocks(p), SSNAL_NT, 0, s>>>(p, y, r, pv, Ap, cgs, part);
+  cg_step_kernel<<<cg_blocks(p), SSNAL_NT, 0, s>>>(p, y, r, pv, Ap, dinv, z, cgs, part);
   return cudaGetLastError();
 }
 

@@ -10,6 +10,8 @@
 // direction inner products + the unit-step Armijo trial, enqueued together).
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -52,18 +54,41 @@ cudaError_t launch_pspace_direction(const double* A, long long n, long long q, l
                                     cudaStream_t stream);
 
 cudaError_t launch_cg_init(long long p, const double* b, double* y, double* r, double* pv,
-                           const double* g2, double eta, double tau, double sigma, double* cgs,
-                           double* part, cudaStream_t s);
+                           const double* dinv, const double* g2, double eta, double tau,
+                           double* cgs, double* part, cudaStream_t s);
+cudaError_t launch_cg_jacobi(long long q, const double* colsq, const double* u, double asa,
+                             double sigma, double* dinv, cudaStream_t s);
+cudaError_t launch_csc_colsq(const CsrOp& op, const uint8_t* keep, double* out, double* part,
+                             cudaStream_t s);
 cudaError_t launch_cg_project(long long p, const double* x, const double* aJ, const double* dot,
                               double asa, double* out, cudaStream_t s);
 cudaError_t launch_cg_ap(long long p, const double* pv, const double* zq, const double* aJ,
                          double asa, double sigma, double* Ap, double* cgs, double* part,
                          cudaStream_t s);
 cudaError_t launch_cg_step(long long p, double* y, double* r, const double* pv, const double* Ap,
-                           double* cgs, double* part, cudaStream_t s);
+                           const double* dinv, double* z, double* cgs, double* part,
+                           cudaStream_t s);
 cudaError_t launch_cg_dir(long long p, const double* r, double* pv, const double* cgs,
                           cudaStream_t s);
 cudaError_t launch_scatter_zero(const int32_t* rows, long long p, double* dst, cudaStream_t s);
+cudaError_t launch_cg_check(long long n, const double* zn, double sigma, double* cgs, double* part,
+                            cudaStream_t s);
+cudaError_t launch_sparse_gram_rows(const CsrOp& op, const int32_t* rows, long long p, double* G,
+                                    cudaStream_t s);
+cudaError_t launch_sparse_gram_cols(const CsrOp& op, const uint8_t* free_rows, double* G,
+                                    cudaStream_t s);
+cudaError_t launch_qspace_assemble(long long m, const double* u, double asa, double sigma,
+                                   double* G, cudaStream_t s);
+cudaError_t launch_pspace_solve(const int32_t* J, long long p, const double* grad, const double* a,
+                                double sigma, double asa, double* Q, double* vecs, double* y,
+                                int* info, cudaStream_t s);
+
+// direct reduced systems of the sparse operator: min(p, q) up to this size (M buffer)
+constexpr long long SPARSE_DIRECT_MAX = 2048;
+// forcing-term cap of the matrix-free CG route (see cg_direction)
+constexpr double SPARSE_CG_ETA = 1e-4;
+// max / mean column sum of squares above which the factor-space Jacobi PCG is used
+constexpr double HOT_COLUMN_SPREAD = 50.0;
 
 namespace {
 
@@ -116,10 +141,10 @@ struct Layout {
   void *ws_proj, *ws_red, *ws_xt, *ws_gram, *ws_cmp, *ws_ps;
   // sparse operator: sample-space CG buffers, scattered vector, CSC partial slots
   double *ys, *tq, *cg_gJ, *cg_aJ, *cg_b, *cg_y, *cg_r, *cg_pv, *cg_Ap, *cg_zq, *cg_w, *cgs,
-      *cg_part, *csc_part;
+      *cg_part, *csc_part, *cg_d, *cg_u, *cg_z;
 };
 
-size_t cg_part_doubles(long long n) { return (size_t)stream_blocks(n, 4) + 8; }
+size_t cg_part_doubles(long long n) { return 2 * (size_t)stream_blocks(n, 4) + 8; }
 
 Layout carve(char* base, long long n, long long n_phys, long long q, size_t* total,
              const ssnal_csr_operator_t* csr = nullptr) {
@@ -172,9 +197,15 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
     L.cg_Ap = cv.take<double>(n);
     L.cg_zq = cv.take<double>(n);
     L.cg_w = cv.take<double>(n);
+    L.cg_d = cv.take<double>(q);
+    L.cg_u = cv.take<double>(q);
+    L.cg_z = cv.take<double>(q);
     L.cgs = cv.take<double>(16);
     L.cg_part = cv.take<double>(cg_part_doubles(n));
     L.csc_part = cv.take<double>(csr->nslots > 0 ? csr->nslots : 1);
+    const long long md = std::min<long long>(SPARSE_DIRECT_MAX, std::max(q, n));
+    L.M = cv.take<double>((size_t)md * md);
+    L.ws_ps = cv.take<double>(4 * (size_t)md);
   }
   *total = cv.off + 256;
   return L;
@@ -213,7 +244,7 @@ struct Driver {
   cudaStream_t S;
   Layout L;
   Pinned* H;
-  long long syncs = 0, newton = 0, projections = 0, cg_iters = 0;
+  long long syncs = 0, newton = 0, projections = 0, cg_iters = 0, cg_fallbacks = 0;
   double lam_kkt = 0.0, lam_cur = 0.0;
   double sigma = 1.0;
   double c_norm = 0.0;
@@ -246,41 +277,172 @@ struct Driver {
     return 8.0 * P.n_phys * P.q + (P.row_sign ? 8.0 * P.n_phys : 0.0);
   }
 
-  // sample-space CG for the sparse operator: t = -X^T s + sigma X_J^T P_J y
-  void cg_direction(long long p, double asa, const double* g2_dev) {
+  void cg_report(long long p) {
+    cg_iters += (long long)H->cg[6];
+    if (std::getenv("SSNAL_DEBUG_CG"))
+      std::fprintf(stderr, "cg p=%lld sigma=%.3g it=%d |r|=%.3e |res|=%.3e tol=%.3e done=%g\n", p,
+                   sigma, (int)H->cg[6], std::sqrt(H->cg[0]), std::sqrt(H->cg[3]),
+                   std::sqrt(H->cg[4]), H->cg[5]);
+  }
+
+  // Factor-space Jacobi-preconditioned CG for p >= q (Zipf-hot columns make the
+  // sample-space spectrum spread; column scaling flattens it):
+  //   (I_q + sigma X_J^T P_J X_J) t = -X^T s,  D = diag(.)  (ref solver.py:151-172 role)
+  // Newton residual of d = -s - sigma P~ X t:  sigma X X_J^T P_J X_J r_t.
+  bool cg_direction_q(long long p, double asa, const double* g2_dev, int max_it) {
     const CsrOp& op = *P.csr;
-    ck(launch_gather(L.J, p, L.grad, L.cg_gJ, S));
+    const long long q = P.q;
     ck(launch_gather(L.J, p, P.a, L.cg_aJ, S));
-    dots({{L.cg_aJ, L.cg_gJ}}, L.cgs + 7, p);
-    ck(launch_cg_project(p, L.cg_gJ, L.cg_aJ, L.cgs + 7, asa, L.cg_b, S));
-    // reference target min(eta, ||grad||^(1+tau)) on the Newton residual (ref solver.py:229);
-    // the sample-space residual maps to it through sigma X Z^T P: scaled by 1/sigma
-    ck(launch_cg_init(p, L.cg_b, L.cg_y, L.cg_r, L.cg_pv, g2_dev, O.eta, O.tau, sigma, L.cgs,
-                      L.cg_part, S));
-    for (int it = 0; it < O.cg_max_iters;) {
-      for (int b = 0; b < CG_BATCH && it < O.cg_max_iters; ++b, ++it) {
-        ck(launch_scatter(L.J, p, L.cg_pv, L.ys, S));
-        ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
-        ck(launch_csr_xd(op, L.J, p, L.tq, L.cg_zq, S));
-        dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
-        ck(launch_cg_ap(p, L.cg_pv, L.cg_zq, L.cg_aJ, asa, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
-        ck(launch_cg_step(p, L.cg_y, L.cg_r, L.cg_pv, L.cg_Ap, L.cgs, L.cg_part, S));
-        ck(launch_cg_dir(p, L.cg_r, L.cg_pv, L.cgs, S));
+    ck(launch_scatter(L.J, p, L.cg_aJ, L.ys, S));
+    ck(launch_csc_xt(op, L.ys, L.cg_u, L.csc_part, S));  // u = X_J^T a_J
+    ck(launch_scatter_zero(L.J, p, L.ys, S));
+    ck(launch_csc_colsq(op, L.fr, L.cg_d, L.csc_part, S));
+    ck(launch_cg_jacobi(q, L.cg_d, L.cg_u, asa, sigma, L.cg_d, S));
+    ck(launch_vec(4, q, -1.0, L.gr, nullptr, nullptr, L.cg_b, S));
+    ck(launch_cg_init(q, L.cg_b, L.cg_y, L.cg_r, L.cg_pv, L.cg_d, g2_dev,
+                      std::min(O.eta, SPARSE_CG_ETA), O.tau, L.cgs, L.cg_part, S));
+    // v (q) -> out (q) = sigma-free part X_J^T P X_J v, via zq (p) and ys (n)
+    auto gram_apply = [&](const double* v, double* out) {
+      ck(launch_csr_xd(op, L.J, p, v, L.cg_zq, S));
+      dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
+      ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
+      ck(launch_scatter(L.J, p, L.cg_w, L.ys, S));
+      ck(launch_csc_xt(op, L.ys, out, L.csc_part, S));
+      ck(launch_scatter_zero(L.J, p, L.ys, S));
+    };
+    for (int it = 0; it < max_it;) {
+      for (int b = 0; b < CG_BATCH && it < max_it; ++b, ++it) {
+        gram_apply(L.cg_pv, L.tq);
+        ck(launch_cg_ap(q, L.cg_pv, L.tq, L.tq, 0.0, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
+        ck(launch_cg_step(q, L.cg_y, L.cg_r, L.cg_pv, L.cg_Ap, L.cg_d, L.cg_z, L.cgs, L.cg_part,
+                          S));
+        ck(launch_cg_dir(q, L.cg_z, L.cg_pv, L.cgs, S));
       }
+      gram_apply(L.cg_r, L.tq);
+      ck(launch_csr_xd(op, nullptr, P.n_phys, L.tq, L.tmp, S));
+      ck(launch_cg_check(P.n, L.tmp, sigma, L.cgs, L.cg_part, S));
       ck(cudaMemcpyAsync(H->cg, L.cgs, sizeof(double) * 8, cudaMemcpyDeviceToHost, S));
       ck(cudaStreamSynchronize(S));
       ++syncs;
       if (H->cg[5] != 0.0) break;
     }
-    cg_iters += (long long)H->cg[6];
+    cg_report(p);
+    ck(cudaMemcpyAsync(L.t, L.cg_y, sizeof(double) * q, cudaMemcpyDeviceToDevice, S));
+    return H->cg[5] != 0.0;
+  }
+
+  // sample-space CG for the sparse operator: t = -X^T s + sigma X_J^T P_J y
+  bool cg_direction(long long p, double asa, const double* g2_dev, int max_it) {
+    const CsrOp& op = *P.csr;
+    ck(launch_gather(L.J, p, L.grad, L.cg_gJ, S));
+    ck(launch_gather(L.J, p, P.a, L.cg_aJ, S));
+    dots({{L.cg_aJ, L.cg_gJ}}, L.cgs + 7, p);
+    ck(launch_cg_project(p, L.cg_gJ, L.cg_aJ, L.cgs + 7, asa, L.cg_b, S));
+    // target min(eta, ||grad||^(1+tau)) (ref solver.py:229) on the TRUE Newton residual,
+    // eta capped at SPARSE_CG_ETA: the reference falls back to an exact solve when its CG
+    // stalls; the matrix-free path instead solves tighter from the start
+    ck(launch_cg_init(p, L.cg_b, L.cg_y, L.cg_r, L.cg_pv, nullptr, g2_dev,
+                      std::min(O.eta, SPARSE_CG_ETA), O.tau, L.cgs, L.cg_part, S));
+    for (int it = 0; it < max_it;) {
+      for (int b = 0; b < CG_BATCH && it < max_it; ++b, ++it) {
+        ck(launch_scatter(L.J, p, L.cg_pv, L.ys, S));
+        ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
+        ck(launch_csr_xd(op, L.J, p, L.tq, L.cg_zq, S));
+        dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
+        ck(launch_cg_ap(p, L.cg_pv, L.cg_zq, L.cg_aJ, asa, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
+        ck(launch_cg_step(p, L.cg_y, L.cg_r, L.cg_pv, L.cg_Ap, nullptr, nullptr, L.cgs, L.cg_part,
+                          S));
+        ck(launch_cg_dir(p, L.cg_r, L.cg_pv, L.cgs, S));
+      }
+      // Newton residual of the direction built from y (Algorithm 3 Step 1 test):
+      // (Q + sigma Q P~ Q) d + Q s = sigma^2 X X_J^T P Q_JJ P r
+      dots({{L.cg_aJ, L.cg_r}}, L.cgs + 7, p);
+      ck(launch_cg_project(p, L.cg_r, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
+      ck(launch_scatter(L.J, p, L.cg_w, L.ys, S));
+      ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
+      ck(launch_scatter_zero(L.J, p, L.ys, S));
+      ck(launch_csr_xd(op, L.J, p, L.tq, L.cg_zq, S));
+      dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
+      ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
+      ck(launch_scatter(L.J, p, L.cg_w, L.ys, S));
+      ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
+      ck(launch_scatter_zero(L.J, p, L.ys, S));
+      ck(launch_csr_xd(op, nullptr, P.n_phys, L.tq, L.tmp, S));
+      ck(launch_cg_check(P.n, L.tmp, sigma * sigma, L.cgs, L.cg_part, S));
+      ck(cudaMemcpyAsync(H->cg, L.cgs, sizeof(double) * 8, cudaMemcpyDeviceToHost, S));
+      ck(cudaStreamSynchronize(S));
+      ++syncs;
+      if (H->cg[5] != 0.0) break;
+    }
+    cg_report(p);
     // w = P_J y, t = -g_r + sigma X^T scatter(w)
     dots({{L.cg_aJ, L.cg_y}}, L.cgs + 7, p);
     ck(launch_cg_project(p, L.cg_y, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
-    ck(launch_scatter(L.J, p, L.cg_w, L.ys, S));
-    ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
+    sparse_t_from_sample(L.cg_w, p);
+    return H->cg[5] != 0.0;
+  }
+
+  // Column-popularity spread of A (max / mean column sum of squares), once per solve:
+  // a large spread (Zipf-hot columns) selects the Jacobi-preconditioned factor-space
+  // CG even when p < q.
+  bool hot_columns() {
+    if (col_spread < 0.0) {
+      ck(cudaMemsetAsync(L.tfree, 1, P.n, S));
+      ck(launch_csc_colsq(*P.csr, L.tfree, L.cg_d, L.csc_part, S));
+      std::vector<double> cs(P.q);
+      ck(cudaMemcpyAsync(cs.data(), L.cg_d, sizeof(double) * P.q, cudaMemcpyDeviceToHost, S));
+      ck(cudaStreamSynchronize(S));
+      double mx = 0.0, sum = 0.0;
+      for (double v : cs) { mx = std::max(mx, v); sum += v; }
+      col_spread = sum > 0.0 ? mx / (sum / P.q) : 1.0;
+    }
+    return col_spread > HOT_COLUMN_SPREAD;
+  }
+  double col_spread = -1.0;
+
+  // matrix-free reduced Newton solve; on CG failure fall back to the direct system
+  // when it fits (ref solver.py:251-255), else keep iterating up to 4x the budget
+  void sparse_iterative(long long p, double asa, const double* g2_dev) {
+    const bool can_direct = std::min<long long>(p, P.q) <= SPARSE_DIRECT_MAX;
+    const int max_it = can_direct ? O.cg_max_iters : 4 * O.cg_max_iters;
+    const bool ok = (p < P.q && !hot_columns()) ? cg_direction(p, asa, g2_dev, max_it)
+                                                : cg_direction_q(p, asa, g2_dev, max_it);
+    if (!ok && can_direct) {
+      ++cg_fallbacks;
+      sparse_direct(p, asa);
+    }
+  }
+
+  // t = -g_r + sigma X_J^T w  for a sample-space w (p, already in range(P_J))
+  void sparse_t_from_sample(const double* w, long long p) {
+    ck(launch_scatter(L.J, p, w, L.ys, S));
+    ck(launch_csc_xt(*P.csr, L.ys, L.tq, L.csc_part, S));
     ck(launch_scatter_zero(L.J, p, L.ys, S));
     ck(launch_vec(4, P.q, sigma, L.tq, nullptr, nullptr, L.t, S));  // sigma X^T P_J y
     ck(launch_vec(3, P.q, 0.0, L.t, L.gr, nullptr, L.t, S));       // - X^T s
+  }
+
+  // direct reduced systems for the sparse operator (ref solver.py:238-246):
+  //   p < q : Q_JJ by sparse row merges, (I + sigma P Q_JJ P) y = P g_J, t from y;
+  //   p >= q: X_J^T X_J by masked column merges, (I + sigma X_J^T P X_J) t = -X^T s.
+  void sparse_direct(long long p, double asa) {
+    const CsrOp& op = *P.csr;
+    if (p < P.q) {
+      ck(launch_sparse_gram_rows(op, L.J, p, L.M, S));
+      double* y = (double*)L.ws_ps + 3 * p;
+      ck(launch_pspace_solve(L.J, p, L.grad, P.a, sigma, asa, L.M, (double*)L.ws_ps, y, L.info,
+                             S));
+      sparse_t_from_sample(y, p);
+      return;
+    }
+    ck(launch_sparse_gram_cols(op, L.fr, L.M, S));
+    // u = X_J^T a_J (the rank-one correction's factor vector)
+    ck(launch_gather(L.J, p, P.a, L.cg_aJ, S));
+    ck(launch_scatter(L.J, p, L.cg_aJ, L.ys, S));
+    ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
+    ck(launch_scatter_zero(L.J, p, L.ys, S));
+    ck(launch_qspace_assemble(P.q, L.tq, asa, sigma, L.M, S));
+    ck(launch_chol_solve(L.M, P.q, L.gr, -1.0, L.t, L.info, S));
   }
 
   // ---------------------------------------------------------------- plumbing
@@ -421,15 +583,23 @@ struct Driver {
       dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}, {L.s, L.grad}}, L.scal, P.n);
       return;
     }
-    if (P.csr) {  // matrix-free sample-space CG (q is large for sparse data)
+    if (P.csr) {  // direct when min(p, q) is small, else matrix-free sample-space CG
+      const long long lim = std::min<long long>(O.direct_solve_threshold, SPARSE_DIRECT_MAX);
       timed(SSNAL_OP_NEWTON, 0.0, [&] {
         ck(launch_compact(L.fr, P.n, L.J, L.pcount, L.ws_cmp, S));
-        cg_direction(p, asa, g2_dev);
+        if (std::min<long long>(p, P.q) <= lim) sparse_direct(p, asa);
+        else sparse_iterative(p, asa, g2_dev);
       });
       xd(L.t, L.qdir, 1);
       timed(SSNAL_OP_VEC, 8.0 * P.n * 5, [&] {
         ck(launch_hs_apply(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.ws_red, S));
       });
+      if (std::min<long long>(p, P.q) > lim) {
+        // inexact y: X t is not Q d.  Recompute the exact image (t = X^T d, Qd = X t)
+        // so Qw stays Q w along the iterates and psi / the Armijo test are exact.
+        xt({L.dir}, L.t);
+        xd(L.t, L.qdir, 1);
+      }
       dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}}, L.scal, P.n);
       dots({{L.t, nullptr}}, L.scal + 3, P.q);
       return;
@@ -542,6 +712,7 @@ struct Driver {
   // returns inner iterations; sets flags; leaves Pi(u) in L.xp and its record in cur
   int ssn_solve(double eps_k, double delta_k, bool& converged, bool& hit_max, ProjState& cur) {
     const double coeff = std::sqrt(O.lambda_min_surrogate / sigma);
+    const bool dbg = std::getenv("SSNAL_DEBUG_CG") != nullptr;
     const double floor_ = 1e-12 * (1.0 + c_norm);
     // start: u = x - sigma (Qw + c), Pi(u), s, grad
     vec(0, -sigma, L.x, L.qw, P.c, L.u);
@@ -617,6 +788,10 @@ struct Driver {
           break;
         }
       }
+      if (dbg)
+        std::fprintf(stderr, "ssn it=%d |g|=%.3e eps=%.3e dist=%.3e alpha=%.3g steep=%d p=%lld\n",
+                     it, gnorm, coeff * eps_k, coeff * delta_k * dist, alpha, (int)steepest_dir,
+                     (long long)cur.nfree);
       accept(alpha, j);
       cur = rec;
       ++its;
@@ -701,6 +876,8 @@ struct Driver {
     rep->syncs = syncs;
     rep->newton_steps = newton;
     rep->projections = projections;
+    rep->cg_iters = cg_iters;
+    rep->cg_fallbacks = cg_fallbacks;
     for (int k = 0; k < SSNAL_NOPS; ++k) {
       rep->op_calls[k] = op_calls[k];
       rep->op_bytes[k] = op_bytes[k];

@@ -217,6 +217,21 @@ size_t pspace_ws_bytes(long long p, long long q) {
   return (size_t)((gram_ksplit(p, q) + 1) * p * p + 4 * p + GX_SPLIT * q + 64) * sizeof(double);
 }
 
+// Given Q_JJ (p x p, overwritten): y = P_J (I + sigma P_J Q_JJ P_J)^{-1} P_J grad_J.
+// vecs: 4p doubles (aJ, qa, b, scratch).  Used by the sparse operator's direct route.
+cudaError_t launch_pspace_solve(const int32_t* J, long long p, const double* grad, const double* a,
+                                double sigma, double asa, double* Q, double* vecs, double* y,
+                                int* info, cudaStream_t stream) {
+  double* aJ = vecs;
+  double* qa = aJ + p;
+  double* b = qa + p;
+  { note_launch(); pspace_assemble_kernel<<<1, 1024, 0, stream>>>(J, p, grad, a, sigma, asa, Q, aJ, qa, b); }
+  cudaError_t e = launch_chol_solve(Q, p, b, 1.0, y, info, stream);
+  if (e != cudaSuccess) return e;
+  { note_launch(); pspace_project_kernel<<<1, 1024, 0, stream>>>(p, aJ, asa, y); }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pspace_direction(const double* A, long long n, long long q, long long lda,
                                     const double* rs, int svr, const int32_t* J, long long p,
                                     const double* grad, const double* a, double sigma, double asa,

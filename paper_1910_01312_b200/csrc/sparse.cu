@@ -67,6 +67,35 @@ __global__ void __launch_bounds__(256) csc_xt_kernel(const int64_t* __restrict__
   }
 }
 
+// masked column sums of squares on the same segment plan:
+//   out[k] = sum_{i : keep[i]} A_ik^2  (the Jacobi diagonal of X_J^T X_J)
+__global__ void __launch_bounds__(256) csc_colsq_kernel(const int64_t* __restrict__ seg_beg,
+                                                        const int64_t* __restrict__ seg_end,
+                                                        const int32_t* __restrict__ seg_col,
+                                                        const int32_t* __restrict__ seg_slot,
+                                                        long long nseg,
+                                                        const int32_t* __restrict__ rowidx,
+                                                        const double* __restrict__ valt,
+                                                        const uint8_t* __restrict__ keep,
+                                                        double* __restrict__ out,
+                                                        double* __restrict__ part) {
+  const long long s = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nseg) return;
+  const long long k0 = seg_beg[s], k1 = seg_end[s];
+  double acc = 0.0;
+  for (long long k = k0 + lane; k < k1; k += 32) {
+    const double v = valt[k];
+    if (keep[rowidx[k]]) acc = fma(v, v, acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    const int slot = seg_slot[s];
+    if (slot < 0) out[seg_col[s]] = acc;
+    else part[slot] = acc;
+  }
+}
+
 // split columns: out[col] = sum of its partial slots [pbeg, pend) in order
 __global__ void csc_fold_kernel(const int32_t* __restrict__ fold_col,
                                 const int32_t* __restrict__ fold_beg, long long nfold,
@@ -99,6 +128,79 @@ __global__ void gather_kernel(const int32_t* __restrict__ rows, long long p,
   if (r < p) dst[r] = src[rows[r]];
 }
 
+// Gram of m selected sparse vectors (CSR rows or CSC columns, sorted indices):
+//   G[r][c] = s_r s_c sum_{k in idx_r cap idx_c, keep[k]} val_r[k] val_c[k]
+// one thread per (r, c >= r) pair merging the two sorted index lists (fixed order,
+// deterministic), mirrored into the lower triangle.  Used for the direct reduced
+// Newton systems of the sparse operator when min(p, q) is small (the p x p Q_JJ
+// of ref solver.py:224-246, or the q x q X_J^T X_J factor-space Gram).
+static constexpr int GT = 16;
+__global__ void __launch_bounds__(GT * GT) sparse_gram_kernel(
+    const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+    const double* __restrict__ val, const int32_t* __restrict__ sel, long long m,
+    const uint8_t* __restrict__ keep, const double* __restrict__ sign, double* __restrict__ G) {
+  const long long r = (long long)blockIdx.y * GT + threadIdx.y;
+  const long long c = (long long)blockIdx.x * GT + threadIdx.x;
+  if (blockIdx.x < blockIdx.y || r >= m || c >= m || c < r) return;
+  const long long vr = sel ? (long long)sel[r] : r, vc = sel ? (long long)sel[c] : c;
+  long long i = ptr[vr], j = ptr[vc];
+  const long long ie = ptr[vr + 1], je = ptr[vc + 1];
+  double s = 0.0;
+  while (i < ie && j < je) {
+    const int a = idx[i], b = idx[j];
+    if (a == b) {
+      if (!keep || keep[a]) s = fma(val[i], val[j], s);
+      ++i;
+      ++j;
+    } else if (a < b) {
+      ++i;
+    } else {
+      ++j;
+    }
+  }
+  if (sign) s *= sign[vr] * sign[vc];
+  G[r * m + c] = s;
+  G[c * m + r] = s;
+}
+
+cudaError_t launch_sparse_gram_rows(const CsrOp& op, const int32_t* rows, long long p, double* G,
+                                    cudaStream_t stream) {
+  const unsigned nt = (unsigned)ceil_div(p, (long long)GT);
+  note_launch();
+  sparse_gram_kernel<<<dim3(nt, nt), dim3(GT, GT), 0, stream>>>(
+      op.indptr, op.indices, op.values, rows, p, nullptr, op.row_sign, G);
+  return cudaGetLastError();
+}
+
+// X_J^T X_J over the CSC columns keeping rows with free[row] != 0 (row signs square away)
+cudaError_t launch_sparse_gram_cols(const CsrOp& op, const uint8_t* free_rows, double* G,
+                                    cudaStream_t stream) {
+  const unsigned nt = (unsigned)ceil_div(op.q, (long long)GT);
+  note_launch();
+  sparse_gram_kernel<<<dim3(nt, nt), dim3(GT, GT), 0, stream>>>(
+      op.colptr, op.rowidx, op.valt, nullptr, op.q, free_rows, nullptr, G);
+  return cudaGetLastError();
+}
+
+// M = I + sigma (G - u u^T / asa)  in place  (asa == 0: M = I + sigma G)
+__global__ void qspace_assemble_kernel(long long m, const double* __restrict__ u, double asa,
+                                       double sigma, double* __restrict__ G) {
+  const double inv = asa != 0.0 ? 1.0 / asa : 0.0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m * m;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long r = k / m, c = k % m;
+    G[k] = (r == c ? 1.0 : 0.0) + sigma * (G[k] - inv * u[r] * u[c]);
+  }
+}
+
+cudaError_t launch_qspace_assemble(long long m, const double* u, double asa, double sigma,
+                                   double* G, cudaStream_t stream) {
+  note_launch();
+  qspace_assemble_kernel<<<(unsigned)min(ceil_div(m * m, 256LL), 4096LL), 256, 0, stream>>>(
+      m, u, asa, sigma, G);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_csr_xd(const CsrOp& op, const int32_t* rows, long long nrows, const double* d,
                           double* out, cudaStream_t stream) {
   const long long threads = nrows * SUB;
@@ -114,6 +216,20 @@ cudaError_t launch_csc_xt(const CsrOp& op, const double* v, double* out, double*
   csc_xt_kernel<<<(unsigned)ceil_div(op.nseg * 32, 256LL), 256, 0, stream>>>(
       op.seg_beg, op.seg_end, op.seg_col, op.seg_slot, op.nseg, op.rowidx, op.valt, op.row_sign,
       v, out, part);
+  if (op.nfold > 0) {
+    note_launch();
+    csc_fold_kernel<<<(unsigned)ceil_div(op.nfold, 256LL), 256, 0, stream>>>(
+        op.fold_col, op.fold_beg, op.nfold, part, out);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csc_colsq(const CsrOp& op, const uint8_t* keep, double* out, double* part,
+                             cudaStream_t stream) {
+  note_launch();
+  csc_colsq_kernel<<<(unsigned)ceil_div(op.nseg * 32, 256LL), 256, 0, stream>>>(
+      op.seg_beg, op.seg_end, op.seg_col, op.seg_slot, op.nseg, op.rowidx, op.valt, keep, out,
+      part);
   if (op.nfold > 0) {
     note_launch();
     csc_fold_kernel<<<(unsigned)ceil_div(op.nfold, 256LL), 256, 0, stream>>>(

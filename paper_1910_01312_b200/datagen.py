@@ -52,27 +52,50 @@ def _distinct_uniform_cols(rng, n, q, k):
     return cols
 
 
+def _zipf_ranks(rng, shape, s, q, head=4096):
+    """0-based ranks from Zipf(s) on [1, q] by inverse CDF: exact table for the
+    ``head`` most popular ranks, midpoint-integral approximation of the tail mass
+    (relative pmf error < 1e-6 past rank 4096)."""
+    h = min(head, q)
+    pmf = np.arange(1, h + 1, dtype=np.float64) ** (-s)
+    lo = h + 0.5
+    tail = (lo ** (1 - s) - (q + 0.5) ** (1 - s)) / (s - 1) if q > h else 0.0
+    z = pmf.sum() + tail
+    cdf = np.cumsum(pmf) / z
+    u = rng.random(shape)
+    out = np.searchsorted(cdf, u)  # < h: head rank
+    t = out >= h
+    if t.any():
+        m = (u[t] - cdf[-1]) * z * (s - 1)
+        r = np.ceil((lo ** (1 - s) - m) ** (1.0 / (1 - s)) - 0.5)
+        out[t] = np.clip(r, h + 1, q).astype(np.int64) - 1
+    return np.minimum(out, q - 1)
+
+
 def _distinct_zipf_cols(rng, n, q, k, s=1.1):
     """Columns drawn with Zipf(s) popularity over a random column permutation."""
-    ranks = np.arange(1, q + 1, dtype=np.float64)
-    pmf = ranks ** (-s)
-    cdf = np.cumsum(pmf)
-    cdf /= cdf[-1]
     perm = rng.permutation(q)
     out = np.empty((n, k), dtype=np.int64)
     chunk = 1 << 16
     for start in range(0, n, chunk):
         stop = min(start + chunk, n)
         m = stop - start
-        draw = np.searchsorted(cdf, rng.random((m, 3 * k)))
-        block = perm[np.minimum(draw, q - 1)]
-        for r in range(m):
+        block = np.sort(perm[_zipf_ranks(rng, (m, 3 * k), s, q)], axis=1)
+        dup = np.zeros(block.shape, dtype=bool)
+        dup[:, 1:] = block[:, 1:] == block[:, :-1]
+        # keep k distinct candidates per row chosen uniformly: random keys, duplicates last
+        keys = rng.random(block.shape)
+        keys[dup] = 2.0
+        pick = np.argsort(keys, axis=1)[:, :k]
+        sel = np.take_along_axis(block, pick, axis=1)
+        short = np.flatnonzero((~dup).sum(axis=1) < k)
+        for r in short:  # hot columns collided too often: top up with more draws
             uniq = np.unique(block[r])
-            while uniq.size < k:  # hot columns collide: top up with more draws
-                extra = perm[np.minimum(np.searchsorted(cdf, rng.random(2 * k)), q - 1)]
+            while uniq.size < k:
+                extra = perm[_zipf_ranks(rng, (2 * k,), s, q)]
                 uniq = np.unique(np.concatenate([uniq, extra]))
-            pick = rng.choice(uniq.size, size=k, replace=False)
-            out[start + r] = np.sort(uniq[pick])
+            sel[r] = uniq[rng.choice(uniq.size, size=k, replace=False)]
+        out[start:stop] = np.sort(sel, axis=1)
     return out
 
 

@@ -118,7 +118,7 @@ class CsrKernelOperator:
             A = sp.csr_matrix((data, indices, indptr), shape=shape)
         else:
             A = sp.csr_matrix(samples)
-        A.sort_indices()
+        A.sum_duplicates()  # sorted, duplicate-free rows (the Gram merges rely on it)
         A = A.astype(np.float64)
         self.n_phys, self.q = A.shape
         self.n = self.n_phys

@@ -561,7 +561,8 @@ def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_devi
     if rep.max_outer_reached:
         notes.append(f"max_outer={alm_opts.max_outer} reached")
     problem.native_counters = {"syncs": rep.syncs, "newton": rep.newton_steps,
-                               "projections": rep.projections}
+                               "projections": rep.projections, "cg_iters": rep.cg_iters,
+                               "cg_fallbacks": rep.cg_fallbacks}
     problem.op_profile = {name: {"calls": int(rep.op_calls[k]), "seconds": float(rep.op_seconds[k]),
                                  "bytes": float(rep.op_bytes[k])}
                           for k, name in enumerate(_lib.OP_NAMES)}
