@@ -248,6 +248,36 @@ int ssnal_alm_solve_dense(const ssnal_dense_problem_t* problem, const ssnal_opti
                           ssnal_report_t* report, void* ws, size_t ws_bytes,
                           ssnal_progress_fn progress, void* progress_ctx, void* stream);
 
+/* ---- row-sharded path ------------------------------------------------------
+ * One process per GPU, rank r owning a slice of the n dual slots (rows of X).
+ * The cross-slot reductions of the projection (ref projection.py:152-211) are
+ * split into shard-local records the host all-gathers and folds in rank order:
+ *   mode 0 (eval at lam[t]):  rec[t*8 + 0..4] = { sum a clip(v - lam a, l, u),
+ *     sum a^2 over slots free just right of lam, ... just left, nearest breakpoint
+ *     > lam (+inf), nearest breakpoint < lam (-inf) }
+ *   mode 1 (apply at lam[t]): x_out / free_out (T x n) and rec[t*8 + 0..5] =
+ *     { sum v^2, sum (v-x)^2, sum (x-ref)^2, sum_free a^2, nfree, sum x(2v-x) }
+ * with v = A - coef[t] B.  coef and lam are HOST arrays of T <= 16; rec is a
+ * DEVICE array of 8 T doubles.  ws: ssnal_proj_local_ws_bytes(n, T). */
+size_t ssnal_proj_local_ws_bytes(int64_t n, int T);
+int ssnal_proj_local(const double* A, const double* B, const double* coef, const double* lam,
+                     const double* a, const double* l, const double* u, double l_const,
+                     double u_const, int64_t n, int T, int mode, double* x_out, uint8_t* free_out,
+                     const double* ref, double* rec, void* ws, void* stream);
+/* out[i] = sum_{r<k} src[r*len + i] in rank order (the all-gathered partials of
+ * X^T v, Gram blocks and dot records; deterministic). */
+int ssnal_sum_slices(int k, int64_t len, const double* src, double* out, void* stream);
+/* out = alpha*add + beta*free(y - coef*a): ssnal_hs_apply with the global
+ * coef = a_J'y_J / a_J'a_J supplied (ref projection.py:214-225). */
+int ssnal_hs_apply_coef(const uint8_t* free_mask, const double* a, const double* y, int64_t n,
+                        double beta, const double* add, double alpha, double coef, double* out,
+                        void* stream);
+/* M = I + sigma (M - shift I - u u'/asa) in place (u NULL or asa == 0: no rank-one
+ * term): the factor-space Newton matrix from the rank-summed Gram of
+ * ssnal_dense_gram(sigma = 1, a'a = 0) blocks (shift = world size). */
+int ssnal_qspace_assemble(int64_t m, const double* u, double asa, double sigma, double shift,
+                          double* M, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -114,6 +114,12 @@ _SIGNATURES.update({
     "ssnal_csr_xt": (_I, [ctypes.POINTER(CsrOperator), _P, _P, _P, _P]),
     "ssnal_alm_solve_dense": (_I, [ctypes.POINTER(DenseProblem), ctypes.POINTER(Options), _P, _P,
                                    _P, ctypes.POINTER(Report), _P, _SZ, PROGRESS_FN, _P, _P]),
+    "ssnal_proj_local_ws_bytes": (_SZ, [_I64, _I]),
+    "ssnal_proj_local": (_I, [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I64, _I, _I, _P, _P, _P, _P,
+                              _P, _P]),
+    "ssnal_sum_slices": (_I, [_I, _I64, _P, _P, _P]),
+    "ssnal_hs_apply_coef": (_I, [_P, _P, _P, _I64, _D, _P, _D, _D, _P, _P]),
+    "ssnal_qspace_assemble": (_I, [_I64, _P, _D, _D, _D, _P, _P]),
 })
 
 _lib = None

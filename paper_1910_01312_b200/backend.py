@@ -211,6 +211,34 @@ class CudaBackend:
         self._timed("chol_solve", 16 * m * m, _lib.call, "ssnal_chol_solve", _ptr(M), int(m),
                     _ptr(b), float(scale), _ptr(x), _ptr(info), self.stream())
 
+    # ---------------------------------------------------------------- sharded path
+    def proj_local(self, A, box, T, lam, mode, rec, B=None, coefs=None, x_out=None,
+                   free_out=None, ref=None):
+        """Shard-local projection records at host multipliers ``lam`` (csrc/dist.cu)."""
+        n = box.n
+        lam_arr = (_lib.ctypes.c_double * T)(*[float(v) for v in lam])
+        coef_arr = None
+        if B is not None:
+            coef_arr = (_lib.ctypes.c_double * T)(*[float(c) for c in coefs])
+        ws = self.ws("proj_local", self.lib.ssnal_proj_local_ws_bytes(n, T))
+        _lib.call("ssnal_proj_local", _ptr(A), _ptr(B),
+                  _lib.ctypes.cast(coef_arr, _lib.ctypes.c_void_p) if coef_arr is not None else None,
+                  _lib.ctypes.cast(lam_arr, _lib.ctypes.c_void_p), _ptr(box.a_dev), _ptr(box.l_dev),
+                  _ptr(box.u_dev), box.l_const, box.u_const, n, T, int(mode), _ptr(x_out),
+                  _ptr(free_out), _ptr(ref), _ptr(rec), _ptr(ws), self.stream())
+
+    def sum_slices(self, k, src, out):
+        """out = sum of the k equal slices of src, in slice order."""
+        _lib.call("ssnal_sum_slices", int(k), out.numel(), _ptr(src), _ptr(out), self.stream())
+
+    def hs_apply_coef(self, free, a, y, beta, add, alpha, coef, out):
+        _lib.call("ssnal_hs_apply_coef", _ptr(free), _ptr(a), _ptr(y), y.numel(), float(beta),
+                  _ptr(add), float(alpha), float(coef), _ptr(out), self.stream())
+
+    def qspace_assemble(self, m, u, asa, sigma, shift, M):
+        _lib.call("ssnal_qspace_assemble", int(m), _ptr(u), float(asa), float(sigma), float(shift),
+                  _ptr(M), self.stream())
+
 
 _DEFAULT = {}
 

@@ -44,6 +44,19 @@ cudaError_t launch_pspace_direction(const double* A, long long n, long long q, l
                                     const double* grad, const double* a, double sigma, double asa,
                                     const double* g_r, double* t, int* info, void* ws,
                                     cudaStream_t stream);
+size_t proj_local_ws_bytes(long long n, int T);
+cudaError_t launch_proj_local(const double* A, const double* B, const double* coef,
+                              const double* lam, const double* a, const double* l,
+                              const double* u, double lc, double uc, long long n, int T, int mode,
+                              double* x_out, uint8_t* free_out, const double* ref, double* rec,
+                              void* ws, cudaStream_t s);
+cudaError_t launch_sum_slices(int k, long long len, const double* src, double* out,
+                              cudaStream_t s);
+cudaError_t launch_hs_apply_coef(const uint8_t* fm, const double* a, const double* y, long long n,
+                                 double beta, const double* add, double alpha, double coef,
+                                 double* out, cudaStream_t s);
+cudaError_t launch_qspace_shift_assemble(long long m, const double* u, double asa, double sigma,
+                                         double shift, double* M, cudaStream_t s);
 }  // namespace ssnal
 
 #include <atomic>
@@ -246,6 +259,43 @@ int ssnal_chol_solve(double* M, int64_t m, const double* b, double scale, double
                      void* stream) {
   if (m < 1 || !M || !b || !x || !info) return fail_arg("ssnal_chol_solve", "size/null");
   return check("ssnal_chol_solve", launch_chol_solve(M, m, b, scale, x, info, S(stream)));
+}
+
+/* ---- row-sharded path (csrc/dist.cu) ---- */
+size_t ssnal_proj_local_ws_bytes(int64_t n, int T) { return proj_local_ws_bytes(n, T); }
+
+int ssnal_proj_local(const double* A, const double* B, const double* coef, const double* lam,
+                     const double* a, const double* l, const double* u, double l_const,
+                     double u_const, int64_t n, int T, int mode, double* x_out, uint8_t* free_out,
+                     const double* ref, double* rec, void* ws, void* stream) {
+  if (n < 1) return fail_arg("ssnal_proj_local", "n < 1");
+  if (T < 1 || T > SSNAL_MAX_TRIALS) return fail_arg("ssnal_proj_local", "T must be in [1, 16]");
+  if (!A || !a || !lam || !rec || !ws) return fail_arg("ssnal_proj_local", "null A/a/lam/rec/ws");
+  if (B && !coef) return fail_arg("ssnal_proj_local", "B given without coef");
+  if (mode != 0 && mode != 1) return fail_arg("ssnal_proj_local", "mode must be 0 or 1");
+  return check("ssnal_proj_local", launch_proj_local(A, B, coef, lam, a, l, u, l_const, u_const,
+                                                     n, T, mode, x_out, free_out, ref, rec, ws,
+                                                     S(stream)));
+}
+
+int ssnal_sum_slices(int k, int64_t len, const double* src, double* out, void* stream) {
+  if (k < 1 || len < 1 || !src || !out) return fail_arg("ssnal_sum_slices", "size/null");
+  return check("ssnal_sum_slices", launch_sum_slices(k, len, src, out, S(stream)));
+}
+
+int ssnal_hs_apply_coef(const uint8_t* free_mask, const double* a, const double* y, int64_t n,
+                        double beta, const double* add, double alpha, double coef, double* out,
+                        void* stream) {
+  if (n < 1 || !free_mask || !a || !y || !out) return fail_arg("ssnal_hs_apply_coef", "null/size");
+  return check("ssnal_hs_apply_coef", launch_hs_apply_coef(free_mask, a, y, n, beta, add, alpha,
+                                                           coef, out, S(stream)));
+}
+
+int ssnal_qspace_assemble(int64_t m, const double* u, double asa, double sigma, double shift,
+                          double* M, void* stream) {
+  if (m < 1 || !M) return fail_arg("ssnal_qspace_assemble", "size/null");
+  return check("ssnal_qspace_assemble",
+               launch_qspace_shift_assemble(m, u, asa, sigma, shift, M, S(stream)));
 }
 
 }  // extern "C"

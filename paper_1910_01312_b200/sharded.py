@@ -1,0 +1,309 @@
+"""Row-sharded SSsNAL: one process per GPU, each rank owning a contiguous slice of
+the samples (rows of X) and of the dual vector.
+
+BASELINE configs 3 and 4 are quoted "row-sharded over 1/2/4/8 GPUs".  The data
+products split cleanly by rows: X d is rank-local, X^T v is a sum of rank-local
+partials.  The places the path genuinely couples the slots are
+
+  * X^T v (q-vector) and the factor-space Gram X_J^T X_J (q x q),
+  * the inner products of the line search / stopping tests,
+  * the projection's multiplier lambda (one equality constraint over all n),
+
+and each is reduced here through an all-gather of a small fixed-size record
+followed by an ordered fold (csrc/dist.cu ``ssnal_sum_slices`` on the device, or
+numpy in rank order on the host for the scalar records), so every rank holds
+bit-identical scalars and takes identical branches -- the reduction order never
+depends on NCCL's algorithm choice.
+
+The projection search runs the safeguarded Newton of csrc/proj.cu one pass per
+all-gather: each pass evaluates, rank-locally, f(lambda) = sum a clip(v - lambda
+a, l, u), the one-sided slopes and the nearest breakpoints (ssnal_proj_local mode
+0); the host folds the records and either lands exactly on the affine piece that
+holds the root (the reference's interpolation, ref projection.py:204-208) or
+moves lambda.  The Newton system is always the q x q factor-space one (the
+Woodbury p x p dual would need the free rows of other ranks).
+
+The solver control flow is solver._Engine / ssn_solve / alm_solve unchanged:
+``ShardedBackend`` makes every reduction global and ``ShardedEngine`` replaces
+the direction assembly.  torch.distributed (NCCL on GPUs, gloo in the CPU tests)
+is the transport only.
+"""
+
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .backend import F64, as_device, default_backend
+from .errors import InfeasibleProblemError, InputError, InternalError
+from .operators import LinearKernelOperator
+from .projection import BoxLineSet
+from .solver import QpProblem, _Engine
+
+MAX_PASSES = 200  # projection search passes per call (warm-started: typically 1-3)
+
+
+class ShardComm:
+    """Rank / world of a torch.distributed group and the all-gather transport."""
+
+    def __init__(self, group=None):
+        if not dist.is_initialized():
+            raise InputError("torch.distributed is not initialised")
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def all_gather(self, t):
+        """(world, *t.shape) tensor of every rank's t (same device as t)."""
+        t = t.contiguous()
+        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        if self.world == 1:
+            out[0].copy_(t)
+        elif self.nccl:
+            dist.all_gather_into_tensor(out, t, group=self.group)
+        else:
+            dist.all_gather(list(out.unbind(0)), t, group=self.group)
+        return out
+
+    def all_gather_objects(self, obj):
+        out = [None] * self.world
+        dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+def shard_range(n, rank, world):
+    """Contiguous balanced slice [lo, hi) of n rows for ``rank``."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class ShardedBackend:
+    """A device backend whose reductions are global over the group.  Everything
+    not overridden (memory, element-wise kernels, local products) is the wrapped
+    single-GPU backend's."""
+
+    name = "sharded"
+
+    def __init__(self, base, comm):
+        self.base = base
+        self.comm = comm
+        self.rec = base.zeros(16 * 8)  # (T <= 16) x 8 shard record
+        self.collectives = 0
+
+    def __getattr__(self, name):
+        return getattr(self.base, name)
+
+    # ---------------------------------------------------------------- reductions
+    def allsum(self, t):
+        """t <- sum over ranks of t (in place), folded in rank order."""
+        if self.comm.world == 1:
+            return
+        flat = t.view(-1)
+        g = self.comm.all_gather(flat)
+        self.collectives += 1
+        self.base.sum_slices(self.comm.world, g, flat)
+
+    def dots(self, pairs, out, mask=None, replicated=False):
+        self.base.dots(pairs, out, mask)
+        if not replicated:
+            self.allsum(out[: len(pairs)])
+
+    def dense_xt(self, op, vs, out):
+        self.base.dense_xt(op, vs, out)
+        self.allsum(out[: len(vs)])
+
+    def _fold(self, rec_dev, T, mode):
+        """All-gather the (T, 8) shard records and fold them in rank order (host)."""
+        g = self.comm.all_gather(rec_dev[: 8 * T]).cpu().numpy().reshape(self.comm.world, T, 8)
+        self.collectives += 1
+        out = g[0].copy()
+        for r in range(1, self.comm.world):
+            if mode == 0:
+                out[:, :3] += g[r, :, :3]
+                out[:, 3] = np.minimum(out[:, 3], g[r, :, 3])
+                out[:, 4] = np.maximum(out[:, 4], g[r, :, 4])
+            else:
+                out[:, :6] += g[r, :, :6]
+        return out
+
+    # ---------------------------------------------------------------- projection
+    def project(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
+                ref=None, phases=None, passes=None, hint=0.0, newton=None):
+        """Global projection of T trial points v_t = A - coefs[t] B (rank slices);
+        writes the T global state records, x_out / free_out rank-locally."""
+        d = float(getattr(box, "d_global", box.d))
+        coefs = [float(c) for c in coefs] if B is not None else None
+        lam = [float(hint)] * T
+        lo, hi = [-math.inf] * T, [math.inf] * T
+        done = [False] * T
+        npass = 0
+        while not all(done):
+            npass += 1
+            if npass > MAX_PASSES:
+                raise InternalError("sharded projection: multiplier search did not converge")
+            act = [t for t in range(T) if not done[t]]
+            self.base.proj_local(A, box, len(act), [lam[t] for t in act], 0, self.rec, B=B,
+                                 coefs=[coefs[t] for t in act] if B is not None else None)
+            rec = self._fold(self.rec, len(act), 0)
+            for j, t in enumerate(act):
+                f, s_r, s_l, b_r, b_l = (float(v) for v in rec[j, :5])
+                g, c = d - f, lam[t]
+                if g < 0.0:  # root to the right (phi' = d - f is non-decreasing)
+                    lo[t] = c
+                    if s_r > 0.0:
+                        ln = c - g / s_r
+                        if ln <= b_r:  # affine piece [c, b_r] holds the root: exact
+                            lam[t], done[t] = ln, True
+                            continue
+                    else:
+                        if not math.isfinite(b_r):
+                            raise InfeasibleProblemError("a'x = d above the box range")
+                        ln = b_r
+                else:        # root at or left of c; the leftmost root, as the reference
+                    if g == 0.0 and (s_l > 0.0 or not math.isfinite(b_l)):
+                        done[t] = True
+                        continue
+                    hi[t] = c
+                    if s_l > 0.0:
+                        ln = c - g / s_l
+                        if ln >= b_l:
+                            lam[t], done[t] = ln, True
+                            continue
+                    else:
+                        if not math.isfinite(b_l):
+                            raise InfeasibleProblemError("a'x = d below the box range")
+                        ln = b_l
+                if not (lo[t] < ln < hi[t]) and math.isfinite(lo[t]) and math.isfinite(hi[t]):
+                    ln = 0.5 * (lo[t] + hi[t])
+                lam[t] = ln
+        self.base.proj_local(A, box, T, lam, 1, self.rec, B=B, coefs=coefs, x_out=x_out,
+                             free_out=free_out, ref=ref)
+        rec = self._fold(self.rec, T, 1)
+        host = np.zeros(T, dtype=_lib.PROJ_STATE_DTYPE)
+        for t in range(T):
+            host[t]["lam"] = lam[t]
+            host[t]["sum_v2"], host[t]["sum_r2"], host[t]["sum_dref2"] = rec[t, 0:3]
+            host[t]["sum_a2_free"] = rec[t, 3]
+            host[t]["nfree"] = int(round(rec[t, 4]))
+            host[t]["sum_xv"] = rec[t, 5]
+            host[t]["status"] = _lib.PROJ_APPLIED
+            host[t]["passes"] = npass
+        states[:T].copy_(torch.from_numpy(host.view(np.uint8).reshape(T, -1)))
+
+
+class ShardedEngine(_Engine):
+    """solver._Engine over a rank slice; the Newton system is assembled from the
+    rank-summed factor-space Gram."""
+
+    def __init__(self, problem, t_max=4):
+        super().__init__(problem, t_max)
+        be = self.be
+        c2 = be.zeros(1)
+        be.dots([(problem.c, None)], c2)
+        self.c_norm = math.sqrt(float(c2[0]))
+        self.zero = be.zeros(1)
+        self.am = be.empty(self.n)
+
+    def direction(self, p, sigma, asa=0.0):
+        if p == 0:
+            return super().direction(p, sigma, asa)
+        be, base, op = self.be, self.be.base, self.op
+        if self.q > self.pb_direct_limit():
+            raise InternalError("q x q system larger than direct_solve_threshold")
+        base.compact(self.free, self.J, self.pcount)
+        # M_r = I + X_Jr^T X_Jr (sigma = 1, no rank-one term), summed over ranks
+        base.dense_gram(op, self.J, self.pcount, self.n, self.box.a_dev, 1.0, self.zero, self.M,
+                        self.m1)
+        be.allsum(self.M)
+        # u = X_J^T a_J (global), then M = I + sigma (G - u u'/a'a), G = sum M_r - world I
+        base.hs_apply_coef(self.free, self.box.a_dev, self.box.a_dev, 1.0, None, 0.0, 0.0, self.am)
+        op.xt([self.am], self.gr[1:2])
+        base.qspace_assemble(self.q, self.gr[1], asa, sigma, float(be.comm.world), self.M)
+        base.chol_solve(self.M, self.q, self.gr[0], -1.0, self.t[0], self.info)
+        op.x(self.t, self.qdir.view(1, -1), k=1)
+        # d = -s - sigma P_J(Qd) with the global coefficient a_J'(Qd)_J / a_J'a_J
+        be.dots([(self.box.a_dev, self.qdir)], self.scal[8:9], mask=self.free)
+        aq = float(self.scal[8])
+        coef = aq / asa if asa != 0.0 else 0.0
+        base.hs_apply_coef(self.free, self.box.a_dev, self.qdir, -sigma, self.s, -1.0, coef,
+                           self.dir)
+        be.dots([(self.grad, self.dir), (self.w, self.qw), (self.w, self.qdir)], self.scal)
+        be.dots([(self.t[0], None)], self.scal[3:4], replicated=True)
+
+
+class ShardedQpProblem(QpProblem):
+    """Rank slice of min 1/2 x'Qx + c'x s.t. a'x = d, l <= x <= u."""
+
+    def __init__(self, q_op, c, constraint, d_global, comm, layout):
+        super().__init__(q_op, c, constraint)
+        constraint.d_global = float(d_global)
+        self.comm = comm
+        self.layout = layout  # (kind, n_phys_total, lo, hi)
+
+    def engine(self):
+        if self._engine is None:
+            self._engine = ShardedEngine(self)
+        return self._engine
+
+
+def _local_backend(comm, backend=None):
+    return ShardedBackend(backend or default_backend(), comm)
+
+
+def build_csvc_dual_sharded(features, labels, C, comm, backend=None):
+    """Rank slice of the C-SVC dual (ref svm.py:95-108): ``features``/``labels`` are
+    THIS rank's rows (shard_range gives the conventional split)."""
+    be = _local_backend(comm, backend)
+    y = np.asarray(labels.detach().cpu().numpy() if isinstance(labels, torch.Tensor) else labels,
+                   dtype=np.float64)
+    if not np.all(np.abs(y) == 1.0):
+        raise InputError("classification labels must be +1/-1")
+    if not C > 0:
+        raise InputError("C must be positive")
+    n_loc = y.shape[0]
+    sizes = comm.all_gather_objects(n_loc)
+    op = LinearKernelOperator(features, labels=y, backend=be)
+    box = BoxLineSet(a=y, d=0.0, l=np.zeros(n_loc), u=np.full(n_loc, float(C)), backend=be)
+    lo = int(sum(sizes[: comm.rank]))
+    return ShardedQpProblem(op, -np.ones(n_loc), box, 0.0, comm,
+                            ("csvc", int(sum(sizes)), lo, lo + n_loc))
+
+
+def build_svr_dual_sharded(features, targets, C, epsilon, comm, backend=None):
+    """Rank slice of the eps-SVR dual (ref svm.py:111-127): local variables are
+    [x+ ; x-] of this rank's rows."""
+    be = _local_backend(comm, backend)
+    t = np.asarray(targets.detach().cpu().numpy() if isinstance(targets, torch.Tensor) else targets,
+                   dtype=np.float64)
+    if not C > 0 or epsilon < 0:
+        raise InputError("need C > 0 and epsilon >= 0")
+    n_loc = t.shape[0]
+    sizes = comm.all_gather_objects(n_loc)
+    op = LinearKernelOperator(features, svr_block=True, backend=be)
+    c = np.concatenate([epsilon - t, epsilon + t])
+    a = np.concatenate([np.ones(n_loc), -np.ones(n_loc)])
+    box = BoxLineSet(a=a, d=0.0, l=np.zeros(2 * n_loc), u=np.full(2 * n_loc, float(C)),
+                     backend=be)
+    lo = int(sum(sizes[: comm.rank]))
+    return ShardedQpProblem(op, c, box, 0.0, comm, ("svr", int(sum(sizes)), lo, lo + n_loc))
+
+
+def gather_solution(problem, x_local):
+    """Full dual vector (reference ordering) on every rank, from the rank slices."""
+    comm = problem.comm
+    x = torch.as_tensor(x_local, dtype=F64).cpu()
+    parts = comm.all_gather_objects(x.numpy())
+    kind = problem.layout[0]
+    if kind == "csvc":
+        return np.concatenate(parts)
+    plus = np.concatenate([p[: p.size // 2] for p in parts])
+    minus = np.concatenate([p[p.size // 2:] for p in parts])
+    return np.concatenate([plus, minus])
+
+
+__all__ = ["ShardComm", "ShardedBackend", "ShardedEngine", "ShardedQpProblem", "shard_range",
+           "build_csvc_dual_sharded", "build_svr_dual_sharded", "gather_solution"]

@@ -179,3 +179,68 @@ class CpuTestBackend:
         y = np.linalg.solve(L, scale * b.numpy())
         x.copy_(torch.from_numpy(np.linalg.solve(L.T, y)))
         info[0] = 0
+
+    # sharded path --------------------------------------------------------------
+    def proj_local(self, A, box, T, lam, mode, rec, B=None, coefs=None, x_out=None,
+                   free_out=None, ref=None):
+        self._count("proj_local")
+        a = box.a_dev.numpy()
+        l = box.l.numpy()
+        u = box.u.numpy()
+        r = rec.view(-1, 8)
+        for t in range(T):
+            v = A.numpy().copy()
+            if B is not None:
+                v = v - float(coefs[t]) * B.numpy()
+            y = v - lam[t] * a
+            x = np.clip(y, l, u)
+            if mode == 0:
+                with np.errstate(divide="ignore", invalid="ignore"):
+                    t1, t2 = (v - u) / a, (v - l) / a
+                nz = a != 0
+                b0, b1 = np.minimum(t1, t2)[nz], np.maximum(t1, t2)[nz]
+                a2 = (a * a)[nz]
+                right = np.where(b0 > lam[t], b0, np.where(b1 > lam[t], b1, np.inf))
+                left = np.where(b1 < lam[t], b1, np.where(b0 < lam[t], b0, -np.inf))
+                r[t, 0] = float(a @ x)
+                r[t, 1] = float(a2[(b0 <= lam[t]) & (lam[t] < b1)].sum())
+                r[t, 2] = float(a2[(b0 < lam[t]) & (lam[t] <= b1)].sum())
+                r[t, 3] = float(right.min()) if right.size else np.inf
+                r[t, 4] = float(left.max()) if left.size else -np.inf
+            else:
+                lower = y <= l + 1e-12 * (1.0 + np.abs(l))
+                upper = ~lower & (y >= u - 1e-12 * (1.0 + np.abs(u)))
+                free = ~(lower | upper)
+                res = v - x
+                r[t, 0] = float(v @ v)
+                r[t, 1] = float(res @ res)
+                r[t, 2] = float(((x - ref.numpy()) ** 2).sum()) if ref is not None else 0.0
+                r[t, 3] = float((a[free] ** 2).sum())
+                r[t, 4] = float(free.sum())
+                r[t, 5] = float(x @ (2.0 * v - x))
+                if x_out is not None:
+                    x_out.view(-1, box.n)[t].copy_(torch.from_numpy(x))
+                if free_out is not None:
+                    free_out.view(-1, box.n)[t].copy_(torch.from_numpy(free.astype(np.uint8)))
+
+    def sum_slices(self, k, src, out):
+        self._count("sum_slices")
+        sl = src.reshape(k, -1).numpy()
+        acc = sl[0].copy()
+        for j in range(1, k):
+            acc = acc + sl[j]
+        out.view(-1).copy_(torch.from_numpy(acc))
+
+    def hs_apply_coef(self, free, a, y, beta, add, alpha, coef, out):
+        self._count("hs_apply_coef")
+        h = np.where(free.numpy().astype(bool), y.numpy() - coef * a.numpy(), 0.0)
+        r = beta * h + (alpha * add.numpy() if add is not None else 0.0)
+        out.copy_(torch.from_numpy(np.ascontiguousarray(r)))
+
+    def qspace_assemble(self, m, u, asa, sigma, shift, M):
+        self._count("qspace_assemble")
+        G = M.numpy() - shift * np.eye(m)
+        if u is not None and asa != 0.0:
+            uu = u.numpy()
+            G = G - np.outer(uu, uu) / asa
+        M.copy_(torch.from_numpy(np.eye(m) + sigma * G))

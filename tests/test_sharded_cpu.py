@@ -1,0 +1,115 @@
+"""Row-sharded solver host logic on the CPU: world_size 2 over gloo.
+
+Each rank runs solver.alm_solve on its slice through sharded.ShardedBackend (the
+global reductions, the all-gather multiplier search, the rank-summed Newton
+Gram) with the TEST-ONLY CpuTestBackend underneath; the gathered solution must
+match the single-process solve of the whole problem and the golden reference runs.
+"""
+
+import os
+import socket
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT, load_cases
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out_path, task):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cpu_backend import CpuTestBackend
+        from paper_1910_01312_b200 import sharded, solver
+
+        comm = sharded.ShardComm()
+        be = CpuTestBackend()
+        results = {}
+        for idx, c in enumerate(task):
+            n = c["A"].shape[0]
+            lo, hi = sharded.shard_range(n, rank, world)
+            if c["kind"] == "csvc":
+                pb = sharded.build_csvc_dual_sharded(c["A"][lo:hi], c["y"][lo:hi], c["C"], comm,
+                                                     backend=be)
+            else:
+                pb = sharded.build_svr_dual_sharded(c["A"][lo:hi], c["t"][lo:hi], c["C"],
+                                                    c["eps"], comm, backend=be)
+            rep = solver.alm_solve(pb, solver.AlmOptions(tol_kkt=c["tol"]))
+            x = sharded.gather_solution(pb, rep.x_opt)
+            results[f"x{idx}"] = x
+            results[f"r{idx}"] = np.array([rep.kkt_residual, rep.objective, rep.outer_iters,
+                                           rep.total_inner_iters, float(rep.converged),
+                                           pb.backend.collectives])
+        if rank == 0:
+            np.savez(out_path, **results)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(task, world=2):
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "res.npz")
+        mp.spawn(_worker, args=(world, _free_port(), out, task), nprocs=world, join=True)
+        with np.load(out) as z:
+            return {k: z[k] for k in z.files}
+
+
+def _svm_cases():
+    return [c for c in load_cases("solve.npz", "s") if c["kind"] != "dense"]
+
+
+def test_sharded_world2_matches_golden_and_single_process():
+    from cpu_backend import CpuTestBackend
+    from paper_1910_01312_b200 import solver, svm
+
+    cases = _svm_cases()
+    res = _run(cases, world=2)
+    be = CpuTestBackend()
+    for idx, c in enumerate(cases):
+        kkt, obj, outer, inner, conv, coll = res[f"r{idx}"]
+        assert conv == 1.0 and kkt < c["tol"]
+        assert coll > 0  # the ranks really exchanged records
+        assert (outer, inner) == (c["outer"], c["inner"])  # the reference's iteration counts
+        assert obj == pytest.approx(c["obj"], rel=1e-6, abs=1e-9)
+        np.testing.assert_allclose(res[f"x{idx}"], c["x_opt"], atol=1e-6)
+        if c["kind"] == "csvc":
+            single = svm.build_csvc_dual(c["A"], c["y"], c["C"], backend=be)
+        else:
+            single = svm.build_svr_dual(c["A"], c["t"], c["C"], c["eps"], backend=be)
+        ref = solver.alm_solve(single, solver.AlmOptions(tol_kkt=c["tol"]))
+        assert obj == pytest.approx(ref.objective, rel=1e-9, abs=1e-12)
+        np.testing.assert_allclose(res[f"x{idx}"], ref.x_opt, atol=1e-7)
+
+
+def test_sharded_uneven_slices():
+    """n not divisible by the world size, one rank with few rows."""
+    rng = np.random.default_rng(11)
+    n, q = 157, 7
+    A = rng.standard_normal((n, q))
+    y = np.where(A @ rng.standard_normal(q) + 0.3 * rng.standard_normal(n) >= 0, 1.0, -1.0)
+    case = {"kind": "csvc", "A": A, "y": y, "C": 1.0, "tol": 1e-8}
+    res = _run([case], world=3)
+    from cpu_backend import CpuTestBackend
+    from paper_1910_01312_b200 import solver, svm
+
+    ref = solver.alm_solve(svm.build_csvc_dual(A, y, 1.0, backend=CpuTestBackend()),
+                           solver.AlmOptions(tol_kkt=1e-8))
+    kkt, obj, *_ = res["r0"]
+    assert kkt < 1e-8 and ref.converged
+    assert obj == pytest.approx(ref.objective, rel=1e-9)
+    np.testing.assert_allclose(res["x0"], ref.x_opt, atol=1e-7)
+    assert abs(float(y @ res["x0"])) < 1e-9 * (1 + np.abs(res["x0"]).sum())
