@@ -44,11 +44,21 @@ __device__ __forceinline__ void block_reduce(double (&vals)[NV], const int (&ops
   }
   __syncthreads();
   // slot k is combined across warps by thread k (fixed order), then broadcast to thread 0
+  // threads 0..NV-1 fold one slot each in lockstep; the per-slot op is read from a
+  // bit mask built at compile time (a dynamic ops[k] would copy ops[] to local memory)
+  static_assert(NV <= 64, "block_reduce: at most 64 slots");
+  unsigned long long is_sum = 0ull, is_min = 0ull;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    if (ops[k] == 0) is_sum |= 1ull << k;
+    if (ops[k] == 1) is_min |= 1ull << k;
+  }
   for (int k = threadIdx.x; k < NV; k += blockDim.x) {
+    const unsigned op = ((is_sum >> k) & 1ull) ? 0u : (((is_min >> k) & 1ull) ? 1u : 2u);
     double v = smem[k * 32];
     for (int w = 1; w < nwarps; ++w) {
       double x = smem[k * 32 + w];
-      v = ops[k] == 0 ? v + x : (ops[k] == 1 ? fmin(v, x) : fmax(v, x));
+      v = op == 0 ? v + x : (op == 1 ? fmin(v, x) : fmax(v, x));
     }
     smem[k * 32] = v;
   }

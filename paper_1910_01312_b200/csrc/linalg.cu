@@ -151,305 +151,186 @@ __global__ void __launch_bounds__(CH_NT, 1) chol_solve_kernel(double* __restrict
   if (tid == 0) *info = fail;
 }
 
-// Small systems (m <= SMALL_M): the whole lower triangle lives in shared memory
-// (odd row stride: conflict-free column access), right-looking column Cholesky
-// with all 1024 threads on the trailing update, then column-sweep substitutions.
-static constexpr int SMALL_M = 160;
+// ---------------------------------------------------------------------------
+// Latency-first small SPD solve (m <= 160): the matrix is padded to m16 = 16k with
+// an identity tail and (scale b)^T appended as row m16, so the forward substitution
+// L z = b falls out of the factorisation itself (row m16 is just one more row below
+// every panel).  Per 16-column panel:
+//   (1) diagonal block: warp 0, lane i holds row i in registers (compile-time
+//       indices only), pivots by shuffle;
+//   (2) panel TRSM: one thread per row below (row in registers, diagonal-block
+//       entries broadcast from shared memory);
+//   (3) trailing SYRK on the fp64 tensor cores: 8x8 output tiles, four
+//       mma.m8n8k4 per tile for the 16-wide panel, C loaded / stored in place,
+//       the A operand negated so D = S - L21 L21^T in one pass.
+// Back substitution L^T x = z by 16-blocks: warp-0 shuffle solve + one block-wide
+// column update.  Three barriers per panel, two per back-substitution block.
+// Shared row stride ld = m16 + 4 (= 4 mod 16): the m8n8k4 A/B fragments
+// (rows lane/4, k = lane%4) hit 16 distinct bank pairs per phase.
+static constexpr int TC_NB = 16;
+static constexpr int TC_MAX = 160;
+static constexpr int TC_NT = 512;
 
-static constexpr int SM_NT = 512;  // 128 registers/thread: the 32-double row of warp 0 stays in RF
-
-__global__ void __launch_bounds__(SM_NT, 1) chol_small_kernel(const double* __restrict__ M, int m,
-                                                                const double* __restrict__ b,
-                                                                double scale,
-                                                                double* __restrict__ x,
-                                                                int* __restrict__ info) {
-  extern __shared__ double S[];
-  const int ld = m | 1;
-  double* y = S + (size_t)m * ld;
-  __shared__ int fail;
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  if (tid == 0) fail = 0;
-  for (int idx = tid; idx < m * m; idx += blockDim.x) {
-    const int i = idx / m, j = idx % m;
-    if (j <= i) S[i * ld + j] = M[(long long)i * m + j];
-  }
-  for (int i = tid; i < m; i += blockDim.x) y[i] = scale * b[i];
-  __syncthreads();
-  const int lane = tx, warp = ty;
-  __shared__ double rdiag[32];
-  for (int k0 = 0; k0 < m; k0 += 32) {
-    const int kb = min(32, m - k0);
-    // (1) diagonal block, 2-D parallel over its (i, c) pairs: per column one barrier
-    //     for the scaled column, one for the rank-1 update (every thread recomputes
-    //     the pivot sqrt itself instead of waiting on a broadcast)
-    for (int j = 0; j < kb; ++j) {
-      double d = S[(k0 + j) * ld + k0 + j];
-      if (!(d > 0.0)) {
-        if (tid == 0 && fail == 0) fail = k0 + j + 1;
-        d = 1.0;
-      }
-      const double ljj = sqrt(d);
-      __syncthreads();  // everyone has read the pivot before it is overwritten
-      if (tid == 0) {
-        S[(k0 + j) * ld + k0 + j] = ljj;
-        rdiag[j] = 1.0 / ljj;
-      }
-      for (int i = k0 + j + 1 + tid; i < k0 + kb; i += blockDim.x) S[i * ld + k0 + j] /= ljj;
-      __syncthreads();
-      const int r = kb - j - 1;  // trailing rows inside the block
-      for (int idx = tid; idx < r * r; idx += blockDim.x) {
-        const int ii = idx / r, cc = idx % r;
-        if (cc <= ii) {
-          const int i = k0 + j + 1 + ii, c = k0 + j + 1 + cc;
-          S[i * ld + c] = fma(-S[i * ld + k0 + j], S[c * ld + k0 + j], S[i * ld + c]);
-        }
-      }
-    }
-    (void)lane;
-    (void)warp;
-    __syncthreads();
-    // (2) panel: L21 = A21 L11^{-T}, one thread per row (reciprocal diagonal)
-    for (int i = k0 + kb + tid; i < m; i += blockDim.x) {
-      double* row = S + i * ld + k0;
-      for (int j = 0; j < kb; ++j) {
-        double s = row[j];
-        const double* lj = S + (k0 + j) * ld + k0;
-        for (int t = 0; t < j; ++t) s = fma(-row[t], lj[t], s);
-        row[j] = s * rdiag[j];
-      }
-    }
-    __syncthreads();
-    // (3) trailing update A22 -= L21 L21^T (lower triangle)
-    for (int i = k0 + kb + ty; i < m; i += SM_NT / 32) {
-      const double* li = S + i * ld + k0;
-      for (int c = k0 + kb + tx; c <= i; c += 32) {
-        const double* lc = S + c * ld + k0;
-        double s = 0.0;
-        for (int t = 0; t < kb; ++t) s = fma(li[t], lc[t], s);
-        S[i * ld + c] -= s;
-      }
-    }
-    __syncthreads();
-  }
-  // forward L z = y and backward L^T x = z: diagonal block by warp 0 with shuffles,
-  // off-diagonal updates by all threads
-  for (int k0 = 0; k0 < m; k0 += 32) {
-    const int kb = min(32, m - k0);
-    if (warp == 0) {
-      double yv = lane < kb ? y[k0 + lane] : 0.0;
-      for (int j = 0; j < kb; ++j) {
-        if (lane == j) yv = yv / S[(k0 + j) * ld + k0 + j];
-        const double yj = __shfl_sync(0xffffffffu, yv, j);
-        if (lane > j && lane < kb) yv = fma(-S[(k0 + lane) * ld + k0 + j], yj, yv);
-      }
-      if (lane < kb) y[k0 + lane] = yv;
-    }
-    __syncthreads();
-    for (int i = k0 + kb + tid; i < m; i += blockDim.x) {
-      double s = y[i];
-      for (int t = 0; t < kb; ++t) s = fma(-S[i * ld + k0 + t], y[k0 + t], s);
-      y[i] = s;
-    }
-    __syncthreads();
-  }
-  for (int k0 = ((m - 1) / 32) * 32; k0 >= 0; k0 -= 32) {
-    const int kb = min(32, m - k0);
-    if (warp == 0) {
-      double xv = lane < kb ? y[k0 + lane] : 0.0;
-      for (int j = kb - 1; j >= 0; --j) {
-        if (lane == j) xv = xv / S[(k0 + j) * ld + k0 + j];
-        const double xj = __shfl_sync(0xffffffffu, xv, j);
-        if (lane < j) xv = fma(-S[(k0 + j) * ld + k0 + lane], xj, xv);
-      }
-      if (lane < kb) y[k0 + lane] = xv;
-    }
-    __syncthreads();
-    for (int i = tid; i < k0; i += blockDim.x) {
-      double s = y[i];
-      for (int t = 0; t < kb; ++t) s = fma(-S[(k0 + t) * ld + i], y[k0 + t], s);
-      y[i] = s;
-    }
-    __syncthreads();
-  }
-  for (int i = tid; i < m; i += blockDim.x) x[i] = y[i];
-  if (tid == 0) *info = fail;
+__device__ __forceinline__ void tc_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
 }
 
-// Blocked (NB = 16) shared-memory Cholesky + solves for m <= SMALL_M.
-//  - 16 x 16 diagonal blocks: warp 0, lane i holds row i in registers; pivots by
-//    shuffle, rsqrt, no block barrier inside the block;
-//  - panel: one thread per row below, the 16-wide row in registers, reciprocal
-//    pivots (16-step dependent chain);
-//  - trailing update: each thread keeps one L row (16 values) in registers and
-//    sweeps columns, one shared load per FMA;
-//  - substitutions: 16-row diagonal blocks by warp 0 with shuffles, off-diagonal
-//    updates by all threads.  Three block barriers per 16 columns.
-constexpr int NB16 = 16;
-
-__device__ __forceinline__ void warp_chol16(double* S, int ld, int k0, int kb, int lane,
-                                            double* rdiag, int* fail) {
-  double r[NB16];
-#pragma unroll
-  for (int c = 0; c < NB16; ++c)
-    r[c] = (lane < kb && c <= lane) ? S[(k0 + lane) * ld + k0 + c] : (c == lane ? 1.0 : 0.0);
-  double mydiag = 1.0;
-#pragma unroll
-  for (int j = 0; j < NB16; ++j) {
-    double d = __shfl_sync(0xffffffffu, r[j], j);
-    if (j < kb && !(d > 0.0)) {
-      if (lane == 0 && *fail == 0) *fail = k0 + j + 1;
-      d = 1.0;
-    }
-    const double inv = rsqrt(d);
-    const double ljj = d * inv;
-    if (lane == j) mydiag = ljj;
-    r[j] = (lane == j) ? ljj : r[j] * inv;
-#pragma unroll
-    for (int c = j + 1; c < NB16; ++c) {
-      const double lcj = __shfl_sync(0xffffffffu, r[j], c);
-      if (lane >= c) r[c] = fma(-r[j], lcj, r[c]);
-    }
+// column J of the 16x16 diagonal block; template recursion keeps every register
+// index a compile-time constant (no local-memory arrays)
+template <int J>
+__device__ __forceinline__ void tc_diag_step(double (&r)[TC_NB], int lane, int k0, double* rdg,
+                                             int* fail) {
+  double d = __shfl_sync(0xffffffffu, r[J], J);
+  if (!(d > 0.0)) {
+    if (lane == 0 && *fail == 0) *fail = k0 + J + 1;
+    d = 1.0;
   }
-  if (lane < kb) {
-#pragma unroll
-    for (int c = 0; c < NB16; ++c)
-      if (c <= lane) S[(k0 + lane) * ld + k0 + c] = r[c];
-    rdiag[lane] = 1.0 / mydiag;
+  const double inv = rsqrt(d);
+  const double sq = d * inv;
+  if (lane == J) {
+    r[J] = sq;
+    rdg[k0 + J] = inv;
+  } else if (lane > J) {
+    r[J] *= inv;
   }
+#pragma unroll
+  for (int c = J + 1; c < TC_NB; ++c) {
+    const double lcj = __shfl_sync(0xffffffffu, r[J], c);
+    if (lane >= c) r[c] = fma(-r[J], lcj, r[c]);
+  }
+  if constexpr (J + 1 < TC_NB) tc_diag_step<J + 1>(r, lane, k0, rdg, fail);
 }
 
-__global__ void __launch_bounds__(SM_NT, 1) chol_small16_kernel(const double* __restrict__ M, int m,
-                                                                  const double* __restrict__ b,
-                                                                  double scale,
-                                                                  double* __restrict__ x,
-                                                                  int* __restrict__ info) {
+__global__ void __launch_bounds__(TC_NT, 1) chol_tc_kernel(const double* __restrict__ M, int m,
+                                                           const double* __restrict__ b,
+                                                           double scale,
+                                                           double* __restrict__ x,
+                                                           int* __restrict__ info) {
   extern __shared__ double S[];
-  const int ld = m | 1;
-  double* y = S + (size_t)m * ld;
+  const int m16 = (m + TC_NB - 1) / TC_NB * TC_NB;
+  const int ld = m16 + 4;
+  double* rdg = S + (size_t)(m16 + 8) * ld;  // reciprocal pivots, m16
   __shared__ int fail;
-  __shared__ double rdiag[NB16];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) fail = 0;
-  for (int idx = tid; idx < m * m; idx += blockDim.x) {
-    const int i = idx / m, j = idx % m;
-    if (j <= i) S[i * ld + j] = M[(long long)i * m + j];
+  // lower triangle of M, identity tail, b row, zero pad rows (m16, m16 + 8)
+  for (int idx = tid; idx < (m16 + 8) * m16; idx += blockDim.x) {
+    const int i = idx / m16, j = idx % m16;
+    double v = 0.0;
+    if (i < m) {
+      if (j <= i) v = M[(long long)i * m + j];
+    } else if (i < m16) {
+      v = (i == j) ? 1.0 : 0.0;
+    } else if (i == m16) {
+      v = j < m ? scale * b[j] : 0.0;
+    }
+    S[i * ld + j] = v;
   }
-  for (int i = tid; i < m; i += blockDim.x) y[i] = scale * b[i];
   __syncthreads();
-  for (int k0 = 0; k0 < m; k0 += NB16) {
-    const int kb = min(NB16, m - k0);
-    if (warp == 0) warp_chol16(S, ld, k0, kb, lane, rdiag, &fail);
-    __syncthreads();
-    // panel rows below: L21 = A21 L11^{-T}
-    for (int i = k0 + kb + tid; i < m; i += blockDim.x) {
-      double row[NB16];
-#pragma unroll
-      for (int j = 0; j < NB16; ++j) row[j] = j < kb ? S[i * ld + k0 + j] : 0.0;
-#pragma unroll
-      for (int j = 0; j < NB16; ++j) {
-        if (j < kb) {
-          double s = row[j];
-#pragma unroll
-          for (int t = 0; t < j; ++t) s = fma(-row[t], S[(k0 + j) * ld + k0 + t], s);
-          row[j] = s * rdiag[j];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < NB16; ++j)
-        if (j < kb) S[i * ld + k0 + j] = row[j];
-    }
-    __syncthreads();
-    // trailing update A22 -= L21 L21^T: thread (rows by warp, columns by lane)
-    const int r0 = k0 + kb;
-    for (int i = r0 + warp; i < m; i += SM_NT / 32) {
-      double li[NB16];
-#pragma unroll
-      for (int t = 0; t < NB16; ++t) li[t] = t < kb ? S[i * ld + k0 + t] : 0.0;
-      for (int c = r0 + lane; c <= i; c += 32) {
-        const double* lc = S + c * ld + k0;
-        double s = 0.0;
-#pragma unroll
-        for (int t = 0; t < NB16; ++t)
-          if (t < kb) s = fma(li[t], lc[t], s);
-        S[i * ld + c] -= s;
-      }
-    }
-    __syncthreads();
-  }
-  // forward L z = y
-  for (int k0 = 0; k0 < m; k0 += NB16) {
-    const int kb = min(NB16, m - k0);
+  for (int k0 = 0; k0 < m16; k0 += TC_NB) {
+    // (1) diagonal block
     if (warp == 0) {
-      double yv = lane < kb ? y[k0 + lane] : 0.0;
-      const double lrow_diag = lane < kb ? S[(k0 + lane) * ld + k0 + lane] : 1.0;
+      double r[TC_NB];
 #pragma unroll
-      for (int j = 0; j < NB16; ++j) {
-        if (j < kb) {
-          if (lane == j) yv = yv / lrow_diag;
-          const double yj = __shfl_sync(0xffffffffu, yv, j);
-          if (lane > j && lane < kb) yv = fma(-S[(k0 + lane) * ld + k0 + j], yj, yv);
-        }
+      for (int c = 0; c < TC_NB; ++c)
+        r[c] = (lane < TC_NB && c <= lane) ? S[(k0 + lane) * ld + k0 + c] : 0.0;
+      tc_diag_step<0>(r, lane, k0, rdg, &fail);
+      if (lane < TC_NB) {
+#pragma unroll
+        for (int c = 0; c < TC_NB; ++c)
+          if (c <= lane) S[(k0 + lane) * ld + k0 + c] = r[c];
       }
-      if (lane < kb) y[k0 + lane] = yv;
     }
     __syncthreads();
-    for (int i = k0 + kb + tid; i < m; i += blockDim.x) {
-      double s = y[i];
+    // (2) panel TRSM for rows k0+16 .. m16 (the b row included)
+    const int r0 = k0 + TC_NB;
+    for (int i = r0 + tid; i <= m16; i += blockDim.x) {
+      double row[TC_NB];
 #pragma unroll
-      for (int t = 0; t < NB16; ++t)
-        if (t < kb) s = fma(-S[i * ld + k0 + t], y[k0 + t], s);
-      y[i] = s;
+      for (int t = 0; t < TC_NB; ++t) row[t] = S[i * ld + k0 + t];
+      // right-looking inside the row: short dependent chain (mul, fma) per column
+#pragma unroll
+      for (int j = 0; j < TC_NB; ++j) {
+        row[j] *= rdg[k0 + j];
+#pragma unroll
+        for (int t = j + 1; t < TC_NB; ++t) row[t] = fma(-row[j], S[(k0 + t) * ld + k0 + j], row[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < TC_NB; ++t) S[i * ld + k0 + t] = row[t];
+    }
+    __syncthreads();
+    // (3) SYRK: rows [r0, m16 + 8) x cols [r0, m16), lower tiles (I >= C)
+    const int nr = (m16 + 8 - r0) / 8, nc = (m16 - r0) / 8;
+    // tile enumeration: row tile I in [0, nr), col tile C in [0, min(I, nc - 1)]
+    int ntiles = 0;
+    for (int I = 0; I < nr; ++I) ntiles += min(I, nc - 1) + 1;
+    if (nc > 0) {
+      for (int tix = warp; tix < ntiles; tix += TC_NT / 32) {
+        int I = 0, rem = tix;
+        while (rem >= min(I, nc - 1) + 1) { rem -= min(I, nc - 1) + 1; ++I; }
+        const int C = rem;
+        const int ri = r0 + 8 * I, ci = r0 + 8 * C;
+        double* cp = S + (ri + (lane >> 2)) * ld + ci + 2 * (lane & 3);
+        double c0 = cp[0], c1 = cp[1];
+#pragma unroll
+        for (int q = 0; q < TC_NB; q += 4) {
+          const double a = -S[(ri + (lane >> 2)) * ld + k0 + q + (lane & 3)];
+          const double bb = S[(ci + (lane >> 2)) * ld + k0 + q + (lane & 3)];
+          tc_dmma(c0, c1, a, bb);
+        }
+        cp[0] = c0;
+        cp[1] = c1;
+      }
     }
     __syncthreads();
   }
-  // backward L^T x = z
-  for (int k0 = ((m - 1) / NB16) * NB16; k0 >= 0; k0 -= NB16) {
-    const int kb = min(NB16, m - k0);
+  // back substitution L^T x = z (z in row m16, overwritten by x)
+  double* z = S + (size_t)m16 * ld;
+  for (int k0 = m16 - TC_NB; k0 >= 0; k0 -= TC_NB) {
     if (warp == 0) {
-      double xv = lane < kb ? y[k0 + lane] : 0.0;
-      const double ldiag = lane < kb ? S[(k0 + lane) * ld + k0 + lane] : 1.0;
+      double zv = lane < TC_NB ? z[k0 + lane] : 0.0;
 #pragma unroll
-      for (int j = NB16 - 1; j >= 0; --j) {
-        if (j < kb) {
-          if (lane == j) xv = xv / ldiag;
-          const double xj = __shfl_sync(0xffffffffu, xv, j);
-          if (lane < j) xv = fma(-S[(k0 + j) * ld + k0 + lane], xj, xv);
-        }
+      for (int j = TC_NB - 1; j >= 0; --j) {
+        if (lane == j) zv *= rdg[k0 + j];
+        const double xj = __shfl_sync(0xffffffffu, zv, j);
+        if (lane < j) zv = fma(-S[(k0 + j) * ld + k0 + lane], xj, zv);
       }
-      if (lane < kb) y[k0 + lane] = xv;
+      if (lane < TC_NB) z[k0 + lane] = zv;
     }
     __syncthreads();
-    for (int i = tid; i < k0; i += blockDim.x) {
-      double s = y[i];
+    for (int j = tid; j < k0; j += blockDim.x) {
+      double s = z[j];
 #pragma unroll
-      for (int t = 0; t < NB16; ++t)
-        if (t < kb) s = fma(-S[(k0 + t) * ld + i], y[k0 + t], s);
-      y[i] = s;
+      for (int t = 0; t < TC_NB; ++t) s = fma(-S[(k0 + t) * ld + j], z[k0 + t], s);
+      z[j] = s;
     }
     __syncthreads();
   }
-  for (int i = tid; i < m; i += blockDim.x) x[i] = y[i];
+  for (int i = tid; i < m; i += blockDim.x) x[i] = z[i];
   if (tid == 0) *info = fail;
+}
+
+size_t chol_tc_smem(int m) {
+  const int m16 = (m + TC_NB - 1) / TC_NB * TC_NB;
+  return ((size_t)(m16 + 8) * (m16 + 4) + m16) * sizeof(double);
 }
 
 cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
                               int* info, cudaStream_t stream) {
-  if (m <= SMALL_M) {
+  if (m <= TC_MAX) {
     const int mi = (int)m;
-    const size_t smem = ((size_t)mi * (mi | 1) + mi) * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(chol_small16_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    { note_launch(); chol_small16_kernel<<<1, SM_NT, smem, stream>>>(M, mi, b, scale, x, info); }
-    return cudaGetLastError();
-  }
-  if (m <= 0) {
-    const int mi = (int)m;
-    const size_t smem = ((size_t)mi * (mi | 1) + mi) * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(chol_small_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    { note_launch(); chol_small_kernel<<<1, SM_NT, smem, stream>>>(M, mi, b, scale, x, info); }
+    const size_t smem = chol_tc_smem(mi);
+    static size_t attr = 0;
+    if (smem > attr) {
+      cudaError_t e = cudaFuncSetAttribute(chol_tc_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)chol_tc_smem(TC_MAX));
+      if (e != cudaSuccess) return e;
+      attr = chol_tc_smem(TC_MAX);
+    }
+    { note_launch(); chol_tc_kernel<<<1, TC_NT, smem, stream>>>(M, mi, b, scale, x, info); }
     return cudaGetLastError();
   }
   size_t smem = (size_t)(NB * (NB + 1) + PANEL_ROWS * (NB + 1)) * sizeof(double);

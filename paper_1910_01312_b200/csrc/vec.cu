@@ -48,8 +48,11 @@ __global__ void __launch_bounds__(SSNAL_NT) dots_kernel(DotArgs p) {
     for (int j = 0; j < MAXDOT; ++j) p.part[blockIdx.x * MAXDOT + j] = acc[j];
   if (!last_block_arrive(p.ticket, gridDim.x)) return;
   block_fold_partials<MAXDOT>(p.part, gridDim.x, MAXDOT, ops, acc, red);
-  if (threadIdx.x == 0)
-    for (int j = 0; j < p.k; ++j) p.out[j] = acc[j];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < MAXDOT; ++j)
+      if (j < p.k) p.out[j] = acc[j];
+  }
 }
 
 size_t reduce_ws_bytes(long long n) {

@@ -1,0 +1,50 @@
+"""Dev microbenchmarks of latency-bound kernels (CUDA events, warm, per call)."""
+import sys; sys.path.insert(0, '.')
+import numpy as np, torch
+import __graft_entry__ as g; g.build()
+from paper_1910_01312_b200.backend import default_backend
+from paper_1910_01312_b200 import projection
+be = default_backend()
+def timeit(fn, reps=50):
+    """GPU time per call: the calls captured into one CUDA graph, replayed (no host gaps)."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3): fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        for _ in range(reps): fn()
+    gr.replay(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    gr.replay()
+    e1.record(); e1.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / reps
+rng = np.random.default_rng(0)
+for m in (32, 64, 115, 160, 200, 300):
+    B = rng.standard_normal((m, m + 5)); M0 = torch.from_numpy(np.eye(m) + 10 * B @ B.T / m).cuda()
+    M = M0.clone(); b = torch.from_numpy(rng.standard_normal(m)).cuda(); x = be.empty(m); info = be.zeros(1, torch.int32)
+    def f():
+        M.copy_(M0); be.chol_solve(M, m, b, 1.0, x, info)
+    t = timeit(f)
+    tc = timeit(lambda: M.copy_(M0))
+    xs = np.linalg.solve(M0.cpu().numpy(), b.cpu().numpy())
+    print(f"chol m={m}: {t - tc:.1f} us  err={np.abs(x.cpu().numpy()-xs).max():.2e}")
+for n in (50_000, 1_000_000):
+    a = np.where(rng.random(n) < .5, 1., -1.); v = torch.from_numpy(rng.standard_normal(n)).cuda()
+    box = projection.BoxLineSet(a, 0.0, np.zeros(n), np.ones(n))
+    st = be.new_states(4); xo = be.empty((4, n)); fo = be.zeros((4, n), torch.uint8)
+    Bv = torch.from_numpy(rng.standard_normal(n) * 1e-3).cuda()
+    be.project(v, box, st, 1, x_out=xo, free_out=fo)
+    lam = float(be.read_states(st.cpu())[0]['lam'])
+    t1 = timeit(lambda: be.project(v, box, st, 1, x_out=xo, free_out=fo, hint=lam))
+    t4 = timeit(lambda: be.project(v, box, st, 4, B=Bv, coefs=[1, .5, .25, .125], x_out=xo, free_out=fo, hint=lam))
+    tc = timeit(lambda: be.project(v, box, st, 1, x_out=xo, free_out=fo, hint=0.0))
+    print(f"project n={n}: warm T=1 {t1:.1f} us, warm T=4 {t4:.1f} us, cold-hint T=1 {tc:.1f} us, passes={be.read_states(st.cpu())[0]['passes']}")
+    out = be.zeros(8)
+    w = [torch.from_numpy(rng.standard_normal(n)).cuda() for _ in range(8)]
+    for k in (1, 4):
+        print(f"dots n={n} k={k}: {timeit(lambda: be.dots([(w[j], w[j+4]) for j in range(k)], out)):.1f} us")
+    print(f"vec n={n}: {timeit(lambda: be.vec(2, 0.5, w[0], w[1], None, w[2])):.1f} us")
