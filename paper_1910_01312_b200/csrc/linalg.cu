@@ -203,6 +203,33 @@ __device__ __forceinline__ void tc_diag_step(double (&r)[TC_NB], int lane, int k
   if constexpr (J + 1 < TC_NB) tc_diag_step<J + 1>(r, lane, k0, rdg, fail);
 }
 
+// factor the 16x16 diagonal block at (k0, k0) in place (warp-wide call)
+__device__ __forceinline__ void tc_factor_diag(double* S, int ld, int k0, int lane, double* rdg,
+                                               int* fail) {
+  double r[TC_NB];
+#pragma unroll
+  for (int c = 0; c < TC_NB; ++c)
+    r[c] = (lane < TC_NB && c <= lane) ? S[(k0 + lane) * ld + k0 + c] : 0.0;
+  tc_diag_step<0>(r, lane, k0, rdg, fail);
+  if (lane < TC_NB) {
+#pragma unroll
+    for (int c = 0; c < TC_NB; ++c)
+      if (c <= lane) S[(k0 + lane) * ld + k0 + c] = r[c];
+  }
+}
+
+// S[ri..ri+8)[ci..ci+8) -= L[ri..][k0..k0+16) L[ci..][k0..k0+16)^T  (4 x m8n8k4)
+__device__ __forceinline__ void tc_syrk_tile(double* S, int ld, int k0, int ri, int ci, int lane) {
+  double* cp = S + (ri + (lane >> 2)) * ld + ci + 2 * (lane & 3);
+  double c0 = cp[0], c1 = cp[1];
+  const double* ap = S + (ri + (lane >> 2)) * ld + k0 + (lane & 3);
+  const double* bp = S + (ci + (lane >> 2)) * ld + k0 + (lane & 3);
+#pragma unroll
+  for (int q = 0; q < TC_NB; q += 4) tc_dmma(c0, c1, -ap[q], bp[q]);
+  cp[0] = c0;
+  cp[1] = c1;
+}
+
 __global__ void __launch_bounds__(TC_NT, 1) chol_tc_kernel(const double* __restrict__ M, int m,
                                                            const double* __restrict__ b,
                                                            double scale,
@@ -215,35 +242,31 @@ __global__ void __launch_bounds__(TC_NT, 1) chol_tc_kernel(const double* __restr
   __shared__ int fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) fail = 0;
-  // lower triangle of M, identity tail, b row, zero pad rows (m16, m16 + 8)
-  for (int idx = tid; idx < (m16 + 8) * m16; idx += blockDim.x) {
-    const int i = idx / m16, j = idx % m16;
-    double v = 0.0;
-    if (i < m) {
-      if (j <= i) v = M[(long long)i * m + j];
-    } else if (i < m16) {
-      v = (i == j) ? 1.0 : 0.0;
-    } else if (i == m16) {
-      v = j < m ? scale * b[j] : 0.0;
-    }
-    S[i * ld + j] = v;
-  }
-  __syncthreads();
-  for (int k0 = 0; k0 < m16; k0 += TC_NB) {
-    // (1) diagonal block
-    if (warp == 0) {
-      double r[TC_NB];
-#pragma unroll
-      for (int c = 0; c < TC_NB; ++c)
-        r[c] = (lane < TC_NB && c <= lane) ? S[(k0 + lane) * ld + k0 + c] : 0.0;
-      tc_diag_step<0>(r, lane, k0, rdg, &fail);
-      if (lane < TC_NB) {
-#pragma unroll
-        for (int c = 0; c < TC_NB; ++c)
-          if (c <= lane) S[(k0 + lane) * ld + k0 + c] = r[c];
+  // lower triangle of M by asynchronous 8-byte copies (every load in flight at
+  // once: M sits in L2 from the assembling kernel); identity tail, b row and zero
+  // padding by plain stores
+  for (int i = warp; i < m16 + 8; i += TC_NT / 32) {
+    for (int j = lane; j < m16; j += 32) {
+      if (i < m && j <= i) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(S + i * ld + j);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst),
+                     "l"(M + (long long)i * m + j));
+      } else {
+        double v = 0.0;
+        if (i >= m && i < m16) v = (i == j) ? 1.0 : 0.0;
+        else if (i == m16) v = j < m ? scale * b[j] : 0.0;
+        S[i * ld + j] = v;
       }
     }
-    __syncthreads();
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  // diagonal block 0; afterwards every diagonal block is factored by warp 0 right
+  // after it has applied the previous panel's update to that block, overlapping the
+  // other warps' trailing update (one-panel look-ahead)
+  if (warp == 0) tc_factor_diag(S, ld, 0, lane, rdg, &fail);
+  __syncthreads();
+  for (int k0 = 0; k0 < m16; k0 += TC_NB) {
     // (2) panel TRSM for rows k0+16 .. m16 (the b row included)
     const int r0 = k0 + TC_NB;
     for (int i = r0 + tid; i <= m16; i += blockDim.x) {
@@ -261,27 +284,33 @@ __global__ void __launch_bounds__(TC_NT, 1) chol_tc_kernel(const double* __restr
       for (int t = 0; t < TC_NB; ++t) S[i * ld + k0 + t] = row[t];
     }
     __syncthreads();
-    // (3) SYRK: rows [r0, m16 + 8) x cols [r0, m16), lower tiles (I >= C)
+    // (3) SYRK: rows [r0, m16 + 8) x cols [r0, m16), lower tiles (I >= C).  The three
+    // tiles of the next diagonal block (I, C < 2) go to warp 0, which then factors
+    // that block; the other warps take the remaining tiles round-robin.
     const int nr = (m16 + 8 - r0) / 8, nc = (m16 - r0) / 8;
-    // tile enumeration: row tile I in [0, nr), col tile C in [0, min(I, nc - 1)]
-    int ntiles = 0;
-    for (int I = 0; I < nr; ++I) ntiles += min(I, nc - 1) + 1;
     if (nc > 0) {
-      for (int tix = warp; tix < ntiles; tix += TC_NT / 32) {
-        int I = 0, rem = tix;
-        while (rem >= min(I, nc - 1) + 1) { rem -= min(I, nc - 1) + 1; ++I; }
-        const int C = rem;
-        const int ri = r0 + 8 * I, ci = r0 + 8 * C;
-        double* cp = S + (ri + (lane >> 2)) * ld + ci + 2 * (lane & 3);
-        double c0 = cp[0], c1 = cp[1];
-#pragma unroll
-        for (int q = 0; q < TC_NB; q += 4) {
-          const double a = -S[(ri + (lane >> 2)) * ld + k0 + q + (lane & 3)];
-          const double bb = S[(ci + (lane >> 2)) * ld + k0 + q + (lane & 3)];
-          tc_dmma(c0, c1, a, bb);
+      if (warp == 0) {
+        tc_syrk_tile(S, ld, k0, r0, r0, lane);
+        tc_syrk_tile(S, ld, k0, r0 + 8, r0, lane);
+        tc_syrk_tile(S, ld, k0, r0 + 8, r0 + 8, lane);
+        __syncwarp();
+        tc_factor_diag(S, ld, r0, lane, rdg, &fail);
+      } else {
+        // tiles after the first three, in (I, C) order; warp w takes every 15th
+        // starting at w - 1: walk (I, C) forward without divisions
+        int I = 2, C = 0, skip = warp - 1;
+        while (I < nr) {
+          const int rowlen = min(I, nc - 1) + 1;
+          if (C + skip < rowlen) {
+            C += skip;
+            tc_syrk_tile(S, ld, k0, r0 + 8 * I, r0 + 8 * C, lane);
+            skip = TC_NT / 32 - 1;
+          } else {
+            skip -= rowlen - C;
+            C = 0;
+            ++I;
+          }
         }
-        cp[0] = c0;
-        cp[1] = c1;
       }
     }
     __syncthreads();
