@@ -18,8 +18,12 @@ namespace ssnal {
 
 namespace {
 
-constexpr int NSTAGE = 4;
-constexpr int STAGE_BYTES = 48 * 1024;
+#ifndef SSNAL_NSTAGE
+#define SSNAL_NSTAGE 4
+#define SSNAL_STAGE_KB 48
+#endif
+constexpr int NSTAGE = SSNAL_NSTAGE;
+constexpr int STAGE_BYTES = SSNAL_STAGE_KB * 1024;
 constexpr int NCONS = 8;                      // consumer warps
 constexpr int NTHREADS = (NCONS + 1) * 32;    // + one producer warp
 constexpr int ROWS_CTA = 512;                 // rows per CTA slab (coefficients fit in smem)
@@ -201,6 +205,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
     if (lane == 0 && r1 > r0) produce(p, r0, r1, ring, full, empty);
     return;
   }
+  // row signs of the slab staged once (a global load per row sat on the critical path
+  // of every row's reduction)
+  __shared__ double rs_s[ROWS_CTA];
+  for (long long r = threadIdx.x; r < r1 - r0; r += NCONS * 32) rs_s[r] = p.rs ? p.rs[r0 + r] : 1.0;
+  asm volatile("bar.sync 1, %0;" ::"r"(NCONS * 32) : "memory");
   const long long pairs = p.q / 2;
   // this lane's slice of d: pairs lane, lane+32, ... (CP*... <= 8 per lane for q <= 512)
   double2 dv[KV][CP * 2];
@@ -220,28 +229,48 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
     const int nr = (int)min((long long)p.rows_per_stage, r1 - rb);
     mbar_wait(&full[s], (uint32_t)((ch / NSTAGE) & 1));
     const double* st = reinterpret_cast<const double*>(ring + (size_t)s * STAGE_BYTES);
-    for (int r = warp; r < nr; r += NCONS) {
+    // two rows per warp iteration: their shuffle trees interleave
+    for (int r = warp; r < nr; r += 2 * NCONS) {
+      const int r2 = r + NCONS;
+      const bool two = r2 < nr;
       const double2* row = reinterpret_cast<const double2*>(st + (size_t)r * p.lda);
-      double acc[KV];
+      const double2* row2 = reinterpret_cast<const double2*>(st + (size_t)(two ? r2 : r) * p.lda);
+      double acc[KV], acc2[KV];
 #pragma unroll
-      for (int j = 0; j < KV; ++j) acc[j] = 0.0;
+      for (int j = 0; j < KV; ++j) acc[j] = acc2[j] = 0.0;
 #pragma unroll
       for (int c = 0; c < CP * 2; ++c) {
         const long long pc = lane + 32LL * c;
         if (pc < pairs) {
           const double2 a = row[pc];
+          const double2 b2 = row2[pc];
 #pragma unroll
-          for (int j = 0; j < KV; ++j) acc[j] = fma(a.y, dv[j][c].y, fma(a.x, dv[j][c].x, acc[j]));
+          for (int j = 0; j < KV; ++j) {
+            acc[j] = fma(a.y, dv[j][c].y, fma(a.x, dv[j][c].x, acc[j]));
+            acc2[j] = fma(b2.y, dv[j][c].y, fma(b2.x, dv[j][c].x, acc2[j]));
+          }
         }
       }
-      const long long gr = rb + r;
 #pragma unroll
-      for (int j = 0; j < KV; ++j) {
-        const double sum = warp_sum(acc[j]);
-        if (lane == 0) {
-          const double val = p.rs ? p.rs[gr] * sum : sum;
-          p.out[(long long)j * p.nlog + gr] = val;
-          if (p.svr) p.out[(long long)j * p.nlog + gr + p.n] = -val;
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int j = 0; j < KV; ++j) {
+          acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+          acc2[j] += __shfl_xor_sync(0xffffffffu, acc2[j], o);
+        }
+      }
+      if (lane == 0) {
+        const int rl = (int)(rb - r0) + r;
+#pragma unroll
+        for (int j = 0; j < KV; ++j) {
+          const double val = rs_s[rl] * acc[j];
+          p.out[(long long)j * p.nlog + rb + r] = val;
+          if (p.svr) p.out[(long long)j * p.nlog + rb + r + p.n] = -val;
+          if (two) {
+            const double val2 = rs_s[rl + NCONS] * acc2[j];
+            p.out[(long long)j * p.nlog + rb + r2] = val2;
+            if (p.svr) p.out[(long long)j * p.nlog + rb + r2 + p.n] = -val2;
+          }
         }
       }
     }

@@ -48,3 +48,25 @@ for n in (50_000, 1_000_000):
     for k in (1, 4):
         print(f"dots n={n} k={k}: {timeit(lambda: be.dots([(w[j], w[j+4]) for j in range(k)], out)):.1f} us")
     print(f"vec n={n}: {timeit(lambda: be.vec(2, 0.5, w[0], w[1], None, w[2])):.1f} us")
+# streaming products on config-1 shapes (A 50000 x 300, 120 MB)
+from paper_1910_01312_b200 import operators
+n, q = 50_000, 300
+A = torch.from_numpy(rng.standard_normal((n, q))).cuda()
+y = torch.from_numpy(np.where(rng.random(n) < .5, 1., -1.)).cuda()
+op = operators.LinearKernelOperator(A, labels=y)
+v = torch.from_numpy(rng.standard_normal(n)).cuda(); d = torch.from_numpy(rng.standard_normal((1, q))).cuda()
+gr = be.empty((2, q)); out = be.empty((1, n))
+flush = torch.empty(256 << 20, dtype=torch.uint8, device='cuda')
+t_f = timeit(lambda: flush.fill_(1), reps=10)
+t_xd = timeit(lambda: (flush.fill_(1), op.x(d, out, k=1)), reps=10) - t_f
+t_xt = timeit(lambda: (flush.fill_(1), op.xt([v], gr)), reps=10) - t_f
+t_xd_w = timeit(lambda: op.x(d, out, k=1), reps=20)
+t_xt_w = timeit(lambda: op.xt([v], gr), reps=20)
+gb = n * q * 8 / 1e9
+print(f"xd cold {t_xd:.1f} us ({gb/t_xd*1e6:.0f} GB/s)  warm {t_xd_w:.1f} us ({gb/t_xd_w*1e6:.0f} GB/s)")
+print(f"xt cold {t_xt:.1f} us ({gb/t_xt*1e6:.0f} GB/s)  warm {t_xt_w:.1f} us ({gb/t_xt_w*1e6:.0f} GB/s)")
+dd = d[0].clone()
+t_mv = timeit(lambda: (flush.fill_(1), torch.mv(A, dd)), reps=10) - t_f
+t_sum = timeit(lambda: (flush.fill_(1), A.sum()), reps=10) - t_f
+t_cp = timeit(lambda: (flush.fill_(1), flush[:n*q*8//2].copy_(flush[n*q*8//2:n*q*8])), reps=10) - t_f
+print(f"reference points (cold): cuBLAS dgemv {t_mv:.1f} us ({gb/t_mv*1e6:.0f} GB/s), torch sum {t_sum:.1f} us ({gb/t_sum*1e6:.0f} GB/s), 60MB->60MB copy {t_cp:.1f} us ({gb/t_cp*1e6:.0f} GB/s r+w)")
