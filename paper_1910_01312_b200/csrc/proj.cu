@@ -644,6 +644,217 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_fused_kernel(ProjArgs p, double
   st->in_count = -1;
 }
 
+// ------------------------------------------------------------------ cluster
+// Small-n variant (n <= CL_CTAS * CL_NT * CL_EPT, e.g. the 50,000-slot config-1
+// dual): one thread-block CLUSTER of 16 CTAs per trial, every slot's (v, a) held in
+// registers across all passes (read from HBM/L2 once), and the per-pass reduction
+// exchanged through distributed shared memory: each CTA publishes its 8-value
+// partial, one cluster barrier, every CTA folds the 16 partials in rank order (so
+// all hold identical state) and takes the Newton step itself.  No grid-wide
+// barrier, no second launch, and the T line-search trials run as T independent
+// clusters side by side.  Partials are double-buffered by pass parity: a CTA can
+// only overwrite a buffer after every CTA has passed the following barrier.
+static constexpr int CL_CTAS = 16;
+static constexpr int CL_NT = 512;
+static constexpr int CL_EPT = 8;
+static constexpr int CL_MAX_PASSES = 12;
+static constexpr int CL_SMEM = 2 * CL_EPT * CL_NT * (int)sizeof(double);
+
+__global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
+    proj_cluster_kernel(ProjArgs p, double hint) {
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ double red[8 * 32];
+  __shared__ double gath[2][CL_CTAS][8];  // [pass parity][source rank][slot], filled by pushes
+  __shared__ double res[8];
+  __shared__ double sh[8];
+  __shared__ int sh_status;
+  // breakpoints do not depend on lambda: computed once (two divisions per slot),
+  // kept in shared memory beside the registers holding v and a
+  extern __shared__ double bp_dyn[];  // [2][CL_EPT][CL_NT]
+  double (*bpa)[CL_NT] = reinterpret_cast<double (*)[CL_NT]>(bp_dyn);
+  double (*bpb)[CL_NT] = reinterpret_cast<double (*)[CL_NT]>(bp_dyn + CL_EPT * CL_NT);
+  const unsigned rank = cluster.block_rank();
+  const int t = blockIdx.y;
+  const int tid = threadIdx.x;
+  const long long stride = (long long)CL_CTAS * CL_NT;
+  const long long base = (long long)rank * CL_NT + tid;
+  double v[CL_EPT], a[CL_EPT];
+  // all loads first (every element's request in flight at once), then the math
+#pragma unroll
+  for (int k = 0; k < CL_EPT; ++k) {
+    const long long i = min(base + k * stride, p.n - 1);
+    v[k] = __ldg(p.A + i);
+    a[k] = __ldg(p.a + i);
+  }
+  if (p.B) {
+    double bv[CL_EPT];
+#pragma unroll
+    for (int k = 0; k < CL_EPT; ++k) bv[k] = __ldg(p.B + min(base + k * stride, p.n - 1));
+#pragma unroll
+    for (int k = 0; k < CL_EPT; ++k) v[k] = __dsub_rn(v[k], __dmul_rn(p.coef[t], bv[k]));
+  }
+#pragma unroll
+  for (int k = 0; k < CL_EPT; ++k) {
+    const long long i = base + k * stride;
+    if (i >= p.n) { v[k] = 0.0; a[k] = 0.0; }
+    double ta = 0.0, tb = 0.0;
+    if (a[k] != 0.0) {
+      const double l = p.l ? p.l[i] : p.lc, u = p.u ? p.u[i] : p.uc;
+      const double t1 = __ddiv_rn(__dsub_rn(v[k], u), a[k]);
+      const double t2 = __ddiv_rn(__dsub_rn(v[k], l), a[k]);
+      ta = fmin(t1, t2);
+      tb = fmax(t1, t2);
+    }
+    bpa[k][tid] = ta;
+    bpb[k][tid] = tb;
+  }
+  double c = hint, lo = -INFINITY, hi = INFINITY, lam = 0.0, tmin = INFINITY, tmax = -INFINITY;
+  int status = PROJ_NEWTON, passes = 0;
+  const int ops[8] = {0, 0, 0, 1, 2, 1, 2, 0};
+  for (int pass = 0; status == PROJ_NEWTON && pass < CL_MAX_PASSES; ++pass) {
+    double vals[8] = {0.0, 0.0, 0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0.0};
+#pragma unroll
+    for (int k = 0; k < CL_EPT; ++k) {
+      const long long i = base + k * stride;
+      if (i >= p.n || a[k] == 0.0) continue;
+      const double l = p.l ? p.l[i] : p.lc, u = p.u ? p.u[i] : p.uc;
+      const double ta = bpa[k][tid], tb = bpb[k][tid];
+      vals[0] += contrib(v[k], a[k], l, u, c);
+      const double a2 = a[k] * a[k];
+      if (ta <= c && c < tb) vals[1] += a2;
+      if (ta < c && c <= tb) vals[2] += a2;
+      if (ta > c) vals[3] = fmin(vals[3], ta); else if (ta < c) vals[4] = fmax(vals[4], ta);
+      if (tb > c) vals[3] = fmin(vals[3], tb); else if (tb < c) vals[4] = fmax(vals[4], tb);
+      vals[5] = fmin(vals[5], ta);
+      vals[6] = fmax(vals[6], tb);
+      vals[7] += 1.0;
+    }
+    block_reduce<8>(vals, ops, red);
+    const int buf = pass & 1;
+    // push this CTA's partial into slot [rank] of every CTA of the cluster
+    if (tid == 0)
+      for (int k = 0; k < 8; ++k) red[k] = vals[k];
+    __syncthreads();
+    if (tid < CL_CTAS * 8) {
+      double* dst = cluster.map_shared_rank(&gath[buf][rank][0], tid >> 3);
+      dst[tid & 7] = red[tid & 7];
+    }
+    cluster.sync();  // arrive.release / wait.acquire: every push of this pass is visible
+    if (tid < 8) {
+      const int op = (tid == 3 || tid == 5) ? 1 : ((tid == 4 || tid == 6) ? 2 : 0);  // = ops[tid]
+      double r = gath[buf][0][tid];
+      for (int q = 1; q < CL_CTAS; ++q) {
+        const double x = gath[buf][q][tid];
+        r = op == 0 ? r + x : (op == 1 ? fmin(r, x) : fmax(r, x));
+      }
+      res[tid] = r;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (pass == 0) { tmin = res[5]; tmax = res[6]; }
+      if (res[7] == 0.0) {
+        lam = 0.0;
+        status = PROJ_DONE;
+      } else {
+        newton_update(p.d - res[0], res[1], res[2], res[3], res[4], tmin, p.d, c, lo, hi, lam,
+                      status);
+      }
+      sh[0] = c; sh[1] = lo; sh[2] = hi; sh[3] = lam; sh[4] = tmin; sh[5] = tmax;
+      sh_status = status;
+    }
+    __syncthreads();
+    c = sh[0]; lo = sh[1]; hi = sh[2]; lam = sh[3]; tmin = sh[4]; tmax = sh[5];
+    status = sh_status;
+    passes = pass + 1;
+  }
+  // apply at lambda: x, free mask, the six fused sums
+  double s6[6] = {0, 0, 0, 0, 0, 0};
+  if (status == PROJ_DONE) {
+    double* xo = p.x_out ? p.x_out + (long long)t * p.n : nullptr;
+    unsigned char* fo = p.free_out ? p.free_out + (long long)t * p.n : nullptr;
+#pragma unroll
+    for (int k = 0; k < CL_EPT; ++k) {
+      const long long i = base + k * stride;
+      if (i >= p.n) continue;
+      const double l = p.l ? p.l[i] : p.lc, u = p.u ? p.u[i] : p.uc;
+      const double y = __dsub_rn(v[k], __dmul_rn(lam, a[k]));
+      const double x = fmin(fmax(y, l), u);
+      const bool lower = y <= __dadd_rn(l, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(l))));
+      const bool upper = !lower && (y >= __dsub_rn(u, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(u)))));
+      const bool fr = !(lower || upper);
+      if (xo) xo[i] = x;
+      if (fo) fo[i] = fr ? 1 : 0;
+      const double r = v[k] - x;
+      s6[0] += v[k] * v[k];
+      s6[1] += r * r;
+      if (p.ref) { const double dd = x - p.ref[i]; s6[2] += dd * dd; }
+      if (fr) { s6[3] += a[k] * a[k]; s6[4] += 1.0; }
+      s6[5] += x * (2.0 * v[k] - x);
+    }
+  }
+  const int ops6[6] = {0, 0, 0, 0, 0, 0};
+  block_reduce<6>(s6, ops6, red);
+  const int buf = passes & 1;  // the buffer no CTA can still be reading
+  if (tid == 0)
+    for (int k = 0; k < 6; ++k) red[k] = s6[k];
+  __syncthreads();
+  if (tid < 6) {
+    double* dst = cluster.map_shared_rank(&gath[buf][rank][0], 0);
+    dst[tid] = red[tid];
+  }
+  // every CTA arrives (release); only rank 0 waits and folds, the others may exit:
+  // after the last pass barrier nothing else is written into their shared memory
+  cluster.barrier_arrive();
+  if (rank != 0) return;
+  cluster.barrier_wait();
+  if (tid == 0) {
+    ProjState* st = p.st + t;
+    if (status == PROJ_DONE) {
+      double r[6];
+      for (int k = 0; k < 6; ++k) {
+        r[k] = gath[buf][0][k];
+        for (int q = 1; q < CL_CTAS; ++q) r[k] += gath[buf][q][k];
+      }
+      st->sum_v2 = r[0];
+      st->sum_r2 = r[1];
+      st->sum_dref2 = r[2];
+      st->sum_a2_free = r[3];
+      st->nfree = (long long)r[4];
+      st->sum_xv = r[5];
+      st->lam = lam;
+      st->status = PROJ_APPLIED;
+    } else {
+      st->lam = c;
+      st->lo = lo;
+      st->hi = hi;
+      st->status = status;
+    }
+    st->tmin = tmin;
+    st->tmax = tmax;
+    st->passes = passes;
+    st->in_count = -1;
+  }
+}
+
+static bool cluster_ok(long long n, int T) {
+  static int ok = -1;
+  if (ok < 0) {
+    int dev = 0, sup = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sup, cudaDevAttrClusterLaunch, dev);
+    ok = sup ? 1 : 0;
+    if (ok && cudaFuncSetAttribute(proj_cluster_kernel,
+                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      ok = 0;
+    if (ok && cudaFuncSetAttribute(proj_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   CL_SMEM) != cudaSuccess)
+      ok = 0;
+  }
+  // single trials keep the grid-wide fused kernel (measured equal or faster at T = 1);
+  // batched line-search trials run as independent clusters
+  return ok == 1 && n <= (long long)CL_CTAS * CL_NT * CL_EPT && T >= 2;
+}
+
 int proj_blocks(long long n) {
   long long b = ceil_div(n, (long long)SSNAL_NT * 4);
   if (b < 1) b = 1;
@@ -675,6 +886,11 @@ cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
   p.lc = L.lc; p.uc = L.uc; p.d = L.d; p.n = L.n; p.st = L.st; p.part = L.part;
   p.x_out = L.x_out; p.free_out = L.free_out; p.ref = L.ref;
   const int nblk = proj_blocks(L.n);
+  if (L.newton > 0 && L.passes == 0 && L.phases == PHASE_APPLY && cluster_ok(L.n, L.T)) {
+    note_launch();
+    proj_cluster_kernel<<<dim3(CL_CTAS, L.T), CL_NT, CL_SMEM, stream>>>(p, L.hint);
+    return cudaGetLastError();
+  }
   const int nbf = std::min(nblk, fused_capacity() / L.T);  // co-resident grid for grid.sync
   if (L.newton > 0 && L.passes == 0 && L.phases == PHASE_APPLY && nbf >= 1) {
     int* active = (int*)((char*)L.part + (size_t)3 * L.T * nblk * PSTRIDE * sizeof(double));
