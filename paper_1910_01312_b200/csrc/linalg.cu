@@ -4,8 +4,12 @@
 // followed by blocked forward / backward substitution -- all inside ONE CTA so
 // the factor never leaves L2 and no host round trip is needed.
 // Replaces scipy.linalg.solve(..., assume_a="sym") of ref solver.py:175-191.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "ssnal_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace ssnal {
 
@@ -341,6 +345,198 @@ __global__ void __launch_bounds__(TC_NT, 1) chol_tc_kernel(const double* __restr
   if (tid == 0) *info = fail;
 }
 
+
+// ---------------------------------------------------------------------------
+// Grid-wide SPD solve for 160 < m <= 2048 (q-space systems of configs 1/4, p-space
+// systems up to direct_solve_threshold): M (row-major, lower triangle used) stays in
+// L2; one cooperative launch over all SMs, three grid barriers per 32-column panel:
+//   (1) CTA 0: 32x32 diagonal block (warp 0, registers + shuffles; identity-padded
+//       past m) and the forward-substitution block z_k = L_kk^{-1} z_k;
+//   (2) all CTAs: panel TRSM, one thread per row below (row in registers, L_kk and
+//       its reciprocal pivots staged in each CTA's shared memory);
+//   (3) all warps: trailing SYRK as 8x8 DMMA tiles (k = 32: eight m8n8k4 per tile)
+//       plus the forward update of z below the panel.
+// Back substitution L^T x = z by CTA 0 (32-blocks: warp shuffle solve + column
+// update).  Replaces the single-CTA blocked kernel, which was latency-bound on one
+// SM for these sizes.
+static constexpr int BG_NB = 32;
+static constexpr int BG_NT = 256;
+
+template <int J>
+__device__ __forceinline__ void bg_diag_step(double (&r)[BG_NB], int lane, double* rd, int k0,
+                                             int* fail) {
+  double d = __shfl_sync(0xffffffffu, r[J], J);
+  if (!(d > 0.0)) {
+    if (lane == 0 && *fail == 0) *fail = k0 + J + 1;
+    d = 1.0;
+  }
+  const double inv = rsqrt(d);
+  const double sq = d * inv;
+  if (lane == J) {
+    r[J] = sq;
+    rd[J] = inv;
+  } else if (lane > J) {
+    r[J] *= inv;
+  }
+#pragma unroll
+  for (int c = J + 1; c < BG_NB; ++c) {
+    const double lcj = __shfl_sync(0xffffffffu, r[J], c);
+    if (lane >= c) r[c] = fma(-r[J], lcj, r[c]);
+  }
+  if constexpr (J + 1 < BG_NB) bg_diag_step<J + 1>(r, lane, rd, k0, fail);
+}
+
+__global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M, int m,
+                                                         const double* __restrict__ b,
+                                                         double scale, double* __restrict__ x,
+                                                         int* __restrict__ info) {
+  // z = scale b is built and solved in place in x
+  double* z = x;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double D[BG_NB][BG_NB + 1];
+  __shared__ double rd[BG_NB];
+  __shared__ int fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long gtid = (long long)blockIdx.x * BG_NT + tid;
+  const long long gthreads = (long long)gridDim.x * BG_NT;
+  const int gwarp = blockIdx.x * (BG_NT / 32) + warp, nwarps = gridDim.x * (BG_NT / 32);
+  if (tid == 0) fail = 0;
+  for (long long i = gtid; i < m; i += gthreads) z[i] = scale * b[i];
+  grid.sync();
+  for (int k0 = 0; k0 < m; k0 += BG_NB) {
+    const int kb = min(BG_NB, m - k0);
+    // (1) diagonal block + forward block
+    if (blockIdx.x == 0 && warp == 0) {
+      double r[BG_NB];
+#pragma unroll
+      for (int c = 0; c < BG_NB; ++c)
+        r[c] = (lane < kb && c < kb && c <= lane) ? M[(long long)(k0 + lane) * m + k0 + c]
+                                                  : (lane == c ? 1.0 : 0.0);
+      bg_diag_step<0>(r, lane, rd, k0, &fail);
+      __syncwarp();
+      if (lane < kb) {
+#pragma unroll
+        for (int c = 0; c < BG_NB; ++c)
+          if (c <= lane && c < kb) M[(long long)(k0 + lane) * m + k0 + c] = r[c];
+      }
+      // z_k = L_kk^{-1} z_k (lane i holds z_i; row i of L_kk in r)
+      double zv = lane < kb ? z[k0 + lane] : 0.0;
+#pragma unroll
+      for (int j = 0; j < BG_NB; ++j) {
+        if (lane == j) zv *= rd[j];
+        const double zj = __shfl_sync(0xffffffffu, zv, j);
+        if (lane > j) zv = fma(-r[j], zj, zv);
+      }
+      if (lane < kb) z[k0 + lane] = zv;
+    }
+    grid.sync();
+    const int r0 = k0 + kb;
+    if (r0 >= m) break;
+    // (2) panel TRSM rows [r0, m)
+    for (int idx = tid; idx < BG_NB * BG_NB; idx += BG_NT) {
+      const int i = idx / BG_NB, j = idx % BG_NB;
+      D[i][j] = (i < kb && j < kb && j <= i) ? M[(long long)(k0 + i) * m + k0 + j] : 0.0;
+    }
+    if (tid < BG_NB) rd[tid] = tid < kb ? 1.0 / M[(long long)(k0 + tid) * m + k0 + tid] : 0.0;
+    __syncthreads();
+    for (long long i = r0 + gtid; i < m; i += gthreads) {
+      double row[BG_NB];
+#pragma unroll
+      for (int t = 0; t < BG_NB; ++t) row[t] = t < kb ? M[i * m + k0 + t] : 0.0;
+#pragma unroll
+      for (int j = 0; j < BG_NB; ++j) {
+        row[j] *= rd[j];
+#pragma unroll
+        for (int t = j + 1; t < BG_NB; ++t) row[t] = fma(-row[j], D[t][j], row[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < BG_NB; ++t)
+        if (t < kb) M[i * m + k0 + t] = row[t];
+    }
+    grid.sync();
+    // (3) SYRK tiles over [r0, m) and the forward update of z
+    const int nt = (m - r0 + 7) / 8;
+    const long long ntiles = (long long)nt * (nt + 1) / 2;
+    for (long long tix = gwarp; tix < ntiles; tix += nwarps) {
+      // tile (I, C), C <= I, from the triangular index
+      int I = (int)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);
+      while ((long long)(I + 1) * (I + 2) / 2 <= tix) ++I;
+      while ((long long)I * (I + 1) / 2 > tix) --I;
+      const int C = (int)(tix - (long long)I * (I + 1) / 2);
+      const int ri = r0 + 8 * I + (lane >> 2), ci = r0 + 8 * C + (lane >> 2);
+      const int cc = r0 + 8 * C + 2 * (lane & 3);
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < BG_NB; q += 4) {
+        const int kk = q + (lane & 3);
+        const double av = (ri < m && kk < kb) ? -M[(long long)ri * m + k0 + kk] : 0.0;
+        const double bv = (ci < m && kk < kb) ? M[(long long)ci * m + k0 + kk] : 0.0;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c0), "+d"(c1)
+                     : "d"(av), "d"(bv));
+      }
+      if (ri < m) {
+        if (cc < m && cc <= ri) M[(long long)ri * m + cc] += c0;
+        if (cc + 1 < m && cc + 1 <= ri) M[(long long)ri * m + cc + 1] += c1;
+      }
+    }
+    for (long long c = r0 + gtid; c < m; c += gthreads) {
+      double s = z[c];
+      for (int t = 0; t < kb; ++t) s = fma(-M[c * m + k0 + t], z[k0 + t], s);
+      z[c] = s;
+    }
+    grid.sync();
+  }
+  if (blockIdx.x != 0) return;
+  // back substitution L^T x = z in CTA 0 (reciprocal pivots staged in shared memory)
+  __shared__ double rdall[2048];
+  for (int i = tid; i < m; i += BG_NT) rdall[i] = 1.0 / M[(long long)i * m + i];
+  __syncthreads();
+  for (int k0 = ((m - 1) / BG_NB) * BG_NB; k0 >= 0; k0 -= BG_NB) {
+    const int kb = min(BG_NB, m - k0);
+    if (warp == 0) {
+      // column `lane` of the block (L[k0+j][k0+lane], j = 0..31) into registers first:
+      // the 32-step chain below then never waits on L2
+      double col[BG_NB];
+#pragma unroll
+      for (int j = 0; j < BG_NB; ++j)
+        col[j] = (j < kb && lane < j) ? M[(long long)(k0 + j) * m + k0 + lane] : 0.0;
+      double zv = lane < kb ? z[k0 + lane] : 0.0;
+#pragma unroll
+      for (int j = BG_NB - 1; j >= 0; --j) {
+        if (j < kb) {
+          if (lane == j) zv *= rdall[k0 + j];
+          const double xj = __shfl_sync(0xffffffffu, zv, j);
+          if (lane < j) zv = fma(-col[j], xj, zv);
+        }
+      }
+      if (lane < kb) z[k0 + lane] = zv;
+    }
+    __syncthreads();
+    for (int j = tid; j < k0; j += BG_NT) {
+      double s = z[j];
+      for (int t = 0; t < kb; ++t) s = fma(-M[(long long)(k0 + t) * m + j], z[k0 + t], s);
+      z[j] = s;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < m; i += BG_NT) x[i] = z[i];
+  if (tid == 0) *info = fail;
+}
+
+static int big_grid() {
+  static int g = -1;
+  if (g < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chol_big_kernel, BG_NT, 0);
+    g = sms * (per < 1 ? 1 : (per > 2 ? 2 : per));
+  }
+  return g;
+}
+
+
 size_t chol_tc_smem(int m) {
   const int m16 = (m + TC_NB - 1) / TC_NB * TC_NB;
   return ((size_t)(m16 + 8) * (m16 + 4) + m16) * sizeof(double);
@@ -361,6 +557,13 @@ cudaError_t launch_chol_solve(double* M, long long m, const double* b, double sc
     }
     { note_launch(); chol_tc_kernel<<<1, TC_NT, smem, stream>>>(M, mi, b, scale, x, info); }
     return cudaGetLastError();
+  }
+  if (m <= 2048) {
+    int mi = (int)m;
+    void* args[] = {&M, &mi, (void*)&b, &scale, &x, &info};
+    note_launch();
+    return cudaLaunchCooperativeKernel((void*)chol_big_kernel, dim3(big_grid()), dim3(BG_NT), args,
+                                       0, stream);
   }
   size_t smem = (size_t)(NB * (NB + 1) + PANEL_ROWS * (NB + 1)) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -23,7 +23,7 @@ def timeit(fn, reps=50):
     e1.record(); e1.synchronize()
     return e0.elapsed_time(e1) * 1e3 / reps
 rng = np.random.default_rng(0)
-for m in (32, 64, 115, 160, 200, 300):
+for m in (32, 64, 115, 160, 200, 300, 500, 1000, 2000):
     B = rng.standard_normal((m, m + 5)); M0 = torch.from_numpy(np.eye(m) + 10 * B @ B.T / m).cuda()
     M = M0.clone(); b = torch.from_numpy(rng.standard_normal(m)).cuda(); x = be.empty(m); info = be.zeros(1, torch.int32)
     def f():

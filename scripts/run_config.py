@@ -22,7 +22,10 @@ if scale != 1.0:
 t0 = time.time()
 cfg = datagen.make_config(k, **kw)
 tgen = time.time() - t0
-if cfg["task"] == "csvc":
+if "indptr" in cfg:
+    pb = P.build_csvc_dual((cfg["indptr"], cfg["indices"], cfg["data"], cfg["shape"]), cfg["y"],
+                           cfg["C"])
+elif cfg["task"] == "csvc":
     pb = P.build_csvc_dual(cfg["A"], cfg["y"], cfg["C"])
 else:
     pb = P.build_svr_dual(cfg["A"], cfg["t"], cfg["C"], cfg["epsilon"])
