@@ -30,6 +30,13 @@ cudaError_t launch_dots(int k, const double* const* xs, const double* const* ys,
                         const uint8_t* mask, long long n, double* out, void* ws, cudaStream_t s);
 cudaError_t launch_vec(int op, long long n, double alpha, const double* x, const double* y,
                        const double* z, double* out, cudaStream_t s);
+cudaError_t launch_hs_apply_dots(const uint8_t* fm, const double* a, const double* y, long long n,
+                                 double beta, const double* add, double alpha, double* out,
+                                 const double* g, const double* w, const double* qw,
+                                 double* dots_out, void* ws, cudaStream_t stream);
+cudaError_t launch_accept(long long n, double alpha, double cu, double* w, const double* d,
+                          double* qw, const double* qd, double* u, double* xp, const double* txj,
+                          uint8_t* fr, const uint8_t* tfj, cudaStream_t stream);
 cudaError_t launch_hs_apply(const uint8_t* fm, const double* a, const double* y, long long n,
                             double beta, const double* add, double alpha, double* out, void* ws,
                             cudaStream_t s);
@@ -623,10 +630,11 @@ struct Driver {
       }
     });
     xd(L.t, L.qdir, 1);
-    timed(SSNAL_OP_VEC, 8.0 * P.n * 5, [&] {
-      ck(launch_hs_apply(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.ws_red, S));
+    // d = -s - sigma P(Qd) and {g'd, w'Qw, w'Qd} in one pass
+    timed(SSNAL_OP_VEC, 8.0 * P.n * 10, [&] {
+      ck(launch_hs_apply_dots(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.grad, L.w,
+                              L.qw, L.scal, L.ws_red, S));
     });
-    dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}}, L.scal, P.n);
     dots({{L.t, nullptr}}, L.scal + 3, P.q);
   }
 
@@ -700,11 +708,10 @@ struct Driver {
   }
 
   void accept(double alpha, int j) {
-    vec(2, alpha, L.w, L.dir, nullptr, L.w);
-    vec(2, alpha, L.qw, L.qdir, nullptr, L.qw);
-    vec(2, -(sigma * alpha), L.u, L.qdir, nullptr, L.u);
-    ck(cudaMemcpyAsync(L.xp, L.tx + (size_t)j * P.n, sizeof(double) * P.n, cudaMemcpyDeviceToDevice, S));
-    ck(cudaMemcpyAsync(L.fr, L.tfree + (size_t)j * P.n, P.n, cudaMemcpyDeviceToDevice, S));
+    timed(SSNAL_OP_VEC, 8.0 * P.n * 8 + 2.0 * P.n, [&] {
+      ck(launch_accept(P.n, alpha, -(sigma * alpha), L.w, L.dir, L.qw, L.qdir, L.u, L.xp,
+                       L.tx + (size_t)j * P.n, L.fr, L.tfree + (size_t)j * P.n, S));
+    });
     ck(cudaMemcpyAsync(L.st_cur, L.st_trial + j, sizeof(ProjState), cudaMemcpyDeviceToDevice, S));
   }
 

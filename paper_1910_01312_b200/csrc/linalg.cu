@@ -234,18 +234,40 @@ __device__ __forceinline__ void tc_syrk_tile(double* S, int ld, int k0, int ri, 
   cp[1] = c1;
 }
 
+// p-space mode: the kernel also assembles the Woodbury system from the raw Gram
+// (M = Q_JJ) and projects the solution -- the work of pspace_assemble_kernel and
+// pspace_project_kernel (newton.cu), same expressions and reduction trees
+struct TcPspace {
+  const int32_t* J;
+  const double* grad;
+  const double* a;
+  double sigma, asa;
+};
+
+template <bool PS>
 __global__ void __launch_bounds__(TC_NT, 1) chol_tc_kernel(const double* __restrict__ M, int m,
                                                            const double* __restrict__ b,
                                                            double scale,
                                                            double* __restrict__ x,
-                                                           int* __restrict__ info) {
+                                                           int* __restrict__ info, TcPspace ps) {
   extern __shared__ double S[];
   const int m16 = (m + TC_NB - 1) / TC_NB * TC_NB;
   const int ld = m16 + 4;
   double* rdg = S + (size_t)(m16 + 8) * ld;  // reciprocal pivots, m16
+  double* aJ = rdg + m16;                     // p-space mode: a_J, grad_J, Q a_J
+  double* gJ = aJ + m16;
+  double* qa = gJ + m16;
   __shared__ int fail;
+  __shared__ double red2[2 * 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) fail = 0;
+  if (PS) {
+    for (int r = tid; r < m; r += TC_NT) {
+      const int j = ps.J[r];
+      aJ[r] = ps.a[j];
+      gJ[r] = ps.grad[j];
+    }
+  }
   // lower triangle of M by asynchronous 8-byte copies (every load in flight at
   // once: M sits in L2 from the assembling kernel); identity tail, b row and zero
   // padding by plain stores
@@ -258,13 +280,44 @@ __global__ void __launch_bounds__(TC_NT, 1) chol_tc_kernel(const double* __restr
       } else {
         double v = 0.0;
         if (i >= m && i < m16) v = (i == j) ? 1.0 : 0.0;
-        else if (i == m16) v = j < m ? scale * b[j] : 0.0;
+        else if (i == m16 && !PS) v = j < m ? scale * b[j] : 0.0;
         S[i * ld + j] = v;
       }
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if (PS) {
+    // qa = Q a_J (warp per row, lanes stride the row, warp_sum: pspace_assemble's order)
+    for (int r = warp; r < m; r += TC_NT / 32) {
+      double sacc = 0.0;
+      for (int c = lane; c < m; c += 32) sacc += (c <= r ? S[r * ld + c] : S[c * ld + r]) * aJ[c];
+      sacc = warp_sum(sacc);
+      if (lane == 0) qa[r] = sacc;
+    }
+    __syncthreads();
+    double v2[2] = {0.0, 0.0};  // a'Qa, a'g
+    for (int r = tid; r < m; r += TC_NT) {
+      v2[0] += aJ[r] * qa[r];
+      v2[1] += aJ[r] * gJ[r];
+    }
+    const int ops2[2] = {0, 0};
+    block_reduce<2>(v2, ops2, red2);
+    if (tid == 0) { red2[0] = v2[0]; red2[1] = v2[1]; }
+    __syncthreads();
+    const double aqa = red2[0], ag = red2[1];
+    const bool proj = ps.asa != 0.0;
+    const double inv = proj ? 1.0 / ps.asa : 0.0;
+    for (int i = warp; i < m; i += TC_NT / 32) {
+      for (int c = lane; c <= i; c += 32) {
+        double mm = S[i * ld + c];
+        if (proj) mm = mm - (aJ[i] * qa[c] + qa[i] * aJ[c]) * inv + aqa * inv * inv * aJ[i] * aJ[c];
+        S[i * ld + c] = (i == c ? 1.0 : 0.0) + ps.sigma * mm;
+      }
+    }
+    for (int j = tid; j < m; j += TC_NT) S[m16 * ld + j] = proj ? gJ[j] - aJ[j] * (ag * inv) : gJ[j];
+    __syncthreads();
+  }
   // diagonal block 0; afterwards every diagonal block is factored by warp 0 right
   // after it has applied the previous panel's update to that block, overlapping the
   // other warps' trailing update (one-panel look-ahead)
@@ -341,7 +394,19 @@ __global__ void __launch_bounds__(TC_NT, 1) chol_tc_kernel(const double* __restr
     }
     __syncthreads();
   }
-  for (int i = tid; i < m; i += blockDim.x) x[i] = z[i];
+  if (PS) {  // y <- P_J y = y - (a_J'y / a'a) a_J  (pspace_project_kernel's order)
+    double v1[1] = {0.0};
+    if (ps.asa != 0.0)
+      for (int r = tid; r < m; r += TC_NT) v1[0] += aJ[r] * z[r];
+    const int ops1[1] = {0};
+    block_reduce<1>(v1, ops1, red2);
+    if (tid == 0) red2[0] = v1[0];
+    __syncthreads();
+    const double coef = ps.asa != 0.0 ? red2[0] / ps.asa : 0.0;
+    for (int i = tid; i < m; i += TC_NT) x[i] = ps.asa != 0.0 ? z[i] - coef * aJ[i] : z[i];
+  } else {
+    for (int i = tid; i < m; i += blockDim.x) x[i] = z[i];
+  }
   if (tid == 0) *info = fail;
 }
 
@@ -537,9 +602,29 @@ static int big_grid() {
 }
 
 
-size_t chol_tc_smem(int m) {
+size_t chol_tc_smem(int m, bool ps = false) {
   const int m16 = (m + TC_NB - 1) / TC_NB * TC_NB;
-  return ((size_t)(m16 + 8) * (m16 + 4) + m16) * sizeof(double);
+  return ((size_t)(m16 + 8) * (m16 + 4) + (ps ? 4 : 1) * m16) * sizeof(double);
+}
+
+// p-space Woodbury solve for p <= 160 in one launch: Q (p x p Gram, overwritten
+// only in shared memory), y = P_J (I + sigma P_J Q P_J)^{-1} P_J grad_J
+cudaError_t launch_chol_pspace(const double* Q, long long p, const int32_t* J, const double* grad,
+                               const double* a, double sigma, double asa, double* y, int* info,
+                               cudaStream_t stream) {
+  if (p > TC_MAX) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(chol_tc_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)chol_tc_smem(TC_MAX, true));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  TcPspace ps{J, grad, a, sigma, asa};
+  const int pi = (int)p;
+  { note_launch(); chol_tc_kernel<true><<<1, TC_NT, chol_tc_smem(pi, true), stream>>>(Q, pi, nullptr, 1.0, y, info, ps); }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
@@ -549,13 +634,13 @@ cudaError_t launch_chol_solve(double* M, long long m, const double* b, double sc
     const size_t smem = chol_tc_smem(mi);
     static size_t attr = 0;
     if (smem > attr) {
-      cudaError_t e = cudaFuncSetAttribute(chol_tc_kernel,
+      cudaError_t e = cudaFuncSetAttribute(chol_tc_kernel<false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)chol_tc_smem(TC_MAX));
       if (e != cudaSuccess) return e;
       attr = chol_tc_smem(TC_MAX);
     }
-    { note_launch(); chol_tc_kernel<<<1, TC_NT, smem, stream>>>(M, mi, b, scale, x, info); }
+    { note_launch(); chol_tc_kernel<false><<<1, TC_NT, smem, stream>>>(M, mi, b, scale, x, info, TcPspace{}); }
     return cudaGetLastError();
   }
   if (m <= 2048) {

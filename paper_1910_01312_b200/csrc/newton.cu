@@ -13,6 +13,9 @@
 
 namespace ssnal {
 
+cudaError_t launch_chol_pspace(const double* Q, long long p, const int32_t* J, const double* grad,
+                               const double* a, double sigma, double asa, double* y, int* info,
+                               cudaStream_t stream);
 cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
                               int* info, cudaStream_t stream);
 
@@ -225,6 +228,7 @@ cudaError_t launch_pspace_solve(const int32_t* J, long long p, const double* gra
   double* aJ = vecs;
   double* qa = aJ + p;
   double* b = qa + p;
+  if (p <= 160) return launch_chol_pspace(Q, p, J, grad, a, sigma, asa, y, info, stream);
   { note_launch(); pspace_assemble_kernel<<<1, 1024, 0, stream>>>(J, p, grad, a, sigma, asa, Q, aJ, qa, b); }
   cudaError_t e = launch_chol_solve(Q, p, b, 1.0, y, info, stream);
   if (e != cudaSuccess) return e;
@@ -249,10 +253,15 @@ cudaError_t launch_pspace_direction(const double* A, long long n, long long q, l
   const int ks = gram_ksplit(p, q);
   { note_launch(); rows_gram_kernel<<<dim3(ntile * (ntile + 1) / 2, ks), 256, 0, stream>>>(g, gpart, ntile); }
   { note_launch(); rows_gram_fold_kernel<<<(unsigned)ceil_div(p * p, 256), 256, 0, stream>>>(gpart, p * p, ks, Q); }
-  { note_launch(); pspace_assemble_kernel<<<1, 1024, 0, stream>>>(J, p, grad, a, sigma, asa, Q, aJ, qa, b); }
-  cudaError_t e = launch_chol_solve(Q, p, b, 1.0, y, info, stream);
-  if (e != cudaSuccess) return e;
-  { note_launch(); pspace_project_kernel<<<1, 1024, 0, stream>>>(p, aJ, asa, y); }
+  if (p <= 160) {  // assemble + Cholesky + projection in one single-CTA launch
+    cudaError_t e = launch_chol_pspace(Q, p, J, grad, a, sigma, asa, y, info, stream);
+    if (e != cudaSuccess) return e;
+  } else {
+    { note_launch(); pspace_assemble_kernel<<<1, 1024, 0, stream>>>(J, p, grad, a, sigma, asa, Q, aJ, qa, b); }
+    cudaError_t e = launch_chol_solve(Q, p, b, 1.0, y, info, stream);
+    if (e != cudaSuccess) return e;
+    { note_launch(); pspace_project_kernel<<<1, 1024, 0, stream>>>(p, aJ, asa, y); }
+  }
   { note_launch(); gather_xt_kernel<<<dim3((unsigned)ceil_div(q, 256), GX_SPLIT), 256, 0, stream>>>(g, y, part); }
   { note_launch(); pspace_finish_kernel<<<(unsigned)ceil_div(q, 256), 256, 0, stream>>>(part, q, sigma, g_r, t); }
   return cudaGetLastError();

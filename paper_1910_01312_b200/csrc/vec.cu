@@ -135,6 +135,94 @@ cudaError_t launch_hs_apply(const uint8_t* fm, const double* a, const double* y,
   return cudaGetLastError();
 }
 
+// Newton direction epilogue, one pass: out = alpha*add + beta*P y (as hs_finish) and
+// the three line-search inner products {g'out, w'qw, w'y} of the new direction,
+// folded in fixed order into dots_out[0..2] (replaces hs_finish + a dots launch).
+struct HsDotArgs {
+  const uint8_t* fm;
+  const double* a;
+  const double* y;
+  long long n;
+  double beta, alpha;
+  const double* add;
+  double* out;
+  const double* sums;
+  const double* g;
+  const double* w;
+  const double* qw;
+  double* dots_out;
+  unsigned int* ticket;
+  double* part;
+};
+
+__global__ void __launch_bounds__(SSNAL_NT) hs_finish_dots_kernel(HsDotArgs p) {
+  __shared__ double red[3 * 32];
+  const double ay = p.sums[0], aa = p.sums[1];
+  const double coef = aa != 0.0 ? ay / aa : 0.0;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double yi = p.y[i];
+    double py = p.fm[i] ? __dsub_rn(yi, __dmul_rn(coef, p.a[i])) : 0.0;
+    double r = p.beta * py;
+    if (p.add) r = p.alpha * p.add[i] + r;
+    p.out[i] = r;
+    const double wi = p.w[i];
+    acc[0] += p.g[i] * r;
+    acc[1] += wi * p.qw[i];
+    acc[2] += wi * yi;
+  }
+  const int ops[3] = {0, 0, 0};
+  block_reduce<3>(acc, ops, red);
+  if (threadIdx.x == 0)
+    for (int j = 0; j < 3; ++j) p.part[blockIdx.x * 3 + j] = acc[j];
+  if (!last_block_arrive(p.ticket, gridDim.x)) return;
+  block_fold_partials<3>(p.part, gridDim.x, 3, ops, acc, red);
+  if (threadIdx.x == 0)
+    for (int j = 0; j < 3; ++j) p.dots_out[j] = acc[j];
+}
+
+cudaError_t launch_hs_apply_dots(const uint8_t* fm, const double* a, const double* y, long long n,
+                                 double beta, const double* add, double alpha, double* out,
+                                 const double* g, const double* w, const double* qw,
+                                 double* dots_out, void* ws, cudaStream_t stream) {
+  double* sums = (double*)((char*)ws + reduce_ws_bytes(n));
+  const double* xs[2] = {a, a};
+  const double* ys[2] = {y, nullptr};
+  cudaError_t e = launch_dots(2, xs, ys, fm, n, sums, ws, stream);
+  if (e != cudaSuccess) return e;
+  HsDotArgs p{fm, a, y, n, beta, alpha, add, out, sums, g, w, qw, dots_out,
+              (unsigned int*)ws, (double*)((char*)ws + TICKET_BYTES)};
+  { note_launch(); hs_finish_dots_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(p); }
+  return cudaGetLastError();
+}
+
+// Accepted Armijo step, one pass: w += alpha d, Qw += alpha Qd, u += cu Qd (cu =
+// -sigma alpha), Pi(u) and the free mask from trial j (replaces 3 vec launches + 2 copies;
+// same numpy-ordered arithmetic as vec op 2)
+__global__ void accept_kernel(long long n, double alpha, double cu, double* __restrict__ w,
+                              const double* __restrict__ d, double* __restrict__ qw,
+                              const double* __restrict__ qd, double* __restrict__ u,
+                              double* __restrict__ xp, const double* __restrict__ txj,
+                              uint8_t* __restrict__ fr, const uint8_t* __restrict__ tfj) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double qdi = qd[i];
+    w[i] = __dadd_rn(w[i], __dmul_rn(alpha, d[i]));
+    qw[i] = __dadd_rn(qw[i], __dmul_rn(alpha, qdi));
+    u[i] = __dadd_rn(u[i], __dmul_rn(cu, qdi));
+    xp[i] = txj[i];
+    fr[i] = tfj[i];
+  }
+}
+
+cudaError_t launch_accept(long long n, double alpha, double cu, double* w, const double* d,
+                          double* qw, const double* qd, double* u, double* xp, const double* txj,
+                          uint8_t* fr, const uint8_t* tfj, cudaStream_t stream) {
+  { note_launch(); accept_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(n, alpha, cu, w, d, qw, qd, u, xp, txj, fr, tfj); }
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- compaction
 // Tile = SSNAL_NT threads x CPT contiguous elements; pass 1 counts per tile and
 // the last block scans tile counts; pass 2 writes ascending indices.
