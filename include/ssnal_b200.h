@@ -278,6 +278,16 @@ int ssnal_hs_apply_coef(const uint8_t* free_mask, const double* a, const double*
 int ssnal_qspace_assemble(int64_t m, const double* u, double asa, double sigma, double shift,
                           double* M, void* stream);
 
+/* Fused SsN gradient of the dense operator (ref solver.py:143-148):
+ *   s = w - x_p (written), g_r = X^T s (q), grad = X g_r (n_log), *g2 = ||grad||^2
+ * with *g2 a DEVICE double; two streaming sweeps of A.  ws: ssnal_gradient_ws_bytes
+ * (zero-initialised once; the kernels leave their tickets at zero). */
+size_t ssnal_gradient_ws_bytes(int64_t n_phys, int64_t q);
+int ssnal_dense_gradient(const double* A, int64_t n_phys, int64_t q, int64_t lda,
+                         const double* row_sign, int svr_block, const double* w, const double* xp,
+                         double* s_out, double* g_r, double* grad, double* g2, void* ws,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

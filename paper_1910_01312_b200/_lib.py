@@ -120,6 +120,8 @@ _SIGNATURES.update({
     "ssnal_sum_slices": (_I, [_I, _I64, _P, _P, _P]),
     "ssnal_hs_apply_coef": (_I, [_P, _P, _P, _I64, _D, _P, _D, _D, _P, _P]),
     "ssnal_qspace_assemble": (_I, [_I64, _P, _D, _D, _D, _P, _P]),
+    "ssnal_gradient_ws_bytes": (_SZ, [_I64, _I64]),
+    "ssnal_dense_gradient": (_I, [_P, _I64, _I64, _I64, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
 })
 
 _lib = None

@@ -193,6 +193,14 @@ class CudaBackend:
                     _ptr(op.A), op.n_phys, op.q, op.lda, _ptr(op.row_sign), int(op.svr_block), k,
                     _ptr(d), _ptr(out), self.stream())
 
+    def dense_gradient(self, op, w, xp, s_out, g_r, grad, g2):
+        """s = w - xp, g_r = X^T s, grad = X g_r, g2 = ||grad||^2 (device), fused."""
+        ws = self.ws("gradient", self.lib.ssnal_gradient_ws_bytes(op.n_phys, op.q))
+        self._timed("dense_gradient", 2 * self.dense_bytes(op, 1, "t"), _lib.call,
+                    "ssnal_dense_gradient", _ptr(op.A), op.n_phys, op.q, op.lda, _ptr(op.row_sign),
+                    int(op.svr_block), _ptr(w), _ptr(xp), _ptr(s_out), _ptr(g_r), _ptr(grad),
+                    _ptr(g2), _ptr(ws), self.stream())
+
     def dense_gram(self, op, J, p_dev, p_max, a, sigma, asa_dev, M, m1):
         ws = self.ws("gram", self.lib.ssnal_gram_ws_bytes(op.q))
         self._timed("dense_gram", 0, _lib.call, "ssnal_dense_gram", _ptr(op.A), op.n_phys, op.q,

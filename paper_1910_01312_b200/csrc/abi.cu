@@ -45,6 +45,11 @@ cudaError_t launch_pspace_direction(const double* A, long long n, long long q, l
                                     const double* g_r, double* t, int* info, void* ws,
                                     cudaStream_t stream);
 size_t proj_local_ws_bytes(long long n, int T);
+size_t gradient_ws_bytes(long long n_phys, long long q);
+cudaError_t launch_dense_gradient(const double* A, long long n, long long q, long long lda,
+                                  const double* rs, int svr, const double* w, const double* xp,
+                                  double* s_out, double* g_r, double* grad, double* g2, void* ws,
+                                  cudaStream_t stream);
 cudaError_t launch_proj_local(const double* A, const double* B, const double* coef,
                               const double* lam, const double* a, const double* l,
                               const double* u, double lc, double uc, long long n, int T, int mode,
@@ -296,6 +301,21 @@ int ssnal_qspace_assemble(int64_t m, const double* u, double asa, double sigma, 
   if (m < 1 || !M) return fail_arg("ssnal_qspace_assemble", "size/null");
   return check("ssnal_qspace_assemble",
                launch_qspace_shift_assemble(m, u, asa, sigma, shift, M, S(stream)));
+}
+
+/* ---- fused SsN gradient ---- */
+size_t ssnal_gradient_ws_bytes(int64_t n_phys, int64_t q) { return gradient_ws_bytes(n_phys, q); }
+
+int ssnal_dense_gradient(const double* A, int64_t n_phys, int64_t q, int64_t lda,
+                         const double* row_sign, int svr_block, const double* w, const double* xp,
+                         double* s_out, double* g_r, double* grad, double* g2, void* ws,
+                         void* stream) {
+  if (n_phys < 1 || q < 1 || lda < q) return fail_arg("ssnal_dense_gradient", "bad shape");
+  if (!A || !w || !xp || !s_out || !g_r || !grad || !g2 || !ws)
+    return fail_arg("ssnal_dense_gradient", "null pointer");
+  return check("ssnal_dense_gradient",
+               launch_dense_gradient(A, n_phys, q, lda, row_sign, svr_block, w, xp, s_out, g_r,
+                                     grad, g2, ws, S(stream)));
 }
 
 }  // extern "C"

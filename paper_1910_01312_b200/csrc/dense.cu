@@ -162,14 +162,33 @@ bool stream_ok(const double* A, long long lda, long long q);
 int stream_grid(long long n);
 cudaError_t launch_stream_xt(const double* A, long long n, long long q, long long lda,
                              const double* rs, int svr, int k, const double* const* vs, int kofs,
-                             int ktot, double* part, cudaStream_t stream);
+                             int ktot, double* part, cudaStream_t stream,
+                             const double* vsub = nullptr, double* vout = nullptr);
 cudaError_t launch_stream_xd(const double* A, long long n, long long q, long long lda,
                              const double* rs, int svr, int k, const double* d, double* out,
-                             long long nlog, cudaStream_t stream);
+                             long long nlog, cudaStream_t stream, double* sq_part = nullptr,
+                             double* sq_out = nullptr, unsigned int* sq_ticket = nullptr);
+cudaError_t launch_vec(int op, long long n, double alpha, const double* x, const double* y,
+                       const double* z, double* out, cudaStream_t s);
+cudaError_t launch_dots(int k, const double* const* xs, const double* const* ys,
+                        const uint8_t* mask, long long n, double* out, void* ws, cudaStream_t s);
+size_t reduce_ws_bytes(long long n);
 
 size_t dense_xt_ws_bytes(long long n_phys, long long q, int k) {
   const long long splits = max((long long)xt_splits(n_phys), (long long)stream_grid(n_phys));
   return (size_t)splits * k * q * sizeof(double);
+}
+
+// layout: [0, 256) tickets at FIXED offsets (a workspace reused across problem sizes
+// must never see a ticket where another size wrote partial sums), then the dots
+// fallback's workspace (its own ticket at byte 256), the per-CTA squared-norm
+// partials, the X^T partials
+static size_t grad_red_bytes(long long n_phys) {
+  return (reduce_ws_bytes(2 * n_phys) + 255) / 256 * 256;
+}
+size_t gradient_ws_bytes(long long n_phys, long long q) {
+  return 256 + grad_red_bytes(n_phys) + (size_t)(stream_grid(n_phys) + 32) * sizeof(double) +
+         dense_xt_ws_bytes(n_phys, q, 1);
 }
 
 static bool vec2_ok(const double* A, long long lda, long long q) {
@@ -571,6 +590,39 @@ cudaError_t launch_dense_gram(const double* A, long long n, long long q, long lo
   { note_launch(); gram_assemble_kernel<<<(unsigned)ceil_div(q * q, 256), 256, 0, stream>>>(g.part, q, m1, sigma,
                                                                           asa_dev, M); }
   return cudaGetLastError();
+}
+
+// Fused SsN gradient (ref solver.py:143-148 with the linear-kernel operator):
+//   s = w - Pi(u);  g_r = X^T s;  grad = X g_r;  *g2 = ||grad||^2
+// streaming route: the X^T pass stages s on the fly (and writes it), the X pass
+// accumulates ||grad||^2 -- two sweeps of A, no separate elementwise or dot launch.
+cudaError_t launch_dense_gradient(const double* A, long long n, long long q, long long lda,
+                                  const double* rs, int svr, const double* w, const double* xp,
+                                  double* s_out, double* g_r, double* grad, double* g2, void* ws,
+                                  cudaStream_t stream) {
+  const long long nlog = svr ? 2 * n : n;
+  char* base = (char*)ws;
+  unsigned int* ticket = (unsigned int*)base;
+  void* red_ws = (void*)(base + 256);
+  double* sq_part = (double*)(base + 256 + grad_red_bytes(n));
+  double* part = sq_part + stream_grid(n) + 32;
+  if (stream_ok(A, lda, q) && q <= 512) {
+    const double* vs[1] = {w};
+    cudaError_t e = launch_stream_xt(A, n, q, lda, rs, svr, 1, vs, 0, 1, part, stream, xp, s_out);
+    if (e != cudaSuccess) return e;
+    { note_launch(); dense_xt_fold_kernel<<<(unsigned)ceil_div(q * 32, 256LL), 256, 0, stream>>>(part, stream_grid(n), 1, q, g_r); }
+    return launch_stream_xd(A, n, q, lda, rs, svr, 1, g_r, grad, nlog, stream, sq_part, g2, ticket);
+  }
+  cudaError_t e = launch_vec(3, nlog, 0.0, w, xp, nullptr, s_out, stream);
+  if (e != cudaSuccess) return e;
+  const double* vs[1] = {s_out};
+  e = launch_dense_xt(A, n, q, lda, rs, svr, 1, vs, g_r, part, stream);
+  if (e != cudaSuccess) return e;
+  e = launch_dense_x(A, n, q, lda, rs, svr, 1, g_r, grad, stream);
+  if (e != cudaSuccess) return e;
+  const double* xs[1] = {grad};
+  const double* ys[1] = {nullptr};
+  return launch_dots(1, xs, ys, nullptr, nlog, g2, red_ws, stream);
 }
 
 }  // namespace ssnal

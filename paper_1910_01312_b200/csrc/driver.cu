@@ -30,6 +30,11 @@ cudaError_t launch_dots(int k, const double* const* xs, const double* const* ys,
                         const uint8_t* mask, long long n, double* out, void* ws, cudaStream_t s);
 cudaError_t launch_vec(int op, long long n, double alpha, const double* x, const double* y,
                        const double* z, double* out, cudaStream_t s);
+size_t gradient_ws_bytes(long long n_phys, long long q);
+cudaError_t launch_dense_gradient(const double* A, long long n, long long q, long long lda,
+                                  const double* rs, int svr, const double* w, const double* xp,
+                                  double* s_out, double* g_r, double* grad, double* g2, void* ws,
+                                  cudaStream_t stream);
 cudaError_t launch_hs_apply_dots(const uint8_t* fm, const double* a, const double* y, long long n,
                                  double beta, const double* add, double alpha, double* out,
                                  const double* g, const double* w, const double* qw,
@@ -145,7 +150,7 @@ struct Layout {
   long long* pcount;
   int* info;
   ProjState *st_cur, *st_trial, *st_kkt;
-  void *ws_proj, *ws_red, *ws_xt, *ws_gram, *ws_cmp, *ws_ps;
+  void *ws_proj, *ws_red, *ws_xt, *ws_gram, *ws_cmp, *ws_ps, *ws_grad;
   // sparse operator: sample-space CG buffers, scattered vector, CSC partial slots
   double *ys, *tq, *cg_gJ, *cg_aJ, *cg_b, *cg_y, *cg_r, *cg_pv, *cg_Ap, *cg_zq, *cg_w, *cgs,
       *cg_part, *csc_part, *cg_d, *cg_u, *cg_z;
@@ -190,6 +195,7 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
   L.ws_cmp = cv.take<char>(compact_ws_bytes(n));
   if (!sparse) {
     L.ws_xt = cv.take<char>(dense_xt_ws_bytes(n_phys, q, 2));
+    L.ws_grad = cv.take<char>(gradient_ws_bytes(n_phys, q));
     L.ws_gram = cv.take<char>(gram_ws_bytes(q));
     L.ws_ps = cv.take<char>(pspace_ws_bytes(q, q));
   } else {
@@ -577,10 +583,21 @@ struct Driver {
   }
 
   // ---------------------------------------------------------------- inner pieces
-  void gradient() {
+  // s = w - Pi(u), g_r = X^T s, grad = X g_r; with g2: ||grad||^2 into that device slot
+  // (dense: one fused call, csrc/dense.cu launch_dense_gradient)
+  void gradient(double* g2 = nullptr) {
+    if (!P.csr) {
+      // both sweeps of A (X^T then X) are accounted to the X^T class
+      timed(SSNAL_OP_XT, 2.0 * a_bytes() + 8.0 * (4 * P.n + 2 * P.q), [&] {
+        ck(launch_dense_gradient(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.w, L.xp,
+                                 L.s, L.gr, L.grad, g2 ? g2 : L.scal + NSCAL - 1, L.ws_grad, S));
+      });
+      return;
+    }
     vec(3, 0.0, L.w, L.xp, nullptr, L.s);
     xt({L.s}, L.gr);
     xd(L.gr, L.grad, 1);
+    if (g2) dots({{L.grad, nullptr}}, g2, P.n);
   }
 
   void direction(long long p, double asa, const double* g2_dev) {
@@ -650,10 +667,7 @@ struct Driver {
   // [gradient, ||grad||^2] + direction + unit trial, one sync
   void advance(long long p, double asa, bool with_gradient, double& gnorm2, double dotsv[4],
                ProjState& trial0) {
-    if (with_gradient) {
-      gradient();
-      dots({{L.grad, nullptr}}, L.scal + 4, P.n);
-    }
+    if (with_gradient) gradient(L.scal + 4);
     // ||grad||^2 of this point on the device: scal[4] after a gradient, scal[0] at the start
     direction(p, asa, with_gradient ? L.scal + 4 : L.scal + 0);
     const double coef = sigma;

@@ -85,6 +85,13 @@ struct StreamArgs {
   const double* d;  // [k][q]
   double* out;      // [k][nlog]
   long long nlog;
+  // fused gradient: XT stages coef = v - vsub and writes the difference to vout;
+  // XD accumulates sum out^2 (per-CTA partials, last-CTA fold into *sq_out)
+  const double* vsub;
+  double* vout;
+  double* sq_part;
+  double* sq_out;
+  unsigned int* sq_ticket;
 };
 
 // Producer: stream rows [r0, r1) of A through the ring.  Returns after the last issue.
@@ -132,7 +139,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xt_kernel(StreamArgs p) {
 #pragma unroll
     for (int j = 0; j < KV; ++j) {
       double cv = p.v[j][gr];
-      if (p.svr) cv = __dsub_rn(cv, p.v[j][gr + p.n]);
+      if (p.vsub && j == 0) {  // s = w - Pi(u) (numpy order, as vec op 3), written out
+        cv = __dsub_rn(cv, p.vsub[gr]);
+        p.vout[gr] = cv;
+      }
+      if (p.svr) {
+        double c2 = p.v[j][gr + p.n];
+        if (p.vsub && j == 0) {
+          c2 = __dsub_rn(c2, p.vsub[gr + p.n]);
+          p.vout[gr + p.n] = c2;
+        }
+        cv = __dsub_rn(cv, c2);
+      }
       coef_s[r][j] = sg * cv;
     }
   }
@@ -223,6 +241,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
     }
   const long long rows = r1 - r0;
   const long long nchunk = rows > 0 ? ceil_div(rows, (long long)p.rows_per_stage) : 0;
+  double sq = 0.0;  // lane 0: sum of squares of this warp's outputs (fused gradient norm)
   for (long long ch = 0; ch < nchunk; ++ch) {
     const int s = (int)(ch % NSTAGE);
     const long long rb = r0 + ch * p.rows_per_stage;
@@ -266,16 +285,41 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
           const double val = rs_s[rl] * acc[j];
           p.out[(long long)j * p.nlog + rb + r] = val;
           if (p.svr) p.out[(long long)j * p.nlog + rb + r + p.n] = -val;
+          if (j == 0) sq = fma(val, val, p.svr ? fma(val, val, sq) : sq);
           if (two) {
             const double val2 = rs_s[rl + NCONS] * acc2[j];
             p.out[(long long)j * p.nlog + rb + r2] = val2;
             if (p.svr) p.out[(long long)j * p.nlog + rb + r2 + p.n] = -val2;
+            if (j == 0) sq = fma(val2, val2, p.svr ? fma(val2, val2, sq) : sq);
           }
         }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (p.sq_out) {  // consumer warps only (the producer warp has returned)
+    __shared__ double wsq[NCONS];
+    __shared__ bool last;
+    if (lane == 0) wsq[warp] = sq;
+    asm volatile("bar.sync 1, %0;" ::"r"(NCONS * 32) : "memory");
+    if (threadIdx.x == 0) {
+      double c = 0.0;
+      for (int w = 0; w < NCONS; ++w) c += wsq[w];
+      p.sq_part[blockIdx.x] = c;
+      __threadfence();
+      last = atomicAdd(p.sq_ticket, 1u) == gridDim.x - 1;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NCONS * 32) : "memory");
+    if (last && warp == 0) {
+      double c = 0.0;
+      for (unsigned b = lane; b < gridDim.x; b += 32) c += __ldcg(p.sq_part + b);
+      c = warp_sum(c);
+      if (lane == 0) {
+        *p.sq_out = c;
+        *p.sq_ticket = 0u;
+      }
+    }
   }
 }
 
@@ -311,8 +355,11 @@ int stream_grid(long long n) {
 // X^T [v0 (, v1)] into part[grid][k][q]; caller folds.  k <= 2.
 cudaError_t launch_stream_xt(const double* A, long long n, long long q, long long lda,
                              const double* rs, int svr, int k, const double* const* vs, int kofs,
-                             int ktot, double* part, cudaStream_t stream) {
+                             int ktot, double* part, cudaStream_t stream, const double* vsub,
+                             double* vout) {
   StreamArgs p{};
+  p.vsub = vsub;
+  p.vout = vout;
   p.A = A; p.n = n; p.q = q; p.lda = lda; p.rs = rs; p.svr = svr;
   p.rows_per_stage = rows_per_stage(lda);
   p.v[0] = vs[kofs];
@@ -334,8 +381,12 @@ cudaError_t launch_stream_xt(const double* A, long long n, long long q, long lon
 
 cudaError_t launch_stream_xd(const double* A, long long n, long long q, long long lda,
                              const double* rs, int svr, int k, const double* d, double* out,
-                             long long nlog, cudaStream_t stream) {
+                             long long nlog, cudaStream_t stream, double* sq_part, double* sq_out,
+                             unsigned int* sq_ticket) {
   StreamArgs p{};
+  p.sq_part = sq_part;
+  p.sq_out = sq_out;
+  p.sq_ticket = sq_ticket;
   p.A = A; p.n = n; p.q = q; p.lda = lda; p.rs = rs; p.svr = svr;
   p.rows_per_stage = rows_per_stage(lda);
   p.d = d;

@@ -208,6 +208,15 @@ class ShardedEngine(_Engine):
         self.zero = be.zeros(1)
         self.am = be.empty(self.n)
 
+    def gradient(self, g2=None):
+        """Unfused: X^T s is all-gathered between the two products."""
+        op, be = self.op, self.be
+        be.vec(3, 0.0, self.w, self.xp, None, self.s)
+        op.xt([self.s], self.gr[:1])
+        op.x(self.gr[:1], self.grad.view(1, -1), k=1)
+        if g2 is not None:
+            be.dots([(self.grad, None)], g2)
+
     def direction(self, p, sigma, asa=0.0):
         if p == 0:
             return super().direction(p, sigma, asa)

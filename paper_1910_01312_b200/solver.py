@@ -254,12 +254,12 @@ class _Engine:
         return res, int(st["nfree"][0]), obj
 
     # ------------------------------------------------------------ inner pieces
-    def gradient(self):
-        """s = w - Pi(u); grad = Q s = X (X^T s); g_r = X^T s kept for the solve."""
+    def gradient(self, g2=None):
+        """s = w - Pi(u); grad = Q s = X (X^T s); g_r = X^T s kept for the solve; with
+        ``g2`` (a device slot) also ||grad||^2 -- one fused library call, as the driver."""
         op, be = self.op, self.be
-        be.vec(3, 0.0, self.w, self.xp, None, self.s)
-        op.xt([self.s], self.gr[:1])
-        op.x(self.gr[:1], self.grad.view(1, -1), k=1)
+        be.dense_gradient(op, self.w, self.xp, self.s, self.gr[0], self.grad,
+                          g2 if g2 is not None else self.scal[15:16])
 
     def start_inner(self, x, w, qw, sigma):
         """u = x - sigma (Qw + c), its projection, s and grad (ref solver.py:343-348)."""
@@ -335,8 +335,7 @@ class _Engine:
         point + the alpha = 1 trial projection, all enqueued, then ONE host sync.
         Returns (||grad||^2, [g'd, w'Qw, w'Qd, d'Qd], trial-0 record)."""
         if with_gradient:
-            self.gradient()
-            self.be.dots([(self.grad, None)], self.scal[4:5])
+            self.gradient(self.scal[4:5])
         self.direction(p, sigma, asa)
         self.enqueue_unit_trial()
         sc, st = self.fetch(self.st_trial, 1, info=(p > 0))

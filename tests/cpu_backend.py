@@ -142,6 +142,17 @@ class CpuTestBackend:
         for j in range(k):
             o[j] = torch.from_numpy(X @ dd[j])
 
+    def dense_gradient(self, op, w, xp, s_out, g_r, grad, g2):
+        self._count("dense_gradient")
+        X = self._x_rows(op)
+        s = w.numpy() - xp.numpy()
+        s_out.copy_(torch.from_numpy(s))
+        gr = X.T @ s
+        g_r.copy_(torch.from_numpy(gr))
+        gv = X @ gr
+        grad.copy_(torch.from_numpy(gv))
+        g2.view(-1)[0] = float(gv @ gv)
+
     def dense_gram(self, op, J, p_dev, p_max, a, sigma, asa_dev, M, m1):
         self._count("dense_gram")
         X = self._x_rows(op)
