@@ -111,6 +111,28 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _sweep_bytes(problem):
+    """Algorithmic HBM bytes of one sweep of A (X d or X^T v): A, labels, in/out vectors."""
+    op = problem.q_op
+    return 8 * op.n_phys * op.q + 8 * op.n_phys + 8 * (problem.n + op.q)
+
+
+def _ncu_traffic():
+    """DRAM read + write bytes per launch of the committed ncu --set full capture of
+    stream_xd_kernel (profiles/r1_ncu_stream_xd.txt), or None."""
+    try:
+        vals = {}
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_stream_xd.txt")) as fh:
+            for line in fh:
+                parts = line.split()
+                if parts and parts[0] == "raw" and parts[1].startswith("dram__bytes_"):
+                    scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}[parts[2]]
+                    vals[parts[1]] = float(parts[3]) * scale
+        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+    except Exception:
+        return None
+
+
 def cpu_oracle_solve(cfg):
     """Numpy restatement of the reference path (oracle/), stable psi evaluation."""
     import oracle as O
@@ -266,15 +288,21 @@ def run_ours(args, rank, world, local_rank):
     roof = None
     ptotal = float(np.sum(prof_wall)) if prof_wall else 0.0
     if kern:
-        # the roofline is reported for the streaming operator products (the HBM-bound
-        # kernels the path is built on); every op class's share is listed beside it
-        stream = {k: v for k, v in kern.items() if k in ("dense_xt", "dense_x")}
-        name, (cnt, secs, nbytes) = max(stream.items(), key=lambda kv: kv[1][1])
+        # dominant kernel of the launch list (profiles/r1_launches_config1_solve.txt): the
+        # streaming sweeps of A (stream_xd / stream_xt, both HBM bound).  achieved = their
+        # algorithmic bytes / their device time, measured live here over the K profiled
+        # solves (op classes dense_xt, which also holds the fused gradient's two sweeps,
+        # and dense_x); traffic = DRAM bytes per launch of one ncu --set full capture
+        sweeps = [kern[k] for k in ("dense_xt", "dense_x") if k in kern]
+        cnt = sum(v[0] for v in sweeps)
+        secs = sum(v[1] for v in sweeps)
+        nbytes = sum(v[2] for v in sweeps)
         achieved = (nbytes / secs) / 1e9 if secs > 0 and nbytes > 0 else 0.0
-        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak if peak else None, "traffic": None,
-                "peak_kind": peak_kind, "launches": cnt, "mean_launch_us": secs / cnt * 1e6,
-                "algorithmic_bytes_per_launch": nbytes / max(cnt, 1),
+        roof = {"bound": "hbm", "kernel": "stream_xd_kernel / stream_xt_kernel (sweeps of A)",
+                "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak if peak else None,
+                "traffic": _ncu_traffic(), "peak_kind": peak_kind, "sweeps": cnt,
+                "algorithmic_bytes_per_sweep": _sweep_bytes(problem),
                 "share_of_step": secs / ptotal if ptotal else None,
                 "measured": "CUDA events on the solver stream, K extra profiled solves",
                 "ops": {k: {"calls": v[0], "s": v[1], "share": v[1] / ptotal if ptotal else None,
