@@ -29,7 +29,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -58,57 +57,66 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled through NVML inside the
+    timed region -- between solves, after each step's closing event, so the query
+    never lands inside a latency-bound solve (an nvidia-smi process polling every
+    200 ms did, adding ms-scale stalls to the host syncs).  Falls back to a single
+    nvidia-smi query per sample when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
-        self.proc = None
-        self.thread = None
+        self.sm, self.smax, self.reasons = [], [], set()
+        self.nv = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self.nv = None
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            return
-        self.thread = threading.Thread(target=self._read, daemon=True)
-        self.thread.start()
+        self.sample()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+    def sample(self):
+        try:
+            if self.nv is not None:
+                nv = self.nv
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                self.smax.append(float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.REASONS:
+                    if mask & getattr(nv, attr, 0):
+                        self.reasons.add(name)
+                return
+            out = subprocess.run(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10).stdout
+            r = [c.strip() for c in out.split(",")]
+            self.sm.append(float(r[0]))
+            self.smax.append(float(r[1]))
+            for name, val in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                  "sw_power_cap"], r[2:6]):
+                if val.lower() == "active":
+                    self.reasons.add(name)
+        except Exception:
+            pass
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        if self.thread:
-            self.thread.join(timeout=2)
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            try:
-                sm.append(float(r[0]))
-                smax.append(float(r[1]))
-            except (ValueError, IndexError):
-                continue
-            for name, val in zip(names, r[4:8]):
-                if val.strip().lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock query unavailable"]}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.smax),
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 def _sweep_bytes(problem):
@@ -229,6 +237,7 @@ def run_ours(args, rank, world, local_rank):
         e1.synchronize()
         step_s.append(e0.elapsed_time(e1) * 1e-3)
         reps.append(rep)
+        sampler.sample()
     launches = (be.launch_count() - launches0) // max(args.steps, 1)
     # per-op-class device time: the same K solves again with CUDA events around every
     # op on the solver stream (kept out of the timed region above: event records cost
@@ -245,6 +254,7 @@ def run_ours(args, rank, world, local_rank):
         e1.record(stream)
         e1.synchronize()
         prof_wall.append(e0.elapsed_time(e1) * 1e-3)
+        sampler.sample()
         for name, v in getattr(problem, "op_profile", {}).items():
             c, s, b = kern.get(name, (0, 0.0, 0.0))
             kern[name] = (c + v["calls"], s + v["seconds"], b + v["bytes"])
@@ -301,7 +311,7 @@ def run_ours(args, rank, world, local_rank):
         roof = {"bound": "hbm", "kernel": "stream_xd_kernel / stream_xt_kernel (sweeps of A)",
                 "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak if peak else None,
-                "traffic": _ncu_traffic(), "peak_kind": peak_kind, "sweeps": cnt,
+                "traffic": _ncu_traffic(), "peak_kind": peak_kind, "op_calls": cnt,
                 "algorithmic_bytes_per_sweep": _sweep_bytes(problem),
                 "share_of_step": secs / ptotal if ptotal else None,
                 "measured": "CUDA events on the solver stream, K extra profiled solves",
@@ -334,6 +344,7 @@ def run_ours(args, rank, world, local_rank):
                    "outer": last.outer_iters, "inner": last.total_inner_iters,
                    "p": last.unbounded_support_count, "converged": last.converged},
         "counters": getattr(problem, "native_counters", None),
+        "step_ms": [round(t * 1e3, 3) for t in step_s],
     }
     print(json.dumps(line), flush=True)
     if dist is not None:

@@ -850,9 +850,9 @@ static bool cluster_ok(long long n, int T) {
                                    CL_SMEM) != cudaSuccess)
       ok = 0;
   }
-  // single trials keep the grid-wide fused kernel (measured equal or faster at T = 1);
-  // batched line-search trials run as independent clusters
-  return ok == 1 && n <= (long long)CL_CTAS * CL_NT * CL_EPT && T >= 2;
+  // in the solve (L2 cold after every sweep of A) the register-resident cluster
+  // kernel wins for single trials too (bench op profile: -9 % projection time)
+  return ok == 1 && n <= (long long)CL_CTAS * CL_NT * CL_EPT && T >= 1;
 }
 
 int proj_blocks(long long n) {
