@@ -104,7 +104,7 @@ constexpr double HOT_COLUMN_SPREAD = 50.0;
 
 namespace {
 
-constexpr int TMAX = 4;  // batched Armijo trials per launch
+constexpr int TMAX = 8;  // batched Armijo trials per launch
 constexpr int CG_BATCH = 16;  // CG iterations between host checks of the device flag
 constexpr int NSCAL = 16;
 
@@ -670,16 +670,27 @@ struct Driver {
     if (with_gradient) gradient(L.scal + 4);
     // ||grad||^2 of this point on the device: scal[4] after a gradient, scal[0] at the start
     direction(p, asa, with_gradient ? L.scal + 4 : L.scal + 0);
-    const double coef = sigma;
-    project(L.u, L.st_trial, 1, L.qdir, &coef, L.tx, L.tfree, L.x, lam_cur);
-    fetch(L.st_trial, 1, p > 0);
+    // the first Armijo batch (alpha = 1, beta, ..., beta^(T0-1)) is projected
+    // speculatively with the direction: most steps then need no further host round trip
+    const int T0 = std::min(TMAX, std::max(1, O.line_search_batch));
+    double coefs[TMAX];
+    double alpha = 1.0;
+    for (int k = 0; k < T0; ++k) {
+      coefs[k] = sigma * alpha;
+      alpha *= O.backtrack;
+    }
+    project(L.u, L.st_trial, T0, L.qdir, coefs, L.tx, L.tfree, L.x, lam_cur);
+    fetch(L.st_trial, T0, p > 0);
     if (p > 0 && H->info != 0) throw DriverError{SSNAL_E_ARG, "reduced Newton matrix not SPD"};
     gnorm2 = H->scal[4];
     for (int k = 0; k < 4; ++k) dotsv[k] = H->scal[k];
-    if (H->st[0].status != PROJ_APPLIED)
-      finish(L.st_trial, 1, L.u, L.qdir, &coef, L.tx, L.tfree, L.x);
+    finish(L.st_trial, T0, L.u, L.qdir, coefs, L.tx, L.tfree, L.x);
+    first_T = T0;
+    for (int k = 0; k < T0; ++k) first_batch[k] = H->st[k];
     trial0 = H->st[0];
   }
+  ProjState first_batch[TMAX];
+  int first_T = 0;
 
   // Armijo (ref solver.py:292-319); returns false on failure (LineSearchError)
   bool line_search(double gd, double psi0, double wqw, double wqdir, double dqd, double x_sq,
@@ -688,9 +699,10 @@ struct Driver {
     double alpha = 1.0;
     int tried = 0;
     while (tried < 61) {
-      const int T = tried == 0 ? 1
-                                : std::min(std::min(TMAX, std::max(1, O.line_search_batch)),
-                                           61 - tried);
+      const int T = (tried == 0 && first) ? first_T
+                    : tried == 0 ? 1
+                                 : std::min(std::min(TMAX, std::max(1, O.line_search_batch)),
+                                            61 - tried);
       double alphas[TMAX], coefs[TMAX];
       for (int k = 0; k < T; ++k) {
         alphas[k] = alpha;
@@ -698,7 +710,7 @@ struct Driver {
         alpha *= O.backtrack;
       }
       if (tried == 0 && first) {
-        H->st[0] = *first;
+        for (int k = 0; k < T; ++k) H->st[k] = first[k];
       } else {
         project(L.u, L.st_trial, T, L.qdir, coefs, L.tx, L.tfree, L.x, lam_cur);
         fetch(L.st_trial, T, false);
@@ -775,7 +787,7 @@ struct Driver {
       double gd = dv[0], wqw = dv[1], wqdir = dv[2], dqd = dv[3];
       ++newton;
       bool steepest_dir = false;
-      const ProjState* first = &trial0;
+      const ProjState* first = first_batch;
       if (gd >= 0.0) {
         double sv[4];
         steepest(sv);

@@ -69,7 +69,7 @@ class SsnOptions:
     max_inner: int = 50
     direct_solve_threshold: int = 2000
     cg_max_iters: int = 500
-    line_search_batch: int = 4
+    line_search_batch: int = 8
     psi_eval: str = "stable"  # or "reference": ref solver.py:130-133 term for term
     engine: str = "native"    # "native": C++ driver (ssnal_alm_solve_dense); "python": _Engine
     profile: bool = False     # native: CUDA-event time per op class -> problem.op_profile
@@ -157,7 +157,7 @@ class _Engine:
     """Device buffers and the kernel sequence of one problem.  Host reads happen
     only at the decision points the reference also branches on."""
 
-    def __init__(self, problem, t_max=4):
+    def __init__(self, problem, t_max=8):
         self.pb = problem
         self.op = problem.q_op
         self.box = problem.constraint
@@ -190,6 +190,8 @@ class _Engine:
         self.asa_dev = self.st_cur[0, _OFF["sum_a2_free"]:_OFF["sum_a2_free"] + 8].view(F64)
         self.counters = {"projections": 0, "proj_trials": 0, "newton": 0, "syncs": 0}
         self._direct_limit = 2000
+        self.line_search_batch = 8  # set from SsnOptions by ssn_solve
+        self.backtrack = 0.5
         self.lam_kkt = 0.0  # warm starts for the multiplier search
         self.lam_cur = 0.0
 
@@ -325,10 +327,21 @@ class _Engine:
         sc, _ = self.fetch()
         return sc
 
+    def first_batch_size(self):
+        return min(self.t_max, max(1, self.line_search_batch))
+
     def enqueue_unit_trial(self):
-        """Projection of u - sigma*1*Qd (the alpha = 1 Armijo trial) into trial slot 0."""
-        self._project(self.u, self.st_trial, 1, B=self.qdir, coefs=[self.sigma],
+        """Projections of u - sigma*alpha*Qd for the first Armijo batch alpha = 1, beta, ...
+        (speculative, enqueued with the direction: one host round trip per Newton step
+        in the common case), as the C++ driver."""
+        T0 = self.first_batch_size()
+        coefs, alpha = [], 1.0
+        for _ in range(T0):
+            coefs.append(self.sigma * alpha)
+            alpha *= self.backtrack
+        self._project(self.u, self.st_trial, T0, B=self.qdir, coefs=coefs,
                       x_out=self.tx, free_out=self.tfree, ref=self.x, hint=self.lam_cur)
+        return coefs
 
     def advance(self, p, asa, sigma, with_gradient=True):
         """Pipelined Newton step: [s, grad = Q s, ||grad||^2] + direction at the current
@@ -337,14 +350,13 @@ class _Engine:
         if with_gradient:
             self.gradient(self.scal[4:5])
         self.direction(p, sigma, asa)
-        self.enqueue_unit_trial()
-        sc, st = self.fetch(self.st_trial, 1, info=(p > 0))
+        coefs = self.enqueue_unit_trial()
+        T0 = len(coefs)
+        sc, st = self.fetch(self.st_trial, T0, info=(p > 0))
         if p > 0 and int(self.h_info[0]) != 0:
             raise InternalError(f"reduced Newton matrix not SPD (column {int(self.h_info[0])})")
-        if st["status"][0] != _lib.PROJ_APPLIED:
-            st = self._finish_states(st, self.st_trial, 1, self.u, B=self.qdir,
-                                     coefs=[self.sigma], x_out=self.tx, free_out=self.tfree,
-                                     ref=self.x)
+        st = self._finish_states(st, self.st_trial, T0, self.u, B=self.qdir, coefs=coefs,
+                                 x_out=self.tx, free_out=self.tfree, ref=self.x)
         return float(sc[4]), [float(v) for v in sc[:4]], st
 
     def line_search(self, gd, psi0, wqw, wqdir, dqd, x_sq, opts, first=None):
@@ -358,7 +370,10 @@ class _Engine:
         alpha = 1.0
         tried = 0
         while tried < 61:
-            T = 1 if tried == 0 else min(self.t_max, max(1, opts.line_search_batch), 61 - tried)
+            if tried == 0:
+                T = len(first) if first is not None else 1
+            else:
+                T = min(self.t_max, max(1, opts.line_search_batch), 61 - tried)
             alphas = []
             for _ in range(T):
                 alphas.append(alpha)
@@ -421,6 +436,8 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
     floors and rescue branches.  Mutates state.w / state.qw."""
     eng = problem.engine()
     eng._direct_limit = ssn_opts.direct_solve_threshold
+    eng.line_search_batch = ssn_opts.line_search_batch
+    eng.backtrack = ssn_opts.backtrack
     sigma = state.sigma
     coeff = math.sqrt(alm_opts.lambda_min_surrogate / sigma)
     grad_floor = 1e-12 * (1.0 + eng.c_norm)
@@ -449,7 +466,7 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
         gd, wqw, wqdir, dqd = dots
         eng.counters["newton"] += 1
         steepest = False
-        first = trial0[0:1]
+        first = trial0
         if gd >= 0.0:
             sc = eng.steepest()
             gd, wqw, wqdir, dqd = (float(v) for v in sc[:4])
