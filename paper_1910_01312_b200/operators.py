@@ -37,10 +37,19 @@ class LinearKernelOperator:
         self.svr_block = bool(svr_block)
         self.n = 2 * self.n_phys if self.svr_block else self.n_phys
         if labels is not None:
-            lab = as_device(labels, be)
-            check_vector(lab, self.n_phys, "labels")
-            if not bool(torch.all(lab.abs() == 1.0)):
-                raise InputError("labels must be +1/-1")
+            if isinstance(labels, torch.Tensor) and labels.is_cuda:
+                lab = as_device(labels, be)
+                check_vector(lab, self.n_phys, "labels")
+                if not bool(torch.all(lab.abs() == 1.0)):
+                    raise InputError("labels must be +1/-1")
+            else:  # host labels: validated on the host (no device round trip)
+                lab_h = np.asarray(labels.numpy() if isinstance(labels, torch.Tensor) else labels,
+                                   dtype=np.float64)
+                if lab_h.ndim != 1 or lab_h.shape[0] != self.n_phys:
+                    raise InputError(f"labels: expected a vector of length {self.n_phys}")
+                if not np.all(np.abs(lab_h) == 1.0):
+                    raise InputError("labels must be +1/-1")
+                lab = as_device(lab_h, be)
             self.row_sign = lab
         else:
             self.row_sign = None
@@ -156,10 +165,19 @@ class CsrKernelOperator:
             "fold_beg": dev(fold_beg if fold_cols.size else np.zeros(2, np.int32), torch.int32),
         }
         if labels is not None:
-            lab = as_device(labels, be)
-            check_vector(lab, self.n_phys, "labels")
-            if not bool(torch.all(lab.abs() == 1.0)):
-                raise InputError("labels must be +1/-1")
+            if isinstance(labels, torch.Tensor) and labels.is_cuda:
+                lab = as_device(labels, be)
+                check_vector(lab, self.n_phys, "labels")
+                if not bool(torch.all(lab.abs() == 1.0)):
+                    raise InputError("labels must be +1/-1")
+            else:  # host labels: validated on the host (no device round trip)
+                lab_h = np.asarray(labels.numpy() if isinstance(labels, torch.Tensor) else labels,
+                                   dtype=np.float64)
+                if lab_h.ndim != 1 or lab_h.shape[0] != self.n_phys:
+                    raise InputError(f"labels: expected a vector of length {self.n_phys}")
+                if not np.all(np.abs(lab_h) == 1.0):
+                    raise InputError("labels must be +1/-1")
+                lab = as_device(lab_h, be)
             self.row_sign = lab
         else:
             self.row_sign = None

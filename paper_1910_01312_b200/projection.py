@@ -27,7 +27,7 @@ class BoxLineSet:
     construction (ref projection.py:29-54).  Constant bounds are passed to the
     kernels as scalars (no l/u streams)."""
 
-    def __init__(self, a, d, l, u, backend=None):
+    def __init__(self, a, d, l, u, backend=None, a_device=None):
         self.backend = backend or default_backend()
         a_h = np.ascontiguousarray(a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a,
                                    dtype=np.float64)
@@ -48,13 +48,15 @@ class BoxLineSet:
                 f"a'x = {d} unattainable over the box: range is [{lo}, {hi}]")
         self.n = a_h.shape[0]
         self.d = d
-        self.a_dev = as_device(a_h, self.backend)
-        lu = np.unique(l_h)
-        uu = np.unique(u_h)
-        self.l_const = float(lu[0]) if lu.size == 1 else 0.0
-        self.u_const = float(uu[0]) if uu.size == 1 else 0.0
-        self.l_dev = None if lu.size == 1 else as_device(l_h, self.backend)
-        self.u_dev = None if uu.size == 1 else as_device(u_h, self.backend)
+        # a_device: the caller's device copy of the same values (e.g. the labels already
+        # uploaded for the operator), saving a second upload
+        self.a_dev = a_device if a_device is not None else as_device(a_h, self.backend)
+        l_uniform = bool(l_h.min() == l_h.max())
+        u_uniform = bool(u_h.min() == u_h.max())
+        self.l_const = float(l_h[0]) if l_uniform else 0.0
+        self.u_const = float(u_h[0]) if u_uniform else 0.0
+        self.l_dev = None if l_uniform else as_device(l_h, self.backend)
+        self.u_dev = None if u_uniform else as_device(u_h, self.backend)
         self._range_lo, self._range_hi = lo, hi
 
     @property

@@ -49,8 +49,9 @@ def build_csvc_dual(features, labels, C, backend=None):
         op = LinearKernelOperator(features, labels=y, backend=be)
     if op.n != n:
         raise InputError("labels must have one entry per sample")
-    box = BoxLineSet(a=y, d=0.0, l=np.zeros(n), u=np.full(n, float(C)), backend=be)
-    return QpProblem(op, -np.ones(n), box)
+    box = BoxLineSet(a=y, d=0.0, l=np.zeros(n), u=np.full(n, float(C)), backend=be,
+                     a_device=op.row_sign)
+    return QpProblem(op, torch.full((n,), -1.0, dtype=torch.float64, device=be.device), box)
 
 
 def build_svr_dual(features, targets, C, epsilon, backend=None):
