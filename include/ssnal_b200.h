@@ -288,6 +288,18 @@ int ssnal_dense_gradient(const double* A, int64_t n_phys, int64_t q, int64_t lda
                          double* s_out, double* g_r, double* grad, double* g2, void* ws,
                          void* stream);
 
+/* Dense Newton-direction epilogue (ref solver.py:259-269), from t = X^T d:
+ *   qdir = X t;  dir = -s - sigma P_J(qdir)  (P_J from the free mask, a_J'a_J read from
+ *   *asa_dev -- the projection record's sum_a2_free); dots4 (DEVICE, 4 doubles) =
+ *   {grad'dir, w'qw, w'qdir, t't}.  ws: ssnal_gradient_ws_bytes (shared with the
+ *   gradient call; stream-ordered use). */
+int ssnal_dense_direction_epilogue(const double* A, int64_t n_phys, int64_t q, int64_t lda,
+                                   const double* row_sign, int svr_block, const double* t,
+                                   double* qdir, const uint8_t* free_mask, const double* a,
+                                   const double* asa_dev, const double* s, double sigma,
+                                   const double* grad, const double* w, const double* qw,
+                                   double* dir, double* dots4, void* ws, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

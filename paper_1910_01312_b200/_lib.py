@@ -122,6 +122,8 @@ _SIGNATURES.update({
     "ssnal_qspace_assemble": (_I, [_I64, _P, _D, _D, _D, _P, _P]),
     "ssnal_gradient_ws_bytes": (_SZ, [_I64, _I64]),
     "ssnal_dense_gradient": (_I, [_P, _I64, _I64, _I64, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ssnal_dense_direction_epilogue": (_I, [_P, _I64, _I64, _I64, _P, _I, _P, _P, _P, _P, _P, _P,
+                                            _D, _P, _P, _P, _P, _P, _P, _P]),
 })
 
 _lib = None

@@ -201,6 +201,16 @@ class CudaBackend:
                     int(op.svr_block), _ptr(w), _ptr(xp), _ptr(s_out), _ptr(g_r), _ptr(grad),
                     _ptr(g2), _ptr(ws), self.stream())
 
+    def direction_epilogue(self, op, t, qdir, free, a, asa_dev, s, sigma, grad, w, qw, dir_out,
+                           dots4):
+        """qdir = X t, dir = -s - sigma P(qdir), dots4 = {g'dir, w'qw, w'qdir, t't} (fused)."""
+        ws = self.ws("gradient", self.lib.ssnal_gradient_ws_bytes(op.n_phys, op.q))
+        self._timed("dense_x", self.dense_bytes(op, 1, "x"), _lib.call,
+                    "ssnal_dense_direction_epilogue", _ptr(op.A), op.n_phys, op.q, op.lda,
+                    _ptr(op.row_sign), int(op.svr_block), _ptr(t), _ptr(qdir), _ptr(free), _ptr(a),
+                    _ptr(asa_dev), _ptr(s), float(sigma), _ptr(grad), _ptr(w), _ptr(qw),
+                    _ptr(dir_out), _ptr(dots4), _ptr(ws), self.stream())
+
     def dense_gram(self, op, J, p_dev, p_max, a, sigma, asa_dev, M, m1):
         ws = self.ws("gram", self.lib.ssnal_gram_ws_bytes(op.q))
         self._timed("dense_gram", 0, _lib.call, "ssnal_dense_gram", _ptr(op.A), op.n_phys, op.q,

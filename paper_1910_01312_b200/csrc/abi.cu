@@ -46,6 +46,12 @@ cudaError_t launch_pspace_direction(const double* A, long long n, long long q, l
                                     cudaStream_t stream);
 size_t proj_local_ws_bytes(long long n, int T);
 size_t gradient_ws_bytes(long long n_phys, long long q);
+cudaError_t launch_direction_epilogue(const double* A, long long n, long long q, long long lda,
+                                      const double* rs, int svr, const double* t, double* qdir,
+                                      const uint8_t* fm, const double* a, const double* asa_dev,
+                                      const double* s, double sigma, const double* grad,
+                                      const double* w, const double* qw, double* dir,
+                                      double* dots4, void* ws, cudaStream_t stream);
 cudaError_t launch_dense_gradient(const double* A, long long n, long long q, long long lda,
                                   const double* rs, int svr, const double* w, const double* xp,
                                   double* s_out, double* g_r, double* grad, double* g2, void* ws,
@@ -316,6 +322,22 @@ int ssnal_dense_gradient(const double* A, int64_t n_phys, int64_t q, int64_t lda
   return check("ssnal_dense_gradient",
                launch_dense_gradient(A, n_phys, q, lda, row_sign, svr_block, w, xp, s_out, g_r,
                                      grad, g2, ws, S(stream)));
+}
+
+int ssnal_dense_direction_epilogue(const double* A, int64_t n_phys, int64_t q, int64_t lda,
+                                   const double* row_sign, int svr_block, const double* t,
+                                   double* qdir, const uint8_t* free_mask, const double* a,
+                                   const double* asa_dev, const double* s, double sigma,
+                                   const double* grad, const double* w, const double* qw,
+                                   double* dir, double* dots4, void* ws, void* stream) {
+  if (n_phys < 1 || q < 1 || lda < q) return fail_arg("ssnal_dense_direction_epilogue", "bad shape");
+  if (!A || !t || !qdir || !free_mask || !a || !asa_dev || !s || !grad || !w || !qw || !dir ||
+      !dots4 || !ws)
+    return fail_arg("ssnal_dense_direction_epilogue", "null pointer");
+  return check("ssnal_dense_direction_epilogue",
+               launch_direction_epilogue(A, n_phys, q, lda, row_sign, svr_block, t, qdir, free_mask,
+                                         a, asa_dev, s, sigma, grad, w, qw, dir, dots4, ws,
+                                         S(stream)));
 }
 
 }  // extern "C"

@@ -167,7 +167,13 @@ cudaError_t launch_stream_xt(const double* A, long long n, long long q, long lon
 cudaError_t launch_stream_xd(const double* A, long long n, long long q, long long lda,
                              const double* rs, int svr, int k, const double* d, double* out,
                              long long nlog, cudaStream_t stream, double* sq_part = nullptr,
-                             double* sq_out = nullptr, unsigned int* sq_ticket = nullptr);
+                             double* sq_out = nullptr, unsigned int* sq_ticket = nullptr,
+                             int epi = 0, const uint8_t* fm = nullptr, const double* av = nullptr);
+cudaError_t launch_hs_finish_dots(const uint8_t* fm, const double* a, const double* y, long long n,
+                                  double beta, const double* add, double alpha, double* out,
+                                  const double* ay, const double* aa, const double* g,
+                                  const double* w, const double* qw, const double* t, long long q,
+                                  double* dots_out, void* ws, cudaStream_t stream);
 cudaError_t launch_vec(int op, long long n, double alpha, const double* x, const double* y,
                        const double* z, double* out, cudaStream_t s);
 cudaError_t launch_dots(int k, const double* const* xs, const double* const* ys,
@@ -624,5 +630,39 @@ cudaError_t launch_dense_gradient(const double* A, long long n, long long q, lon
   const double* ys[1] = {nullptr};
   return launch_dots(1, xs, ys, nullptr, nlog, g2, red_ws, stream);
 }
+
+// Dense Newton-direction epilogue (ref solver.py:259-269): from t = X^T d
+//   Qd = X t;  d = -s - sigma P_J(Qd)  with a_J'(Qd)_J folded in the X sweep and
+//   a_J'a_J = the projection record's sum_a2_free;  dots = {g'd, w'Qw, w'Qd, t't}
+// two launches (streaming X sweep + one elementwise/dot pass)
+cudaError_t launch_direction_epilogue(const double* A, long long n, long long q, long long lda,
+                                      const double* rs, int svr, const double* t, double* qdir,
+                                      const uint8_t* fm, const double* a, const double* asa_dev,
+                                      const double* s, double sigma, const double* grad,
+                                      const double* w, const double* qw, double* dir,
+                                      double* dots4, void* ws, cudaStream_t stream) {
+  const long long nlog = svr ? 2 * n : n;
+  char* base = (char*)ws;
+  unsigned int* ticket = (unsigned int*)base;
+  void* red_ws = (void*)(base + 256);
+  double* ad = (double*)(base + 128);  // a_J'(Qd)_J slot (inside the ticket page)
+  double* sq_part = (double*)(base + 256 + grad_red_bytes(n));
+  if (stream_ok(A, lda, q) && q <= 512) {
+    cudaError_t e = launch_stream_xd(A, n, q, lda, rs, svr, 1, t, qdir, nlog, stream, sq_part, ad,
+                                     ticket, 2, fm, a);
+    if (e != cudaSuccess) return e;
+  } else {
+    cudaError_t e = launch_dense_x(A, n, q, lda, rs, svr, 1, t, qdir, stream);
+    if (e != cudaSuccess) return e;
+    const double* xs[1] = {a};
+    const double* ys[1] = {qdir};
+    e = launch_dots(1, xs, ys, fm, nlog, ad, red_ws, stream);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_hs_finish_dots(fm, a, qdir, nlog, -sigma, s, -1.0, dir, ad, asa_dev, grad, w, qw,
+                               t, q, dots4, red_ws, stream);
+}
+
+size_t direction_ws_bytes(long long n_phys, long long q) { return gradient_ws_bytes(n_phys, q); }
 
 }  // namespace ssnal

@@ -35,6 +35,12 @@ cudaError_t launch_dense_gradient(const double* A, long long n, long long q, lon
                                   const double* rs, int svr, const double* w, const double* xp,
                                   double* s_out, double* g_r, double* grad, double* g2, void* ws,
                                   cudaStream_t stream);
+cudaError_t launch_direction_epilogue(const double* A, long long n, long long q, long long lda,
+                                      const double* rs, int svr, const double* t, double* qdir,
+                                      const uint8_t* fm, const double* a, const double* asa_dev,
+                                      const double* s, double sigma, const double* grad,
+                                      const double* w, const double* qw, double* dir,
+                                      double* dots4, void* ws, cudaStream_t stream);
 cudaError_t launch_hs_apply_dots(const uint8_t* fm, const double* a, const double* y, long long n,
                                  double beta, const double* add, double alpha, double* out,
                                  const double* g, const double* w, const double* qw,
@@ -646,13 +652,13 @@ struct Driver {
         ck(launch_chol_solve(L.M, P.q, L.gr, -1.0, L.t, L.info, S));
       }
     });
-    xd(L.t, L.qdir, 1);
-    // d = -s - sigma P(Qd) and {g'd, w'Qw, w'Qd} in one pass
-    timed(SSNAL_OP_VEC, 8.0 * P.n * 10, [&] {
-      ck(launch_hs_apply_dots(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.grad, L.w,
-                              L.qw, L.scal, L.ws_red, S));
+    // Qd = X t (a_J'(Qd)_J folded in the sweep), d = -s - sigma P(Qd), and
+    // {g'd, w'Qw, w'Qd, t't}: two launches
+    timed(SSNAL_OP_XD, a_bytes() + 8.0 * (P.n + P.q) + 8.0 * P.n * 8, [&] {
+      ck(launch_direction_epilogue(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.t,
+                                   L.qdir, L.fr, P.a, &L.st_cur->sum_a2_free, L.s, sigma, L.grad,
+                                   L.w, L.qw, L.dir, L.scal, L.ws_grad, S));
     });
-    dots({{L.t, nullptr}}, L.scal + 3, P.q);
   }
 
   void steepest(double out[4]) {

@@ -654,9 +654,13 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_fused_kernel(ProjArgs p, double
 // barrier, no second launch, and the T line-search trials run as T independent
 // clusters side by side.  Partials are double-buffered by pass parity: a CTA can
 // only overwrite a buffer after every CTA has passed the following barrier.
-static constexpr int CL_CTAS = 16;
+#ifndef SSNAL_CL_CTAS
+#define SSNAL_CL_CTAS 16
+#define SSNAL_CL_EPT 8
+#endif
+static constexpr int CL_CTAS = SSNAL_CL_CTAS;
 static constexpr int CL_NT = 512;
-static constexpr int CL_EPT = 8;
+static constexpr int CL_EPT = SSNAL_CL_EPT;
 static constexpr int CL_MAX_PASSES = 12;
 static constexpr int CL_SMEM = 2 * CL_EPT * CL_NT * (int)sizeof(double);
 

@@ -89,6 +89,11 @@ struct StreamArgs {
   // XD accumulates sum out^2 (per-CTA partials, last-CTA fold into *sq_out)
   const double* vsub;
   double* vout;
+  // XD epilogue reduction (last-CTA fold into *sq_out): epi 1 = sum out^2 (gradient
+  // norm), epi 2 = sum over free slots of a_i out_i (the HS product's a_J'(Qd)_J)
+  int epi;
+  const uint8_t* fm;
+  const double* av;
   double* sq_part;
   double* sq_out;
   unsigned int* sq_ticket;
@@ -204,6 +209,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xt_kernel(StreamArgs p) {
   }
 }
 
+// per-row contribution of the XD epilogue reduction (logical rows gr and, for the
+// SVR block, gr + n holding -val)
+__device__ __forceinline__ double epi_term(const StreamArgs& p, long long gr, double val,
+                                           double acc) {
+  if (p.epi == 1) return fma(val, val, p.svr ? fma(val, val, acc) : acc);
+  if (p.epi == 2) {
+    if (p.fm[gr]) acc = fma(p.av[gr], val, acc);
+    if (p.svr && p.fm[gr + p.n]) acc = fma(p.av[gr + p.n], -val, acc);
+  }
+  return acc;
+}
+
 template <int KV, int CP>
 __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
   extern __shared__ __align__(128) char ring[];
@@ -285,12 +302,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
           const double val = rs_s[rl] * acc[j];
           p.out[(long long)j * p.nlog + rb + r] = val;
           if (p.svr) p.out[(long long)j * p.nlog + rb + r + p.n] = -val;
-          if (j == 0) sq = fma(val, val, p.svr ? fma(val, val, sq) : sq);
+          if (j == 0) sq = epi_term(p, rb + r, val, sq);
           if (two) {
             const double val2 = rs_s[rl + NCONS] * acc2[j];
             p.out[(long long)j * p.nlog + rb + r2] = val2;
             if (p.svr) p.out[(long long)j * p.nlog + rb + r2 + p.n] = -val2;
-            if (j == 0) sq = fma(val2, val2, p.svr ? fma(val2, val2, sq) : sq);
+            if (j == 0) sq = epi_term(p, rb + r2, val2, sq);
           }
         }
       }
@@ -298,7 +315,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-  if (p.sq_out) {  // consumer warps only (the producer warp has returned)
+  if (p.epi) {  // consumer warps only (the producer warp has returned)
     __shared__ double wsq[NCONS];
     __shared__ bool last;
     if (lane == 0) wsq[warp] = sq;
@@ -382,8 +399,12 @@ cudaError_t launch_stream_xt(const double* A, long long n, long long q, long lon
 cudaError_t launch_stream_xd(const double* A, long long n, long long q, long long lda,
                              const double* rs, int svr, int k, const double* d, double* out,
                              long long nlog, cudaStream_t stream, double* sq_part, double* sq_out,
-                             unsigned int* sq_ticket) {
+                             unsigned int* sq_ticket, int epi, const uint8_t* fm,
+                             const double* av) {
   StreamArgs p{};
+  p.epi = sq_out ? (epi ? epi : 1) : 0;
+  p.fm = fm;
+  p.av = av;
   p.sq_part = sq_part;
   p.sq_out = sq_out;
   p.sq_ticket = sq_ticket;

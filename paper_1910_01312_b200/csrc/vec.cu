@@ -146,18 +146,28 @@ struct HsDotArgs {
   double beta, alpha;
   const double* add;
   double* out;
-  const double* sums;
+  const double* ay_p;  // a_J'y_J
+  const double* aa_p;  // a_J'a_J
   const double* g;
   const double* w;
   const double* qw;
   double* dots_out;
   unsigned int* ticket;
   double* part;
+  const double* t;     // optional: dots_out[3] = t't (length q), by block 0
+  long long q;
 };
 
 __global__ void __launch_bounds__(SSNAL_NT) hs_finish_dots_kernel(HsDotArgs p) {
   __shared__ double red[3 * 32];
-  const double ay = p.sums[0], aa = p.sums[1];
+  if (p.t && blockIdx.x == 0) {
+    double tt[1] = {0.0};
+    for (long long i = threadIdx.x; i < p.q; i += blockDim.x) tt[0] += p.t[i] * p.t[i];
+    const int ops1[1] = {0};
+    block_reduce<1>(tt, ops1, red);
+    if (threadIdx.x == 0) p.dots_out[3] = tt[0];
+  }
+  const double ay = *p.ay_p, aa = *p.aa_p;
   const double coef = aa != 0.0 ? ay / aa : 0.0;
   double acc[3] = {0.0, 0.0, 0.0};
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
@@ -191,8 +201,19 @@ cudaError_t launch_hs_apply_dots(const uint8_t* fm, const double* a, const doubl
   const double* ys[2] = {y, nullptr};
   cudaError_t e = launch_dots(2, xs, ys, fm, n, sums, ws, stream);
   if (e != cudaSuccess) return e;
-  HsDotArgs p{fm, a, y, n, beta, alpha, add, out, sums, g, w, qw, dots_out,
-              (unsigned int*)ws, (double*)((char*)ws + TICKET_BYTES)};
+  HsDotArgs p{fm, a, y, n, beta, alpha, add, out, sums, sums + 1, g, w, qw, dots_out,
+              (unsigned int*)ws, (double*)((char*)ws + TICKET_BYTES), nullptr, 0};
+  { note_launch(); hs_finish_dots_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(p); }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hs_finish_dots(const uint8_t* fm, const double* a, const double* y, long long n,
+                                  double beta, const double* add, double alpha, double* out,
+                                  const double* ay, const double* aa, const double* g,
+                                  const double* w, const double* qw, const double* t, long long q,
+                                  double* dots_out, void* ws, cudaStream_t stream) {
+  HsDotArgs p{fm, a, y, n, beta, alpha, add, out, ay, aa, g, w, qw, dots_out,
+              (unsigned int*)ws, (double*)((char*)ws + TICKET_BYTES), t, q};
   { note_launch(); hs_finish_dots_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(p); }
   return cudaGetLastError();
 }

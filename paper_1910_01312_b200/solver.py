@@ -307,11 +307,10 @@ class _Engine:
             be.dense_gram(op, self.J, self.pcount, self.n, self.box.a_dev, sigma, self.asa_dev,
                           self.M, self.m1)
             be.chol_solve(self.M, self.q, self.gr[0], -1.0, self.t[0], self.info)
-        op.x(self.t, self.qdir.view(1, -1), k=1)
-        # d = -s - sigma P(Qd)  (ref solver.py:269)
-        be.hs_apply(self.free, self.box.a_dev, self.qdir, -sigma, self.s, -1.0, self.dir)
-        be.dots([(self.grad, self.dir), (self.w, self.qw), (self.w, self.qdir)], self.scal)
-        be.dots([(self.t[0], None)], self.scal[3:4])  # length q, separate reduction
+        # Qd = X t, d = -s - sigma P(Qd) (ref solver.py:269), {g'd, w'Qw, w'Qd, t't}: one
+        # fused library call (a_J'a_J from the projection record), as the C++ driver
+        be.direction_epilogue(op, self.t[0], self.qdir, self.free, self.box.a_dev, self.asa_dev,
+                              self.s, sigma, self.grad, self.w, self.qw, self.dir, self.scal[0:4])
 
     def pb_direct_limit(self):
         return self._direct_limit

@@ -41,8 +41,10 @@ for n in (50_000, 1_000_000):
     lam = float(be.read_states(st.cpu())[0]['lam'])
     t1 = timeit(lambda: be.project(v, box, st, 1, x_out=xo, free_out=fo, hint=lam))
     t4 = timeit(lambda: be.project(v, box, st, 4, B=Bv, coefs=[1, .5, .25, .125], x_out=xo, free_out=fo, hint=lam))
+    st8 = be.new_states(8); xo8 = be.empty((8, n)); fo8 = be.zeros((8, n), torch.uint8)
+    t8 = timeit(lambda: be.project(v, box, st8, 8, B=Bv, coefs=[2.0 ** -k for k in range(8)], x_out=xo8, free_out=fo8, hint=lam))
     tc = timeit(lambda: be.project(v, box, st, 1, x_out=xo, free_out=fo, hint=0.0))
-    print(f"project n={n}: warm T=1 {t1:.1f} us, warm T=4 {t4:.1f} us, cold-hint T=1 {tc:.1f} us, passes={be.read_states(st.cpu())[0]['passes']}")
+    print(f"project n={n}: warm T=1 {t1:.1f} us, warm T=4 {t4:.1f} us, T=8 {t8:.1f} us, cold-hint T=1 {tc:.1f} us, passes={be.read_states(st.cpu())[0]['passes']}")
     out = be.zeros(8)
     w = [torch.from_numpy(rng.standard_normal(n)).cuda() for _ in range(8)]
     for k in (1, 4):

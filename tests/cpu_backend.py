@@ -153,6 +153,24 @@ class CpuTestBackend:
         grad.copy_(torch.from_numpy(gv))
         g2.view(-1)[0] = float(gv @ gv)
 
+    def direction_epilogue(self, op, t, qdir, free, a, asa_dev, s, sigma, grad, w, qw, dir_out,
+                           dots4):
+        self._count("direction_epilogue")
+        X = self._x_rows(op)
+        qd = X @ t.reshape(-1).numpy()
+        qdir.view(-1).copy_(torch.from_numpy(qd))
+        fm = free.numpy().astype(bool)
+        av = a.numpy()
+        aa = float(asa_dev.view(-1)[0])
+        coef = float((av[fm] * qd[fm]).sum()) / aa if aa != 0.0 else 0.0
+        d = -s.numpy() - sigma * np.where(fm, qd - coef * av, 0.0)
+        dir_out.copy_(torch.from_numpy(d))
+        tv = t.reshape(-1).numpy()
+        vals = [float(grad.numpy() @ d), float(w.numpy() @ qw.numpy()), float(w.numpy() @ qd),
+                float(tv @ tv)]
+        for k in range(4):
+            dots4.view(-1)[k] = vals[k]
+
     def dense_gram(self, op, J, p_dev, p_max, a, sigma, asa_dev, M, m1):
         self._count("dense_gram")
         X = self._x_rows(op)
