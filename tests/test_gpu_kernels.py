@@ -269,3 +269,77 @@ def test_csr_products(pkg, n, q, nnz_row, zipf):
     np.testing.assert_allclose(g, X.T @ v, rtol=1e-12, atol=1e-11 * max(1, np.abs(X).sum(axis=0).max()))
     if zipf and n > 1000:
         assert op.nslots > 0  # hot columns were split
+
+
+@pytest.mark.parametrize("shape,svr,aligned", [((3001, 300), False, True), ((2000, 51), False, False),
+                                                ((1500, 64), True, True)])
+def test_fused_gradient_and_direction_epilogue(pkg, shape, svr, aligned):
+    """ssnal_dense_gradient / ssnal_dense_direction_epilogue against the unfused kernels
+    (streaming route when q is even and A 16-byte aligned, fallback otherwise)."""
+    from paper_1910_01312_b200 import operators
+
+    be = pkg.default_backend()
+    rng = np.random.default_rng(shape[0] + shape[1])
+    n_phys, q = shape
+    A = _dev(rng.standard_normal((n_phys, q)))
+    labels = None if svr else np.where(rng.random(n_phys) < 0.5, 1.0, -1.0)
+    op = operators.LinearKernelOperator(A, labels=labels, svr_block=svr)
+    n = op.n
+    w, xp, a = (_dev(rng.standard_normal(n)) for _ in range(3))
+    s, grad, g2 = be.empty(n), be.empty(n), be.zeros(4)
+    gr = be.empty((1, q))
+    be.dense_gradient(op, w, xp, s, gr[0], grad, g2[0:1])
+    s_ref = w - xp
+    gr_ref = op.xt([s_ref])
+    grad_ref = op.x(gr_ref)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(s, s_ref)
+    np.testing.assert_allclose(gr.cpu().numpy(), gr_ref.cpu().numpy(), rtol=1e-13, atol=1e-12)
+    np.testing.assert_allclose(grad.cpu().numpy(), grad_ref.cpu().numpy(), rtol=1e-13, atol=1e-11)
+    assert float(g2[0]) == pytest.approx(float(grad_ref @ grad_ref), rel=1e-13)
+    # direction epilogue from a random t and free mask
+    t = _dev(rng.standard_normal(q))
+    free = _dev((rng.random(n) < 0.3).astype(np.uint8), torch.uint8)
+    fm = free.cpu().numpy().astype(bool)
+    av = a.cpu().numpy()
+    asa = be.zeros(1)
+    asa[0] = float((av[fm] ** 2).sum())
+    qw = _dev(rng.standard_normal(n))
+    qdir, dirv, dots4 = be.empty(n), be.empty(n), be.zeros(4)
+    sigma = 3.7
+    be.direction_epilogue(op, t, qdir, free, a, asa, s, sigma, grad, w, qw, dirv, dots4)
+    qd_ref = op.x(t.view(1, -1))[0].cpu().numpy()
+    coef = float((av[fm] * qd_ref[fm]).sum()) / float(asa[0])
+    d_ref = -s.cpu().numpy() - sigma * np.where(fm, qd_ref - coef * av, 0.0)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(qdir.cpu().numpy(), qd_ref, rtol=1e-13, atol=1e-11)
+    np.testing.assert_allclose(dirv.cpu().numpy(), d_ref, rtol=1e-11, atol=1e-10)
+    ref4 = [grad.cpu().numpy() @ d_ref, w.cpu().numpy() @ qw.cpu().numpy(),
+            w.cpu().numpy() @ qd_ref, t.cpu().numpy() @ t.cpu().numpy()]
+    np.testing.assert_allclose(dots4.cpu().numpy(), ref4, rtol=1e-10)
+
+
+def test_cluster_projection_matches_grid_kernel(pkg):
+    """The cluster route (n <= 65536, every trial count) and the grid-wide fused route
+    (larger n) solve the same projections: lambda to 1e-12, free masks identical."""
+    from paper_1910_01312_b200 import projection
+
+    be = pkg.default_backend()
+    rng = np.random.default_rng(21)
+    for n in (1000, 65536, 70000):  # cluster, cluster (limit), grid-wide
+        a = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+        v = rng.standard_normal(n) * 2.0
+        B = rng.standard_normal(n) * 0.05
+        box = projection.BoxLineSet(a, 0.0, np.zeros(n), np.ones(n))
+        coefs = [2.0 ** -k for k in range(8)]
+        st = be.new_states(8)
+        xo = be.empty((8, n))
+        fo = be.zeros((8, n), torch.uint8)
+        be.project(_dev(v), box, st, 8, B=_dev(B), coefs=coefs, x_out=xo, free_out=fo)
+        rec = be.read_states(st.cpu())
+        bl = O.BoxLine(a, 0.0, np.zeros(n), np.ones(n))
+        for k in range(8):
+            x_ref, lam_ref, free_ref = O.project(v - coefs[k] * B, bl)
+            assert abs(rec[k]["lam"] - lam_ref) <= 1e-12 * (1 + abs(lam_ref))
+            np.testing.assert_allclose(xo[k].cpu().numpy(), x_ref, atol=1e-12)
+            np.testing.assert_array_equal(fo[k].cpu().numpy().astype(bool), free_ref)
