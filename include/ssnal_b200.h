@@ -44,6 +44,9 @@ typedef struct ssnal_proj_state_t {
   double sum_a2_free;             /* a_J' a_J over the free set (a' Sigma a)            */
   double sum_xv;                  /* sum x_i (2 v_i - x_i) = ||v||^2 - ||v - x||^2 without
                                      cancellation (the psi term of ref solver.py:130-133) */
+  double sum_bh;                  /* trials with a base point only (sum_v2 is 0 then):
+                                     Bregman divergence of h = |.|^2/2 - dist(., K)^2/2
+                                     between the trial and the base, psi differences  */
   long long nfree;                /* p = |J|                                            */
   int status;                     /* 3 applied, 2 lambda known, <0 infeasible, else searching */
   int passes;                     /* K-ary bracketing passes used                       */
@@ -84,6 +87,19 @@ int ssnal_project(const double* A, const double* B, const double* coef,
                   ssnal_proj_state_t* state, void* ws,
                   double* x_out, uint8_t* free_out, const double* ref,
                   double lam_hint, int newton_passes, int phases, int passes, void* stream);
+
+/* Line-search trials: as ssnal_project, plus the projection base = Pi(u) (multiplier
+ * base_lam) of the base point the trials A - coef[t] B start from.  Each record then
+ * carries sum_bh = the Bregman divergence of h = |.|^2/2 - dist(., K)^2/2 between
+ * trial and base (sum_v2 = 0), from which psi(w + alpha d) - psi(w) is formed without
+ * cancellation (ref solver.py:292-319 evaluates psi_t and psi_0 separately). */
+int ssnal_project_ex(const double* A, const double* B, const double* coef,
+                     const double* a, const double* l, const double* u,
+                     double l_const, double u_const, double d, int64_t n, int T,
+                     ssnal_proj_state_t* state, void* ws,
+                     double* x_out, uint8_t* free_out, const double* ref,
+                     const double* base, double base_lam,
+                     double lam_hint, int newton_passes, int phases, int passes, void* stream);
 
 /* ---- HS-Jacobian -------------------------------------------------------
  * Replaces ref projection.py:214-225 hs_jacobian_apply.
@@ -212,7 +228,8 @@ typedef struct ssnal_options_t {
   int max_outer;
   double mu, backtrack, tau, eta;                                         /* SsnOptions */
   int max_inner, direct_solve_threshold, cg_max_iters, line_search_batch;
-  int psi_stable;           /* 1: psi via sum Pi(u)(2u - Pi(u)); 0: reference formula */
+  int psi_stable;           /* 0: reference formula; 1: psi via sum Pi(u)(2u - Pi(u));
+                               2: Armijo on psi differences (Bregman form, ssnal_project_ex) */
   int profile;              /* 1: CUDA-event timing per op class into the report      */
 } ssnal_options_t;
 
@@ -257,13 +274,15 @@ int ssnal_alm_solve_dense(const ssnal_dense_problem_t* problem, const ssnal_opti
  *     > lam (+inf), nearest breakpoint < lam (-inf) }
  *   mode 1 (apply at lam[t]): x_out / free_out (T x n) and rec[t*8 + 0..5] =
  *     { sum v^2, sum (v-x)^2, sum (x-ref)^2, sum_free a^2, nfree, sum x(2v-x) }
+ *     (base != NULL: slot 0 is the Bregman term of ssnal_project_ex instead of sum v^2)
  * with v = A - coef[t] B.  coef and lam are HOST arrays of T <= 16; rec is a
  * DEVICE array of 8 T doubles.  ws: ssnal_proj_local_ws_bytes(n, T). */
 size_t ssnal_proj_local_ws_bytes(int64_t n, int T);
 int ssnal_proj_local(const double* A, const double* B, const double* coef, const double* lam,
                      const double* a, const double* l, const double* u, double l_const,
                      double u_const, int64_t n, int T, int mode, double* x_out, uint8_t* free_out,
-                     const double* ref, double* rec, void* ws, void* stream);
+                     const double* ref, const double* base, double base_lam, double* rec,
+                     void* ws, void* stream);
 /* out[i] = sum_{r<k} src[r*len + i] in rank order (the all-gathered partials of
  * X^T v, Gram blocks and dot records; deterministic). */
 int ssnal_sum_slices(int k, int64_t len, const double* src, double* out, void* stream);

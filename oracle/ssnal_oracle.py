@@ -289,15 +289,19 @@ def set_psi_mode(mode):
     """'reference' (ref solver.py:130-133 verbatim) or 'stable': the same psi with
     ||u||^2 - ||u - Pi(u)||^2 evaluated as Pi(u)'(2u - Pi(u)) -- identical in exact
     arithmetic, free of the cancellation that stalls Armijo when ||u|| >> ||Pi(u)||
-    (the product path's evaluation)."""
-    if mode not in ("reference", "stable"):
+    (the product path's evaluation).
+    The product's 'delta' mode (line search on psi differences)
+    is restated too: psi(w + a d) - psi(w) = a g'd + a^2 d'Qd / 2 + B_h / sigma with
+    B_h = sum (x_t - Pi)(u_t - (x_t + Pi)/2 - lam_bar a) the Bregman divergence of
+    h = |.|^2/2 - dist(., K)^2/2, and no psi-resolution floor."""
+    if mode not in ("reference", "stable", "delta"):
         raise ValueError(mode)
     PSI_MODE["mode"] = mode
 
 
 def psi_value(w_qw, u, px, x_sq, sigma):
     """ref solver.py:130-133."""
-    if PSI_MODE["mode"] == "stable":
+    if PSI_MODE["mode"] in ("stable", "delta"):
         return 0.5 * w_qw + float(px.dot(2.0 * u - px)) / (2.0 * sigma) - x_sq / (2.0 * sigma)
     r = u - px
     return 0.5 * w_qw + (float(u.dot(u)) - float(r.dot(r))) / (2.0 * sigma) - x_sq / (2.0 * sigma)
@@ -405,7 +409,13 @@ def newton_direction(s, grad, free, sigma, op, a, opts):
     return direction, q_dir, dqd
 
 
-def line_search(w, qw, direction, q_dir, dqd, grad, psi0, u, x_k, sigma, bl, opts):
+def bregman(xt, lam_t, px, lam, u_t, a):
+    """B_h between a trial projection (xt, lam_t) at u_t and the base projection
+    (px, lam) (csrc/proj.cu bregman_term)."""
+    return float(((xt - px) * (u_t - 0.5 * (xt + px) - 0.5 * (lam_t + lam) * a)).sum())
+
+
+def line_search(w, qw, direction, q_dir, dqd, grad, psi0, u, x_k, sigma, bl, opts, base=None):
     """Armijo backtracking, one projection per trial; ref solver.py:292-319.
 
     Returns (alpha, w_new, qw_new, psi_new, u_new, (px, lam, free))."""
@@ -420,8 +430,15 @@ def line_search(w, qw, direction, q_dir, dqd, grad, psi0, u, x_k, sigma, bl, opt
         u_t = u - (sigma * alpha) * q_dir
         pr = project(u_t, bl)
         quad = w_qw + 2.0 * alpha * w_qdir + alpha * alpha * dqd
-        psi_t = psi_value(quad, u_t, pr[0], x_sq, sigma)
-        if psi_t <= psi0 + opts.mu * alpha * gd:
+        if PSI_MODE["mode"] == "delta":
+            dpsi = alpha * gd + 0.5 * alpha * alpha * dqd + bregman(
+                pr[0], pr[1], base[0], base[1], u_t, bl.a) / sigma
+            psi_t = psi0 + dpsi
+            ok = dpsi <= opts.mu * alpha * gd
+        else:
+            psi_t = psi_value(quad, u_t, pr[0], x_sq, sigma)
+            ok = psi_t <= psi0 + opts.mu * alpha * gd
+        if ok:
             return alpha, w + alpha * direction, qw + alpha * q_dir, psi_t, u_t, pr
         alpha *= opts.backtrack
     raise LineSearchFailed("Armijo backtracking exceeded 60 halvings")
@@ -461,12 +478,14 @@ def ssn_solve(st, op, c, bl, alm, ssn, eps_k, delta_k, trace=None):
             dqd = float(direction.dot(q_dir))
             steepest = True
         psi0 = psi_value(float(st["w"].dot(st["qw"])), u, pr[0], x_sq, sigma)
-        if ssn.mu * abs(float(grad.dot(direction))) <= 1e-16 * (1.0 + abs(psi0)):
+        delta = PSI_MODE["mode"] == "delta"
+        if not delta and ssn.mu * abs(float(grad.dot(direction))) <= 1e-16 * (1.0 + abs(psi0)):
             converged, exhausted = True, False
             break
         try:
             _, st["w"], st["qw"], _, u, pr = line_search(
-                st["w"], st["qw"], direction, q_dir, dqd, grad, psi0, u, x_k, sigma, bl, ssn)
+                st["w"], st["qw"], direction, q_dir, dqd, grad, psi0, u, x_k, sigma, bl, ssn,
+                base=pr)
         except LineSearchFailed:
             if steepest:
                 exhausted = False
@@ -474,12 +493,13 @@ def ssn_solve(st, op, c, bl, alm, ssn, eps_k, delta_k, trace=None):
             direction = -grad
             q_dir = op.matvec(direction)
             dqd = float(direction.dot(q_dir))
-            if ssn.mu * float(grad.dot(grad)) <= 1e-16 * (1.0 + abs(psi0)):
+            if not delta and ssn.mu * float(grad.dot(grad)) <= 1e-16 * (1.0 + abs(psi0)):
                 exhausted = False
                 break
             try:
                 _, st["w"], st["qw"], _, u, pr = line_search(
-                    st["w"], st["qw"], direction, q_dir, dqd, grad, psi0, u, x_k, sigma, bl, ssn)
+                    st["w"], st["qw"], direction, q_dir, dqd, grad, psi0, u, x_k, sigma, bl, ssn,
+                base=pr)
             except LineSearchFailed:
                 exhausted = False
                 break

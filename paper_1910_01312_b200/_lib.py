@@ -20,6 +20,7 @@ PROJ_STATE_DTYPE = np.dtype([
     ("below_max", "f8"), ("above_min", "f8"), ("in_min", "f8"), ("in_max", "f8"),
     ("in_count", "i8"), ("lam", "f8"), ("tmin", "f8"), ("tmax", "f8"),
     ("sum_v2", "f8"), ("sum_r2", "f8"), ("sum_dref2", "f8"), ("sum_a2_free", "f8"), ("sum_xv", "f8"),
+    ("sum_bh", "f8"),
     ("nfree", "i8"), ("status", "i4"), ("passes", "i4"), ("ticket", "u4"), ("pad_", "u4"),
 ])
 
@@ -47,6 +48,8 @@ _SIGNATURES = {
     "ssnal_compact_ws_bytes": (_SZ, [_I64]),
     "ssnal_project": (_I, [_P, _P, _P, _P, _P, _P, _D, _D, _D, _I64, _I, _P, _P, _P, _P, _P,
                            _D, _I, _I, _I, _P]),
+    "ssnal_project_ex": (_I, [_P, _P, _P, _P, _P, _P, _D, _D, _D, _I64, _I, _P, _P, _P, _P, _P,
+                              _P, _D, _D, _I, _I, _I, _P]),
     "ssnal_hs_apply": (_I, [_P, _P, _P, _I64, _D, _P, _D, _P, _P, _P]),
     "ssnal_dots": (_I, [_I, _P, _P, _P, _I64, _P, _P, _P]),
     "ssnal_vec": (_I, [_I, _I64, _D, _P, _P, _P, _P, _P]),
@@ -116,7 +119,7 @@ _SIGNATURES.update({
                                    _P, ctypes.POINTER(Report), _P, _SZ, PROGRESS_FN, _P, _P]),
     "ssnal_proj_local_ws_bytes": (_SZ, [_I64, _I]),
     "ssnal_proj_local": (_I, [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I64, _I, _I, _P, _P, _P, _P,
-                              _P, _P]),
+                              _D, _P, _P, _P]),
     "ssnal_sum_slices": (_I, [_I, _I64, _P, _P, _P]),
     "ssnal_hs_apply_coef": (_I, [_P, _P, _P, _I64, _D, _P, _D, _D, _P, _P]),
     "ssnal_qspace_assemble": (_I, [_I64, _P, _D, _D, _D, _P, _P]),

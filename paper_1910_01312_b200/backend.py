@@ -102,7 +102,8 @@ class CudaBackend:
     KARY_PASSES = 0
 
     def project(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
-                ref=None, phases=None, passes=None, hint=0.0, newton=None):
+                ref=None, phases=None, passes=None, hint=0.0, newton=None, base=None,
+                base_lam=0.0):
         n = box.n
         if newton is None:
             newton = self.NEWTON_PASSES
@@ -118,11 +119,11 @@ class CudaBackend:
         per_phase = 8 * n * (2 + (B is not None) + (box.l_dev is not None) + (box.u_dev is not None))
         self._timed(
             "project", per_phase * (newton + 1), _lib.call,
-            "ssnal_project", _ptr(A), _ptr(B),
+            "ssnal_project_ex", _ptr(A), _ptr(B),
             _lib.ctypes.cast(coef_arr, _lib.ctypes.c_void_p) if coef_arr is not None else None,
             _ptr(box.a_dev), _ptr(box.l_dev), _ptr(box.u_dev), box.l_const, box.u_const, box.d,
-            n, T, _ptr(states), _ptr(ws), _ptr(x_out), _ptr(free_out), _ptr(ref),
-            float(hint), int(newton), phases, passes, self.stream())
+            n, T, _ptr(states), _ptr(ws), _ptr(x_out), _ptr(free_out), _ptr(ref), _ptr(base),
+            float(base_lam), float(hint), int(newton), phases, passes, self.stream())
 
     def project_sync(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
                      ref=None, hint=0.0):
@@ -231,7 +232,7 @@ class CudaBackend:
 
     # ---------------------------------------------------------------- sharded path
     def proj_local(self, A, box, T, lam, mode, rec, B=None, coefs=None, x_out=None,
-                   free_out=None, ref=None):
+                   free_out=None, ref=None, base=None, base_lam=0.0):
         """Shard-local projection records at host multipliers ``lam`` (csrc/dist.cu)."""
         n = box.n
         lam_arr = (_lib.ctypes.c_double * T)(*[float(v) for v in lam])
@@ -243,7 +244,8 @@ class CudaBackend:
                   _lib.ctypes.cast(coef_arr, _lib.ctypes.c_void_p) if coef_arr is not None else None,
                   _lib.ctypes.cast(lam_arr, _lib.ctypes.c_void_p), _ptr(box.a_dev), _ptr(box.l_dev),
                   _ptr(box.u_dev), box.l_const, box.u_const, n, T, int(mode), _ptr(x_out),
-                  _ptr(free_out), _ptr(ref), _ptr(rec), _ptr(ws), self.stream())
+                  _ptr(free_out), _ptr(ref), _ptr(base), float(base_lam), _ptr(rec), _ptr(ws),
+                  self.stream())
 
     def sum_slices(self, k, src, out):
         """out = sum of the k equal slices of src, in slice order."""

@@ -59,8 +59,9 @@ cudaError_t launch_dense_gradient(const double* A, long long n, long long q, lon
 cudaError_t launch_proj_local(const double* A, const double* B, const double* coef,
                               const double* lam, const double* a, const double* l,
                               const double* u, double lc, double uc, long long n, int T, int mode,
-                              double* x_out, uint8_t* free_out, const double* ref, double* rec,
-                              void* ws, cudaStream_t s);
+                              double* x_out, uint8_t* free_out, const double* ref,
+                              const double* base, double base_lam, double* rec, void* ws,
+                              cudaStream_t s);
 cudaError_t launch_sum_slices(int k, long long len, const double* src, double* out,
                               cudaStream_t s);
 cudaError_t launch_hs_apply_coef(const uint8_t* fm, const double* a, const double* y, long long n,
@@ -123,11 +124,11 @@ size_t ssnal_dense_xt_ws_bytes(int64_t n_phys, int64_t q, int k) {
 size_t ssnal_gram_ws_bytes(int64_t q) { return gram_ws_bytes(q); }
 size_t ssnal_compact_ws_bytes(int64_t n) { return compact_ws_bytes(n); }
 
-int ssnal_project(const double* A, const double* B, const double* coef, const double* a,
-                  const double* l, const double* u, double l_const, double u_const, double d,
-                  int64_t n, int T, ssnal_proj_state_t* state, void* ws, double* x_out,
-                  uint8_t* free_out, const double* ref, double lam_hint, int newton_passes,
-                  int phases, int passes, void* stream) {
+int ssnal_project_ex(const double* A, const double* B, const double* coef, const double* a,
+                     const double* l, const double* u, double l_const, double u_const, double d,
+                     int64_t n, int T, ssnal_proj_state_t* state, void* ws, double* x_out,
+                     uint8_t* free_out, const double* ref, const double* base, double base_lam,
+                     double lam_hint, int newton_passes, int phases, int passes, void* stream) {
   if (n < 1) return fail_arg("ssnal_project", "n < 1");
   if (T < 1 || T > SSNAL_MAX_TRIALS) return fail_arg("ssnal_project", "T must be in [1, 16]");
   if (!A || !a || !state || !ws) return fail_arg("ssnal_project", "null A/a/state/ws");
@@ -137,9 +138,20 @@ int ssnal_project(const double* A, const double* B, const double* coef, const do
   L.A = A; L.B = B; L.coef = coef; L.a = a; L.l = l; L.u = u;
   L.lc = l_const; L.uc = u_const; L.d = d; L.n = n; L.T = T;
   L.st = state; L.part = (double*)ws; L.x_out = x_out; L.free_out = free_out; L.ref = ref;
+  L.base = base; L.base_lam = base_lam;
   L.phases = phases; L.passes = passes;
   L.hint = lam_hint; L.newton = newton_passes < 0 ? 0 : newton_passes;
   return check("ssnal_project", launch_project(L, S(stream)));
+}
+
+int ssnal_project(const double* A, const double* B, const double* coef, const double* a,
+                  const double* l, const double* u, double l_const, double u_const, double d,
+                  int64_t n, int T, ssnal_proj_state_t* state, void* ws, double* x_out,
+                  uint8_t* free_out, const double* ref, double lam_hint, int newton_passes,
+                  int phases, int passes, void* stream) {
+  return ssnal_project_ex(A, B, coef, a, l, u, l_const, u_const, d, n, T, state, ws, x_out,
+                          free_out, ref, nullptr, 0.0, lam_hint, newton_passes, phases, passes,
+                          stream);
 }
 
 int ssnal_hs_apply(const uint8_t* free_mask, const double* a, const double* y, int64_t n,
@@ -278,15 +290,16 @@ size_t ssnal_proj_local_ws_bytes(int64_t n, int T) { return proj_local_ws_bytes(
 int ssnal_proj_local(const double* A, const double* B, const double* coef, const double* lam,
                      const double* a, const double* l, const double* u, double l_const,
                      double u_const, int64_t n, int T, int mode, double* x_out, uint8_t* free_out,
-                     const double* ref, double* rec, void* ws, void* stream) {
+                     const double* ref, const double* base, double base_lam, double* rec,
+                     void* ws, void* stream) {
   if (n < 1) return fail_arg("ssnal_proj_local", "n < 1");
   if (T < 1 || T > SSNAL_MAX_TRIALS) return fail_arg("ssnal_proj_local", "T must be in [1, 16]");
   if (!A || !a || !lam || !rec || !ws) return fail_arg("ssnal_proj_local", "null A/a/lam/rec/ws");
   if (B && !coef) return fail_arg("ssnal_proj_local", "B given without coef");
   if (mode != 0 && mode != 1) return fail_arg("ssnal_proj_local", "mode must be 0 or 1");
   return check("ssnal_proj_local", launch_proj_local(A, B, coef, lam, a, l, u, l_const, u_const,
-                                                     n, T, mode, x_out, free_out, ref, rec, ws,
-                                                     S(stream)));
+                                                     n, T, mode, x_out, free_out, ref, base,
+                                                     base_lam, rec, ws, S(stream)));
 }
 
 int ssnal_sum_slices(int k, int64_t len, const double* src, double* out, void* stream) {

@@ -36,6 +36,8 @@ struct LocalArgs {
   double* x_out;
   unsigned char* free_out;
   const double* ref;
+  const double* base;  // line-search base Pi (slot 0 becomes the Bregman term, proj.cu)
+  double base_lam;
   double* part;  // [T][nblk][DREC]
 };
 
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_local_eval_kernel(LocalArgs p) 
 }
 
 // x = clip(v - lam a, l, u), free mask (ref projection.py:134-149 tolerance, as in
-// proj.cu's apply) and {sum v^2, sum (v-x)^2, sum (x-ref)^2, sum_free a^2, nfree,
+// proj.cu's apply) and {sum v^2 (with a base: the Bregman term), sum (v-x)^2, sum (x-ref)^2, sum_free a^2, nfree,
 // sum x(2v - x)}
 __global__ void __launch_bounds__(SSNAL_NT) proj_local_apply_kernel(LocalArgs p) {
   __shared__ double red[6 * 32];
@@ -103,7 +105,12 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_local_apply_kernel(LocalArgs p)
     if (xo) xo[i] = x;
     if (fo) fo[i] = fr ? 1 : 0;
     const double r = v - x;
-    sv2 += v * v;
+    if (p.base) {
+      const double xb = p.base[i];
+      sv2 += (x - xb) * (v - 0.5 * (x + xb) - 0.5 * (lam + p.base_lam) * a);
+    } else {
+      sv2 += v * v;
+    }
     sr2 += r * r;
     sxv += x * (2.0 * v - x);
     if (p.ref) { const double dd = x - p.ref[i]; sd2 += dd * dd; }
@@ -141,11 +148,13 @@ size_t proj_local_ws_bytes(long long n, int T) {
 cudaError_t launch_proj_local(const double* A, const double* B, const double* coef,
                               const double* lam, const double* a, const double* l,
                               const double* u, double lc, double uc, long long n, int T, int mode,
-                              double* x_out, uint8_t* free_out, const double* ref, double* rec,
-                              void* ws, cudaStream_t s) {
+                              double* x_out, uint8_t* free_out, const double* ref,
+                              const double* base, double base_lam, double* rec, void* ws,
+                              cudaStream_t s) {
   LocalArgs p;
   p.A = A; p.B = B; p.a = a; p.l = l; p.u = u; p.lc = lc; p.uc = uc; p.n = n;
   p.x_out = x_out; p.free_out = free_out; p.ref = ref; p.part = (double*)ws;
+  p.base = base; p.base_lam = base_lam;
   for (int t = 0; t < T; ++t) {
     p.coef[t] = B ? coef[t] : 0.0;
     p.lam[t] = lam[t];

@@ -160,6 +160,7 @@ struct Layout {
   // sparse operator: sample-space CG buffers, scattered vector, CSC partial slots
   double *ys, *tq, *cg_gJ, *cg_aJ, *cg_b, *cg_y, *cg_r, *cg_pv, *cg_Ap, *cg_zq, *cg_w, *cgs,
       *cg_part, *csc_part, *cg_d, *cg_u, *cg_z;
+  CscJ cj;  // J-restricted CSC (matrix-free Newton systems)
 };
 
 size_t cg_part_doubles(long long n) { return 2 * (size_t)stream_blocks(n, 4) + 8; }
@@ -225,6 +226,8 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
     const long long md = std::min<long long>(SPARSE_DIRECT_MAX, std::max(q, n));
     L.M = cv.take<double>((size_t)md * md);
     L.ws_ps = cv.take<double>(4 * (size_t)md);
+    char* cj = cv.take<char>(cscj_ws_bytes(*csr));
+    if (base) L.cj = cscj_layout(*csr, cj);
   }
   *total = cv.off + 256;
   return L;
@@ -312,9 +315,7 @@ struct Driver {
     const CsrOp& op = *P.csr;
     const long long q = P.q;
     ck(launch_gather(L.J, p, P.a, L.cg_aJ, S));
-    ck(launch_scatter(L.J, p, L.cg_aJ, L.ys, S));
-    ck(launch_csc_xt(op, L.ys, L.cg_u, L.csc_part, S));  // u = X_J^T a_J
-    ck(launch_scatter_zero(L.J, p, L.ys, S));
+    ck(launch_cscj_xt(op, L.cj, L.cg_aJ, L.cg_u, L.csc_part, S));  // u = X_J^T a_J
     ck(launch_csc_colsq(op, L.fr, L.cg_d, L.csc_part, S));
     ck(launch_cg_jacobi(q, L.cg_d, L.cg_u, asa, sigma, L.cg_d, S));
     ck(launch_vec(4, q, -1.0, L.gr, nullptr, nullptr, L.cg_b, S));
@@ -325,9 +326,7 @@ struct Driver {
       ck(launch_csr_xd(op, L.J, p, v, L.cg_zq, S));
       dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
       ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
-      ck(launch_scatter(L.J, p, L.cg_w, L.ys, S));
-      ck(launch_csc_xt(op, L.ys, out, L.csc_part, S));
-      ck(launch_scatter_zero(L.J, p, L.ys, S));
+      ck(launch_cscj_xt(op, L.cj, L.cg_w, out, L.csc_part, S));
     };
     for (int it = 0; it < max_it;) {
       for (int b = 0; b < CG_BATCH && it < max_it; ++b, ++it) {
@@ -364,8 +363,7 @@ struct Driver {
                       std::min(O.eta, SPARSE_CG_ETA), O.tau, L.cgs, L.cg_part, S));
     for (int it = 0; it < max_it;) {
       for (int b = 0; b < CG_BATCH && it < max_it; ++b, ++it) {
-        ck(launch_scatter(L.J, p, L.cg_pv, L.ys, S));
-        ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
+        ck(launch_cscj_xt(op, L.cj, L.cg_pv, L.tq, L.csc_part, S));
         ck(launch_csr_xd(op, L.J, p, L.tq, L.cg_zq, S));
         dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
         ck(launch_cg_ap(p, L.cg_pv, L.cg_zq, L.cg_aJ, asa, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
@@ -377,15 +375,11 @@ struct Driver {
       // (Q + sigma Q P~ Q) d + Q s = sigma^2 X X_J^T P Q_JJ P r
       dots({{L.cg_aJ, L.cg_r}}, L.cgs + 7, p);
       ck(launch_cg_project(p, L.cg_r, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
-      ck(launch_scatter(L.J, p, L.cg_w, L.ys, S));
-      ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
-      ck(launch_scatter_zero(L.J, p, L.ys, S));
+      ck(launch_cscj_xt(op, L.cj, L.cg_w, L.tq, L.csc_part, S));
       ck(launch_csr_xd(op, L.J, p, L.tq, L.cg_zq, S));
       dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
       ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
-      ck(launch_scatter(L.J, p, L.cg_w, L.ys, S));
-      ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
-      ck(launch_scatter_zero(L.J, p, L.ys, S));
+      ck(launch_cscj_xt(op, L.cj, L.cg_w, L.tq, L.csc_part, S));
       ck(launch_csr_xd(op, nullptr, P.n_phys, L.tq, L.tmp, S));
       ck(launch_cg_check(P.n, L.tmp, sigma * sigma, L.cgs, L.cg_part, S));
       ck(cudaMemcpyAsync(H->cg, L.cgs, sizeof(double) * 8, cudaMemcpyDeviceToHost, S));
@@ -397,7 +391,7 @@ struct Driver {
     // w = P_J y, t = -g_r + sigma X^T scatter(w)
     dots({{L.cg_aJ, L.cg_y}}, L.cgs + 7, p);
     ck(launch_cg_project(p, L.cg_y, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
-    sparse_t_from_sample(L.cg_w, p);
+    sparse_t_from_sample(L.cg_w, p, true);
     return H->cg[5] != 0.0;
   }
 
@@ -424,6 +418,7 @@ struct Driver {
   void sparse_iterative(long long p, double asa, const double* g2_dev) {
     const bool can_direct = std::min<long long>(p, P.q) <= SPARSE_DIRECT_MAX;
     const int max_it = can_direct ? O.cg_max_iters : 4 * O.cg_max_iters;
+    ck(launch_cscj_build(*P.csr, L.fr, L.J, p, L.cj, S));  // X_J's CSC for every CG product
     const bool ok = (p < P.q && !hot_columns()) ? cg_direction(p, asa, g2_dev, max_it)
                                                 : cg_direction_q(p, asa, g2_dev, max_it);
     if (!ok && can_direct) {
@@ -433,10 +428,14 @@ struct Driver {
   }
 
   // t = -g_r + sigma X_J^T w  for a sample-space w (p, already in range(P_J))
-  void sparse_t_from_sample(const double* w, long long p) {
-    ck(launch_scatter(L.J, p, w, L.ys, S));
-    ck(launch_csc_xt(*P.csr, L.ys, L.tq, L.csc_part, S));
-    ck(launch_scatter_zero(L.J, p, L.ys, S));
+  void sparse_t_from_sample(const double* w, long long p, bool cj = false) {
+    if (cj) {
+      ck(launch_cscj_xt(*P.csr, L.cj, w, L.tq, L.csc_part, S));
+    } else {
+      ck(launch_scatter(L.J, p, w, L.ys, S));
+      ck(launch_csc_xt(*P.csr, L.ys, L.tq, L.csc_part, S));
+      ck(launch_scatter_zero(L.J, p, L.ys, S));
+    }
     ck(launch_vec(4, P.q, sigma, L.tq, nullptr, nullptr, L.t, S));  // sigma X^T P_J y
     ck(launch_vec(3, P.q, 0.0, L.t, L.gr, nullptr, L.t, S));       // - X^T s
   }
@@ -481,6 +480,10 @@ struct Driver {
     pl.lc = P.l_const; pl.uc = P.u_const; pl.d = P.d; pl.n = P.n; pl.T = T;
     pl.st = st; pl.part = (double*)L.ws_proj; pl.x_out = xo; pl.free_out = fo; pl.ref = ref;
     pl.phases = phases; pl.passes = passes; pl.hint = hint; pl.newton = newton_passes;
+    if (B && O.psi_stable == 2) {  // line-search trials: psi differences from the base point
+      pl.base = L.xp;
+      pl.base_lam = lam_cur;
+    }
     // algorithmic bytes: each streaming launch reads v (+B), a (+l, u vectors); apply
     // also writes x and the mask
     const double per = 8.0 * P.n * (2 + (B != nullptr) + (P.l != nullptr) + (P.u != nullptr));
@@ -725,8 +728,11 @@ struct Driver {
       for (int k = 0; k < T; ++k) {
         const double a = alphas[k];
         const double quad = wqw + 2.0 * a * wqdir + a * a * dqd;
-        const double pt = psi(quad, H->st[k], x_sq);
-        if (pt <= psi0 + O.mu * a * gd) {
+        // delta mode: psi(w + a d) - psi(w) = a g'd + a^2 d'Qd / 2 + B_h / sigma
+        const bool ok = O.psi_stable == 2
+                            ? a * gd + 0.5 * a * a * dqd + H->st[k].sum_bh / sigma <= O.mu * a * gd
+                            : psi(quad, H->st[k], x_sq) <= psi0 + O.mu * a * gd;
+        if (ok) {
           lam_cur = H->st[k].lam;
           alpha_out = a;
           j_out = k;
@@ -781,11 +787,13 @@ struct Driver {
       const double gnorm = std::sqrt(gnorm2);
       const double dist = std::sqrt(cur.sum_dref2);
       if (gnorm <= coeff * eps_k && gnorm <= coeff * delta_k * dist) {
+        if (dbg) std::fprintf(stderr, "ssn stop it=%d criteria |g|=%.3e\n", it, gnorm);
         converged = true;
         exhausted = false;
         break;
       }
       if (gnorm <= floor_) {
+        if (dbg) std::fprintf(stderr, "ssn stop it=%d floor |g|=%.3e\n", it, gnorm);
         converged = true;
         exhausted = false;
         break;
@@ -802,7 +810,12 @@ struct Driver {
         first = nullptr;
       }
       const double psi0 = psi(wqw, cur, x_sq);
-      if (O.mu * std::fabs(gd) <= 1e-16 * (1.0 + std::fabs(psi0))) {
+      // predicted decrease below the resolution of psi (ref solver.py:369-371); the
+      // delta mode forms psi differences directly and has no such floor
+      if (O.psi_stable != 2 && O.mu * std::fabs(gd) <= 1e-16 * (1.0 + std::fabs(psi0))) {
+        if (dbg)
+          std::fprintf(stderr, "ssn stop it=%d resolution |g|=%.3e gd=%.3e psi0=%.6e crit=%.3e\n",
+                       it, gnorm, gd, psi0, coeff * eps_k);
         converged = true;
         exhausted = false;
         break;
@@ -818,7 +831,7 @@ struct Driver {
         double sv[4];
         steepest(sv);
         gd = sv[0]; wqw = sv[1]; wqdir = sv[2]; dqd = sv[3];
-        if (O.mu * (-gd) <= 1e-16 * (1.0 + std::fabs(psi0))) {
+        if (O.psi_stable != 2 && O.mu * (-gd) <= 1e-16 * (1.0 + std::fabs(psi0))) {
           exhausted = false;
           break;
         }
@@ -849,6 +862,7 @@ struct Driver {
     else ck(cudaMemsetAsync(L.x, 0, nb, S));
     if (w0) ck(cudaMemcpyAsync(L.w, w0, nb, cudaMemcpyDeviceToDevice, S));
     else ck(cudaMemsetAsync(L.w, 0, nb, S));
+    if (P.csr) ck(cudaMemsetAsync(L.cj.ticket, 0, sizeof(unsigned int), S));
     ck(cudaMemsetAsync(L.qw, 0, nb, S));
     dots({{P.c, nullptr}}, L.scal, P.n);
     fetch(nullptr, 0, false);

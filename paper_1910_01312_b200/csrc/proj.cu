@@ -48,7 +48,21 @@ struct ProjArgs {
   double* x_out;             // [T][n] or null
   unsigned char* free_out;   // [T][n] or null
   const double* ref;         // reference vector for sum (x - ref)^2, or null
+  const double* base;        // Pi at the line-search base point, or null (see bregman_term)
+  double base_lam;           // its multiplier
 };
+
+// Line-search trial from the base point u (projection Pi, multiplier lam_b) to
+// v = u - coef*Qd (projection x, multiplier lam): the i-th term of the Bregman
+// divergence of h(v) = 1/2 ||v||^2 - 1/2 dist(v, K)^2 (grad h = Pi),
+//   B_h = sum_i (x_i - Pi_i)(v_i - (x_i + Pi_i)/2 - lam_bar a_i),  lam_bar = (lam + lam_b)/2
+// (the lam_bar a shift is exact since a'x = a'Pi = d and removes the large part of
+// every free-slot term).  psi(w + alpha d) - psi(w) = alpha g'd + alpha^2 d'Qd / 2 + B_h / sigma
+// then needs no difference of O(||u||^2) sums.
+__device__ __forceinline__ double bregman_term(double x, double xb, double v, double a,
+                                               double lam_bar) {
+  return (x - xb) * (v - 0.5 * (x + xb) - lam_bar * a);
+}
 
 __device__ __forceinline__ void load_elem(const ProjArgs& p, int t, long long i, double& v,
                                           double& a, double& l, double& u) {
@@ -438,7 +452,7 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_apply_kernel(ProjArgs p) {
     if (xo) xo[i] = x;
     if (fo) fo[i] = fr ? 1 : 0;
     double r = v - x;
-    sv2 += v * v;
+    sv2 += p.base ? bregman_term(x, p.base[i], v, a, 0.5 * (lam + p.base_lam)) : v * v;
     sr2 += r * r;
     sxv += x * (2.0 * v - x);
     if (p.ref) { double dd = x - p.ref[i]; sd2 += dd * dd; }
@@ -455,7 +469,8 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_apply_kernel(ProjArgs p) {
   block_fold_partials<6>(p.part + (long long)t * gridDim.x * PSTRIDE, gridDim.x, PSTRIDE, ops, r,
                          red);
   if (threadIdx.x != 0) return;
-  st->sum_v2 = r[0];
+  st->sum_v2 = p.base ? 0.0 : r[0];
+  st->sum_bh = p.base ? r[0] : 0.0;
   st->sum_r2 = r[1];
   st->sum_dref2 = r[2];
   st->sum_a2_free = r[3];
@@ -604,7 +619,7 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_fused_kernel(ProjArgs p, double
       if (xo) xo[i] = x;
       if (fo) fo[i] = fr ? 1 : 0;
       const double r = v - x;
-      s6[0] += v * v;
+      s6[0] += p.base ? bregman_term(x, p.base[i], v, a, 0.5 * (lam + p.base_lam)) : v * v;
       s6[1] += r * r;
       if (p.ref) { const double dd = x - p.ref[i]; s6[2] += dd * dd; }
       if (fr) { s6[3] += a * a; s6[4] += 1.0; }
@@ -623,7 +638,8 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_fused_kernel(ProjArgs p, double
     const int ops6[6] = {0, 0, 0, 0, 0, 0};
     block_fold_partials<6>(part, nb, PSTRIDE, ops6, r, red);
     if (threadIdx.x != 0) return;
-    st->sum_v2 = r[0];
+    st->sum_v2 = p.base ? 0.0 : r[0];
+    st->sum_bh = p.base ? r[0] : 0.0;
     st->sum_r2 = r[1];
     st->sum_dref2 = r[2];
     st->sum_a2_free = r[3];
@@ -789,7 +805,8 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
       if (xo) xo[i] = x;
       if (fo) fo[i] = fr ? 1 : 0;
       const double r = v[k] - x;
-      s6[0] += v[k] * v[k];
+      s6[0] += p.base ? bregman_term(x, p.base[i], v[k], a[k], 0.5 * (lam + p.base_lam))
+                      : v[k] * v[k];
       s6[1] += r * r;
       if (p.ref) { const double dd = x - p.ref[i]; s6[2] += dd * dd; }
       if (fr) { s6[3] += a[k] * a[k]; s6[4] += 1.0; }
@@ -819,7 +836,8 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
         r[k] = gath[buf][0][k];
         for (int q = 1; q < CL_CTAS; ++q) r[k] += gath[buf][q][k];
       }
-      st->sum_v2 = r[0];
+      st->sum_v2 = p.base ? 0.0 : r[0];
+      st->sum_bh = p.base ? r[0] : 0.0;
       st->sum_r2 = r[1];
       st->sum_dref2 = r[2];
       st->sum_a2_free = r[3];
@@ -889,6 +907,7 @@ cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
   for (int t = 0; t < SSNAL_MAX_TRIALS; ++t) p.coef[t] = (L.coef && t < L.T) ? L.coef[t] : 0.0; p.a = L.a; p.l = L.l; p.u = L.u;
   p.lc = L.lc; p.uc = L.uc; p.d = L.d; p.n = L.n; p.st = L.st; p.part = L.part;
   p.x_out = L.x_out; p.free_out = L.free_out; p.ref = L.ref;
+  p.base = L.base; p.base_lam = L.base_lam;
   const int nblk = proj_blocks(L.n);
   if (L.newton > 0 && L.passes == 0 && L.phases == PHASE_APPLY && cluster_ok(L.n, L.T)) {
     note_launch();

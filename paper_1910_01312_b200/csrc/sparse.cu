@@ -12,6 +12,9 @@
 #include "common.cuh"
 #include "ssnal_internal.h"
 
+#include <algorithm>
+#include <cstdint>
+
 namespace ssnal {
 
 static constexpr int SUB = 8;  // lanes per row in X d
@@ -255,6 +258,197 @@ cudaError_t launch_gather(const int32_t* rows, long long p, const double* src, d
                           cudaStream_t stream) {
   note_launch();
   gather_kernel<<<(unsigned)ceil_div(p, 256LL), 256, 0, stream>>>(rows, p, src, dst);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- J-restricted CSC
+// X_J^T w for the matrix-free reduced Newton systems: the CSC entries of the free
+// rows J, built once per Newton step (one pass over the CSC) and reused by every CG
+// iteration of that step, so a product reads nnz(X_J) instead of nnz(X) and gathers
+// from the p-vector w (row slot = position in J) instead of a scattered n-vector.
+// Segments keep the operator's plan (same columns, same fold slots, entries in CSC
+// order), so the product stays deterministic.  Row signs are folded into the values.
+static constexpr int CJ_WARPS = 8;  // segments per block
+
+__device__ __forceinline__ long long block_exclusive_scan_ll(long long v, long long* sm,
+                                                             long long* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) sm[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    const long long x = lane < nw ? sm[lane] : 0;
+    long long xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += t;
+    }
+    if (lane < nw) sm[lane] = xi - x;
+    if (lane == nw - 1) sm[32] = xi;
+  }
+  __syncthreads();
+  const long long r = sm[warp] + incl - v;
+  *total = sm[32];
+  __syncthreads();
+  return r;
+}
+
+// pass 1: kept entries per segment (warp per segment) and per block; the last block
+// turns the block counts into exclusive offsets
+__global__ void __launch_bounds__(CJ_WARPS * 32) cscj_count_kernel(
+    const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ seg_end, long long nseg,
+    const int32_t* __restrict__ rowidx, const uint8_t* __restrict__ keep, int* __restrict__ cnt,
+    long long* __restrict__ blk, unsigned int* ticket, int nblk) {
+  __shared__ long long sm[33];
+  __shared__ int wc[CJ_WARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long s = (long long)blockIdx.x * CJ_WARPS + warp;
+  int c = 0;
+  if (s < nseg) {
+    for (long long k = seg_beg[s] + lane; k < seg_end[s]; k += 32) c += keep[rowidx[k]] ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[s] = c;
+  }
+  if (lane == 0) wc[warp] = s < nseg ? c : 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < CJ_WARPS; ++w) t += wc[w];
+    blk[blockIdx.x] = t;
+  }
+  if (!last_block_arrive(ticket, gridDim.x)) return;
+  long long carry = 0;
+  for (int start = 0; start < nblk; start += blockDim.x) {
+    const int idx = start + threadIdx.x;
+    const long long v = idx < nblk ? __ldcg(blk + idx) : 0;
+    long long tot;
+    const long long ex = block_exclusive_scan_ll(v, sm, &tot);
+    if (idx < nblk) blk[idx] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) blk[nblk] = carry;
+}
+
+// pass 2: compact the kept entries of each segment (ballot + popc keeps CSC order)
+__global__ void __launch_bounds__(CJ_WARPS * 32) cscj_fill_kernel(
+    const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ seg_end, long long nseg,
+    const int32_t* __restrict__ rowidx, const double* __restrict__ valt,
+    const double* __restrict__ rs, const uint8_t* __restrict__ keep,
+    const int32_t* __restrict__ posJ, const int* __restrict__ cnt,
+    const long long* __restrict__ blk, int64_t* __restrict__ jbeg, int64_t* __restrict__ jend,
+    int32_t* __restrict__ jpos, double* __restrict__ jval) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long s = (long long)blockIdx.x * CJ_WARPS + warp;
+  if (s >= nseg) return;
+  long long off = blk[blockIdx.x];
+  for (int w = 0; w < warp; ++w) off += cnt[(long long)blockIdx.x * CJ_WARPS + w];
+  if (lane == 0) {
+    jbeg[s] = off;
+    jend[s] = off + cnt[s];
+  }
+  const long long k1 = seg_end[s];
+  for (long long k0 = seg_beg[s]; k0 < k1; k0 += 32) {
+    const long long k = k0 + lane;
+    int r = 0;
+    bool kp = false;
+    if (k < k1) {
+      r = rowidx[k];
+      kp = keep[r] != 0;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, kp);
+    if (kp) {
+      const long long o = off + __popc(bal & ((1u << lane) - 1u));
+      jpos[o] = posJ[r];
+      jval[o] = rs ? valt[k] * rs[r] : valt[k];
+    }
+    off += __popc(bal);
+  }
+}
+
+// pos[J[r]] = r
+__global__ void index_map_kernel(const int32_t* __restrict__ J, long long p,
+                                 int32_t* __restrict__ pos) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < p) pos[J[r]] = (int32_t)r;
+}
+
+// out = X_J^T w on the J-restricted CSC (w indexed by position in J)
+__global__ void __launch_bounds__(256) cscj_xt_kernel(
+    const int64_t* __restrict__ jbeg, const int64_t* __restrict__ jend,
+    const int32_t* __restrict__ seg_col, const int32_t* __restrict__ seg_slot, long long nseg,
+    const int32_t* __restrict__ jpos, const double* __restrict__ jval,
+    const double* __restrict__ w, double* __restrict__ out, double* __restrict__ part) {
+  const long long s = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nseg) return;
+  const long long k0 = jbeg[s], k1 = jend[s];
+  double acc = 0.0;
+  for (long long k = k0 + lane; k < k1; k += 32) acc = fma(jval[k], __ldg(w + jpos[k]), acc);
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    const int slot = seg_slot[s];
+    if (slot < 0) out[seg_col[s]] = acc;
+    else part[slot] = acc;
+  }
+}
+
+size_t cscj_ws_bytes(const CsrOp& op) {
+  const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
+  return 256 + sizeof(int32_t) * (size_t)op.n + sizeof(int) * (size_t)op.nseg +
+         sizeof(long long) * (size_t)(nblk + 1) + 2 * sizeof(int64_t) * (size_t)op.nseg +
+         (sizeof(int32_t) + sizeof(double)) * (size_t)op.nnz + 8 * 256;
+}
+
+static char* al256(char* p) { return (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255); }
+
+CscJ cscj_layout(const CsrOp& op, void* ws) {
+  const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
+  CscJ c;
+  char* p = al256((char*)ws);
+  c.ticket = (unsigned int*)p; p = al256(p + 256);
+  c.posJ = (int32_t*)p; p = al256(p + sizeof(int32_t) * op.n);
+  c.cnt = (int*)p; p = al256(p + sizeof(int) * op.nseg);
+  c.blk = (long long*)p; p = al256(p + sizeof(long long) * (nblk + 1));
+  c.beg = (int64_t*)p; p = al256(p + sizeof(int64_t) * op.nseg);
+  c.end = (int64_t*)p; p = al256(p + sizeof(int64_t) * op.nseg);
+  c.pos = (int32_t*)p; p = al256(p + sizeof(int32_t) * op.nnz);
+  c.val = (double*)p;
+  return c;
+}
+
+cudaError_t launch_cscj_build(const CsrOp& op, const uint8_t* keep, const int32_t* J, long long p,
+                              const CscJ& c, cudaStream_t stream) {
+  const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
+  note_launch();
+  index_map_kernel<<<(unsigned)ceil_div(std::max(p, 1LL), 256LL), 256, 0, stream>>>(J, p, c.posJ);
+  note_launch();
+  cscj_count_kernel<<<(unsigned)nblk, CJ_WARPS * 32, 0, stream>>>(
+      op.seg_beg, op.seg_end, op.nseg, op.rowidx, keep, c.cnt, c.blk, c.ticket, (int)nblk);
+  note_launch();
+  cscj_fill_kernel<<<(unsigned)nblk, CJ_WARPS * 32, 0, stream>>>(
+      op.seg_beg, op.seg_end, op.nseg, op.rowidx, op.valt, op.row_sign, keep, c.posJ, c.cnt,
+      c.blk, c.beg, c.end, c.pos, c.val);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cscj_xt(const CsrOp& op, const CscJ& c, const double* w, double* out,
+                           double* part, cudaStream_t stream) {
+  note_launch();
+  cscj_xt_kernel<<<(unsigned)ceil_div(op.nseg * 32, 256LL), 256, 0, stream>>>(
+      c.beg, c.end, op.seg_col, op.seg_slot, op.nseg, c.pos, c.val, w, out, part);
+  if (op.nfold > 0) {
+    note_launch();
+    csc_fold_kernel<<<(unsigned)ceil_div(op.nfold, 256LL), 256, 0, stream>>>(
+        op.fold_col, op.fold_beg, op.nfold, part, out);
+  }
   return cudaGetLastError();
 }
 

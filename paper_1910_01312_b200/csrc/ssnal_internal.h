@@ -34,6 +34,23 @@ cudaError_t launch_scatter(const int32_t* rows, long long p, const double* src, 
 cudaError_t launch_gather(const int32_t* rows, long long p, const double* src, double* dst,
                           cudaStream_t stream);
 
+// J-restricted CSC of the free rows (sparse.cu): rebuilt per Newton step
+struct CscJ {
+  unsigned int* ticket;
+  int32_t* posJ;   // position in J of each kept row (n)
+  int* cnt;        // kept entries per segment
+  long long* blk;  // per-block offsets
+  int64_t *beg, *end;
+  int32_t* pos;    // row slot in J per kept entry
+  double* val;     // signed values
+};
+size_t cscj_ws_bytes(const CsrOp& op);
+CscJ cscj_layout(const CsrOp& op, void* ws);
+cudaError_t launch_cscj_build(const CsrOp& op, const uint8_t* keep, const int32_t* J, long long p,
+                              const CscJ& c, cudaStream_t stream);
+cudaError_t launch_cscj_xt(const CsrOp& op, const CscJ& c, const double* w, double* out,
+                           double* part, cudaStream_t stream);
+
 struct ProjLaunch {
   const double *A, *B, *coef, *a, *l, *u;
   double lc, uc, d;
@@ -44,6 +61,8 @@ struct ProjLaunch {
   double* x_out;
   unsigned char* free_out;
   const double* ref;
+  const double* base = nullptr;  // line-search base Pi: sum_bh instead of sum_v2
+  double base_lam = 0.0;
   int phases;
   int passes;
   double hint;  // warm-start multiplier for the Newton passes

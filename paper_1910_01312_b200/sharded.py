@@ -132,7 +132,8 @@ class ShardedBackend:
 
     # ---------------------------------------------------------------- projection
     def project(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
-                ref=None, phases=None, passes=None, hint=0.0, newton=None):
+                ref=None, phases=None, passes=None, hint=0.0, newton=None, base=None,
+                base_lam=0.0):
         """Global projection of T trial points v_t = A - coefs[t] B (rank slices);
         writes the T global state records, x_out / free_out rank-locally."""
         d = float(getattr(box, "d_global", box.d))
@@ -181,12 +182,14 @@ class ShardedBackend:
                     ln = 0.5 * (lo[t] + hi[t])
                 lam[t] = ln
         self.base.proj_local(A, box, T, lam, 1, self.rec, B=B, coefs=coefs, x_out=x_out,
-                             free_out=free_out, ref=ref)
+                             free_out=free_out, ref=ref, base=base, base_lam=base_lam)
         rec = self._fold(self.rec, T, 1)
         host = np.zeros(T, dtype=_lib.PROJ_STATE_DTYPE)
         for t in range(T):
             host[t]["lam"] = lam[t]
             host[t]["sum_v2"], host[t]["sum_r2"], host[t]["sum_dref2"] = rec[t, 0:3]
+            if base is not None:  # slot 0 carries the Bregman term (dist.cu)
+                host[t]["sum_bh"], host[t]["sum_v2"] = rec[t, 0], 0.0
             host[t]["sum_a2_free"] = rec[t, 3]
             host[t]["nfree"] = int(round(rec[t, 4]))
             host[t]["sum_xv"] = rec[t, 5]

@@ -209,9 +209,17 @@ class _Engine:
         st = self.be.read_states(self.h_st[:T]).copy() if states is not None else None
         return sc, st
 
+    def _trial_base(self, B):
+        """Line-search trials in the 'delta' psi mode carry the Bregman term against the
+        base projection Pi(u) = self.xp (csrc/proj.cu bregman_term)."""
+        if B is not None and getattr(self, "psi_delta", False):
+            return {"base": self.xp, "base_lam": self.lam_cur}
+        return {}
+
     def _project(self, A, states, T=1, B=None, coefs=None, x_out=None, free_out=None, ref=None,
                  hint=0.0):
-        self.be.project(A, self.box, states, T, B, coefs, x_out, free_out, ref, hint=hint)
+        self.be.project(A, self.box, states, T, B, coefs, x_out, free_out, ref, hint=hint,
+                        **self._trial_base(B))
         self.counters["projections"] += 1
         self.counters["proj_trials"] += T
 
@@ -225,7 +233,8 @@ class _Engine:
             if rounds > 20:
                 raise InternalError("projection failed to bracket the multiplier")
             self.be.project(A, self.box, states, T, B, coefs, x_out, free_out, ref,
-                            phases=_lib.PHASE_EXACT | _lib.PHASE_APPLY, passes=8, newton=0)
+                            phases=_lib.PHASE_EXACT | _lib.PHASE_APPLY, passes=8, newton=0,
+                            **self._trial_base(B))
             _, st = self.fetch(states, T)
         for s in st["status"]:
             raise_on_status(int(s))
@@ -388,9 +397,16 @@ class _Engine:
                                          coefs=coefs, x_out=self.tx, free_out=self.tfree,
                                          ref=self.x)
             for j, a in enumerate(alphas):
-                quad = wqw + 2.0 * a * wqdir + a * a * dqd
-                psi_t = _psi(quad, st[j], x_sq, sigma, opts.psi_eval)
-                if psi_t <= psi0 + opts.mu * a * gd:
+                if opts.psi_eval == "delta":
+                    # psi(w + a d) - psi(w) = a g'd + a^2 d'Qd / 2 + B_h / sigma
+                    dpsi = a * gd + 0.5 * a * a * dqd + float(st[j]["sum_bh"]) / sigma
+                    psi_t = psi0 + dpsi
+                    ok = dpsi <= opts.mu * a * gd
+                else:
+                    quad = wqw + 2.0 * a * wqdir + a * a * dqd
+                    psi_t = _psi(quad, st[j], x_sq, sigma, opts.psi_eval)
+                    ok = psi_t <= psi0 + opts.mu * a * gd
+                if ok:
                     self.lam_cur = float(st["lam"][j])
                     return a, j, st[j], psi_t
             tried += T
@@ -437,6 +453,8 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
     eng._direct_limit = ssn_opts.direct_solve_threshold
     eng.line_search_batch = ssn_opts.line_search_batch
     eng.backtrack = ssn_opts.backtrack
+    delta = ssn_opts.psi_eval == "delta"
+    eng.psi_delta = delta
     sigma = state.sigma
     coeff = math.sqrt(alm_opts.lambda_min_surrogate / sigma)
     grad_floor = 1e-12 * (1.0 + eng.c_norm)
@@ -472,7 +490,9 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
             steepest = True
             first = None
         psi0 = _psi(wqw, cur, x_sq, sigma, ssn_opts.psi_eval)
-        if ssn_opts.mu * abs(gd) <= 1e-16 * (1.0 + abs(psi0)):
+        # predicted decrease below the resolution of psi (ref solver.py:369-371); the
+        # 'delta' mode forms psi differences directly and has no such floor
+        if not delta and ssn_opts.mu * abs(gd) <= 1e-16 * (1.0 + abs(psi0)):
             converged, exhausted = True, False
             break
         try:
@@ -484,7 +504,7 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
                 break
             sc = eng.steepest()
             gd, wqw, wqdir, dqd = (float(v) for v in sc[:4])
-            if ssn_opts.mu * (-gd) <= 1e-16 * (1.0 + abs(psi0)):
+            if not delta and ssn_opts.mu * (-gd) <= 1e-16 * (1.0 + abs(psi0)):
                 exhausted = False
                 break
             try:
@@ -524,6 +544,9 @@ def _native_ok(problem, alm_opts, ssn_opts):
             and alm_opts.eps_seq is _half_powers and alm_opts.delta_seq is _half_powers)
 
 
+_PSI_MODES = {"reference": 0, "stable": 1, "delta": 2}
+
+
 def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_device):
     """The same loop through the C++ driver (csrc/driver.cu): one C-ABI call."""
     import ctypes
@@ -553,7 +576,7 @@ def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_devi
         tau=ssn_opts.tau, eta=ssn_opts.eta, max_inner=ssn_opts.max_inner,
         direct_solve_threshold=ssn_opts.direct_solve_threshold,
         cg_max_iters=ssn_opts.cg_max_iters, line_search_batch=ssn_opts.line_search_batch,
-        psi_stable=int(ssn_opts.psi_eval != "reference"), profile=int(bool(ssn_opts.profile)))
+        psi_stable=_PSI_MODES[ssn_opts.psi_eval], profile=int(bool(ssn_opts.profile)))
     x0d = None if x0 is None else as_device(x0, be)
     w0d = None if w0 is None else as_device(w0, be)
     if x0d is not None:

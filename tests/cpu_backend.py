@@ -15,6 +15,15 @@ from paper_1910_01312_b200 import _lib
 F64 = torch.float64
 
 
+
+def _bregman(x, base, v, a, lam, base_lam):
+    """sum (x - Pi_b)(v - (x + Pi_b)/2 - lam_bar a): the trial's Bregman term
+    (csrc/proj.cu bregman_term); 0 without a base point."""
+    if base is None:
+        return 0.0
+    xb = base.numpy()
+    return float(((x - xb) * (v - 0.5 * (x + xb) - 0.5 * (lam + base_lam) * a)).sum())
+
 class CpuTestBackend:
     name = "cpu-test"
 
@@ -54,7 +63,7 @@ class CpuTestBackend:
 
     # projection --------------------------------------------------------------
     def project(self, A, box, states, T=1, B=None, coefs=None, x_out=None, free_out=None,
-                ref=None, phases=7, passes=6, hint=0.0, newton=3):
+                ref=None, phases=7, passes=6, hint=0.0, newton=3, base=None, base_lam=0.0):
         self._count("project")
         a = box.a_dev.numpy()
         l = box.l.numpy()
@@ -68,7 +77,8 @@ class CpuTestBackend:
             x, lam, free = O.project(v, bl)
             r = v - x
             rec[t]["lam"] = lam
-            rec[t]["sum_v2"] = float(v @ v)
+            rec[t]["sum_v2"] = 0.0 if base is not None else float(v @ v)
+            rec[t]["sum_bh"] = _bregman(x, base, v, a, lam, base_lam)
             rec[t]["sum_r2"] = float(r @ r)
             rec[t]["sum_xv"] = float(x @ (2.0 * v - x))
             rec[t]["sum_dref2"] = float(((x - ref.numpy()) ** 2).sum()) if ref is not None else 0.0
@@ -211,7 +221,7 @@ class CpuTestBackend:
 
     # sharded path --------------------------------------------------------------
     def proj_local(self, A, box, T, lam, mode, rec, B=None, coefs=None, x_out=None,
-                   free_out=None, ref=None):
+                   free_out=None, ref=None, base=None, base_lam=0.0):
         self._count("proj_local")
         a = box.a_dev.numpy()
         l = box.l.numpy()
@@ -241,7 +251,8 @@ class CpuTestBackend:
                 upper = ~lower & (y >= u - 1e-12 * (1.0 + np.abs(u)))
                 free = ~(lower | upper)
                 res = v - x
-                r[t, 0] = float(v @ v)
+                r[t, 0] = (float(v @ v) if base is None
+                           else _bregman(x, base, v, a, lam[t], base_lam))
                 r[t, 1] = float(res @ res)
                 r[t, 2] = float(((x - ref.numpy()) ** 2).sum()) if ref is not None else 0.0
                 r[t, 3] = float((a[free] ** 2).sum())
