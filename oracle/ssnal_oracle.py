@@ -26,7 +26,7 @@ __all__ = [
     "grad_phi", "breakpoints", "classify_free", "project", "hs_apply",
     "DenseQ", "FactoredQ", "SvrFactoredQ",
     "AlmOpts", "SsnOpts", "psi_value", "newton_direction", "line_search",
-    "ssn_solve", "kkt_residual", "alm_solve", "set_psi_mode", "PSI_MODE",
+    "ssn_solve", "kkt_residual", "alm_solve", "set_psi_mode", "PSI_MODE", "bregman",
     "csvc_problem", "svr_problem", "objective",
 ]
 

@@ -70,7 +70,10 @@ class SsnOptions:
     direct_solve_threshold: int = 2000
     cg_max_iters: int = 500
     line_search_batch: int = 8
-    psi_eval: str = "stable"  # or "reference": ref solver.py:130-133 term for term
+    # "delta": Armijo on psi differences (Bregman term fused into the trial projections,
+    # no psi-resolution stop); "stable": psi via sum Pi(2u - Pi);
+    # "reference": ref solver.py:130-133 term for term
+    psi_eval: str = "delta"
     engine: str = "native"    # "native": C++ driver (ssnal_alm_solve_dense); "python": _Engine
     profile: bool = False     # native: CUDA-event time per op class -> problem.op_profile
 

@@ -33,7 +33,7 @@ def _problem(P, c):
 
 
 @pytest.mark.parametrize("engine", ["native", "python"])
-@pytest.mark.parametrize("psi_eval", ["reference", "stable"])
+@pytest.mark.parametrize("psi_eval", ["reference", "stable", "delta"])
 def test_alm_solve_golden(pkg, psi_eval, engine):
     for c in load_cases("solve.npz", "s"):
         rep = pkg.alm_solve(_problem(pkg, c), pkg.AlmOptions(tol_kkt=c["tol"]),
@@ -167,3 +167,57 @@ def test_sparse_csvc_vs_oracle_and_dense(pkg, n, q, density, C, route):
     assert rep.objective == pytest.approx(ref["objective"], rel=1e-6)
     assert rep.objective == pytest.approx(dense.objective, rel=1e-6)
     assert abs(float(y @ rep.x_opt)) <= 1e-9 * (1 + np.abs(rep.x_opt).sum())
+
+
+def _oracle_solve(mode, op, c, bl, **ssn):
+    O.set_psi_mode(mode)
+    try:
+        return O.alm_solve(op, c, bl, O.AlmOpts(tol_kkt=1e-6), O.SsnOpts(**ssn))
+    finally:
+        O.set_psi_mode("reference")
+
+
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("route", ["direct", "cg"])
+def test_sparse_config_shapes_vs_oracle(pkg, k, route):
+    """BASELINE configs 2 (uniform columns, C = 1) and 3 (Zipf columns, C = 0.1) from
+    the same generators at n = 5000, q = 1000: the delta line search with
+    max_inner = 200 (the options the full-size runs use) reaches R_KKT <= 1e-6 on both
+    Newton-system routes, and the objective matches the oracle (same algorithm, delta
+    mode) to 1e-6.  route "cg" (threshold 16) runs the matrix-free CG on the
+    J-restricted CSC (sample space for config 2, Jacobi factor space for Zipf data)."""
+    import scipy.sparse as sp
+
+    from paper_1910_01312_b200 import datagen
+
+    cfg = datagen.make_config(k, n=5000, q=1000)
+    A = sp.csr_matrix((cfg["data"], cfg["indices"], cfg["indptr"]), shape=cfg["shape"])
+    ssn = pkg.SsnOptions(psi_eval="delta", max_inner=200,
+                         direct_solve_threshold=2000 if route == "direct" else 16)
+    pb = pkg.build_csvc_dual((cfg["indptr"], cfg["indices"], cfg["data"], cfg["shape"]), cfg["y"],
+                             cfg["C"])
+    rep = pkg.alm_solve(pb, pkg.AlmOptions(tol_kkt=1e-6), ssn)
+    assert rep.converged and rep.kkt_residual <= 1e-6, (rep.kkt_residual, rep.warnings)
+    if route == "cg":
+        assert pb.native_counters["cg_iters"] > 0
+    op, c, bl = O.csvc_problem(A.toarray(), cfg["y"], cfg["C"])
+    ref = _oracle_solve("delta", op, c, bl, max_inner=200)
+    assert ref["converged"]
+    assert rep.objective == pytest.approx(ref["objective"], rel=1e-6)
+    assert abs(float(cfg["y"] @ rep.x_opt)) <= 1e-9 * (1 + np.abs(rep.x_opt).sum())
+    assert rep.x_opt.min() >= 0.0 and rep.x_opt.max() <= cfg["C"]
+
+
+def test_delta_line_search_matches_stable_on_config1_shape(pkg):
+    """On a well-conditioned dense problem the delta Armijo test accepts the same
+    steps as the stable psi evaluation: same counts, objective to 1e-10."""
+    from paper_1910_01312_b200 import datagen
+
+    cfg = datagen.config1(seed=5, n=20000, q=200)
+    pb = pkg.build_csvc_dual(cfg["A"], cfg["y"], cfg["C"])
+    reps = {m: pkg.alm_solve(pb, pkg.AlmOptions(tol_kkt=1e-6), pkg.SsnOptions(psi_eval=m))
+            for m in ("stable", "delta")}
+    a, b = reps["stable"], reps["delta"]
+    assert a.converged and b.converged
+    assert (a.outer_iters, a.total_inner_iters) == (b.outer_iters, b.total_inner_iters)
+    assert b.objective == pytest.approx(a.objective, rel=1e-10)

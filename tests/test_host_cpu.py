@@ -28,11 +28,13 @@ def _problem(mods, c, be):
     return svm.build_svr_dual(c["A"], c["t"], c["C"], c["eps"], backend=be)
 
 
-def test_alm_solve_host_logic_matches_reference(mods):
+@pytest.mark.parametrize("psi_eval", ["stable", "delta"])
+def test_alm_solve_host_logic_matches_reference(mods, psi_eval):
     solver = mods[2]
     be = CpuTestBackend()
     for c in load_cases("solve.npz", "s"):
-        rep = solver.alm_solve(_problem(mods, c, be), solver.AlmOptions(tol_kkt=c["tol"]))
+        rep = solver.alm_solve(_problem(mods, c, be), solver.AlmOptions(tol_kkt=c["tol"]),
+                               solver.SsnOptions(psi_eval=psi_eval))
         assert rep.objective == pytest.approx(c["obj"], rel=1e-6, abs=1e-9)
         if c["kind"] != "dense":
             assert rep.converged and rep.kkt_residual < c["tol"]

@@ -73,3 +73,51 @@ def test_alm_solve_matches_reference():
             assert (rep["outer_iters"], rep["total_inner_iters"]) == (c["outer"], c["inner"])
         x_ref = c["x_opt"]
         assert np.linalg.norm(rep["x_opt"] - x_ref) <= 1e-4 * (1 + np.linalg.norm(x_ref))
+
+
+def test_alm_solve_delta_mode_matches_reference_counts():
+    """The delta line search (Armijo on psi differences) takes the
+    reference's steps on every golden SVM case: same outer/inner counts and solution."""
+    O.set_psi_mode("delta")
+    try:
+        for c in load_cases("solve.npz", "s"):
+            if c["kind"] == "dense":
+                continue
+            op, cc, bl = _problem(c)
+            rep = O.alm_solve(op, cc, bl, O.AlmOpts(tol_kkt=c["tol"]))
+            assert rep["converged"] and rep["kkt_residual"] < c["tol"]
+            assert (rep["outer_iters"], rep["total_inner_iters"]) == (c["outer"], c["inner"])
+            assert rep["objective"] == pytest.approx(c["obj"], rel=1e-6, abs=1e-9)
+    finally:
+        O.set_psi_mode("reference")
+
+
+def test_bregman_term_is_the_psi_difference():
+    """psi(w + a d) - psi(w) = a g'd + a^2 d'Qd / 2 + B_h / sigma exactly (up to
+    rounding) for random dense data: the identity the delta mode rests on."""
+    rng = np.random.default_rng(7)
+    n, q = 300, 20
+    A = rng.standard_normal((n, q))
+    y = np.where(rng.standard_normal(n) > 0, 1.0, -1.0)
+    op, c, bl = O.csvc_problem(A, y, 1.0)
+    x = np.clip(rng.random(n), 0, 1.0)
+    w = rng.standard_normal(n) * 0.1
+    d = rng.standard_normal(n) * 0.1
+    sigma = 3.0
+    qw, qd = op.matvec(w), op.matvec(d)
+    u = x - sigma * (qw + c)
+    px, lam, _ = O.project(u, bl)
+    O.set_psi_mode("stable")
+    try:
+        psi0 = O.psi_value(float(w @ qw), u, px, float(x @ x), sigma)
+        gd = float((w - px) @ qd)
+        for alpha in (1.0, 0.5, 1e-3):
+            ut = u - sigma * alpha * qd
+            pt, lt, _ = O.project(ut, bl)
+            wt = w + alpha * d
+            psi_t = O.psi_value(float(wt @ op.matvec(wt)), ut, pt, float(x @ x), sigma)
+            dpsi = alpha * gd + 0.5 * alpha ** 2 * float(d @ qd) + O.bregman(pt, lt, px, lam, ut,
+                                                                              bl.a) / sigma
+            assert dpsi == pytest.approx(psi_t - psi0, rel=1e-9, abs=1e-12)
+    finally:
+        O.set_psi_mode("reference")
