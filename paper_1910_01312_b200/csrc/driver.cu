@@ -501,6 +501,11 @@ struct Driver {
   // rare: a trial needed more bracketing than the default launch
   bool finish(ProjState* st_dev, int T, const double* A, const double* B, const double* coefs,
               double* xo, uint8_t* fo, const double* ref) {
+    static const bool dbg_proj = std::getenv("SSNAL_DEBUG_PROJ") != nullptr;
+    if (dbg_proj)
+      for (int t = 0; t < T; ++t)
+        std::fprintf(stderr, "proj T=%d t=%d passes=%d status=%d nfree=%lld lam=%.6g\n", T, t,
+                     H->st[t].passes, H->st[t].status, (long long)H->st[t].nfree, H->st[t].lam);
     bool extra = false;
     for (int round = 0;; ++round) {
       bool pending = false;
