@@ -168,7 +168,8 @@ cudaError_t launch_stream_xd(const double* A, long long n, long long q, long lon
                              const double* rs, int svr, int k, const double* d, double* out,
                              long long nlog, cudaStream_t stream, double* sq_part = nullptr,
                              double* sq_out = nullptr, unsigned int* sq_ticket = nullptr,
-                             int epi = 0, const uint8_t* fm = nullptr, const double* av = nullptr);
+                             int epi = 0, const uint8_t* fm = nullptr, const double* av = nullptr,
+                             double* sq_out2 = nullptr);
 cudaError_t launch_hs_finish_dots(const uint8_t* fm, const double* a, const double* y, long long n,
                                   double beta, const double* add, double alpha, double* out,
                                   const double* ay, const double* aa, const double* g,
@@ -193,7 +194,7 @@ static size_t grad_red_bytes(long long n_phys) {
   return (reduce_ws_bytes(2 * n_phys) + 255) / 256 * 256;
 }
 size_t gradient_ws_bytes(long long n_phys, long long q) {
-  return 256 + grad_red_bytes(n_phys) + (size_t)(stream_grid(n_phys) + 32) * sizeof(double) +
+  return 256 + grad_red_bytes(n_phys) + (size_t)(2 * stream_grid(n_phys) + 32) * sizeof(double) +
          dense_xt_ws_bytes(n_phys, q, 1);
 }
 
@@ -611,7 +612,7 @@ cudaError_t launch_dense_gradient(const double* A, long long n, long long q, lon
   unsigned int* ticket = (unsigned int*)base;
   void* red_ws = (void*)(base + 256);
   double* sq_part = (double*)(base + 256 + grad_red_bytes(n));
-  double* part = sq_part + stream_grid(n) + 32;
+  double* part = sq_part + 2 * stream_grid(n) + 32;
   if (stream_ok(A, lda, q) && q <= 512) {
     const double* vs[1] = {w};
     cudaError_t e = launch_stream_xt(A, n, q, lda, rs, svr, 1, vs, 0, 1, part, stream, xp, s_out);
@@ -661,6 +662,88 @@ cudaError_t launch_direction_epilogue(const double* A, long long n, long long q,
   }
   return launch_hs_finish_dots(fm, a, qdir, nlog, -sigma, s, -1.0, dir, ad, asa_dev, grad, w, qw,
                                t, q, dots4, red_ws, stream);
+}
+
+// Start of an inner solve in factor space: s = w - Pi(u) staged in one X^T sweep,
+// r = X^T s (the gradient's factor; grad = X r is formed later by the direction
+// epilogue).
+cudaError_t launch_gradient_factor(const double* A, long long n, long long q, long long lda,
+                                   const double* rs, int svr, const double* w, const double* xp,
+                                   double* s_out, double* r, void* ws, cudaStream_t stream) {
+  const long long nlog = svr ? 2 * n : n;
+  char* base = (char*)ws;
+  double* sq_part = (double*)(base + 256 + grad_red_bytes(n));
+  double* part = sq_part + 2 * stream_grid(n) + 32;
+  if (stream_ok(A, lda, q) && q <= 512) {
+    const double* vs[1] = {w};
+    cudaError_t e = launch_stream_xt(A, n, q, lda, rs, svr, 1, vs, 0, 1, part, stream, xp, s_out);
+    if (e != cudaSuccess) return e;
+    note_launch();
+    dense_xt_fold_kernel<<<(unsigned)ceil_div(q * 32, 256LL), 256, 0, stream>>>(
+        part, stream_grid(n), 1, q, r);
+    return cudaGetLastError();
+  }
+  cudaError_t e = launch_vec(3, nlog, 0.0, w, xp, nullptr, s_out, stream);
+  if (e != cudaSuccess) return e;
+  const double* vs[1] = {s_out};
+  return launch_dense_xt(A, n, q, lda, rs, svr, 1, vs, r, part, stream);
+}
+
+// grad = X r with ||grad||^2 folded into *g2 (one sweep; the Sigma = 0 steps)
+cudaError_t launch_grad_from_factor(const double* A, long long n, long long q, long long lda,
+                                    const double* rs, int svr, const double* r, double* grad,
+                                    double* g2, void* ws, cudaStream_t stream) {
+  const long long nlog = svr ? 2 * n : n;
+  char* base = (char*)ws;
+  unsigned int* ticket = (unsigned int*)base;
+  void* red_ws = (void*)(base + 256);
+  double* sq_part = (double*)(base + 256 + grad_red_bytes(n));
+  if (stream_ok(A, lda, q) && q <= 512)
+    return launch_stream_xd(A, n, q, lda, rs, svr, 1, r, grad, nlog, stream, sq_part, g2, ticket);
+  cudaError_t e = launch_dense_x(A, n, q, lda, rs, svr, 1, r, grad, stream);
+  if (e != cudaSuccess) return e;
+  const double* xs[1] = {grad};
+  const double* ys[1] = {nullptr};
+  return launch_dots(1, xs, ys, nullptr, nlog, g2, red_ws, stream);
+}
+
+// Factor-space Newton epilogue: ONE sweep X [t, r] gives Qd and the gradient
+// grad = X r of the current point (a_J'(Qd)_J and ||grad||^2 folded in the sweep), then
+// d = -s - sigma P_J(Qd) and {g'd, w'Qw, w'Qd, t't} as launch_direction_epilogue.
+// t2 = [t ; r] (2q), qg = [Qd ; grad] (2 nlog).
+cudaError_t launch_direction_epilogue_q(const double* A, long long n, long long q, long long lda,
+                                        const double* rs, int svr, const double* t2, double* qg,
+                                        const uint8_t* fm, const double* a,
+                                        const double* asa_dev, const double* s, double sigma,
+                                        const double* w, const double* qw, double* dir,
+                                        double* dots4, double* g2, void* ws,
+                                        cudaStream_t stream) {
+  const long long nlog = svr ? 2 * n : n;
+  char* base = (char*)ws;
+  unsigned int* ticket = (unsigned int*)base;
+  void* red_ws = (void*)(base + 256);
+  double* ad = (double*)(base + 128);
+  double* sq_part = (double*)(base + 256 + grad_red_bytes(n));
+  double* qdir = qg;
+  double* grad = qg + nlog;
+  if (stream_ok(A, lda, q) && q <= 512) {
+    cudaError_t e = launch_stream_xd(A, n, q, lda, rs, svr, 2, t2, qg, nlog, stream, sq_part, ad,
+                                     ticket, 3, fm, a, g2);
+    if (e != cudaSuccess) return e;
+  } else {
+    cudaError_t e = launch_dense_x(A, n, q, lda, rs, svr, 2, t2, qg, stream);
+    if (e != cudaSuccess) return e;
+    const double* xs[1] = {a};
+    const double* ys[1] = {qdir};
+    e = launch_dots(1, xs, ys, fm, nlog, ad, red_ws, stream);
+    if (e != cudaSuccess) return e;
+    const double* gx[1] = {grad};
+    const double* gy[1] = {nullptr};
+    e = launch_dots(1, gx, gy, nullptr, nlog, g2, red_ws, stream);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_hs_finish_dots(fm, a, qdir, nlog, -sigma, s, -1.0, dir, ad, asa_dev, grad, w, qw,
+                               t2, q, dots4, red_ws, stream);
 }
 
 size_t direction_ws_bytes(long long n_phys, long long q) { return gradient_ws_bytes(n_phys, q); }

@@ -101,6 +101,29 @@ cudaError_t launch_pspace_solve(const int32_t* J, long long p, const double* gra
                                 double sigma, double asa, double* Q, double* vecs, double* y,
                                 int* info, cudaStream_t s);
 
+cudaError_t launch_gradient_factor(const double* A, long long n, long long q, long long lda,
+                                   const double* rs, int svr, const double* w, const double* xp,
+                                   double* s_out, double* r, void* ws, cudaStream_t stream);
+cudaError_t launch_direction_epilogue_q(const double* A, long long n, long long q, long long lda,
+                                        const double* rs, int svr, const double* t2, double* qg,
+                                        const uint8_t* fm, const double* a,
+                                        const double* asa_dev, const double* s, double sigma,
+                                        const double* w, const double* qw, double* dir,
+                                        double* dots4, double* g2, void* ws, cudaStream_t stream);
+cudaError_t launch_grad_from_factor(const double* A, long long n, long long q, long long lda,
+                                    const double* rs, int svr, const double* r, double* grad,
+                                    double* g2, void* ws, cudaStream_t stream);
+cudaError_t launch_rows_grad(const double* A, long long n, long long q, long long lda,
+                             const double* rs, int svr, const int32_t* J, long long p,
+                             const double* r, double* grad, cudaStream_t stream);
+size_t accept_q_ws_bytes(long long n, long long q);
+cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long long lda,
+                            const double* rs, int svr, long long n, double alpha, double cu,
+                            double* w, const double* d, double* qw, const double* qd, double* u,
+                            double* xp, const double* txj, uint8_t* fr, const uint8_t* tfj,
+                            double* s, const double* t, double* xw, double* xpi, double* r,
+                            double* part, cudaStream_t stream);
+
 // direct reduced systems of the sparse operator: min(p, q) up to this size (M buffer)
 constexpr long long SPARSE_DIRECT_MAX = 2048;
 // forcing-term cap of the matrix-free CG route (see cg_direction)
@@ -151,6 +174,9 @@ Pinned* pinned_buffer() {
 struct Layout {
   double *x, *w, *qw, *u, *xp, *s, *grad, *qdir, *dir, *tmp, *qx, *qwx, *best_x, *tx;
   double *gr, *t, *M, *m1, *scal;
+  // dense operator, factor-space gradient: r = t + q (t2 = [t ; r]), X^T w, X^T Pi(u),
+  // accept partials; qdir and grad are adjacent ([Qd ; grad] from one X sweep)
+  double *r, *xw, *xpi, *qpart;
   uint8_t *fr, *tfree;
   int32_t* J;
   long long* pcount;
@@ -176,8 +202,7 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
   L.u = cv.take<double>(n);
   L.xp = cv.take<double>(n);
   L.s = cv.take<double>(n);
-  L.grad = cv.take<double>(n);
-  L.qdir = cv.take<double>(n);
+  L.qdir = cv.take<double>(2 * (size_t)n);
   L.dir = cv.take<double>(n);
   L.tmp = cv.take<double>(n);
   L.qx = cv.take<double>(n);
@@ -185,7 +210,12 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
   L.best_x = cv.take<double>(n);
   L.tx = cv.take<double>((size_t)TMAX * n);
   L.gr = cv.take<double>(2 * q);
-  L.t = cv.take<double>(q);
+  L.grad = L.qdir ? L.qdir + n : nullptr;
+  L.t = cv.take<double>(2 * (size_t)q);
+  L.r = L.t ? L.t + q : nullptr;
+  L.xw = cv.take<double>(q);
+  L.xpi = cv.take<double>(q);
+  L.qpart = sparse ? nullptr : cv.take<double>(accept_q_ws_bytes(n, q) / sizeof(double) + 1);
   L.M = sparse ? nullptr : cv.take<double>((size_t)q * q);
   L.m1 = cv.take<double>(q);
   L.scal = cv.take<double>(NSCAL);
@@ -614,8 +644,25 @@ struct Driver {
     if (g2) dots({{L.grad, nullptr}}, g2, P.n);
   }
 
+  // start of an inner solve (dense): s = w - Pi(u), r = X^T s (one sweep), X^T Pi = X^T w - r
+  void start_factor() {
+    timed(SSNAL_OP_XT, a_bytes() + 8.0 * (3 * P.n + P.q), [&] {
+      ck(launch_gradient_factor(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.w, L.xp,
+                                L.s, L.r, L.ws_grad, S));
+    });
+    ck(launch_vec(3, P.q, 0.0, L.xw, L.r, nullptr, L.xpi, S));
+  }
+
   void direction(long long p, double asa, const double* g2_dev) {
+    tdir = L.t;
     if (p == 0) {  // Sigma = 0: d = -s, Qd = -grad (ref solver.py:221-222)
+      if (qgrad()) {  // grad = X r (one sweep, ||grad||^2 folded); t = X^T d = -r
+        timed(SSNAL_OP_XD, a_bytes() + 8.0 * (P.n + P.q), [&] {
+          ck(launch_grad_from_factor(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.r,
+                                     L.grad, L.scal + 4, L.ws_grad, S));
+        });
+        ck(launch_vec(4, P.q, -1.0, L.r, nullptr, nullptr, L.t, S));
+      }
       vec(4, -1.0, L.s, nullptr, nullptr, L.dir);
       vec(4, -1.0, L.grad, nullptr, nullptr, L.qdir);
       dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}, {L.s, L.grad}}, L.scal, P.n);
@@ -650,16 +697,31 @@ struct Driver {
     const double m = (double)std::min<long long>(p, P.q);
     timed(SSNAL_OP_NEWTON, 8.0 * p * P.q + 16.0 * m * m, [&] {
       ck(launch_compact(L.fr, P.n, L.J, L.pcount, L.ws_cmp, S));
+      const double* g_r = qgrad() ? L.r : L.gr;
       if (p < P.q) {
+        // factor-space gradient: the right-hand side needs grad_J = X_J r only
+        if (qgrad())
+          ck(launch_rows_grad(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, p, L.r,
+                              L.grad, S));
         ck(launch_pspace_direction(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, p,
-                                   L.grad, P.a, sigma, asa, L.gr, L.t, L.info, L.ws_ps, S));
+                                   L.grad, P.a, sigma, asa, g_r, L.t, L.info, L.ws_ps, S));
       } else {
         const double* asa_dev = &L.st_cur->sum_a2_free;
         ck(launch_dense_gram(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, L.pcount,
                              P.n, P.a, sigma, asa_dev, L.M, L.m1, L.ws_gram, S));
-        ck(launch_chol_solve(L.M, P.q, L.gr, -1.0, L.t, L.info, S));
+        ck(launch_chol_solve(L.M, P.q, g_r, -1.0, L.t, L.info, S));
       }
     });
+    if (qgrad()) {
+      // ONE sweep X [t, r]: Qd and this point's gradient (a_J'(Qd)_J and ||grad||^2
+      // folded), then d = -s - sigma P(Qd) and {g'd, w'Qw, w'Qd, t't}
+      timed(SSNAL_OP_XD, a_bytes() + 8.0 * (2 * P.n + 2 * P.q) + 8.0 * P.n * 8, [&] {
+        ck(launch_direction_epilogue_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.t,
+                                       L.qdir, L.fr, P.a, &L.st_cur->sum_a2_free, L.s, sigma,
+                                       L.w, L.qw, L.dir, L.scal, L.scal + 4, L.ws_grad, S));
+      });
+      return;
+    }
     // Qd = X t (a_J'(Qd)_J folded in the sweep), d = -s - sigma P(Qd), and
     // {g'd, w'Qw, w'Qd, t't}: two launches
     timed(SSNAL_OP_XD, a_bytes() + 8.0 * (P.n + P.q) + 8.0 * P.n * 8, [&] {
@@ -669,8 +731,13 @@ struct Driver {
     });
   }
 
+  // dense operator: the SsN gradient is kept in factor space
+  bool qgrad() const { return P.csr == nullptr; }
+  const double* tdir = nullptr;  // X^T d of the current direction (factor-space update)
+
   void steepest(double out[4]) {
     vec(4, -1.0, L.grad, nullptr, nullptr, L.dir);
+    tdir = L.gr + P.q;
     xt({L.dir}, L.gr + P.q);
     xd(L.gr + P.q, L.qdir, 1);
     dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}, {L.dir, L.qdir}}, L.scal, P.n);
@@ -681,7 +748,9 @@ struct Driver {
   // [gradient, ||grad||^2] + direction + unit trial, one sync
   void advance(long long p, double asa, bool with_gradient, double& gnorm2, double dotsv[4],
                ProjState& trial0) {
-    if (with_gradient) gradient(L.scal + 4);
+    // dense: the accept pass already produced r = X^T s; grad = X r comes with the
+    // direction's sweep
+    if (with_gradient && !qgrad()) gradient(L.scal + 4);
     // ||grad||^2 of this point on the device: scal[4] after a gradient, scal[0] at the start
     direction(p, asa, with_gradient ? L.scal + 4 : L.scal + 0);
     // the first Armijo batch (alpha = 1, beta, ..., beta^(T0-1)) is projected
@@ -751,6 +820,17 @@ struct Driver {
   }
 
   void accept(double alpha, int j) {
+    if (qgrad()) {  // + s, and X^T w, X^T Pi(u), r = X^T s updated from the changed slots
+      timed(SSNAL_OP_VEC, 8.0 * P.n * 9 + 2.0 * P.n, [&] {
+        ck(launch_accept_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, P.n, alpha,
+                           -(sigma * alpha), L.w, L.dir, L.qw, L.qdir, L.u, L.xp,
+                           L.tx + (size_t)j * P.n, L.fr, L.tfree + (size_t)j * P.n, L.s, tdir,
+                           L.xw, L.xpi, L.r, L.qpart, S));
+      });
+      ck(cudaMemcpyAsync(L.st_cur, L.st_trial + j, sizeof(ProjState), cudaMemcpyDeviceToDevice,
+                         S));
+      return;
+    }
     timed(SSNAL_OP_VEC, 8.0 * P.n * 8 + 2.0 * P.n, [&] {
       ck(launch_accept(P.n, alpha, -(sigma * alpha), L.w, L.dir, L.qw, L.qdir, L.u, L.xp,
                        L.tx + (size_t)j * P.n, L.fr, L.tfree + (size_t)j * P.n, S));
@@ -767,15 +847,27 @@ struct Driver {
     // start: u = x - sigma (Qw + c), Pi(u), s, grad
     vec(0, -sigma, L.x, L.qw, P.c, L.u);
     project(L.u, L.st_cur, 1, nullptr, nullptr, L.xp, L.fr, L.x, lam_cur);
-    gradient();
-    dots({{L.grad, nullptr}, {L.x, nullptr}}, L.scal, P.n);
+    if (qgrad()) {
+      // X^T w from the outer refresh (kkt_and_refresh), r = X^T s in one sweep,
+      // X^T Pi = X^T w - r; the gradient norm comes with the first direction
+      ck(cudaMemcpyAsync(L.xw, L.gr + P.q, sizeof(double) * P.q, cudaMemcpyDeviceToDevice, S));
+      start_factor();
+      dots({{L.x, nullptr}}, L.scal + 1, P.n);
+    } else {
+      gradient();
+      dots({{L.grad, nullptr}, {L.x, nullptr}}, L.scal, P.n);
+    }
     fetch(L.st_cur, 1, false);
     double gnorm2 = H->scal[0];
     const double x_sq = H->scal[1];
     if (H->st[0].status != PROJ_APPLIED) {
       finish(L.st_cur, 1, L.u, nullptr, nullptr, L.xp, L.fr, L.x);
-      gradient();
-      dots({{L.grad, nullptr}, {L.x, nullptr}}, L.scal, P.n);
+      if (qgrad()) {
+        start_factor();
+      } else {
+        gradient();
+        dots({{L.grad, nullptr}, {L.x, nullptr}}, L.scal, P.n);
+      }
       fetch(nullptr, 0, false);
       gnorm2 = H->scal[0];
     }
@@ -785,6 +877,7 @@ struct Driver {
     ProjState trial0;
     double unused;
     advance(cur.nfree, cur.sum_a2_free, false, unused, dv, trial0);
+    if (qgrad()) gnorm2 = unused;  // ||X r||^2 from the direction's sweep
     converged = false;
     bool exhausted = true;
     int its = 0;

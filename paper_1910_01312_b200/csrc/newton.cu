@@ -267,4 +267,164 @@ cudaError_t launch_pspace_direction(const double* A, long long n, long long q, l
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- factor-space gradient
+// The SsN gradient grad = Q s = X r with r = X^T s, s = w - Pi(u), kept in factor space
+// across Newton steps:
+//   X^T w  moves by alpha t per accepted step (t = X^T d, the Newton system's solution;
+//          Qw moves by alpha X t = alpha Qd, so the pair stays consistent),
+//   X^T Pi moves by X^T (Pi_new - Pi_old), whose support is the slots whose projection
+//          changed -- about the free set, O(p) rows -- gathered in the accept pass.
+// So a Newton step sweeps A once (X [t, r] in the epilogue) instead of three times.
+
+// grad[J[k]] = x_{J_k} . r  (warp per row; the p-space system's right-hand side)
+__global__ void __launch_bounds__(256) rows_grad_kernel(RowsArgs g, const double* __restrict__ r,
+                                                        double* __restrict__ grad) {
+  const long long k = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= g.p) return;
+  double sg;
+  const double* row = logical_row(g, g.J[k], sg);
+  double acc = 0.0;
+  for (long long c = lane; c < g.q; c += 32) acc = fma(__ldg(row + c), r[c], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) grad[g.J[k]] = sg * acc;
+}
+
+cudaError_t launch_rows_grad(const double* A, long long n, long long q, long long lda,
+                             const double* rs, int svr, const int32_t* J, long long p,
+                             const double* r, double* grad, cudaStream_t stream) {
+  if (p < 1) return cudaSuccess;
+  RowsArgs g{A, n, q, lda, rs, svr, J, p};
+  note_launch();
+  rows_grad_kernel<<<(unsigned)ceil_div(p * 32, 256LL), 256, 0, stream>>>(g, r, grad);
+  return cudaGetLastError();
+}
+
+// Accepted Armijo step (as accept_kernel, same numpy-ordered arithmetic) plus
+//   s = w_new - Pi_new  and  part[block][c] = sum over changed slots i of this block's
+//   contiguous chunk (ascending i) of (Pi_new - Pi_old)_i x_i[c]
+// (changed slots collected per 256-slot tile by ballot + warp prefix into smem).
+static constexpr int AQ_NT = 256;
+static constexpr int AQ_MAXC = 8;  // q <= 2048
+struct AcceptQArgs {
+  RowsArgs g;  // logical rows of X (J unused)
+  long long n;
+  double alpha, cu;
+  double *w, *qw, *u, *xp, *s;
+  const double *d, *qd, *txj;
+  uint8_t* fr;
+  const uint8_t* tfj;
+  double* part;  // [grid][q]
+};
+
+template <int NC>
+__global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
+  __shared__ int list[AQ_NT];
+  __shared__ double dval[AQ_NT];
+  __shared__ int wcnt[AQ_NT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long chunk = ceil_div(ceil_div(a.n, (long long)gridDim.x), (long long)AQ_NT) * AQ_NT;
+  const long long b0 = (long long)blockIdx.x * chunk, b1 = min(a.n, b0 + chunk);
+  double acc[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) acc[k] = 0.0;
+  for (long long base = b0; base < b1; base += AQ_NT) {
+    const long long i = base + tid;
+    double dpi = 0.0;
+    if (i < b1) {
+      const double qdi = a.qd[i];
+      const double wn = __dadd_rn(a.w[i], __dmul_rn(a.alpha, a.d[i]));
+      a.w[i] = wn;
+      a.qw[i] = __dadd_rn(a.qw[i], __dmul_rn(a.alpha, qdi));
+      a.u[i] = __dadd_rn(a.u[i], __dmul_rn(a.cu, qdi));
+      const double xn = a.txj[i];
+      dpi = xn - a.xp[i];
+      a.xp[i] = xn;
+      a.fr[i] = a.tfj[i];
+      a.s[i] = __dsub_rn(wn, xn);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, dpi != 0.0);
+    if (lane == 0) wcnt[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < AQ_NT / 32; ++w) {
+      off += w < warp ? wcnt[w] : 0;
+      tot += wcnt[w];
+    }
+    if (dpi != 0.0) {
+      const int o = off + __popc(bal & ((1u << lane) - 1u));
+      list[o] = (int)(i - b0);
+      dval[o] = dpi;
+    }
+    __syncthreads();
+    for (int k = 0; k < tot; ++k) {
+      double sg;
+      const double* row = logical_row(a.g, b0 + list[k], sg);
+      const double f = dval[k] * sg;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const long long col = tid + (long long)c * AQ_NT;
+        if (col < a.g.q) acc[c] = fma(f, __ldg(row + col), acc[c]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const long long col = tid + (long long)c * AQ_NT;
+    if (col < a.g.q) a.part[(long long)blockIdx.x * a.g.q + col] = acc[c];
+  }
+}
+
+int accept_q_grid(long long n) {
+  long long g = ceil_div(n, (long long)AQ_NT * 4);
+  return (int)max(1LL, min(g, 148LL * 4));
+}
+
+size_t accept_q_ws_bytes(long long n, long long q) {
+  return (size_t)accept_q_grid(n) * q * sizeof(double);
+}
+
+// xpi += sum_b part[b] (block order), xw += alpha t, r = xw - xpi
+__global__ void qgrad_fold_kernel(const double* __restrict__ part, int nb, long long q,
+                                  double alpha, const double* __restrict__ t,
+                                  double* __restrict__ xw, double* __restrict__ xpi,
+                                  double* __restrict__ r) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= q) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[(long long)b * q + c];
+  const double pi = xpi[c] + s;
+  const double ww = __dadd_rn(xw[c], __dmul_rn(alpha, t[c]));
+  xpi[c] = pi;
+  xw[c] = ww;
+  r[c] = ww - pi;
+}
+
+cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long long lda,
+                            const double* rs, int svr, long long n, double alpha, double cu,
+                            double* w, const double* d, double* qw, const double* qd, double* u,
+                            double* xp, const double* txj, uint8_t* fr, const uint8_t* tfj,
+                            double* s, const double* t, double* xw, double* xpi, double* r,
+                            double* part, cudaStream_t stream) {
+  if (q > (long long)AQ_NT * AQ_MAXC) return cudaErrorInvalidValue;
+  AcceptQArgs a;
+  a.g = RowsArgs{A, n_phys, q, lda, rs, svr, nullptr, 0};
+  a.n = n; a.alpha = alpha; a.cu = cu;
+  a.w = w; a.qw = qw; a.u = u; a.xp = xp; a.s = s; a.d = d; a.qd = qd; a.txj = txj;
+  a.fr = fr; a.tfj = tfj; a.part = part;
+  const int grid = accept_q_grid(n);
+  const int nc = (int)ceil_div(q, (long long)AQ_NT);
+  note_launch();
+  if (nc <= 1) accept_q_kernel<1><<<grid, AQ_NT, 0, stream>>>(a);
+  else if (nc <= 2) accept_q_kernel<2><<<grid, AQ_NT, 0, stream>>>(a);
+  else if (nc <= 4) accept_q_kernel<4><<<grid, AQ_NT, 0, stream>>>(a);
+  else accept_q_kernel<8><<<grid, AQ_NT, 0, stream>>>(a);
+  note_launch();
+  qgrad_fold_kernel<<<(unsigned)ceil_div(q, 256LL), 256, 0, stream>>>(part, grid, q, alpha, t, xw,
+                                                                      xpi, r);
+  return cudaGetLastError();
+}
+
 }  // namespace ssnal

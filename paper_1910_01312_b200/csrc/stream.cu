@@ -97,6 +97,9 @@ struct StreamArgs {
   double* sq_part;
   double* sq_out;
   unsigned int* sq_ticket;
+  // epi 3 (k = 2, the factor-space Newton epilogue X [t, r]): output 0 folds as epi 2,
+  // output 1 (the gradient X r) as epi 1 into *sq_out2 (partials at sq_part + grid)
+  double* sq_out2;
 };
 
 // Producer: stream rows [r0, r1) of A through the ring.  Returns after the last issue.
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xt_kernel(StreamArgs p) {
 __device__ __forceinline__ double epi_term(const StreamArgs& p, long long gr, double val,
                                            double acc) {
   if (p.epi == 1) return fma(val, val, p.svr ? fma(val, val, acc) : acc);
-  if (p.epi == 2) {
+  if (p.epi >= 2) {  // 2, and output 0 of 3
     if (p.fm[gr]) acc = fma(p.av[gr], val, acc);
     if (p.svr && p.fm[gr + p.n]) acc = fma(p.av[gr + p.n], -val, acc);
   }
@@ -259,6 +262,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
   const long long rows = r1 - r0;
   const long long nchunk = rows > 0 ? ceil_div(rows, (long long)p.rows_per_stage) : 0;
   double sq = 0.0;  // lane 0: sum of squares of this warp's outputs (fused gradient norm)
+  double sq2 = 0.0;  // epi 3: sum of squares of output 1
   for (long long ch = 0; ch < nchunk; ++ch) {
     const int s = (int)(ch % NSTAGE);
     const long long rb = r0 + ch * p.rows_per_stage;
@@ -303,11 +307,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
           p.out[(long long)j * p.nlog + rb + r] = val;
           if (p.svr) p.out[(long long)j * p.nlog + rb + r + p.n] = -val;
           if (j == 0) sq = epi_term(p, rb + r, val, sq);
+          if (KV == 2 && j == 1 && p.epi == 3) sq2 = fma(val, val, p.svr ? fma(val, val, sq2) : sq2);
           if (two) {
             const double val2 = rs_s[rl + NCONS] * acc2[j];
             p.out[(long long)j * p.nlog + rb + r2] = val2;
             if (p.svr) p.out[(long long)j * p.nlog + rb + r2 + p.n] = -val2;
             if (j == 0) sq = epi_term(p, rb + r2, val2, sq);
+            if (KV == 2 && j == 1 && p.epi == 3)
+              sq2 = fma(val2, val2, p.svr ? fma(val2, val2, sq2) : sq2);
           }
         }
       }
@@ -316,24 +323,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   if (p.epi) {  // consumer warps only (the producer warp has returned)
-    __shared__ double wsq[NCONS];
+    __shared__ double wsq[NCONS], wsq2[NCONS];
     __shared__ bool last;
-    if (lane == 0) wsq[warp] = sq;
+    if (lane == 0) {
+      wsq[warp] = sq;
+      wsq2[warp] = sq2;
+    }
     asm volatile("bar.sync 1, %0;" ::"r"(NCONS * 32) : "memory");
     if (threadIdx.x == 0) {
-      double c = 0.0;
-      for (int w = 0; w < NCONS; ++w) c += wsq[w];
+      double c = 0.0, c2 = 0.0;
+      for (int w = 0; w < NCONS; ++w) {
+        c += wsq[w];
+        c2 += wsq2[w];
+      }
       p.sq_part[blockIdx.x] = c;
+      if (p.epi == 3) p.sq_part[gridDim.x + blockIdx.x] = c2;
       __threadfence();
       last = atomicAdd(p.sq_ticket, 1u) == gridDim.x - 1;
     }
     asm volatile("bar.sync 1, %0;" ::"r"(NCONS * 32) : "memory");
     if (last && warp == 0) {
-      double c = 0.0;
-      for (unsigned b = lane; b < gridDim.x; b += 32) c += __ldcg(p.sq_part + b);
+      double c = 0.0, c2 = 0.0;
+      for (unsigned b = lane; b < gridDim.x; b += 32) {
+        c += __ldcg(p.sq_part + b);
+        if (p.epi == 3) c2 += __ldcg(p.sq_part + gridDim.x + b);
+      }
       c = warp_sum(c);
+      c2 = warp_sum(c2);
       if (lane == 0) {
         *p.sq_out = c;
+        if (p.epi == 3) *p.sq_out2 = c2;
         *p.sq_ticket = 0u;
       }
     }
@@ -400,8 +419,9 @@ cudaError_t launch_stream_xd(const double* A, long long n, long long q, long lon
                              const double* rs, int svr, int k, const double* d, double* out,
                              long long nlog, cudaStream_t stream, double* sq_part, double* sq_out,
                              unsigned int* sq_ticket, int epi, const uint8_t* fm,
-                             const double* av) {
+                             const double* av, double* sq_out2) {
   StreamArgs p{};
+  p.sq_out2 = sq_out2;
   p.epi = sq_out ? (epi ? epi : 1) : 0;
   p.fm = fm;
   p.av = av;
