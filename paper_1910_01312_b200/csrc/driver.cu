@@ -961,6 +961,7 @@ struct Driver {
     if (w0) ck(cudaMemcpyAsync(L.w, w0, nb, cudaMemcpyDeviceToDevice, S));
     else ck(cudaMemsetAsync(L.w, 0, nb, S));
     if (P.csr) ck(cudaMemsetAsync(L.cj.ticket, 0, sizeof(unsigned int), S));
+    else ck(cudaMemsetAsync(L.qpart, 0, 256, S));  // accept_q ticket
     ck(cudaMemsetAsync(L.qw, 0, nb, S));
     dots({{P.c, nullptr}}, L.scal, P.n);
     fetch(nullptr, 0, false);

@@ -315,6 +315,11 @@ struct AcceptQArgs {
   uint8_t* fr;
   const uint8_t* tfj;
   double* part;  // [grid][q]
+  unsigned int* ticket;
+  int* touched;  // [grid]: this CTA saw a changed slot (its partial is nonzero)
+  // last-CTA fold: xpi += sum_b part[b] (block order), xw += alpha t, r = xw - xpi
+  const double* t;
+  double *xw, *xpi, *r;
 };
 
 template <int NC>
@@ -328,6 +333,7 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
   double acc[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) acc[k] = 0.0;
+  int any = 0;
   for (long long base = b0; base < b1; base += AQ_NT) {
     const long long i = base + tid;
     double dpi = 0.0;
@@ -358,7 +364,30 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
       dval[o] = dpi;
     }
     __syncthreads();
-    for (int k = 0; k < tot; ++k) {
+    any |= tot;
+    // changed rows four at a time: their loads are in flight together
+    int k = 0;
+    for (; k + 4 <= tot; k += 4) {
+      double sg[4], f[4], v[4][NC];
+      const double* row[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        row[u] = logical_row(a.g, b0 + list[k + u], sg[u]);
+        f[u] = dval[k + u] * sg[u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const long long col = tid + (long long)c * AQ_NT;
+          v[u][c] = col < a.g.q ? __ldg(row[u] + col) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = fma(f[u], v[u][c], acc[c]);
+    }
+    for (; k < tot; ++k) {
       double sg;
       const double* row = logical_row(a.g, b0 + list[k], sg);
       const double f = dval[k] * sg;
@@ -370,36 +399,61 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
     }
     __syncthreads();
   }
+  if (any) {
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const long long col = tid + (long long)c * AQ_NT;
-    if (col < a.g.q) a.part[(long long)blockIdx.x * a.g.q + col] = acc[c];
+    for (int c = 0; c < NC; ++c) {
+      const long long col = tid + (long long)c * AQ_NT;
+      if (col < a.g.q) a.part[(long long)blockIdx.x * a.g.q + col] = acc[c];
+    }
+  }
+  if (tid == 0) a.touched[blockIdx.x] = any ? 1 : 0;
+  if (!last_block_arrive(a.ticket, gridDim.x)) return;
+  // fold only the CTAs that saw a change (typically a handful), in block order
+  // touched CTAs listed in block order: all flags loaded at once, ballot + warp prefix
+  __shared__ int blist[148 * 8];
+  int m = 0;
+  for (unsigned c0 = 0; c0 < gridDim.x; c0 += AQ_NT) {
+    const unsigned b = c0 + tid;
+    const bool f = b < gridDim.x && __ldcg(a.touched + b) != 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wcnt[warp] = __popc(bal);
+    __syncthreads();
+    int off = m, tot = 0;
+#pragma unroll
+    for (int w = 0; w < AQ_NT / 32; ++w) {
+      off += w < warp ? wcnt[w] : 0;
+      tot += wcnt[w];
+    }
+    if (f) blist[off + __popc(bal & ((1u << lane) - 1u))] = (int)b;
+    m += tot;
+    __syncthreads();
+  }
+  for (long long c = tid; c < a.g.q; c += AQ_NT) {
+    double sum = 0.0;
+    int k = 0;
+    for (; k + 4 <= m; k += 4) {  // four independent loads in flight, summed in order
+      const double v0 = __ldcg(a.part + (long long)blist[k] * a.g.q + c);
+      const double v1 = __ldcg(a.part + (long long)blist[k + 1] * a.g.q + c);
+      const double v2 = __ldcg(a.part + (long long)blist[k + 2] * a.g.q + c);
+      const double v3 = __ldcg(a.part + (long long)blist[k + 3] * a.g.q + c);
+      sum = (((sum + v0) + v1) + v2) + v3;
+    }
+    for (; k < m; ++k) sum += __ldcg(a.part + (long long)blist[k] * a.g.q + c);
+    const double pi = a.xpi[c] + sum;
+    const double ww = __dadd_rn(a.xw[c], __dmul_rn(a.alpha, a.t[c]));
+    a.xpi[c] = pi;
+    a.xw[c] = ww;
+    a.r[c] = ww - pi;
   }
 }
 
 int accept_q_grid(long long n) {
-  long long g = ceil_div(n, (long long)AQ_NT * 4);
-  return (int)max(1LL, min(g, 148LL * 4));
+  long long g = ceil_div(n, (long long)AQ_NT);
+  return (int)max(1LL, min(g, 148LL * 8));
 }
 
 size_t accept_q_ws_bytes(long long n, long long q) {
-  return (size_t)accept_q_grid(n) * q * sizeof(double);
-}
-
-// xpi += sum_b part[b] (block order), xw += alpha t, r = xw - xpi
-__global__ void qgrad_fold_kernel(const double* __restrict__ part, int nb, long long q,
-                                  double alpha, const double* __restrict__ t,
-                                  double* __restrict__ xw, double* __restrict__ xpi,
-                                  double* __restrict__ r) {
-  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= q) return;
-  double s = 0.0;
-  for (int b = 0; b < nb; ++b) s += part[(long long)b * q + c];
-  const double pi = xpi[c] + s;
-  const double ww = __dadd_rn(xw[c], __dmul_rn(alpha, t[c]));
-  xpi[c] = pi;
-  xw[c] = ww;
-  r[c] = ww - pi;
+  return 256 + 148 * 8 * sizeof(int) + (size_t)accept_q_grid(n) * q * sizeof(double);
 }
 
 cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long long lda,
@@ -413,7 +467,11 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
   a.g = RowsArgs{A, n_phys, q, lda, rs, svr, nullptr, 0};
   a.n = n; a.alpha = alpha; a.cu = cu;
   a.w = w; a.qw = qw; a.u = u; a.xp = xp; a.s = s; a.d = d; a.qd = qd; a.txj = txj;
-  a.fr = fr; a.tfj = tfj; a.part = part;
+  a.fr = fr; a.tfj = tfj;
+  a.ticket = (unsigned int*)part;  // zeroed workspace; reset by the last CTA
+  a.touched = (int*)((char*)part + 256);
+  a.part = (double*)((char*)part + 256 + 148 * 8 * sizeof(int));
+  a.t = t; a.xw = xw; a.xpi = xpi; a.r = r;
   const int grid = accept_q_grid(n);
   const int nc = (int)ceil_div(q, (long long)AQ_NT);
   note_launch();
@@ -421,9 +479,6 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
   else if (nc <= 2) accept_q_kernel<2><<<grid, AQ_NT, 0, stream>>>(a);
   else if (nc <= 4) accept_q_kernel<4><<<grid, AQ_NT, 0, stream>>>(a);
   else accept_q_kernel<8><<<grid, AQ_NT, 0, stream>>>(a);
-  note_launch();
-  qgrad_fold_kernel<<<(unsigned)ceil_div(q, 256LL), 256, 0, stream>>>(part, grid, q, alpha, t, xw,
-                                                                      xpi, r);
   return cudaGetLastError();
 }
 

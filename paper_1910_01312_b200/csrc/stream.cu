@@ -14,6 +14,8 @@
 #include "common.cuh"
 #include "ssnal_internal.h"
 
+#include <cstdlib>
+
 namespace ssnal {
 
 namespace {
@@ -26,7 +28,9 @@ constexpr int NSTAGE = SSNAL_NSTAGE;
 constexpr int STAGE_BYTES = SSNAL_STAGE_KB * 1024;
 constexpr int NCONS = 8;                      // consumer warps
 constexpr int NTHREADS = (NCONS + 1) * 32;    // + one producer warp
-constexpr int ROWS_CTA = 512;                 // rows per CTA slab (coefficients fit in smem)
+constexpr int ROWS_CTA = 512;
+constexpr int XD_WARPS1 = 8;                  // X d consumer warps, one right-hand side
+constexpr int XD_WARPS2 = 8;                  // ... two right-hand sides (16: -7 % on config 1)                 // rows per CTA slab (coefficients fit in smem)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -224,8 +228,8 @@ __device__ __forceinline__ double epi_term(const StreamArgs& p, long long gr, do
   return acc;
 }
 
-template <int KV, int CP>
-__global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
+template <int KV, int CP, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) stream_xd_kernel(StreamArgs p) {
   extern __shared__ __align__(128) char ring[];
   __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -234,20 +238,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCONS);
+      mbar_init(&empty[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (warp == NCONS) {
+  if (warp == NCW) {
     if (lane == 0 && r1 > r0) produce(p, r0, r1, ring, full, empty);
     return;
   }
   // row signs of the slab staged once (a global load per row sat on the critical path
   // of every row's reduction)
   __shared__ double rs_s[ROWS_CTA];
-  for (long long r = threadIdx.x; r < r1 - r0; r += NCONS * 32) rs_s[r] = p.rs ? p.rs[r0 + r] : 1.0;
-  asm volatile("bar.sync 1, %0;" ::"r"(NCONS * 32) : "memory");
+  for (long long r = threadIdx.x; r < r1 - r0; r += NCW * 32) rs_s[r] = p.rs ? p.rs[r0 + r] : 1.0;
+  asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
   const long long pairs = p.q / 2;
   // this lane's slice of d: pairs lane, lane+32, ... (CP*... <= 8 per lane for q <= 512)
   double2 dv[KV][CP * 2];
@@ -270,8 +274,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
     mbar_wait(&full[s], (uint32_t)((ch / NSTAGE) & 1));
     const double* st = reinterpret_cast<const double*>(ring + (size_t)s * STAGE_BYTES);
     // two rows per warp iteration: their shuffle trees interleave
-    for (int r = warp; r < nr; r += 2 * NCONS) {
-      const int r2 = r + NCONS;
+    for (int r = warp; r < nr; r += 2 * NCW) {
+      const int r2 = r + NCW;
       const bool two = r2 < nr;
       const double2* row = reinterpret_cast<const double2*>(st + (size_t)r * p.lda);
       const double2* row2 = reinterpret_cast<const double2*>(st + (size_t)(two ? r2 : r) * p.lda);
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
           if (j == 0) sq = epi_term(p, rb + r, val, sq);
           if (KV == 2 && j == 1 && p.epi == 3) sq2 = fma(val, val, p.svr ? fma(val, val, sq2) : sq2);
           if (two) {
-            const double val2 = rs_s[rl + NCONS] * acc2[j];
+            const double val2 = rs_s[rl + NCW] * acc2[j];
             p.out[(long long)j * p.nlog + rb + r2] = val2;
             if (p.svr) p.out[(long long)j * p.nlog + rb + r2 + p.n] = -val2;
             if (j == 0) sq = epi_term(p, rb + r2, val2, sq);
@@ -323,16 +327,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   if (p.epi) {  // consumer warps only (the producer warp has returned)
-    __shared__ double wsq[NCONS], wsq2[NCONS];
+    __shared__ double wsq[NCW], wsq2[NCW];
     __shared__ bool last;
     if (lane == 0) {
       wsq[warp] = sq;
       wsq2[warp] = sq2;
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(NCONS * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
     if (threadIdx.x == 0) {
       double c = 0.0, c2 = 0.0;
-      for (int w = 0; w < NCONS; ++w) {
+      for (int w = 0; w < NCW; ++w) {
         c += wsq[w];
         c2 += wsq2[w];
       }
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) stream_xd_kernel(StreamArgs p) {
       __threadfence();
       last = atomicAdd(p.sq_ticket, 1u) == gridDim.x - 1;
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(NCONS * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
     if (last && warp == 0) {
       double c = 0.0, c2 = 0.0;
       for (unsigned b = lane; b < gridDim.x; b += 32) {
@@ -365,12 +369,13 @@ int rows_per_stage(long long lda) {
 }
 
 template <class K>
-cudaError_t launch_stream(K kernel, const StreamArgs& p, int grid, cudaStream_t stream) {
+cudaError_t launch_stream(K kernel, const StreamArgs& p, int grid, cudaStream_t stream,
+                          int threads = NTHREADS) {
   const int smem = NSTAGE * STAGE_BYTES;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch();
-  kernel<<<grid, NTHREADS, smem, stream>>>(p);
+  kernel<<<grid, threads, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -436,14 +441,30 @@ cudaError_t launch_stream_xd(const double* A, long long n, long long q, long lon
   const int grid = stream_grid(n);
   const long long pairs = q / 2;
   const int cp = (int)ceil_div(pairs, 64LL);  // lanes hold 2*CP pairs each
+  // consumer warps: XD_WARPS2 for two right-hand sides (twice the FMA and shuffle work
+  // per streamed byte), XD_WARPS1 for one
+  static const int w1 = std::getenv("SSNAL_XD_WARPS1") ? std::atoi(std::getenv("SSNAL_XD_WARPS1"))
+                                                       : XD_WARPS1;
+  static const int w2 = std::getenv("SSNAL_XD_WARPS2") ? std::atoi(std::getenv("SSNAL_XD_WARPS2"))
+                                                       : XD_WARPS2;
   if (k == 2) {
-    if (cp <= 1) return launch_stream(stream_xd_kernel<2, 1>, p, grid, stream);
-    if (cp <= 2) return launch_stream(stream_xd_kernel<2, 2>, p, grid, stream);
-    return launch_stream(stream_xd_kernel<2, 4>, p, grid, stream);
+    if (w2 == 16) {
+      if (cp <= 1) return launch_stream(stream_xd_kernel<2, 1, 16>, p, grid, stream, 17 * 32);
+      if (cp <= 2) return launch_stream(stream_xd_kernel<2, 2, 16>, p, grid, stream, 17 * 32);
+      return launch_stream(stream_xd_kernel<2, 4, 16>, p, grid, stream, 17 * 32);
+    }
+    if (cp <= 1) return launch_stream(stream_xd_kernel<2, 1, 8>, p, grid, stream);
+    if (cp <= 2) return launch_stream(stream_xd_kernel<2, 2, 8>, p, grid, stream);
+    return launch_stream(stream_xd_kernel<2, 4, 8>, p, grid, stream);
   }
-  if (cp <= 1) return launch_stream(stream_xd_kernel<1, 1>, p, grid, stream);
-  if (cp <= 2) return launch_stream(stream_xd_kernel<1, 2>, p, grid, stream);
-  return launch_stream(stream_xd_kernel<1, 4>, p, grid, stream);
+  if (w1 == 16) {
+    if (cp <= 1) return launch_stream(stream_xd_kernel<1, 1, 16>, p, grid, stream, 17 * 32);
+    if (cp <= 2) return launch_stream(stream_xd_kernel<1, 2, 16>, p, grid, stream, 17 * 32);
+    return launch_stream(stream_xd_kernel<1, 4, 16>, p, grid, stream, 17 * 32);
+  }
+  if (cp <= 1) return launch_stream(stream_xd_kernel<1, 1, 8>, p, grid, stream);
+  if (cp <= 2) return launch_stream(stream_xd_kernel<1, 2, 8>, p, grid, stream);
+  return launch_stream(stream_xd_kernel<1, 4, 8>, p, grid, stream);
 }
 
 }  // namespace ssnal
