@@ -127,10 +127,11 @@ def _sweep_bytes(problem):
 
 def _ncu_traffic():
     """DRAM read + write bytes per launch of the committed ncu --set full capture of
-    stream_xd_kernel (profiles/r1_ncu_stream_xd.txt), or None."""
+    the per-Newton-step sweep stream_xd_kernel<2> (X [t, r]; profiles/r1_ncu_stream_xd2.txt),
+    or None."""
     try:
         vals = {}
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_stream_xd.txt")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_stream_xd2.txt")) as fh:
             for line in fh:
                 parts = line.split()
                 if parts and parts[0] == "raw" and parts[1].startswith("dram__bytes_"):
@@ -145,7 +146,7 @@ def cpu_oracle_solve(cfg):
     """Numpy restatement of the reference path (oracle/), stable psi evaluation."""
     import oracle as O
 
-    O.set_psi_mode("stable")
+    O.set_psi_mode("delta")  # the product's default line search (DESIGN.md section 3)
     op, c, bl = O.csvc_problem(cfg["A"], cfg["y"], cfg["C"])
     t0 = time.perf_counter()
     rep = O.alm_solve(op, c, bl, O.AlmOpts(tol_kkt=TOL))
@@ -298,17 +299,19 @@ def run_ours(args, rank, world, local_rank):
     roof = None
     ptotal = float(np.sum(prof_wall)) if prof_wall else 0.0
     if kern:
-        # dominant kernel of the launch list (profiles/r1_launches_config1_solve.txt): the
-        # streaming sweeps of A (stream_xd / stream_xt, both HBM bound).  achieved = their
-        # algorithmic bytes / their device time, measured live here over the K profiled
-        # solves (op classes dense_xt, which also holds the fused gradient's two sweeps,
-        # and dense_x); traffic = DRAM bytes per launch of one ncu --set full capture
+        # dominant HBM-bound kernel of the launch list (profiles/r1_launches_config1_solve.txt):
+        # the streaming sweeps of A -- per Newton step ONE stream_xd<2> (X [t, r]: Qd and the
+        # gradient), plus the inner-solve start (X^T s) and the KKT/refresh sweeps.
+        # achieved = their algorithmic bytes / their device time, measured live here over
+        # the K profiled solves (op classes dense_xt and dense_x hold exactly the sweeps);
+        # traffic = DRAM bytes per launch of one ncu --set full capture of stream_xd<2>
         sweeps = [kern[k] for k in ("dense_xt", "dense_x") if k in kern]
         cnt = sum(v[0] for v in sweeps)
         secs = sum(v[1] for v in sweeps)
         nbytes = sum(v[2] for v in sweeps)
         achieved = (nbytes / secs) / 1e9 if secs > 0 and nbytes > 0 else 0.0
-        roof = {"bound": "hbm", "kernel": "stream_xd_kernel / stream_xt_kernel (sweeps of A)",
+        roof = {"bound": "hbm",
+                "kernel": "stream_xd_kernel<2> / stream_xd / stream_xt (sweeps of A)",
                 "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak if peak else None,
                 "traffic": _ncu_traffic(), "peak_kind": peak_kind, "op_calls": cnt,

@@ -717,7 +717,7 @@ cudaError_t launch_direction_epilogue_q(const double* A, long long n, long long 
                                         const double* asa_dev, const double* s, double sigma,
                                         const double* w, const double* qw, double* dir,
                                         double* dots4, double* g2, void* ws,
-                                        cudaStream_t stream) {
+                                        cudaStream_t stream, int parts) {
   const long long nlog = svr ? 2 * n : n;
   char* base = (char*)ws;
   unsigned int* ticket = (unsigned int*)base;
@@ -726,7 +726,8 @@ cudaError_t launch_direction_epilogue_q(const double* A, long long n, long long 
   double* sq_part = (double*)(base + 256 + grad_red_bytes(n));
   double* qdir = qg;
   double* grad = qg + nlog;
-  if (stream_ok(A, lda, q) && q <= 512) {
+  if (!(parts & 1)) {
+  } else if (stream_ok(A, lda, q) && q <= 512) {
     cudaError_t e = launch_stream_xd(A, n, q, lda, rs, svr, 2, t2, qg, nlog, stream, sq_part, ad,
                                      ticket, 3, fm, a, g2);
     if (e != cudaSuccess) return e;
@@ -742,6 +743,7 @@ cudaError_t launch_direction_epilogue_q(const double* A, long long n, long long 
     e = launch_dots(1, gx, gy, nullptr, nlog, g2, red_ws, stream);
     if (e != cudaSuccess) return e;
   }
+  if (!(parts & 2)) return cudaGetLastError();
   return launch_hs_finish_dots(fm, a, qdir, nlog, -sigma, s, -1.0, dir, ad, asa_dev, grad, w, qw,
                                t2, q, dots4, red_ws, stream);
 }

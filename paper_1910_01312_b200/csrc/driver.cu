@@ -109,7 +109,8 @@ cudaError_t launch_direction_epilogue_q(const double* A, long long n, long long 
                                         const uint8_t* fm, const double* a,
                                         const double* asa_dev, const double* s, double sigma,
                                         const double* w, const double* qw, double* dir,
-                                        double* dots4, double* g2, void* ws, cudaStream_t stream);
+                                        double* dots4, double* g2, void* ws, cudaStream_t stream,
+                                        int parts);
 cudaError_t launch_grad_from_factor(const double* A, long long n, long long q, long long lda,
                                     const double* rs, int svr, const double* r, double* grad,
                                     double* g2, void* ws, cudaStream_t stream);
@@ -715,10 +716,16 @@ struct Driver {
     if (qgrad()) {
       // ONE sweep X [t, r]: Qd and this point's gradient (a_J'(Qd)_J and ||grad||^2
       // folded), then d = -s - sigma P(Qd) and {g'd, w'Qw, w'Qd, t't}
-      timed(SSNAL_OP_XD, a_bytes() + 8.0 * (2 * P.n + 2 * P.q) + 8.0 * P.n * 8, [&] {
+      // sweep: A + labels, [Qd ; grad] written, mask + a read for the a_J'(Qd)_J fold
+      timed(SSNAL_OP_XD, a_bytes() + 16.0 * P.n + 9.0 * P.n + 16.0 * P.q, [&] {
         ck(launch_direction_epilogue_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.t,
                                        L.qdir, L.fr, P.a, &L.st_cur->sum_a2_free, L.s, sigma,
-                                       L.w, L.qw, L.dir, L.scal, L.scal + 4, L.ws_grad, S));
+                                       L.w, L.qw, L.dir, L.scal, L.scal + 4, L.ws_grad, S, 1));
+      });
+      timed(SSNAL_OP_VEC, 8.0 * P.n * 7 + 1.0 * P.n, [&] {
+        ck(launch_direction_epilogue_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.t,
+                                       L.qdir, L.fr, P.a, &L.st_cur->sum_a2_free, L.s, sigma,
+                                       L.w, L.qw, L.dir, L.scal, L.scal + 4, L.ws_grad, S, 2));
       });
       return;
     }

@@ -228,6 +228,17 @@ __device__ __forceinline__ double epi_term(const StreamArgs& p, long long gr, do
   return acc;
 }
 
+// epi_term with the epi >= 2 coefficients read from the staged slab copy (row rl)
+__device__ __forceinline__ double epi_term_s(const StreamArgs& p, const double (*ec)[ROWS_CTA],
+                                             int rl, double val, double acc) {
+  if (p.epi == 1) return fma(val, val, p.svr ? fma(val, val, acc) : acc);
+  if (p.epi >= 2) {
+    acc = fma(ec[0][rl], val, acc);
+    if (p.svr) acc = fma(ec[1][rl], -val, acc);
+  }
+  return acc;
+}
+
 template <int KV, int CP, int NCW>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1) stream_xd_kernel(StreamArgs p) {
   extern __shared__ __align__(128) char ring[];
@@ -250,7 +261,18 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) stream_xd_kernel(StreamArgs
   // row signs of the slab staged once (a global load per row sat on the critical path
   // of every row's reduction)
   __shared__ double rs_s[ROWS_CTA];
-  for (long long r = threadIdx.x; r < r1 - r0; r += NCW * 32) rs_s[r] = p.rs ? p.rs[r0 + r] : 1.0;
+  // epi >= 2: the fold coefficients free_i ? a_i : 0 of the slab's logical rows (and of
+  // their SVR mirrors), staged likewise -- lane 0 read them per row from global memory,
+  // a dependent load on every row of the epilogue sweep
+  __shared__ double ec_s[2][ROWS_CTA];
+  for (long long r = threadIdx.x; r < r1 - r0; r += NCW * 32) {
+    rs_s[r] = p.rs ? p.rs[r0 + r] : 1.0;
+    if (p.epi >= 2) {
+      const long long g = r0 + r;
+      ec_s[0][r] = p.fm[g] ? p.av[g] : 0.0;
+      if (p.svr) ec_s[1][r] = p.fm[g + p.n] ? p.av[g + p.n] : 0.0;
+    }
+  }
   asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
   const long long pairs = p.q / 2;
   // this lane's slice of d: pairs lane, lane+32, ... (CP*... <= 8 per lane for q <= 512)
@@ -295,32 +317,35 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) stream_xd_kernel(StreamArgs
           }
         }
       }
+      // reduce-scatter butterfly over the 2 KV row sums: each level halves the values a
+      // lane keeps, so the 2 KV totals land in different lane groups (KV = 2: 6 shuffles
+      // instead of 20) and their epilogues run in parallel, one writer lane per output:
+      //   value index v = 2*bit4 (+ bit3 for KV = 2): row = bit4, right-hand side j = bit3
+      const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
+      double z;
+      if constexpr (KV == 2) {
+        const double s0 = b4 ? acc[0] : acc2[0], s1 = b4 ? acc[1] : acc2[1];
+        const double k0 = b4 ? acc2[0] : acc[0], k1 = b4 ? acc2[1] : acc[1];
+        const double w0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+        const double w1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+        z = (b3 ? w1 : w0) + __shfl_xor_sync(0xffffffffu, b3 ? w0 : w1, 8);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
+        for (int o = 4; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+      } else {
+        z = (b4 ? acc2[0] : acc[0]) + __shfl_xor_sync(0xffffffffu, b4 ? acc[0] : acc2[0], 16);
 #pragma unroll
-        for (int j = 0; j < KV; ++j) {
-          acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-          acc2[j] += __shfl_xor_sync(0xffffffffu, acc2[j], o);
-        }
+        for (int o = 8; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
       }
-      if (lane == 0) {
-        const int rl = (int)(rb - r0) + r;
-#pragma unroll
-        for (int j = 0; j < KV; ++j) {
-          const double val = rs_s[rl] * acc[j];
-          p.out[(long long)j * p.nlog + rb + r] = val;
-          if (p.svr) p.out[(long long)j * p.nlog + rb + r + p.n] = -val;
-          if (j == 0) sq = epi_term(p, rb + r, val, sq);
-          if (KV == 2 && j == 1 && p.epi == 3) sq2 = fma(val, val, p.svr ? fma(val, val, sq2) : sq2);
-          if (two) {
-            const double val2 = rs_s[rl + NCW] * acc2[j];
-            p.out[(long long)j * p.nlog + rb + r2] = val2;
-            if (p.svr) p.out[(long long)j * p.nlog + rb + r2 + p.n] = -val2;
-            if (j == 0) sq = epi_term(p, rb + r2, val2, sq);
-            if (KV == 2 && j == 1 && p.epi == 3)
-              sq2 = fma(val2, val2, p.svr ? fma(val2, val2, sq2) : sq2);
-          }
-        }
+      const int jo = KV == 2 ? b3 : 0;
+      const bool writer = (lane & (KV == 2 ? 7 : 15)) == 0 && (b4 == 0 || two);
+      if (writer) {
+        const int rr = b4 ? r2 : r;
+        const int rl = (int)(rb - r0) + rr;
+        const double val = rs_s[rl] * z;
+        p.out[(long long)jo * p.nlog + rb + rr] = val;
+        if (p.svr) p.out[(long long)jo * p.nlog + rb + rr + p.n] = -val;
+        if (jo == 0) sq = epi_term_s(p, ec_s, rl, val, sq);
+        if (KV == 2 && jo == 1 && p.epi == 3) sq2 = fma(val, val, p.svr ? fma(val, val, sq2) : sq2);
       }
     }
     __syncwarp();
@@ -329,6 +354,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) stream_xd_kernel(StreamArgs
   if (p.epi) {  // consumer warps only (the producer warp has returned)
     __shared__ double wsq[NCW], wsq2[NCW];
     __shared__ bool last;
+    sq = warp_sum(sq);  // writer lanes hold the per-lane partials
+    sq2 = warp_sum(sq2);
     if (lane == 0) {
       wsq[warp] = sq;
       wsq2[warp] = sq2;
@@ -434,7 +461,13 @@ cudaError_t launch_stream_xd(const double* A, long long n, long long q, long lon
   p.sq_out = sq_out;
   p.sq_ticket = sq_ticket;
   p.A = A; p.n = n; p.q = q; p.lda = lda; p.rs = rs; p.svr = svr;
-  p.rows_per_stage = rows_per_stage(lda);
+  // whole rounds of 2 rows x XD warps per stage (q = 300: 16 rows of 2.4 KB instead of
+  // 20, whose 4-row second round left 3/4 of the warps idle)
+  {
+    const int wmax = 16;  // the larger consumer count either instantiation may use
+    const int r = rows_per_stage(lda);
+    p.rows_per_stage = r >= 2 * wmax ? r / (2 * wmax) * (2 * wmax) : (r >= 16 ? r / 16 * 16 : r);
+  }
   p.d = d;
   p.out = out;
   p.nlog = nlog;
