@@ -123,7 +123,8 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
                             double* w, const double* d, double* qw, const double* qd, double* u,
                             double* xp, const double* txj, uint8_t* fr, const uint8_t* tfj,
                             double* s, const double* t, double* xw, double* xpi, double* r,
-                            double* part, cudaStream_t stream);
+                            double* part, const ProjState* st_src, ProjState* st_dst,
+                            cudaStream_t stream);
 
 // direct reduced systems of the sparse operator: min(p, q) up to this size (M buffer)
 constexpr long long SPARSE_DIRECT_MAX = 2048;
@@ -156,12 +157,18 @@ struct Carver {
   }
 };
 
+// Device "blob" read back by every host decision in ONE copy: scalars at 0, the
+// Cholesky info at 128, then st_trial[TMAX], st_cur, st_kkt (carve keeps them contiguous)
+constexpr size_t BLOB_ST = 256;
+constexpr size_t BLOB_BYTES = BLOB_ST + (TMAX + 2) * sizeof(ProjState);
+
 struct Pinned {
   double scal[NSCAL];
   double cg[8];
   int info;
   int pad;
   ProjState st[TMAX];
+  alignas(256) char blob[BLOB_BYTES];
 };
 
 Pinned* pinned_buffer() {
@@ -219,15 +226,19 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
   L.qpart = sparse ? nullptr : cv.take<double>(accept_q_ws_bytes(n, q) / sizeof(double) + 1);
   L.M = sparse ? nullptr : cv.take<double>((size_t)q * q);
   L.m1 = cv.take<double>(q);
-  L.scal = cv.take<double>(NSCAL);
+  {  // contiguous read-back blob (see BLOB_ST)
+    char* blob = cv.take<char>(BLOB_BYTES);
+    L.scal = reinterpret_cast<double*>(blob);
+    L.info = reinterpret_cast<int*>(blob ? blob + 128 : nullptr);
+    L.st_trial = reinterpret_cast<ProjState*>(blob ? blob + BLOB_ST : nullptr);
+    L.st_cur = L.st_trial ? L.st_trial + TMAX : nullptr;
+    L.st_kkt = L.st_trial ? L.st_trial + TMAX + 1 : nullptr;
+  }
   L.fr = cv.take<uint8_t>(n);
   L.tfree = cv.take<uint8_t>((size_t)TMAX * n);
   L.J = cv.take<int32_t>(n);
   L.pcount = cv.take<long long>(1);
-  L.info = cv.take<int>(1);
-  L.st_cur = cv.take<ProjState>(1);
-  L.st_trial = cv.take<ProjState>(TMAX);
-  L.st_kkt = cv.take<ProjState>(1);
+
   L.ws_proj = cv.take<char>(proj_ws_bytes(n, TMAX));
   L.ws_red = cv.take<char>(reduce_ws_bytes(n) + 64);
   L.ws_cmp = cv.take<char>(compact_ws_bytes(n));
@@ -495,12 +506,20 @@ struct Driver {
   }
 
   // ---------------------------------------------------------------- plumbing
+  // one D2H copy of the blob prefix that holds the scalars, info and the T states
   void fetch(const ProjState* states, int T, bool info) {
-    ck(cudaMemcpyAsync(H->scal, L.scal, sizeof(double) * NSCAL, cudaMemcpyDeviceToHost, S));
-    if (states) ck(cudaMemcpyAsync(H->st, states, sizeof(ProjState) * T, cudaMemcpyDeviceToHost, S));
-    if (info) ck(cudaMemcpyAsync(&H->info, L.info, sizeof(int), cudaMemcpyDeviceToHost, S));
+    const char* base = reinterpret_cast<const char*>(L.scal);
+    size_t st_off = 0, bytes = 128 + sizeof(int);
+    if (states) {
+      st_off = (size_t)(reinterpret_cast<const char*>(states) - base);
+      bytes = st_off + sizeof(ProjState) * T;
+    }
+    ck(cudaMemcpyAsync(H->blob, base, bytes, cudaMemcpyDeviceToHost, S));
     ck(cudaStreamSynchronize(S));
     ++syncs;
+    std::memcpy(H->scal, H->blob, sizeof(double) * NSCAL);
+    if (info) std::memcpy(&H->info, H->blob + 128, sizeof(int));
+    if (states) std::memcpy(H->st, H->blob + st_off, sizeof(ProjState) * T);
   }
 
   void project(const double* A, ProjState* st, int T, const double* B, const double* coefs,
@@ -832,10 +851,8 @@ struct Driver {
         ck(launch_accept_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, P.n, alpha,
                            -(sigma * alpha), L.w, L.dir, L.qw, L.qdir, L.u, L.xp,
                            L.tx + (size_t)j * P.n, L.fr, L.tfree + (size_t)j * P.n, L.s, tdir,
-                           L.xw, L.xpi, L.r, L.qpart, S));
+                           L.xw, L.xpi, L.r, L.qpart, L.st_trial + j, L.st_cur, S));
       });
-      ck(cudaMemcpyAsync(L.st_cur, L.st_trial + j, sizeof(ProjState), cudaMemcpyDeviceToDevice,
-                         S));
       return;
     }
     timed(SSNAL_OP_VEC, 8.0 * P.n * 8 + 2.0 * P.n, [&] {

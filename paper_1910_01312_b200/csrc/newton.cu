@@ -320,6 +320,9 @@ struct AcceptQArgs {
   // last-CTA fold: xpi += sum_b part[b] (block order), xw += alpha t, r = xw - xpi
   const double* t;
   double *xw, *xpi, *r;
+  // accepted trial's projection record -> current record (replaces a D2D memcpy)
+  const ProjState* st_src;
+  ProjState* st_dst;
 };
 
 template <int NC>
@@ -328,6 +331,9 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
   __shared__ double dval[AQ_NT];
   __shared__ int wcnt[AQ_NT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (blockIdx.x == 0 && a.st_dst && tid < (int)(sizeof(ProjState) / sizeof(unsigned int)))
+    reinterpret_cast<unsigned int*>(a.st_dst)[tid] =
+        reinterpret_cast<const unsigned int*>(a.st_src)[tid];
   const long long chunk = ceil_div(ceil_div(a.n, (long long)gridDim.x), (long long)AQ_NT) * AQ_NT;
   const long long b0 = (long long)blockIdx.x * chunk, b1 = min(a.n, b0 + chunk);
   double acc[NC];
@@ -461,7 +467,8 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
                             double* w, const double* d, double* qw, const double* qd, double* u,
                             double* xp, const double* txj, uint8_t* fr, const uint8_t* tfj,
                             double* s, const double* t, double* xw, double* xpi, double* r,
-                            double* part, cudaStream_t stream) {
+                            double* part, const ProjState* st_src, ProjState* st_dst,
+                            cudaStream_t stream) {
   if (q > (long long)AQ_NT * AQ_MAXC) return cudaErrorInvalidValue;
   AcceptQArgs a;
   a.g = RowsArgs{A, n_phys, q, lda, rs, svr, nullptr, 0};
@@ -472,6 +479,7 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
   a.touched = (int*)((char*)part + 256);
   a.part = (double*)((char*)part + 256 + 148 * 8 * sizeof(int));
   a.t = t; a.xw = xw; a.xpi = xpi; a.r = r;
+  a.st_src = st_src; a.st_dst = st_dst;
   const int grid = accept_q_grid(n);
   const int nc = (int)ceil_div(q, (long long)AQ_NT);
   note_launch();
