@@ -399,8 +399,17 @@ template <class K>
 cudaError_t launch_stream(K kernel, const StreamArgs& p, int grid, cudaStream_t stream,
                           int threads = NTHREADS) {
   const int smem = NSTAGE * STAGE_BYTES;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  // the smem opt-in once per kernel (a host API call per launch sat on the critical path
+  // right after every host decision)
+  static const void* done[64];
+  static int ndone = 0;
+  bool seen = false;
+  for (int i = 0; i < ndone; ++i) seen |= done[i] == (const void*)kernel;
+  if (!seen) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (ndone < 64) done[ndone++] = (const void*)kernel;
+  }
   note_launch();
   kernel<<<grid, threads, smem, stream>>>(p);
   return cudaGetLastError();
