@@ -169,12 +169,26 @@ struct Pinned {
   int pad;
   ProjState st[TMAX];
   alignas(256) char blob[BLOB_BYTES];
+  alignas(64) volatile unsigned int seq;  // written by publish_kernel after the blob
 };
+
+// Host decision read-back without a copy-engine round trip: one CTA stores the blob
+// prefix straight into the mapped pinned buffer, fences system-wide, then bumps the
+// sequence word the host spins on.
+__global__ void publish_kernel(const unsigned int* __restrict__ src, unsigned int nwords,
+                               unsigned int* dst, volatile unsigned int* seq_word,
+                               unsigned int seq) {
+  for (unsigned int i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) *seq_word = seq;
+}
 
 Pinned* pinned_buffer() {
   static thread_local Pinned* buf = nullptr;
   if (!buf) {
-    if (cudaHostAlloc(&buf, sizeof(Pinned), cudaHostAllocDefault) != cudaSuccess) buf = nullptr;
+    if (cudaHostAlloc(&buf, sizeof(Pinned), cudaHostAllocMapped) != cudaSuccess) buf = nullptr;
+    else buf->seq = 0u;
   }
   return buf;
 }
@@ -507,15 +521,55 @@ struct Driver {
 
   // ---------------------------------------------------------------- plumbing
   // one D2H copy of the blob prefix that holds the scalars, info and the T states
+  // SSNAL_TRACE_SYNC: GPU idle across each host decision = (event recorded right
+  // after the host resumes) - (event recorded before the sync), summed and printed
+  cudaEvent_t tr_a = nullptr, tr_b = nullptr;
+  double tr_idle = 0.0;
+  long long tr_n = 0;
+  bool tr_on = std::getenv("SSNAL_TRACE_SYNC") != nullptr;
+  void trace_resume() {
+    if (!tr_on || !tr_a) return;
+    ck(cudaEventRecord(tr_b, S));
+    ck(cudaEventSynchronize(tr_b));
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, tr_a, tr_b));
+    tr_idle += ms;
+    ++tr_n;
+  }
+
   void fetch(const ProjState* states, int T, bool info) {
+    if (tr_on) {
+      if (!tr_a) {
+        cudaEventCreate(&tr_a);
+        cudaEventCreate(&tr_b);
+      }
+      ck(cudaEventRecord(tr_a, S));
+    }
     const char* base = reinterpret_cast<const char*>(L.scal);
     size_t st_off = 0, bytes = 128 + sizeof(int);
     if (states) {
       st_off = (size_t)(reinterpret_cast<const char*>(states) - base);
       bytes = st_off + sizeof(ProjState) * T;
     }
-    ck(cudaMemcpyAsync(H->blob, base, bytes, cudaMemcpyDeviceToHost, S));
-    ck(cudaStreamSynchronize(S));
+    const unsigned int seq = H->seq + 1u;
+    note_launch();
+    publish_kernel<<<1, 256, 0, S>>>(reinterpret_cast<const unsigned int*>(base),
+                                     (unsigned int)((bytes + 3) / 4),
+                                     reinterpret_cast<unsigned int*>(H->blob), &H->seq, seq);
+    ck(cudaGetLastError());
+    // spin on the sequence word; every 4096 polls ask the stream whether it failed or
+    // drained without publishing (then fall back to a plain synchronize)
+    for (unsigned long long spin = 1;; ++spin) {
+      if (H->seq == seq) break;
+      if ((spin & 4095u) == 0u) {
+        const cudaError_t q = cudaStreamQuery(S);
+        if (q != cudaSuccess && q != cudaErrorNotReady) ck(q);
+        if (q == cudaSuccess && H->seq != seq) {
+          ck(cudaStreamSynchronize(S));
+          if (H->seq != seq) throw DriverError{SSNAL_E_DEVICE, "read-back did not publish"};
+        }
+      }
+    }
     ++syncs;
     std::memcpy(H->scal, H->blob, sizeof(double) * NSCAL);
     if (info) std::memcpy(&H->info, H->blob + 128, sizeof(int));
@@ -846,6 +900,7 @@ struct Driver {
   }
 
   void accept(double alpha, int j) {
+    trace_resume();
     if (qgrad()) {  // + s, and X^T w, X^T Pi(u), r = X^T s updated from the changed slots
       timed(SSNAL_OP_VEC, 8.0 * P.n * 9 + 2.0 * P.n, [&] {
         ck(launch_accept_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, P.n, alpha,
@@ -1066,6 +1121,9 @@ struct Driver {
     }
     rep->wall_time =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (tr_on)
+      std::fprintf(stderr, "trace: %lld host decisions before accept, GPU idle %.3f ms total\n",
+                   tr_n, tr_idle);
   }
 };
 
