@@ -124,10 +124,7 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
                             double* xp, const double* txj, uint8_t* fr, const uint8_t* tfj,
                             double* s, const double* t, double* xw, double* xpi, double* r,
                             double* part, const ProjState* st_src, ProjState* st_dst,
-                            cudaStream_t stream, const int* dec = nullptr,
-                            const double* dec_alpha = nullptr, const double* tx = nullptr,
-                            const uint8_t* tfree = nullptr, const ProjState* st_trial = nullptr,
-                            double sigma = 0.0);
+                            cudaStream_t stream);
 
 // direct reduced systems of the sparse operator: min(p, q) up to this size (M buffer)
 constexpr long long SPARSE_DIRECT_MAX = 2048;
@@ -185,76 +182,6 @@ __global__ void publish_kernel(const unsigned int* __restrict__ src, unsigned in
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) *seq_word = seq;
-}
-
-// Device-side decision of a Newton step from the speculative first Armijo batch (the
-// host's ssn_solve tests, same expressions, no FMA contraction): stopping test, descent
-// check, psi-resolution stop, then the first trial passing Armijo.  Only STEP_ACCEPTED
-// makes the following accept_q launch apply trial j; every other code leaves the state
-// untouched for the host's own path (steepest descent, further batches, stop).
-struct StepParams {
-  double ce, cd, floor_, sigma, mu, x_sq, beta;
-  int mode, T, allow;
-};
-
-__device__ __forceinline__ double psi_dev(double wqw, const ProjState& r, double x_sq, double sigma,
-                                          int mode) {
-  const double diff = mode ? r.sum_xv : __dsub_rn(r.sum_v2, r.sum_r2);
-  return __dsub_rn(__dadd_rn(__dmul_rn(0.5, wqw), __ddiv_rn(diff, __dmul_rn(2.0, sigma))),
-                   __ddiv_rn(x_sq, __dmul_rn(2.0, sigma)));
-}
-
-__global__ void select_step_kernel(const double* __restrict__ scal, const ProjState* __restrict__ cur,
-                                   const ProjState* __restrict__ trial, StepParams sp, int* dec,
-                                   double* dec_alpha) {
-  if (threadIdx.x != 0) return;
-  int code = STEP_NO_TRIAL, jj = -1;
-  double alpha_acc = 0.0;
-  const double gnorm = __dsqrt_rn(scal[4]);
-  const double dist = __dsqrt_rn(cur->sum_dref2);
-  const double gd = scal[0], wqw = scal[1], wqdir = scal[2], dqd = scal[3];
-  if ((gnorm <= sp.ce && gnorm <= __dmul_rn(sp.cd, dist)) || gnorm <= sp.floor_) {
-    code = STEP_CONVERGED;
-  } else if (!(gd < 0.0)) {
-    code = STEP_NONDESCENT;
-  } else {
-    const double psi0 = psi_dev(wqw, *cur, sp.x_sq, sp.sigma, sp.mode);
-    if (sp.mode != 2 &&
-        __dmul_rn(sp.mu, fabs(gd)) <= __dmul_rn(1e-16, __dadd_rn(1.0, fabs(psi0)))) {
-      code = STEP_RESOLUTION;
-    } else {
-      for (int k = 0; k < sp.T; ++k)
-        if (trial[k].status != PROJ_APPLIED) code = STEP_UNAPPLIED;
-      if (code != STEP_UNAPPLIED) {
-        double a = 1.0;
-        for (int k = 0; k < sp.T; ++k) {
-          bool ok;
-          if (sp.mode == 2) {
-            const double lhs = __dadd_rn(
-                __dadd_rn(__dmul_rn(a, gd), __dmul_rn(__dmul_rn(__dmul_rn(0.5, a), a), dqd)),
-                __ddiv_rn(trial[k].sum_bh, sp.sigma));
-            ok = lhs <= __dmul_rn(__dmul_rn(sp.mu, a), gd);
-          } else {
-            const double quad = __dadd_rn(__dadd_rn(wqw, __dmul_rn(__dmul_rn(2.0, a), wqdir)),
-                                          __dmul_rn(__dmul_rn(a, a), dqd));
-            const double pt = psi_dev(quad, trial[k], sp.x_sq, sp.sigma, sp.mode);
-            ok = pt <= __dadd_rn(psi0, __dmul_rn(__dmul_rn(sp.mu, a), gd));
-          }
-          if (ok) {
-            code = STEP_ACCEPTED;
-            jj = k;
-            alpha_acc = a;
-            break;
-          }
-          a = __dmul_rn(a, sp.beta);
-        }
-      }
-    }
-  }
-  if (code == STEP_ACCEPTED && !sp.allow) code = STEP_NONE;
-  dec[0] = code;
-  dec[1] = jj;
-  *dec_alpha = alpha_acc;
 }
 
 Pinned* pinned_buffer() {
@@ -610,15 +537,7 @@ struct Driver {
     ++tr_n;
   }
 
-  // one read-back = publish (enqueue the copy into the mapped pinned blob) + wait (spin on
-  // its sequence word); split so work can be enqueued between the two
-  struct Pub {
-    unsigned int seq;
-    size_t st_off;
-    int T;
-    bool info, states;
-  };
-  Pub publish(const ProjState* states, int T, bool info) {
+  void fetch(const ProjState* states, int T, bool info) {
     if (tr_on) {
       if (!tr_a) {
         cudaEventCreate(&tr_a);
@@ -627,7 +546,7 @@ struct Driver {
       ck(cudaEventRecord(tr_a, S));
     }
     const char* base = reinterpret_cast<const char*>(L.scal);
-    size_t st_off = 0, bytes = 152;  // scalars, info, step decision
+    size_t st_off = 0, bytes = 128 + sizeof(int);
     if (states) {
       st_off = (size_t)(reinterpret_cast<const char*>(states) - base);
       bytes = st_off + sizeof(ProjState) * T;
@@ -638,28 +557,24 @@ struct Driver {
                                      (unsigned int)((bytes + 3) / 4),
                                      reinterpret_cast<unsigned int*>(H->blob), &H->seq, seq);
     ck(cudaGetLastError());
-    return Pub{seq, st_off, T, info, states != nullptr};
-  }
-  void wait(const Pub& pb) {
     // spin on the sequence word; every 4096 polls ask the stream whether it failed or
     // drained without publishing (then fall back to a plain synchronize)
     for (unsigned long long spin = 1;; ++spin) {
-      if (H->seq == pb.seq) break;
+      if (H->seq == seq) break;
       if ((spin & 4095u) == 0u) {
         const cudaError_t q = cudaStreamQuery(S);
         if (q != cudaSuccess && q != cudaErrorNotReady) ck(q);
-        if (q == cudaSuccess && H->seq != pb.seq) {
+        if (q == cudaSuccess && H->seq != seq) {
           ck(cudaStreamSynchronize(S));
-          if (H->seq != pb.seq) throw DriverError{SSNAL_E_DEVICE, "read-back did not publish"};
+          if (H->seq != seq) throw DriverError{SSNAL_E_DEVICE, "read-back did not publish"};
         }
       }
     }
     ++syncs;
     std::memcpy(H->scal, H->blob, sizeof(double) * NSCAL);
-    if (pb.info) std::memcpy(&H->info, H->blob + 128, sizeof(int));
-    if (pb.states) std::memcpy(H->st, H->blob + pb.st_off, sizeof(ProjState) * pb.T);
+    if (info) std::memcpy(&H->info, H->blob + 128, sizeof(int));
+    if (states) std::memcpy(H->st, H->blob + st_off, sizeof(ProjState) * T);
   }
-  void fetch(const ProjState* states, int T, bool info) { wait(publish(states, T, info)); }
 
   void project(const double* A, ProjState* st, int T, const double* B, const double* coefs,
                double* xo, uint8_t* fo, const double* ref, double hint, int newton_passes = 3,
@@ -911,19 +826,8 @@ struct Driver {
   }
 
   // [gradient, ||grad||^2] + direction + unit trial, one sync
-  // device-decided steps (dense operator): parameters of the current inner solve and
-  // the decision read back with the first batch
-  StepParams sp{};
-  bool dev_step = false;
-  int dev_code = STEP_NONE, dev_j = -1;
-  double dev_alpha = 0.0;
-  int* dev_dec() const { return reinterpret_cast<int*>(reinterpret_cast<char*>(L.scal) + 132); }
-  double* dev_alpha_ptr() const {
-    return reinterpret_cast<double*>(reinterpret_cast<char*>(L.scal) + 144);
-  }
-
   void advance(long long p, double asa, bool with_gradient, double& gnorm2, double dotsv[4],
-               ProjState& trial0, bool allow_accept = false) {
+               ProjState& trial0) {
     // dense: the accept pass already produced r = X^T s; grad = X r comes with the
     // direction's sweep
     if (with_gradient && !qgrad()) gradient(L.scal + 4);
@@ -939,34 +843,7 @@ struct Driver {
       alpha *= O.backtrack;
     }
     project(L.u, L.st_trial, T0, L.qdir, coefs, L.tx, L.tfree, L.x, lam_cur);
-    if (dev_step) {
-      // decide the step on the device and apply an accepted trial before the host even
-      // wakes up (the host follows the published decision)
-      StepParams q = sp;
-      q.T = T0;
-      q.allow = allow_accept ? 1 : 0;
-      note_launch();
-      select_step_kernel<<<1, 32, 0, S>>>(L.scal, L.st_cur, L.st_trial, q, dev_dec(),
-                                          dev_alpha_ptr());
-      ck(cudaGetLastError());
-      // publish first, then the accept pass: it runs while the host wakes up and
-      // enqueues the next direction behind it
-      const Pub pb = publish(L.st_trial, T0, p > 0);
-      timed(SSNAL_OP_VEC, 8.0 * P.n * 9 + 2.0 * P.n, [&] {
-        ck(launch_accept_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, P.n, 0.0, 0.0,
-                           L.w, L.dir, L.qw, L.qdir, L.u, L.xp, nullptr, L.fr, nullptr, L.s,
-                           tdir, L.xw, L.xpi, L.r, L.qpart, nullptr, L.st_cur, S, dev_dec(),
-                           dev_alpha_ptr(), L.tx, L.tfree, L.st_trial, sigma));
-      });
-      wait(pb);
-    } else {
-      fetch(L.st_trial, T0, p > 0);
-    }
-    if (dev_step) {
-      std::memcpy(&dev_code, H->blob + 132, sizeof(int));
-      std::memcpy(&dev_j, H->blob + 136, sizeof(int));
-      std::memcpy(&dev_alpha, H->blob + 144, sizeof(double));
-    }
+    fetch(L.st_trial, T0, p > 0);
     if (p > 0 && H->info != 0) throw DriverError{SSNAL_E_ARG, "reduced Newton matrix not SPD"};
     gnorm2 = H->scal[4];
     for (int k = 0; k < 4; ++k) dotsv[k] = H->scal[k];
@@ -1075,14 +952,10 @@ struct Driver {
     }
     cur = H->st[0];
     lam_cur = cur.lam;
-    // dense operator: Newton steps decided and applied on the device (select_step_kernel)
-    dev_step = qgrad() && std::getenv("SSNAL_HOST_STEPS") == nullptr;
-    sp = StepParams{coeff * eps_k, coeff * delta_k, floor_, sigma, O.mu, x_sq, O.backtrack,
-                    O.psi_stable, 0, 0};
     double dv[4];
     ProjState trial0;
     double unused;
-    advance(cur.nfree, cur.sum_a2_free, false, unused, dv, trial0, O.max_inner > 0);
+    advance(cur.nfree, cur.sum_a2_free, false, unused, dv, trial0);
     if (qgrad()) gnorm2 = unused;  // ||X r||^2 from the direction's sweep
     converged = false;
     bool exhausted = true;
@@ -1090,19 +963,6 @@ struct Driver {
     for (int it = 0; it < O.max_inner; ++it) {
       const double gnorm = std::sqrt(gnorm2);
       const double dist = std::sqrt(cur.sum_dref2);
-      if (dev_step && dev_code == STEP_ACCEPTED) {  // the device already took this step
-        ++newton;
-        const ProjState rec = first_batch[dev_j];
-        lam_cur = rec.lam;
-        if (dbg)
-          std::fprintf(stderr, "ssn it=%d |g|=%.3e eps=%.3e dist=%.3e alpha=%.3g steep=0 p=%lld\n",
-                       it, gnorm, coeff * eps_k, coeff * delta_k * dist, dev_alpha,
-                       (long long)cur.nfree);
-        cur = rec;
-        ++its;
-        advance(cur.nfree, cur.sum_a2_free, true, gnorm2, dv, trial0, it + 1 < O.max_inner);
-        continue;
-      }
       if (gnorm <= coeff * eps_k && gnorm <= coeff * delta_k * dist) {
         if (dbg) std::fprintf(stderr, "ssn stop it=%d criteria |g|=%.3e\n", it, gnorm);
         converged = true;
@@ -1164,7 +1024,7 @@ struct Driver {
       accept(alpha, j);
       cur = rec;
       ++its;
-      advance(cur.nfree, cur.sum_a2_free, true, gnorm2, dv, trial0, it + 1 < O.max_inner);
+      advance(cur.nfree, cur.sum_a2_free, true, gnorm2, dv, trial0);
     }
     hit_max = exhausted;
     return its;

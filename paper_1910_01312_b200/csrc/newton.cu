@@ -323,32 +323,14 @@ struct AcceptQArgs {
   // accepted trial's projection record -> current record (replaces a D2D memcpy)
   const ProjState* st_src;
   ProjState* st_dst;
-  // device-decided step (select_step_kernel, driver.cu): when dec is set, alpha / trial j
-  // come from it and code != ACCEPTED makes the whole launch a no-op
-  const int* dec;        // [code, j]
-  const double* dec_alpha;
-  const double* tx;      // trial projections [T][n] and masks [T][n] (j picks one)
-  const uint8_t* tfree;
-  const ProjState* st_trial;
-  double sigma;
 };
 
 template <int NC>
 __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
-  // (a is a by-value kernel parameter: the device-decision branch edits this block's copy)
   __shared__ int list[AQ_NT];
   __shared__ double dval[AQ_NT];
   __shared__ int wcnt[AQ_NT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (a.dec) {  // block-uniform: every CTA reads the same device decision
-    if (a.dec[0] != STEP_ACCEPTED) return;
-    const int j = a.dec[1];
-    a.alpha = *a.dec_alpha;
-    a.cu = -(a.sigma * a.alpha);
-    a.txj = a.tx + (long long)j * a.n;
-    a.tfj = a.tfree + (long long)j * a.n;
-    a.st_src = a.st_trial + j;
-  }
   if (blockIdx.x == 0 && a.st_dst && tid < (int)(sizeof(ProjState) / sizeof(unsigned int)))
     reinterpret_cast<unsigned int*>(a.st_dst)[tid] =
         reinterpret_cast<const unsigned int*>(a.st_src)[tid];
@@ -486,13 +468,9 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
                             double* xp, const double* txj, uint8_t* fr, const uint8_t* tfj,
                             double* s, const double* t, double* xw, double* xpi, double* r,
                             double* part, const ProjState* st_src, ProjState* st_dst,
-                            cudaStream_t stream, const int* dec, const double* dec_alpha,
-                            const double* tx, const uint8_t* tfree, const ProjState* st_trial,
-                            double sigma) {
+                            cudaStream_t stream) {
   if (q > (long long)AQ_NT * AQ_MAXC) return cudaErrorInvalidValue;
   AcceptQArgs a;
-  a.dec = dec; a.dec_alpha = dec_alpha; a.tx = tx; a.tfree = tfree; a.st_trial = st_trial;
-  a.sigma = sigma;
   a.g = RowsArgs{A, n_phys, q, lda, rs, svr, nullptr, 0};
   a.n = n; a.alpha = alpha; a.cu = cu;
   a.w = w; a.qw = qw; a.u = u; a.xp = xp; a.s = s; a.d = d; a.qd = qd; a.txj = txj;

@@ -18,17 +18,6 @@ enum ProjStatus {
   PROJ_INFEASIBLE_HIGH = -2,
 };
 
-// device-side Newton-step decision codes (driver.cu select_step_kernel)
-enum StepCode {
-  STEP_NONE = 0,
-  STEP_CONVERGED = 1,    // inner stopping test met: no step
-  STEP_NONDESCENT = 2,   // g'd >= 0: the host takes the steepest-descent rescue
-  STEP_RESOLUTION = 3,   // predicted decrease below psi's resolution (non-delta modes)
-  STEP_UNAPPLIED = 4,    // a first-batch trial needs more projection passes
-  STEP_NO_TRIAL = 5,     // no first-batch step length passed Armijo
-  STEP_ACCEPTED = 6,     // trial j accepted and applied on the device
-};
-
 enum ProjPhase { PHASE_RANGE = 1, PHASE_EXACT = 2, PHASE_APPLY = 4 };
 
 // ProjState is the device record ssnal_proj_state_t of the public header.
