@@ -434,22 +434,49 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
     m += tot;
     __syncthreads();
   }
-  for (long long c = tid; c < a.g.q; c += AQ_NT) {
-    double sum = 0.0;
-    int k = 0;
-    for (; k + 4 <= m; k += 4) {  // four independent loads in flight, summed in order
-      const double v0 = __ldcg(a.part + (long long)blist[k] * a.g.q + c);
-      const double v1 = __ldcg(a.part + (long long)blist[k + 1] * a.g.q + c);
-      const double v2 = __ldcg(a.part + (long long)blist[k + 2] * a.g.q + c);
-      const double v3 = __ldcg(a.part + (long long)blist[k + 3] * a.g.q + c);
-      sum = (((sum + v0) + v1) + v2) + v3;
+  // columns in chunks of 256: warp w sums the touched CTAs k = w, w + 8, ... (k order),
+  // lane l columns c0 + l + 32 i (i < 8; coalesced), two k at a time so 16 loads are in
+  // flight per lane; the 8 warp partials are then added in warp order (deterministic)
+  __shared__ double wsum[AQ_NT / 32][AQ_NT];
+  for (long long c0 = 0; c0 < a.g.q; c0 += AQ_NT) {
+    double acc8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc8[i] = 0.0;
+    int k = warp;
+    for (; k + AQ_NT / 32 < m; k += 2 * (AQ_NT / 32)) {
+      const double* p0 = a.part + (long long)blist[k] * a.g.q + c0 + lane;
+      const double* p1 = a.part + (long long)blist[k + AQ_NT / 32] * a.g.q + c0 + lane;
+      double v0[8], v1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool in = c0 + lane + 32 * i < a.g.q;
+        v0[i] = in ? __ldcg(p0 + 32 * i) : 0.0;
+        v1[i] = in ? __ldcg(p1 + 32 * i) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc8[i] = (acc8[i] + v0[i]) + v1[i];
     }
-    for (; k < m; ++k) sum += __ldcg(a.part + (long long)blist[k] * a.g.q + c);
-    const double pi = a.xpi[c] + sum;
-    const double ww = __dadd_rn(a.xw[c], __dmul_rn(a.alpha, a.t[c]));
-    a.xpi[c] = pi;
-    a.xw[c] = ww;
-    a.r[c] = ww - pi;
+    if (k < m) {
+      const double* p0 = a.part + (long long)blist[k] * a.g.q + c0 + lane;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (c0 + lane + 32 * i < a.g.q) acc8[i] += __ldcg(p0 + 32 * i);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) wsum[warp][lane + 32 * i] = acc8[i];
+    __syncthreads();
+    const long long c = c0 + tid;
+    if (c < a.g.q) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < AQ_NT / 32; ++w) sum += wsum[w][tid];
+      const double pi = a.xpi[c] + sum;
+      const double ww = __dadd_rn(a.xw[c], __dmul_rn(a.alpha, a.t[c]));
+      a.xpi[c] = pi;
+      a.xw[c] = ww;
+      a.r[c] = ww - pi;
+    }
+    __syncthreads();
   }
 }
 

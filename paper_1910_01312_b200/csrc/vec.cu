@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(SSNAL_NT) dots_kernel(DotArgs p) {
 }
 
 size_t reduce_ws_bytes(long long n) {
-  return TICKET_BYTES + (size_t)stream_blocks(n, 4) * MAXDOT * sizeof(double);
+  // capacity for the one-element-per-thread grids of the latency-bound passes
+  return TICKET_BYTES + (size_t)stream_blocks(n, 1) * MAXDOT * sizeof(double);
 }
 
 cudaError_t launch_dots(int k, const double* const* xs, const double* const* ys,
@@ -214,7 +215,8 @@ cudaError_t launch_hs_finish_dots(const uint8_t* fm, const double* a, const doub
                                   double* dots_out, void* ws, cudaStream_t stream) {
   HsDotArgs p{fm, a, y, n, beta, alpha, add, out, ay, aa, g, w, qw, dots_out,
               (unsigned int*)ws, (double*)((char*)ws + TICKET_BYTES), t, q};
-  { note_launch(); hs_finish_dots_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(p); }
+  // one slot per thread (n = 5e4: 196 CTAs): no serial grid-stride chain of loads
+  { note_launch(); hs_finish_dots_kernel<<<stream_blocks(n, 1), SSNAL_NT, 0, stream>>>(p); }
   return cudaGetLastError();
 }
 
