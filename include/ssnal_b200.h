@@ -121,7 +121,9 @@ int ssnal_dots(int k, const double* const* xs, const double* const* ys,
  * op 1: out = (x - y) - z                            -- x - Qx - c (KKT map)
  * op 2: out = x + alpha * y                          -- w + alpha d, Qw + alpha Qd
  * op 3: out = x - y                                  -- s(w) = w - Pi(u(w))
- * op 4: out = alpha * x                              */
+ * op 4: out = alpha * x
+ * op 5: out = x * y (elementwise)                    -- Jacobi preconditioner apply
+ * op 6: out = 1 / (1 + alpha * max(x - y, 0))        -- Jacobi inverse diagonal */
 int ssnal_vec(int op, int64_t n, double alpha, const double* x, const double* y,
               const double* z, double* out, void* stream);
 
@@ -199,6 +201,20 @@ int ssnal_csr_xd(const ssnal_csr_operator_t* op, const int32_t* rows, int64_t nr
 /* out = X^T v (q), v of length n; ws >= nslots doubles */
 int ssnal_csr_xt(const ssnal_csr_operator_t* op, const double* v, double* out, void* ws,
                  void* stream);
+/* out = X_J^T w for a p-vector w indexed by position in J (J = ascending rows with
+ * keep != 0, p = |J|): builds the J-restricted CSC once (count + ballot compaction)
+ * and runs the nnz-balanced segmented product on it.  The CG products of the reduced
+ * Newton system (ref solver.py:151-172) use the same two steps.  ws >=
+ * ssnal_csr_restricted_ws_bytes(op), zeroed once before first use. */
+size_t ssnal_csr_restricted_ws_bytes(const ssnal_csr_operator_t* op);
+int ssnal_csr_xt_restricted(const ssnal_csr_operator_t* op, const uint8_t* keep,
+                            const int32_t* J, int64_t p, const double* w, double* out, void* ws,
+                            void* stream);
+/* out[k] = sum_{i : keep[i] != 0} A[i,k]^2 (q): the Jacobi diagonal of X_J^T X_J for the
+ * factor-space CG (row signs square away); ws >= nslots doubles.  Replaces the diagonal
+ * the reference's CG branch would read off Q_JJ (ref solver.py:151-172, 253-258). */
+int ssnal_csr_colsq(const ssnal_csr_operator_t* op, const uint8_t* keep, double* out, void* ws,
+                    void* stream);
 
 /* ---- native SSsNAL driver ------------------------------------------------
  * The whole Algorithm 1 / Algorithm 3 loop of ref solver.py:331-530 (alm_solve,

@@ -230,6 +230,20 @@ class CudaBackend:
         self._timed("chol_solve", 16 * m * m, _lib.call, "ssnal_chol_solve", _ptr(M), int(m),
                     _ptr(b), float(scale), _ptr(x), _ptr(info), self.stream())
 
+    # ---------------------------------------------------------------- CSR operator
+    def csr_xt(self, op, v, out):
+        """out = X^T v (q) on the operator's CSC segment plan."""
+        _lib.call("ssnal_csr_xt", op._cref, _ptr(v), _ptr(out), _ptr(op.part), self.stream())
+
+    def csr_x(self, op, d, out):
+        """out = X d (n)."""
+        _lib.call("ssnal_csr_xd", op._cref, None, op.n, _ptr(d), _ptr(out), self.stream())
+
+    def csr_colsq(self, op, keep, out):
+        """out[k] = sum over rows with keep != 0 of A_ik^2 (Jacobi diagonal of X_J^T X_J)."""
+        _lib.call("ssnal_csr_colsq", op._cref, _ptr(keep), _ptr(out), _ptr(op.part),
+                  self.stream())
+
     # ---------------------------------------------------------------- sharded path
     def proj_local(self, A, box, T, lam, mode, rec, B=None, coefs=None, x_out=None,
                    free_out=None, ref=None, base=None, base_lam=0.0):

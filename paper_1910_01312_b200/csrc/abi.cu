@@ -171,8 +171,8 @@ int ssnal_dots(int k, const double* const* xs, const double* const* ys, const ui
 
 int ssnal_vec(int op, int64_t n, double alpha, const double* x, const double* y, const double* z,
               double* out, void* stream) {
-  if (op < 0 || op > 4 || n < 1 || !x || !out) return fail_arg("ssnal_vec", "op/size/null");
-  if ((op == 1 || op == 2 || op == 3 || op == 0) && !y) return fail_arg("ssnal_vec", "y required");
+  if (op < 0 || op > 6 || n < 1 || !x || !out) return fail_arg("ssnal_vec", "op/size/null");
+  if ((op == 1 || op == 2 || op == 3 || op == 0 || op >= 5) && !y) return fail_arg("ssnal_vec", "y required");
   if (op == 1 && !z) return fail_arg("ssnal_vec", "z required for op 1");
   return check("ssnal_vec", launch_vec(op, n, alpha, x, y, z, out, S(stream)));
 }
@@ -241,6 +241,30 @@ int ssnal_csr_xt(const ssnal_csr_operator_t* op, const double* v, double* out, v
   if (!csr_ok(op) || !v || !out || (op->nslots > 0 && !ws))
     return fail_arg("ssnal_csr_xt", "operator/null");
   return check("ssnal_csr_xt", launch_csc_xt(*op, v, out, (double*)ws, S(stream)));
+}
+
+size_t ssnal_csr_restricted_ws_bytes(const ssnal_csr_operator_t* op) {
+  if (!csr_ok(op)) return 0;
+  return cscj_ws_bytes(*op) + 256 + sizeof(double) * (size_t)(op->nslots + 1);
+}
+
+int ssnal_csr_xt_restricted(const ssnal_csr_operator_t* op, const uint8_t* keep,
+                            const int32_t* J, int64_t p, const double* w, double* out, void* ws,
+                            void* stream) {
+  if (!csr_ok(op) || !keep || !out || !ws || p < 0 || p > op->n || (p > 0 && (!J || !w)))
+    return fail_arg("ssnal_csr_xt_restricted", "operator/null/size");
+  const CscJ c = cscj_layout(*op, ws);
+  double* part = (double*)(((uintptr_t)ws + cscj_ws_bytes(*op) + 255) & ~(uintptr_t)255);
+  cudaError_t e = launch_cscj_build(*op, keep, J, p, c, S(stream));
+  if (e == cudaSuccess) e = launch_cscj_xt(*op, c, w, out, part, S(stream));
+  return check("ssnal_csr_xt_restricted", e);
+}
+
+int ssnal_csr_colsq(const ssnal_csr_operator_t* op, const uint8_t* keep, double* out, void* ws,
+                    void* stream) {
+  if (!csr_ok(op) || !keep || !out || (op->nslots > 0 && !ws))
+    return fail_arg("ssnal_csr_colsq", "operator/null");
+  return check("ssnal_csr_colsq", launch_csc_colsq(*op, keep, out, (double*)ws, S(stream)));
 }
 
 int ssnal_alm_solve_dense(const ssnal_dense_problem_t* problem, const ssnal_options_t* options,

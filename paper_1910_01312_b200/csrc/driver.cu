@@ -76,8 +76,6 @@ cudaError_t launch_cg_init(long long p, const double* b, double* y, double* r, d
                            double* cgs, double* part, cudaStream_t s);
 cudaError_t launch_cg_jacobi(long long q, const double* colsq, const double* u, double asa,
                              double sigma, double* dinv, cudaStream_t s);
-cudaError_t launch_csc_colsq(const CsrOp& op, const uint8_t* keep, double* out, double* part,
-                             cudaStream_t s);
 cudaError_t launch_cg_project(long long p, const double* x, const double* aJ, const double* dot,
                               double asa, double* out, cudaStream_t s);
 cudaError_t launch_cg_ap(long long p, const double* pv, const double* zq, const double* aJ,
@@ -289,9 +287,17 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
   return L;
 }
 
-void ck(cudaError_t e) {
-  if (e != cudaSuccess) throw DriverError{(int)e, cudaGetErrorString(e)};
+// SSNAL_SYNC_CHECK=1: synchronise after every checked call and name the driver line of
+// the first failure (a fault is otherwise reported at the next host decision)
+void ck_at(cudaError_t e, int line) {
+  static const int sync_check = std::getenv("SSNAL_SYNC_CHECK") ? 1 : 0;
+  if (e == cudaSuccess && sync_check) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (sync_check) std::fprintf(stderr, "ssnal driver: %s at driver.cu:%d\n", cudaGetErrorString(e), line);
+    throw DriverError{(int)e, cudaGetErrorString(e)};
+  }
 }
+#define ck(e) ck_at((e), __LINE__)
 
 // CUDA-event timing per op class (ssnal_options_t.profile); events are pooled
 struct Prof {

@@ -216,8 +216,17 @@ static int gram_ksplit(long long p, long long q) {
   return (int)max(s, 1LL);
 }
 
+// Workspace for any system order p' <= p: the split-K factor grows as p' shrinks (fewer
+// tile pairs), so the bound is the max over tile counts, each at its largest p'.
+// (Sizing with the split of p itself under-allocated p' < p: e.g. q = 400 sized at
+// p = 400 -> 11 splits, but p' = 380 takes 13 and its partial tiles ran past the end.)
 size_t pspace_ws_bytes(long long p, long long q) {
-  return (size_t)((gram_ksplit(p, q) + 1) * p * p + 4 * p + GX_SPLIT * q + 64) * sizeof(double);
+  long long worst = 0;
+  for (long long nt = 1; nt <= ceil_div(max(p, 1LL), (long long)RT); ++nt) {
+    const long long pp = min(p, nt * RT);
+    worst = max(worst, (gram_ksplit(pp, q) + 1) * pp * pp);
+  }
+  return (size_t)(worst + 4 * p + GX_SPLIT * q + 64) * sizeof(double);
 }
 
 // Given Q_JJ (p x p, overwritten): y = P_J (I + sigma P_J Q_JJ P_J)^{-1} P_J grad_J.

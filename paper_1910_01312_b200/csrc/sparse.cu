@@ -20,6 +20,10 @@ namespace ssnal {
 static constexpr int SUB = 8;  // lanes per row in X d
 
 // out[r] = rs[i] * sum_k val[k] d[col[k]],  i = rows ? rows[r] : r  (r < nrows)
+// Each lane sums entries sl, sl + SUB, sl + 2 SUB, ... of its row in order; the index /
+// value loads of XD_UNROLL such entries are issued before their gathers (predicated),
+// so a 30-50 nnz row is one or two rounds of independent loads instead of a chain.
+static constexpr int XD_UNROLL = 4;
 __global__ void __launch_bounds__(256) csr_xd_kernel(const int64_t* __restrict__ indptr,
                                                      const int32_t* __restrict__ indices,
                                                      const double* __restrict__ values,
@@ -30,10 +34,23 @@ __global__ void __launch_bounds__(256) csr_xd_kernel(const int64_t* __restrict__
   const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / SUB;
   const int sl = threadIdx.x & (SUB - 1);
   if (g >= nrows) return;
-  const long long i = rows ? (long long)rows[g] : g;
-  const long long k0 = indptr[i], k1 = indptr[i + 1];
+  const long long i = rows ? (long long)__ldg(rows + g) : g;
+  const long long k0 = __ldg(indptr + i), k1 = __ldg(indptr + i + 1);
   double s = 0.0;
-  for (long long k = k0 + sl; k < k1; k += SUB) s = fma(values[k], __ldg(d + indices[k]), s);
+  for (long long kb = k0 + sl; kb < k1; kb += XD_UNROLL * SUB) {
+    int idx[XD_UNROLL];
+    double v[XD_UNROLL];
+#pragma unroll
+    for (int u = 0; u < XD_UNROLL; ++u) {
+      const long long k = kb + u * SUB;
+      const bool ok = k < k1;
+      idx[u] = ok ? __ldg(indices + k) : 0;
+      v[u] = ok ? __ldg(values + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < XD_UNROLL; ++u)
+      if (kb + u * SUB < k1) s = fma(v[u], __ldg(d + idx[u]), s);
+  }
 #pragma unroll
   for (int o = SUB / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, SUB);
   if (sl == 0) out[g] = rs ? rs[i] * s : s;
@@ -344,7 +361,7 @@ __global__ void __launch_bounds__(CJ_WARPS * 32) cscj_fill_kernel(
     const double* __restrict__ rs, const uint8_t* __restrict__ keep,
     const int32_t* __restrict__ posJ, const int* __restrict__ cnt,
     const long long* __restrict__ blk, int64_t* __restrict__ jbeg, int64_t* __restrict__ jend,
-    int32_t* __restrict__ jpos, double* __restrict__ jval) {
+    int32_t* __restrict__ jpos, double* __restrict__ jval, int32_t* __restrict__ jseg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long s = (long long)blockIdx.x * CJ_WARPS + warp;
   if (s >= nseg) return;
@@ -368,6 +385,7 @@ __global__ void __launch_bounds__(CJ_WARPS * 32) cscj_fill_kernel(
       const long long o = off + __popc(bal & ((1u << lane) - 1u));
       jpos[o] = posJ[r];
       jval[o] = rs ? valt[k] * rs[r] : valt[k];
+      jseg[o] = (int32_t)s;
     }
     off += __popc(bal);
   }
@@ -380,37 +398,184 @@ __global__ void index_map_kernel(const int32_t* __restrict__ J, long long p,
   if (r < p) pos[J[r]] = (int32_t)r;
 }
 
-// out = X_J^T w on the J-restricted CSC (w indexed by position in J)
+// out = X_J^T w on the J-restricted CSC (w indexed by position in J), nnz-balanced:
+// the kept entries are cut into CH-entry chunks, one warp per chunk, CH_E consecutive
+// entries per lane.  Each lane runs a sequential segmented sum over its entries
+// (segment ids from cscj_fill), the lanes' open partials are joined by a warp
+// segmented scan, and a segment that crosses a chunk boundary leaves its chunk
+// partials in cval / ctail for cscj_fix_kernel, which adds them in chunk order.
+// Zipf data leave most of the ~1e6 column segments with 0-3 kept entries, where a
+// warp per segment ran at ~1/10 of the HBM rate; here every lane streams CH_E entries.
+// Fixed chunking => fixed summation order: deterministic run to run.
+static constexpr int CH_E = 8;
+static constexpr int CH = 32 * CH_E;
+
+__device__ __forceinline__ void seg_write(int s, double v, const int32_t* __restrict__ seg_col,
+                                          const int32_t* __restrict__ seg_slot,
+                                          double* __restrict__ out, double* __restrict__ part) {
+  const int slot = seg_slot[s];
+  if (slot < 0) out[seg_col[s]] = v;
+  else part[slot] = v;
+}
+
 __global__ void __launch_bounds__(256) cscj_xt_kernel(
-    const int64_t* __restrict__ jbeg, const int64_t* __restrict__ jend,
-    const int32_t* __restrict__ seg_col, const int32_t* __restrict__ seg_slot, long long nseg,
+    const long long* __restrict__ total, const int32_t* __restrict__ jseg,
     const int32_t* __restrict__ jpos, const double* __restrict__ jval,
-    const double* __restrict__ w, double* __restrict__ out, double* __restrict__ part) {
-  const long long s = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int32_t* __restrict__ seg_col, const int32_t* __restrict__ seg_slot,
+    const double* __restrict__ w, double* __restrict__ out, double* __restrict__ part,
+    double* __restrict__ cval, double* __restrict__ ctail, uint8_t* __restrict__ cflag) {
+  const long long nnz = *total;
+  const long long nch = (nnz + CH - 1) / CH;
   const int lane = threadIdx.x & 31;
-  if (s >= nseg) return;
-  const long long k0 = jbeg[s], k1 = jend[s];
-  double acc = 0.0;
-  for (long long k = k0 + lane; k < k1; k += 32) acc = fma(jval[k], __ldg(w + jpos[k]), acc);
-  acc = warp_sum(acc);
-  if (lane == 0) {
-    const int slot = seg_slot[s];
-    if (slot < 0) out[seg_col[s]] = acc;
-    else part[slot] = acc;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  constexpr int NONE = 0x7fffffff;
+  for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nch; c += nw) {
+    const long long c0 = c * CH, e0 = c0 + lane * CH_E;
+    // the chunk's first segment F continues from the previous chunk?
+    const int F = jseg[c0];
+    const bool chunk_in = c0 > 0 && jseg[c0 - 1] == F;
+    const int next = c0 + CH < nnz ? jseg[c0 + CH] : NONE;
+    int sg[CH_E];
+    double pr[CH_E];
+    {
+      const int4* s4 = reinterpret_cast<const int4*>(jseg + e0);
+      const int4* p4 = reinterpret_cast<const int4*>(jpos + e0);
+      const double2* v2 = reinterpret_cast<const double2*>(jval + e0);
+      int ps[CH_E];
+      double vv[CH_E];
+#pragma unroll
+      for (int h = 0; h < CH_E / 4; ++h) {
+        const int4 a = __ldg(s4 + h), b = __ldg(p4 + h);
+        sg[4 * h] = a.x; sg[4 * h + 1] = a.y; sg[4 * h + 2] = a.z; sg[4 * h + 3] = a.w;
+        ps[4 * h] = b.x; ps[4 * h + 1] = b.y; ps[4 * h + 2] = b.z; ps[4 * h + 3] = b.w;
+      }
+#pragma unroll
+      for (int h = 0; h < CH_E / 2; ++h) {
+        const double2 v = __ldg(v2 + h);
+        vv[2 * h] = v.x; vv[2 * h + 1] = v.y;
+      }
+      // gathers of w after all index loads are in flight
+      double wg[CH_E];
+#pragma unroll
+      for (int u = 0; u < CH_E; ++u) {
+        const bool ok = e0 + u < nnz;
+        if (!ok) sg[u] = NONE;
+        pr[u] = ok ? vv[u] : 0.0;
+        wg[u] = ok ? __ldg(w + ps[u]) : 0.0;
+      }
+      // sequential segmented sums over the lane's entries
+      const int head = sg[0];
+      int cur = sg[0];
+      double run = 0.0, hsum = 0.0;
+      bool single = true;
+#pragma unroll
+      for (int u = 0; u < CH_E; ++u) {
+        if (sg[u] != cur) {
+          if (single) {
+            hsum = run;
+            single = false;
+          } else if (cur != NONE) {
+            seg_write(cur, run, seg_col, seg_slot, out, part);  // started and ended in lane
+          }
+          cur = sg[u];
+          run = 0.0;
+        }
+        run = fma(pr[u], wg[u], run);
+      }
+      // warp segmented inclusive scan of the open tails (cur, run)
+      const int prevK = __shfl_up_sync(0xffffffffu, cur, 1);
+      bool reset = lane == 0 || !single || prevK != cur;
+      double S = run;
+      {
+        bool r = reset;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double vs = __shfl_up_sync(0xffffffffu, S, o);
+          const bool rs_ = __shfl_up_sync(0xffffffffu, r, o);
+          if (lane >= o && !r) {
+            S += vs;
+            r = rs_;
+          }
+        }
+      }
+      const double prevS = __shfl_up_sync(0xffffffffu, S, 1);
+      const int nextHead = __shfl_down_sync(0xffffffffu, head, 1);
+      bool wrote_close = false;
+      // (a) a head segment that closes inside this lane (lane holds >= 2 segments)
+      if (!single && head != NONE) {
+        const double tot = (lane > 0 && prevK == head) ? prevS + hsum : hsum;
+        if (chunk_in && head == F) {
+          cval[c] = tot;
+          wrote_close = true;
+        } else {
+          seg_write(head, tot, seg_col, seg_slot, out, part);
+        }
+      }
+      // (b) the lane's tail segment: closes at the lane end unless the next lane (or the
+      // next chunk) continues it
+      bool owns_tail = false;
+      if (cur != NONE) {
+        const bool cont = lane < 31 ? (nextHead == cur) : (next == cur);
+        if (!cont) {
+          if (chunk_in && cur == F) {
+            cval[c] = S;
+            wrote_close = true;
+          } else {
+            seg_write(cur, S, seg_col, seg_slot, out, part);
+          }
+        } else if (lane == 31) {
+          if (chunk_in && cur == F) {
+            cval[c] = S;  // F spans the whole chunk and continues
+          } else {
+            ctail[c] = S;
+            owns_tail = true;
+          }
+        }
+      }
+      const unsigned cl = __ballot_sync(0xffffffffu, wrote_close);
+      const unsigned ot = __ballot_sync(0xffffffffu, owns_tail);
+      if (lane == 0) cflag[c] = (uint8_t)((cl ? 1 : 0) | (ot ? 2 : 0));
+    }
+  }
+}
+
+// segments that cross chunk boundaries: tail partial + the following chunks' first-
+// segment partials, in chunk order, up to the chunk where the segment closes
+__global__ void __launch_bounds__(256) cscj_fix_kernel(
+    const long long* __restrict__ total, const int32_t* __restrict__ jseg,
+    const int32_t* __restrict__ seg_col, const int32_t* __restrict__ seg_slot,
+    const double* __restrict__ cval, const double* __restrict__ ctail,
+    const uint8_t* __restrict__ cflag, double* __restrict__ out, double* __restrict__ part) {
+  const long long nnz = *total;
+  const long long nch = (nnz + CH - 1) / CH;
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < nch;
+       c += (long long)gridDim.x * blockDim.x) {
+    if (!(cflag[c] & 2)) continue;
+    double t = ctail[c];
+    for (long long d = c + 1; d < nch; ++d) {
+      t += cval[d];
+      if (cflag[d] & 1) break;
+    }
+    seg_write(jseg[c * CH + CH - 1], t, seg_col, seg_slot, out, part);
   }
 }
 
 size_t cscj_ws_bytes(const CsrOp& op) {
   const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
+  const long long cap = op.nnz + CH;  // vector loads of the last chunk stay inside
+  const long long nch = ceil_div(cap, (long long)CH);
   return 256 + sizeof(int32_t) * (size_t)op.n + sizeof(int) * (size_t)op.nseg +
          sizeof(long long) * (size_t)(nblk + 1) + 2 * sizeof(int64_t) * (size_t)op.nseg +
-         (sizeof(int32_t) + sizeof(double)) * (size_t)op.nnz + 8 * 256;
+         (2 * sizeof(int32_t) + sizeof(double)) * (size_t)cap + (2 * sizeof(double) + 1) * nch +
+         12 * 256;
 }
 
 static char* al256(char* p) { return (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255); }
 
 CscJ cscj_layout(const CsrOp& op, void* ws) {
   const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
+  const long long cap = op.nnz + CH;
+  const long long nch = ceil_div(cap, (long long)CH);
   CscJ c;
   char* p = al256((char*)ws);
   c.ticket = (unsigned int*)p; p = al256(p + 256);
@@ -419,8 +584,12 @@ CscJ cscj_layout(const CsrOp& op, void* ws) {
   c.blk = (long long*)p; p = al256(p + sizeof(long long) * (nblk + 1));
   c.beg = (int64_t*)p; p = al256(p + sizeof(int64_t) * op.nseg);
   c.end = (int64_t*)p; p = al256(p + sizeof(int64_t) * op.nseg);
-  c.pos = (int32_t*)p; p = al256(p + sizeof(int32_t) * op.nnz);
-  c.val = (double*)p;
+  c.pos = (int32_t*)p; p = al256(p + sizeof(int32_t) * cap);
+  c.seg = (int32_t*)p; p = al256(p + sizeof(int32_t) * cap);
+  c.val = (double*)p; p = al256(p + sizeof(double) * cap);
+  c.cval = (double*)p; p = al256(p + sizeof(double) * nch);
+  c.ctail = (double*)p; p = al256(p + sizeof(double) * nch);
+  c.cflag = (uint8_t*)p;
   return c;
 }
 
@@ -435,15 +604,28 @@ cudaError_t launch_cscj_build(const CsrOp& op, const uint8_t* keep, const int32_
   note_launch();
   cscj_fill_kernel<<<(unsigned)nblk, CJ_WARPS * 32, 0, stream>>>(
       op.seg_beg, op.seg_end, op.nseg, op.rowidx, op.valt, op.row_sign, keep, c.posJ, c.cnt,
-      c.blk, c.beg, c.end, c.pos, c.val);
+      c.blk, c.beg, c.end, c.pos, c.val, c.seg);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cscj_xt(const CsrOp& op, const CscJ& c, const double* w, double* out,
                            double* part, cudaStream_t stream) {
+  const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
+  const long long* total = c.blk + nblk;  // kept entries (cscj_count_kernel)
+  // segments without kept entries are never visited: start from zero
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * op.q, stream);
+  if (e == cudaSuccess && op.nslots > 0)
+    e = cudaMemsetAsync(part, 0, sizeof(double) * op.nslots, stream);
+  if (e != cudaSuccess) return e;
+  const long long nch_max = ceil_div(op.nnz, (long long)CH);
+  const unsigned grid = (unsigned)std::max(1LL, std::min(ceil_div(nch_max, 8LL), 148LL * 8));
   note_launch();
-  cscj_xt_kernel<<<(unsigned)ceil_div(op.nseg * 32, 256LL), 256, 0, stream>>>(
-      c.beg, c.end, op.seg_col, op.seg_slot, op.nseg, c.pos, c.val, w, out, part);
+  cscj_xt_kernel<<<grid, 256, 0, stream>>>(total, c.seg, c.pos, c.val, op.seg_col, op.seg_slot,
+                                           w, out, part, c.cval, c.ctail, c.cflag);
+  note_launch();
+  cscj_fix_kernel<<<(unsigned)std::max(1LL, std::min(ceil_div(nch_max, 256LL), 148LL * 4)), 256,
+                    0, stream>>>(total, c.seg, op.seg_col, op.seg_slot, c.cval, c.ctail, c.cflag,
+                                 out, part);
   if (op.nfold > 0) {
     note_launch();
     csc_fold_kernel<<<(unsigned)ceil_div(op.nfold, 256LL), 256, 0, stream>>>(

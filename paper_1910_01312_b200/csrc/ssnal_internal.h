@@ -28,6 +28,8 @@ cudaError_t launch_csr_xd(const CsrOp& op, const int32_t* rows, long long nrows,
                           double* out, cudaStream_t stream);
 cudaError_t launch_csc_xt(const CsrOp& op, const double* v, double* out, double* part,
                           cudaStream_t stream);
+cudaError_t launch_csc_colsq(const CsrOp& op, const uint8_t* keep, double* out, double* part,
+                             cudaStream_t s);
 cudaError_t launch_fill(double* dst, long long n, double v, cudaStream_t stream);
 cudaError_t launch_scatter(const int32_t* rows, long long p, const double* src, double* dst,
                            cudaStream_t stream);
@@ -43,6 +45,9 @@ struct CscJ {
   int64_t *beg, *end;
   int32_t* pos;    // row slot in J per kept entry
   double* val;     // signed values
+  int32_t* seg;    // segment id per kept entry (nnz-balanced product)
+  double *cval, *ctail;  // per 256-entry chunk: first-segment / open-tail partial sums
+  uint8_t* cflag;        // bit 0: first segment closes in the chunk; bit 1: owns an open tail
 };
 size_t cscj_ws_bytes(const CsrOp& op);
 CscJ cscj_layout(const CsrOp& op, void* ws);

@@ -93,6 +93,8 @@ __global__ void vec_kernel(int op, long long n, double alpha, const double* __re
       case 1: r = __dsub_rn(__dsub_rn(x[i], y[i]), z[i]); break;
       case 2: r = __dadd_rn(x[i], __dmul_rn(alpha, y[i])); break;
       case 3: r = __dsub_rn(x[i], y[i]); break;
+      case 5: r = __dmul_rn(x[i], y[i]); break;
+      case 6: r = 1.0 / (1.0 + alpha * fmax(x[i] - y[i], 0.0)); break;
       default: r = __dmul_rn(alpha, x[i]); break;
     }
     out[i] = r;

@@ -195,21 +195,17 @@ class CsrKernelOperator:
         self.host_csr = A  # kept for callers (oracle checks, columns())
 
     def xt(self, vs, out=None):
-        from . import _lib
-
+        """X^T v_j on the CSC plan (through the backend, so a sharded backend can sum
+        the rank partials)."""
         out = out if out is not None else self.backend.empty((len(vs), self.q))
         for j, v in enumerate(vs):
-            _lib.call("ssnal_csr_xt", self._cref, v.data_ptr(), out[j].data_ptr(),
-                      self.part.data_ptr(), self.backend.stream())
+            self.backend.csr_xt(self, v, out[j])
         return out
 
     def x(self, d, out=None, k=1):
-        from . import _lib
-
         out = out if out is not None else self.backend.empty((k, self.n))
         for j in range(k):
-            _lib.call("ssnal_csr_xd", self._cref, None, self.n, d[j].data_ptr(),
-                      out[j].data_ptr(), self.backend.stream())
+            self.backend.csr_x(self, d[j], out[j])
         return out
 
     def matvec(self, v):

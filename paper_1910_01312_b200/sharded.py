@@ -116,6 +116,14 @@ class ShardedBackend:
         self.base.dense_xt(op, vs, out)
         self.allsum(out[: len(vs)])
 
+    def csr_xt(self, op, v, out):
+        self.base.csr_xt(op, v, out)
+        self.allsum(out)
+
+    def csr_colsq(self, op, keep, out):
+        self.base.csr_colsq(op, keep, out)
+        self.allsum(out)
+
     def _fold(self, rec_dev, T, mode):
         """All-gather the (T, 8) shard records and fold them in rank order (host)."""
         g = self.comm.all_gather(rec_dev[: 8 * T]).cpu().numpy().reshape(self.comm.world, T, 8)
@@ -223,6 +231,8 @@ class ShardedEngine(_Engine):
     def direction(self, p, sigma, asa=0.0):
         if p == 0:
             return super().direction(p, sigma, asa)
+        if self.op.kind == "csr":
+            return self._direction_cg(p, sigma, asa)
         be, base, op = self.be, self.be.base, self.op
         if self.q > self.pb_direct_limit():
             raise InternalError("q x q system larger than direct_solve_threshold")
@@ -245,6 +255,108 @@ class ShardedEngine(_Engine):
                            self.dir)
         be.dots([(self.grad, self.dir), (self.w, self.qw), (self.w, self.qdir)], self.scal)
         be.dots([(self.t[0], None)], self.scal[3:4], replicated=True)
+
+
+    # ------------------------------------------------------------ sparse operator
+    CG_BATCH = 16        # iterations between true-residual checks (csrc/driver.cu)
+    SPARSE_CG_ETA = 1e-4  # forcing-term cap of the matrix-free route
+
+    def _cg_buffers(self):
+        if getattr(self, "_cgq", None) is None:
+            e = self.be.empty
+            self._cgq = {k: e(self.q) for k in ("u", "uu", "dinv", "y", "r", "z", "pv", "gq",
+                                                 "tq")}
+            self._cgn = {k: e(self.n) for k in ("zn", "wn")}
+        return self._cgq, self._cgn
+
+    def _gram_apply(self, v, out):
+        """out = X_J^T X_J v (global q-vector; the rank-one term is applied by the
+        caller): X v and the free-row mask are rank-local, X^T is all-gathered."""
+        base, op = self.be.base, self.op
+        _, nb = self._cg_buffers()
+        op.x(v.view(1, -1), nb["zn"].view(1, -1), k=1)
+        base.hs_apply_coef(self.free, self.box.a_dev, nb["zn"], 1.0, None, 0.0, 0.0, nb["wn"])
+        op.xt([nb["wn"]], out.view(1, -1))
+
+    def _direction_cg(self, p, sigma, asa):
+        """Factor-space Jacobi-preconditioned CG of csrc/driver.cu cg_direction_q over row
+        shards: (I_q + sigma X_J^T P_J X_J) t = -X^T s.  The q-vectors are replicated
+        (every X^T product is rank-summed in rank order), so the CG scalars are the same
+        on every rank; one all-gather of a q-vector per iteration.  Stopping test on the
+        TRUE Newton residual sigma X X_J^T P X_J r every CG_BATCH iterations against
+        min(eta, ||grad||^(1+tau)) (ref solver.py:229, eta capped as the driver)."""
+        be, base, op = self.be, self.be.base, self.op
+        qb, nb = self._cg_buffers()
+        inv_asa = 1.0 / asa if asa != 0.0 else 0.0
+        # u = X_J^T a_J; Jacobi dinv = 1 / (1 + sigma max(colsq_J - u^2/a'a, 0))
+        base.hs_apply_coef(self.free, self.box.a_dev, self.box.a_dev, 1.0, None, 0.0, 0.0,
+                           self.am)
+        op.xt([self.am], qb["u"].view(1, -1))
+        be.csr_colsq(op, self.free, qb["z"])
+        base.vec(5, 0.0, qb["u"], qb["u"], None, qb["uu"])
+        base.vec(4, inv_asa, qb["uu"], None, None, qb["uu"])
+        base.vec(6, sigma, qb["z"], qb["uu"], None, qb["dinv"])
+        # y = 0, r = b = -X^T s, z = D^-1 r, pv = z
+        base.vec(4, 0.0, qb["u"], None, None, qb["y"])
+        base.vec(4, -1.0, self.gr[0], None, None, qb["r"])
+        base.vec(5, 0.0, qb["dinv"], qb["r"], None, qb["z"])
+        qb["pv"].copy_(qb["z"])
+        be.dots([(qb["r"], qb["z"]), (qb["r"], None)], self.scal[8:10], replicated=True)
+        be.dots([(self.grad, None)], self.scal[11:12])
+        sc, _ = self.fetch()
+        rz, rr = float(sc[8]), float(sc[9])
+        gnorm = math.sqrt(max(float(sc[11]), 0.0))
+        tol = min(min(self.cg_eta, self.SPARSE_CG_ETA), gnorm ** (1.0 + self.cg_tau))
+        done = rr == 0.0
+        it = 0
+        max_it = 4 * self.cg_max_iters
+        while not done and it < max_it:
+            for _ in range(self.CG_BATCH):
+                if it >= max_it:
+                    break
+                it += 1
+                self._gram_apply(qb["pv"], qb["gq"])
+                be.dots([(qb["pv"], None), (qb["pv"], qb["gq"]), (qb["u"], qb["pv"])],
+                        self.scal[8:11], replicated=True)
+                sc, _ = self.fetch()
+                c = float(sc[10]) * inv_asa
+                pap = float(sc[8]) + sigma * (float(sc[9]) - c * float(sc[10]))
+                alpha = rz / pap if pap > 0.0 else 0.0
+                base.vec(2, alpha, qb["y"], qb["pv"], None, qb["y"])
+                # r -= alpha (pv + sigma (gq - c u))
+                base.vec(2, -alpha, qb["r"], qb["pv"], None, qb["r"])
+                base.vec(2, -alpha * sigma, qb["r"], qb["gq"], None, qb["r"])
+                base.vec(2, alpha * sigma * c, qb["r"], qb["u"], None, qb["r"])
+                base.vec(5, 0.0, qb["dinv"], qb["r"], None, qb["z"])
+                be.dots([(qb["r"], qb["z"]), (qb["r"], None)], self.scal[8:10], replicated=True)
+                sc, _ = self.fetch()
+                rz_new = float(sc[8])
+                beta = rz_new / rz if rz != 0.0 else 0.0
+                rz = rz_new
+                base.vec(2, beta, qb["z"], qb["pv"], None, qb["pv"])
+            # true Newton residual: sigma X (X_J^T P X_J r)
+            self._gram_apply(qb["r"], qb["gq"])
+            be.dots([(qb["u"], qb["r"])], self.scal[8:9], replicated=True)
+            sc, _ = self.fetch()
+            base.vec(2, -float(sc[8]) * inv_asa, qb["gq"], qb["u"], None, qb["tq"])
+            op.x(qb["tq"].view(1, -1), nb["zn"].view(1, -1), k=1)
+            be.dots([(nb["zn"], None)], self.scal[8:9])
+            sc, _ = self.fetch()
+            done = sigma * math.sqrt(max(float(sc[8]), 0.0)) <= tol
+        self.counters["cg_iters"] = self.counters.get("cg_iters", 0) + it
+        self.t[0].copy_(qb["y"])
+        # d = -s - sigma P_J(X t) with the global coefficient a_J'(X t)_J / a_J'a_J
+        op.x(self.t, self.qdir.view(1, -1), k=1)
+        be.dots([(self.box.a_dev, self.qdir)], self.scal[8:9], mask=self.free)
+        sc, _ = self.fetch()
+        coef = float(sc[8]) * inv_asa
+        base.hs_apply_coef(self.free, self.box.a_dev, self.qdir, -sigma, self.s, -1.0, coef,
+                           self.dir)
+        # inexact t: the exact image Qd = X (X^T d) keeps Qw = Q w (as the driver)
+        op.xt([self.dir], self.gr[1:2])
+        op.x(self.gr[1:2], self.qdir.view(1, -1), k=1)
+        be.dots([(self.grad, self.dir), (self.w, self.qw), (self.w, self.qdir)], self.scal)
+        be.dots([(self.gr[1], None)], self.scal[3:4], replicated=True)
 
 
 class ShardedQpProblem(QpProblem):
@@ -278,7 +390,14 @@ def build_csvc_dual_sharded(features, labels, C, comm, backend=None):
         raise InputError("C must be positive")
     n_loc = y.shape[0]
     sizes = comm.all_gather_objects(n_loc)
-    op = LinearKernelOperator(features, labels=y, backend=be)
+    from .svm import _is_sparse
+
+    if _is_sparse(features):  # CSR rows of this shard (BASELINE configs 3, 4)
+        from .operators import CsrKernelOperator
+
+        op = CsrKernelOperator(features, labels=y, backend=be)
+    else:
+        op = LinearKernelOperator(features, labels=y, backend=be)
     box = BoxLineSet(a=y, d=0.0, l=np.zeros(n_loc), u=np.full(n_loc, float(C)), backend=be)
     lo = int(sum(sizes[: comm.rank]))
     return ShardedQpProblem(op, -np.ones(n_loc), box, 0.0, comm,

@@ -179,7 +179,7 @@ class _Engine:
         self.pcount = be.zeros(1, torch.int64)
         self.gr = e((2, q))
         self.t = e((1, q))
-        self.M = e((q, q))
+        self._M = None  # q x q system, allocated on first use (q may be 1e6 for CSR)
         self.m1 = e(q)
         self.scal = be.zeros(16)
         self.info = be.zeros(1, torch.int32)
@@ -197,6 +197,12 @@ class _Engine:
         self.backtrack = 0.5
         self.lam_kkt = 0.0  # warm starts for the multiplier search
         self.lam_cur = 0.0
+
+    @property
+    def M(self):
+        if self._M is None:
+            self._M = self.be.empty((self.q, self.q))
+        return self._M
 
     # ------------------------------------------------------------ host reads
     def fetch(self, states=None, T=1, info=False):
@@ -456,6 +462,7 @@ def ssn_solve(state, problem, alm_opts, ssn_opts, eps_k, delta_k, trace=None):
     eng._direct_limit = ssn_opts.direct_solve_threshold
     eng.line_search_batch = ssn_opts.line_search_batch
     eng.backtrack = ssn_opts.backtrack
+    eng.cg_eta, eng.cg_tau, eng.cg_max_iters = ssn_opts.eta, ssn_opts.tau, ssn_opts.cg_max_iters
     delta = ssn_opts.psi_eval == "delta"
     eng.psi_delta = delta
     sigma = state.sigma
@@ -538,6 +545,8 @@ def _native_ok(problem, alm_opts, ssn_opts):
     from .operators import CsrKernelOperator, LinearKernelOperator
 
     if isinstance(problem.q_op, CsrKernelOperator):
+        if getattr(problem, "comm", None) is not None:  # row-sharded: sharded.ShardedEngine
+            return False
         if not (alm_opts.eps_seq is _half_powers and alm_opts.delta_seq is _half_powers):
             raise InputError("the sparse operator runs only in the native driver, which uses "
                              "the reference's default eps/delta sequences")

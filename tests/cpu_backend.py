@@ -112,6 +112,10 @@ class CpuTestBackend:
             r = xv + alpha * y.numpy()
         elif op == 3:
             r = xv - y.numpy()
+        elif op == 5:
+            r = xv * y.numpy()
+        elif op == 6:
+            r = 1.0 / (1.0 + alpha * np.maximum(xv - y.numpy(), 0.0))
         else:
             r = alpha * xv
         out.copy_(torch.from_numpy(np.ascontiguousarray(r)))
@@ -129,6 +133,29 @@ class CpuTestBackend:
         idx = np.flatnonzero(mask.numpy())
         idx_out[: idx.size] = torch.from_numpy(idx.astype(np.int32))
         count_out[0] = idx.size
+
+    # CSR operator --------------------------------------------------------------
+    @staticmethod
+    def _csr_signed(op):
+        A = op.host_csr
+        if op.row_sign is not None:
+            import scipy.sparse as sp
+            A = sp.diags(op.row_sign.cpu().numpy()) @ A
+        return A.tocsr()
+
+    def csr_xt(self, op, v, out):
+        self._count("csr_xt")
+        out.copy_(torch.from_numpy(np.ascontiguousarray(self._csr_signed(op).T @ v.numpy())))
+
+    def csr_x(self, op, d, out):
+        self._count("csr_x")
+        out.copy_(torch.from_numpy(np.ascontiguousarray(self._csr_signed(op) @ d.numpy())))
+
+    def csr_colsq(self, op, keep, out):
+        self._count("csr_colsq")
+        A = op.host_csr
+        k = keep.numpy().astype(np.float64)
+        out.copy_(torch.from_numpy(np.ascontiguousarray(A.multiply(A).T @ k)))
 
     # dense operator ------------------------------------------------------------
     @staticmethod

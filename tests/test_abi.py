@@ -36,3 +36,22 @@ def test_no_cpu_fallback_without_cuda():
 
     with pytest.raises(CudaUnavailableError):
         default_backend()
+
+
+def test_pspace_workspace_bounds_every_smaller_system():
+    """ssnal_pspace_ws_bytes(p, q) must cover every system order p' <= p: the split-K
+    factor of the row Gram grows as p' shrinks (regression: sized at p = q = 400 the
+    workspace was 0.8 MB short for p' = 380, whose partial tiles then ran past it)."""
+    from paper_1910_01312_b200 import _lib
+
+    lib = _lib.load()
+
+    def need(p, q):  # csrc/newton.cu gram_ksplit + launch_pspace_direction layout
+        nt = -(-p // 64)
+        pairs = nt * (nt + 1) // 2
+        s = max(1, min(-(-296 // pairs), -(-q // 32), 16))
+        return ((s + 1) * p * p + 4 * p + 16 * q + 64) * 8
+
+    for q in (50, 300, 400, 1000, 2048):
+        have = lib.ssnal_pspace_ws_bytes(q, q)
+        assert all(have >= need(p, q) for p in range(1, q + 1)), q

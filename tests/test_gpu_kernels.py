@@ -271,6 +271,55 @@ def test_csr_products(pkg, n, q, nnz_row, zipf):
         assert op.nslots > 0  # hot columns were split
 
 
+@pytest.mark.parametrize("keep_frac", [0.0, 0.004, 0.16, 0.7, 1.0])
+def test_csr_restricted_products(pkg, keep_frac):
+    """X_J^T w on the J-restricted CSC (nnz-balanced chunked segmented sums, chunk-
+    crossing segments fixed up in order, split hot columns folded) and X_J d over a
+    row list, against scipy.  One column sits in every row (20,000 entries: ten
+    2048-entry segments, each spanning several 256-entry chunks); Zipf columns give
+    long runs of 0-3-entry segments; J from empty to all rows."""
+    import ctypes
+
+    import scipy.sparse as sp
+
+    from paper_1910_01312_b200 import _lib
+    from paper_1910_01312_b200.operators import CsrKernelOperator
+
+    rng = np.random.default_rng(int(keep_frac * 1000) + 7)
+    n, q, k = 20000, 5000, 12
+    rows = np.repeat(np.arange(n), k)
+    cols = np.minimum(rng.zipf(1.1, size=n * k) - 1, q - 1)
+    cols[::k] = 17  # the all-rows column
+    A = sp.csr_matrix((rng.standard_normal(rows.size), (rows, cols)), shape=(n, q))
+    A.sum_duplicates()
+    y = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+    op = CsrKernelOperator(A, labels=y)
+    X = (sp.diags(y) @ A).tocsr()
+    keep = (rng.random(n) < keep_frac).astype(np.uint8)
+    J = np.flatnonzero(keep).astype(np.int32)
+    p = J.size
+    w = rng.standard_normal(max(p, 1))
+    be = pkg.default_backend()
+    ws = be.zeros(int(_lib.load().ssnal_csr_restricted_ws_bytes(op._cref)), torch.uint8)
+    out = be.empty(q)
+    keep_d, J_d, w_d = _dev(keep, torch.uint8), _dev(np.r_[J, 0].astype(np.int32), torch.int32), _dev(w)
+    for _ in range(2):  # the second call reuses the workspace (stale entries past nnz_J)
+        _lib.call("ssnal_csr_xt_restricted", op._cref, keep_d.data_ptr(), J_d.data_ptr(), p,
+                  w_d.data_ptr(), out.data_ptr(), ws.data_ptr(), be.stream())
+        ref = X[J].T @ w[:p] if p else np.zeros(q)
+        scale = 1e-12 * (float((abs(X[J]).T @ np.abs(w[:p])).max()) if p else 1.0)
+        np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-12, atol=scale)
+        w = rng.standard_normal(max(p, 1))
+        w_d = _dev(w)
+    d = rng.standard_normal(q)
+    zo = be.empty(max(p, 1))
+    if p:
+        _lib.call("ssnal_csr_xd", op._cref, J_d.data_ptr(), p, _dev(d).data_ptr(), zo.data_ptr(),
+                  be.stream())
+        np.testing.assert_allclose(zo.cpu().numpy()[:p], X[J] @ d, rtol=1e-12,
+                                   atol=1e-12 * np.abs(X).sum(axis=1).max())
+
+
 @pytest.mark.parametrize("shape,svr,aligned", [((3001, 300), False, True), ((2000, 51), False, False),
                                                 ((1500, 64), True, True)])
 def test_fused_gradient_and_direction_epilogue(pkg, shape, svr, aligned):

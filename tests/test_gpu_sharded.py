@@ -122,5 +122,17 @@ def test_sharded_world1_nccl_matches_native(pkg):
                             pkg.AlmOptions(tol_kkt=1e-6))
         assert rep.converged and nat.converged
         assert rep.objective == pytest.approx(nat.objective, rel=1e-6)
+        # sparse operator (config-3 generator, Zipf columns): rank-local CSR products and
+        # the sharded factor-space CG vs the single-GPU native driver
+        cfg = datagen.make_config(3, n=6000, q=1500)
+        csr = (cfg["indptr"], cfg["indices"], cfg["data"], cfg["shape"])
+        pb = sharded.build_csvc_dual_sharded(csr, cfg["y"], cfg["C"], comm)
+        ssn = pkg.SsnOptions(max_inner=200)
+        rep = pkg.alm_solve(pb, pkg.AlmOptions(tol_kkt=1e-6), ssn)
+        nat = pkg.alm_solve(pkg.build_csvc_dual(csr, cfg["y"], cfg["C"]),
+                            pkg.AlmOptions(tol_kkt=1e-6), ssn)
+        assert rep.converged and nat.converged and rep.kkt_residual <= 1e-6
+        assert pb.engine().counters.get("cg_iters", 0) > 0
+        assert rep.objective == pytest.approx(nat.objective, rel=1e-6)
     finally:
         dist.destroy_process_group()
