@@ -841,7 +841,8 @@ struct Driver {
     direction(p, asa, with_gradient ? L.scal + 4 : L.scal + 0);
     // the first Armijo batch (alpha = 1, beta, ..., beta^(T0-1)) is projected
     // speculatively with the direction: most steps then need no further host round trip
-    const int T0 = std::min(TMAX, std::max(1, O.line_search_batch));
+    const int T0 = std::min(std::min(TMAX, std::max(1, O.line_search_batch)),
+                            proj_wave_trials(P.n));
     double coefs[TMAX];
     double alpha = 1.0;
     for (int k = 0; k < T0; ++k) {
@@ -870,7 +871,8 @@ struct Driver {
     while (tried < 61) {
       const int T = (tried == 0 && first) ? first_T
                     : tried == 0 ? 1
-                                 : std::min(std::min(TMAX, std::max(1, O.line_search_batch)),
+                                 : std::min(std::min(std::min(TMAX, std::max(1, O.line_search_batch)),
+                                                     proj_wave_trials(P.n)),
                                             61 - tried);
       double alphas[TMAX], coefs[TMAX];
       for (int k = 0; k < T; ++k) {

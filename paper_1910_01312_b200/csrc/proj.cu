@@ -877,6 +877,25 @@ static bool cluster_ok(long long n, int T) {
   return ok == 1 && n <= (long long)CL_CTAS * CL_NT * CL_EPT && T >= 1;
 }
 
+// Line-search trials one cluster-projection launch runs in a single wave: a 16-CTA
+// cluster needs 16 SMs of one GPC, so only ~7 fit on a B200 at once -- an 8-trial
+// batch ran as two waves (2x the latency of 7).  Not limited without the cluster path.
+int proj_wave_trials(long long n) {
+  if (!cluster_ok(n, 1)) return SSNAL_MAX_TRIALS;
+  static int w = -1;
+  if (w < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL_CTAS, 1, 1);
+    cfg.blockDim = dim3(CL_NT, 1, 1);
+    cfg.dynamicSmemBytes = CL_SMEM;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, (void*)proj_cluster_kernel, &cfg) != cudaSuccess || c < 1)
+      c = SSNAL_MAX_TRIALS;
+    w = c;
+  }
+  return w;
+}
+
 int proj_blocks(long long n) {
   long long b = ceil_div(n, (long long)SSNAL_NT * 4);
   if (b < 1) b = 1;

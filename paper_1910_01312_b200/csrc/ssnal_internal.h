@@ -75,6 +75,7 @@ struct ProjLaunch {
 };
 
 int proj_blocks(long long n);
+int proj_wave_trials(long long n);
 size_t proj_ws_bytes(long long n, int T);
 cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream);
 
