@@ -210,6 +210,11 @@ size_t ssnal_csr_restricted_ws_bytes(const ssnal_csr_operator_t* op);
 int ssnal_csr_xt_restricted(const ssnal_csr_operator_t* op, const uint8_t* keep,
                             const int32_t* J, int64_t p, const double* w, double* out, void* ws,
                             void* stream);
+/* out[r] = row_sign[J[r]] * A[J[r],:] . d (r < p) through the same build's packed
+ * J-restricted CSR (the CG's X_J d).  Same workspace as ssnal_csr_xt_restricted. */
+int ssnal_csr_xd_restricted(const ssnal_csr_operator_t* op, const uint8_t* keep,
+                            const int32_t* J, int64_t p, const double* d, double* out, void* ws,
+                            void* stream);
 /* out[k] = sum_{i : keep[i] != 0} A[i,k]^2 (q): the Jacobi diagonal of X_J^T X_J for the
  * factor-space CG (row signs square away); ws >= nslots doubles.  Replaces the diagonal
  * the reference's CG branch would read off Q_JJ (ref solver.py:151-172, 253-258). */

@@ -118,6 +118,7 @@ _SIGNATURES.update({
     "ssnal_csr_colsq": (_I, [ctypes.POINTER(CsrOperator), _P, _P, _P, _P]),
     "ssnal_csr_restricted_ws_bytes": (ctypes.c_size_t, [ctypes.POINTER(CsrOperator)]),
     "ssnal_csr_xt_restricted": (_I, [ctypes.POINTER(CsrOperator), _P, _P, _I64, _P, _P, _P, _P]),
+    "ssnal_csr_xd_restricted": (_I, [ctypes.POINTER(CsrOperator), _P, _P, _I64, _P, _P, _P, _P]),
     "ssnal_alm_solve_dense": (_I, [ctypes.POINTER(DenseProblem), ctypes.POINTER(Options), _P, _P,
                                    _P, ctypes.POINTER(Report), _P, _SZ, PROGRESS_FN, _P, _P]),
     "ssnal_proj_local_ws_bytes": (_SZ, [_I64, _I]),

@@ -260,6 +260,17 @@ int ssnal_csr_xt_restricted(const ssnal_csr_operator_t* op, const uint8_t* keep,
   return check("ssnal_csr_xt_restricted", e);
 }
 
+int ssnal_csr_xd_restricted(const ssnal_csr_operator_t* op, const uint8_t* keep,
+                            const int32_t* J, int64_t p, const double* d, double* out, void* ws,
+                            void* stream) {
+  if (!csr_ok(op) || !keep || !ws || p < 0 || p > op->n || (p > 0 && (!J || !d || !out)))
+    return fail_arg("ssnal_csr_xd_restricted", "operator/null/size");
+  const CscJ c = cscj_layout(*op, ws);
+  cudaError_t e = launch_cscj_build(*op, keep, J, p, c, S(stream));
+  if (e == cudaSuccess) e = launch_csrj_xd(c, p, d, out, S(stream));
+  return check("ssnal_csr_xd_restricted", e);
+}
+
 int ssnal_csr_colsq(const ssnal_csr_operator_t* op, const uint8_t* keep, double* out, void* ws,
                     void* stream) {
   if (!csr_ok(op) || !keep || !out || (op->nslots > 0 && !ws))

@@ -467,12 +467,19 @@ struct GramArgs {
   const long long* p_dev;
   double* part;  // [GSPLIT][q][q] (upper tile pairs + full diagonal tiles)
   int ntile;
+  // m1 = X_J^T a_J rides on the diagonal tiles' staged rows: weights w_r = a_{J_r} times
+  // the row sign, part_m1[split][q]
+  const double* a;
+  const double* rs;
+  int svr;
+  double* part_m1;
 };
 
 // grid.x = tile pair index (ti <= tj), grid.y = split
 __global__ void __launch_bounds__(256) gram_kernel(GramArgs g) {
   __shared__ double sA[GK][GLD];
   __shared__ double sB[GK][GLD];
+  __shared__ double sw[GK];
   const long long p = *g.p_dev;
   // decode (ti, tj) from the linear upper-triangle index
   int pair = blockIdx.x, ti = 0;
@@ -486,7 +493,21 @@ __global__ void __launch_bounds__(256) gram_kernel(GramArgs g) {
 #pragma unroll
   for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
   const long long ci = (long long)ti * GT, cj = (long long)tj * GT;
+  const bool diag = ti == tj;
+  double m1acc = 0.0;  // thread c < GT of a diagonal tile: column ci + c of m1
   for (long long kb = k0; kb < k1; kb += GK) {
+    if (diag && threadIdx.x < GK) {  // gram_m1's weights, same order of operations
+      const long long r = kb + threadIdx.x;
+      double w = 0.0;
+      if (r < k1) {
+        const long long li = g.J[r];
+        const long long pr = li >= g.n ? li - g.n : li;
+        w = g.a[li];
+        if (g.rs) w *= g.rs[pr];
+        if (g.svr && li >= g.n) w = -w;
+      }
+      sw[threadIdx.x] = w;
+    }
     // stage GK gathered rows x 64 columns of both tiles
     for (int idx = threadIdx.x; idx < GK * GT; idx += blockDim.x) {
       int kr = idx / GT, c = idx % GT;
@@ -503,6 +524,10 @@ __global__ void __launch_bounds__(256) gram_kernel(GramArgs g) {
       sB[kr][c] = vb;
     }
     __syncthreads();
+    if (diag && threadIdx.x < GT) {
+      const int nk = (int)min((long long)GK, k1 - kb);
+      for (int kr = 0; kr < nk; ++kr) m1acc = fma(sw[kr], sA[kr][threadIdx.x], m1acc);
+    }
 #pragma unroll
     for (int kk = 0; kk < GK; kk += 4) {
       const double a = sA[kk + (lane & 3)][warp * 8 + (lane >> 2)];
@@ -514,6 +539,8 @@ __global__ void __launch_bounds__(256) gram_kernel(GramArgs g) {
     }
     __syncthreads();
   }
+  if (diag && threadIdx.x < GT && ci + threadIdx.x < g.q)
+    g.part_m1[blockIdx.y * g.q + ci + threadIdx.x] = m1acc;
   // C fragment: row = lane/4, cols = 2*(lane%4) + {0,1}
   double* dst = g.part + (long long)blockIdx.y * g.q * g.q;
   const long long row = ci + warp * 8 + (lane >> 2);
@@ -525,28 +552,6 @@ __global__ void __launch_bounds__(256) gram_kernel(GramArgs g) {
       if (col + 1 < g.q) dst[row * g.q + col + 1] = acc[t][1];
     }
   }
-}
-
-// m1 partials: part_m1[split][q] = sum_{r in split} w_r x_{J_r}
-__global__ void __launch_bounds__(256) gram_m1_kernel(GramArgs g, const double* __restrict__ a,
-                                                      const double* __restrict__ rs, int svr,
-                                                      double* __restrict__ part_m1) {
-  const long long p = *g.p_dev;
-  const long long chunk = ceil_div(ceil_div(p, GSPLIT), 4) * 4;
-  const long long k0 = blockIdx.y * chunk;
-  const long long k1 = min(p, k0 + chunk);
-  const long long col = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= g.q) return;
-  double s = 0.0;
-  for (long long r = k0; r < k1; ++r) {
-    long long li = g.J[r];
-    long long pr = li >= g.n ? li - g.n : li;
-    double w = a[li];
-    if (rs) w *= rs[pr];
-    if (svr && li >= g.n) w = -w;
-    s = fma(w, __ldg(g.A + pr * g.lda + col), s);
-  }
-  part_m1[blockIdx.y * g.q + col] = s;
 }
 
 __global__ void gram_m1_fold_kernel(const double* __restrict__ part_m1, long long q,
@@ -590,9 +595,9 @@ cudaError_t launch_dense_gram(const double* A, long long n, long long q, long lo
   g.part = (double*)ws;
   g.ntile = (int)ceil_div(q, GT);
   double* part_m1 = g.part + (long long)GSPLIT * q * q;
+  g.a = a; g.rs = rs; g.svr = svr; g.part_m1 = part_m1;
   int npairs = g.ntile * (g.ntile + 1) / 2;
   { note_launch(); gram_kernel<<<dim3(npairs, GSPLIT), 256, 0, stream>>>(g); }
-  { note_launch(); gram_m1_kernel<<<dim3((unsigned)ceil_div(q, 256), GSPLIT), 256, 0, stream>>>(g, a, rs, svr, part_m1); }
   { note_launch(); gram_m1_fold_kernel<<<(unsigned)ceil_div(q, 256), 256, 0, stream>>>(part_m1, q, m1); }
   { note_launch(); gram_assemble_kernel<<<(unsigned)ceil_div(q * q, 256), 256, 0, stream>>>(g.part, q, m1, sigma,
                                                                           asa_dev, M); }

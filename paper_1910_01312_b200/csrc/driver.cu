@@ -385,7 +385,7 @@ struct Driver {
                       std::min(O.eta, SPARSE_CG_ETA), O.tau, L.cgs, L.cg_part, S));
     // v (q) -> out (q) = sigma-free part X_J^T P X_J v, via zq (p) and ys (n)
     auto gram_apply = [&](const double* v, double* out) {
-      ck(launch_csr_xd(op, L.J, p, v, L.cg_zq, S));
+      ck(launch_csrj_xd(L.cj, p, v, L.cg_zq, S));
       dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
       ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
       ck(launch_cscj_xt(op, L.cj, L.cg_w, out, L.csc_part, S));
@@ -426,7 +426,7 @@ struct Driver {
     for (int it = 0; it < max_it;) {
       for (int b = 0; b < CG_BATCH && it < max_it; ++b, ++it) {
         ck(launch_cscj_xt(op, L.cj, L.cg_pv, L.tq, L.csc_part, S));
-        ck(launch_csr_xd(op, L.J, p, L.tq, L.cg_zq, S));
+        ck(launch_csrj_xd(L.cj, p, L.tq, L.cg_zq, S));
         dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
         ck(launch_cg_ap(p, L.cg_pv, L.cg_zq, L.cg_aJ, asa, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
         ck(launch_cg_step(p, L.cg_y, L.cg_r, L.cg_pv, L.cg_Ap, nullptr, nullptr, L.cgs, L.cg_part,
@@ -438,7 +438,7 @@ struct Driver {
       dots({{L.cg_aJ, L.cg_r}}, L.cgs + 7, p);
       ck(launch_cg_project(p, L.cg_r, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
       ck(launch_cscj_xt(op, L.cj, L.cg_w, L.tq, L.csc_part, S));
-      ck(launch_csr_xd(op, L.J, p, L.tq, L.cg_zq, S));
+      ck(launch_csrj_xd(L.cj, p, L.tq, L.cg_zq, S));
       dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
       ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
       ck(launch_cscj_xt(op, L.cj, L.cg_w, L.tq, L.csc_part, S));

@@ -560,14 +560,88 @@ __global__ void __launch_bounds__(256) cscj_fix_kernel(
   }
 }
 
+// J-restricted CSR (once per Newton step of the CG route): row lengths of J's rows,
+// block sums + last-block exclusive scan, then per block the row offsets and a warp per
+// row copying (index, sign * value).  The CG's X_J d then reads p contiguous rows.
+static constexpr int RJ_NT = 256;
+__global__ void __launch_bounds__(RJ_NT) csrj_count_kernel(const int64_t* __restrict__ indptr,
+                                                           const int32_t* __restrict__ J,
+                                                           long long p, long long* __restrict__ rblk,
+                                                           unsigned int* ticket, int nblk) {
+  __shared__ long long sm[33];
+  const long long r = (long long)blockIdx.x * RJ_NT + threadIdx.x;
+  long long len = 0;
+  if (r < p) {
+    const int i = J[r];
+    len = indptr[i + 1] - indptr[i];
+  }
+  long long tot;
+  block_exclusive_scan_ll(len, sm, &tot);
+  if (threadIdx.x == 0) rblk[blockIdx.x] = tot;
+  if (!last_block_arrive(ticket, gridDim.x)) return;
+  long long carry = 0;
+  for (int start = 0; start < nblk; start += RJ_NT) {
+    const int idx = start + threadIdx.x;
+    const long long v = idx < nblk ? __ldcg(rblk + idx) : 0;
+    long long t;
+    const long long ex = block_exclusive_scan_ll(v, sm, &t);
+    if (idx < nblk) rblk[idx] = carry + ex;
+    carry += t;
+  }
+  if (threadIdx.x == 0) rblk[nblk] = carry;
+}
+
+__global__ void __launch_bounds__(RJ_NT) csrj_fill_kernel(
+    const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+    const double* __restrict__ values, const double* __restrict__ rs,
+    const int32_t* __restrict__ J, long long p, const long long* __restrict__ rblk, int nblk,
+    int64_t* __restrict__ rptr, int32_t* __restrict__ ridx, double* __restrict__ rval) {
+  __shared__ long long sm[33];
+  __shared__ long long off[RJ_NT];
+  const long long r0 = (long long)blockIdx.x * RJ_NT;
+  const long long r = r0 + threadIdx.x;
+  long long len = 0;
+  if (r < p) {
+    const int i = J[r];
+    len = indptr[i + 1] - indptr[i];
+  }
+  long long tot;
+  const long long ex = block_exclusive_scan_ll(len, sm, &tot);
+  off[threadIdx.x] = rblk[blockIdx.x] + ex;
+  if (r < p) rptr[r] = off[threadIdx.x];
+  if (blockIdx.x == nblk - 1 && threadIdx.x == 0) rptr[p] = rblk[nblk];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = warp; t < RJ_NT && r0 + t < p; t += RJ_NT / 32) {
+    const int i = J[r0 + t];
+    const long long k0 = indptr[i], k1 = indptr[i + 1], o = off[t];
+    const double sg = rs ? rs[i] : 1.0;
+    for (long long k = k0 + lane; k < k1; k += 32) {
+      ridx[o + (k - k0)] = indices[k];
+      rval[o + (k - k0)] = sg * values[k];
+    }
+  }
+}
+
+cudaError_t launch_csrj_xd(const CscJ& c, long long p, const double* d, double* out,
+                           cudaStream_t stream) {
+  if (p < 1) return cudaSuccess;
+  note_launch();
+  csr_xd_kernel<<<(unsigned)ceil_div(p * SUB, 256LL), 256, 0, stream>>>(
+      c.rptr, c.ridx, c.rval, nullptr, nullptr, p, d, out);
+  return cudaGetLastError();
+}
+
 size_t cscj_ws_bytes(const CsrOp& op) {
   const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
   const long long cap = op.nnz + CH;  // vector loads of the last chunk stay inside
   const long long nch = ceil_div(cap, (long long)CH);
+  const long long rb = ceil_div(op.n, (long long)RJ_NT) + 1;
   return 256 + sizeof(int32_t) * (size_t)op.n + sizeof(int) * (size_t)op.nseg +
          sizeof(long long) * (size_t)(nblk + 1) + 2 * sizeof(int64_t) * (size_t)op.nseg +
          (2 * sizeof(int32_t) + sizeof(double)) * (size_t)cap + (2 * sizeof(double) + 1) * nch +
-         12 * 256;
+         sizeof(int64_t) * (size_t)(op.n + 1) + (sizeof(int32_t) + sizeof(double)) * (size_t)op.nnz +
+         sizeof(long long) * (size_t)rb + 16 * 256;
 }
 
 static char* al256(char* p) { return (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255); }
@@ -589,7 +663,11 @@ CscJ cscj_layout(const CsrOp& op, void* ws) {
   c.val = (double*)p; p = al256(p + sizeof(double) * cap);
   c.cval = (double*)p; p = al256(p + sizeof(double) * nch);
   c.ctail = (double*)p; p = al256(p + sizeof(double) * nch);
-  c.cflag = (uint8_t*)p;
+  c.cflag = (uint8_t*)p; p = al256(p + nch);
+  c.rptr = (int64_t*)p; p = al256(p + sizeof(int64_t) * (op.n + 1));
+  c.ridx = (int32_t*)p; p = al256(p + sizeof(int32_t) * op.nnz);
+  c.rval = (double*)p; p = al256(p + sizeof(double) * op.nnz);
+  c.rblk = (long long*)p;
   return c;
 }
 
@@ -605,6 +683,14 @@ cudaError_t launch_cscj_build(const CsrOp& op, const uint8_t* keep, const int32_
   cscj_fill_kernel<<<(unsigned)nblk, CJ_WARPS * 32, 0, stream>>>(
       op.seg_beg, op.seg_end, op.nseg, op.rowidx, op.valt, op.row_sign, keep, c.posJ, c.cnt,
       c.blk, c.beg, c.end, c.pos, c.val, c.seg);
+  if (p > 0) {
+    const int rb = (int)ceil_div(p, (long long)RJ_NT);
+    note_launch();
+    csrj_count_kernel<<<rb, RJ_NT, 0, stream>>>(op.indptr, J, p, c.rblk, c.ticket, rb);
+    note_launch();
+    csrj_fill_kernel<<<rb, RJ_NT, 0, stream>>>(op.indptr, op.indices, op.values, op.row_sign, J,
+                                               p, c.rblk, rb, c.rptr, c.ridx, c.rval);
+  }
   return cudaGetLastError();
 }
 

@@ -48,6 +48,12 @@ struct CscJ {
   int32_t* seg;    // segment id per kept entry (nnz-balanced product)
   double *cval, *ctail;  // per 256-entry chunk: first-segment / open-tail partial sums
   uint8_t* cflag;        // bit 0: first segment closes in the chunk; bit 1: owns an open tail
+  // J-restricted CSR: the free rows' entries packed contiguously (row signs folded), so
+  // every CG product X_J d streams them without the J -> indptr indirection
+  int64_t* rptr;   // p + 1
+  int32_t* ridx;
+  double* rval;
+  long long* rblk; // per-block row-length offsets
 };
 size_t cscj_ws_bytes(const CsrOp& op);
 CscJ cscj_layout(const CsrOp& op, void* ws);
@@ -55,6 +61,8 @@ cudaError_t launch_cscj_build(const CsrOp& op, const uint8_t* keep, const int32_
                               const CscJ& c, cudaStream_t stream);
 cudaError_t launch_cscj_xt(const CsrOp& op, const CscJ& c, const double* w, double* out,
                            double* part, cudaStream_t stream);
+cudaError_t launch_csrj_xd(const CscJ& c, long long p, const double* d, double* out,
+                           cudaStream_t stream);
 
 struct ProjLaunch {
   const double *A, *B, *coef, *a, *l, *u;

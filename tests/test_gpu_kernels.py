@@ -318,6 +318,11 @@ def test_csr_restricted_products(pkg, keep_frac):
                   be.stream())
         np.testing.assert_allclose(zo.cpu().numpy()[:p], X[J] @ d, rtol=1e-12,
                                    atol=1e-12 * np.abs(X).sum(axis=1).max())
+        # packed J-restricted CSR (the CG's X_J d): bit-identical to the row-list product
+        z2 = be.empty(p)
+        _lib.call("ssnal_csr_xd_restricted", op._cref, keep_d.data_ptr(), J_d.data_ptr(), p,
+                  _dev(d).data_ptr(), z2.data_ptr(), ws.data_ptr(), be.stream())
+        assert torch.equal(z2, zo[:p])
 
 
 @pytest.mark.parametrize("shape,svr,aligned", [((3001, 300), False, True), ((2000, 51), False, False),
