@@ -685,7 +685,6 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ double red[8 * 32];
   __shared__ double gath[2][CL_CTAS][8];  // [pass parity][source rank][slot], filled by pushes
-  __shared__ double res[8];
   __shared__ double sh[8];
   __shared__ int sh_status;
   // breakpoints do not depend on lambda: computed once (two divisions per slot),
@@ -749,38 +748,55 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
       vals[6] = fmax(vals[6], tb);
       vals[7] += 1.0;
     }
-    block_reduce<8>(vals, ops, red);
-    const int buf = pass & 1;
-    // push this CTA's partial into slot [rank] of every CTA of the cluster
-    if (tid == 0)
-      for (int k = 0; k < 8; ++k) red[k] = vals[k];
-    __syncthreads();
-    if (tid < CL_CTAS * 8) {
-      double* dst = cluster.map_shared_rank(&gath[buf][rank][0], tid >> 3);
-      dst[tid & 7] = red[tid & 7];
+    // warp trees, then slot k folded across warps by thread k (block_reduce's order) and
+    // pushed straight into slot [rank] of every CTA of the cluster; after the cluster
+    // barrier EVERY thread folds the 16 rank partials and runs the (deterministic) Newton
+    // update itself: two barriers per pass instead of six
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double w = ops[k] == 0 ? warp_sum(vals[k]) : (ops[k] == 1 ? warp_min(vals[k]) : warp_max(vals[k]));
+      if (lane == 0) red[k * 32 + warp] = w;
     }
-    cluster.sync();  // arrive.release / wait.acquire: every push of this pass is visible
+    __syncthreads();
+    const int buf = pass & 1;
     if (tid < 8) {
       const int op = (tid == 3 || tid == 5) ? 1 : ((tid == 4 || tid == 6) ? 2 : 0);  // = ops[tid]
-      double r = gath[buf][0][tid];
-      for (int q = 1; q < CL_CTAS; ++q) {
-        const double x = gath[buf][q][tid];
+      double r = red[tid * 32];
+      for (int w = 1; w < CL_NT / 32; ++w) {
+        const double x = red[tid * 32 + w];
         r = op == 0 ? r + x : (op == 1 ? fmin(r, x) : fmax(r, x));
       }
-      res[tid] = r;
+#pragma unroll 4
+      for (int q = 0; q < CL_CTAS; ++q) *cluster.map_shared_rank(&gath[buf][rank][tid], q) = r;
     }
-    __syncthreads();
-    if (tid == 0) {
-      if (pass == 0) { tmin = res[5]; tmax = res[6]; }
-      if (res[7] == 0.0) {
-        lam = 0.0;
-        status = PROJ_DONE;
-      } else {
-        newton_update(p.d - res[0], res[1], res[2], res[3], res[4], tmin, p.d, c, lo, hi, lam,
-                      status);
+    cluster.sync();  // arrive.release / wait.acquire: every push of this pass is visible
+    if (warp == 0) {
+      // lane k < 8 folds slot k over the ranks (fixed order), lane 0 runs the update
+      double r = 0.0;
+      if (lane < 8) {
+        const int op = (lane == 3 || lane == 5) ? 1 : ((lane == 4 || lane == 6) ? 2 : 0);
+        r = gath[buf][0][lane];
+        for (int q = 1; q < CL_CTAS; ++q) {
+          const double x = gath[buf][q][lane];
+          r = op == 0 ? r + x : (op == 1 ? fmin(r, x) : fmax(r, x));
+        }
       }
-      sh[0] = c; sh[1] = lo; sh[2] = hi; sh[3] = lam; sh[4] = tmin; sh[5] = tmax;
-      sh_status = status;
+      double res_[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) res_[k] = __shfl_sync(0xffffffffu, r, k);
+      if (lane == 0) {
+        if (pass == 0) { tmin = res_[5]; tmax = res_[6]; }
+        if (res_[7] == 0.0) {
+          lam = 0.0;
+          status = PROJ_DONE;
+        } else {
+          newton_update(p.d - res_[0], res_[1], res_[2], res_[3], res_[4], tmin, p.d, c, lo, hi,
+                        lam, status);
+        }
+        sh[0] = c; sh[1] = lo; sh[2] = hi; sh[3] = lam; sh[4] = tmin; sh[5] = tmax;
+        sh_status = status;
+      }
     }
     __syncthreads();
     c = sh[0]; lo = sh[1]; hi = sh[2]; lam = sh[3]; tmin = sh[4]; tmax = sh[5];
