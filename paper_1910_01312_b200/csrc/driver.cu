@@ -369,6 +369,13 @@ struct Driver {
                    std::sqrt(H->cg[4]), H->cg[5]);
   }
 
+  // zq = X_J v on the packed J rows with cgs[7] = a_J . zq folded in
+  void xd_dot(long long p, const double* v) {
+    ck(launch_csrj_xd_dot(L.cj, p, v, L.cg_zq, L.cg_aJ, L.cgs + 7, L.cg_part,
+                          (int)cg_part_doubles(P.n) - 8, reinterpret_cast<unsigned int*>(L.cgs + 8),
+                          S));
+  }
+
   // Factor-space Jacobi-preconditioned CG for p >= q (Zipf-hot columns make the
   // sample-space spectrum spread; column scaling flattens it):
   //   (I_q + sigma X_J^T P_J X_J) t = -X^T s,  D = diag(.)  (ref solver.py:151-172 role)
@@ -385,8 +392,7 @@ struct Driver {
                       std::min(O.eta, SPARSE_CG_ETA), O.tau, L.cgs, L.cg_part, S));
     // v (q) -> out (q) = sigma-free part X_J^T P X_J v, via zq (p) and ys (n)
     auto gram_apply = [&](const double* v, double* out) {
-      ck(launch_csrj_xd(L.cj, p, v, L.cg_zq, S));
-      dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
+      xd_dot(p, v);
       ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
       ck(launch_cscj_xt(op, L.cj, L.cg_w, out, L.csc_part, S));
     };
@@ -426,8 +432,7 @@ struct Driver {
     for (int it = 0; it < max_it;) {
       for (int b = 0; b < CG_BATCH && it < max_it; ++b, ++it) {
         ck(launch_cscj_xt(op, L.cj, L.cg_pv, L.tq, L.csc_part, S));
-        ck(launch_csrj_xd(L.cj, p, L.tq, L.cg_zq, S));
-        dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
+        xd_dot(p, L.tq);
         ck(launch_cg_ap(p, L.cg_pv, L.cg_zq, L.cg_aJ, asa, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
         ck(launch_cg_step(p, L.cg_y, L.cg_r, L.cg_pv, L.cg_Ap, nullptr, nullptr, L.cgs, L.cg_part,
                           S));
@@ -438,8 +443,7 @@ struct Driver {
       dots({{L.cg_aJ, L.cg_r}}, L.cgs + 7, p);
       ck(launch_cg_project(p, L.cg_r, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
       ck(launch_cscj_xt(op, L.cj, L.cg_w, L.tq, L.csc_part, S));
-      ck(launch_csrj_xd(L.cj, p, L.tq, L.cg_zq, S));
-      dots({{L.cg_aJ, L.cg_zq}}, L.cgs + 7, p);
+      xd_dot(p, L.tq);
       ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
       ck(launch_cscj_xt(op, L.cj, L.cg_w, L.tq, L.csc_part, S));
       ck(launch_csr_xd(op, nullptr, P.n_phys, L.tq, L.tmp, S));

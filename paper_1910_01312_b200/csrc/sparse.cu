@@ -116,15 +116,19 @@ __global__ void __launch_bounds__(256) csc_colsq_kernel(const int64_t* __restric
   }
 }
 
-// split columns: out[col] = sum of its partial slots [pbeg, pend) in order
+// split columns: out[col] = sum of its partial slots [pbeg, pend), a warp per column
+// (lanes stride the slots, fixed shuffle tree: deterministic).  Zipf-hot columns have
+// up to ~2000 slots; a thread walking them serially sat on the critical path.
 __global__ void csc_fold_kernel(const int32_t* __restrict__ fold_col,
                                 const int32_t* __restrict__ fold_beg, long long nfold,
                                 const double* __restrict__ part, double* __restrict__ out) {
-  const long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long f = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (f >= nfold) return;
   double s = 0.0;
-  for (int k = fold_beg[f]; k < fold_beg[f + 1]; ++k) s += part[k];
-  out[fold_col[f]] = s;
+  for (int k = fold_beg[f] + lane; k < fold_beg[f + 1]; k += 32) s += part[k];
+  s = warp_sum(s);
+  if (lane == 0) out[fold_col[f]] = s;
 }
 
 // dst[i] = 0 for all i in [0, n) that are not overwritten later: zero fill
@@ -238,7 +242,7 @@ cudaError_t launch_csc_xt(const CsrOp& op, const double* v, double* out, double*
       v, out, part);
   if (op.nfold > 0) {
     note_launch();
-    csc_fold_kernel<<<(unsigned)ceil_div(op.nfold, 256LL), 256, 0, stream>>>(
+    csc_fold_kernel<<<(unsigned)ceil_div(op.nfold * 32, 256LL), 256, 0, stream>>>(
         op.fold_col, op.fold_beg, op.nfold, part, out);
   }
   return cudaGetLastError();
@@ -252,7 +256,7 @@ cudaError_t launch_csc_colsq(const CsrOp& op, const uint8_t* keep, double* out, 
       part);
   if (op.nfold > 0) {
     note_launch();
-    csc_fold_kernel<<<(unsigned)ceil_div(op.nfold, 256LL), 256, 0, stream>>>(
+    csc_fold_kernel<<<(unsigned)ceil_div(op.nfold * 32, 256LL), 256, 0, stream>>>(
         op.fold_col, op.fold_beg, op.nfold, part, out);
   }
   return cudaGetLastError();
@@ -322,7 +326,8 @@ __device__ __forceinline__ long long block_exclusive_scan_ll(long long v, long l
 __global__ void __launch_bounds__(CJ_WARPS * 32) cscj_count_kernel(
     const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ seg_end, long long nseg,
     const int32_t* __restrict__ rowidx, const uint8_t* __restrict__ keep, int* __restrict__ cnt,
-    long long* __restrict__ blk, unsigned int* ticket, int nblk) {
+    long long* __restrict__ blk, unsigned int* ticket, int nblk, int32_t* __restrict__ empty,
+    unsigned int* nempty) {
   __shared__ long long sm[33];
   __shared__ int wc[CJ_WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -332,7 +337,10 @@ __global__ void __launch_bounds__(CJ_WARPS * 32) cscj_count_kernel(
     for (long long k = seg_beg[s] + lane; k < seg_end[s]; k += 32) c += keep[rowidx[k]] ? 1 : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == 0) cnt[s] = c;
+    if (lane == 0) {
+      cnt[s] = c;
+      if (c == 0) empty[atomicAdd(nempty, 1u)] = (int32_t)s;  // order irrelevant: zero writes
+    }
   }
   if (lane == 0) wc[warp] = s < nseg ? c : 0;
   __syncthreads();
@@ -545,9 +553,14 @@ __global__ void __launch_bounds__(256) cscj_fix_kernel(
     const long long* __restrict__ total, const int32_t* __restrict__ jseg,
     const int32_t* __restrict__ seg_col, const int32_t* __restrict__ seg_slot,
     const double* __restrict__ cval, const double* __restrict__ ctail,
-    const uint8_t* __restrict__ cflag, double* __restrict__ out, double* __restrict__ part) {
+    const uint8_t* __restrict__ cflag, double* __restrict__ out, double* __restrict__ part,
+    const int32_t* __restrict__ empty, const unsigned int* __restrict__ nempty) {
   const long long nnz = *total;
   const long long nch = (nnz + CH - 1) / CH;
+  const long long ne = *nempty;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne;
+       e += (long long)gridDim.x * blockDim.x)
+    seg_write(empty[e], 0.0, seg_col, seg_slot, out, part);
   for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < nch;
        c += (long long)gridDim.x * blockDim.x) {
     if (!(cflag[c] & 2)) continue;
@@ -623,6 +636,66 @@ __global__ void __launch_bounds__(RJ_NT) csrj_fill_kernel(
   }
 }
 
+// X_J d on the packed rows with the CG's a_J . (X_J d) folded in (replaces a dots
+// launch per CG iteration): grid-stride over 32-row groups on a fixed grid, per-block
+// partial, last-block fold in block order (deterministic)
+__global__ void __launch_bounds__(256) csrj_xd_dot_kernel(
+    const int64_t* __restrict__ rptr, const int32_t* __restrict__ ridx,
+    const double* __restrict__ rval, long long p, const double* __restrict__ d,
+    double* __restrict__ out, const double* __restrict__ wdot, double* dot_out,
+    double* __restrict__ part, unsigned int* ticket) {
+  __shared__ double red[32];
+  const int sl = threadIdx.x & (SUB - 1);
+  double acc[1] = {0.0};
+  // warp-uniform trip count: every lane reaches every full-mask shuffle (a sub-warp past
+  // the last row runs an empty row instead of leaving the loop)
+  const long long wstride = (long long)gridDim.x * blockDim.x / SUB;
+  for (long long g0 = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / SUB; g0 < p;
+       g0 += wstride) {
+    const long long g = g0 + ((threadIdx.x & 31) / SUB);
+    const bool valid = g < p;
+    const long long k0 = valid ? __ldg(rptr + g) : 0, k1 = valid ? __ldg(rptr + g + 1) : 0;
+    double s = 0.0;
+    for (long long kb = k0 + sl; kb < k1; kb += XD_UNROLL * SUB) {
+      int idx[XD_UNROLL];
+      double v[XD_UNROLL];
+#pragma unroll
+      for (int u = 0; u < XD_UNROLL; ++u) {
+        const long long k = kb + u * SUB;
+        const bool ok = k < k1;
+        idx[u] = ok ? __ldg(ridx + k) : 0;
+        v[u] = ok ? __ldg(rval + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < XD_UNROLL; ++u)
+        if (kb + u * SUB < k1) s = fma(v[u], __ldg(d + idx[u]), s);
+    }
+#pragma unroll
+    for (int o = SUB / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, SUB);
+    if (sl == 0 && valid) {
+      out[g] = s;
+      acc[0] = fma(wdot[g], s, acc[0]);
+    }
+  }
+  const int ops[1] = {0};
+  block_reduce<1>(acc, ops, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (!last_block_arrive(ticket, gridDim.x)) return;
+  block_fold_partials<1>(part, gridDim.x, 1, ops, acc, red);
+  if (threadIdx.x == 0) *dot_out = acc[0];
+}
+
+cudaError_t launch_csrj_xd_dot(const CscJ& c, long long p, const double* d, double* out,
+                               const double* wdot, double* dot_out, double* part,
+                               int max_blocks, unsigned int* ticket, cudaStream_t stream) {
+  if (p < 1) return cudaMemsetAsync(dot_out, 0, sizeof(double), stream);
+  const int grid = (int)std::max(1LL, std::min(ceil_div(p * SUB, 256LL), (long long)max_blocks));
+  note_launch();
+  csrj_xd_dot_kernel<<<grid, 256, 0, stream>>>(c.rptr, c.ridx, c.rval, p, d, out, wdot, dot_out,
+                                                part, ticket);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_csrj_xd(const CscJ& c, long long p, const double* d, double* out,
                            cudaStream_t stream) {
   if (p < 1) return cudaSuccess;
@@ -641,7 +714,7 @@ size_t cscj_ws_bytes(const CsrOp& op) {
          sizeof(long long) * (size_t)(nblk + 1) + 2 * sizeof(int64_t) * (size_t)op.nseg +
          (2 * sizeof(int32_t) + sizeof(double)) * (size_t)cap + (2 * sizeof(double) + 1) * nch +
          sizeof(int64_t) * (size_t)(op.n + 1) + (sizeof(int32_t) + sizeof(double)) * (size_t)op.nnz +
-         sizeof(long long) * (size_t)rb + 16 * 256;
+         sizeof(long long) * (size_t)rb + sizeof(int32_t) * (size_t)op.nseg + 18 * 256;
 }
 
 static char* al256(char* p) { return (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255); }
@@ -667,18 +740,23 @@ CscJ cscj_layout(const CsrOp& op, void* ws) {
   c.rptr = (int64_t*)p; p = al256(p + sizeof(int64_t) * (op.n + 1));
   c.ridx = (int32_t*)p; p = al256(p + sizeof(int32_t) * op.nnz);
   c.rval = (double*)p; p = al256(p + sizeof(double) * op.nnz);
-  c.rblk = (long long*)p;
+  c.rblk = (long long*)p; p = al256(p + sizeof(long long) * (ceil_div(op.n, (long long)RJ_NT) + 1));
+  c.empty = (int32_t*)p; p = al256(p + sizeof(int32_t) * op.nseg);
+  c.nempty = (unsigned int*)p;
   return c;
 }
 
 cudaError_t launch_cscj_build(const CsrOp& op, const uint8_t* keep, const int32_t* J, long long p,
                               const CscJ& c, cudaStream_t stream) {
   const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
+  cudaError_t e0 = cudaMemsetAsync(c.nempty, 0, sizeof(unsigned int), stream);
+  if (e0 != cudaSuccess) return e0;
   note_launch();
   index_map_kernel<<<(unsigned)ceil_div(std::max(p, 1LL), 256LL), 256, 0, stream>>>(J, p, c.posJ);
   note_launch();
   cscj_count_kernel<<<(unsigned)nblk, CJ_WARPS * 32, 0, stream>>>(
-      op.seg_beg, op.seg_end, op.nseg, op.rowidx, keep, c.cnt, c.blk, c.ticket, (int)nblk);
+      op.seg_beg, op.seg_end, op.nseg, op.rowidx, keep, c.cnt, c.blk, c.ticket, (int)nblk,
+      c.empty, c.nempty);
   note_launch();
   cscj_fill_kernel<<<(unsigned)nblk, CJ_WARPS * 32, 0, stream>>>(
       op.seg_beg, op.seg_end, op.nseg, op.rowidx, op.valt, op.row_sign, keep, c.posJ, c.cnt,
@@ -698,23 +776,21 @@ cudaError_t launch_cscj_xt(const CsrOp& op, const CscJ& c, const double* w, doub
                            double* part, cudaStream_t stream) {
   const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
   const long long* total = c.blk + nblk;  // kept entries (cscj_count_kernel)
-  // segments without kept entries are never visited: start from zero
-  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * op.q, stream);
-  if (e == cudaSuccess && op.nslots > 0)
-    e = cudaMemsetAsync(part, 0, sizeof(double) * op.nslots, stream);
-  if (e != cudaSuccess) return e;
+  // segments without kept entries are never visited by the chunks: the fix kernel
+  // writes their zeros from the build's list
   const long long nch_max = ceil_div(op.nnz, (long long)CH);
   const unsigned grid = (unsigned)std::max(1LL, std::min(ceil_div(nch_max, 8LL), 148LL * 8));
   note_launch();
   cscj_xt_kernel<<<grid, 256, 0, stream>>>(total, c.seg, c.pos, c.val, op.seg_col, op.seg_slot,
                                            w, out, part, c.cval, c.ctail, c.cflag);
   note_launch();
-  cscj_fix_kernel<<<(unsigned)std::max(1LL, std::min(ceil_div(nch_max, 256LL), 148LL * 4)), 256,
+  cscj_fix_kernel<<<(unsigned)std::max(1LL, std::min(ceil_div(std::max(nch_max, (long long)op.nseg), 256LL),
+                                                      148LL * 4)), 256,
                     0, stream>>>(total, c.seg, op.seg_col, op.seg_slot, c.cval, c.ctail, c.cflag,
-                                 out, part);
+                                 out, part, c.empty, c.nempty);
   if (op.nfold > 0) {
     note_launch();
-    csc_fold_kernel<<<(unsigned)ceil_div(op.nfold, 256LL), 256, 0, stream>>>(
+    csc_fold_kernel<<<(unsigned)ceil_div(op.nfold * 32, 256LL), 256, 0, stream>>>(
         op.fold_col, op.fold_beg, op.nfold, part, out);
   }
   return cudaGetLastError();

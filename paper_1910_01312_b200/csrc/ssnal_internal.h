@@ -54,6 +54,8 @@ struct CscJ {
   int32_t* ridx;
   double* rval;
   long long* rblk; // per-block row-length offsets
+  int32_t* empty;  // segments without kept entries (written as zeros by every product)
+  unsigned int* nempty;
 };
 size_t cscj_ws_bytes(const CsrOp& op);
 CscJ cscj_layout(const CsrOp& op, void* ws);
@@ -63,6 +65,9 @@ cudaError_t launch_cscj_xt(const CsrOp& op, const CscJ& c, const double* w, doub
                            double* part, cudaStream_t stream);
 cudaError_t launch_csrj_xd(const CscJ& c, long long p, const double* d, double* out,
                            cudaStream_t stream);
+cudaError_t launch_csrj_xd_dot(const CscJ& c, long long p, const double* d, double* out,
+                               const double* wdot, double* dot_out, double* part,
+                               int max_blocks, unsigned int* ticket, cudaStream_t stream);
 
 struct ProjLaunch {
   const double *A, *B, *coef, *a, *l, *u;
