@@ -127,11 +127,11 @@ def _sweep_bytes(problem):
 
 def _ncu_traffic():
     """DRAM read + write bytes per launch of the committed ncu --set full capture of
-    the per-Newton-step sweep stream_xd_kernel<2> (X [t, r]; profiles/r1_ncu_stream_xd2.txt),
+    the per-Newton-step sweep stream_xd_kernel<2> (X [t, r]; profiles/r1_ncu_stream_xd_kernel.txt),
     or None."""
     try:
         vals = {}
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_stream_xd2.txt")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_stream_xd_kernel.txt")) as fh:
             for line in fh:
                 parts = line.split()
                 if parts and parts[0] == "raw" and parts[1].startswith("dram__bytes_"):
