@@ -185,8 +185,7 @@ __device__ __forceinline__ void tc_dmma(double& c0, double& c1, double a, double
 // index a compile-time constant (no local-memory arrays)
 template <int J>
 __device__ __forceinline__ void tc_diag_step(double (&r)[TC_NB], int lane, int k0, double* rdg,
-                                             int* fail) {
-  double d = __shfl_sync(0xffffffffu, r[J], J);
+                                             int* fail, double d) {
   if (!(d > 0.0)) {
     if (lane == 0 && *fail == 0) *fail = k0 + J + 1;
     d = 1.0;
@@ -199,12 +198,17 @@ __device__ __forceinline__ void tc_diag_step(double (&r)[TC_NB], int lane, int k
   } else if (lane > J) {
     r[J] *= inv;
   }
+  // next pivot first: lane J+1 updates its own diagonal from its own L[J+1][J] (the
+  // same fma the column loop below performs for c = J+1, so bit-identical) and
+  // broadcasts it before the loop's shuffles -- one shuffle off the serial chain
+  double dn = 0.0;
+  if constexpr (J + 1 < TC_NB) dn = __shfl_sync(0xffffffffu, fma(-r[J], r[J], r[J + 1]), J + 1);
 #pragma unroll
   for (int c = J + 1; c < TC_NB; ++c) {
     const double lcj = __shfl_sync(0xffffffffu, r[J], c);
     if (lane >= c) r[c] = fma(-r[J], lcj, r[c]);
   }
-  if constexpr (J + 1 < TC_NB) tc_diag_step<J + 1>(r, lane, k0, rdg, fail);
+  if constexpr (J + 1 < TC_NB) tc_diag_step<J + 1>(r, lane, k0, rdg, fail, dn);
 }
 
 // factor the 16x16 diagonal block at (k0, k0) in place (warp-wide call)
@@ -214,7 +218,7 @@ __device__ __forceinline__ void tc_factor_diag(double* S, int ld, int k0, int la
 #pragma unroll
   for (int c = 0; c < TC_NB; ++c)
     r[c] = (lane < TC_NB && c <= lane) ? S[(k0 + lane) * ld + k0 + c] : 0.0;
-  tc_diag_step<0>(r, lane, k0, rdg, fail);
+  tc_diag_step<0>(r, lane, k0, rdg, fail, __shfl_sync(0xffffffffu, r[0], 0));
   if (lane < TC_NB) {
 #pragma unroll
     for (int c = 0; c < TC_NB; ++c)
@@ -429,8 +433,7 @@ static constexpr int BG_NT = 256;
 
 template <int J>
 __device__ __forceinline__ void bg_diag_step(double (&r)[BG_NB], int lane, double* rd, int k0,
-                                             int* fail) {
-  double d = __shfl_sync(0xffffffffu, r[J], J);
+                                             int* fail, double d) {
   if (!(d > 0.0)) {
     if (lane == 0 && *fail == 0) *fail = k0 + J + 1;
     d = 1.0;
@@ -443,12 +446,15 @@ __device__ __forceinline__ void bg_diag_step(double (&r)[BG_NB], int lane, doubl
   } else if (lane > J) {
     r[J] *= inv;
   }
+  // next pivot broadcast ahead of the column loop (as tc_diag_step)
+  double dn = 0.0;
+  if constexpr (J + 1 < BG_NB) dn = __shfl_sync(0xffffffffu, fma(-r[J], r[J], r[J + 1]), J + 1);
 #pragma unroll
   for (int c = J + 1; c < BG_NB; ++c) {
     const double lcj = __shfl_sync(0xffffffffu, r[J], c);
     if (lane >= c) r[c] = fma(-r[J], lcj, r[c]);
   }
-  if constexpr (J + 1 < BG_NB) bg_diag_step<J + 1>(r, lane, rd, k0, fail);
+  if constexpr (J + 1 < BG_NB) bg_diag_step<J + 1>(r, lane, rd, k0, fail, dn);
 }
 
 __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M, int m,
@@ -477,7 +483,7 @@ __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M,
       for (int c = 0; c < BG_NB; ++c)
         r[c] = (lane < kb && c < kb && c <= lane) ? M[(long long)(k0 + lane) * m + k0 + c]
                                                   : (lane == c ? 1.0 : 0.0);
-      bg_diag_step<0>(r, lane, rd, k0, &fail);
+      bg_diag_step<0>(r, lane, rd, k0, &fail, __shfl_sync(0xffffffffu, r[0], 0));
       __syncwarp();
       if (lane < kb) {
 #pragma unroll

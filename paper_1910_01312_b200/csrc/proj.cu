@@ -730,7 +730,11 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
   double c = hint, lo = -INFINITY, hi = INFINITY, lam = 0.0, tmin = INFINITY, tmax = -INFINITY;
   int status = PROJ_NEWTON, passes = 0;
   const int ops[8] = {0, 0, 0, 1, 2, 1, 2, 0};
+  bool empty = false;
   for (int pass = 0; status == PROJ_NEWTON && pass < CL_MAX_PASSES; ++pass) {
+    // slots 5-7 (breakpoint range, active-slot count) do not depend on c: reduced and
+    // exchanged on pass 0 only; later passes carry the five Newton quantities
+    const int nv = pass == 0 ? 8 : 5;
     double vals[8] = {0.0, 0.0, 0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0.0};
 #pragma unroll
     for (int k = 0; k < CL_EPT; ++k) {
@@ -744,9 +748,11 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
       if (ta < c && c <= tb) vals[2] += a2;
       if (ta > c) vals[3] = fmin(vals[3], ta); else if (ta < c) vals[4] = fmax(vals[4], ta);
       if (tb > c) vals[3] = fmin(vals[3], tb); else if (tb < c) vals[4] = fmax(vals[4], tb);
-      vals[5] = fmin(vals[5], ta);
-      vals[6] = fmax(vals[6], tb);
-      vals[7] += 1.0;
+      if (pass == 0) {
+        vals[5] = fmin(vals[5], ta);
+        vals[6] = fmax(vals[6], tb);
+        vals[7] += 1.0;
+      }
     }
     // warp trees, then slot k folded across warps by thread k (block_reduce's order) and
     // pushed straight into slot [rank] of every CTA of the cluster; after the cluster
@@ -755,12 +761,13 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
     const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
+      if (k >= nv) break;
       const double w = ops[k] == 0 ? warp_sum(vals[k]) : (ops[k] == 1 ? warp_min(vals[k]) : warp_max(vals[k]));
       if (lane == 0) red[k * 32 + warp] = w;
     }
     __syncthreads();
     const int buf = pass & 1;
-    if (tid < 8) {
+    if (tid < nv) {
       const int op = (tid == 3 || tid == 5) ? 1 : ((tid == 4 || tid == 6) ? 2 : 0);  // = ops[tid]
       double r = red[tid * 32];
       for (int w = 1; w < CL_NT / 32; ++w) {
@@ -774,7 +781,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
     if (warp == 0) {
       // lane k < 8 folds slot k over the ranks (fixed order), lane 0 runs the update
       double r = 0.0;
-      if (lane < 8) {
+      if (lane < nv) {
         const int op = (lane == 3 || lane == 5) ? 1 : ((lane == 4 || lane == 6) ? 2 : 0);
         r = gath[buf][0][lane];
         for (int q = 1; q < CL_CTAS; ++q) {
@@ -786,8 +793,8 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
 #pragma unroll
       for (int k = 0; k < 8; ++k) res_[k] = __shfl_sync(0xffffffffu, r, k);
       if (lane == 0) {
-        if (pass == 0) { tmin = res_[5]; tmax = res_[6]; }
-        if (res_[7] == 0.0) {
+        if (pass == 0) { tmin = res_[5]; tmax = res_[6]; empty = res_[7] == 0.0; }
+        if (empty) {
           lam = 0.0;
           status = PROJ_DONE;
         } else {
