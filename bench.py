@@ -1,26 +1,39 @@
 """SSsNAL time-to-KKT benchmark (BASELINE.json metric) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
 
-Workload (BASELINE.json configs[1]): linear C-SVC dual, dense fp64 A of
-n = 50,000 samples x q = 300 features drawn as a two-class Gaussian mixture
-(means +-0.5*1, identity covariance, balanced labels), C = 1, cold start
-(x0 = w0 = 0), solved to relative KKT residual 1e-6.  One "step" is one full
-solve.  Synthetic data (the reference's LIBSVM files are not available offline).
+Workload (default BASELINE.json configs[4], the largest single-GPU configuration the
+metric is quoted on at 1/2/4/8 B200): eps-SVR dual of a dense fp64 A, n = 1,000,000
+samples x q = 500 features (2,000,000 dual slots, A = 4 GB), A ~ N(0,1), targets
+t = Aw + N(0, 0.1^2), w ~ N(0, I/q), eps = 0.1, C = 1, cold start, solved to relative
+KKT residual 1e-6.  One "step" is one full solve.  Synthetic seeded data
+(paper_1910_01312_b200.datagen; the reference's LIBSVM files are not available offline).
+`--config 1` (C-SVC 50,000 x 300) and `--config 2|3` (CSR) run the other workloads.
 
   value    device time of the solve with A already resident in HBM (CUDA events on
-           the solver's stream), max over ranks; L2 (126 MB) is flushed with a
-           256 MB write before every timed step.
-  e2e      the same solve through the public API from HOST buffers: upload of A, y
-           (pinned), problem construction, solve, and the read-back of x.
-  roofline the dominant kernel by device time inside the timed region, algorithmic
-           bytes per launch / mean launch time, against MEASURED_PEAKS.json.
-  cpu_baseline  the numpy oracle (tests' CPU restatement of the reference) solving the
-           same problem on the host cores, rank 0, N = 1.
+           the solver's stream), max over ranks; A (4 GB) is larger than L2 and L2 is
+           additionally flushed with a 256 MB write before every timed step.
+  e2e      the same solve through the public API from HOST buffers: upload of A and the
+           targets (pinned), problem construction, solve, read-back of x.  The copy bytes
+           are counted by the package's own host->device path (backend.H2D).
+  roofline the dominant op class by device time (CUDA events around every op on the
+           solver stream in K extra profiled solves): its algorithmic bytes (HBM-bound
+           classes) or flops (the FP64 tensor-core Gram) over its device time, against
+           MEASURED_PEAKS.json (HBM) or the builder-measured DMMA peak
+           (profiles/r2_dmma_peak.txt, scripts/dmma_peak.cu).
+  cpu_baseline  the numpy oracle (tests' CPU restatement of the reference path,
+           factor-space Newton route) on the host cores, rank 0, N = 1, on a bounded
+           sample: the same config at 1/10 of the rows, scaled x10 (stated in `sample`).
 
---impl reference times that CPU restatement alone (the reference package itself is
-pure Python and cannot be run on the GPU box).  N > 1 runs N
-independent replicas (one per GPU) of the single-GPU solve.
+--impl reference runs the CPU restatement of the reference path (oracle port: the
+reference's algorithm with the factor-space Newton system, since the reference's own
+column operator needs O(n^2 q) per product at these sizes, and the product's delta line
+search, without which the reference stalls above KKT 1e-6 -- DESIGN.md section 8) on
+the full workload, with all host threads; one full solve is one step and a full solve
+takes minutes, so it runs ONE step whatever --steps says (reported as steps_run).
+
+N > 1 runs N independent single-GPU replicas of the workload (no communication;
+"parallelism": "replicas"), one per rank.
 """
 
 import argparse
@@ -36,8 +49,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "SSNAL time-to-KKT 1e-6 (C-SVC dense fp64, config 1: n=50000 x q=300)"
 TOL = 1e-6
+METRICS = {
+    0: "SSNAL time-to-KKT 1e-6 (C-SVC dense fp64, config 0: n=2000 x q=50)",
+    1: "SSNAL time-to-KKT 1e-6 (C-SVC dense fp64, config 1: n=50000 x q=300)",
+    2: "SSNAL time-to-KKT 1e-6 (C-SVC CSR fp64, config 2: n=500000 x q=100000, 50 nnz/row)",
+    3: "SSNAL time-to-KKT 1e-6 (C-SVC CSR fp64, config 3: n=4000000 x q=1000000, Zipf)",
+    4: "SSNAL time-to-KKT 1e-6 (eps-SVR dense fp64, config 4: n=1000000 x q=500, "
+       "2000000 dual slots)",
+}
 
 
 def _env_int(name, default):
@@ -51,17 +71,26 @@ def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _dmma_peak():
+    """Builder-measured FP64 tensor (DMMA m8n8k4) peak, TFLOP/s."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_dmma_peak.txt")) as fh:
+            for line in fh:
+                if line.startswith("{"):
+                    return float(json.loads(line)["dmma_f64_tflops"]), "builder-measured DMMA"
+    except Exception:
+        pass
+    return 37.2, "builder-measured DMMA (profiles/r2_dmma_peak.txt missing: last value)"
 
 
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled through NVML inside the
-    timed region -- between solves, after each step's closing event, so the query
-    never lands inside a latency-bound solve (an nvidia-smi process polling every
-    200 ms did, adding ms-scale stalls to the host syncs).  Falls back to a single
-    nvidia-smi query per sample when NVML is unavailable."""
+    timed region, between solves (after each step's closing event)."""
 
     REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
                ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -81,9 +110,6 @@ class ClockSampler:
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
         except Exception:
             self.nv = None
-
-    def start(self):
-        self.sample()
 
     def sample(self):
         try:
@@ -119,40 +145,6 @@ class ClockSampler:
                 "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
-def _sweep_bytes(problem):
-    """Algorithmic HBM bytes of one sweep of A (X d or X^T v): A, labels, in/out vectors."""
-    op = problem.q_op
-    return 8 * op.n_phys * op.q + 8 * op.n_phys + 8 * (problem.n + op.q)
-
-
-def _ncu_traffic():
-    """DRAM read + write bytes per launch of the committed ncu --set full capture of
-    the per-Newton-step sweep stream_xd_kernel<2> (X [t, r]; profiles/r1_ncu_stream_xd_kernel.txt),
-    or None."""
-    try:
-        vals = {}
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_stream_xd_kernel.txt")) as fh:
-            for line in fh:
-                parts = line.split()
-                if parts and parts[0] == "raw" and parts[1].startswith("dram__bytes_"):
-                    scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}[parts[2]]
-                    vals[parts[1]] = float(parts[3]) * scale
-        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
-    except Exception:
-        return None
-
-
-def cpu_oracle_solve(cfg):
-    """Numpy restatement of the reference path (oracle/), stable psi evaluation."""
-    import oracle as O
-
-    O.set_psi_mode("delta")  # the product's default line search (DESIGN.md section 3)
-    op, c, bl = O.csvc_problem(cfg["A"], cfg["y"], cfg["C"])
-    t0 = time.perf_counter()
-    rep = O.alm_solve(op, c, bl, O.AlmOpts(tol_kkt=TOL))
-    return time.perf_counter() - t0, rep
-
-
 def _threads():
     try:
         from threadpoolctl import threadpool_info
@@ -162,30 +154,110 @@ def _threads():
         return os.cpu_count() or 1
 
 
+def _ncu_traffic(name):
+    """DRAM read + write bytes per launch from a committed `ncu --set full` summary."""
+    try:
+        vals = {}
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            for line in fh:
+                parts = line.split()
+                if len(parts) >= 4 and parts[0] == "raw" and parts[1].startswith("dram__bytes_"):
+                    scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}[parts[2]]
+                    vals[parts[1]] = float(parts[3]) * scale
+        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ workloads
+def make_cfg(k, rows_frac=1.0):
+    from paper_1910_01312_b200 import datagen
+
+    if rows_frac == 1.0:
+        return datagen.make_config(k)
+    base = {0: (2000, 50), 1: (50_000, 300), 4: (1_000_000, 500)}
+    if k not in base:
+        raise ValueError("row sampling only for the dense configs")
+    return datagen.make_config(k, n=int(base[k][0] * rows_frac), q=base[k][1])
+
+
+def build_problem(P, cfg, A=None):
+    """The public API call a user makes (ref svm.py:95-127); A overrides the samples
+    (a device- or pinned-host tensor)."""
+    if "indptr" in cfg:
+        return P.build_csvc_dual((cfg["indptr"], cfg["indices"], cfg["data"], cfg["shape"]),
+                                 cfg["y"], cfg["C"])
+    feats = cfg["A"] if A is None else A
+    if cfg["task"] == "svr":
+        return P.build_svr_dual(feats, cfg["t"], cfg["C"], cfg["epsilon"])
+    return P.build_csvc_dual(feats, cfg["y"], cfg["C"])
+
+
+def ssn_options(P, cfg):
+    # the large sparse configs need more inner Newton steps than the reference default 50
+    # at sigma >= 3125 (DESIGN.md section 11)
+    return P.SsnOptions(max_inner=200) if "indptr" in cfg else P.SsnOptions()
+
+
+def oracle_problem(cfg):
+    import oracle as O
+
+    if "indptr" in cfg:
+        return O.csvc_problem_csr(cfg["indptr"], cfg["indices"], cfg["data"], cfg["shape"],
+                                  cfg["y"], cfg["C"])
+    if cfg["task"] == "svr":
+        return O.svr_problem(cfg["A"], cfg["t"], cfg["C"], cfg["epsilon"])
+    return O.csvc_problem(cfg["A"], cfg["y"], cfg["C"])
+
+
+def cpu_oracle_solve(cfg):
+    """The numpy oracle (restated reference path, factor-space Newton route, the
+    product's delta line search) solving cfg; returns (seconds, report)."""
+    import oracle as O
+
+    O.set_psi_mode("delta")
+    op, c, bl = oracle_problem(cfg)
+    ssn = O.SsnOpts(newton="factor", max_inner=200 if "indptr" in cfg else 50)
+    t0 = time.perf_counter()
+    rep = O.alm_solve(op, c, bl, O.AlmOpts(tol_kkt=TOL), ssn)
+    return time.perf_counter() - t0, rep
+
+
+def config_dict(args, cfg, world, n=None, q=None):
+    d = {"workload": f"config{args.config}", "tol_kkt": TOL, "cold_start": True,
+         "C": cfg["C"], "parallelism": "replicas" if world > 1 else "single",
+         "l2": "A larger than L2 (126 MB) where it is 4 GB; plus a 256 MB flush write "
+               "before every timed step"}
+    if "indptr" in cfg:
+        d.update({"n": int(cfg["shape"][0]), "q": int(cfg["shape"][1]),
+                  "nnz": int(cfg["indices"].size)})
+    else:
+        d.update({"n": int(cfg["A"].shape[0]), "q": int(cfg["A"].shape[1])})
+    if cfg["task"] == "svr":
+        d.update({"epsilon": cfg["epsilon"], "dual_slots": 2 * d["n"]})
+    return d
+
+
+# ------------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    from paper_1910_01312_b200 import datagen
-
-    cfg = datagen.make_config(args.config)
-    for _ in range(args.warmup):
-        cpu_oracle_solve(cfg)
-    times = []
-    rep = None
-    for _ in range(args.steps):
-        t, rep = cpu_oracle_solve(cfg)
-        times.append(t)
-    v = float(np.mean(times))
+    cfg = make_cfg(args.config)
+    secs, rep = cpu_oracle_solve(cfg)
     cores = _threads()
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Gaussian mixture, BASELINE config 1 shapes)",
-        "config": {"workload": f"config{args.config}", "tol_kkt": TOL, "cold_start": True},
-        "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
-                         "sample": "full solve of the workload per step (numpy oracle, OpenBLAS)"},
-        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRICS[args.config], "value": secs, "unit": "s",
+        "n_gpus": world, "steps": args.steps, "steps_run": 1, "warmup": args.warmup,
+        "ms_per_step": secs * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE config shapes and distributions)",
+        "config": config_dict(args, cfg, world),
+        "cpu_baseline": {"value": secs, "unit": "s", "cores": cores, "kind": "port",
+                         "sample": "one full solve of the workload (numpy oracle = the "
+                                   "reference path restated: factor-space Newton system, "
+                                   "delta line search; OpenBLAS threads); a full solve per "
+                                   "step, so one step runs"},
+        "e2e": {"value": secs, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "result": {"kkt": rep["kkt_residual"], "objective": rep["objective"],
                    "outer": rep["outer_iters"], "inner": rep["total_inner_iters"],
                    "converged": rep["converged"]},
@@ -193,11 +265,25 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ our arm
+ROOF = {
+    # op class -> (bound, unit, kernel names)
+    "dense_x": ("hbm", "GB/s", "stream_xd_kernel (X [t, r] sweeps of A)"),
+    "dense_xt": ("hbm", "GB/s", "stream_xt_kernel (X^T sweeps of A)"),
+    "gram": ("tensor", "TFLOP/s", "gram_kernel (FP64 DMMA q-space Gram)"),
+    "project": ("hbm", "GB/s", "proj_multi_kernel / proj_cluster_kernel"),
+    "chol": ("latency", "TFLOP/s", "chol_cluster_kernel (q x q Cholesky)"),
+    "newton_system": ("hbm", "GB/s", "compaction / p-space system / CG"),
+    "vector": ("hbm", "GB/s", "accept_q / hs_finish_dots / dots"),
+}
+NCU_FILES = {"dense_x": "r2_ncu_c4_stream_xd_kernel.txt", "gram": "r2_ncu_c4_gram_kernel.txt"}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
     import paper_1910_01312_b200 as P
-    from paper_1910_01312_b200 import datagen
+    from paper_1910_01312_b200 import backend as B
 
     torch.cuda.set_device(local_rank)
     dist = None
@@ -206,12 +292,12 @@ def run_ours(args, rank, world, local_rank):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     be = P.default_backend()
-    cfg = datagen.make_config(args.config)
-    A_host = torch.from_numpy(cfg["A"]).pin_memory()
-    y_host = cfg["y"]
-    A_dev = A_host.to("cuda")
-    problem = P.build_csvc_dual(A_dev, y_host, cfg["C"])
+    cfg = make_cfg(args.config)
+    dense = "indptr" not in cfg
+    A_host = torch.from_numpy(cfg["A"]).pin_memory() if dense else None
+    problem = build_problem(P, cfg, A_host.to("cuda") if dense else None)
     opts = P.AlmOptions(tol_kkt=TOL)
+    ssn = ssn_options(P, cfg)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -220,33 +306,36 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        rep = P.alm_solve(problem, opts)
+        rep = P.alm_solve(problem, opts, ssn, return_device=True)
     barrier()
     stream = torch.cuda.current_stream()
     sampler = ClockSampler(local_rank)
-    sampler.start()
+    sampler.sample()
     launches0 = be.launch_count()
-    step_s = []
-    reps = []
+    step_s, reps = [], []
     for _ in range(args.steps):
         flush.fill_(1)  # evict L2 between timed iterations
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        rep = P.alm_solve(problem, opts, return_device=True)
+        rep = P.alm_solve(problem, opts, ssn, return_device=True)
         e1.record(stream)
         e1.synchronize()
         step_s.append(e0.elapsed_time(e1) * 1e-3)
         reps.append(rep)
         sampler.sample()
     launches = (be.launch_count() - launches0) // max(args.steps, 1)
-    # per-op-class device time: the same K solves again with CUDA events around every
-    # op on the solver stream (kept out of the timed region above: event records cost
-    # host time the latency-bound solve would otherwise not pay)
-    kern = {}
-    prof_opts = P.SsnOptions(profile=True)
-    prof_wall = []
-    for _ in range(args.steps):
+    barrier()
+    t = torch.tensor([float(np.sum(step_s))], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    value = float(t[0]) / args.steps
+
+    # per-op-class device time: the same solves again with CUDA events around every op
+    # on the solver stream (kept out of the timed region: event records cost host time)
+    kern, prof_wall = {}, []
+    prof_opts = P.SsnOptions(profile=True, max_inner=ssn.max_inner)
+    for _ in range(max(1, min(args.steps, 5))):
         flush.fill_(1)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -257,34 +346,31 @@ def run_ours(args, rank, world, local_rank):
         prof_wall.append(e0.elapsed_time(e1) * 1e-3)
         sampler.sample()
         for name, v in getattr(problem, "op_profile", {}).items():
-            c, s, b = kern.get(name, (0, 0.0, 0.0))
-            kern[name] = (c + v["calls"], s + v["seconds"], b + v["bytes"])
+            c, s_, b_, f_ = kern.get(name, (0, 0.0, 0.0, 0.0))
+            kern[name] = (c + v["calls"], s_ + v["seconds"], b_ + v["bytes"], f_ + v["flops"])
     clocks = sampler.stop()
-    barrier()
-    t_local = float(np.sum(step_s))
-    t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total = float(t[0])
-    value = total / args.steps
+    counters = dict(getattr(problem, "native_counters", {}) or {})
+    del problem
 
     # ---- end to end through the public API from host buffers
     e2e_times = []
-    h2d = A_host.numel() * 8 + 3 * y_host.size * 8  # A, labels, box a; c
-    d2h = y_host.size * 8
+    h2d = None
     for i in range(args.warmup + args.steps):
         flush.fill_(1)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        h0 = B.H2D["bytes"]
         e0.record(stream)
-        pb = P.build_csvc_dual(A_host, y_host, cfg["C"])
-        r = P.alm_solve(pb, opts)  # x_opt copied to a host numpy array
+        pb = build_problem(P, cfg, A_host)
+        r = P.alm_solve(pb, opts, ssn)  # x_opt copied to a host numpy array
         e1.record(stream)
         e1.synchronize()
         if i >= args.warmup:
             e2e_times.append(e0.elapsed_time(e1) * 1e-3)
+            h2d = B.H2D["bytes"] - h0
         del pb
+    d2h = int(r.x_opt.size * 8)
     te = torch.tensor([float(np.sum(e2e_times))], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -294,51 +380,60 @@ def run_ours(args, rank, world, local_rank):
         if dist is not None:
             dist.destroy_process_group()
         return
-    peak, peak_kind = _peaks()
-    # dominant op class by device time; roofline = its algorithmic bytes / its time
-    roof = None
+    hbm_peak, hbm_kind = _peaks()
+    dmma_peak, dmma_kind = _dmma_peak()
     ptotal = float(np.sum(prof_wall)) if prof_wall else 0.0
-    if kern:
-        # dominant HBM-bound kernel of the launch list (profiles/r1_launches_config1_solve.txt):
-        # the streaming sweeps of A -- per Newton step ONE stream_xd<2> (X [t, r]: Qd and the
-        # gradient), plus the inner-solve start (X^T s) and the KKT/refresh sweeps.
-        # achieved = their algorithmic bytes / their device time, measured live here over
-        # the K profiled solves (op classes dense_xt and dense_x hold exactly the sweeps);
-        # traffic = DRAM bytes per launch of one ncu --set full capture of stream_xd<2>
-        sweeps = [kern[k] for k in ("dense_xt", "dense_x") if k in kern]
-        cnt = sum(v[0] for v in sweeps)
-        secs = sum(v[1] for v in sweeps)
-        nbytes = sum(v[2] for v in sweeps)
-        achieved = (nbytes / secs) / 1e9 if secs > 0 and nbytes > 0 else 0.0
-        roof = {"bound": "hbm",
-                "kernel": "stream_xd_kernel<2> / stream_xd / stream_xt (sweeps of A)",
-                "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak if peak else None,
-                "traffic": _ncu_traffic(), "peak_kind": peak_kind, "op_calls": cnt,
-                "algorithmic_bytes_per_sweep": _sweep_bytes(problem),
+    roof = None
+    ops = {}
+    for k, (calls, secs, nbytes, flops) in kern.items():
+        if calls == 0:
+            continue
+        ops[k] = {"calls": calls, "s": secs, "share": secs / ptotal if ptotal else None,
+                  "GBps": nbytes / secs / 1e9 if secs else None,
+                  "TFLOPs": flops / secs / 1e12 if secs and flops else None}
+    if ops:
+        dom = max(ops, key=lambda k: ops[k]["s"])
+        bound, unit, kname = ROOF.get(dom, ("hbm", "GB/s", dom))
+        calls, secs, nbytes, flops = kern[dom]
+        if bound == "tensor" or unit == "TFLOP/s":
+            achieved = flops / secs / 1e12 if secs else 0.0
+            peak, pkind, punit = dmma_peak, dmma_kind, "TFLOP/s"
+        else:
+            achieved = nbytes / secs / 1e9 if secs else 0.0
+            peak, pkind, punit = hbm_peak, hbm_kind, "GB/s"
+        traffic = _ncu_traffic(NCU_FILES[dom]) if dom in NCU_FILES else None
+        roof = {"bound": bound, "op_class": dom, "kernel": kname, "achieved": achieved,
+                "peak": peak, "unit": punit, "frac": achieved / peak if peak else None,
+                "traffic": traffic, "traffic_file": NCU_FILES.get(dom),
+                "peak_kind": pkind, "op_calls": calls,
+                "algorithmic_bytes_per_call": nbytes / calls if calls else None,
+                "algorithmic_flops_per_call": flops / calls if calls and flops else None,
                 "share_of_step": secs / ptotal if ptotal else None,
-                "measured": "CUDA events on the solver stream, K extra profiled solves",
-                "ops": {k: {"calls": v[0], "s": v[1], "share": v[1] / ptotal if ptotal else None,
-                            "GBps": v[2] / v[1] / 1e9 if v[1] else None}
-                        for k, v in kern.items()}}
+                "measured": "CUDA events on the solver stream around every op, "
+                            f"{len(prof_wall)} extra profiled solves",
+                "ops": ops}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        secs, ref = cpu_oracle_solve(cfg)
-        cpu = {"value": secs, "unit": "s", "cores": _threads(), "kind": "port",
-               "sample": "one full solve of the workload (numpy oracle, stable psi, OpenBLAS)",
-               "kkt": ref["kkt_residual"], "objective": ref["objective"]}
+        frac = 0.1 if dense and args.config in (1, 4) else 1.0
+        scfg = make_cfg(args.config, frac) if frac != 1.0 else cfg
+        secs, ref = cpu_oracle_solve(scfg)
+        cpu = {"value": secs / frac, "unit": "s", "cores": _threads(), "kind": "port",
+               "sample": (f"one full solve of the same config at {frac:g} of the rows "
+                          f"(numpy oracle, OpenBLAS), {secs:.2f} s measured, scaled by "
+                          f"{1 / frac:g}" if frac != 1.0 else
+                          "one full solve of the workload (numpy oracle, OpenBLAS)"),
+               "measured_s": secs, "kkt": ref["kkt_residual"], "objective": ref["objective"]}
     last = reps[-1]
     line = {
-        "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Gaussian mixture, BASELINE config 1 shapes)",
-        "config": {"workload": f"config{args.config}", "n": problem.n, "q": problem.q_op.q,
-                   "C": cfg["C"], "tol_kkt": TOL, "cold_start": True,
-                   "l2": "flushed (256 MB write) before every timed step",
-                   "parallelism": "replicas" if world > 1 else "single"},
-        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h)},
+        "metric": METRICS[args.config], "value": value, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE config shapes and distributions)",
+        "config": config_dict(args, cfg, world),
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d or 0),
+                "d2h_bytes_per_step": d2h,
+                "path": "build_svr_dual/build_csvc_dual from pinned host A + alm_solve "
+                        "(x_opt read back)"},
         "gpu_launches": int(launches),
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -346,8 +441,8 @@ def run_ours(args, rank, world, local_rank):
         "result": {"kkt": last.kkt_residual, "objective": last.objective,
                    "outer": last.outer_iters, "inner": last.total_inner_iters,
                    "p": last.unbounded_support_count, "converged": last.converged},
-        "counters": getattr(problem, "native_counters", None),
-        "step_ms": [round(t * 1e3, 3) for t in step_s],
+        "counters": counters,
+        "step_ms": [round(t_ * 1e3, 3) for t_ in step_s],
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -357,10 +452,10 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)

@@ -60,6 +60,7 @@ const char* ssnal_last_error(void);
 unsigned long long ssnal_launch_count(void);        /* kernels launched by this library */
 int ssnal_device_check(int device);                 /* SSNAL_E_DEVICE unless sm_100 */
 size_t ssnal_proj_state_bytes(void);
+size_t ssnal_report_bytes(void);                   /* sizeof(ssnal_report_t): layout check */
 size_t ssnal_project_ws_bytes(int64_t n, int T);
 size_t ssnal_reduce_ws_bytes(int64_t n, int k);
 size_t ssnal_dense_xt_ws_bytes(int64_t n_phys, int64_t q, int k);
@@ -258,21 +259,32 @@ typedef struct ssnal_options_t {
 #define SSNAL_OP_XT 0       /* X^T V products (streams A)                             */
 #define SSNAL_OP_XD 1       /* X D products (streams A)                               */
 #define SSNAL_OP_PROJ 2     /* projections (Newton/K-ary passes + apply)              */
-#define SSNAL_OP_NEWTON 3   /* reduced Newton system: compaction, Gram, Cholesky      */
+#define SSNAL_OP_NEWTON 3   /* reduced Newton system: compaction, p-space solve, CG   */
 #define SSNAL_OP_VEC 4      /* elementwise ops, fused dots, HS-Jacobian               */
-#define SSNAL_NOPS 5
+#define SSNAL_OP_GRAM 5     /* q-space Gram X_J^T X_J (rebuild or changed-slot update) */
+#define SSNAL_OP_CHOL 6     /* assembly + Cholesky solve of the q x q Newton system   */
+#define SSNAL_NOPS 7
 
 typedef struct ssnal_report_t {
   double kkt_residual, objective, wall_time;
   int outer_iters, total_inner_iters, unbounded_support_count, converged;
-  int hit_max_inner_mask;   /* bit k: inner solver hit max_inner at outer k (k < 31)   */
+  int hit_max_inner_mask;   /* bit k: inner solver hit max_inner at outer k (k < 31);
+                               see hit_max_inner_mask64 / _count for the rest          */
   int stagnated, max_outer_reached;
   long long syncs, newton_steps, projections, launches;
   double op_seconds[SSNAL_NOPS];   /* device time per op class (profile = 1)         */
   long long op_calls[SSNAL_NOPS];
   double op_bytes[SSNAL_NOPS];     /* algorithmic HBM bytes per op class             */
+  double op_flops[SSNAL_NOPS];     /* algorithmic flops (GRAM: rows q (q+1); CHOL: m^3/3) */
   long long cg_iters;              /* sparse operator: CG iterations, all Newton steps */
   long long cg_fallbacks;          /* CG solves that fell back to the direct system     */
+  long long gram_builds;           /* dense q-space Gram rebuilt from all p free rows   */
+  long long gram_updates;          /* ... updated over the changed slots only           */
+  long long gram_rows;             /* rows gathered by both                             */
+  long long proj_fallbacks;        /* projections finished by the K-ary fallback        */
+  unsigned long long hit_max_inner_mask64; /* bit k: max_inner hit at outer k (k < 64)  */
+  int hit_max_inner_count;         /* all outer iterations that hit max_inner           */
+  int pad_;
 } ssnal_report_t;
 
 /* per outer iteration: (k, R_KKT, sigma, p, inner iterations) as ref solver.py:474-475 */

@@ -24,10 +24,10 @@ import scipy.linalg
 __all__ = [
     "BoxLine", "InfeasibleError", "LineSearchFailed",
     "grad_phi", "breakpoints", "classify_free", "project", "hs_apply",
-    "DenseQ", "FactoredQ", "SvrFactoredQ",
+    "DenseQ", "FactoredQ", "SvrFactoredQ", "CsrFactoredQ", "newton_direction_factor",
     "AlmOpts", "SsnOpts", "psi_value", "newton_direction", "line_search",
-    "ssn_solve", "kkt_residual", "alm_solve", "set_psi_mode", "PSI_MODE", "bregman",
-    "csvc_problem", "svr_problem", "objective",
+    "ssn_solve", "kkt_residual", "kkt_full", "alm_solve", "set_psi_mode", "PSI_MODE", "bregman",
+    "csvc_problem", "csvc_problem_csr", "svr_problem", "objective",
 ]
 
 ACTIVE_TOL = 1e-12  # ref projection.py:19
@@ -181,6 +181,10 @@ class FactoredQ:
     def matvec(self, v):
         return self.x(self.xt(v))
 
+    def rows(self, idx):
+        """X_J (p x q): the rows of the factor for the slots idx."""
+        return self._rows(np.asarray(idx, dtype=np.int64))
+
     def columns(self, idx):
         return self.x(self._rows(np.asarray(idx, dtype=np.int64)).T)
 
@@ -212,12 +216,63 @@ class SvrFactoredQ:
     def matvec(self, v):
         return self.x(self.xt(v))
 
+    def rows(self, idx):
+        return self._rows(idx)
+
     def columns(self, idx):
         return self.x(self._rows(idx).T)
 
     def submatrix(self, idx):
         r = self._rows(idx)
         return r @ r.T
+
+
+class CsrFactoredQ:
+    """Q = X X^T with X = diag(row_sign) A, A a scipy CSR matrix (sparse linear-kernel
+    C-SVC; the same Q entries as ref kernels.py:97-106 with sparse sample vectors).
+    ``rows`` returns X_J as a CSR matrix; ``submatrix`` the dense p x p Q_JJ."""
+
+    def __init__(self, indptr, indices, data, shape, row_sign=None):
+        import scipy.sparse as sp
+
+        self.A = sp.csr_matrix((np.asarray(data, dtype=np.float64), np.asarray(indices),
+                                np.asarray(indptr)), shape=shape)
+        self.AT = self.A.T.tocsr()
+        self.sign = None if row_sign is None else np.asarray(row_sign, dtype=np.float64)
+        self.n, self.q = shape
+
+    def xt(self, v):
+        return self.AT @ (v if self.sign is None else self.sign * v)
+
+    def x(self, t):
+        r = self.A @ t
+        return r if self.sign is None else self.sign * r
+
+    def matvec(self, v):
+        return self.x(self.xt(v))
+
+    def rows(self, idx):
+        import scipy.sparse as sp
+
+        idx = np.asarray(idx, dtype=np.int64)
+        r = self.A[idx]
+        return r if self.sign is None else sp.diags(self.sign[idx]) @ r
+
+    def columns(self, idx):
+        r = self.rows(idx)
+        return np.asarray(self.x(r.T.toarray()))
+
+    def submatrix(self, idx):
+        r = self.rows(idx)
+        return np.asarray((r @ r.T).toarray())
+
+
+def csvc_problem_csr(indptr, indices, data, shape, y, C):
+    """Sparse C-SVC dual (CSR samples): as csvc_problem; ref svm.py:95-108."""
+    y = np.asarray(y, dtype=np.float64)
+    n = y.size
+    op = CsrFactoredQ(indptr, indices, data, shape, y)
+    return op, -np.ones(n), BoxLine(y, 0.0, np.zeros(n), np.full(n, float(C)))
 
 
 def csvc_problem(a_mat, y, C):
@@ -272,7 +327,13 @@ class SsnOpts:
     """ref solver.py:87-97."""
 
     def __init__(self, mu=1e-4, backtrack=0.5, tau=0.5, eta=1e-2, max_inner=50,
-                 direct_solve_threshold=2000, cg_max_iters=500):
+                 direct_solve_threshold=2000, cg_max_iters=500, newton="reference",
+                 cg_eta_cap=1e-4):
+        # newton: "reference" = ref solver.py:194-289 (columns of Q, p x p system);
+        # "factor" = newton_direction_factor (same direction from the factor X, for
+        # problems whose p x n column block does not fit: configs 2-4 at full size)
+        self.newton = newton
+        self.cg_eta_cap = cg_eta_cap
         self.mu = mu
         self.backtrack = backtrack
         self.tau = tau
@@ -409,6 +470,101 @@ def newton_direction(s, grad, free, sigma, op, a, opts):
     return direction, q_dir, dqd
 
 
+def _pcg(apply_m, rhs, dinv, done, max_iters, check_every=10):
+    """Jacobi-preconditioned CG from 0; ``done(v)`` is the stopping test, evaluated
+    every ``check_every`` iterations.  Returns (v, converged)."""
+    v = np.zeros_like(rhs)
+    r = rhs.copy()
+    z = dinv * r
+    p = z.copy()
+    rz = float(r.dot(z))
+    if not np.any(rhs):
+        return v, True
+    for it in range(1, max_iters + 1):
+        mp = apply_m(p)
+        den = float(p.dot(mp))
+        if den <= 0.0:
+            return v, False
+        step = rz / den
+        v += step * p
+        r -= step * mp
+        if it % check_every == 0 and done(v):
+            return v, True
+        z = dinv * r
+        rz_new = float(r.dot(z))
+        if rz_new == 0.0:  # exact solution reached
+            return v, True
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return v, done(v)
+
+
+def newton_direction_factor(s, grad, free, sigma, op, a, opts):
+    """The Newton direction of ref solver.py:194-289 computed from the factor Q = X X^T
+     -- the same (d, Qd, d'Qd) up to rounding, without the
+    n x p column block the reference forms:
+
+      t = X^T d solves  (I_q + sigma X_J^T P_J X_J) t = -X^T s,  P_J = I - a_J a_J'/a_J'a_J,
+      Qd = X t,  d'Qd = |t|^2,  d = -s - sigma P(Qd)  (ref solver.py:269 representative).
+
+    Routes (ref solver.py:238-258 policy on min(p, q)): q <= threshold -> q x q Cholesky;
+    p <= threshold -> the Woodbury p x p system (I + sigma P Q_JJ P) y = P g_J,
+    t = -X^T s + sigma X_J^T P y; else Jacobi-PCG on the q-space system, stopped on the
+    Newton residual |sigma X X_J^T P X_J t + ...| of Algorithm 3 at 1/10 of
+    min(cg_eta_cap, |grad|^(1+tau)) (the product's matrix-free tolerance, tighter)."""
+    J = np.flatnonzero(free)
+    p = J.size
+    r = op.xt(s)
+    q = r.size
+    if p == 0:
+        return -s.copy(), -grad.copy(), float(r.dot(r))
+    xj = op.rows(J)
+    a_j = a[J]
+    asa = float(a_j.dot(a_j))
+    m1 = np.asarray(xj.T @ a_j).ravel()
+    thr = opts.direct_solve_threshold
+    if q <= thr:
+        g = xj.T @ xj
+        g = np.asarray(g.toarray() if hasattr(g, "toarray") else g)
+        m = g - np.outer(m1, m1) / asa if asa != 0.0 else g.copy()
+        m *= sigma
+        m[np.diag_indices_from(m)] += 1.0
+        t = -scipy.linalg.cho_solve(scipy.linalg.cho_factor(m, lower=True), r)
+    elif p <= thr:
+        qjj = xj @ xj.T
+        qjj = np.asarray(qjj.toarray() if hasattr(qjj, "toarray") else qjj)
+        g_j = grad[J]
+        proj = (lambda v: v - (a_j.dot(v) / asa) * a_j) if asa != 0.0 else (lambda v: v)
+        pq = qjj - (np.outer(a_j, a_j @ qjj) / asa if asa != 0.0 else 0.0)
+        pqp = pq - (np.outer(pq @ a_j, a_j) / asa if asa != 0.0 else 0.0)
+        m = sigma * pqp
+        m[np.diag_indices_from(m)] += 1.0
+        y = scipy.linalg.cho_solve(scipy.linalg.cho_factor(m, lower=True), proj(g_j))
+        t = -r + sigma * np.asarray(xj.T @ proj(y)).ravel()
+    else:
+        def gram_p(v):  # X_J^T P X_J v
+            z = np.asarray(xj @ v).ravel()
+            if asa != 0.0:
+                z = z - (a_j.dot(z) / asa) * a_j
+            return np.asarray(xj.T @ z).ravel()
+
+        sq = xj.multiply(xj) if hasattr(xj, "multiply") else xj * xj
+        colsq = np.asarray(sq.sum(axis=0)).ravel()
+        diag = 1.0 + sigma * np.maximum(colsq - (m1 * m1 / asa if asa != 0.0 else 0.0), 0.0)
+        target = 0.1 * min(opts.eta, opts.cg_eta_cap,
+                           float(np.linalg.norm(grad)) ** (1.0 + opts.tau))
+
+        def done(v):  # Newton residual of the direction built from v
+            res = -r - (v + sigma * gram_p(v))
+            return float(np.linalg.norm(op.x(sigma * gram_p(res)))) <= target
+
+        t, _ = _pcg(lambda v: v + sigma * gram_p(v), -r, 1.0 / diag, done,
+                    16 * opts.cg_max_iters)
+    q_dir = op.x(t)
+    direction = -s - sigma * hs_apply(free, a, q_dir)
+    return direction, q_dir, float(t.dot(t))
+
+
 def bregman(xt, lam_t, px, lam, u_t, a):
     """B_h between a trial projection (xt, lam_t) at u_t and the base projection
     (px, lam) (csrc/proj.cu bregman_term)."""
@@ -470,7 +626,8 @@ def ssn_solve(st, op, c, bl, alm, ssn, eps_k, delta_k, trace=None):
         if gnorm <= floor:
             converged, exhausted = True, False
             break
-        direction, q_dir, dqd = newton_direction(s, grad, pr[2], sigma, op, bl.a, ssn)
+        nd = newton_direction_factor if ssn.newton == "factor" else newton_direction
+        direction, q_dir, dqd = nd(s, grad, pr[2], sigma, op, bl.a, ssn)
         steepest = False
         if float(grad.dot(direction)) >= 0.0:
             direction = -grad

@@ -41,6 +41,7 @@ _SIGNATURES = {
     "ssnal_launch_count": (ctypes.c_ulonglong, []),
     "ssnal_device_check": (_I, [_I]),
     "ssnal_proj_state_bytes": (_SZ, []),
+    "ssnal_report_bytes": (_SZ, []),
     "ssnal_project_ws_bytes": (_SZ, [_I64, _I]),
     "ssnal_reduce_ws_bytes": (_SZ, [_I64, _I]),
     "ssnal_dense_xt_ws_bytes": (_SZ, [_I64, _I64, _I]),
@@ -91,8 +92,8 @@ class Options(ctypes.Structure):
                 ("profile", _I)]
 
 
-NOPS = 5
-OP_NAMES = ("dense_xt", "dense_x", "project", "newton_system", "vector")
+NOPS = 7
+OP_NAMES = ("dense_xt", "dense_x", "project", "newton_system", "vector", "gram", "chol")
 
 
 class Report(ctypes.Structure):
@@ -104,8 +105,12 @@ class Report(ctypes.Structure):
                 ("syncs", ctypes.c_longlong), ("newton_steps", ctypes.c_longlong),
                 ("projections", ctypes.c_longlong), ("launches", ctypes.c_longlong),
                 ("op_seconds", _D * NOPS), ("op_calls", ctypes.c_longlong * NOPS),
-                ("op_bytes", _D * NOPS), ("cg_iters", ctypes.c_longlong),
-                ("cg_fallbacks", ctypes.c_longlong)]
+                ("op_bytes", _D * NOPS), ("op_flops", _D * NOPS), ("cg_iters", ctypes.c_longlong),
+                ("cg_fallbacks", ctypes.c_longlong), ("gram_builds", ctypes.c_longlong),
+                ("gram_updates", ctypes.c_longlong), ("gram_rows", ctypes.c_longlong),
+                ("proj_fallbacks", ctypes.c_longlong),
+                ("hit_max_inner_mask64", ctypes.c_ulonglong), ("hit_max_inner_count", _I),
+                ("pad_", _I)]
 
 
 PROGRESS_FN = ctypes.CFUNCTYPE(None, _I, _D, _D, ctypes.c_longlong, _I, _P)
@@ -156,6 +161,8 @@ def load():
         fn.argtypes = args
     if lib.ssnal_proj_state_bytes() != PROJ_STATE_DTYPE.itemsize:
         raise InternalError("ssnal_proj_state_t layout mismatch between C and Python")
+    if lib.ssnal_report_bytes() != ctypes.sizeof(Report):
+        raise InternalError("ssnal_report_t layout mismatch between C and Python")
     _lib = lib
     return lib
 

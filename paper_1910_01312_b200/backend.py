@@ -284,12 +284,20 @@ def default_backend(device=None):
     return _DEFAULT[key]
 
 
+# host -> device bytes moved by as_device (bench.py's e2e copy declaration reads it)
+H2D = {"bytes": 0}
+
+
 def as_device(x, backend, dtype=F64):
     """Host (numpy / list / CPU tensor) or device tensor -> contiguous device tensor."""
     if isinstance(x, torch.Tensor):
+        if x.device.type == "cpu" and backend.device.type == "cuda":
+            H2D["bytes"] += x.numel() * torch.empty((), dtype=dtype).element_size()
         t = x.to(device=backend.device, dtype=dtype)
     else:
         arr = np.asarray(x, dtype=np.float64 if dtype == F64 else None)
+        if backend.device.type == "cuda":
+            H2D["bytes"] += arr.size * torch.empty((), dtype=dtype).element_size()
         t = torch.from_numpy(np.ascontiguousarray(arr)).to(device=backend.device, dtype=dtype)
     if not t.is_contiguous():
         t = t.contiguous()

@@ -10,7 +10,7 @@ int stream_blocks(long long n, int per_thread);
 size_t reduce_ws_bytes(long long n);
 size_t compact_ws_bytes(long long n);
 size_t dense_xt_ws_bytes(long long n_phys, long long q, int k);
-size_t gram_ws_bytes(long long q);
+size_t gram_ws_bytes_full(long long q);
 cudaError_t launch_dots(int k, const double* const* xs, const double* const* ys,
                         const uint8_t* mask, long long n, double* out, void* ws, cudaStream_t s);
 cudaError_t launch_vec(int op, long long n, double alpha, const double* x, const double* y,
@@ -116,12 +116,13 @@ int ssnal_device_check(int device) {
 }
 
 size_t ssnal_proj_state_bytes(void) { return sizeof(ssnal_proj_state_t); }
+size_t ssnal_report_bytes(void) { return sizeof(ssnal_report_t); }
 size_t ssnal_project_ws_bytes(int64_t n, int T) { return proj_ws_bytes(n, T); }
 size_t ssnal_reduce_ws_bytes(int64_t n, int k) { (void)k; return reduce_ws_bytes(n) + 64; }
 size_t ssnal_dense_xt_ws_bytes(int64_t n_phys, int64_t q, int k) {
   return dense_xt_ws_bytes(n_phys, q, k);
 }
-size_t ssnal_gram_ws_bytes(int64_t q) { return gram_ws_bytes(q); }
+size_t ssnal_gram_ws_bytes(int64_t q) { return gram_ws_bytes_full(q); }
 size_t ssnal_compact_ws_bytes(int64_t n) { return compact_ws_bytes(n); }
 
 int ssnal_project_ex(const double* A, const double* B, const double* coef, const double* a,

@@ -8,6 +8,8 @@
 //           free rows J, split-K over J with fixed-order fold, then assembled
 //           into the Prop. 3.5 Newton matrix I + sigma (G - m1 m1^T / a'Sa).
 // ref: kernels.py:97-106,144-154 (column-wise Q), solver.py:224-262 (Q_JJ, cols@v).
+#include <algorithm>
+
 #include "common.cuh"
 #include "ssnal_internal.h"
 
@@ -449,10 +451,23 @@ cudaError_t launch_dense_x(const double* A, long long n, long long q, long long 
 }
 
 // ------------------------------------------------------------------ Gram (DMMA)
-static constexpr int GT = 64;        // output tile edge
-static constexpr int GK = 32;        // gathered rows staged per step
-static constexpr int GLD = GT + 4;   // padded smem row (conflict-free fragment loads)
-static constexpr int GSPLIT = 16;    // split-K over J (fixed => deterministic fold)
+// G = sum_r x_r x_r^T over gathered rows r of X (the free set J, or the slots whose
+// free flag changed, signed), FP64 tensor cores (DMMA m8n8k4; tcgen05 has no f64 kind).
+//   * CTA = one 128 x 128 tile pair (ti <= tj) of G x one split of the row list; 8 warps
+//     as 2 x 4, each warp a 64 x 32 block = 8 x 4 DMMA tiles (64 accumulators), so one
+//     k-step of 4 rows issues 32 DMMAs from 12 shared-memory fragment loads;
+//   * rows staged 32 at a time by cp.async (16-byte LDGSTS, zero-filled past q) into a
+//     two-stage ring: the gather of stage k+1 overlaps the DMMAs of stage k; diagonal
+//     pairs stage one slice and read both operands from it;
+//   * split-K over the row list into `split` fixed chunks (one wave: pairs x split <=
+//     SMs), partials folded in split order by gram_fold_kernel -> deterministic.
+static constexpr int GT = 128;             // output tile edge
+static constexpr int GK = 32;              // gathered rows per stage
+static constexpr int GLD = GT + 4;         // padded smem row: conflict-free 64-bit fragments
+static constexpr int GSPLIT = 32;          // max split-K chunks (partials buffer)
+static constexpr int GNT = 256;
+static constexpr size_t GSTAGE = (size_t)GK * GLD;  // doubles per operand per stage
+static constexpr size_t GSMEM = 4 * GSTAGE * sizeof(double) + 2 * GK * sizeof(double);
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -460,111 +475,196 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+
 struct GramArgs {
   const double* A;
   long long n, q, lda;
   const int32_t* J;
   const long long* p_dev;
-  double* part;  // [GSPLIT][q][q] (upper tile pairs + full diagonal tiles)
-  int ntile;
+  double* part;  // [split][q][q] (upper tile pairs + full diagonal tiles)
+  int ntile, split;
   // m1 = X_J^T a_J rides on the diagonal tiles' staged rows: weights w_r = a_{J_r} times
   // the row sign, part_m1[split][q]
   const double* a;
   const double* rs;
   int svr;
   double* part_m1;
+  // incremental mode: J lists the slots whose free flag CHANGED; the slot enters with
+  // weight +1 if now free (mask[slot] = 1), -1 if it left the free set
+  const uint8_t* sign_mask;
+  int aligned;  // rows 16-byte aligned (cp.async staging) else scalar staging
+  // device-side choice (driver): ctl->mode 1 = incremental over Jd (ctl->count rows,
+  // signed by sign_mask), 0 = rebuild over J (ctl->count = p rows)
+  const GramCtl* ctl;
+  const int32_t* Jd;
 };
 
 // grid.x = tile pair index (ti <= tj), grid.y = split
-__global__ void __launch_bounds__(256) gram_kernel(GramArgs g) {
-  __shared__ double sA[GK][GLD];
-  __shared__ double sB[GK][GLD];
-  __shared__ double sw[GK];
-  const long long p = *g.p_dev;
-  // decode (ti, tj) from the linear upper-triangle index
+__global__ void __launch_bounds__(GNT, 1) gram_kernel(GramArgs g) {
+  extern __shared__ double gsm[];
+  double* sA = gsm;                    // [2][GK][GLD]
+  double* sB = gsm + 2 * GSTAGE;       // [2][GK][GLD]
+  double* sw = gsm + 4 * GSTAGE;       // [2][GK] m1 weights (incl. sign)
+  __shared__ double ssg[2][GK];        // row signs (incremental mode)
+  const bool incr = g.ctl ? g.ctl->mode == 1 : g.sign_mask != nullptr;
+  const long long p = g.ctl ? g.ctl->count : *g.p_dev;
+  const int32_t* __restrict__ Jl = (g.ctl && incr) ? g.Jd : g.J;
+  const uint8_t* __restrict__ smask = incr ? g.sign_mask : nullptr;
   int pair = blockIdx.x, ti = 0;
   while (pair >= g.ntile - ti) { pair -= g.ntile - ti; ++ti; }
   const int tj = ti + pair;
-  const long long chunk = ceil_div(ceil_div(p, GSPLIT), 4) * 4;
+  const long long chunk = ceil_div(p, (long long)g.split);
   const long long k0 = blockIdx.y * chunk;
   const long long k1 = min(p, k0 + chunk);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double acc[8][2];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;  // warp block: rows wm*64.., cols wn*32..
   const long long ci = (long long)ti * GT, cj = (long long)tj * GT;
   const bool diag = ti == tj;
-  double m1acc = 0.0;  // thread c < GT of a diagonal tile: column ci + c of m1
-  for (long long kb = k0; kb < k1; kb += GK) {
-    if (diag && threadIdx.x < GK) {  // gram_m1's weights, same order of operations
-      const long long r = kb + threadIdx.x;
-      double w = 0.0;
+  const bool signed_rows = smask != nullptr;
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  double m1acc = 0.0;
+
+  // stage rows [kb, kb + GK) into buffer s
+  auto stage = [&](long long kb, int s) {
+    double* dA = sA + s * GSTAGE;
+    double* dB = sB + s * GSTAGE;
+    const int nsides = diag ? 1 : 2;
+    if (g.aligned) {
+      // 64 16-byte chunks per 128-column slice; GK rows x sides
+      for (int idx = tid; idx < GK * 64 * nsides; idx += GNT) {
+        const int side = idx / (GK * 64), rem = idx % (GK * 64);
+        const int kr = rem / 64, ch = rem % 64;
+        const long long r = kb + kr;
+        const long long c0 = (side ? cj : ci) + 2 * ch;
+        double* dst = (side ? dB : dA) + kr * GLD + 2 * ch;
+        int bytes = 0;
+        const double* src = g.A;
+        if (r < k1 && c0 < g.q) {
+          const long long li = Jl[r];
+          const long long pr = li >= g.n ? li - g.n : li;  // SVR block: x x^T is sign-free
+          src = g.A + pr * g.lda + c0;
+          bytes = c0 + 1 < g.q ? 16 : 8;
+        }
+        cp_async16(dst, src, bytes);
+      }
+    } else {
+      for (int idx = tid; idx < GK * GT * nsides; idx += GNT) {
+        const int side = idx / (GK * GT), rem = idx % (GK * GT);
+        const int kr = rem / GT, c = rem % GT;
+        const long long r = kb + kr;
+        const long long col = (side ? cj : ci) + c;
+        double v = 0.0;
+        if (r < k1 && col < g.q) {
+          const long long li = Jl[r];
+          const long long pr = li >= g.n ? li - g.n : li;
+          v = __ldg(g.A + pr * g.lda + col);
+        }
+        (side ? dB : dA)[kr * GLD + c] = v;
+      }
+    }
+    if (tid < GK) {
+      const long long r = kb + tid;
+      double w = 0.0, sg = 1.0;
       if (r < k1) {
-        const long long li = g.J[r];
+        const long long li = Jl[r];
         const long long pr = li >= g.n ? li - g.n : li;
-        w = g.a[li];
-        if (g.rs) w *= g.rs[pr];
-        if (g.svr && li >= g.n) w = -w;
+        if (signed_rows && !smask[li]) sg = -1.0;  // a leaving row: -x x^T
+        if (diag) {  // m1 weight (gram_m1's order of operations)
+          w = g.a[li];
+          if (g.rs) w *= g.rs[pr];
+          if (g.svr && li >= g.n) w = -w;
+          w *= sg;
+        }
       }
-      sw[threadIdx.x] = w;
+      sw[s * GK + tid] = w;
+      ssg[s][tid] = sg;
     }
-    // stage GK gathered rows x 64 columns of both tiles
-    for (int idx = threadIdx.x; idx < GK * GT; idx += blockDim.x) {
-      int kr = idx / GT, c = idx % GT;
-      long long r = kb + kr;
-      double va = 0.0, vb = 0.0;
-      if (r < k1) {
-        long long li = g.J[r];
-        long long pr = li >= g.n ? li - g.n : li;  // SVR block: row sign cancels in x x^T
-        const double* row = g.A + pr * g.lda;
-        if (ci + c < g.q) va = __ldg(row + ci + c);
-        if (cj + c < g.q) vb = __ldg(row + cj + c);
-      }
-      sA[kr][c] = va;
-      sB[kr][c] = vb;
-    }
+  };
+
+  int buf = 0;
+  if (k0 < k1) stage(k0, 0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (long long kb = k0; kb < k1; kb += GK) {
+    if (kb + GK < k1) stage(kb + GK, buf ^ 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncthreads();
-    if (diag && threadIdx.x < GT) {
+    const double* cA = sA + buf * GSTAGE;
+    const double* cB = diag ? cA : sB + buf * GSTAGE;
+    if (diag && tid < GT) {  // m1 column ci + tid from the unsigned staged rows
       const int nk = (int)min((long long)GK, k1 - kb);
-      for (int kr = 0; kr < nk; ++kr) m1acc = fma(sw[kr], sA[kr][threadIdx.x], m1acc);
+      for (int kr = 0; kr < nk; ++kr) m1acc = fma(sw[buf * GK + kr], cA[kr * GLD + tid], m1acc);
     }
 #pragma unroll
     for (int kk = 0; kk < GK; kk += 4) {
-      const double a = sA[kk + (lane & 3)][warp * 8 + (lane >> 2)];
+      const int kr = kk + (lane & 3);
+      const double sg = signed_rows ? ssg[buf][kr] : 1.0;
+      double af[8], bf[4];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const double b = sB[kk + (lane & 3)][t * 8 + (lane >> 2)];
-        dmma_8x8x4(acc[t][0], acc[t][1], a, b);
-      }
+      for (int a = 0; a < 8; ++a) af[a] = cA[kr * GLD + wm * 64 + a * 8 + (lane >> 2)] * sg;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = cB[kr * GLD + wn * 32 + b * 8 + (lane >> 2)];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-    __syncthreads();
+    __syncthreads();  // buffer `buf` free for the stage after next
+    buf ^= 1;
   }
-  if (diag && threadIdx.x < GT && ci + threadIdx.x < g.q)
-    g.part_m1[blockIdx.y * g.q + ci + threadIdx.x] = m1acc;
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (diag && tid < GT && ci + tid < g.q) g.part_m1[blockIdx.y * g.q + ci + tid] = m1acc;
   // C fragment: row = lane/4, cols = 2*(lane%4) + {0,1}
   double* dst = g.part + (long long)blockIdx.y * g.q * g.q;
-  const long long row = ci + warp * 8 + (lane >> 2);
-  if (row < g.q) {
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      long long col = cj + t * 8 + 2 * (lane & 3);
-      if (col < g.q) dst[row * g.q + col] = acc[t][0];
-      if (col + 1 < g.q) dst[row * g.q + col + 1] = acc[t][1];
+  for (int a = 0; a < 8; ++a) {
+    const long long row = ci + wm * 64 + a * 8 + (lane >> 2);
+    if (row >= g.q) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const long long col = cj + wn * 32 + b * 8 + 2 * (lane & 3);
+      if (col < g.q) dst[row * g.q + col] = acc[a][b][0];
+      if (col + 1 < g.q) dst[row * g.q + col + 1] = acc[a][b][1];
     }
   }
 }
 
-__global__ void gram_m1_fold_kernel(const double* __restrict__ part_m1, long long q,
-                                    double* __restrict__ m1) {
-  long long col = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= q) return;
-  double s = 0.0;
-  for (int b = 0; b < GSPLIT; ++b) s += part_m1[b * q + col];
-  m1[col] = s;
+// G (= X_J^T X_J in the partials' tile layout: upper tile pairs, lower tiles stored
+// transposed) and m1 from the GSPLIT split-K partials, in split order; accumulate = 1
+// adds them to the kept G / m1 (incremental update over the changed slots)
+__global__ void gram_fold_kernel(const double* __restrict__ part, const double* __restrict__ part_m1,
+                                 long long q, int split, double* __restrict__ G,
+                                 double* __restrict__ m1, int accumulate,
+                                 const GramCtl* __restrict__ ctl) {
+  if (ctl) accumulate = ctl->mode == 1;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < q * q) {
+    const long long i = idx / q, j = idx % q;
+    if (i / GT <= j / GT) {  // stored positions only
+      double s = accumulate ? G[idx] : 0.0;
+      double d = 0.0;
+      for (int b = 0; b < split; ++b) d += part[(long long)b * q * q + idx];
+      G[idx] = s + d;
+    }
+  }
+  if (idx < q) {
+    double d = 0.0;
+    for (int b = 0; b < split; ++b) d += part_m1[b * q + idx];
+    m1[idx] = (accumulate ? m1[idx] : 0.0) + d;
+  }
 }
 
 // M = I + sigma (G - m1 m1^T / asa)   (asa == 0: I + sigma G)
-__global__ void gram_assemble_kernel(const double* __restrict__ part, long long q,
+__global__ void gram_assemble_kernel(const double* __restrict__ G, long long q,
                                      const double* __restrict__ m1, double sigma,
                                      const double* __restrict__ asa_dev,
                                      double* __restrict__ M) {
@@ -573,36 +673,129 @@ __global__ void gram_assemble_kernel(const double* __restrict__ part, long long 
   long long i = idx / q, j = idx % q;
   long long si = i, sj = j;
   if (i / GT > j / GT) { si = j; sj = i; }  // lower tiles are stored transposed
-  double g = 0.0;
-  for (int b = 0; b < GSPLIT; ++b) g += part[(long long)b * q * q + si * q + sj];
+  double g = G[si * q + sj];
   const double asa = *asa_dev;
   if (asa != 0.0) g = g - m1[i] * m1[j] / asa;
   M[idx] = (i == j ? 1.0 : 0.0) + sigma * g;
 }
 
-size_t gram_ws_bytes(long long q) {
-  return (size_t)GSPLIT * q * q * sizeof(double) + (size_t)GSPLIT * q * sizeof(double);
+// chg = (fr != kept), kept = fr: the slots whose free flag changed since the kept Gram
+__global__ void mask_diff_kernel(const uint8_t* __restrict__ fr, uint8_t* __restrict__ kept,
+                                 uint8_t* __restrict__ chg, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint8_t f = fr[i];
+    chg[i] = f != kept[i];
+    kept[i] = f;
+  }
 }
 
+// split-K chunks the partials buffer holds: one wave of tile pairs on up to 192 SMs
+static int gram_split_cap(long long q) {
+  const long long nt = ceil_div(q, GT);
+  const long long npairs = nt * (nt + 1) / 2;
+  return (int)std::max(1LL, std::min((long long)GSPLIT, 192 / npairs));
+}
+
+size_t gram_ws_bytes(long long q) {
+  const size_t sp = (size_t)gram_split_cap(q);
+  return sp * q * q * sizeof(double) + sp * q * sizeof(double);
+}
+
+// G (+)= sum over the listed slots of (+-) x x^T, m1 (+)= sum (+-) a_j x_j
+// driver: rebuild over J (p rows) or update over the changed slots Jd (count d) --
+// whichever gathers fewer rows, with the updates since the last rebuild capped at 2p
+// (bounds the rounding drift of +-x x^T sums); decided on the device, no host sync
+__global__ void gram_select_kernel(GramCtl* c, const long long* __restrict__ p_dev,
+                                   const long long* __restrict__ d_dev, int force_full) {
+  const long long p = *p_dev, d = *d_dev;
+  const bool incr = !force_full && c->valid && 2 * d < p && c->accum + d <= 2 * p;
+  if (incr) {
+    c->mode = 1;
+    c->count = d;
+    c->accum += d;
+    ++c->updates;
+    c->rows += d;
+  } else {
+    c->mode = 0;
+    c->count = p;
+    c->accum = 0;
+    ++c->builds;
+    c->rows += p;
+  }
+  c->valid = 1;
+}
+
+cudaError_t launch_gram_select(GramCtl* ctl, const long long* p_dev, const long long* d_dev,
+                               int force_full, cudaStream_t stream) {
+  note_launch();
+  gram_select_kernel<<<1, 1, 0, stream>>>(ctl, p_dev, d_dev, force_full);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_update(const double* A, long long n, long long q, long long lda,
+                               const double* rs, int svr, const int32_t* J, const long long* p_dev,
+                               const uint8_t* sign_mask, const double* a, double* G, double* m1,
+                               int accumulate, void* ws, cudaStream_t stream,
+                               const GramCtl* ctl, const int32_t* Jd) {
+  static int sms[64];  // per device ordinal
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (sms[dev] <= 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)GSMEM);
+    if (e != cudaSuccess) return e;
+    sms[dev] = v > 0 ? v : 148;
+  }
+  GramArgs g;
+  g.A = A; g.n = n; g.q = q; g.lda = lda; g.J = J; g.p_dev = p_dev;
+  g.part = (double*)ws;
+  g.ntile = (int)ceil_div(q, GT);
+  const int npairs = g.ntile * (g.ntile + 1) / 2;
+  g.split = std::max(1, std::min(gram_split_cap(q), sms[dev] / npairs));  // one wave
+  double* part_m1 = g.part + (long long)gram_split_cap(q) * q * q;
+  g.a = a; g.rs = rs; g.svr = svr; g.part_m1 = part_m1; g.sign_mask = sign_mask;
+  g.aligned = (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  g.ctl = ctl;
+  g.Jd = Jd;
+  { note_launch(); gram_kernel<<<dim3(npairs, g.split), GNT, GSMEM, stream>>>(g); }
+  { note_launch(); gram_fold_kernel<<<(unsigned)ceil_div(q * q, 256), 256, 0, stream>>>(g.part, part_m1, q, g.split, G, m1, accumulate, ctl); }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_assemble(const double* G, long long q, const double* m1, double sigma,
+                                 const double* asa_dev, double* M, cudaStream_t stream) {
+  note_launch();
+  gram_assemble_kernel<<<(unsigned)ceil_div(q * q, 256), 256, 0, stream>>>(G, q, m1, sigma, asa_dev, M);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mask_diff(const uint8_t* fr, uint8_t* kept, uint8_t* chg, long long n,
+                             cudaStream_t stream) {
+  const int blocks = (int)std::min<long long>(ceil_div(n, 256LL * 8), SSNAL_MAX_BLOCKS);
+  note_launch();
+  mask_diff_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, stream>>>(fr, kept, chg, n);
+  return cudaGetLastError();
+}
+
+// one-shot M = I + sigma (X_J^T P X_J) (C-ABI ssnal_dense_gram); G is built in M itself
 cudaError_t launch_dense_gram(const double* A, long long n, long long q, long long lda,
                               const double* rs, int svr, const int32_t* J, const long long* p_dev,
                               long long p_max, const double* a, double sigma,
                               const double* asa_dev, double* M, double* m1, void* ws,
                               cudaStream_t stream) {
   (void)p_max;
-  GramArgs g;
-  g.A = A; g.n = n; g.q = q; g.lda = lda; g.J = J; g.p_dev = p_dev;
-  g.part = (double*)ws;
-  g.ntile = (int)ceil_div(q, GT);
-  double* part_m1 = g.part + (long long)GSPLIT * q * q;
-  g.a = a; g.rs = rs; g.svr = svr; g.part_m1 = part_m1;
-  int npairs = g.ntile * (g.ntile + 1) / 2;
-  { note_launch(); gram_kernel<<<dim3(npairs, GSPLIT), 256, 0, stream>>>(g); }
-  { note_launch(); gram_m1_fold_kernel<<<(unsigned)ceil_div(q, 256), 256, 0, stream>>>(part_m1, q, m1); }
-  { note_launch(); gram_assemble_kernel<<<(unsigned)ceil_div(q * q, 256), 256, 0, stream>>>(g.part, q, m1, sigma,
-                                                                          asa_dev, M); }
-  return cudaGetLastError();
+  double* G = (double*)((char*)ws + gram_ws_bytes(q));  // see gram_ws_bytes_full
+  cudaError_t e = launch_gram_update(A, n, q, lda, rs, svr, J, p_dev, nullptr, a, G, m1, 0, ws,
+                                     stream, nullptr, nullptr);
+  if (e != cudaSuccess) return e;
+  return launch_gram_assemble(G, q, m1, sigma, asa_dev, M, stream);
 }
+
+size_t gram_ws_bytes_full(long long q) { return gram_ws_bytes(q) + (size_t)q * q * sizeof(double); }
 
 // Fused SsN gradient (ref solver.py:143-148 with the linear-kernel operator):
 //   s = w - Pi(u);  g_r = X^T s;  grad = X g_r;  *g2 = ||grad||^2

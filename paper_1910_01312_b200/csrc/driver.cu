@@ -65,6 +65,17 @@ cudaError_t launch_dense_gram(const double* A, long long n, long long q, long lo
                               double* M, double* m1, void* ws, cudaStream_t s);
 cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
                               int* info, cudaStream_t s);
+cudaError_t launch_gram_update(const double* A, long long n, long long q, long long lda,
+                               const double* rs, int svr, const int32_t* J, const long long* p_dev,
+                               const uint8_t* sign_mask, const double* a, double* G, double* m1,
+                               int accumulate, void* ws, cudaStream_t stream,
+                               const GramCtl* ctl, const int32_t* Jd);
+cudaError_t launch_gram_select(GramCtl* ctl, const long long* p_dev, const long long* d_dev,
+                               int force_full, cudaStream_t stream);
+cudaError_t launch_gram_assemble(const double* G, long long q, const double* m1, double sigma,
+                                 const double* asa_dev, double* M, cudaStream_t stream);
+cudaError_t launch_mask_diff(const uint8_t* fr, uint8_t* kept, uint8_t* chg, long long n,
+                             cudaStream_t stream);
 cudaError_t launch_pspace_direction(const double* A, long long n, long long q, long long lda,
                                     const double* rs, int svr, const int32_t* J, long long p,
                                     const double* grad, const double* a, double sigma, double asa,
@@ -200,6 +211,13 @@ struct Layout {
   uint8_t *fr, *tfree;
   int32_t* J;
   long long* pcount;
+  // kept q-space Gram (dense, p >= q): G = X_J^T X_J and m1 = X_J^T a_J of the free set
+  // frg, updated over the slots whose flag changed (chg -> Jd, dcount in the blob)
+  double* G;
+  uint8_t *frg, *chg;
+  int32_t* Jd;
+  long long* dcount;
+  GramCtl* gctl;
   int* info;
   ProjState *st_cur, *st_trial, *st_kkt;
   void *ws_proj, *ws_red, *ws_xt, *ws_gram, *ws_cmp, *ws_ps, *ws_grad;
@@ -237,6 +255,14 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
   L.xpi = cv.take<double>(q);
   L.qpart = sparse ? nullptr : cv.take<double>(accept_q_ws_bytes(n, q) / sizeof(double) + 1);
   L.M = sparse ? nullptr : cv.take<double>((size_t)q * q);
+  if (!sparse) {
+    L.G = cv.take<double>((size_t)q * q);
+    L.frg = cv.take<uint8_t>(n);
+    L.chg = cv.take<uint8_t>(n);
+    L.Jd = cv.take<int32_t>(n);
+    L.dcount = cv.take<long long>(1);
+    L.gctl = cv.take<GramCtl>(1);
+  }
   L.m1 = cv.take<double>(q);
   {  // contiguous read-back blob (see BLOB_ST)
     char* blob = cv.take<char>(BLOB_BYTES);
@@ -329,12 +355,14 @@ struct Driver {
   Layout L;
   Pinned* H;
   long long syncs = 0, newton = 0, projections = 0, cg_iters = 0, cg_fallbacks = 0;
+  long long proj_fallbacks = 0;
   double lam_kkt = 0.0, lam_cur = 0.0;
   double sigma = 1.0;
   double c_norm = 0.0;
   Prof prof;
-  double op_bytes[SSNAL_NOPS] = {0, 0, 0, 0, 0};
-  long long op_calls[SSNAL_NOPS] = {0, 0, 0, 0, 0};
+  double op_bytes[SSNAL_NOPS] = {};
+  double op_flops[SSNAL_NOPS] = {};
+  long long op_calls[SSNAL_NOPS] = {};
 
   Driver(const ssnal_dense_problem_t& p, const ssnal_options_t& o, cudaStream_t s, Layout l,
          Pinned* h)
@@ -598,6 +626,10 @@ struct Driver {
       pl.base = L.xp;
       pl.base_lam = lam_cur;
     }
+    if (B && xo == L.tx) {  // a line-search batch: x / mask of the accepted trial only
+      pl.defer = 1;
+      trial_deferred = proj_defers(P.n, T);
+    }
     // algorithmic bytes: each streaming launch reads v (+B), a (+l, u vectors); apply
     // also writes x and the mask
     const double per = 8.0 * P.n * (2 + (B != nullptr) + (P.l != nullptr) + (P.u != nullptr));
@@ -629,6 +661,7 @@ struct Driver {
       }
       if (!pending) return extra;
       if (round > 20) throw DriverError{SSNAL_E_ARG, "projection failed to bracket the multiplier"};
+      if (!extra) ++proj_fallbacks;
       extra = true;
       project(A, st_dev, T, B, coefs, xo, fo, ref, 0.0, 0, 8, PHASE_EXACT | PHASE_APPLY);
       fetch(st_dev, T, false);
@@ -779,9 +812,9 @@ struct Driver {
       throw DriverError{SSNAL_E_ARG, "q x q system above direct_solve_threshold (no CG path)"};
     // gathered rows of A (p x q) once + the system matrix written and factored
     const double m = (double)std::min<long long>(p, P.q);
-    timed(SSNAL_OP_NEWTON, 8.0 * p * P.q + 16.0 * m * m, [&] {
+    const double* g_r = qgrad() ? L.r : L.gr;
+    timed(SSNAL_OP_NEWTON, p < P.q ? 8.0 * p * P.q + 16.0 * m * m : 1.0 * P.n + 4.0 * p, [&] {
       ck(launch_compact(L.fr, P.n, L.J, L.pcount, L.ws_cmp, S));
-      const double* g_r = qgrad() ? L.r : L.gr;
       if (p < P.q) {
         // factor-space gradient: the right-hand side needs grad_J = X_J r only
         if (qgrad())
@@ -789,13 +822,19 @@ struct Driver {
                               L.grad, S));
         ck(launch_pspace_direction(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, p,
                                    L.grad, P.a, sigma, asa, g_r, L.t, L.info, L.ws_ps, S));
-      } else {
-        const double* asa_dev = &L.st_cur->sum_a2_free;
-        ck(launch_dense_gram(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, L.pcount,
-                             P.n, P.a, sigma, asa_dev, L.M, L.m1, L.ws_gram, S));
-        ck(launch_chol_solve(L.M, P.q, g_r, -1.0, L.t, L.info, S));
       }
     });
+    if (p >= P.q) {
+      const double* asa_dev = &L.st_cur->sum_a2_free;
+      // gathered rows: bytes and flops added once the row count is known (gram_rows)
+      timed(SSNAL_OP_GRAM, 0.0, [&] { gram(); });
+      const double qd = (double)P.q;
+      op_flops[SSNAL_OP_CHOL] += qd * qd * qd / 3.0 + 2.0 * qd * qd;
+      timed(SSNAL_OP_CHOL, 24.0 * qd * qd, [&] {
+        ck(launch_gram_assemble(L.G, P.q, L.m1, sigma, asa_dev, L.M, S));
+        ck(launch_chol_solve(L.M, P.q, g_r, -1.0, L.t, L.info, S));
+      });
+    }
     if (qgrad()) {
       // ONE sweep X [t, r]: Qd and this point's gradient (a_J'(Qd)_J and ||grad||^2
       // folded), then d = -s - sigma P(Qd) and {g'd, w'Qw, w'Qd, t't}
@@ -819,6 +858,21 @@ struct Driver {
                                    L.qdir, L.fr, P.a, &L.st_cur->sum_a2_free, L.s, sigma, L.grad,
                                    L.w, L.qw, L.dir, L.scal, L.ws_grad, S));
     });
+  }
+
+  // Kept q-space Gram G = X_J^T X_J, m1 = X_J^T a_J (sigma-free, valid across outer
+  // iterations): each Newton step of the q-space route either rebuilds it from all p
+  // free rows or updates it over the slots whose free flag changed since (+x x^T
+  // entering, -x x^T leaving) -- whichever gathers fewer rows, decided on the device
+  // (gram_select_kernel; SSNAL_GRAM_FULL=1 always rebuilds).  Jd ascending and the
+  // fixed split-K order keep it deterministic.
+  void gram() {
+    static const int force_full = std::getenv("SSNAL_GRAM_FULL") != nullptr ? 1 : 0;
+    ck(launch_mask_diff(L.fr, L.frg, L.chg, P.n, S));
+    ck(launch_compact(L.chg, P.n, L.Jd, L.dcount, L.ws_cmp, S));
+    ck(launch_gram_select(L.gctl, L.pcount, L.dcount, force_full, S));
+    ck(launch_gram_update(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, L.pcount,
+                          L.fr, P.a, L.G, L.m1, 0, L.ws_gram, S, L.gctl, L.Jd));
   }
 
   // dense operator: the SsN gradient is kept in factor space
@@ -846,7 +900,7 @@ struct Driver {
     // the first Armijo batch (alpha = 1, beta, ..., beta^(T0-1)) is projected
     // speculatively with the direction: most steps then need no further host round trip
     const int T0 = std::min(std::min(TMAX, std::max(1, O.line_search_batch)),
-                            proj_wave_trials(P.n));
+                            proj_wave_trials(P.n, true));
     double coefs[TMAX];
     double alpha = 1.0;
     for (int k = 0; k < T0; ++k) {
@@ -911,8 +965,22 @@ struct Driver {
     return false;
   }
 
+  bool trial_deferred = false;  // the last trial batch left x / mask unwritten
+
+  void materialize(double alpha, int j) {
+    if (!trial_deferred) return;
+    ProjLaunch pl;
+    pl.A = L.u; pl.B = L.qdir; pl.a = P.a; pl.l = P.l; pl.u = P.u;
+    pl.lc = P.l_const; pl.uc = P.u_const; pl.n = P.n;
+    timed(SSNAL_OP_PROJ, 8.0 * P.n * 4 + 1.0 * P.n, [&] {
+      ck(launch_proj_materialize(pl, sigma * alpha, L.st_trial + j, L.tx + (size_t)j * P.n,
+                                 L.tfree + (size_t)j * P.n, S));
+    });
+  }
+
   void accept(double alpha, int j) {
     trace_resume();
+    materialize(alpha, j);
     if (qgrad()) {  // + s, and X^T w, X^T Pi(u), r = X^T s updated from the changed slots
       timed(SSNAL_OP_VEC, 8.0 * P.n * 9 + 2.0 * P.n, [&] {
         ck(launch_accept_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, P.n, alpha,
@@ -1052,7 +1120,10 @@ struct Driver {
     if (w0) ck(cudaMemcpyAsync(L.w, w0, nb, cudaMemcpyDeviceToDevice, S));
     else ck(cudaMemsetAsync(L.w, 0, nb, S));
     if (P.csr) ck(cudaMemsetAsync(L.cj.ticket, 0, sizeof(unsigned int), S));
-    else ck(cudaMemsetAsync(L.qpart, 0, 256, S));  // accept_q ticket
+    else {
+      ck(cudaMemsetAsync(L.qpart, 0, 256, S));  // accept_q ticket
+      ck(cudaMemsetAsync(L.gctl, 0, sizeof(GramCtl), S));  // no kept Gram yet
+    }
     ck(cudaMemsetAsync(L.qw, 0, nb, S));
     dots({{P.c, nullptr}}, L.scal, P.n);
     fetch(nullptr, 0, false);
@@ -1062,7 +1133,8 @@ struct Driver {
     int outer = 0, inner_total = 0, inner_last = 0, stalled = 0;
     long long p_last = -1;
     bool converged = false, stagnated = false, max_outer = false;
-    int hit_mask = 0;
+    int hit_mask = 0, hit_count = 0;
+    unsigned long long hit_mask64 = 0ull;
     double res = INFINITY, obj_last = 0.0;
     double best_res = INFINITY, best_obj = 0.0;
     long long best_p = 0;
@@ -1098,6 +1170,8 @@ struct Driver {
       const double e = std::pow(0.5, k);
       inner_last = ssn_solve(e, e, conv_in, hit, cur);
       if (hit && k < 31) hit_mask |= 1 << k;
+      if (hit && k < 64) hit_mask64 |= 1ull << k;
+      if (hit) ++hit_count;
       inner_total += inner_last;
       ck(cudaMemcpyAsync(L.x, L.xp, nb, cudaMemcpyDeviceToDevice, S));
       p_last = cur.nfree;
@@ -1121,9 +1195,24 @@ struct Driver {
     rep->projections = projections;
     rep->cg_iters = cg_iters;
     rep->cg_fallbacks = cg_fallbacks;
+    GramCtl gc{};
+    if (!P.csr) {
+      ck(cudaMemcpyAsync(&gc, L.gctl, sizeof(GramCtl), cudaMemcpyDeviceToHost, S));
+      ck(cudaStreamSynchronize(S));
+    }
+    rep->gram_builds = gc.builds;
+    rep->gram_updates = gc.updates;
+    const long long gram_rows = gc.rows;
+    rep->gram_rows = gram_rows;
+    op_bytes[SSNAL_OP_GRAM] = 8.0 * (double)gram_rows * P.q;
+    op_flops[SSNAL_OP_GRAM] = (double)gram_rows * P.q * (P.q + 1.0);
+    rep->proj_fallbacks = proj_fallbacks;
+    rep->hit_max_inner_mask64 = hit_mask64;
+    rep->hit_max_inner_count = hit_count;
     for (int k = 0; k < SSNAL_NOPS; ++k) {
       rep->op_calls[k] = op_calls[k];
       rep->op_bytes[k] = op_bytes[k];
+      rep->op_flops[k] = op_flops[k];
       rep->op_seconds[k] = 0.0;
     }
     for (auto& r : prof.recs) {

@@ -64,6 +64,12 @@ __device__ __forceinline__ double bregman_term(double x, double xb, double v, do
   return (x - xb) * (v - 0.5 * (x + xb) - lam_bar * a);
 }
 
+// (v - bound) / a with numpy's rounding; division by +-1 is exact in IEEE arithmetic,
+// so the SVM duals (a = labels or (e; -e)) skip the DP division bit-identically
+__device__ __forceinline__ double bp_div(double x, double a) {
+  return a == 1.0 ? x : (a == -1.0 ? -x : __ddiv_rn(x, a));
+}
+
 __device__ __forceinline__ void load_elem(const ProjArgs& p, int t, long long i, double& v,
                                           double& a, double& l, double& u) {
   v = p.A[i];
@@ -98,7 +104,7 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_range_kernel(ProjArgs p) {
     double v, a, l, u;
     load_elem(p, t, i, v, a, l, u);
     if (a != 0.0) {
-      double t1 = __ddiv_rn(__dsub_rn(v, u), a), t2 = __ddiv_rn(__dsub_rn(v, l), a);
+      double t1 = bp_div(__dsub_rn(v, u), a), t2 = bp_div(__dsub_rn(v, l), a);
       tmin = fmin(tmin, fmin(t1, t2));
       tmax = fmax(tmax, fmax(t1, t2));
       nnz += 1.0;
@@ -174,7 +180,7 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_pass_kernel(ProjArgs p) {
     double v, a, l, u;
     load_elem(p, t, i, v, a, l, u);
     if (a == 0.0) continue;
-    double t1 = __ddiv_rn(__dsub_rn(v, u), a), t2 = __ddiv_rn(__dsub_rn(v, l), a);
+    double t1 = bp_div(__dsub_rn(v, u), a), t2 = bp_div(__dsub_rn(v, l), a);
     double ta = fmin(t1, t2), tb = fmax(t1, t2);
     bool in_a = ta > lo && ta <= hi, in_b = tb > lo && tb <= hi;
     if (ta <= lo) bmax = fmax(bmax, ta); else if (ta > hi) amin = fmin(amin, ta);
@@ -267,7 +273,7 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_newton_kernel(ProjArgs p, int f
     double v, a, l, u;
     load_elem(p, t, i, v, a, l, u);
     if (a == 0.0) continue;
-    double t1 = __ddiv_rn(__dsub_rn(v, u), a), t2 = __ddiv_rn(__dsub_rn(v, l), a);
+    double t1 = bp_div(__dsub_rn(v, u), a), t2 = bp_div(__dsub_rn(v, l), a);
     double ta = fmin(t1, t2), tb = fmax(t1, t2);
     fsum += contrib(v, a, l, u, c);
     const double a2 = a * a;
@@ -551,7 +557,7 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_fused_kernel(ProjArgs p, double
         double v, a, l, u;
         load_elem(p, t, i, v, a, l, u);
         if (a == 0.0) continue;
-        const double t1 = __ddiv_rn(__dsub_rn(v, u), a), t2 = __ddiv_rn(__dsub_rn(v, l), a);
+        const double t1 = bp_div(__dsub_rn(v, u), a), t2 = bp_div(__dsub_rn(v, l), a);
         const double ta = fmin(t1, t2), tb = fmax(t1, t2);
         vals[0] += contrib(v, a, l, u, c);
         const double a2 = a * a;
@@ -719,8 +725,8 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
     double ta = 0.0, tb = 0.0;
     if (a[k] != 0.0) {
       const double l = p.l ? p.l[i] : p.lc, u = p.u ? p.u[i] : p.uc;
-      const double t1 = __ddiv_rn(__dsub_rn(v[k], u), a[k]);
-      const double t2 = __ddiv_rn(__dsub_rn(v[k], l), a[k]);
+      const double t1 = bp_div(__dsub_rn(v[k], u), a[k]);
+      const double t2 = bp_div(__dsub_rn(v[k], l), a[k]);
       ta = fmin(t1, t2);
       tb = fmax(t1, t2);
     }
@@ -881,6 +887,244 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
   }
 }
 
+
+// ------------------------------------------------------------------ multi-trial
+// Large-n projection (n above the cluster path's register capacity, e.g. the
+// 2,000,000-slot config-4 dual): ALL T line-search trials of a batch in ONE
+// cooperative launch that reads each slot's (u, Qd, a) ONCE per pass.  The 8 warps of
+// a block are split into T trial groups of 8/T warps; the groups walk the same slots
+// (the repeats hit L1), so a pass costs one read of the inputs whatever T is, where
+// the trial-per-blockIdx.y kernels read them T times.  Per pass: per-warp Newton sums
+// -> per-trial block partial -> grid barrier -> every block folds the partials of every
+// trial in block order (identical state everywhere, uniform branching) and takes the
+// safeguarded Newton step (newton_update).  Up to PM_MAX_PASSES passes (cheap once
+// the inputs sit in L2), then the apply pass: the six fused sums per trial, and x /
+// the free mask written only when asked (a batch defers them: the driver materialises
+// the ONE accepted trial, proj_materialize_kernel).
+static constexpr int PM_NT = 256;
+static constexpr int PM_WARPS = PM_NT / 32;
+static constexpr int PM_MAX_PASSES = 16;
+static constexpr int PM_UNROLL = 4;
+static constexpr int PM_INACTIVE = 99;
+
+template <int T>
+__global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hint,
+                                                           int max_newton, int nt, int write_x) {
+  cg::grid_group grid = cg::this_grid();
+  constexpr int G = PM_WARPS / T;  // warps per trial group
+  __shared__ double wred[PM_WARPS][8];
+  __shared__ double s_c[T], s_lo[T], s_hi[T], s_lam[T], s_tmin[T], s_tmax[T], s_coef[T];
+  __shared__ int s_status[T], s_passes[T];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = warp % T, g = warp / T;
+  const unsigned nb = gridDim.x;
+  const long long region = (long long)T * nb * PSTRIDE;
+  if (threadIdx.x < T) {
+    s_c[threadIdx.x] = hint;
+    s_lo[threadIdx.x] = -INFINITY;
+    s_hi[threadIdx.x] = INFINITY;
+    s_lam[threadIdx.x] = 0.0;
+    s_tmin[threadIdx.x] = INFINITY;
+    s_tmax[threadIdx.x] = -INFINITY;
+    s_status[threadIdx.x] = (int)threadIdx.x < nt ? PROJ_NEWTON : PM_INACTIVE;
+    s_passes[threadIdx.x] = 0;
+#pragma unroll
+    for (int k = 0; k < T; ++k)  // static indices: no local copy of the param array
+      if ((int)threadIdx.x == k) s_coef[k] = p.coef[k];
+  }
+  __syncthreads();
+  const double coef = s_coef[t];
+  const long long stride = (long long)nb * G * 32;
+  const long long start = ((long long)blockIdx.x * G + g) * 32 + lane;
+  const int ops[8] = {0, 0, 0, 1, 2, 1, 2, 0};
+  for (int pass = 0;; ++pass) {
+    const int status = s_status[t];
+    const double c = s_c[t];
+    double vals[8] = {0.0, 0.0, 0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0.0};
+    if (status == PROJ_NEWTON) {
+      for (long long i0 = start; i0 < p.n; i0 += PM_UNROLL * stride) {
+        double uu[PM_UNROLL], bb[PM_UNROLL], aa[PM_UNROLL];
+#pragma unroll
+        for (int k = 0; k < PM_UNROLL; ++k) {  // every load of the chunk in flight first
+          const long long i = i0 + k * stride;
+          const bool in = i < p.n;
+          uu[k] = in ? __ldg(p.A + i) : 0.0;
+          bb[k] = (in && p.B) ? __ldg(p.B + i) : 0.0;
+          aa[k] = in ? __ldg(p.a + i) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < PM_UNROLL; ++k) {
+          const long long i = i0 + k * stride;
+          if (i >= p.n || aa[k] == 0.0) continue;
+          const double v = p.B ? __dsub_rn(uu[k], __dmul_rn(coef, bb[k])) : uu[k];
+          const double a = aa[k];
+          const double l = p.l ? p.l[i] : p.lc, u = p.u ? p.u[i] : p.uc;
+          const double t1 = bp_div(__dsub_rn(v, u), a), t2 = bp_div(__dsub_rn(v, l), a);
+          const double ta = fmin(t1, t2), tb = fmax(t1, t2);
+          vals[0] += contrib(v, a, l, u, c);
+          const double a2 = a * a;
+          if (ta <= c && c < tb) vals[1] += a2;
+          if (ta < c && c <= tb) vals[2] += a2;
+          if (ta > c) vals[3] = fmin(vals[3], ta); else if (ta < c) vals[4] = fmax(vals[4], ta);
+          if (tb > c) vals[3] = fmin(vals[3], tb); else if (tb < c) vals[4] = fmax(vals[4], tb);
+          if (pass == 0) {
+            vals[5] = fmin(vals[5], ta);
+            vals[6] = fmax(vals[6], tb);
+            vals[7] += 1.0;
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double w = ops[k] == 0 ? warp_sum(vals[k]) : (ops[k] == 1 ? warp_min(vals[k]) : warp_max(vals[k]));
+        if (lane == 0) wred[warp][k] = w;
+      }
+    }
+    __syncthreads();
+    double* part = p.part + (pass & 1) * region;
+    if (status == PROJ_NEWTON && g == 0 && lane < 8) {  // the trial's G warps, in order
+      const int op = (lane == 3 || lane == 5) ? 1 : ((lane == 4 || lane == 6) ? 2 : 0);  // ops[lane]
+      double r = wred[t][lane];
+      for (int gg = 1; gg < G; ++gg) {
+        const double x = wred[gg * T + t][lane];
+        r = op == 0 ? r + x : (op == 1 ? fmin(r, x) : fmax(r, x));
+      }
+      part[((long long)t * nb + blockIdx.x) * PSTRIDE + lane] = r;
+    }
+    grid.sync();
+    if (status == PROJ_NEWTON && g == 0) {
+      // lane folds blocks lane, lane + 32, ... (fixed order), then a fixed warp tree:
+      // every block gets bit-identical totals
+      double r[8] = {0.0, 0.0, 0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0.0};
+      const double* base = part + (long long)t * nb * PSTRIDE;
+      for (unsigned b = lane; b < nb; b += 32) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double x = __ldcg(base + (long long)b * PSTRIDE + k);
+          r[k] = ops[k] == 0 ? r[k] + x : (ops[k] == 1 ? fmin(r[k], x) : fmax(r[k], x));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        r[k] = ops[k] == 0 ? warp_sum(r[k]) : (ops[k] == 1 ? warp_min(r[k]) : warp_max(r[k]));
+      if (lane == 0) {
+        double cc = s_c[t], lo = s_lo[t], hi = s_hi[t], lam = s_lam[t], tmin = s_tmin[t];
+        int stt = status;
+        if (pass == 0) {
+          tmin = r[5];
+          s_tmin[t] = r[5];
+          s_tmax[t] = r[6];
+        }
+        if (pass == 0 && r[7] == 0.0) {  // a == 0: the constraint is 0 = d, clip only
+          lam = 0.0;
+          stt = PROJ_DONE;
+        } else {
+          newton_update(p.d - r[0], r[1], r[2], r[3], r[4], tmin, p.d, cc, lo, hi, lam, stt);
+        }
+        s_c[t] = cc; s_lo[t] = lo; s_hi[t] = hi; s_lam[t] = lam; s_status[t] = stt;
+        s_passes[t] = pass + 1;
+      }
+    }
+    __syncthreads();
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < T; ++k) any |= s_status[k] == PROJ_NEWTON;
+    if (!any || pass + 1 >= max_newton) break;
+  }
+  // apply: the six fused sums per trial (+ x and the mask when written)
+  const int status = s_status[t];
+  const double lam = s_lam[t];
+  double s6[6] = {0, 0, 0, 0, 0, 0};
+  if (status == PROJ_DONE) {
+    double* xo = (write_x && p.x_out) ? p.x_out + (long long)t * p.n : nullptr;
+    unsigned char* fo = (write_x && p.free_out) ? p.free_out + (long long)t * p.n : nullptr;
+    const double lam_bar = 0.5 * (lam + p.base_lam);
+    for (long long i = start; i < p.n; i += stride) {
+      double v, a, l, u;
+      load_elem(p, t, i, v, a, l, u);
+      const double y = __dsub_rn(v, __dmul_rn(lam, a));
+      const double x = fmin(fmax(y, l), u);
+      const bool lower = y <= __dadd_rn(l, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(l))));
+      const bool upper = !lower && (y >= __dsub_rn(u, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(u)))));
+      const bool fr = !(lower || upper);
+      if (xo) xo[i] = x;
+      if (fo) fo[i] = fr ? 1 : 0;
+      const double r = v - x;
+      s6[0] += p.base ? bregman_term(x, __ldg(p.base + i), v, a, lam_bar) : v * v;
+      s6[1] += r * r;
+      if (p.ref) { const double dd = x - __ldg(p.ref + i); s6[2] += dd * dd; }
+      if (fr) { s6[3] += a * a; s6[4] += 1.0; }
+      s6[5] += x * (2.0 * v - x);
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double w = warp_sum(s6[k]);
+      if (lane == 0) wred[warp][k] = w;
+    }
+  }
+  __syncthreads();
+  double* part = p.part + 2 * region;
+  if (status == PROJ_DONE && g == 0 && lane < 6) {
+    double r = wred[t][lane];
+    for (int gg = 1; gg < G; ++gg) r += wred[gg * T + t][lane];
+    part[((long long)t * nb + blockIdx.x) * PSTRIDE + lane] = r;
+  }
+  grid.sync();
+  if (blockIdx.x != 0 || g != 0 || status == PM_INACTIVE) return;
+  ProjState* st = p.st + t;
+  if (status == PROJ_DONE) {
+    double r[6] = {0, 0, 0, 0, 0, 0};
+    const double* base = part + (long long)t * nb * PSTRIDE;
+    for (unsigned b = lane; b < nb; b += 32) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) r[k] += __ldcg(base + (long long)b * PSTRIDE + k);
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) r[k] = warp_sum(r[k]);
+    if (lane != 0) return;
+    st->sum_v2 = p.base ? 0.0 : r[0];
+    st->sum_bh = p.base ? r[0] : 0.0;
+    st->sum_r2 = r[1];
+    st->sum_dref2 = r[2];
+    st->sum_a2_free = r[3];
+    st->nfree = (long long)r[4];
+    st->sum_xv = r[5];
+    st->lam = lam;
+    st->status = PROJ_APPLIED;
+  } else {
+    if (lane != 0) return;
+    st->lam = s_c[t];  // Newton iterate for the K-ary fallback (tmin for infeasible-low)
+    st->lo = s_lo[t];
+    st->hi = s_hi[t];
+    st->status = status;
+  }
+  st->tmin = s_tmin[t];
+  st->tmax = s_tmax[t];
+  st->passes = s_passes[t];
+  st->in_count = -1;
+}
+
+// x and the free mask of ONE trial of a deferred batch: v = A - coef B at the trial's
+// multiplier (read from its device state), the apply pass's arithmetic bit for bit
+__global__ void __launch_bounds__(SSNAL_NT) proj_materialize_kernel(ProjArgs p, double coef,
+                                                                    const ProjState* st,
+                                                                    double* __restrict__ x_out,
+                                                                    unsigned char* __restrict__ f_out) {
+  const double lam = st->lam;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = __ldg(p.A + i);
+    if (p.B) v = __dsub_rn(v, __dmul_rn(coef, __ldg(p.B + i)));
+    const double a = __ldg(p.a + i);
+    const double l = p.l ? p.l[i] : p.lc, u = p.u ? p.u[i] : p.uc;
+    const double y = __dsub_rn(v, __dmul_rn(lam, a));
+    const bool lower = y <= __dadd_rn(l, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(l))));
+    const bool upper = !lower && (y >= __dsub_rn(u, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(u)))));
+    x_out[i] = fmin(fmax(y, l), u);
+    f_out[i] = (lower || upper) ? 0 : 1;
+  }
+}
+
 static bool cluster_ok(long long n, int T) {
   static int ok = -1;
   if (ok < 0) {
@@ -900,10 +1144,18 @@ static bool cluster_ok(long long n, int T) {
   return ok == 1 && n <= (long long)CL_CTAS * CL_NT * CL_EPT && T >= 1;
 }
 
+static bool multi_ok(long long n, int T) {
+  return T >= 1 && T <= PM_WARPS && !cluster_ok(n, T);
+}
+
 // Line-search trials one cluster-projection launch runs in a single wave: a 16-CTA
 // cluster needs 16 SMs of one GPC, so only ~7 fit on a B200 at once -- an 8-trial
 // batch ran as two waves (2x the latency of 7).  Not limited without the cluster path.
-int proj_wave_trials(long long n) {
+int proj_wave_trials(long long n, bool first) {
+  // multi-trial kernel: every trial costs a full set of per-slot FP64 work per pass (the
+  // inputs are read once), and the unit step is accepted on most Newton steps -- the
+  // speculative batch is (1, beta); a backtracking batch, 4 step lengths
+  if (multi_ok(n, 1)) return first ? 2 : 4;
   if (!cluster_ok(n, 1)) return SSNAL_MAX_TRIALS;
   static int w = -1;
   if (w < 0) {
@@ -943,6 +1195,52 @@ static int fused_capacity() {
   return cap;
 }
 
+template <int T>
+static int multi_capacity() {
+  static int cap[64];  // per device ordinal
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cap[dev] <= 0) {
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, proj_multi_kernel<T>, PM_NT, 0);
+    cap[dev] = sms * std::min(per, 2);
+  }
+  return cap[dev];
+}
+
+
+// whether a batched projection of T trials leaves x / the mask unwritten (the driver
+// then materialises the accepted trial with launch_proj_materialize)
+bool proj_defers(long long n, int T) { return T > 1 && multi_ok(n, T); }
+
+template <int T>
+static cudaError_t launch_multi(ProjArgs& p, const ProjLaunch& L, cudaStream_t stream) {
+  constexpr int G = PM_WARPS / T;
+  long long nb = ceil_div(L.n, (long long)G * 32 * PM_UNROLL);
+  nb = std::min<long long>(nb, std::min(multi_capacity<T>(), proj_blocks(L.n)));
+  if (nb < 1) nb = 1;
+  double hint = L.hint;
+  int maxn = std::max(L.newton, PM_MAX_PASSES);
+  int nt = L.T;
+  int write_x = (L.T == 1 || !L.defer) ? 1 : 0;
+  void* args[] = {&p, &hint, &maxn, &nt, &write_x};
+  note_launch();
+  return cudaLaunchCooperativeKernel((void*)proj_multi_kernel<T>, dim3((unsigned)nb), dim3(PM_NT),
+                                     args, 0, stream);
+}
+
+cudaError_t launch_proj_materialize(const ProjLaunch& L, double coef, const ProjState* st,
+                                    double* x_out, unsigned char* f_out, cudaStream_t stream) {
+  ProjArgs p{};
+  p.A = L.A; p.B = L.B; p.a = L.a; p.l = L.l; p.u = L.u; p.lc = L.lc; p.uc = L.uc; p.n = L.n;
+  const int nblk = (int)std::min<long long>(ceil_div(L.n, (long long)SSNAL_NT * 4), SSNAL_MAX_BLOCKS);
+  note_launch();
+  proj_materialize_kernel<<<nblk, SSNAL_NT, 0, stream>>>(p, coef, st, x_out, f_out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
   ProjArgs p;
   p.A = L.A; p.B = L.B;
@@ -955,6 +1253,12 @@ cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
     note_launch();
     proj_cluster_kernel<<<dim3(CL_CTAS, L.T), CL_NT, CL_SMEM, stream>>>(p, L.hint);
     return cudaGetLastError();
+  }
+  if (L.newton > 0 && L.passes == 0 && L.phases == PHASE_APPLY && multi_ok(L.n, L.T)) {
+    if (L.T == 1) return launch_multi<1>(p, L, stream);
+    if (L.T == 2) return launch_multi<2>(p, L, stream);
+    if (L.T <= 4) return launch_multi<4>(p, L, stream);
+    return launch_multi<8>(p, L, stream);
   }
   const int nbf = std::min(nblk, fused_capacity() / L.T);  // co-resident grid for grid.sync
   if (L.newton > 0 && L.passes == 0 && L.phases == PHASE_APPLY && nbf >= 1) {

@@ -24,6 +24,12 @@ enum ProjPhase { PHASE_RANGE = 1, PHASE_EXACT = 2, PHASE_APPLY = 4 };
 using ProjState = ssnal_proj_state_t;
 using CsrOp = ssnal_csr_operator_t;
 
+// device-side control of the kept q-space Gram (dense.cu gram_select_kernel)
+struct GramCtl {
+  long long count, accum, builds, updates, rows;
+  int mode, valid;
+};
+
 cudaError_t launch_csr_xd(const CsrOp& op, const int32_t* rows, long long nrows, const double* d,
                           double* out, cudaStream_t stream);
 cudaError_t launch_csc_xt(const CsrOp& op, const double* v, double* out, double* part,
@@ -85,11 +91,15 @@ struct ProjLaunch {
   int passes;
   double hint;  // warm-start multiplier for the Newton passes
   int newton;   // Newton passes (0: start from the full breakpoint range instead)
+  int defer = 0;  // batched trials may leave x / the mask unwritten (see proj_defers)
 };
 
 int proj_blocks(long long n);
-int proj_wave_trials(long long n);
+int proj_wave_trials(long long n, bool first = false);
 size_t proj_ws_bytes(long long n, int T);
 cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream);
+bool proj_defers(long long n, int T);
+cudaError_t launch_proj_materialize(const ProjLaunch& L, double coef, const ProjState* st,
+                                    double* x_out, unsigned char* f_out, cudaStream_t stream);
 
 }  // namespace ssnal

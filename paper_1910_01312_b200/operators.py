@@ -149,7 +149,14 @@ class CsrKernelOperator:
         seg_slot[split] = np.arange(int(split.sum()))
         fold_cols = np.flatnonzero(nseg_col > 1)
         fold_beg = np.concatenate([[0], np.cumsum(nseg_col[fold_cols])]).astype(np.int32)
-        dev = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=be.device)  # noqa: E731
+        from .backend import H2D
+
+        def dev(a, dt):
+            t = torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=be.device)
+            if be.device.type == "cuda":
+                H2D["bytes"] += t.numel() * t.element_size()
+            return t
+
         self._t = {
             "indptr": dev(A.indptr.astype(np.int64), torch.int64),
             "indices": dev(A.indices.astype(np.int32), torch.int32),

@@ -603,8 +603,11 @@ def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_devi
         cb = _lib.PROGRESS_FN()
     _lib.call("ssnal_alm_solve_dense", ctypes.byref(prob), ctypes.byref(opts), ptr(x0d), ptr(w0d),
               ptr(x_out), ctypes.byref(rep), ptr(ws), ws.numel(), cb, None, be.stream())
-    notes = [f"inner solver hit max_inner at outer iteration {k}" for k in range(31)
-             if rep.hit_max_inner_mask >> k & 1]
+    notes = [f"inner solver hit max_inner at outer iteration {k}" for k in range(64)
+             if rep.hit_max_inner_mask64 >> k & 1]
+    if rep.hit_max_inner_count > len(notes):
+        notes.append(f"inner solver hit max_inner at {rep.hit_max_inner_count - len(notes)} "
+                     "more outer iterations (k >= 64)")
     if rep.stagnated:
         notes.append("stagnated at the attainable accuracy for sigma_max; returning the best "
                      "iterate")
@@ -612,9 +615,11 @@ def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_devi
         notes.append(f"max_outer={alm_opts.max_outer} reached")
     problem.native_counters = {"syncs": rep.syncs, "newton": rep.newton_steps,
                                "projections": rep.projections, "cg_iters": rep.cg_iters,
-                               "cg_fallbacks": rep.cg_fallbacks}
+                               "cg_fallbacks": rep.cg_fallbacks,
+                               "gram_builds": rep.gram_builds, "gram_updates": rep.gram_updates,
+                               "gram_rows": rep.gram_rows, "proj_fallbacks": rep.proj_fallbacks}
     problem.op_profile = {name: {"calls": int(rep.op_calls[k]), "seconds": float(rep.op_seconds[k]),
-                                 "bytes": float(rep.op_bytes[k])}
+                                 "bytes": float(rep.op_bytes[k]), "flops": float(rep.op_flops[k])}
                           for k, name in enumerate(_lib.OP_NAMES)}
     return SolveReport(
         x_opt=x_out if return_device else x_out.cpu().numpy(),

@@ -66,9 +66,14 @@ def build_svr_dual(features, targets, C, epsilon, backend=None):
     op = LinearKernelOperator(features, svr_block=True, backend=be)
     if op.n_phys != n:
         raise InputError("targets must have one entry per sample")
-    c = np.concatenate([epsilon - t, epsilon + t])
+    # c = (eps - t; eps + t) and a = (e; -e) formed on the device from ONE upload of t
+    t_dev = as_device(t, be)
+    c = torch.cat([epsilon - t_dev, epsilon + t_dev])
+    a_dev = torch.cat([torch.ones(n, dtype=torch.float64, device=be.device),
+                       torch.full((n,), -1.0, dtype=torch.float64, device=be.device)])
     a = np.concatenate([np.ones(n), -np.ones(n)])
-    box = BoxLineSet(a=a, d=0.0, l=np.zeros(2 * n), u=np.full(2 * n, float(C)), backend=be)
+    box = BoxLineSet(a=a, d=0.0, l=np.zeros(2 * n), u=np.full(2 * n, float(C)), backend=be,
+                     a_device=a_dev)
     return QpProblem(op, c, box)
 
 

@@ -135,6 +135,37 @@ def test_projection_batched_trials(pkg):
     del B
 
 
+@pytest.mark.parametrize("T", [1, 2, 3, 5, 8])
+def test_projection_batched_trials_large_n(pkg, T):
+    """n above the cluster kernel's capacity: the multi-trial cooperative kernel (every
+    trial of the batch from ONE read of u, Qd, a per pass) matches the oracle trial by
+    trial; eps-SVR-shaped constraint a = (e; -e)."""
+    rng = np.random.default_rng(30 + T)
+    m = 150_000
+    n = 2 * m
+    a = np.concatenate([np.ones(m), -np.ones(m)])
+    box = pkg.BoxLineSet(a, 0.0, np.zeros(n), np.ones(n))
+    be = box.backend
+    u = rng.standard_normal(n) * 2
+    qd = rng.standard_normal(n)
+    coefs = [5.0 * 0.5 ** j for j in range(T)]
+    states = be.new_states(T)
+    xo = be.empty((T, n))
+    fo = be.empty((T, n), torch.uint8)
+    st = be.project_sync(_dev(u), box, states, T=T, B=_dev(qd), coefs=coefs, x_out=xo,
+                         free_out=fo, hint=0.3)
+    bl = O.BoxLine(a, 0.0, np.zeros(n), np.ones(n))
+    for t, cf in enumerate(coefs):
+        v = u - cf * qd
+        x_ref, lam_ref, free_ref = O.project(v, bl)
+        assert abs(float(st["lam"][t]) - lam_ref) <= 1e-12 * (1.0 + abs(lam_ref))
+        assert np.abs(xo[t].cpu().numpy() - x_ref).max() <= 1e-12
+        np.testing.assert_array_equal(fo[t].cpu().numpy().astype(bool), free_ref)
+        assert st["sum_v2"][t] == pytest.approx(v @ v, rel=1e-12)
+        assert st["sum_r2"][t] == pytest.approx(((v - x_ref) ** 2).sum(), rel=1e-10, abs=1e-14)
+        assert st["nfree"][t] == free_ref.sum()
+
+
 def test_hs_jacobian_golden(pkg):
     for c in load_cases("hs_jacobian.npz", "h"):
         py = pkg.hs_jacobian_apply(_dev(c["free"], torch.uint8), c["a"], c["y"]).cpu().numpy()
@@ -188,9 +219,10 @@ def test_dense_products(pkg, shape, svr, signed):
     assert np.abs(out.T - ref).max() <= 1e-12 * np.abs(X).sum(axis=1).max() * np.abs(d).max()
 
 
-@pytest.mark.parametrize("m", [1, 7, 33, 115, 160, 161, 300, 517])
+@pytest.mark.parametrize("m", [1, 7, 33, 115, 160, 161, 300, 500, 517, 768, 769, 1100])
 def test_cholesky_solve_sizes(pkg, m):
-    """Both Cholesky routes (shared-memory resident m <= 160, blocked otherwise)."""
+    """Every Cholesky route: shared-memory resident (m <= 160), one 16-CTA cluster
+    (m <= 768), grid-wide cooperative (m <= 2048)."""
     be = pkg.default_backend()
     rng = np.random.default_rng(m)
     G = rng.standard_normal((m, m + 3))

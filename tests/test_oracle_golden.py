@@ -121,3 +121,68 @@ def test_bregman_term_is_the_psi_difference():
             assert dpsi == pytest.approx(psi_t - psi0, rel=1e-9, abs=1e-12)
     finally:
         O.set_psi_mode("reference")
+
+
+def _factor_ops(c):
+    """The golden case's Q = G'G as a dense and a CSR factor X = G' (n x k)."""
+    import scipy.sparse as sp
+
+    X = np.ascontiguousarray(c["G"].T)
+    Xs = sp.csr_matrix(X)
+    return [O.FactoredQ(X), O.CsrFactoredQ(Xs.indptr, Xs.indices, Xs.data, X.shape)]
+
+
+def test_factor_newton_direction_matches_reference():
+    """newton_direction_factor (the oracle route for configs 2-4 at full size) gives the
+    reference's Qd, d'Qd and d on every golden Newton case, on all three routes
+    (q x q Cholesky, p x p Woodbury, Jacobi-PCG) and for dense and CSR factors."""
+    checked = {"q": 0, "p": 0, "cg": 0}
+    for c in load_cases("newton.npz", "n"):
+        q = c["G"].T @ c["G"]
+        bl = _bl(c)
+        sigma = c["sigma"]
+        u = c["x"] - sigma * (q @ c["w"] + c["c"])
+        x, lam, free = O.project(u, bl)
+        s = c["w"] - x
+        p, k = int(free.sum()), c["G"].shape[0]
+        routes = {"q": O.SsnOpts(direct_solve_threshold=max(k, 1)),
+                  "cg": O.SsnOpts(direct_solve_threshold=0, cg_eta_cap=1e-15)}
+        if 0 < p < k:
+            routes["p"] = O.SsnOpts(direct_solve_threshold=p)
+        for op in _factor_ops(c):
+            for name, opts in routes.items():
+                d, qd, dqd = O.newton_direction_factor(s, op.matvec(s), free, sigma, op, bl.a,
+                                                       opts)
+                tol = 1e-9 if name != "cg" else 1e-7
+                sc = 1.0 + np.linalg.norm(c["qdir"])
+                assert np.linalg.norm(qd - c["qdir"]) <= tol * sc, (name, p, k)
+                assert abs(dqd - c["dqd"]) <= tol * (1.0 + abs(c["dqd"])), (name, p, k)
+                assert np.linalg.norm(d - c["dir"]) <= tol * (1.0 + np.linalg.norm(c["dir"]))
+                checked[name] += 1
+    assert all(v > 0 for v in checked.values()), checked
+
+
+@pytest.mark.parametrize("mode", ["reference", "delta"])
+def test_factor_route_solves_golden_svm_cases(mode):
+    """alm_solve with the factor-space Newton route (dense and CSR samples) reproduces
+    the reference's outer/inner counts and objective on the golden SVM cases."""
+    import scipy.sparse as sp
+
+    O.set_psi_mode(mode)
+    try:
+        for c in load_cases("solve.npz", "s"):
+            if c["kind"] == "dense":
+                continue
+            probs = [_problem(c)]
+            if c["kind"] == "csvc":
+                A = sp.csr_matrix(c["A"])
+                probs.append(O.csvc_problem_csr(A.indptr, A.indices, A.data, A.shape, c["y"],
+                                                c["C"]))
+            for op, cc, bl in probs:
+                rep = O.alm_solve(op, cc, bl, O.AlmOpts(tol_kkt=c["tol"]),
+                                  O.SsnOpts(newton="factor"))
+                assert rep["converged"] and rep["kkt_residual"] < c["tol"]
+                assert (rep["outer_iters"], rep["total_inner_iters"]) == (c["outer"], c["inner"])
+                assert rep["objective"] == pytest.approx(c["obj"], rel=1e-8, abs=1e-9)
+    finally:
+        O.set_psi_mode("reference")
