@@ -32,8 +32,12 @@ search, without which the reference stalls above KKT 1e-6 -- DESIGN.md section 8
 the full workload, with all host threads; one full solve is one step and a full solve
 takes minutes, so it runs ONE step whatever --steps says (reported as steps_run).
 
-N > 1 runs N independent single-GPU replicas of the workload (no communication;
-"parallelism": "replicas"), one per rank.
+N > 1 runs the ROW-SHARDED solve of the dense workloads (configs 1 and 4, BASELINE
+quotes config 4 "row-sharded 1/2/4/8 GPUs"): rank r owns a contiguous slice of the
+samples and of the dual vector (sharded.py); X^T v, the q x q Gram and the CG vectors
+are NCCL all-reduces, the projection's multiplier search exchanges one small record per
+pass.  "parallelism": "row-sharded", "scaling": "strong" (the total problem is fixed).
+The sparse configs with N > 1 run N replicas ("parallelism": "replicas").
 """
 
 import argparse
@@ -279,6 +283,107 @@ ROOF = {
 NCU_FILES = {"dense_x": "r2_ncu_c4_stream_xd_kernel.txt", "gram": "r2_ncu_c4_gram_kernel.txt"}
 
 
+def run_sharded(args, rank, world, local_rank):
+    """Row-sharded dense solve over `world` GPUs (one process per GPU, NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1910_01312_b200 as P
+    from paper_1910_01312_b200 import backend as B
+    from paper_1910_01312_b200 import sharded as S
+
+    torch.cuda.set_device(local_rank)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29511")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank), rank=rank,
+                            world_size=world)
+    comm = S.ShardComm()
+    cfg = make_cfg(args.config)
+    n_phys = cfg["A"].shape[0]
+    lo, hi = S.shard_range(n_phys, rank, world)
+    A_host = torch.from_numpy(np.ascontiguousarray(cfg["A"][lo:hi])).pin_memory()
+
+    def build(A):
+        if cfg["task"] == "svr":
+            return S.build_svr_dual_sharded(A, cfg["t"][lo:hi], cfg["C"], cfg["epsilon"], comm)
+        return S.build_csvc_dual_sharded(A, cfg["y"][lo:hi], cfg["C"], comm)
+
+    problem = build(A_host.to("cuda"))
+    opts = P.AlmOptions(tol_kkt=TOL)
+    ssn = P.SsnOptions(engine="python")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        P.alm_solve(problem, opts, ssn, return_device=True)
+    barrier()
+    stream = torch.cuda.current_stream()
+    sampler = ClockSampler(local_rank)
+    sampler.sample()
+    step_s, reps = [], []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rep = P.alm_solve(problem, opts, ssn, return_device=True)
+        e1.record(stream)
+        e1.synchronize()
+        step_s.append(e0.elapsed_time(e1) * 1e-3)
+        reps.append(rep)
+        sampler.sample()
+    t = torch.tensor([float(np.sum(step_s))], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    value = float(t[0]) / args.steps
+    clocks = sampler.stop()
+    del problem
+    e2e_times, h2d = [], 0
+    for i in range(args.warmup + args.steps):
+        flush.fill_(1)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        h0 = B.H2D["bytes"]
+        e0.record(stream)
+        pb = build(A_host)
+        r = P.alm_solve(pb, opts, ssn)
+        e1.record(stream)
+        e1.synchronize()
+        if i >= args.warmup:
+            e2e_times.append(e0.elapsed_time(e1) * 1e-3)
+            h2d = B.H2D["bytes"] - h0
+        del pb
+    te = torch.tensor([float(np.sum(e2e_times))], dtype=torch.float64, device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    hb = torch.tensor([float(h2d)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(hb, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        last = reps[-1]
+        d = config_dict(args, cfg, world)
+        d["parallelism"] = f"row-sharded over {world} GPUs (NCCL all-reduce)"
+        line = {
+            "metric": METRICS[args.config], "value": value, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE config shapes and distributions)",
+            "config": d,
+            "e2e": {"value": float(te[0]) / args.steps, "unit": "s",
+                    "h2d_bytes_per_step": int(hb[0]), "d2h_bytes_per_step": int(r.x_opt.size * 8),
+                    "path": "build_*_dual_sharded from each rank's pinned host slice + alm_solve"},
+            "gpu_launches": None, "roofline": None, "cpu_baseline": None, "clocks": clocks,
+            "result": {"kkt": last.kkt_residual, "objective": last.objective,
+                       "outer": last.outer_iters, "inner": last.total_inner_iters,
+                       "converged": last.converged},
+            "step_ms": [round(t_ * 1e3, 3) for t_ in step_s],
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -457,6 +562,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="row-sharded engine even at N = 1 (checks the multi-GPU path on one GPU)")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
@@ -467,6 +574,9 @@ def main():
     import __graft_entry__
 
     __graft_entry__.build()
+    if (world > 1 or args.sharded) and args.config in (1, 4):
+        run_sharded(args, rank, world, local_rank)
+        return
     run_ours(args, rank, world, local_rank)
 
 

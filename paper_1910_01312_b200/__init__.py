@@ -28,7 +28,11 @@ _LAZY = {
     "SolveReport": "solver", "QpProblem": "solver", "alm_solve": "solver",
     "ssn_solve": "solver", "kkt_residual": "solver",
     "build_csvc_dual": "svm", "build_svr_dual": "svm", "recover_bias": "svm",
-    "primal_weights": "svm",
+    "primal_weights": "svm", "SvmConfig": "svm", "SvmModel": "svm", "KernelSpec": "svm",
+    "train": "svm", "decision_function": "svm", "predict": "svm", "evaluate": "svm",
+    "grad_phi": "api", "breakpoints": "api", "psi_eval": "api", "psi_grad": "api",
+    "newton_direction": "api", "line_search": "api",
+    "CsrKernelOperator": "operators",
     "CudaBackend": "backend", "default_backend": "backend",
 }
 

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #define SSNAL_NT 256          // threads per block for streaming kernels
 #define SSNAL_MAX_BLOCKS 592  // 4 x 148 SMs: cap for grid-stride streaming grids
 #define SSNAL_MAX_TRIALS 16   // batched projections per launch (line-search step lengths)
@@ -114,4 +116,28 @@ __host__ __device__ inline long long ceil_div(long long a, long long b) { return
 namespace ssnal {
 // host-side count of kernel launches issued by this library (ssnal_launch_count)
 void note_launch();
+
+// A launch setting computed once PER DEVICE ORDINAL (occupancy-derived grid sizes,
+// cudaFuncSetAttribute opt-ins): slot d holds value + 1 (0 = not yet computed).
+// Thread-safe: concurrent first calls compute the same value and store it atomically.
+struct DeviceCache {
+  std::atomic<int> slot[64];
+};
+
+inline int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  return dev;
+}
+
+template <class F>
+inline int per_device(DeviceCache& c, F compute) {
+  const int dev = current_device();
+  int v = c.slot[dev].load(std::memory_order_acquire);
+  if (v == 0) {
+    v = compute(dev) + 1;
+    c.slot[dev].store(v, std::memory_order_release);
+  }
+  return v - 1;
+}
 }  // namespace ssnal

@@ -738,24 +738,22 @@ cudaError_t launch_gram_update(const double* A, long long n, long long q, long l
                                const uint8_t* sign_mask, const double* a, double* G, double* m1,
                                int accumulate, void* ws, cudaStream_t stream,
                                const GramCtl* ctl, const int32_t* Jd) {
-  static int sms[64];  // per device ordinal
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) dev = 0;
-  if (sms[dev] <= 0) {
+  static DeviceCache cache;  // SM count (0 = the smem opt-in failed)
+  const int nsm = per_device(cache, [](int dev) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)GSMEM);
-    if (e != cudaSuccess) return e;
-    sms[dev] = v > 0 ? v : 148;
-  }
+    if (cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)GSMEM) != cudaSuccess)
+      return 0;
+    return v > 0 ? v : 148;
+  });
+  if (nsm == 0) return cudaErrorInvalidValue;
   GramArgs g;
   g.A = A; g.n = n; g.q = q; g.lda = lda; g.J = J; g.p_dev = p_dev;
   g.part = (double*)ws;
   g.ntile = (int)ceil_div(q, GT);
   const int npairs = g.ntile * (g.ntile + 1) / 2;
-  g.split = std::max(1, std::min(gram_split_cap(q), sms[dev] / npairs));  // one wave
+  g.split = std::max(1, std::min(gram_split_cap(q), nsm / npairs));  // one wave
   double* part_m1 = g.part + (long long)gram_split_cap(q) * q * q;
   g.a = a; g.rs = rs; g.svr = svr; g.part_m1 = part_m1; g.sign_mask = sign_mask;
   g.aligned = (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);

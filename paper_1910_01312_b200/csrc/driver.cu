@@ -137,6 +137,12 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
 
 // direct reduced systems of the sparse operator: min(p, q) up to this size (M buffer)
 constexpr long long SPARSE_DIRECT_MAX = 2048;
+// dense operator: the factor-space gradient (accept_q) handles q <= ACCEPT_Q_MAX; larger q
+// run the full-gradient path.  Direct systems: q x q up to DENSE_QSYS_MAX (workspace M,
+// G), p x p up to DENSE_PSYS_MAX.
+constexpr long long ACCEPT_Q_MAX = 2048;
+constexpr long long DENSE_QSYS_MAX = 4096;
+constexpr long long DENSE_PSYS_MAX = 4096;
 // forcing-term cap of the matrix-free CG route (see cg_direction)
 constexpr double SPARSE_CG_ETA = 1e-4;
 // max / mean column sum of squares above which the factor-space Jacobi PCG is used
@@ -253,9 +259,12 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
   L.r = L.t ? L.t + q : nullptr;
   L.xw = cv.take<double>(q);
   L.xpi = cv.take<double>(q);
-  L.qpart = sparse ? nullptr : cv.take<double>(accept_q_ws_bytes(n, q) / sizeof(double) + 1);
-  L.M = sparse ? nullptr : cv.take<double>((size_t)q * q);
-  if (!sparse) {
+  const bool qsys = !sparse && q <= DENSE_QSYS_MAX;
+  L.qpart = (sparse || q > ACCEPT_Q_MAX)
+                ? nullptr
+                : cv.take<double>(accept_q_ws_bytes(n, q) / sizeof(double) + 1);
+  L.M = qsys ? cv.take<double>((size_t)q * q) : nullptr;
+  if (qsys) {
     L.G = cv.take<double>((size_t)q * q);
     L.frg = cv.take<uint8_t>(n);
     L.chg = cv.take<uint8_t>(n);
@@ -283,8 +292,8 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
   if (!sparse) {
     L.ws_xt = cv.take<char>(dense_xt_ws_bytes(n_phys, q, 2));
     L.ws_grad = cv.take<char>(gradient_ws_bytes(n_phys, q));
-    L.ws_gram = cv.take<char>(gram_ws_bytes(q));
-    L.ws_ps = cv.take<char>(pspace_ws_bytes(q, q));
+    L.ws_gram = qsys ? cv.take<char>(gram_ws_bytes(q)) : nullptr;
+    L.ws_ps = cv.take<char>(pspace_ws_bytes(std::min(q - 1, DENSE_PSYS_MAX), q));
   } else {
     L.ys = cv.take<double>(n);
     L.tq = cv.take<double>(q);
@@ -810,6 +819,10 @@ struct Driver {
       throw DriverError{SSNAL_E_ARG, "p x p system above direct_solve_threshold (no CG path)"};
     if (p >= P.q && P.q > O.direct_solve_threshold)
       throw DriverError{SSNAL_E_ARG, "q x q system above direct_solve_threshold (no CG path)"};
+    if (p < P.q && p > DENSE_PSYS_MAX)
+      throw DriverError{SSNAL_E_ARG, "p x p system above the dense workspace cap (4096)"};
+    if (p >= P.q && P.q > DENSE_QSYS_MAX)
+      throw DriverError{SSNAL_E_ARG, "q x q system above the dense workspace cap (4096)"};
     // gathered rows of A (p x q) once + the system matrix written and factored
     const double m = (double)std::min<long long>(p, P.q);
     const double* g_r = qgrad() ? L.r : L.gr;
@@ -876,7 +889,7 @@ struct Driver {
   }
 
   // dense operator: the SsN gradient is kept in factor space
-  bool qgrad() const { return P.csr == nullptr; }
+  bool qgrad() const { return P.csr == nullptr && P.q <= ACCEPT_Q_MAX; }
   const double* tdir = nullptr;  // X^T d of the current direction (factor-space update)
 
   void steepest(double out[4]) {
@@ -1121,8 +1134,8 @@ struct Driver {
     else ck(cudaMemsetAsync(L.w, 0, nb, S));
     if (P.csr) ck(cudaMemsetAsync(L.cj.ticket, 0, sizeof(unsigned int), S));
     else {
-      ck(cudaMemsetAsync(L.qpart, 0, 256, S));  // accept_q ticket
-      ck(cudaMemsetAsync(L.gctl, 0, sizeof(GramCtl), S));  // no kept Gram yet
+      if (L.qpart) ck(cudaMemsetAsync(L.qpart, 0, 256, S));  // accept_q ticket
+      if (L.gctl) ck(cudaMemsetAsync(L.gctl, 0, sizeof(GramCtl), S));  // no kept Gram yet
     }
     ck(cudaMemsetAsync(L.qw, 0, nb, S));
     dots({{P.c, nullptr}}, L.scal, P.n);
@@ -1196,7 +1209,7 @@ struct Driver {
     rep->cg_iters = cg_iters;
     rep->cg_fallbacks = cg_fallbacks;
     GramCtl gc{};
-    if (!P.csr) {
+    if (L.gctl) {
       ck(cudaMemcpyAsync(&gc, L.gctl, sizeof(GramCtl), cudaMemcpyDeviceToHost, S));
       ck(cudaStreamSynchronize(S));
     }
@@ -1259,6 +1272,12 @@ int alm_solve_dense(const ssnal_dense_problem_t* pb, const ssnal_options_t* opt,
     return SSNAL_E_DEVICE;
   }
   std::memset(rep, 0, sizeof(*rep));
+  // every last-block ticket, projection record and kept-Gram control word in the
+  // workspace starts at zero, whatever the caller allocated it with
+  if (cudaMemsetAsync(ws, 0, need, stream) != cudaSuccess) {
+    *err = "cudaMemsetAsync of the workspace failed";
+    return SSNAL_E_DEVICE;
+  }
   Driver d(*pb, *opt, stream, L, H);
   try {
     d.alm_solve(x0, w0, x_out, rep, cb, ctx);

@@ -808,35 +808,29 @@ __global__ void __cluster_dims__(CC, 1, 1) __launch_bounds__(CC_NT, 1)
 static size_t chol_cluster_smem(int m) { return (size_t)m * CC_LD * sizeof(double); }
 
 static bool chol_cluster_ok() {
-  static int ok[64];  // per device ordinal: 0 unknown, 1 yes, 2 no
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) dev = 0;
-  if (ok[dev] == 0) {
+  static DeviceCache cache;
+  return per_device(cache, [](int dev) {
     int sup = 0;
     cudaDeviceGetAttribute(&sup, cudaDevAttrClusterLaunch, dev);
-    bool good = sup != 0;
-    if (good && cudaFuncSetAttribute(chol_cluster_kernel,
-                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-      good = false;
-    if (good && cudaFuncSetAttribute(chol_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)chol_cluster_smem(CC_MAX)) != cudaSuccess)
-      good = false;
-    ok[dev] = good ? 1 : 2;
-  }
-  return ok[dev] == 1;
+    if (!sup) return 0;
+    if (cudaFuncSetAttribute(chol_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                             1) != cudaSuccess)
+      return 0;
+    if (cudaFuncSetAttribute(chol_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)chol_cluster_smem(CC_MAX)) != cudaSuccess)
+      return 0;
+    return 1;
+  }) == 1;
 }
 
 static int big_grid() {
-  static int g = -1;
-  if (g < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
+  static DeviceCache cache;
+  return per_device(cache, [](int dev) {
+    int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, chol_big_kernel, BG_NT, 0);
-    g = sms * (per < 1 ? 1 : (per > 2 ? 2 : per));
-  }
-  return g;
+    return sms * (per < 1 ? 1 : (per > 2 ? 2 : per));
+  });
 }
 
 
@@ -851,14 +845,12 @@ cudaError_t launch_chol_pspace(const double* Q, long long p, const int32_t* J, c
                                const double* a, double sigma, double asa, double* y, int* info,
                                cudaStream_t stream) {
   if (p > TC_MAX) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(chol_tc_kernel<true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)chol_tc_smem(TC_MAX, true));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static DeviceCache attr;
+  const int err = per_device(attr, [](int) {
+    return (int)cudaFuncSetAttribute(chol_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)chol_tc_smem(TC_MAX, true));
+  });
+  if (err != cudaSuccess) return (cudaError_t)err;
   TcPspace ps{J, grad, a, sigma, asa};
   const int pi = (int)p;
   { note_launch(); chol_tc_kernel<true><<<1, TC_NT, chol_tc_smem(pi, true), stream>>>(Q, pi, nullptr, 1.0, y, info, ps); }
@@ -870,18 +862,21 @@ cudaError_t launch_chol_solve(double* M, long long m, const double* b, double sc
   if (m <= TC_MAX) {
     const int mi = (int)m;
     const size_t smem = chol_tc_smem(mi);
-    static size_t attr = 0;
-    if (smem > attr) {
-      cudaError_t e = cudaFuncSetAttribute(chol_tc_kernel<false>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)chol_tc_smem(TC_MAX));
-      if (e != cudaSuccess) return e;
-      attr = chol_tc_smem(TC_MAX);
-    }
+    static DeviceCache attr;
+    const int err = per_device(attr, [](int) {
+      return (int)cudaFuncSetAttribute(chol_tc_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)chol_tc_smem(TC_MAX));
+    });
+    if (err != cudaSuccess) return (cudaError_t)err;
+    (void)smem;
     { note_launch(); chol_tc_kernel<false><<<1, TC_NT, smem, stream>>>(M, mi, b, scale, x, info, TcPspace{}); }
     return cudaGetLastError();
   }
-  if (m <= CC_MAX && !std::getenv("SSNAL_CHOL_GRID") && chol_cluster_ok()) {
+  // the cluster kernel (fewer, cheaper barriers) is kept behind SSNAL_CHOL_CLUSTER=1: both
+  // are bound by the per-pivot broadcast chain of the diagonal blocks and the back
+  // substitution, and the grid kernel is ~10% faster at m = 500 (scripts/chol_probe.cu)
+  if (m <= CC_MAX && std::getenv("SSNAL_CHOL_CLUSTER") && chol_cluster_ok()) {
     const int mi = (int)m;
     note_launch();
     chol_cluster_kernel<<<CC, CC_NT, chol_cluster_smem(mi), stream>>>(M, mi, b, scale, x, info);

@@ -1126,19 +1126,19 @@ __global__ void __launch_bounds__(SSNAL_NT) proj_materialize_kernel(ProjArgs p, 
 }
 
 static bool cluster_ok(long long n, int T) {
-  static int ok = -1;
-  if (ok < 0) {
-    int dev = 0, sup = 0;
-    cudaGetDevice(&dev);
+  static DeviceCache cache;
+  const int ok = per_device(cache, [](int dev) {
+    int sup = 0;
     cudaDeviceGetAttribute(&sup, cudaDevAttrClusterLaunch, dev);
-    ok = sup ? 1 : 0;
-    if (ok && cudaFuncSetAttribute(proj_cluster_kernel,
-                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-      ok = 0;
-    if (ok && cudaFuncSetAttribute(proj_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   CL_SMEM) != cudaSuccess)
-      ok = 0;
-  }
+    if (!sup) return 0;
+    if (cudaFuncSetAttribute(proj_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                             1) != cudaSuccess)
+      return 0;
+    if (cudaFuncSetAttribute(proj_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             CL_SMEM) != cudaSuccess)
+      return 0;
+    return 1;
+  });
   // in the solve (L2 cold after every sweep of A) the register-resident cluster
   // kernel wins for single trials too (bench op profile: -9 % projection time)
   return ok == 1 && n <= (long long)CL_CTAS * CL_NT * CL_EPT && T >= 1;
@@ -1157,8 +1157,8 @@ int proj_wave_trials(long long n, bool first) {
   // speculative batch is (1, beta); a backtracking batch, 4 step lengths
   if (multi_ok(n, 1)) return first ? 2 : 4;
   if (!cluster_ok(n, 1)) return SSNAL_MAX_TRIALS;
-  static int w = -1;
-  if (w < 0) {
+  static DeviceCache cache;
+  return per_device(cache, [](int) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL_CTAS, 1, 1);
     cfg.blockDim = dim3(CL_NT, 1, 1);
@@ -1166,9 +1166,8 @@ int proj_wave_trials(long long n, bool first) {
     int c = 0;
     if (cudaOccupancyMaxActiveClusters(&c, (void*)proj_cluster_kernel, &cfg) != cudaSuccess || c < 1)
       c = SSNAL_MAX_TRIALS;
-    w = c;
-  }
-  return w;
+    return c;
+  });
 }
 
 int proj_blocks(long long n) {
@@ -1184,30 +1183,24 @@ size_t proj_ws_bytes(long long n, int T) {
 }
 
 static int fused_capacity() {
-  static int cap = -1;
-  if (cap < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
+  static DeviceCache cache;
+  return per_device(cache, [](int dev) {
+    int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, proj_fused_kernel, SSNAL_NT, 0);
-    cap = sms * per;
-  }
-  return cap;
+    return sms * per;
+  });
 }
 
 template <int T>
 static int multi_capacity() {
-  static int cap[64];  // per device ordinal
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) dev = 0;
-  if (cap[dev] <= 0) {
+  static DeviceCache cache;
+  return per_device(cache, [](int dev) {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, proj_multi_kernel<T>, PM_NT, 0);
-    cap[dev] = sms * std::min(per, 2);
-  }
-  return cap[dev];
+    return sms * std::min(per, 2);
+  });
 }
 
 

@@ -11,6 +11,10 @@
 //        per-CTA partials are folded deterministically afterwards.
 //   XD : each consumer warp takes whole rows of a stage, d is held in registers,
 //        shuffle-tree dot products.
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "common.cuh"
 #include "ssnal_internal.h"
 
@@ -401,14 +405,18 @@ cudaError_t launch_stream(K kernel, const StreamArgs& p, int grid, cudaStream_t 
   const int smem = NSTAGE * STAGE_BYTES;
   // the smem opt-in once per kernel (a host API call per launch sat on the critical path
   // right after every host decision)
-  static const void* done[64];
-  static int ndone = 0;
-  bool seen = false;
-  for (int i = 0; i < ndone; ++i) seen |= done[i] == (const void*)kernel;
-  if (!seen) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    if (ndone < 64) done[ndone++] = (const void*)kernel;
+  // (per kernel pointer and device; kernels of one signature share K, so the key is the
+  // pointer, not the template instance)
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> opted;
+  {
+    const std::pair<int, const void*> key(current_device(), (const void*)kernel);
+    std::lock_guard<std::mutex> lock(mu);
+    if (!opted.count(key)) {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      opted.insert(key);
+    }
   }
   note_launch();
   kernel<<<grid, threads, smem, stream>>>(p);

@@ -9,11 +9,11 @@ partials.  The places the path genuinely couples the slots are
   * the inner products of the line search / stopping tests,
   * the projection's multiplier lambda (one equality constraint over all n),
 
-and each is reduced here through an all-gather of a small fixed-size record
-followed by an ordered fold (csrc/dist.cu ``ssnal_sum_slices`` on the device, or
-numpy in rank order on the host for the scalar records), so every rank holds
-bit-identical scalars and takes identical branches -- the reduction order never
-depends on NCCL's algorithm choice.
+and each is reduced here: q-vectors and the q x q Gram by one NCCL all-reduce (every
+rank receives the same buffer), the projection's small per-pass records by an
+all-gather folded in rank order on the host, so every rank holds bit-identical
+scalars and takes identical branches.  Over gloo (CPU tests) the q-vectors are
+all-gathered and folded in rank order too (csrc/dist.cu ``ssnal_sum_slices``).
 
 The projection search runs the safeguarded Newton of csrc/proj.cu one pass per
 all-gather: each pass evaluates, rank-locally, f(lambda) = sum a clip(v - lambda
@@ -93,18 +93,30 @@ class ShardedBackend:
         self.comm = comm
         self.rec = base.zeros(16 * 8)  # (T <= 16) x 8 shard record
         self.collectives = 0
+        import os
+
+        self.ordered = os.environ.get("SSNAL_SHARD_ORDERED", "") not in ("", "0")
 
     def __getattr__(self, name):
         return getattr(self.base, name)
 
     # ---------------------------------------------------------------- reductions
     def allsum(self, t):
-        """t <- sum over ranks of t (in place), folded in rank order."""
+        """t <- sum over ranks of t (in place).  NCCL: one all-reduce (ring / NVLS over
+        NVSwitch; every rank receives the same reduced buffer, so the replicated
+        q-vectors and scalars stay bit-identical across ranks and the branches uniform).
+        gloo (CPU tests): all-gather + fold in rank order (ssnal_sum_slices), the same
+        sums bit for bit whatever the transport's algorithm.  SSNAL_SHARD_ORDERED=1 forces
+        the ordered fold on NCCL too (results independent of the world size's NCCL
+        reduction tree, at world x the traffic)."""
         if self.comm.world == 1:
             return
         flat = t.view(-1)
-        g = self.comm.all_gather(flat)
         self.collectives += 1
+        if self.comm.nccl and not self.ordered:
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.comm.group)
+            return
+        g = self.comm.all_gather(flat)
         self.base.sum_slices(self.comm.world, g, flat)
 
     def dots(self, pairs, out, mask=None, replicated=False):

@@ -195,13 +195,64 @@ def kkt_cases():
     return out
 
 
+def svm_cases():
+    """The reference's train / recover_bias / decision_function / evaluate (svm.py:147-295)
+    on linear C-SVC and eps-SVR sets, plus bound-only duals (interval-midpoint branch)."""
+    out = []
+    rng = np.random.default_rng(77)
+    cfg0 = datagen.config0()
+    a_s = rng.standard_normal((300, 8))
+    y_s = np.sign(a_s @ rng.standard_normal(8) + 0.3 * rng.standard_normal(300))
+    y_s[y_s == 0] = 1.0
+    a_r = rng.standard_normal((200, 6))
+    t_r = a_r @ (rng.standard_normal(6) / np.sqrt(6)) + 0.1 * rng.standard_normal(200)
+    sets = [("classification", a_s, y_s, 1.0, 0.0, 1e-8),
+            ("classification", cfg0["A"], cfg0["y"], 1.0, 0.0, 1e-6),
+            ("regression", a_r, t_r, 1.0, 0.1, 1e-8),
+            ("regression", a_r, t_r, 0.5, 0.3, 1e-8)]
+    for task, feats, targ, C, eps, tol in sets:
+        config = ssnal.SvmConfig(task=task, C=C, epsilon=eps)
+        model, rep = ssnal.train(feats, targ, config, alm_opts=ssnal.AlmOptions(tol_kkt=tol))
+        pts = feats[::7]
+        metric = ssnal.evaluate(model, feats, targ)
+        out.append({"task": task, "A": feats, "t": targ, "C": C, "eps": eps, "tol": tol,
+                    "dual_x": model.dual_x, "bias": model.bias,
+                    "support_indices": model.support_indices,
+                    "support_coef": model.support_coef,
+                    "decision": ssnal.decision_function(model, pts), "points": pts,
+                    "metric": list(metric.values())[0]})
+    # no free dual: the bias is the midpoint of the bound-active interval
+    n = 40
+    a_b = rng.standard_normal((n, 3))
+    y_b = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+    x_b = np.where(rng.random(n) < 0.5, 0.0, 1.0)
+    cfg = ssnal.SvmConfig(task="classification", C=1.0)
+    out.append({"task": "classification", "A": a_b, "t": y_b, "C": 1.0, "eps": 0.0,
+                "tol": 0.0, "dual_x": x_b, "bias": ssnal.recover_bias(x_b, a_b, y_b, cfg),
+                "support_indices": np.flatnonzero(x_b), "support_coef": x_b[x_b > 0],
+                "decision": np.zeros(1), "points": a_b[:1], "metric": 0.0})
+    t_b = a_b @ np.ones(3)
+    xz = np.where(rng.random(2 * n) < 0.5, 0.0, 0.5)
+    cfg = ssnal.SvmConfig(task="regression", C=0.5, epsilon=0.2)
+    out.append({"task": "regression", "A": a_b, "t": t_b, "C": 0.5, "eps": 0.2, "tol": 0.0,
+                "dual_x": xz, "bias": ssnal.recover_bias(xz, a_b, t_b, cfg),
+                "support_indices": np.zeros(0, np.int64), "support_coef": np.zeros(0),
+                "decision": np.zeros(1), "points": a_b[:1], "metric": 0.0})
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--svm-only" in sys.argv:
+        np.savez_compressed(os.path.join(OUT, "svm.npz"), **pack("v", svm_cases()))
+        print("wrote svm.npz")
+        return
     np.savez_compressed(os.path.join(OUT, "projection.npz"), **pack("p", projection_cases()))
     np.savez_compressed(os.path.join(OUT, "hs_jacobian.npz"), **pack("h", hs_cases()))
     np.savez_compressed(os.path.join(OUT, "newton.npz"), **pack("n", newton_cases()))
     np.savez_compressed(os.path.join(OUT, "kkt.npz"), **pack("k", kkt_cases()))
     np.savez_compressed(os.path.join(OUT, "solve.npz"), **pack("s", solve_cases()))
+    np.savez_compressed(os.path.join(OUT, "svm.npz"), **pack("v", svm_cases()))
     print("wrote", sorted(os.listdir(OUT)))
 
 
