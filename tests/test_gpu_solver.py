@@ -225,3 +225,21 @@ def test_delta_line_search_matches_stable_on_config1_shape(pkg):
     assert a.converged and b.converged
     assert (a.outer_iters, a.total_inner_iters) == (b.outer_iters, b.total_inner_iters)
     assert b.objective == pytest.approx(a.objective, rel=1e-10)
+
+
+def test_dense_q_above_accept_q_limit_uses_full_gradient_path(pkg):
+    """q = 2300 > 2048 (the factor-space accept kernel's limit) with a small free set
+    (p < q: the p x p Woodbury system): the driver runs the full-gradient path and matches
+    the oracle -- it used to fail at the first accepted step."""
+    rng = np.random.default_rng(23)
+    n, q = 3000, 2300
+    A = rng.standard_normal((n, q)) / np.sqrt(q)
+    y = np.sign(A @ rng.standard_normal(q) + 0.05 * rng.standard_normal(n))
+    y[y == 0] = 1.0
+    pb = pkg.build_csvc_dual(A, y, pkg.SvmConfig(C=1.0))
+    rep = pkg.alm_solve(pb, pkg.AlmOptions(tol_kkt=1e-6))
+    assert rep.converged and rep.kkt_residual <= 1e-6
+    op, c, bl = O.csvc_problem(A, y, 1.0)
+    ref = _oracle_solve("delta", op, c, bl)
+    assert ref["converged"]
+    assert rep.objective == pytest.approx(ref["objective"], rel=1e-6)
