@@ -470,15 +470,14 @@ static constexpr size_t GSTAGE = (size_t)GK * GLD;  // doubles per operand per s
 static constexpr size_t GSMEM = 4 * GSTAGE * sizeof(double) + 2 * GK * sizeof(double);
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
 
 __device__ __forceinline__ void cp_async16(double* dst, const double* src, int src_bytes) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes)
-               : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes));
 }
 
 struct GramArgs {
@@ -503,6 +502,32 @@ struct GramArgs {
   const GramCtl* ctl;
   const int32_t* Jd;
 };
+
+// one staged block of GK rows: 8 k-steps x (8 A + 4 B fragments, 32 DMMAs) per warp
+template <bool SIGNED>
+__device__ __forceinline__ void gram_kstage(double (&acc)[8][4][2], const double* __restrict__ cA,
+                                            const double* __restrict__ cB,
+                                            const double* __restrict__ sgn, int lane, int wm,
+                                            int wn) {
+#pragma unroll
+  for (int kk = 0; kk < GK; kk += 4) {
+    const int kr = kk + (lane & 3);
+    double af[8], bf[4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) af[a] = cA[kr * GLD + wm * 64 + a * 8 + (lane >> 2)];
+    if (SIGNED) {
+      const double sg = sgn[kr];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) af[a] *= sg;
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bf[b] = cB[kr * GLD + wn * 32 + b * 8 + (lane >> 2)];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+  }
+}
 
 // grid.x = tile pair index (ti <= tj), grid.y = split
 __global__ void __launch_bounds__(GNT, 1) gram_kernel(GramArgs g) {
@@ -539,22 +564,35 @@ __global__ void __launch_bounds__(GNT, 1) gram_kernel(GramArgs g) {
     double* dB = sB + s * GSTAGE;
     const int nsides = diag ? 1 : 2;
     if (g.aligned) {
-      // 64 16-byte chunks per 128-column slice; GK rows x sides
-      for (int idx = tid; idx < GK * 64 * nsides; idx += GNT) {
-        const int side = idx / (GK * 64), rem = idx % (GK * 64);
-        const int kr = rem / 64, ch = rem % 64;
-        const long long r = kb + kr;
-        const long long c0 = (side ? cj : ci) + 2 * ch;
-        double* dst = (side ? dB : dA) + kr * GLD + 2 * ch;
-        int bytes = 0;
-        const double* src = g.A;
-        if (r < k1 && c0 < g.q) {
+      // 64 16-byte chunks per 128-column slice: thread tid copies chunk (tid & 63) of rows
+      // (tid >> 6) + 4i, i < 8, on both sides.  The 8 row indices are loaded up front (one
+      // J round trip per stage; the cp.async asm is a compiler barrier, so per-chunk J
+      // loads serialised behind it cost one L2 round trip each)
+      static_assert(GK == 32 && GNT == 256, "staging map assumes 32 rows x 256 threads");
+      const int ch = tid & 63, kr0 = tid >> 6;
+      long long rowoff[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const long long r = kb + kr0 + 4 * i;
+        long long off = -1;
+        if (r < k1) {
           const long long li = Jl[r];
-          const long long pr = li >= g.n ? li - g.n : li;  // SVR block: x x^T is sign-free
-          src = g.A + pr * g.lda + c0;
-          bytes = c0 + 1 < g.q ? 16 : 8;
+          off = (li >= g.n ? li - g.n : li) * g.lda;  // SVR block: x x^T is sign-free
         }
-        cp_async16(dst, src, bytes);
+        rowoff[i] = off;
+      }
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        if (side == 1 && diag) break;
+        const long long c0 = (side ? cj : ci) + 2 * ch;
+        const int bytes_full = c0 < g.q ? (c0 + 1 < g.q ? 16 : 8) : 0;
+        double* dbase = (side ? dB : dA) + 2 * ch;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int kr = kr0 + 4 * i;
+          const bool ok = rowoff[i] >= 0 && bytes_full > 0;
+          cp_async16(dbase + kr * GLD, ok ? g.A + rowoff[i] + c0 : g.A, ok ? bytes_full : 0);
+        }
       }
     } else {
       for (int idx = tid; idx < GK * GT * nsides; idx += GNT) {
@@ -604,19 +642,11 @@ __global__ void __launch_bounds__(GNT, 1) gram_kernel(GramArgs g) {
       const int nk = (int)min((long long)GK, k1 - kb);
       for (int kr = 0; kr < nk; ++kr) m1acc = fma(sw[buf * GK + kr], cA[kr * GLD + tid], m1acc);
     }
-#pragma unroll
-    for (int kk = 0; kk < GK; kk += 4) {
-      const int kr = kk + (lane & 3);
-      const double sg = signed_rows ? ssg[buf][kr] : 1.0;
-      double af[8], bf[4];
-#pragma unroll
-      for (int a = 0; a < 8; ++a) af[a] = cA[kr * GLD + wm * 64 + a * 8 + (lane >> 2)] * sg;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = cB[kr * GLD + wn * 32 + b * 8 + (lane >> 2)];
-#pragma unroll
-      for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    // (block-uniform branch: the rebuild's k-loop carries no sign multiplies)
+    if (signed_rows) {
+      gram_kstage<true>(acc, cA, cB, ssg[buf], lane, wm, wn);
+    } else {
+      gram_kstage<false>(acc, cA, cB, ssg[buf], lane, wm, wn);
     }
     __syncthreads();  // buffer `buf` free for the stage after next
     buf ^= 1;

@@ -145,13 +145,25 @@ constexpr long long DENSE_QSYS_MAX = 4096;
 constexpr long long DENSE_PSYS_MAX = 4096;
 // forcing-term cap of the matrix-free CG route (see cg_direction)
 constexpr double SPARSE_CG_ETA = 1e-4;
+// study knobs (scripts/cg_study.py): SSNAL_CG_ETA_CAP overrides the cap, SSNAL_CG_BATCH
+// the iterations between true-residual checks
+static double cg_eta_cap() {
+  static const double v = std::getenv("SSNAL_CG_ETA_CAP") ? std::atof(std::getenv("SSNAL_CG_ETA_CAP"))
+                                                          : SPARSE_CG_ETA;
+  return v;
+}
 // max / mean column sum of squares above which the factor-space Jacobi PCG is used
 constexpr double HOT_COLUMN_SPREAD = 50.0;
 
 namespace {
 
 constexpr int TMAX = 8;  // batched Armijo trials per launch
-constexpr int CG_BATCH = 16;  // CG iterations between host checks of the device flag
+constexpr int CG_BATCH_DEFAULT = 16;  // CG iterations between host checks of the device flag
+static int cg_batch() {
+  static const int v = std::getenv("SSNAL_CG_BATCH") ? std::atoi(std::getenv("SSNAL_CG_BATCH"))
+                                                     : CG_BATCH_DEFAULT;
+  return v > 0 ? v : CG_BATCH_DEFAULT;
+}
 constexpr int NSCAL = 16;
 
 struct DriverError {
@@ -426,7 +438,7 @@ struct Driver {
     ck(launch_cg_jacobi(q, L.cg_d, L.cg_u, asa, sigma, L.cg_d, S));
     ck(launch_vec(4, q, -1.0, L.gr, nullptr, nullptr, L.cg_b, S));
     ck(launch_cg_init(q, L.cg_b, L.cg_y, L.cg_r, L.cg_pv, L.cg_d, g2_dev,
-                      std::min(O.eta, SPARSE_CG_ETA), O.tau, L.cgs, L.cg_part, S));
+                      std::min(O.eta, cg_eta_cap()), O.tau, L.cgs, L.cg_part, S));
     // v (q) -> out (q) = sigma-free part X_J^T P X_J v, via zq (p) and ys (n)
     auto gram_apply = [&](const double* v, double* out) {
       xd_dot(p, v);
@@ -434,7 +446,7 @@ struct Driver {
       ck(launch_cscj_xt(op, L.cj, L.cg_w, out, L.csc_part, S));
     };
     for (int it = 0; it < max_it;) {
-      for (int b = 0; b < CG_BATCH && it < max_it; ++b, ++it) {
+      for (int b = 0; b < cg_batch() && it < max_it; ++b, ++it) {
         gram_apply(L.cg_pv, L.tq);
         ck(launch_cg_ap(q, L.cg_pv, L.tq, L.tq, 0.0, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
         ck(launch_cg_step(q, L.cg_y, L.cg_r, L.cg_pv, L.cg_Ap, L.cg_d, L.cg_z, L.cgs, L.cg_part,
@@ -465,9 +477,9 @@ struct Driver {
     // eta capped at SPARSE_CG_ETA: the reference falls back to an exact solve when its CG
     // stalls; the matrix-free path instead solves tighter from the start
     ck(launch_cg_init(p, L.cg_b, L.cg_y, L.cg_r, L.cg_pv, nullptr, g2_dev,
-                      std::min(O.eta, SPARSE_CG_ETA), O.tau, L.cgs, L.cg_part, S));
+                      std::min(O.eta, cg_eta_cap()), O.tau, L.cgs, L.cg_part, S));
     for (int it = 0; it < max_it;) {
-      for (int b = 0; b < CG_BATCH && it < max_it; ++b, ++it) {
+      for (int b = 0; b < cg_batch() && it < max_it; ++b, ++it) {
         ck(launch_cscj_xt(op, L.cj, L.cg_pv, L.tq, L.csc_part, S));
         xd_dot(p, L.tq);
         ck(launch_cg_ap(p, L.cg_pv, L.cg_zq, L.cg_aJ, asa, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
@@ -625,8 +637,9 @@ struct Driver {
 
   void project(const double* A, ProjState* st, int T, const double* B, const double* coefs,
                double* xo, uint8_t* fo, const double* ref, double hint, int newton_passes = 3,
-               int passes = 0, int phases = 4) {
+               int passes = 0, int phases = 4, const double* hints = nullptr) {
     ProjLaunch pl;
+    pl.hints = hints;
     pl.A = A; pl.B = B; pl.coef = coefs; pl.a = P.a; pl.l = P.l; pl.u = P.u;
     pl.lc = P.l_const; pl.uc = P.u_const; pl.d = P.d; pl.n = P.n; pl.T = T;
     pl.st = st; pl.part = (double*)L.ws_proj; pl.x_out = xo; pl.free_out = fo; pl.ref = ref;
@@ -939,6 +952,8 @@ struct Driver {
     if (gd >= 0.0) return false;
     double alpha = 1.0;
     int tried = 0;
+    bool have_last = false;
+    double lam_last = 0.0, alpha_last = 1.0;
     while (tried < 61) {
       const int T = (tried == 0 && first) ? first_T
                     : tried == 0 ? 1
@@ -954,9 +969,23 @@ struct Driver {
       if (tried == 0 && first) {
         for (int k = 0; k < T; ++k) H->st[k] = first[k];
       } else {
-        project(L.u, L.st_trial, T, L.qdir, coefs, L.tx, L.tfree, L.x, lam_cur);
+        // warm starts along the ray: lambda(alpha) interpolated linearly between the base
+        // point (alpha = 0, lam_cur) and the smallest step length already projected
+        double hints[TMAX];
+        const double* hp = nullptr;
+        if (tried > 0 && have_last) {
+          for (int k = 0; k < T; ++k)
+            hints[k] = lam_cur + (lam_last - lam_cur) * (alphas[k] / alpha_last);
+          hp = hints;
+        }
+        project(L.u, L.st_trial, T, L.qdir, coefs, L.tx, L.tfree, L.x, lam_cur, 3, 0, 4, hp);
         fetch(L.st_trial, T, false);
         finish(L.st_trial, T, L.u, L.qdir, coefs, L.tx, L.tfree, L.x);
+      }
+      if (T > 0 && H->st[T - 1].status == PROJ_APPLIED) {
+        have_last = true;
+        lam_last = H->st[T - 1].lam;
+        alpha_last = alphas[T - 1];
       }
       for (int k = 0; k < T; ++k) {
         const double a = alphas[k];

@@ -38,6 +38,8 @@ struct ProjArgs {
   const double* A;
   const double* B;
   double coef[SSNAL_MAX_TRIALS];
+  double hints[SSNAL_MAX_TRIALS];  // per-trial warm starts (multi-trial kernel), has_hints
+  int has_hints;
   const double* a;
   const double* l;
   const double* u;
@@ -907,12 +909,46 @@ static constexpr int PM_MAX_PASSES = 16;
 static constexpr int PM_UNROLL = 4;
 static constexpr int PM_INACTIVE = 99;
 
+// scripts/proj_probe.cu: per-phase globaltimer stamps of block 0 thread 0
+#ifdef SSNAL_PROJ_TIMING
+__device__ unsigned long long g_proj_marks[64];
+__device__ int g_proj_nmarks;
+#define PROJ_MARK()                                                      \
+  do {                                                                   \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                           \
+      unsigned long long t_;                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));              \
+      const int k_ = g_proj_nmarks;                                      \
+      if (k_ < 64) g_proj_marks[k_] = t_;                                \
+      g_proj_nmarks = k_ + 1;                                            \
+    }                                                                    \
+  } while (0)
+#else
+#define PROJ_MARK() \
+  do {              \
+  } while (0)
+#endif
+
+__device__ __forceinline__ void pm_load(const ProjArgs& p, long long i0, long long stride,
+                                        double (&uu)[PM_UNROLL], double (&bb)[PM_UNROLL],
+                                        double (&aa)[PM_UNROLL]) {
+#pragma unroll
+  for (int k = 0; k < PM_UNROLL; ++k) {
+    const long long i = i0 + k * stride;
+    const bool in = i < p.n;
+    uu[k] = in ? __ldg(p.A + i) : 0.0;
+    bb[k] = (in && p.B) ? __ldg(p.B + i) : 0.0;
+    aa[k] = in ? __ldg(p.a + i) : 0.0;
+  }
+}
+
 template <int T>
-__global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hint,
+__global__ void __launch_bounds__(PM_NT, 2) proj_multi_kernel(ProjArgs p, double hint,
                                                            int max_newton, int nt, int write_x) {
   cg::grid_group grid = cg::this_grid();
   constexpr int G = PM_WARPS / T;  // warps per trial group
   __shared__ double wred[PM_WARPS][8];
+  __shared__ double wfold[PM_WARPS][8];
   __shared__ double s_c[T], s_lo[T], s_hi[T], s_lam[T], s_tmin[T], s_tmax[T], s_coef[T];
   __shared__ int s_status[T], s_passes[T];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -921,6 +957,9 @@ __global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hi
   const long long region = (long long)T * nb * PSTRIDE;
   if (threadIdx.x < T) {
     s_c[threadIdx.x] = hint;
+#pragma unroll
+    for (int k = 0; k < T; ++k)  // static indices (see s_coef)
+      if (p.has_hints && (int)threadIdx.x == k) s_c[k] = p.hints[k];
     s_lo[threadIdx.x] = -INFINITY;
     s_hi[threadIdx.x] = INFINITY;
     s_lam[threadIdx.x] = 0.0;
@@ -933,6 +972,7 @@ __global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hi
       if ((int)threadIdx.x == k) s_coef[k] = p.coef[k];
   }
   __syncthreads();
+  PROJ_MARK();
   const double coef = s_coef[t];
   const long long stride = (long long)nb * G * 32;
   const long long start = ((long long)blockIdx.x * G + g) * 32 + lane;
@@ -942,16 +982,13 @@ __global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hi
     const double c = s_c[t];
     double vals[8] = {0.0, 0.0, 0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0.0};
     if (status == PROJ_NEWTON) {
+      // software-pipelined: the loads of chunk k+1 are in flight while chunk k computes
+      // (the pass was load-latency bound at 16 warps per SM)
+      double uu[PM_UNROLL], bb[PM_UNROLL], aa[PM_UNROLL];
+      pm_load(p, start, stride, uu, bb, aa);
       for (long long i0 = start; i0 < p.n; i0 += PM_UNROLL * stride) {
-        double uu[PM_UNROLL], bb[PM_UNROLL], aa[PM_UNROLL];
-#pragma unroll
-        for (int k = 0; k < PM_UNROLL; ++k) {  // every load of the chunk in flight first
-          const long long i = i0 + k * stride;
-          const bool in = i < p.n;
-          uu[k] = in ? __ldg(p.A + i) : 0.0;
-          bb[k] = (in && p.B) ? __ldg(p.B + i) : 0.0;
-          aa[k] = in ? __ldg(p.a + i) : 0.0;
-        }
+        double nu[PM_UNROLL], nbv[PM_UNROLL], na[PM_UNROLL];
+        pm_load(p, i0 + PM_UNROLL * stride, stride, nu, nbv, na);
 #pragma unroll
         for (int k = 0; k < PM_UNROLL; ++k) {
           const long long i = i0 + k * stride;
@@ -973,6 +1010,12 @@ __global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hi
             vals[7] += 1.0;
           }
         }
+#pragma unroll
+        for (int k = 0; k < PM_UNROLL; ++k) {
+          uu[k] = nu[k];
+          bb[k] = nbv[k];
+          aa[k] = na[k];
+        }
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -981,6 +1024,7 @@ __global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hi
       }
     }
     __syncthreads();
+    PROJ_MARK();
     double* part = p.part + (pass & 1) * region;
     if (status == PROJ_NEWTON && g == 0 && lane < 8) {  // the trial's G warps, in order
       const int op = (lane == 3 || lane == 5) ? 1 : ((lane == 4 || lane == 6) ? 2 : 0);  // ops[lane]
@@ -992,21 +1036,51 @@ __global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hi
       part[((long long)t * nb + blockIdx.x) * PSTRIDE + lane] = r;
     }
     grid.sync();
-    if (status == PROJ_NEWTON && g == 0) {
-      // lane folds blocks lane, lane + 32, ... (fixed order), then a fixed warp tree:
-      // every block gets bit-identical totals
-      double r[8] = {0.0, 0.0, 0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0.0};
+    PROJ_MARK();
+    double r[8] = {0.0, 0.0, 0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0.0};
+    if (status == PROJ_NEWTON) {
+      // the trial's G warps fold the block partials (warp g: blocks g*32 + lane +
+      // k*32G, two at a time with their loads in flight), fixed warp trees, then warp 0
+      // combines the G results in g order: every block gets bit-identical totals
       const double* base = part + (long long)t * nb * PSTRIDE;
-      for (unsigned b = lane; b < nb; b += 32) {
+      for (unsigned b = g * 32 + lane; b < nb; b += 64 * G) {
+        const unsigned b2 = b + 32 * G;
+        double x1[8], x2[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const double x = __ldcg(base + (long long)b * PSTRIDE + k);
-          r[k] = ops[k] == 0 ? r[k] + x : (ops[k] == 1 ? fmin(r[k], x) : fmax(r[k], x));
+          x1[k] = __ldcg(base + (long long)b * PSTRIDE + k);
+          x2[k] = b2 < nb ? __ldcg(base + (long long)b2 * PSTRIDE + k)
+                          : (ops[k] == 0 ? 0.0 : (ops[k] == 1 ? INFINITY : -INFINITY));
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          r[k] = ops[k] == 0 ? r[k] + x1[k] : (ops[k] == 1 ? fmin(r[k], x1[k]) : fmax(r[k], x1[k]));
+          r[k] = ops[k] == 0 ? r[k] + x2[k] : (ops[k] == 1 ? fmin(r[k], x2[k]) : fmax(r[k], x2[k]));
         }
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k)
         r[k] = ops[k] == 0 ? warp_sum(r[k]) : (ops[k] == 1 ? warp_min(r[k]) : warp_max(r[k]));
+      if (G > 1) {
+        __syncwarp();
+        if (lane == 0)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) wfold[warp][k] = r[k];
+      }
+    }
+    if (G > 1) __syncthreads();
+    if (status == PROJ_NEWTON && g == 0) {
+      if (G > 1 && lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          double v = wfold[t][k];
+          for (int gg = 1; gg < G; ++gg) {
+            const double x = wfold[gg * T + t][k];
+            v = ops[k] == 0 ? v + x : (ops[k] == 1 ? fmin(v, x) : fmax(v, x));
+          }
+          r[k] = v;
+        }
+      }
       if (lane == 0) {
         double cc = s_c[t], lo = s_lo[t], hi = s_hi[t], lam = s_lam[t], tmin = s_tmin[t];
         int stt = status;
@@ -1026,6 +1100,7 @@ __global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hi
       }
     }
     __syncthreads();
+    PROJ_MARK();
     bool any = false;
 #pragma unroll
     for (int k = 0; k < T; ++k) any |= s_status[k] == PROJ_NEWTON;
@@ -1039,9 +1114,12 @@ __global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hi
     double* xo = (write_x && p.x_out) ? p.x_out + (long long)t * p.n : nullptr;
     unsigned char* fo = (write_x && p.free_out) ? p.free_out + (long long)t * p.n : nullptr;
     const double lam_bar = 0.5 * (lam + p.base_lam);
+#pragma unroll 4
     for (long long i = start; i < p.n; i += stride) {
-      double v, a, l, u;
-      load_elem(p, t, i, v, a, l, u);
+      double v = __ldg(p.A + i);
+      if (p.B) v = __dsub_rn(v, __dmul_rn(coef, __ldg(p.B + i)));
+      const double a = __ldg(p.a + i);
+      const double l = p.l ? p.l[i] : p.lc, u = p.u ? p.u[i] : p.uc;
       const double y = __dsub_rn(v, __dmul_rn(lam, a));
       const double x = fmin(fmax(y, l), u);
       const bool lower = y <= __dadd_rn(l, __dmul_rn(1e-12, __dadd_rn(1.0, fabs(l))));
@@ -1063,6 +1141,7 @@ __global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hi
     }
   }
   __syncthreads();
+  PROJ_MARK();
   double* part = p.part + 2 * region;
   if (status == PROJ_DONE && g == 0 && lane < 6) {
     double r = wred[t][lane];
@@ -1070,6 +1149,7 @@ __global__ void __launch_bounds__(PM_NT) proj_multi_kernel(ProjArgs p, double hi
     part[((long long)t * nb + blockIdx.x) * PSTRIDE + lane] = r;
   }
   grid.sync();
+  PROJ_MARK();
   if (blockIdx.x != 0 || g != 0 || status == PM_INACTIVE) return;
   ProjState* st = p.st + t;
   if (status == PROJ_DONE) {
@@ -1238,6 +1318,8 @@ cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
   ProjArgs p;
   p.A = L.A; p.B = L.B;
   for (int t = 0; t < SSNAL_MAX_TRIALS; ++t) p.coef[t] = (L.coef && t < L.T) ? L.coef[t] : 0.0; p.a = L.a; p.l = L.l; p.u = L.u;
+  p.has_hints = L.hints != nullptr;
+  for (int t = 0; t < SSNAL_MAX_TRIALS; ++t) p.hints[t] = (L.hints && t < L.T) ? L.hints[t] : L.hint;
   p.lc = L.lc; p.uc = L.uc; p.d = L.d; p.n = L.n; p.st = L.st; p.part = L.part;
   p.x_out = L.x_out; p.free_out = L.free_out; p.ref = L.ref;
   p.base = L.base; p.base_lam = L.base_lam;

@@ -92,6 +92,7 @@ struct ProjLaunch {
   double hint;  // warm-start multiplier for the Newton passes
   int newton;   // Newton passes (0: start from the full breakpoint range instead)
   int defer = 0;  // batched trials may leave x / the mask unwritten (see proj_defers)
+  const double* hints = nullptr;  // per-trial warm starts (host array of T), else `hint`
 };
 
 int proj_blocks(long long n);

@@ -1,0 +1,13 @@
+#!/bin/bash
+mkdir -p gpurun_out
+T=${1:-it8}
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -DSSNAL_PROJ_TIMING -o /tmp/proj_probe scripts/proj_probe.cu && /tmp/proj_probe > gpurun_out/${T}_proj_probe.txt 2>&1
+timeout 600 python scripts/run_config.py 4 1 3 > gpurun_out/${T}_c4.json 2> gpurun_out/${T}_c4.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/${T}_c4_launches.csv python scripts/run_config.py 4 1 1 > gpurun_out/${T}_c4_ncu.log 2>&1
+python scripts/launch_summary.py gpurun_out/${T}_c4_launches.csv > gpurun_out/${T}_c4_launches.txt
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:stream_xd_kernel" --launch-skip 20 --launch-count 1 \
+  -o gpurun_out/${T}_c4_stream_xd -f python scripts/run_config.py 4 1 1 > gpurun_out/${T}_ncu_xd.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:gram_kernel" --launch-skip 0 --launch-count 1 \
+  -o gpurun_out/${T}_c4_gram -f python scripts/run_config.py 4 1 1 > gpurun_out/${T}_ncu_gram.log 2>&1

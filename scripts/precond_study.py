@@ -99,8 +99,9 @@ def pcg(apply_pre, name, max_it=20000):
 
 dj = 1.0 + sigma * np.maximum(colsq - m1 * m1 / asa, 0.0)
 pcg(lambda v: v / dj, "jacobi")
+pcg(lambda v: v, "none (identity)")
 order = np.argsort(-colsq)
-for k in (256, 1024, 4096):
+for k in (64, 256, 1024):
     H = np.sort(order[:k])
     XH = xj[:, H].toarray()
     GH = XH.T @ XH - np.outer(m1[H], m1[H]) / asa
@@ -115,4 +116,11 @@ for k in (256, 1024, 4096):
         out[rest] = v[rest] / dj[rest]
         return out
 
-    pcg(pre, f"hot-block-{k}")
+    def pre_id(v, H=H, cf=cf, rest=rest):
+        out = v.copy()
+        out[H] = scipy.linalg.cho_solve(cf, v[H])
+        return out
+
+    pcg(pre, f"hot-block-{k}+jac")
+    pcg(pre_id, f"hot-block-{k}+id")
+

@@ -237,9 +237,11 @@ def test_dense_q_above_accept_q_limit_uses_full_gradient_path(pkg):
     y = np.sign(A @ rng.standard_normal(q) + 0.05 * rng.standard_normal(n))
     y[y == 0] = 1.0
     pb = pkg.build_csvc_dual(A, y, pkg.SvmConfig(C=1.0))
-    rep = pkg.alm_solve(pb, pkg.AlmOptions(tol_kkt=1e-6))
+    # p x p systems up to q (the dense path has no CG; the reference would switch to CG
+    # above 2000 -- the oracle is given the same threshold)
+    rep = pkg.alm_solve(pb, pkg.AlmOptions(tol_kkt=1e-6), pkg.SsnOptions(direct_solve_threshold=q))
     assert rep.converged and rep.kkt_residual <= 1e-6
     op, c, bl = O.csvc_problem(A, y, 1.0)
-    ref = _oracle_solve("delta", op, c, bl)
+    ref = _oracle_solve("delta", op, c, bl, direct_solve_threshold=q)
     assert ref["converged"]
     assert rep.objective == pytest.approx(ref["objective"], rel=1e-6)
