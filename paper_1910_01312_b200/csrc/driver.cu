@@ -144,7 +144,9 @@ constexpr long long ACCEPT_Q_MAX = 2048;
 constexpr long long DENSE_QSYS_MAX = 4096;
 constexpr long long DENSE_PSYS_MAX = 4096;
 // forcing-term cap of the matrix-free CG route (see cg_direction)
-constexpr double SPARSE_CG_ETA = 1e-4;
+// (1e-4 in round 1; the reference's own eta = 1e-2 converges configs 2 and 3 at full size
+// -- 3.0 s / 113 s, objectives equal to the oracle's to 1e-12 -- so no cap below it)
+constexpr double SPARSE_CG_ETA = 1e-2;
 // study knobs (scripts/cg_study.py): SSNAL_CG_ETA_CAP overrides the cap, SSNAL_CG_BATCH
 // the iterations between true-residual checks
 static double cg_eta_cap() {
@@ -651,6 +653,12 @@ struct Driver {
     if (B && xo == L.tx) {  // a line-search batch: x / mask of the accepted trial only
       pl.defer = 1;
       trial_deferred = proj_defers(P.n, T);
+      if (qgrad() && slope_ok && !hints) {
+        // lambda(alpha) ~ lam_cur - sigma alpha a_J'(Qd)_J / a_J'a_J: the direction
+        // epilogue's fold (ws_grad + 128) and the base point's a_J'a_J
+        pl.slope_num = reinterpret_cast<const double*>(static_cast<const char*>(L.ws_grad) + 128);
+        pl.slope_den = &L.st_cur->sum_a2_free;
+      }
     }
     // algorithmic bytes: each streaming launch reads v (+B), a (+l, u vectors); apply
     // also writes x and the mask
@@ -792,8 +800,11 @@ struct Driver {
     ck(launch_vec(3, P.q, 0.0, L.xw, L.r, nullptr, L.xpi, S));
   }
 
+  bool slope_ok = false;  // ws_grad + 128 holds a_J'(Qd)_J of the current direction
+
   void direction(long long p, double asa, const double* g2_dev) {
     tdir = L.t;
+    slope_ok = false;
     if (p == 0) {  // Sigma = 0: d = -s, Qd = -grad (ref solver.py:221-222)
       if (qgrad()) {  // grad = X r (one sweep, ||grad||^2 folded); t = X^T d = -r
         timed(SSNAL_OP_XD, a_bytes() + 8.0 * (P.n + P.q), [&] {
@@ -862,6 +873,7 @@ struct Driver {
       });
     }
     if (qgrad()) {
+      slope_ok = true;
       // ONE sweep X [t, r]: Qd and this point's gradient (a_J'(Qd)_J and ||grad||^2
       // folded), then d = -s - sigma P(Qd) and {g'd, w'Qw, w'Qd, t't}
       // sweep: A + labels, [Qd ; grad] written, mask + a read for the a_J'(Qd)_J fold
@@ -906,6 +918,7 @@ struct Driver {
   const double* tdir = nullptr;  // X^T d of the current direction (factor-space update)
 
   void steepest(double out[4]) {
+    slope_ok = false;
     vec(4, -1.0, L.grad, nullptr, nullptr, L.dir);
     tdir = L.gr + P.q;
     xt({L.dir}, L.gr + P.q);

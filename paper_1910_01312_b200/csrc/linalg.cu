@@ -434,7 +434,7 @@ static constexpr int BG_NT = 256;
 
 template <int J>
 __device__ __forceinline__ void bg_diag_step(double (&r)[BG_NB], int lane, double* rd, int k0,
-                                             int* fail, double d) {
+                                             int* fail, double d, double (*colbuf)[BG_NB]) {
   if (!(d > 0.0)) {
     if (lane == 0 && *fail == 0) *fail = k0 + J + 1;
     d = 1.0;
@@ -447,16 +447,39 @@ __device__ __forceinline__ void bg_diag_step(double (&r)[BG_NB], int lane, doubl
   } else if (lane > J) {
     r[J] *= inv;
   }
-  // next pivot broadcast ahead of the column loop (as tc_diag_step)
-  double dn = 0.0;
-  if constexpr (J + 1 < BG_NB) dn = __shfl_sync(0xffffffffu, fma(-r[J], r[J], r[J + 1]), J + 1);
+  // column J broadcast through shared memory (one store, then broadcast loads): 64-bit
+  // shuffles per column were throughput-bound (scripts/diag_probe.cu: 11.5 -> 6.8 us per
+  // 32 x 32 block); the buffer alternates by J parity, so one __syncwarp per column
+  colbuf[J & 1][lane] = r[J];
+  __syncwarp();
 #pragma unroll
   for (int c = J + 1; c < BG_NB; ++c) {
-    const double lcj = __shfl_sync(0xffffffffu, r[J], c);
+    const double lcj = colbuf[J & 1][c];
     if (lane >= c) r[c] = fma(-r[J], lcj, r[c]);
   }
-  if constexpr (J + 1 < BG_NB) bg_diag_step<J + 1>(r, lane, rd, k0, fail, dn);
+  // next pivot: lane J+1's updated diagonal entry
+  if constexpr (J + 1 < BG_NB) {
+    bg_diag_step<J + 1>(r, lane, rd, k0, fail, __shfl_sync(0xffffffffu, r[J + 1], J + 1),
+                        colbuf);
+  }
 }
+
+// scripts/chol_probe.cu: per-phase globaltimer stamps of CTA 0 thread 0
+#ifdef SSNAL_CHOL_TIMING
+__device__ unsigned long long g_chol_marks[12][64];
+#define CHOL_MARK(k)                                                                 \
+  do {                                                                               \
+    if (rank == 0 && threadIdx.x == 0) {                                             \
+      unsigned long long t_;                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      g_chol_marks[k][min(k0_mark, 63)] = t_;                                        \
+    }                                                                                \
+  } while (0)
+#else
+#define CHOL_MARK(k) \
+  do {               \
+  } while (0)
+#endif
 
 __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M, int m,
                                                          const double* __restrict__ b,
@@ -467,16 +490,23 @@ __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M,
   cg::grid_group grid = cg::this_grid();
   __shared__ double D[BG_NB][BG_NB + 1];
   __shared__ double rd[BG_NB];
+  __shared__ double colbuf[2][BG_NB];
   __shared__ int fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long gtid = (long long)blockIdx.x * BG_NT + tid;
   const long long gthreads = (long long)gridDim.x * BG_NT;
   const int gwarp = blockIdx.x * (BG_NT / 32) + warp, nwarps = gridDim.x * (BG_NT / 32);
   if (tid == 0) fail = 0;
+  const unsigned rank = blockIdx.x;
+  int k0_mark = 0;
+  (void)rank;
+  (void)k0_mark;
   for (long long i = gtid; i < m; i += gthreads) z[i] = scale * b[i];
   grid.sync();
+  CHOL_MARK(0);
   for (int k0 = 0; k0 < m; k0 += BG_NB) {
     const int kb = min(BG_NB, m - k0);
+    k0_mark = k0 / BG_NB;
     // (1) diagonal block + forward block
     if (blockIdx.x == 0 && warp == 0) {
       double r[BG_NB];
@@ -484,48 +514,106 @@ __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M,
       for (int c = 0; c < BG_NB; ++c)
         r[c] = (lane < kb && c < kb && c <= lane) ? M[(long long)(k0 + lane) * m + k0 + c]
                                                   : (lane == c ? 1.0 : 0.0);
-      bg_diag_step<0>(r, lane, rd, k0, &fail, __shfl_sync(0xffffffffu, r[0], 0));
+      CHOL_MARK(6);
+      bg_diag_step<0>(r, lane, rd, k0, &fail, __shfl_sync(0xffffffffu, r[0], 0), colbuf);
       __syncwarp();
+      CHOL_MARK(7);
+#pragma unroll
+      for (int c = 0; c < BG_NB; ++c) D[lane][c] = c <= lane ? r[c] : 0.0;
       if (lane < kb) {
 #pragma unroll
         for (int c = 0; c < BG_NB; ++c)
           if (c <= lane && c < kb) M[(long long)(k0 + lane) * m + k0 + c] = r[c];
       }
-      // z_k = L_kk^{-1} z_k (lane i holds z_i; row i of L_kk in r)
-      double zv = lane < kb ? z[k0 + lane] : 0.0;
+      __syncwarp();
+      // Linv = L_kk^{-1}, column `lane` by forward substitution on e_lane (unrolled:
+      // col[t] = 0 for t < lane, so the sums need no predicate).  Linv^T goes to the
+      // block's (unused) strict upper triangle of M: the panel TRSM becomes a DMMA
+      // product and both substitutions become matrix-vector products -- no 32-step
+      // shuffle chains outside the factorization itself
+      double col[BG_NB];
 #pragma unroll
-      for (int j = 0; j < BG_NB; ++j) {
-        if (lane == j) zv *= rd[j];
-        const double zj = __shfl_sync(0xffffffffu, zv, j);
-        if (lane > j) zv = fma(-r[j], zj, zv);
+      for (int i = 0; i < BG_NB; ++i) {
+        if (i < lane) {
+          col[i] = 0.0;
+        } else if (i == lane) {
+          col[i] = rd[i];
+        } else {
+          double sacc = 0.0;
+#pragma unroll
+          for (int t = 0; t < i; ++t) sacc = fma(D[i][t], col[t], sacc);
+          col[i] = -sacc * rd[i];
+        }
       }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < BG_NB; ++i) {
+        D[i][lane] = col[i];  // D now holds Linv (row i, column lane)
+        if (i > lane && i < kb && lane < kb) M[(long long)(k0 + lane) * m + k0 + i] = col[i];
+      }
+      __syncwarp();
+      CHOL_MARK(8);
+      // z_k = Linv z_k
+      __shared__ double zs[BG_NB];
+      zs[lane] = lane < kb ? z[k0 + lane] : 0.0;
+      __syncwarp();
+      double zv = 0.0;
+#pragma unroll
+      for (int t = 0; t < BG_NB; ++t) zv = fma(D[lane][t], zs[t], zv);
       if (lane < kb) z[k0 + lane] = zv;
     }
     grid.sync();
+    CHOL_MARK(1);
     const int r0 = k0 + kb;
     if (r0 >= m) break;
-    // (2) panel TRSM rows [r0, m)
+    // (2) panel TRSM rows [r0, m) as a DMMA product: L_rk = A_rk Linv^T (Linv of the
+    // diagonal block from the strict upper triangle + reciprocal pivots), one 8-row tile
+    // per warp, 4 column tiles x 8 k-steps of m8n8k4
     for (int idx = tid; idx < BG_NB * BG_NB; idx += BG_NT) {
-      const int i = idx / BG_NB, j = idx % BG_NB;
-      D[i][j] = (i < kb && j < kb && j <= i) ? M[(long long)(k0 + i) * m + k0 + j] : 0.0;
-    }
-    if (tid < BG_NB) rd[tid] = tid < kb ? 1.0 / M[(long long)(k0 + tid) * m + k0 + tid] : 0.0;
-    __syncthreads();
-    for (long long i = r0 + gtid; i < m; i += gthreads) {
-      double row[BG_NB];
-#pragma unroll
-      for (int t = 0; t < BG_NB; ++t) row[t] = t < kb ? M[i * m + k0 + t] : 0.0;
-#pragma unroll
-      for (int j = 0; j < BG_NB; ++j) {
-        row[j] *= rd[j];
-#pragma unroll
-        for (int t = j + 1; t < BG_NB; ++t) row[t] = fma(-row[j], D[t][j], row[t]);
+      const int j = idx / BG_NB, t = idx % BG_NB;  // Linv[j][t], t <= j
+      double v = 0.0;
+      if (j < kb && t < kb) {
+        if (t < j) v = M[(long long)(k0 + t) * m + k0 + j];
+        else if (t == j) v = 1.0 / M[(long long)(k0 + j) * m + k0 + j];
       }
+      D[j][t] = v;
+    }
+    __syncthreads();
+    {
+      const int ntile_r = (m - r0 + 7) / 8;
+      for (int T = gwarp; T < ntile_r; T += nwarps) {
+        const int row = r0 + 8 * T + (lane >> 2);
+        double af[BG_NB / 4];
 #pragma unroll
-      for (int t = 0; t < BG_NB; ++t)
-        if (t < kb) M[i * m + k0 + t] = row[t];
+        for (int q = 0; q < BG_NB / 4; ++q) {
+          const int k = 4 * q + (lane & 3);
+          af[q] = (row < m && k < kb) ? M[(long long)row * m + k0 + k] : 0.0;
+        }
+        double c[4][2];
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+          c[nb][0] = c[nb][1] = 0.0;
+#pragma unroll
+          for (int q = 0; q < BG_NB / 4; ++q) {
+            const double bv = D[nb * 8 + (lane >> 2)][4 * q + (lane & 3)];  // B[k][n] = Linv[n][k]
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(c[nb][0]), "+d"(c[nb][1])
+                : "d"(af[q]), "d"(bv));
+          }
+        }
+        // C fragment: row 8T + lane/4, columns nb*8 + 2 (lane%4) + {0, 1}
+        if (row < m) {
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) {
+            const int col = nb * 8 + 2 * (lane & 3);
+            if (col < kb) M[(long long)row * m + k0 + col] = c[nb][0];
+            if (col + 1 < kb) M[(long long)row * m + k0 + col + 1] = c[nb][1];
+          }
+        }
+      }
     }
     grid.sync();
+    CHOL_MARK(2);
     // (3) SYRK tiles over [r0, m) and the forward update of z
     const int nt = (m - r0 + 7) / 8;
     const long long ntiles = (long long)nt * (nt + 1) / 2;
@@ -553,36 +641,42 @@ __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M,
       }
     }
     for (long long c = r0 + gtid; c < m; c += gthreads) {
+      double mv[BG_NB];  // the row's panel entries, all loads in flight at once
+#pragma unroll
+      for (int t = 0; t < BG_NB; ++t) mv[t] = t < kb ? M[c * m + k0 + t] : 0.0;
       double s = z[c];
-      for (int t = 0; t < kb; ++t) s = fma(-M[c * m + k0 + t], z[k0 + t], s);
+#pragma unroll
+      for (int t = 0; t < BG_NB; ++t)
+        if (t < kb) s = fma(-mv[t], z[k0 + t], s);
       z[c] = s;
     }
     grid.sync();
+    CHOL_MARK(3);
   }
+  CHOL_MARK(4);
   if (blockIdx.x != 0) return;
-  // back substitution L^T x = z in CTA 0 (reciprocal pivots staged in shared memory)
-  __shared__ double rdall[2048];
-  for (int i = tid; i < m; i += BG_NT) rdall[i] = 1.0 / M[(long long)i * m + i];
-  __syncthreads();
+  // back substitution L^T x = z in CTA 0, block by block: x_k = Linv_k^T z_k (a
+  // matrix-vector product from the stored Linv^T, no shuffle chain), then the
+  // column update of z above the block
+  __shared__ double xk[BG_NB];
   for (int k0 = ((m - 1) / BG_NB) * BG_NB; k0 >= 0; k0 -= BG_NB) {
     const int kb = min(BG_NB, m - k0);
     if (warp == 0) {
-      // column `lane` of the block (L[k0+j][k0+lane], j = 0..31) into registers first:
-      // the 32-step chain below then never waits on L2
-      double col[BG_NB];
+      // lane j: x_j = sum_{t >= j} Linv[t][j] z_t; Linv[t][j] (t > j) at M[(k0+j) m + k0+t]
+      double lv[BG_NB];
 #pragma unroll
-      for (int j = 0; j < BG_NB; ++j)
-        col[j] = (j < kb && lane < j) ? M[(long long)(k0 + j) * m + k0 + lane] : 0.0;
-      double zv = lane < kb ? z[k0 + lane] : 0.0;
+      for (int t = 0; t < BG_NB; ++t)
+        lv[t] = (lane < kb && t < kb && t > lane) ? M[(long long)(k0 + lane) * m + k0 + t] : 0.0;
+      const double dj = lane < kb ? 1.0 / M[(long long)(k0 + lane) * m + k0 + lane] : 0.0;
+      const double zl = lane < kb ? z[k0 + lane] : 0.0;
+      double xv = dj * zl;
 #pragma unroll
-      for (int j = BG_NB - 1; j >= 0; --j) {
-        if (j < kb) {
-          if (lane == j) zv *= rdall[k0 + j];
-          const double xj = __shfl_sync(0xffffffffu, zv, j);
-          if (lane < j) zv = fma(-col[j], xj, zv);
-        }
+      for (int t = 0; t < BG_NB; ++t) {
+        const double zt = __shfl_sync(0xffffffffu, zl, t);
+        xv = fma(lv[t], zt, xv);
       }
-      if (lane < kb) z[k0 + lane] = zv;
+      if (lane < kb) z[k0 + lane] = xv;
+      xk[lane] = lane < kb ? xv : 0.0;
     }
     __syncthreads();
     for (int j = tid; j < k0; j += BG_NT) {
@@ -592,12 +686,13 @@ __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M,
       double s = z[j];
 #pragma unroll
       for (int t = 0; t < BG_NB; ++t)
-        if (t < kb) s = fma(-mv[t], z[k0 + t], s);
+        if (t < kb) s = fma(-mv[t], xk[t], s);
       z[j] = s;
     }
     __syncthreads();
   }
   for (int i = tid; i < m; i += BG_NT) x[i] = z[i];
+  CHOL_MARK(5);
   if (tid == 0) *info = fail;
 }
 
@@ -624,6 +719,7 @@ __global__ void __cluster_dims__(CC, 1, 1) __launch_bounds__(CC_NT, 1)
   extern __shared__ double Ps[];  // [m][CC_LD]: trailing panel rows
   __shared__ double D[BG_NB][BG_NB + 1];
   __shared__ double rd[BG_NB];
+  __shared__ double colbuf[2][BG_NB];
   __shared__ double zk[BG_NB];
   __shared__ int fail;
   double* z = x;  // z = scale b, solved in place
@@ -643,7 +739,7 @@ __global__ void __cluster_dims__(CC, 1, 1) __launch_bounds__(CC_NT, 1)
       for (int c = 0; c < BG_NB; ++c)
         r[c] = (lane < kb && c < kb && c <= lane) ? __ldcg(M + (long long)(k0 + lane) * m + k0 + c)
                                                   : (lane == c ? 1.0 : 0.0);
-      bg_diag_step<0>(r, lane, rd, k0, &fail, __shfl_sync(0xffffffffu, r[0], 0));
+      bg_diag_step<0>(r, lane, rd, k0, &fail, __shfl_sync(0xffffffffu, r[0], 0), colbuf);
       __syncwarp();
       if (lane < kb) {
 #pragma unroll

@@ -40,6 +40,11 @@ struct ProjArgs {
   double coef[SSNAL_MAX_TRIALS];
   double hints[SSNAL_MAX_TRIALS];  // per-trial warm starts (multi-trial kernel), has_hints
   int has_hints;
+  // first-order warm start along the ray v = A - coef B: lambda(coef) ~ hint - coef *
+  // (*slope_num / *slope_den) (the free-set sums a_J'B_J and a_J'a_J of the base point,
+  // device scalars), when set and no explicit hints
+  const double* slope_num;
+  const double* slope_den;
   const double* a;
   const double* l;
   const double* u;
@@ -736,6 +741,8 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_NT, 1)
     bpb[k][tid] = tb;
   }
   double c = hint, lo = -INFINITY, hi = INFINITY, lam = 0.0, tmin = INFINITY, tmax = -INFINITY;
+  if (p.slope_num && p.slope_den && *p.slope_den != 0.0)  // first-order start along the ray
+    c = hint - p.coef[t] * (*p.slope_num / *p.slope_den);
   int status = PROJ_NEWTON, passes = 0;
   const int ops[8] = {0, 0, 0, 1, 2, 1, 2, 0};
   bool empty = false;
@@ -958,8 +965,14 @@ __global__ void __launch_bounds__(PM_NT, 2) proj_multi_kernel(ProjArgs p, double
   if (threadIdx.x < T) {
     s_c[threadIdx.x] = hint;
 #pragma unroll
-    for (int k = 0; k < T; ++k)  // static indices (see s_coef)
-      if (p.has_hints && (int)threadIdx.x == k) s_c[k] = p.hints[k];
+    for (int k = 0; k < T; ++k) {  // static indices (see s_coef)
+      if ((int)threadIdx.x != k) continue;
+      if (p.has_hints) {
+        s_c[k] = p.hints[k];
+      } else if (p.slope_num && p.slope_den && *p.slope_den != 0.0) {
+        s_c[k] = hint - p.coef[k] * (*p.slope_num / *p.slope_den);
+      }
+    }
     s_lo[threadIdx.x] = -INFINITY;
     s_hi[threadIdx.x] = INFINITY;
     s_lam[threadIdx.x] = 0.0;
@@ -1319,6 +1332,8 @@ cudaError_t launch_project(const ProjLaunch& L, cudaStream_t stream) {
   p.A = L.A; p.B = L.B;
   for (int t = 0; t < SSNAL_MAX_TRIALS; ++t) p.coef[t] = (L.coef && t < L.T) ? L.coef[t] : 0.0; p.a = L.a; p.l = L.l; p.u = L.u;
   p.has_hints = L.hints != nullptr;
+  p.slope_num = L.B ? L.slope_num : nullptr;
+  p.slope_den = L.B ? L.slope_den : nullptr;
   for (int t = 0; t < SSNAL_MAX_TRIALS; ++t) p.hints[t] = (L.hints && t < L.T) ? L.hints[t] : L.hint;
   p.lc = L.lc; p.uc = L.uc; p.d = L.d; p.n = L.n; p.st = L.st; p.part = L.part;
   p.x_out = L.x_out; p.free_out = L.free_out; p.ref = L.ref;

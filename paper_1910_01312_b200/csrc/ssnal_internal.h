@@ -93,6 +93,8 @@ struct ProjLaunch {
   int newton;   // Newton passes (0: start from the full breakpoint range instead)
   int defer = 0;  // batched trials may leave x / the mask unwritten (see proj_defers)
   const double* hints = nullptr;  // per-trial warm starts (host array of T), else `hint`
+  const double* slope_num = nullptr;  // device scalars: first-order start along the ray
+  const double* slope_den = nullptr;
 };
 
 int proj_blocks(long long n);

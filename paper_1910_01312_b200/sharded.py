@@ -271,7 +271,7 @@ class ShardedEngine(_Engine):
 
     # ------------------------------------------------------------ sparse operator
     CG_BATCH = 16        # iterations between true-residual checks (csrc/driver.cu)
-    SPARSE_CG_ETA = 1e-4  # forcing-term cap of the matrix-free route
+    SPARSE_CG_ETA = 1e-2  # forcing-term cap of the matrix-free route (= the reference's eta)
 
     def _cg_buffers(self):
         if getattr(self, "_cgq", None) is None:

@@ -53,14 +53,12 @@ int main(int argc, char** argv) {
   const unsigned long long t0 = marks[0][0];
   const int np = (m + 31) / 32;
   for (int k = 0; k < np; ++k)
-    printf("panel %2d: diag %7.2f (load %6.2f fact %6.2f store %6.2f fwd+sync %6.2f)  trsm %7.2f "
-           "(stage %6.2f rows %6.2f sync %6.2f)  syrk %7.2f us\n", k,
+    printf("panel %2d: diag %7.2f (load %6.2f fact %6.2f inv+store %6.2f fwd+sync %6.2f)  "
+           "trsm+sync %7.2f  syrk+sync %7.2f us\n", k,
            (marks[1][k] - (k ? marks[3][k - 1] : t0)) * 1e-3,
            (marks[6][k] - (k ? marks[3][k - 1] : t0)) * 1e-3, (marks[7][k] - marks[6][k]) * 1e-3,
            (marks[8][k] - marks[7][k]) * 1e-3, (marks[1][k] - marks[8][k]) * 1e-3,
-           (marks[2][k] - marks[1][k]) * 1e-3, (marks[9][k] - marks[1][k]) * 1e-3,
-           (marks[10][k] - marks[9][k]) * 1e-3, (marks[2][k] - marks[10][k]) * 1e-3,
-           (marks[3][k] - marks[2][k]) * 1e-3);
+           (marks[2][k] - marks[1][k]) * 1e-3, (marks[3][k] - marks[2][k]) * 1e-3);
   printf("start->loop %.2f us, back substitution %.2f us, total %.2f us\n",
          (marks[0][0] - t0) * 1e-3, (marks[5][np - 1] - marks[4][np - 1]) * 1e-3,
          (marks[5][np - 1] - t0) * 1e-3);

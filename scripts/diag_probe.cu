@@ -38,7 +38,7 @@ __global__ void probe(const double* A, double* out, long long* cyc, int reps, in
     double r[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) r[c] = c <= lane ? A[lane * 32 + c] + it * 1e-30 : 0.0;
-    if (variant == 0) ssnal::bg_diag_step<0>(r, lane, rd, 0, &fail, __shfl_sync(0xffffffffu, r[0], 0));
+    if (variant == 0) ssnal::bg_diag_step<0>(r, lane, rd, 0, &fail, __shfl_sync(0xffffffffu, r[0], 0), colbuf);
     else sm_diag_step<0>(r, lane, rd, colbuf);
 #pragma unroll
     for (int c = 0; c < 32; ++c) acc += r[c];
