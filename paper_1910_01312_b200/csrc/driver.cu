@@ -751,8 +751,16 @@ struct Driver {
 
   // ---------------------------------------------------------------- outer pieces
   // returns residual; p and objective through refs; refreshes Qw when w given
+  bool cold_zero = false;  // x = w = 0 (cold start, first outer iteration)
+
   double kkt_and_refresh(double* x, double* w, double* qw_out, long long& p, double& obj) {
-    if (w) {
+    if (w && cold_zero) {
+      // X^T [x, w] = 0 and Q x = Q w = 0: no sweep of A needed
+      ck(cudaMemsetAsync(L.gr, 0, sizeof(double) * 2 * P.q, S));
+      ck(cudaMemsetAsync(L.qx, 0, sizeof(double) * P.n, S));
+      ck(cudaMemsetAsync(qw_out, 0, sizeof(double) * P.n, S));
+      cold_zero = false;
+    } else if (w) {
       xt({x, w}, L.gr);
       xd(L.gr, L.qwx, 2);
       ck(cudaMemcpyAsync(L.qx, L.qwx, sizeof(double) * P.n, cudaMemcpyDeviceToDevice, S));
@@ -1174,6 +1182,7 @@ struct Driver {
     else ck(cudaMemsetAsync(L.x, 0, nb, S));
     if (w0) ck(cudaMemcpyAsync(L.w, w0, nb, cudaMemcpyDeviceToDevice, S));
     else ck(cudaMemsetAsync(L.w, 0, nb, S));
+    cold_zero = x0 == nullptr && w0 == nullptr;
     if (P.csr) ck(cudaMemsetAsync(L.cj.ticket, 0, sizeof(unsigned int), S));
     else {
       if (L.qpart) ck(cudaMemsetAsync(L.qpart, 0, 256, S));  // accept_q ticket

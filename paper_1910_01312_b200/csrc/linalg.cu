@@ -186,7 +186,7 @@ __device__ __forceinline__ void tc_dmma(double& c0, double& c1, double a, double
 // index a compile-time constant (no local-memory arrays)
 template <int J>
 __device__ __forceinline__ void tc_diag_step(double (&r)[TC_NB], int lane, int k0, double* rdg,
-                                             int* fail, double d) {
+                                             int* fail, double d, double (*colbuf)[TC_NB]) {
   if (!(d > 0.0)) {
     if (lane == 0 && *fail == 0) *fail = k0 + J + 1;
     d = 1.0;
@@ -199,27 +199,28 @@ __device__ __forceinline__ void tc_diag_step(double (&r)[TC_NB], int lane, int k
   } else if (lane > J) {
     r[J] *= inv;
   }
-  // next pivot first: lane J+1 updates its own diagonal from its own L[J+1][J] (the
-  // same fma the column loop below performs for c = J+1, so bit-identical) and
-  // broadcasts it before the loop's shuffles -- one shuffle off the serial chain
-  double dn = 0.0;
-  if constexpr (J + 1 < TC_NB) dn = __shfl_sync(0xffffffffu, fma(-r[J], r[J], r[J + 1]), J + 1);
+  // column J broadcast through shared memory (one store + broadcast loads; the 64-bit
+  // shuffles per column were throughput-bound, scripts/diag_probe.cu), buffer by parity
+  if (lane < TC_NB) colbuf[J & 1][lane] = r[J];
+  __syncwarp();
 #pragma unroll
   for (int c = J + 1; c < TC_NB; ++c) {
-    const double lcj = __shfl_sync(0xffffffffu, r[J], c);
+    const double lcj = colbuf[J & 1][c];
     if (lane >= c) r[c] = fma(-r[J], lcj, r[c]);
   }
-  if constexpr (J + 1 < TC_NB) tc_diag_step<J + 1>(r, lane, k0, rdg, fail, dn);
+  if constexpr (J + 1 < TC_NB)
+    tc_diag_step<J + 1>(r, lane, k0, rdg, fail, __shfl_sync(0xffffffffu, r[J + 1], J + 1), colbuf);
 }
 
 // factor the 16x16 diagonal block at (k0, k0) in place (warp-wide call)
 __device__ __forceinline__ void tc_factor_diag(double* S, int ld, int k0, int lane, double* rdg,
                                                int* fail) {
+  __shared__ double colbuf[2][TC_NB];
   double r[TC_NB];
 #pragma unroll
   for (int c = 0; c < TC_NB; ++c)
     r[c] = (lane < TC_NB && c <= lane) ? S[(k0 + lane) * ld + k0 + c] : 0.0;
-  tc_diag_step<0>(r, lane, k0, rdg, fail, __shfl_sync(0xffffffffu, r[0], 0));
+  tc_diag_step<0>(r, lane, k0, rdg, fail, __shfl_sync(0xffffffffu, r[0], 0), colbuf);
   if (lane < TC_NB) {
 #pragma unroll
     for (int c = 0; c < TC_NB; ++c)

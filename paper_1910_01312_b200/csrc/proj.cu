@@ -21,6 +21,7 @@
 //   exact  : direct sums at <= 4 candidate breakpoints -> lambda      (status 2)
 //   apply  : x = clip(v - lambda a), free mask, fused reductions
 #include <algorithm>
+#include <cstdlib>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -936,16 +937,64 @@ __device__ int g_proj_nmarks;
   } while (0)
 #endif
 
-__device__ __forceinline__ void pm_load(const ProjArgs& p, long long i0, long long stride,
-                                        double (&uu)[PM_UNROLL], double (&bb)[PM_UNROLL],
-                                        double (&aa)[PM_UNROLL]) {
+// one slot's Newton-pass terms at c (contrib, one-sided slopes, nearest breakpoints,
+// and on pass 0 the breakpoint range and count)
+__device__ __forceinline__ void pm_slot(double uu, double bb, double a, double l, double u,
+                                        double coef, bool hasB, double c, bool first,
+                                        double (&vals)[8]) {
+  if (a == 0.0) return;
+  const double v = hasB ? __dsub_rn(uu, __dmul_rn(coef, bb)) : uu;
+  const double t1 = bp_div(__dsub_rn(v, u), a), t2 = bp_div(__dsub_rn(v, l), a);
+  const double ta = fmin(t1, t2), tb = fmax(t1, t2);
+  vals[0] += contrib(v, a, l, u, c);
+  const double a2 = a * a;
+  if (ta <= c && c < tb) vals[1] += a2;
+  if (ta < c && c <= tb) vals[2] += a2;
+  if (ta > c) vals[3] = fmin(vals[3], ta); else if (ta < c) vals[4] = fmax(vals[4], ta);
+  if (tb > c) vals[3] = fmin(vals[3], tb); else if (tb < c) vals[4] = fmax(vals[4], tb);
+  if (first) {
+    vals[5] = fmin(vals[5], ta);
+    vals[6] = fmax(vals[6], tb);
+    vals[7] += 1.0;
+  }
+}
+
+// The Newton pass over this warp's slots: 32-bit indices, the argument pointers hoisted
+// into registers, constant bounds specialised (CB), full chunks of PM_UNROLL slots loaded
+// together without per-slot guards, a guarded tail.  (The generic loop spent most of
+// its issue slots on 64-bit index arithmetic, bounds predicates and reloads of kernel
+// parameters.)
+template <bool CB>
+__device__ __forceinline__ void pm_pass(const ProjArgs& p, double coef, double c, bool first,
+                                        int start, int stride, double (&vals)[8]) {
+  const double* __restrict__ A = p.A;
+  const double* __restrict__ B = p.B;
+  const double* __restrict__ av = p.a;
+  const double* __restrict__ lv = p.l;
+  const double* __restrict__ uv = p.u;
+  const double lc = p.lc, uc = p.uc;
+  const bool hasB = B != nullptr;
+  const int n = (int)p.n;
+  int i = start;
+  const int full_end = n - (PM_UNROLL - 1) * stride;
+  for (; i < full_end; i += PM_UNROLL * stride) {
+    double uu[PM_UNROLL], bb[PM_UNROLL], aa[PM_UNROLL], ll[PM_UNROLL], ul[PM_UNROLL];
 #pragma unroll
-  for (int k = 0; k < PM_UNROLL; ++k) {
-    const long long i = i0 + k * stride;
-    const bool in = i < p.n;
-    uu[k] = in ? __ldg(p.A + i) : 0.0;
-    bb[k] = (in && p.B) ? __ldg(p.B + i) : 0.0;
-    aa[k] = in ? __ldg(p.a + i) : 0.0;
+    for (int k = 0; k < PM_UNROLL; ++k) {
+      const int ik = i + k * stride;
+      uu[k] = __ldg(A + ik);
+      bb[k] = hasB ? __ldg(B + ik) : 0.0;
+      aa[k] = __ldg(av + ik);
+      ll[k] = CB ? lc : (lv ? __ldg(lv + ik) : lc);
+      ul[k] = CB ? uc : (uv ? __ldg(uv + ik) : uc);
+    }
+#pragma unroll
+    for (int k = 0; k < PM_UNROLL; ++k) pm_slot(uu[k], bb[k], aa[k], ll[k], ul[k], coef, hasB, c, first, vals);
+  }
+  for (; i < n; i += stride) {
+    const double uu = __ldg(A + i), bb = hasB ? __ldg(B + i) : 0.0, a = __ldg(av + i);
+    const double l = CB ? lc : (lv ? __ldg(lv + i) : lc), u = CB ? uc : (uv ? __ldg(uv + i) : uc);
+    pm_slot(uu, bb, a, l, u, coef, hasB, c, first, vals);
   }
 }
 
@@ -995,41 +1044,8 @@ __global__ void __launch_bounds__(PM_NT, 2) proj_multi_kernel(ProjArgs p, double
     const double c = s_c[t];
     double vals[8] = {0.0, 0.0, 0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0.0};
     if (status == PROJ_NEWTON) {
-      // software-pipelined: the loads of chunk k+1 are in flight while chunk k computes
-      // (the pass was load-latency bound at 16 warps per SM)
-      double uu[PM_UNROLL], bb[PM_UNROLL], aa[PM_UNROLL];
-      pm_load(p, start, stride, uu, bb, aa);
-      for (long long i0 = start; i0 < p.n; i0 += PM_UNROLL * stride) {
-        double nu[PM_UNROLL], nbv[PM_UNROLL], na[PM_UNROLL];
-        pm_load(p, i0 + PM_UNROLL * stride, stride, nu, nbv, na);
-#pragma unroll
-        for (int k = 0; k < PM_UNROLL; ++k) {
-          const long long i = i0 + k * stride;
-          if (i >= p.n || aa[k] == 0.0) continue;
-          const double v = p.B ? __dsub_rn(uu[k], __dmul_rn(coef, bb[k])) : uu[k];
-          const double a = aa[k];
-          const double l = p.l ? p.l[i] : p.lc, u = p.u ? p.u[i] : p.uc;
-          const double t1 = bp_div(__dsub_rn(v, u), a), t2 = bp_div(__dsub_rn(v, l), a);
-          const double ta = fmin(t1, t2), tb = fmax(t1, t2);
-          vals[0] += contrib(v, a, l, u, c);
-          const double a2 = a * a;
-          if (ta <= c && c < tb) vals[1] += a2;
-          if (ta < c && c <= tb) vals[2] += a2;
-          if (ta > c) vals[3] = fmin(vals[3], ta); else if (ta < c) vals[4] = fmax(vals[4], ta);
-          if (tb > c) vals[3] = fmin(vals[3], tb); else if (tb < c) vals[4] = fmax(vals[4], tb);
-          if (pass == 0) {
-            vals[5] = fmin(vals[5], ta);
-            vals[6] = fmax(vals[6], tb);
-            vals[7] += 1.0;
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < PM_UNROLL; ++k) {
-          uu[k] = nu[k];
-          bb[k] = nbv[k];
-          aa[k] = na[k];
-        }
-      }
+      if (p.l || p.u) pm_pass<false>(p, coef, c, pass == 0, (int)start, (int)stride, vals);
+      else pm_pass<true>(p, coef, c, pass == 0, (int)start, (int)stride, vals);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const double w = ops[k] == 0 ? warp_sum(vals[k]) : (ops[k] == 1 ? warp_min(vals[k]) : warp_max(vals[k]));
@@ -1127,11 +1143,17 @@ __global__ void __launch_bounds__(PM_NT, 2) proj_multi_kernel(ProjArgs p, double
     double* xo = (write_x && p.x_out) ? p.x_out + (long long)t * p.n : nullptr;
     unsigned char* fo = (write_x && p.free_out) ? p.free_out + (long long)t * p.n : nullptr;
     const double lam_bar = 0.5 * (lam + p.base_lam);
+    const double* __restrict__ A = p.A;
+    const double* __restrict__ B = p.B;
+    const double* __restrict__ av = p.a;
+    const double* __restrict__ base = p.base;
+    const double* __restrict__ ref = p.ref;
+    const int n = (int)p.n, istride = (int)stride;
 #pragma unroll 4
-    for (long long i = start; i < p.n; i += stride) {
-      double v = __ldg(p.A + i);
-      if (p.B) v = __dsub_rn(v, __dmul_rn(coef, __ldg(p.B + i)));
-      const double a = __ldg(p.a + i);
+    for (int i = (int)start; i < n; i += istride) {
+      double v = __ldg(A + i);
+      if (B) v = __dsub_rn(v, __dmul_rn(coef, __ldg(B + i)));
+      const double a = __ldg(av + i);
       const double l = p.l ? p.l[i] : p.lc, u = p.u ? p.u[i] : p.uc;
       const double y = __dsub_rn(v, __dmul_rn(lam, a));
       const double x = fmin(fmax(y, l), u);
@@ -1141,9 +1163,9 @@ __global__ void __launch_bounds__(PM_NT, 2) proj_multi_kernel(ProjArgs p, double
       if (xo) xo[i] = x;
       if (fo) fo[i] = fr ? 1 : 0;
       const double r = v - x;
-      s6[0] += p.base ? bregman_term(x, __ldg(p.base + i), v, a, lam_bar) : v * v;
+      s6[0] += base ? bregman_term(x, __ldg(base + i), v, a, lam_bar) : v * v;
       s6[1] += r * r;
-      if (p.ref) { const double dd = x - __ldg(p.ref + i); s6[2] += dd * dd; }
+      if (ref) { const double dd = x - __ldg(ref + i); s6[2] += dd * dd; }
       if (fr) { s6[3] += a * a; s6[4] += 1.0; }
       s6[5] += x * (2.0 * v - x);
     }
@@ -1238,7 +1260,7 @@ static bool cluster_ok(long long n, int T) {
 }
 
 static bool multi_ok(long long n, int T) {
-  return T >= 1 && T <= PM_WARPS && !cluster_ok(n, T);
+  return T >= 1 && T <= PM_WARPS && n < (1LL << 31) - (1LL << 24) && !cluster_ok(n, T);
 }
 
 // Line-search trials one cluster-projection launch runs in a single wave: a 16-CTA
@@ -1248,7 +1270,10 @@ int proj_wave_trials(long long n, bool first) {
   // multi-trial kernel: every trial costs a full set of per-slot FP64 work per pass (the
   // inputs are read once), and the unit step is accepted on most Newton steps -- the
   // speculative batch is (1, beta); a backtracking batch, 4 step lengths
-  if (multi_ok(n, 1)) return first ? 2 : 4;
+  if (multi_ok(n, 1)) {
+    static const int fb = std::getenv("SSNAL_FIRST_BATCH") ? std::atoi(std::getenv("SSNAL_FIRST_BATCH")) : 2;
+    return first ? std::max(1, std::min(fb, PM_WARPS)) : 4;
+  }
   if (!cluster_ok(n, 1)) return SSNAL_MAX_TRIALS;
   static DeviceCache cache;
   return per_device(cache, [](int) {
@@ -1303,6 +1328,7 @@ bool proj_defers(long long n, int T) { return T > 1 && multi_ok(n, T); }
 
 template <int T>
 static cudaError_t launch_multi(ProjArgs& p, const ProjLaunch& L, cudaStream_t stream) {
+  if (L.n >= (1LL << 31) - (1LL << 24)) return cudaErrorInvalidValue;  // 32-bit slot indices
   constexpr int G = PM_WARPS / T;
   long long nb = ceil_div(L.n, (long long)G * 32 * PM_UNROLL);
   nb = std::min<long long>(nb, std::min(multi_capacity<T>(), proj_blocks(L.n)));

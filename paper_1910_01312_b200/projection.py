@@ -31,33 +31,55 @@ class BoxLineSet:
         self.backend = backend or default_backend()
         a_h = np.ascontiguousarray(a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a,
                                    dtype=np.float64)
-        l_h = np.ascontiguousarray(l.detach().cpu().numpy() if isinstance(l, torch.Tensor) else l,
-                                   dtype=np.float64)
-        u_h = np.ascontiguousarray(u.detach().cpu().numpy() if isinstance(u, torch.Tensor) else u,
-                                   dtype=np.float64)
-        if a_h.ndim != 1 or a_h.shape != l_h.shape or a_h.shape != u_h.shape:
+        if a_h.ndim != 1:
             raise InputError("a, l, u must be one-dimensional vectors of equal length")
-        if not np.all(l_h < u_h):
-            raise InputError("box must satisfy l < u componentwise")
+        n = a_h.shape[0]
         d = float(d)
-        lo = float(np.sum(np.where(a_h > 0, a_h * l_h, a_h * u_h)))
-        hi = float(np.sum(np.where(a_h > 0, a_h * u_h, a_h * l_h)))
+        # l / u: vectors as in the reference, or scalars (a constant bound for every slot:
+        # the SVM builders pass l = 0, u = C and skip three passes over n-length arrays)
+        l_uniform, l_c, l_h = self._bound(l, n)
+        u_uniform, u_c, u_h = self._bound(u, n)
+        if l_uniform and u_uniform:
+            if not l_c < u_c:
+                raise InputError("box must satisfy l < u componentwise")
+            a_sum = float(a_h.sum())
+            a_abs = float(np.abs(a_h).sum())
+            pos, neg = 0.5 * (a_sum + a_abs), 0.5 * (a_sum - a_abs)  # sums of a_i > 0, a_i < 0
+            lo, hi = pos * l_c + neg * u_c, pos * u_c + neg * l_c
+        else:
+            l_v = l_h if l_h is not None else np.full(n, l_c)
+            u_v = u_h if u_h is not None else np.full(n, u_c)
+            if not np.all(l_v < u_v):
+                raise InputError("box must satisfy l < u componentwise")
+            lo = float(np.sum(np.where(a_h > 0, a_h * l_v, a_h * u_v)))
+            hi = float(np.sum(np.where(a_h > 0, a_h * u_v, a_h * l_v)))
         slack = 1e-12 * (1.0 + abs(d) + max(abs(lo), abs(hi)))
         if not (lo - slack <= d <= hi + slack):
             raise InfeasibleProblemError(
                 f"a'x = {d} unattainable over the box: range is [{lo}, {hi}]")
-        self.n = a_h.shape[0]
+        self.n = n
         self.d = d
         # a_device: the caller's device copy of the same values (e.g. the labels already
         # uploaded for the operator), saving a second upload
         self.a_dev = a_device if a_device is not None else as_device(a_h, self.backend)
-        l_uniform = bool(l_h.min() == l_h.max())
-        u_uniform = bool(u_h.min() == u_h.max())
-        self.l_const = float(l_h[0]) if l_uniform else 0.0
-        self.u_const = float(u_h[0]) if u_uniform else 0.0
+        self.l_const = l_c if l_uniform else 0.0
+        self.u_const = u_c if u_uniform else 0.0
         self.l_dev = None if l_uniform else as_device(l_h, self.backend)
         self.u_dev = None if u_uniform else as_device(u_h, self.backend)
         self._range_lo, self._range_hi = lo, hi
+
+    @staticmethod
+    def _bound(b, n):
+        """(uniform, constant, host vector or None) for a scalar or an n-vector bound."""
+        if np.isscalar(b) or (isinstance(b, np.ndarray) and b.ndim == 0):
+            return True, float(b), None
+        b_h = np.ascontiguousarray(b.detach().cpu().numpy() if isinstance(b, torch.Tensor) else b,
+                                   dtype=np.float64)
+        if b_h.shape != (n,):
+            raise InputError("a, l, u must be one-dimensional vectors of equal length")
+        if n and bool(np.all(b_h == b_h[0])):
+            return True, float(b_h[0]), None
+        return False, 0.0, b_h
 
     @property
     def a(self):
