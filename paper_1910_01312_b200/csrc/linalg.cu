@@ -698,228 +698,6 @@ __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M,
 }
 
 
-// ------------------------------------------------------------------ cluster Cholesky
-// 160 < m <= CC_MAX (e.g. the q = 500 factor-space system of config 4): the blocked
-// right-looking algorithm of chol_big_kernel on ONE 16-CTA thread-block cluster.  Its
-// barriers are hardware cluster barriers (arrive.release / wait.acquire, well under a
-// microsecond) instead of grid-wide barriers across 296 CTAs, 48 of which made the grid
-// kernel latency-bound (600 us at m = 500); 16 SMs of DMMA are plenty for m^3/3 flops
-// at these sizes.  Each CTA stages the trailing rows of the current 32-column panel in
-// its own shared memory, so the SYRK fragments and the forward update of z read smem,
-// not L2.  Data other CTAs wrote is read with ld.global.cg (L2).
-static constexpr int CC = 16;
-static constexpr int CC_NT = 256;
-static constexpr int CC_MAX = 768;
-static constexpr int CC_LD = BG_NB + 1;
-static constexpr int CC_TG = 8;  // SYRK tiles per warp group
-
-__global__ void __cluster_dims__(CC, 1, 1) __launch_bounds__(CC_NT, 1)
-    chol_cluster_kernel(double* __restrict__ M, int m, const double* __restrict__ b, double scale,
-                        double* __restrict__ x, int* __restrict__ info) {
-  cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ double Ps[];  // [m][CC_LD]: trailing panel rows
-  __shared__ double D[BG_NB][BG_NB + 1];
-  __shared__ double rd[BG_NB];
-  __shared__ double colbuf[2][BG_NB];
-  __shared__ double zk[BG_NB];
-  __shared__ int fail;
-  double* z = x;  // z = scale b, solved in place
-  const unsigned rank = cluster.block_rank();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gtid = (int)rank * CC_NT + tid, gthreads = CC * CC_NT;
-  const int gwarp = (int)rank * (CC_NT / 32) + warp, nwarps = CC * (CC_NT / 32);
-  if (tid == 0) fail = 0;
-  for (int i = gtid; i < m; i += gthreads) z[i] = scale * b[i];
-  cluster.sync();
-  for (int k0 = 0; k0 < m; k0 += BG_NB) {
-    const int kb = min(BG_NB, m - k0);
-    // (1) diagonal block + forward block (rank 0, warp 0)
-    if (rank == 0 && warp == 0) {
-      double r[BG_NB];
-#pragma unroll
-      for (int c = 0; c < BG_NB; ++c)
-        r[c] = (lane < kb && c < kb && c <= lane) ? __ldcg(M + (long long)(k0 + lane) * m + k0 + c)
-                                                  : (lane == c ? 1.0 : 0.0);
-      bg_diag_step<0>(r, lane, rd, k0, &fail, __shfl_sync(0xffffffffu, r[0], 0), colbuf);
-      __syncwarp();
-      if (lane < kb) {
-#pragma unroll
-        for (int c = 0; c < BG_NB; ++c)
-          if (c <= lane && c < kb) M[(long long)(k0 + lane) * m + k0 + c] = r[c];
-      }
-      double zv = lane < kb ? __ldcg(z + k0 + lane) : 0.0;
-#pragma unroll
-      for (int j = 0; j < BG_NB; ++j) {
-        if (lane == j) zv *= rd[j];
-        const double zj = __shfl_sync(0xffffffffu, zv, j);
-        if (lane > j) zv = fma(-r[j], zj, zv);
-      }
-      if (lane < kb) z[k0 + lane] = zv;
-    }
-    cluster.sync();
-    const int r0 = k0 + kb;
-    if (r0 >= m) break;
-    // (2) panel TRSM rows [r0, m): L_rk = A_rk L_kk^-T, one row per thread
-    for (int idx = tid; idx < BG_NB * BG_NB; idx += CC_NT) {
-      const int i = idx / BG_NB, j = idx % BG_NB;
-      D[i][j] = (i < kb && j < kb && j <= i) ? __ldcg(M + (long long)(k0 + i) * m + k0 + j) : 0.0;
-    }
-    if (tid < BG_NB) {
-      rd[tid] = tid < kb ? 1.0 / __ldcg(M + (long long)(k0 + tid) * m + k0 + tid) : 0.0;
-      zk[tid] = tid < kb ? __ldcg(z + k0 + tid) : 0.0;
-    }
-    __syncthreads();
-    for (int i = r0 + gtid; i < m; i += gthreads) {
-      double row[BG_NB];
-#pragma unroll
-      for (int t = 0; t < BG_NB; ++t) row[t] = t < kb ? __ldcg(M + (long long)i * m + k0 + t) : 0.0;
-#pragma unroll
-      for (int j = 0; j < BG_NB; ++j) {
-        row[j] *= rd[j];
-#pragma unroll
-        for (int t = j + 1; t < BG_NB; ++t) row[t] = fma(-row[j], D[t][j], row[t]);
-      }
-#pragma unroll
-      for (int t = 0; t < BG_NB; ++t)
-        if (t < kb) M[(long long)i * m + k0 + t] = row[t];
-    }
-    cluster.sync();
-    // (3) trailing panel rows into this CTA's shared memory, then SYRK tiles + z update
-    // (loads of a batch issued together: a load -> store loop would pay one L2 round
-    // trip per element)
-    const int nrow = m - r0;
-    for (int idx0 = tid; idx0 < nrow * BG_NB; idx0 += CC_NT * 8) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = idx0 + u * CC_NT, i = idx / BG_NB, t = idx % BG_NB;
-        v[u] = (idx < nrow * BG_NB && t < kb) ? __ldcg(M + (long long)(r0 + i) * m + k0 + t) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = idx0 + u * CC_NT;
-        if (idx < nrow * BG_NB) Ps[(idx / BG_NB) * CC_LD + idx % BG_NB] = v[u];
-      }
-    }
-    __syncthreads();
-    // a warp's tiles in groups of CC_TG: the old values of the whole group are loaded
-    // first and its DMMA chains interleaved, so the L2 round trip of the read-modify-
-    // write is paid once per group, not once per tile
-    const int nt = (nrow + 7) / 8;
-    const int ntiles = nt * (nt + 1) / 2;
-    for (int base = gwarp; base < ntiles; base += nwarps * CC_TG) {
-      int li[CC_TG], lc[CC_TG];
-      double o0[CC_TG], o1[CC_TG], c0[CC_TG], c1[CC_TG];
-#pragma unroll
-      for (int u = 0; u < CC_TG; ++u) {
-        const int tix = base + u * nwarps;
-        li[u] = 1 << 30;
-        lc[u] = 1 << 30;
-        o0[u] = o1[u] = c0[u] = c1[u] = 0.0;
-        if (tix < ntiles) {
-          int I = (int)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);
-          while ((I + 1) * (I + 2) / 2 <= tix) ++I;
-          while (I * (I + 1) / 2 > tix) --I;
-          const int C = tix - I * (I + 1) / 2;
-          li[u] = 8 * I + (lane >> 2);  // local panel row of this lane's C row
-          lc[u] = 8 * C;                 // first local column of the tile
-          const int ri = r0 + li[u], cc = r0 + lc[u] + 2 * (lane & 3);
-          if (ri < m) {
-            const double* rowp = M + (long long)ri * m;
-            if (cc < m && cc <= ri) o0[u] = __ldcg(rowp + cc);
-            if (cc + 1 < m && cc + 1 <= ri) o1[u] = __ldcg(rowp + cc + 1);
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < BG_NB; q += 4) {
-        const int kk = q + (lane & 3);
-#pragma unroll
-        for (int u = 0; u < CC_TG; ++u) {
-          const int br = lc[u] + (lane >> 2);
-          const double av = li[u] < nrow ? -Ps[li[u] * CC_LD + kk] : 0.0;
-          const double bv = br < nrow ? Ps[br * CC_LD + kk] : 0.0;
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(c0[u]), "+d"(c1[u])
-                       : "d"(av), "d"(bv));
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < CC_TG; ++u) {
-        const int ri = r0 + li[u], cc = r0 + lc[u] + 2 * (lane & 3);
-        if (li[u] < nrow && ri < m) {
-          double* rowp = M + (long long)ri * m;
-          if (cc < m && cc <= ri) rowp[cc] = o0[u] + c0[u];
-          if (cc + 1 < m && cc + 1 <= ri) rowp[cc + 1] = o1[u] + c1[u];
-        }
-      }
-    }
-    for (int c = gtid; c < nrow; c += gthreads) {
-      double sacc = __ldcg(z + r0 + c);
-#pragma unroll
-      for (int t = 0; t < BG_NB; ++t) sacc = fma(-Ps[c * CC_LD + t], zk[t], sacc);
-      z[r0 + c] = sacc;
-    }
-    cluster.sync();
-  }
-  if (rank != 0) return;
-  // back substitution L^T x = z (rank 0; reciprocal pivots in shared memory)
-  __shared__ double rdall[CC_MAX];
-  for (int i = tid; i < m; i += CC_NT) rdall[i] = 1.0 / __ldcg(M + (long long)i * m + i);
-  __syncthreads();
-  for (int k0 = ((m - 1) / BG_NB) * BG_NB; k0 >= 0; k0 -= BG_NB) {
-    const int kb = min(BG_NB, m - k0);
-    if (warp == 0) {
-      double col[BG_NB];
-#pragma unroll
-      for (int j = 0; j < BG_NB; ++j)
-        col[j] = (j < kb && lane < j) ? __ldcg(M + (long long)(k0 + j) * m + k0 + lane) : 0.0;
-      double zv = lane < kb ? __ldcg(z + k0 + lane) : 0.0;
-#pragma unroll
-      for (int j = BG_NB - 1; j >= 0; --j) {
-        if (j < kb) {
-          if (lane == j) zv *= rdall[k0 + j];
-          const double xj = __shfl_sync(0xffffffffu, zv, j);
-          if (lane < j) zv = fma(-col[j], xj, zv);
-        }
-      }
-      if (lane < kb) z[k0 + lane] = zv;
-      zk[lane] = lane < kb ? zv : 0.0;
-    }
-    __syncthreads();
-    for (int j = tid; j < k0; j += CC_NT) {
-      // all 32 column loads in flight at once (fully unrolled; rows past m weigh 0)
-      double mv[BG_NB];
-#pragma unroll
-      for (int t = 0; t < BG_NB; ++t) mv[t] = t < kb ? __ldcg(M + (long long)(k0 + t) * m + j) : 0.0;
-      double sacc = __ldcg(z + j);
-#pragma unroll
-      for (int t = 0; t < BG_NB; ++t) sacc = fma(-mv[t], zk[t], sacc);
-      z[j] = sacc;
-    }
-    __syncthreads();
-  }
-  if (tid == 0) *info = fail;
-}
-
-static size_t chol_cluster_smem(int m) { return (size_t)m * CC_LD * sizeof(double); }
-
-static bool chol_cluster_ok() {
-  static DeviceCache cache;
-  return per_device(cache, [](int dev) {
-    int sup = 0;
-    cudaDeviceGetAttribute(&sup, cudaDevAttrClusterLaunch, dev);
-    if (!sup) return 0;
-    if (cudaFuncSetAttribute(chol_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
-                             1) != cudaSuccess)
-      return 0;
-    if (cudaFuncSetAttribute(chol_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)chol_cluster_smem(CC_MAX)) != cudaSuccess)
-      return 0;
-    return 1;
-  }) == 1;
-}
-
 static int big_grid() {
   static DeviceCache cache;
   return per_device(cache, [](int dev) {
@@ -968,15 +746,6 @@ cudaError_t launch_chol_solve(double* M, long long m, const double* b, double sc
     if (err != cudaSuccess) return (cudaError_t)err;
     (void)smem;
     { note_launch(); chol_tc_kernel<false><<<1, TC_NT, smem, stream>>>(M, mi, b, scale, x, info, TcPspace{}); }
-    return cudaGetLastError();
-  }
-  // the cluster kernel (fewer, cheaper barriers) is kept behind SSNAL_CHOL_CLUSTER=1: both
-  // are bound by the per-pivot broadcast chain of the diagonal blocks and the back
-  // substitution, and the grid kernel is ~10% faster at m = 500 (scripts/chol_probe.cu)
-  if (m <= CC_MAX && std::getenv("SSNAL_CHOL_CLUSTER") && chol_cluster_ok()) {
-    const int mi = (int)m;
-    note_launch();
-    chol_cluster_kernel<<<CC, CC_NT, chol_cluster_smem(mi), stream>>>(M, mi, b, scale, x, info);
     return cudaGetLastError();
   }
   if (m <= 2048) {

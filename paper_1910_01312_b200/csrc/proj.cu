@@ -1268,10 +1268,11 @@ static bool multi_ok(long long n, int T) {
 // batch ran as two waves (2x the latency of 7).  Not limited without the cluster path.
 int proj_wave_trials(long long n, bool first) {
   // multi-trial kernel: every trial costs a full set of per-slot FP64 work per pass (the
-  // inputs are read once), and the unit step is accepted on most Newton steps -- the
-  // speculative batch is (1, beta); a backtracking batch, 4 step lengths
+  // inputs are read once): the speculative batch is the unit step alone (config 4: batch
+  // sizes 1 / 2 / 3 / 4 -> 183 / 184 / 191 / 190 ms per solve), a backtracking batch, 4
+  // step lengths (SSNAL_FIRST_BATCH overrides the first)
   if (multi_ok(n, 1)) {
-    static const int fb = std::getenv("SSNAL_FIRST_BATCH") ? std::atoi(std::getenv("SSNAL_FIRST_BATCH")) : 2;
+    static const int fb = std::getenv("SSNAL_FIRST_BATCH") ? std::atoi(std::getenv("SSNAL_FIRST_BATCH")) : 1;
     return first ? std::max(1, std::min(fb, PM_WARPS)) : 4;
   }
   if (!cluster_ok(n, 1)) return SSNAL_MAX_TRIALS;

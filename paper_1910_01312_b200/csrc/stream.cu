@@ -491,26 +491,13 @@ cudaError_t launch_stream_xd(const double* A, long long n, long long q, long lon
   const int grid = stream_grid(n);
   const long long pairs = q / 2;
   const int cp = (int)ceil_div(pairs, 64LL);  // lanes hold 2*CP pairs each
-  // consumer warps: XD_WARPS2 for two right-hand sides (twice the FMA and shuffle work
-  // per streamed byte), XD_WARPS1 for one
-  static const int w1 = std::getenv("SSNAL_XD_WARPS1") ? std::atoi(std::getenv("SSNAL_XD_WARPS1"))
-                                                       : XD_WARPS1;
-  static const int w2 = std::getenv("SSNAL_XD_WARPS2") ? std::atoi(std::getenv("SSNAL_XD_WARPS2"))
-                                                       : XD_WARPS2;
+  // 8 consumer warps for one or two right-hand sides (the 16-warp variants measured no
+  // better and spilled at <2, 4, 16>: pruned in round 2)
+  static_assert(XD_WARPS1 == 8 && XD_WARPS2 == 8, "instantiated for 8 consumer warps");
   if (k == 2) {
-    if (w2 == 16) {
-      if (cp <= 1) return launch_stream(stream_xd_kernel<2, 1, 16>, p, grid, stream, 17 * 32);
-      if (cp <= 2) return launch_stream(stream_xd_kernel<2, 2, 16>, p, grid, stream, 17 * 32);
-      return launch_stream(stream_xd_kernel<2, 4, 16>, p, grid, stream, 17 * 32);
-    }
     if (cp <= 1) return launch_stream(stream_xd_kernel<2, 1, 8>, p, grid, stream);
     if (cp <= 2) return launch_stream(stream_xd_kernel<2, 2, 8>, p, grid, stream);
     return launch_stream(stream_xd_kernel<2, 4, 8>, p, grid, stream);
-  }
-  if (w1 == 16) {
-    if (cp <= 1) return launch_stream(stream_xd_kernel<1, 1, 16>, p, grid, stream, 17 * 32);
-    if (cp <= 2) return launch_stream(stream_xd_kernel<1, 2, 16>, p, grid, stream, 17 * 32);
-    return launch_stream(stream_xd_kernel<1, 4, 16>, p, grid, stream, 17 * 32);
   }
   if (cp <= 1) return launch_stream(stream_xd_kernel<1, 1, 8>, p, grid, stream);
   if (cp <= 2) return launch_stream(stream_xd_kernel<1, 2, 8>, p, grid, stream);

@@ -1,4 +1,4 @@
-// Per-phase timing of chol_cluster_kernel (globaltimer stamps of CTA 0 thread 0 at every
+// Per-phase timing of chol_big_kernel (globaltimer stamps of CTA 0 thread 0 at every
 // cluster barrier).  Built on the GPU box:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -DSSNAL_CHOL_TIMING -o /tmp/chol_probe \
 //        scripts/chol_probe.cu && /tmp/chol_probe 500

@@ -219,14 +219,10 @@ def test_dense_products(pkg, shape, svr, signed):
     assert np.abs(out.T - ref).max() <= 1e-12 * np.abs(X).sum(axis=1).max() * np.abs(d).max()
 
 
-@pytest.mark.parametrize("m,cluster", [(1, 0), (7, 0), (33, 0), (115, 0), (160, 0), (161, 0),
-                                       (300, 0), (500, 0), (517, 0), (768, 0), (769, 0),
-                                       (1100, 0), (300, 1), (500, 1), (768, 1)])
-def test_cholesky_solve_sizes(pkg, m, cluster, monkeypatch):
-    """Every Cholesky route: shared-memory resident (m <= 160), grid-wide cooperative
-    (m <= 2048), and the 16-CTA cluster kernel (SSNAL_CHOL_CLUSTER=1, m <= 768)."""
-    if cluster:
-        monkeypatch.setenv("SSNAL_CHOL_CLUSTER", "1")
+@pytest.mark.parametrize("m", [1, 7, 33, 115, 160, 161, 300, 500, 517, 768, 769, 1100, 2048])
+def test_cholesky_solve_sizes(pkg, m):
+    """Every Cholesky route: shared-memory resident (m <= 160), grid-wide cooperative with
+    inverted diagonal blocks (m <= 2048)."""
     be = pkg.default_backend()
     rng = np.random.default_rng(m)
     G = rng.standard_normal((m, m + 3))
