@@ -558,29 +558,53 @@ __global__ void __launch_bounds__(GNT, 1) gram_kernel(GramArgs g) {
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   double m1acc = 0.0;
 
-  // stage rows [kb, kb + GK) into buffer s
-  auto stage = [&](long long kb, int s) {
+  // Staging, software-pipelined over THREE stages of row indices: the J entries (and
+  // the m1 weights / signs, which chain J -> a, sign_mask) of stage k+2 are loaded into
+  // registers while stage k computes; stage k+1's cp.async copies are issued from the
+  // registers loaded one iteration earlier.  (With the J loads at the head of each stage
+  // every stage began with a dependent L2 round trip: ncu showed the warps stalled on
+  // the sign extension of the loaded index.)
+  static_assert(GK == 32 && GNT == 256, "staging map assumes 32 rows x 256 threads");
+  const int ch = tid & 63, kr0 = tid >> 6;
+  struct Pre {
+    long long rowoff[8];
+    double w, sg;
+  };
+  auto pre = [&](long long kb, Pre& R) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const long long r = kb + kr0 + 4 * i;
+      long long off = -1;
+      if (r < k1) {
+        const long long li = Jl[r];
+        off = (li >= g.n ? li - g.n : li) * g.lda;  // SVR block: x x^T is sign-free
+      }
+      R.rowoff[i] = off;
+    }
+    R.w = 0.0;
+    R.sg = 1.0;
+    if (tid < GK) {
+      const long long r = kb + tid;
+      if (r < k1) {
+        const long long li = Jl[r];
+        const long long pr = li >= g.n ? li - g.n : li;
+        if (signed_rows && !smask[li]) R.sg = -1.0;  // a leaving row: -x x^T
+        if (diag) {  // m1 weight (gram_m1's order of operations)
+          double w = g.a[li];
+          if (g.rs) w *= g.rs[pr];
+          if (g.svr && li >= g.n) w = -w;
+          R.w = w * R.sg;
+        }
+      }
+    }
+  };
+  // stage rows [kb, kb + GK) into buffer s from prefetched row offsets
+  auto issue = [&](long long kb, int s, const Pre& R) {
     double* dA = sA + s * GSTAGE;
     double* dB = sB + s * GSTAGE;
-    const int nsides = diag ? 1 : 2;
     if (g.aligned) {
       // 64 16-byte chunks per 128-column slice: thread tid copies chunk (tid & 63) of rows
-      // (tid >> 6) + 4i, i < 8, on both sides.  The 8 row indices are loaded up front (one
-      // J round trip per stage; the cp.async asm is a compiler barrier, so per-chunk J
-      // loads serialised behind it cost one L2 round trip each)
-      static_assert(GK == 32 && GNT == 256, "staging map assumes 32 rows x 256 threads");
-      const int ch = tid & 63, kr0 = tid >> 6;
-      long long rowoff[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const long long r = kb + kr0 + 4 * i;
-        long long off = -1;
-        if (r < k1) {
-          const long long li = Jl[r];
-          off = (li >= g.n ? li - g.n : li) * g.lda;  // SVR block: x x^T is sign-free
-        }
-        rowoff[i] = off;
-      }
+      // (tid >> 6) + 4i, i < 8, on both sides
 #pragma unroll
       for (int side = 0; side < 2; ++side) {
         if (side == 1 && diag) break;
@@ -590,11 +614,12 @@ __global__ void __launch_bounds__(GNT, 1) gram_kernel(GramArgs g) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int kr = kr0 + 4 * i;
-          const bool ok = rowoff[i] >= 0 && bytes_full > 0;
-          cp_async16(dbase + kr * GLD, ok ? g.A + rowoff[i] + c0 : g.A, ok ? bytes_full : 0);
+          const bool ok = R.rowoff[i] >= 0 && bytes_full > 0;
+          cp_async16(dbase + kr * GLD, ok ? g.A + R.rowoff[i] + c0 : g.A, ok ? bytes_full : 0);
         }
       }
     } else {
+      const int nsides = diag ? 1 : 2;
       for (int idx = tid; idx < GK * GT * nsides; idx += GNT) {
         const int side = idx / (GK * GT), rem = idx % (GK * GT);
         const int kr = rem / GT, c = rem % GT;
@@ -610,30 +635,23 @@ __global__ void __launch_bounds__(GNT, 1) gram_kernel(GramArgs g) {
       }
     }
     if (tid < GK) {
-      const long long r = kb + tid;
-      double w = 0.0, sg = 1.0;
-      if (r < k1) {
-        const long long li = Jl[r];
-        const long long pr = li >= g.n ? li - g.n : li;
-        if (signed_rows && !smask[li]) sg = -1.0;  // a leaving row: -x x^T
-        if (diag) {  // m1 weight (gram_m1's order of operations)
-          w = g.a[li];
-          if (g.rs) w *= g.rs[pr];
-          if (g.svr && li >= g.n) w = -w;
-          w *= sg;
-        }
-      }
-      sw[s * GK + tid] = w;
-      ssg[s][tid] = sg;
+      sw[s * GK + tid] = R.w;
+      ssg[s][tid] = R.sg;
     }
   };
 
   int buf = 0;
-  if (k0 < k1) stage(k0, 0);
+  Pre R;
+  if (k0 < k1) {
+    pre(k0, R);
+    issue(k0, 0, R);
+  }
   asm volatile("cp.async.commit_group;" ::: "memory");
+  if (k0 + GK < k1) pre(k0 + GK, R);
   for (long long kb = k0; kb < k1; kb += GK) {
-    if (kb + GK < k1) stage(kb + GK, buf ^ 1);
+    if (kb + GK < k1) issue(kb + GK, buf ^ 1, R);
     asm volatile("cp.async.commit_group;" ::: "memory");
+    if (kb + 2 * GK < k1) pre(kb + 2 * GK, R);  // in flight during this stage's DMMAs
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncthreads();
     const double* cA = sA + buf * GSTAGE;

@@ -505,11 +505,12 @@ __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M,
   for (long long i = gtid; i < m; i += gthreads) z[i] = scale * b[i];
   grid.sync();
   CHOL_MARK(0);
-  for (int k0 = 0; k0 < m; k0 += BG_NB) {
-    const int kb = min(BG_NB, m - k0);
-    k0_mark = k0 / BG_NB;
-    // (1) diagonal block + forward block
-    if (blockIdx.x == 0 && warp == 0) {
+  // (1) diagonal block + forward block of panel k0 (CTA 0, warp 0): factor, inverse,
+  // z_k = Linv z_k.  Panel 0 runs before the loop; every later one as the look-ahead of
+  // the previous panel's update phase (it only needs that panel's update of its own
+  // block, done first by the same warp), so it overlaps the other warps' SYRK tiles
+  __shared__ double zs[BG_NB];
+  auto diag_phase = [&](int k0, int kb) {
       double r[BG_NB];
 #pragma unroll
       for (int c = 0; c < BG_NB; ++c)
@@ -555,15 +556,18 @@ __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M,
       __syncwarp();
       CHOL_MARK(8);
       // z_k = Linv z_k
-      __shared__ double zs[BG_NB];
       zs[lane] = lane < kb ? z[k0 + lane] : 0.0;
       __syncwarp();
       double zv = 0.0;
 #pragma unroll
       for (int t = 0; t < BG_NB; ++t) zv = fma(D[lane][t], zs[t], zv);
       if (lane < kb) z[k0 + lane] = zv;
-    }
-    grid.sync();
+      };
+  if (blockIdx.x == 0 && warp == 0) diag_phase(0, min(BG_NB, m));
+  grid.sync();
+  for (int k0 = 0; k0 < m; k0 += BG_NB) {
+    const int kb = min(BG_NB, m - k0);
+    k0_mark = k0 / BG_NB;
     CHOL_MARK(1);
     const int r0 = k0 + kb;
     if (r0 >= m) break;
@@ -615,41 +619,67 @@ __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M,
     }
     grid.sync();
     CHOL_MARK(2);
-    // (3) SYRK tiles over [r0, m) and the forward update of z
-    const int nt = (m - r0 + 7) / 8;
-    const long long ntiles = (long long)nt * (nt + 1) / 2;
-    for (long long tix = gwarp; tix < ntiles; tix += nwarps) {
-      // tile (I, C), C <= I, from the triangular index
-      int I = (int)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);
-      while ((long long)(I + 1) * (I + 2) / 2 <= tix) ++I;
-      while ((long long)I * (I + 1) / 2 > tix) --I;
-      const int C = (int)(tix - (long long)I * (I + 1) / 2);
-      const int ri = r0 + 8 * I + (lane >> 2), ci = r0 + 8 * C + (lane >> 2);
-      const int cc = r0 + 8 * C + 2 * (lane & 3);
-      double c0 = 0.0, c1 = 0.0;
+    // (3) SYRK tiles over [r0, m) and the forward update of z.  The next diagonal block
+    // (tile rows/columns I, C < 4) and its z rows belong to CTA 0's warp 0, which then
+    // factors that block right away (look-ahead); every other warp takes the rest.
+    {
+      const int kb2 = min(BG_NB, m - r0);
+      auto syrk_tile = [&](int I, int C) {
+        const int ri = r0 + 8 * I + (lane >> 2), ci = r0 + 8 * C + (lane >> 2);
+        const int cc = r0 + 8 * C + 2 * (lane & 3);
+        double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-      for (int q = 0; q < BG_NB; q += 4) {
-        const int kk = q + (lane & 3);
-        const double av = (ri < m && kk < kb) ? -M[(long long)ri * m + k0 + kk] : 0.0;
-        const double bv = (ci < m && kk < kb) ? M[(long long)ci * m + k0 + kk] : 0.0;
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                     : "+d"(c0), "+d"(c1)
-                     : "d"(av), "d"(bv));
+        for (int q = 0; q < BG_NB; q += 4) {
+          const int kk = q + (lane & 3);
+          const double av = (ri < m && kk < kb) ? -M[(long long)ri * m + k0 + kk] : 0.0;
+          const double bv = (ci < m && kk < kb) ? M[(long long)ci * m + k0 + kk] : 0.0;
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(c0), "+d"(c1)
+                       : "d"(av), "d"(bv));
+        }
+        if (ri < m) {
+          if (cc < m && cc <= ri) M[(long long)ri * m + cc] += c0;
+          if (cc + 1 < m && cc + 1 <= ri) M[(long long)ri * m + cc + 1] += c1;
+        }
+      };
+      auto z_row = [&](long long c) {
+        double mv[BG_NB];  // the row's panel entries, all loads in flight at once
+#pragma unroll
+        for (int t = 0; t < BG_NB; ++t) mv[t] = t < kb ? M[c * m + k0 + t] : 0.0;
+        double sacc = z[c];
+#pragma unroll
+        for (int t = 0; t < BG_NB; ++t)
+          if (t < kb) sacc = fma(-mv[t], z[k0 + t], sacc);
+        z[c] = sacc;
+      };
+      if (blockIdx.x == 0) {
+        // CTA 0: the next diagonal block's tiles (<= 10) spread over its warps, its z rows,
+        // then warp 0 factors the block while warps 1-7 join the general update below
+        const int ntd = (kb2 + 7) / 8;
+        for (int tix = warp; tix < ntd * (ntd + 1) / 2; tix += BG_NT / 32) {
+          int I = 0;
+          while ((I + 1) * (I + 2) / 2 <= tix) ++I;
+          syrk_tile(I, tix - I * (I + 1) / 2);
+        }
+        if (tid < kb2) z_row(r0 + tid);
+        __syncthreads();
+        if (warp == 0) diag_phase(r0, kb2);
       }
-      if (ri < m) {
-        if (cc < m && cc <= ri) M[(long long)ri * m + cc] += c0;
-        if (cc + 1 < m && cc + 1 <= ri) M[(long long)ri * m + cc + 1] += c1;
+      if (!(blockIdx.x == 0 && warp == 0)) {
+        const int gw = gwarp - 1, ngw = nwarps - 1;  // warp 0 of CTA 0 excluded
+        const int nt = (m - r0 + 7) / 8;
+        const long long ntiles = (long long)nt * (nt + 1) / 2;
+        for (long long tix = gw; tix < ntiles; tix += ngw) {
+          int I = (int)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);
+          while ((long long)(I + 1) * (I + 2) / 2 <= tix) ++I;
+          while ((long long)I * (I + 1) / 2 > tix) --I;
+          const int C = (int)(tix - (long long)I * (I + 1) / 2);
+          if (I < 4) continue;  // the next diagonal block: warp 0 of CTA 0
+          syrk_tile(I, C);
+        }
+        const long long gt = gtid - 32, ngt = gthreads - 32;
+        for (long long c = r0 + BG_NB + gt; c < m; c += ngt) z_row(c);
       }
-    }
-    for (long long c = r0 + gtid; c < m; c += gthreads) {
-      double mv[BG_NB];  // the row's panel entries, all loads in flight at once
-#pragma unroll
-      for (int t = 0; t < BG_NB; ++t) mv[t] = t < kb ? M[c * m + k0 + t] : 0.0;
-      double s = z[c];
-#pragma unroll
-      for (int t = 0; t < BG_NB; ++t)
-        if (t < kb) s = fma(-mv[t], z[k0 + t], s);
-      z[c] = s;
     }
     grid.sync();
     CHOL_MARK(3);
