@@ -9,6 +9,8 @@
 //            split columns write partials folded in segment order.  Balanced and
 //            deterministic: no atomics, fixed summation order.
 //   scatter/gather helpers for the sample-space CG of the reduced Newton system.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ssnal_internal.h"
 
@@ -426,6 +428,7 @@ __device__ __forceinline__ void seg_write(int s, double v, const int32_t* __rest
   else part[slot] = v;
 }
 
+template <int CHE>
 __global__ void __launch_bounds__(256) cscj_xt_kernel(
     const long long* __restrict__ total, const int32_t* __restrict__ jseg,
     const int32_t* __restrict__ jpos, const double* __restrict__ jval,
@@ -433,39 +436,39 @@ __global__ void __launch_bounds__(256) cscj_xt_kernel(
     const double* __restrict__ w, double* __restrict__ out, double* __restrict__ part,
     double* __restrict__ cval, double* __restrict__ ctail, uint8_t* __restrict__ cflag) {
   const long long nnz = *total;
-  const long long nch = (nnz + CH - 1) / CH;
+  const long long nch = (nnz + (32 * CHE) - 1) / (32 * CHE);
   const int lane = threadIdx.x & 31;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   constexpr int NONE = 0x7fffffff;
   for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nch; c += nw) {
-    const long long c0 = c * CH, e0 = c0 + lane * CH_E;
+    const long long c0 = c * (32 * CHE), e0 = c0 + lane * CHE;
     // the chunk's first segment F continues from the previous chunk?
     const int F = jseg[c0];
     const bool chunk_in = c0 > 0 && jseg[c0 - 1] == F;
-    const int next = c0 + CH < nnz ? jseg[c0 + CH] : NONE;
-    int sg[CH_E];
-    double pr[CH_E];
+    const int next = c0 + (32 * CHE) < nnz ? jseg[c0 + (32 * CHE)] : NONE;
+    int sg[CHE];
+    double pr[CHE];
     {
       const int4* s4 = reinterpret_cast<const int4*>(jseg + e0);
       const int4* p4 = reinterpret_cast<const int4*>(jpos + e0);
       const double2* v2 = reinterpret_cast<const double2*>(jval + e0);
-      int ps[CH_E];
-      double vv[CH_E];
+      int ps[CHE];
+      double vv[CHE];
 #pragma unroll
-      for (int h = 0; h < CH_E / 4; ++h) {
+      for (int h = 0; h < CHE / 4; ++h) {
         const int4 a = __ldg(s4 + h), b = __ldg(p4 + h);
         sg[4 * h] = a.x; sg[4 * h + 1] = a.y; sg[4 * h + 2] = a.z; sg[4 * h + 3] = a.w;
         ps[4 * h] = b.x; ps[4 * h + 1] = b.y; ps[4 * h + 2] = b.z; ps[4 * h + 3] = b.w;
       }
 #pragma unroll
-      for (int h = 0; h < CH_E / 2; ++h) {
+      for (int h = 0; h < CHE / 2; ++h) {
         const double2 v = __ldg(v2 + h);
         vv[2 * h] = v.x; vv[2 * h + 1] = v.y;
       }
       // gathers of w after all index loads are in flight
-      double wg[CH_E];
+      double wg[CHE];
 #pragma unroll
-      for (int u = 0; u < CH_E; ++u) {
+      for (int u = 0; u < CHE; ++u) {
         const bool ok = e0 + u < nnz;
         if (!ok) sg[u] = NONE;
         pr[u] = ok ? vv[u] : 0.0;
@@ -477,7 +480,7 @@ __global__ void __launch_bounds__(256) cscj_xt_kernel(
       double run = 0.0, hsum = 0.0;
       bool single = true;
 #pragma unroll
-      for (int u = 0; u < CH_E; ++u) {
+      for (int u = 0; u < CHE; ++u) {
         if (sg[u] != cur) {
           if (single) {
             hsum = run;
@@ -549,6 +552,7 @@ __global__ void __launch_bounds__(256) cscj_xt_kernel(
 
 // segments that cross chunk boundaries: tail partial + the following chunks' first-
 // segment partials, in chunk order, up to the chunk where the segment closes
+template <int CHE>
 __global__ void __launch_bounds__(256) cscj_fix_kernel(
     const long long* __restrict__ total, const int32_t* __restrict__ jseg,
     const int32_t* __restrict__ seg_col, const int32_t* __restrict__ seg_slot,
@@ -556,7 +560,7 @@ __global__ void __launch_bounds__(256) cscj_fix_kernel(
     const uint8_t* __restrict__ cflag, double* __restrict__ out, double* __restrict__ part,
     const int32_t* __restrict__ empty, const unsigned int* __restrict__ nempty) {
   const long long nnz = *total;
-  const long long nch = (nnz + CH - 1) / CH;
+  const long long nch = (nnz + (32 * CHE) - 1) / (32 * CHE);
   const long long ne = *nempty;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne;
        e += (long long)gridDim.x * blockDim.x)
@@ -569,7 +573,7 @@ __global__ void __launch_bounds__(256) cscj_fix_kernel(
       t += cval[d];
       if (cflag[d] & 1) break;
     }
-    seg_write(jseg[c * CH + CH - 1], t, seg_col, seg_slot, out, part);
+    seg_write(jseg[c * (32 * CHE) + (32 * CHE) - 1], t, seg_col, seg_slot, out, part);
   }
 }
 
@@ -707,7 +711,7 @@ cudaError_t launch_csrj_xd(const CscJ& c, long long p, const double* d, double* 
 
 size_t cscj_ws_bytes(const CsrOp& op) {
   const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
-  const long long cap = op.nnz + CH;  // vector loads of the last chunk stay inside
+  const long long cap = op.nnz + 32 * 32;  // vector loads of the last chunk (CHE <= 32) stay inside
   const long long nch = ceil_div(cap, (long long)CH);
   const long long rb = ceil_div(op.n, (long long)RJ_NT) + 1;
   return 256 + sizeof(int32_t) * (size_t)op.n + sizeof(int) * (size_t)op.nseg +
@@ -721,7 +725,7 @@ static char* al256(char* p) { return (char*)(((uintptr_t)p + 255) & ~(uintptr_t)
 
 CscJ cscj_layout(const CsrOp& op, void* ws) {
   const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
-  const long long cap = op.nnz + CH;
+  const long long cap = op.nnz + 32 * 32;
   const long long nch = ceil_div(cap, (long long)CH);
   CscJ c;
   char* p = al256((char*)ws);
@@ -772,22 +776,34 @@ cudaError_t launch_cscj_build(const CsrOp& op, const uint8_t* keep, const int32_
   return cudaGetLastError();
 }
 
-cudaError_t launch_cscj_xt(const CsrOp& op, const CscJ& c, const double* w, double* out,
-                           double* part, cudaStream_t stream) {
+template <int CHE>
+static void launch_cscj_xt_che(const CsrOp& op, const CscJ& c, const double* w, double* out,
+                               double* part, cudaStream_t stream) {
   const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
   const long long* total = c.blk + nblk;  // kept entries (cscj_count_kernel)
   // segments without kept entries are never visited by the chunks: the fix kernel
   // writes their zeros from the build's list
-  const long long nch_max = ceil_div(op.nnz, (long long)CH);
+  const long long nch_max = ceil_div(op.nnz, (long long)(32 * CHE));
   const unsigned grid = (unsigned)std::max(1LL, std::min(ceil_div(nch_max, 8LL), 148LL * 8));
   note_launch();
-  cscj_xt_kernel<<<grid, 256, 0, stream>>>(total, c.seg, c.pos, c.val, op.seg_col, op.seg_slot,
-                                           w, out, part, c.cval, c.ctail, c.cflag);
+  cscj_xt_kernel<CHE><<<grid, 256, 0, stream>>>(total, c.seg, c.pos, c.val, op.seg_col,
+                                                 op.seg_slot, w, out, part, c.cval, c.ctail,
+                                                 c.cflag);
   note_launch();
-  cscj_fix_kernel<<<(unsigned)std::max(1LL, std::min(ceil_div(std::max(nch_max, (long long)op.nseg), 256LL),
-                                                      148LL * 4)), 256,
-                    0, stream>>>(total, c.seg, op.seg_col, op.seg_slot, c.cval, c.ctail, c.cflag,
-                                 out, part, c.empty, c.nempty);
+  cscj_fix_kernel<CHE><<<(unsigned)std::max(1LL, std::min(ceil_div(std::max(nch_max, (long long)op.nseg), 256LL),
+                                                           148LL * 4)), 256,
+                         0, stream>>>(total, c.seg, op.seg_col, op.seg_slot, c.cval, c.ctail, c.cflag,
+                                      out, part, c.empty, c.nempty);
+}
+
+cudaError_t launch_cscj_xt(const CsrOp& op, const CscJ& c, const double* w, double* out,
+                           double* part, cudaStream_t stream) {
+  // entries per lane of the nnz-balanced product (SSNAL_CSCJ_CHE = 8 | 16 | 32; the
+  // workspace is sized for the smallest chunk, larger chunks fit)
+  static const int che = std::getenv("SSNAL_CSCJ_CHE") ? std::atoi(std::getenv("SSNAL_CSCJ_CHE")) : 8;
+  if (che == 32) launch_cscj_xt_che<32>(op, c, w, out, part, stream);
+  else if (che == 16) launch_cscj_xt_che<16>(op, c, w, out, part, stream);
+  else launch_cscj_xt_che<8>(op, c, w, out, part, stream);
   if (op.nfold > 0) {
     note_launch();
     csc_fold_kernel<<<(unsigned)ceil_div(op.nfold * 32, 256LL), 256, 0, stream>>>(
