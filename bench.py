@@ -32,12 +32,14 @@ search, without which the reference stalls above KKT 1e-6 -- DESIGN.md section 8
 the full workload, with all host threads; one full solve is one step and a full solve
 takes minutes, so it runs ONE step whatever --steps says (reported as steps_run).
 
-N > 1 runs the ROW-SHARDED solve of the dense workloads (configs 1 and 4, BASELINE
-quotes config 4 "row-sharded 1/2/4/8 GPUs"): rank r owns a contiguous slice of the
-samples and of the dual vector (sharded.py); X^T v, the q x q Gram and the CG vectors
-are NCCL all-reduces, the projection's multiplier search exchanges one small record per
-pass.  "parallelism": "row-sharded", "scaling": "strong" (the total problem is fixed).
-The sparse configs with N > 1 run N replicas ("parallelism": "replicas").
+N > 1 runs the ROW-SHARDED solve of the workload (BASELINE quotes configs 3 and 4
+"row-sharded over 1/2/4/8 GPUs"), every config: rank r owns a contiguous slice of the
+samples and of the dual vector and runs the NATIVE sharded driver
+(ssnal_alm_solve_sharded, csrc/driver.cu) -- X^T v, the q x q Gram, X^T dPi and the dot
+partials are NCCL all-reduces, the projection's multiplier search all-gathers one
+8-double record per trial and pass, all enqueued on the solver stream through the
+library's own NCCL communicator (csrc/comm.cu).  "parallelism": "row-sharded",
+"scaling": "strong" (the total problem is fixed).  `--sharded` runs that path at N = 1.
 """
 
 import argparse
@@ -266,7 +268,7 @@ def run_reference(args, rank, world):
                    "outer": rep["outer_iters"], "inner": rep["total_inner_iters"],
                    "converged": rep["converged"]},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------ our arm
@@ -283,105 +285,37 @@ ROOF = {
 NCU_FILES = {"dense_x": "r2_ncu_c4_stream_xd_kernel.txt", "gram": "r2_ncu_c4_gram_kernel.txt"}
 
 
-def run_sharded(args, rank, world, local_rank):
-    """Row-sharded dense solve over `world` GPUs (one process per GPU, NCCL)."""
-    import torch
-    import torch.distributed as dist
-
-    import paper_1910_01312_b200 as P
-    from paper_1910_01312_b200 import backend as B
+def rank_slice(cfg, rank, world):
+    """This rank's contiguous block of samples (sharded.shard_range): dense rows, CSR
+    rows (row pointers rebased), labels / targets."""
     from paper_1910_01312_b200 import sharded as S
 
-    torch.cuda.set_device(local_rank)
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29511")
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank), rank=rank,
-                            world_size=world)
-    comm = S.ShardComm()
-    cfg = make_cfg(args.config)
-    n_phys = cfg["A"].shape[0]
-    lo, hi = S.shard_range(n_phys, rank, world)
-    A_host = torch.from_numpy(np.ascontiguousarray(cfg["A"][lo:hi])).pin_memory()
+    n = int(cfg["shape"][0]) if "indptr" in cfg else int(cfg["A"].shape[0])
+    lo, hi = S.shard_range(n, rank, world)
+    out = dict(cfg)
+    if "indptr" in cfg:
+        ip = cfg["indptr"]
+        b, e = int(ip[lo]), int(ip[hi])
+        out.update(indptr=np.ascontiguousarray(ip[lo:hi + 1] - ip[lo]),
+                   indices=cfg["indices"][b:e], data=cfg["data"][b:e],
+                   shape=(hi - lo, int(cfg["shape"][1])))
+    else:
+        out["A"] = np.ascontiguousarray(cfg["A"][lo:hi])
+    for k in ("y", "t"):
+        if k in cfg:
+            out[k] = cfg[k][lo:hi]
+    return out
 
-    def build(A):
-        if cfg["task"] == "svr":
-            return S.build_svr_dual_sharded(A, cfg["t"][lo:hi], cfg["C"], cfg["epsilon"], comm)
-        return S.build_csvc_dual_sharded(A, cfg["y"][lo:hi], cfg["C"], comm)
 
-    problem = build(A_host.to("cuda"))
-    opts = P.AlmOptions(tol_kkt=TOL)
-    ssn = P.SsnOptions(engine="python")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-
-    def barrier():
-        dist.barrier()
-        torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
-        P.alm_solve(problem, opts, ssn, return_device=True)
-    barrier()
-    stream = torch.cuda.current_stream()
-    sampler = ClockSampler(local_rank)
-    sampler.sample()
-    step_s, reps = [], []
-    for _ in range(args.steps):
-        flush.fill_(1)
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rep = P.alm_solve(problem, opts, ssn, return_device=True)
-        e1.record(stream)
-        e1.synchronize()
-        step_s.append(e0.elapsed_time(e1) * 1e-3)
-        reps[:] = [rep]  # only the last: a kept x_opt per step grew the allocator mid-run
-        sampler.sample()
-    t = torch.tensor([float(np.sum(step_s))], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    value = float(t[0]) / args.steps
-    clocks = sampler.stop()
-    del problem
-    e2e_times, h2d = [], 0
-    for i in range(args.warmup + args.steps):
-        flush.fill_(1)
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        h0 = B.H2D["bytes"]
-        e0.record(stream)
-        pb = build(A_host)
-        r = P.alm_solve(pb, opts, ssn)
-        e1.record(stream)
-        e1.synchronize()
-        if i >= args.warmup:
-            e2e_times.append(e0.elapsed_time(e1) * 1e-3)
-            h2d = B.H2D["bytes"] - h0
-        del pb
-    te = torch.tensor([float(np.sum(e2e_times))], dtype=torch.float64, device="cuda")
-    dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    hb = torch.tensor([float(h2d)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(hb, op=dist.ReduceOp.SUM)
-    if rank == 0:
-        last = reps[-1]
-        d = config_dict(args, cfg, world)
-        d["parallelism"] = f"row-sharded over {world} GPUs (NCCL all-reduce)"
-        line = {
-            "metric": METRICS[args.config], "value": value, "unit": "s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
-            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded, BASELINE config shapes and distributions)",
-            "config": d,
-            "e2e": {"value": float(te[0]) / args.steps, "unit": "s",
-                    "h2d_bytes_per_step": int(hb[0]), "d2h_bytes_per_step": int(r.x_opt.size * 8),
-                    "path": "build_*_dual_sharded from each rank's pinned host slice + alm_solve"},
-            "gpu_launches": None, "roofline": None, "cpu_baseline": None, "clocks": clocks,
-            "result": {"kkt": last.kkt_residual, "objective": last.objective,
-                       "outer": last.outer_iters, "inner": last.total_inner_iters,
-                       "converged": last.converged},
-            "step_ms": [round(t_ * 1e3, 3) for t_ in step_s],
-        }
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
+def build_sharded(S, cfg, comm, A=None):
+    """The sharded public API call (sharded.build_*_dual_sharded) on this rank's slice."""
+    if "indptr" in cfg:
+        feats = (cfg["indptr"], cfg["indices"], cfg["data"], cfg["shape"])
+    else:
+        feats = cfg["A"] if A is None else A
+    if cfg["task"] == "svr":
+        return S.build_svr_dual_sharded(feats, cfg["t"], cfg["C"], cfg["epsilon"], comm)
+    return S.build_csvc_dual_sharded(feats, cfg["y"], cfg["C"], comm)
 
 
 def run_ours(args, rank, world, local_rank):
@@ -392,15 +326,30 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if world > 1 or sharded:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank), rank=rank,
+                                world_size=world)
     be = P.default_backend()
     cfg = make_cfg(args.config)
+    if sharded:
+        # row-sharded: each rank holds its slice only; the native sharded driver
+        # (ssnal_alm_solve_sharded) over the library's NCCL communicator
+        from paper_1910_01312_b200 import sharded as S
+
+        comm = S.ShardComm()
+        lcfg = rank_slice(cfg, rank, world)
+        build = lambda A=None: build_sharded(S, lcfg, comm, A)  # noqa: E731
+    else:
+        lcfg = cfg
+        build = lambda A=None: build_problem(P, cfg, A)  # noqa: E731
     dense = "indptr" not in cfg
-    A_host = torch.from_numpy(cfg["A"]).pin_memory() if dense else None
-    problem = build_problem(P, cfg, A_host.to("cuda") if dense else None)
+    A_host = torch.from_numpy(lcfg["A"]).pin_memory() if dense else None
+    problem = build(A_host.to("cuda") if dense else None)
     opts = P.AlmOptions(tol_kkt=TOL)
     ssn = ssn_options(P, cfg)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -470,7 +419,7 @@ def run_ours(args, rank, world, local_rank):
         e1 = torch.cuda.Event(enable_timing=True)
         h0 = B.H2D["bytes"]
         e0.record(stream)
-        pb = build_problem(P, cfg, A_host)
+        pb = build(A_host)
         r = P.alm_solve(pb, opts, ssn)  # x_opt copied to a host numpy array
         e1.record(stream)
         e1.synchronize()
@@ -481,9 +430,14 @@ def run_ours(args, rank, world, local_rank):
     d2h = int(r.x_opt.size * 8)
     gc.enable()
     te = torch.tensor([float(np.sum(e2e_times))], dtype=torch.float64, device="cuda")
+    io = torch.tensor([float(h2d or 0), float(d2h)], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        dist.all_reduce(io, op=dist.ReduceOp.SUM)  # every rank's copies
     e2e = float(te[0]) / args.steps
+    h2d, d2h = int(io[0]), int(io[1])
+    if sharded:
+        comm.close()
 
     if rank != 0:
         if dist is not None:
@@ -534,16 +488,25 @@ def run_ours(args, rank, world, local_rank):
                "kkt": ref["kkt_residual"], "objective": ref["objective"],
                "outer": ref["outer_iters"], "inner": ref["total_inner_iters"]}
     last = reps[-1]
+    cdict = config_dict(args, cfg, world)
+    if sharded:
+        cdict["parallelism"] = (f"row-sharded over {world} GPU(s): native sharded driver, "
+                                "NCCL all-reduce (q-vectors, Gram, dots) + all-gather "
+                                "(projection records)")
     line = {
         "metric": METRICS[args.config], "value": value, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": False, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE config shapes and distributions)",
-        "config": config_dict(args, cfg, world),
-        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d or 0),
+        "config": cdict,
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "build_svr_dual/build_csvc_dual from pinned host A + alm_solve "
-                        "(x_opt read back)"},
+                "path": ("build_*_dual_sharded from each rank's pinned host slice + alm_solve "
+                         "(each rank's x_opt slice read back; bytes summed over ranks)"
+                         if sharded else
+                         "build_svr_dual/build_csvc_dual from pinned host A + alm_solve "
+                         "(x_opt read back)")},
         "gpu_launches": int(launches),
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -555,12 +518,26 @@ def run_ours(args, rank, world, local_rank):
         "step_ms": [round(t_ * 1e3, 3) for t_ in step_s],
         "median_ms": round(float(np.median(step_s)) * 1e3, 3),
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist is not None:
         dist.destroy_process_group()
 
 
+_OUT = sys.stdout
+
+
+def emit(line):
+    """The ONE JSON line on the real stdout (library chatter goes to stderr)."""
+    print(json.dumps(line), file=_OUT, flush=True)
+
+
 def main():
+    global _OUT
+    # keep stdout for the JSON line only: native libraries (NCCL's version banner) write
+    # to fd 1 directly, so fd 1 is pointed at stderr and the line goes to a saved copy
+    _OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -580,9 +557,6 @@ def main():
     import __graft_entry__
 
     __graft_entry__.build()
-    if (world > 1 or args.sharded) and args.config in (1, 4):
-        run_sharded(args, rank, world, local_rank)
-        return
     run_ours(args, rank, world, local_rank)
 
 

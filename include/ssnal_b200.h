@@ -302,9 +302,9 @@ int ssnal_alm_solve_dense(const ssnal_dense_problem_t* problem, const ssnal_opti
  * One process per GPU, rank r owning a slice of the n dual slots (rows of X).
  * The cross-slot reductions of the projection (ref projection.py:152-211) are
  * split into shard-local records the host all-gathers and folds in rank order:
- *   mode 0 (eval at lam[t]):  rec[t*8 + 0..4] = { sum a clip(v - lam a, l, u),
+ *   mode 0 (eval at lam[t]):  rec[t*8 + 0..6] = { sum a clip(v - lam a, l, u),
  *     sum a^2 over slots free just right of lam, ... just left, nearest breakpoint
- *     > lam (+inf), nearest breakpoint < lam (-inf) }
+ *     > lam (+inf), nearest breakpoint < lam (-inf), smallest breakpoint, largest }
  *   mode 1 (apply at lam[t]): x_out / free_out (T x n) and rec[t*8 + 0..5] =
  *     { sum v^2, sum (v-x)^2, sum (x-ref)^2, sum_free a^2, nfree, sum x(2v-x) }
  *     (base != NULL: slot 0 is the Bregman term of ssnal_project_ex instead of sum v^2)
@@ -329,6 +329,50 @@ int ssnal_hs_apply_coef(const uint8_t* free_mask, const double* a, const double*
  * ssnal_dense_gram(sigma = 1, a'a = 0) blocks (shift = world size). */
 int ssnal_qspace_assemble(int64_t m, const double* u, double asa, double sigma, double shift,
                           double* M, void* stream);
+
+/* ---- row-sharded native driver ------------------------------------------------
+ * The whole loop of ssnal_alm_solve_dense over world ranks, rank r holding a slice of
+ * the dual slots (rows of X: C-SVC rows, or [x+ ; x-] of its SVR rows) -- the problem
+ * passed is that slice, with d the GLOBAL right-hand side of a'x = d.  Replaces ref
+ * solver.py:429-530 alm_solve for a partitioned sample set: the reference's
+ * cross-slot sums (kernels.py:144-154 X^T v, solver.py:151-172 / 238-269 the Newton
+ * system and its inner products, projection.py:152-211 the multiplier search) become
+ *   allreduce_sum: q-vectors (X^T v, X^T dPi), the kept q x q Gram, dot partials;
+ *   allgather:     the projection search's 8-double records (folded in rank order).
+ * Every rank receives the same reduced buffers, so the host decisions agree.  The
+ * reduced Newton system is always the q x q one (dense: q <= 2048; sparse: q x q direct
+ * for q <= 2048, else the factor-space Jacobi CG).  Both collectives are enqueued on
+ * `stream`; a transport must order them with the solver's kernels on that stream. */
+#define SSNAL_COMM_ID_BYTES 128
+#define SSNAL_COMM_NCCL 1          /* ssnal_nccl_comm_create                              */
+#define SSNAL_COMM_LOOPBACK 2      /* ssnal_loopback_comm_create (tests: ranks = threads) */
+typedef struct ssnal_comm_t {
+  int world, rank;
+  int (*allreduce_sum)(void* ctx, double* buf, int64_t count, void* stream);  /* in place */
+  int (*allgather)(void* ctx, const double* in, double* out, int64_t count, void* stream);
+  void* ctx;
+  int kind;                /* SSNAL_COMM_*, 0 for a caller-provided transport          */
+  int pad_;
+} ssnal_comm_t;
+
+/* NCCL transport (libnccl.so.2 opened at run time): rank 0 makes the id, every rank
+ * calls create with it after selecting its device (one process per GPU). */
+int ssnal_nccl_unique_id(unsigned char* id /* SSNAL_COMM_ID_BYTES */);
+int ssnal_nccl_comm_create(int world, int rank, const unsigned char* id, ssnal_comm_t* out);
+/* Loopback transport: world ranks as host threads of one process on one GPU (each with
+ * its own stream); a collective drains the caller's stream, meets the other ranks at a
+ * host barrier and sums their buffers in rank order -- no kernel waits on a rank. */
+int ssnal_loopback_group_create(int world, void** group);
+int ssnal_loopback_comm_create(void* group, int rank, ssnal_comm_t* out);
+int ssnal_loopback_group_destroy(void* group);
+int ssnal_comm_destroy(ssnal_comm_t* comm);
+
+size_t ssnal_alm_ws_bytes_sharded(int64_t n_phys, int64_t q, int svr_block, int world);
+size_t ssnal_alm_ws_bytes_csr_sharded(const ssnal_csr_operator_t* op, int world);
+int ssnal_alm_solve_sharded(const ssnal_dense_problem_t* problem, const ssnal_options_t* options,
+                            const ssnal_comm_t* comm, const double* x0, const double* w0,
+                            double* x_out, ssnal_report_t* report, void* ws, size_t ws_bytes,
+                            ssnal_progress_fn progress, void* progress_ctx, void* stream);
 
 /* Fused SsN gradient of the dense operator (ref solver.py:143-148):
  *   s = w - x_p (written), g_r = X^T s (q), grad = X g_r (n_log), *g2 = ||grad||^2

@@ -115,6 +115,16 @@ class Report(ctypes.Structure):
 
 PROGRESS_FN = ctypes.CFUNCTYPE(None, _I, _D, _D, ctypes.c_longlong, _I, _P)
 
+COMM_ID_BYTES = 128
+ALLREDUCE_FN = ctypes.CFUNCTYPE(_I, _P, _P, _I64, _P)
+ALLGATHER_FN = ctypes.CFUNCTYPE(_I, _P, _P, _P, _I64, _P)
+
+
+class Comm(ctypes.Structure):
+    """ssnal_comm_t (the row-sharded driver's transport)"""
+    _fields_ = [("world", _I), ("rank", _I), ("allreduce_sum", ALLREDUCE_FN),
+                ("allgather", ALLGATHER_FN), ("ctx", _P), ("kind", _I), ("pad_", _I)]
+
 _SIGNATURES.update({
     "ssnal_alm_ws_bytes": (_SZ, [_I64, _I64, _I]),
     "ssnal_alm_ws_bytes_csr": (_SZ, [ctypes.POINTER(CsrOperator)]),
@@ -126,6 +136,17 @@ _SIGNATURES.update({
     "ssnal_csr_xd_restricted": (_I, [ctypes.POINTER(CsrOperator), _P, _P, _I64, _P, _P, _P, _P]),
     "ssnal_alm_solve_dense": (_I, [ctypes.POINTER(DenseProblem), ctypes.POINTER(Options), _P, _P,
                                    _P, ctypes.POINTER(Report), _P, _SZ, PROGRESS_FN, _P, _P]),
+    "ssnal_alm_ws_bytes_sharded": (_SZ, [_I64, _I64, _I, _I]),
+    "ssnal_alm_ws_bytes_csr_sharded": (_SZ, [ctypes.POINTER(CsrOperator), _I]),
+    "ssnal_alm_solve_sharded": (_I, [ctypes.POINTER(DenseProblem), ctypes.POINTER(Options),
+                                     ctypes.POINTER(Comm), _P, _P, _P, ctypes.POINTER(Report), _P,
+                                     _SZ, PROGRESS_FN, _P, _P]),
+    "ssnal_nccl_unique_id": (_I, [ctypes.c_char_p]),
+    "ssnal_nccl_comm_create": (_I, [_I, _I, ctypes.c_char_p, ctypes.POINTER(Comm)]),
+    "ssnal_loopback_group_create": (_I, [_I, ctypes.POINTER(_P)]),
+    "ssnal_loopback_comm_create": (_I, [_P, _I, ctypes.POINTER(Comm)]),
+    "ssnal_loopback_group_destroy": (_I, [_P]),
+    "ssnal_comm_destroy": (_I, [ctypes.POINTER(Comm)]),
     "ssnal_proj_local_ws_bytes": (_SZ, [_I64, _I]),
     "ssnal_proj_local": (_I, [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I64, _I, _I, _P, _P, _P, _P,
                               _D, _P, _P, _P]),

@@ -33,12 +33,12 @@ cudaError_t launch_dense_gram(const double* A, long long n, long long q, long lo
 cudaError_t launch_chol_solve(double* M, long long m, const double* b, double scale, double* x,
                               int* info, cudaStream_t s);
 size_t pspace_ws_bytes(long long p, long long q);
-size_t alm_ws_bytes(long long n_phys, long long q, int svr);
-size_t alm_ws_bytes_csr(const ssnal_csr_operator_t* op);
+size_t alm_ws_bytes(long long n_phys, long long q, int svr, int world);
+size_t alm_ws_bytes_csr(const ssnal_csr_operator_t* op, int world);
 int alm_solve_dense(const ssnal_dense_problem_t* pb, const ssnal_options_t* opt, const double* x0,
                     const double* w0, double* x_out, ssnal_report_t* rep, void* ws,
                     size_t ws_bytes, ssnal_progress_fn cb, void* ctx, cudaStream_t stream,
-                    const char** err);
+                    const char** err, const ssnal_comm_t* comm);
 cudaError_t launch_pspace_direction(const double* A, long long n, long long q, long long lda,
                                     const double* rs, int svr, const int32_t* J, long long p,
                                     const double* grad, const double* a, double sigma, double asa,
@@ -217,11 +217,19 @@ int ssnal_dense_gram(const double* A, int64_t n_phys, int64_t q, int64_t lda,
 size_t ssnal_pspace_ws_bytes(int64_t p, int64_t q) { return pspace_ws_bytes(p, q); }
 
 size_t ssnal_alm_ws_bytes(int64_t n_phys, int64_t q, int svr_block) {
-  return alm_ws_bytes(n_phys, q, svr_block);
+  return alm_ws_bytes(n_phys, q, svr_block, 0);
 }
 
 size_t ssnal_alm_ws_bytes_csr(const ssnal_csr_operator_t* op) {
-  return op ? alm_ws_bytes_csr(op) : 0;
+  return op ? alm_ws_bytes_csr(op, 0) : 0;
+}
+
+size_t ssnal_alm_ws_bytes_sharded(int64_t n_phys, int64_t q, int svr_block, int world) {
+  return world >= 1 ? alm_ws_bytes(n_phys, q, svr_block, world) : 0;
+}
+
+size_t ssnal_alm_ws_bytes_csr_sharded(const ssnal_csr_operator_t* op, int world) {
+  return (op && world >= 1) ? alm_ws_bytes_csr(op, world) : 0;
 }
 
 static bool csr_ok(const ssnal_csr_operator_t* op) {
@@ -279,26 +287,87 @@ int ssnal_csr_colsq(const ssnal_csr_operator_t* op, const uint8_t* keep, double*
   return check("ssnal_csr_colsq", launch_csc_colsq(*op, keep, out, (double*)ws, S(stream)));
 }
 
+static int alm_solve_common(const char* name, const ssnal_dense_problem_t* problem,
+                            const ssnal_options_t* options, const double* x0, const double* w0,
+                            double* x_out, ssnal_report_t* report, void* ws, size_t ws_bytes,
+                            ssnal_progress_fn progress, void* progress_ctx, void* stream,
+                            const ssnal_comm_t* comm);
+
 int ssnal_alm_solve_dense(const ssnal_dense_problem_t* problem, const ssnal_options_t* options,
                           const double* x0, const double* w0, double* x_out,
                           ssnal_report_t* report, void* ws, size_t ws_bytes,
                           ssnal_progress_fn progress, void* progress_ctx, void* stream) {
+  return alm_solve_common("ssnal_alm_solve_dense", problem, options, x0, w0, x_out, report, ws,
+                          ws_bytes, progress, progress_ctx, stream, nullptr);
+}
+
+int ssnal_alm_solve_sharded(const ssnal_dense_problem_t* problem, const ssnal_options_t* options,
+                            const ssnal_comm_t* comm, const double* x0, const double* w0,
+                            double* x_out, ssnal_report_t* report, void* ws, size_t ws_bytes,
+                            ssnal_progress_fn progress, void* progress_ctx, void* stream) {
+  if (!comm || comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world ||
+      !comm->allreduce_sum || !comm->allgather)
+    return fail_arg("ssnal_alm_solve_sharded", "invalid communicator");
+  return alm_solve_common("ssnal_alm_solve_sharded", problem, options, x0, w0, x_out, report, ws,
+                          ws_bytes, progress, progress_ctx, stream, comm);
+}
+
+int ssnal_nccl_unique_id(unsigned char* id) {
+  if (!id) return fail_arg("ssnal_nccl_unique_id", "null id");
+  const char* err = nullptr;
+  const int rc = nccl_unique_id(id, &err);
+  if (rc != SSNAL_OK) snprintf(g_err, sizeof g_err, "ssnal_nccl_unique_id: %s", err ? err : "failed");
+  return rc;
+}
+
+int ssnal_nccl_comm_create(int world, int rank, const unsigned char* id, ssnal_comm_t* out) {
+  if (!id || !out || world < 1 || rank < 0 || rank >= world)
+    return fail_arg("ssnal_nccl_comm_create", "world/rank/null");
+  const char* err = nullptr;
+  const int rc = nccl_comm_create(world, rank, id, out, &err);
+  if (rc != SSNAL_OK)
+    snprintf(g_err, sizeof g_err, "ssnal_nccl_comm_create: %s", err ? err : "failed");
+  return rc;
+}
+
+int ssnal_loopback_group_create(int world, void** group) {
+  if (!group) return fail_arg("ssnal_loopback_group_create", "null group");
+  const int rc = loop_group_create(world, group);
+  if (rc != SSNAL_OK) return fail_arg("ssnal_loopback_group_create", "world outside 1..16");
+  return rc;
+}
+
+int ssnal_loopback_comm_create(void* group, int rank, ssnal_comm_t* out) {
+  if (!group || !out) return fail_arg("ssnal_loopback_comm_create", "null group/out");
+  const int rc = loop_comm_create(group, rank, out);
+  if (rc != SSNAL_OK) return fail_arg("ssnal_loopback_comm_create", "rank outside the group");
+  return rc;
+}
+
+int ssnal_loopback_group_destroy(void* group) { return loop_group_destroy(group); }
+
+int ssnal_comm_destroy(ssnal_comm_t* comm) { return comm_destroy(comm); }
+
+static int alm_solve_common(const char* name, const ssnal_dense_problem_t* problem,
+                            const ssnal_options_t* options, const double* x0, const double* w0,
+                            double* x_out, ssnal_report_t* report, void* ws, size_t ws_bytes,
+                            ssnal_progress_fn progress, void* progress_ctx, void* stream,
+                            const ssnal_comm_t* comm) {
   if (!problem || !options || !x_out || !report || !ws)
-    return fail_arg("ssnal_alm_solve_dense", "null problem/options/x_out/report/ws");
+    return fail_arg(name, "null problem/options/x_out/report/ws");
   const ssnal_dense_problem_t& p = *problem;
   if (p.csr) {
     if (!csr_ok(p.csr) || p.svr_block || p.n != p.csr->n || p.n_phys != p.csr->n ||
         p.q != p.csr->q || !p.c || !p.a)
-      return fail_arg("ssnal_alm_solve_dense", "inconsistent sparse problem");
+      return fail_arg(name, "inconsistent sparse problem");
   } else if (p.n_phys < 1 || p.q < 1 || p.lda < p.q || !p.A || !p.c || !p.a ||
              p.n != (p.svr_block ? 2 * p.n_phys : p.n_phys)) {
-    return fail_arg("ssnal_alm_solve_dense", "inconsistent problem sizes");
+    return fail_arg(name, "inconsistent problem sizes");
   }
   const char* err = nullptr;
   int rc = alm_solve_dense(problem, options, x0, w0, x_out, report, ws, ws_bytes, progress,
-                           progress_ctx, S(stream), &err);
-  if (rc != SSNAL_OK)
-    snprintf(g_err, sizeof g_err, "ssnal_alm_solve_dense: %s", err ? err : "failed");
+                           progress_ctx, S(stream), &err, comm);
+  if (rc != SSNAL_OK) snprintf(g_err, sizeof g_err, "%s: %s", name, err ? err : "failed");
   return rc;
 }
 

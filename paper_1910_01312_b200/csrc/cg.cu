@@ -124,6 +124,18 @@ cudaError_t launch_cg_check(long long n, const double* zn, double sigma, double*
   return cudaGetLastError();
 }
 
+// sharded stopping test: *sq = ||zn||^2 already all-reduced over the ranks
+__global__ void cg_check_final_kernel(const double* sq, double scale, double* cgs) {
+  cgs[CG_RR] = scale * scale * *sq;
+  if (cgs[CG_RR] <= cgs[CG_TOL2]) cgs[CG_DONE] = 1.0;
+}
+
+cudaError_t launch_cg_check_final(const double* sq, double scale, double* cgs, cudaStream_t s) {
+  note_launch();
+  cg_check_final_kernel<<<1, 1, 0, s>>>(sq, scale, cgs);
+  return cudaGetLastError();
+}
+
 // pv = z + beta pv (z = r unpreconditioned; skipped once converged)
 __global__ void cg_dir_kernel(long long p, const double* __restrict__ r, double* __restrict__ pv,
                               const double* cgs) {

@@ -133,7 +133,7 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
                             double* xp, const double* txj, uint8_t* fr, const uint8_t* tfj,
                             double* s, const double* t, double* xw, double* xpi, double* r,
                             double* part, const ProjState* st_src, ProjState* st_dst,
-                            cudaStream_t stream);
+                            cudaStream_t stream, double* dsum = nullptr);
 
 // direct reduced systems of the sparse operator: min(p, q) up to this size (M buffer)
 constexpr long long SPARSE_DIRECT_MAX = 2048;
@@ -245,12 +245,18 @@ struct Layout {
   double *ys, *tq, *cg_gJ, *cg_aJ, *cg_b, *cg_y, *cg_r, *cg_pv, *cg_Ap, *cg_zq, *cg_w, *cgs,
       *cg_part, *csc_part, *cg_d, *cg_u, *cg_z;
   CscJ cj;  // J-restricted CSC (matrix-free Newton systems)
+  // row-sharded driver: the all-reduced Gram [G ; m1] (q x q + q), the all-reduced
+  // X^T dPi of an accepted step, the projection search state and records (local T x 8,
+  // all-gathered world x T x 8), the shard-local projection partials, HS sums
+  double *Gg, *dsum, *rec_loc, *rec_all, *hsum;
+  SProj* sp;
+  void* ws_plocal;
 };
 
 size_t cg_part_doubles(long long n) { return 2 * (size_t)stream_blocks(n, 4) + 8; }
 
 Layout carve(char* base, long long n, long long n_phys, long long q, size_t* total,
-             const ssnal_csr_operator_t* csr = nullptr) {
+             const ssnal_csr_operator_t* csr = nullptr, int world = 0) {
   Carver cv{base, 0, 0};
   Layout L{};
   const bool sparse = csr != nullptr;
@@ -332,6 +338,16 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
     char* cj = cv.take<char>(cscj_ws_bytes(*csr));
     if (base) L.cj = cscj_layout(*csr, cj);
   }
+  if (world > 0) {
+    const bool qs = sparse ? q <= SPARSE_DIRECT_MAX : qsys;
+    L.Gg = qs ? cv.take<double>((size_t)q * q + q) : nullptr;
+    L.dsum = cv.take<double>(q);
+    L.rec_loc = cv.take<double>(8 * TMAX);
+    L.rec_all = cv.take<double>(8 * (size_t)TMAX * world);
+    L.hsum = cv.take<double>(8);
+    L.sp = cv.take<SProj>(TMAX);
+    L.ws_plocal = cv.take<char>(proj_local_ws_bytes(n, TMAX));
+  }
   *total = cv.off + 256;
   return L;
 }
@@ -387,9 +403,30 @@ struct Driver {
   double op_flops[SSNAL_NOPS] = {};
   long long op_calls[SSNAL_NOPS] = {};
 
+  // row-sharded driver (ssnal_alm_solve_sharded): this rank's slice of the dual slots;
+  // every cross-slot sum goes through C (null: one GPU, no collectives)
+  const ssnal_comm_t* C = nullptr;
+  long long collectives = 0;
+  long long cur_local = 0;  // sharded: this rank's free slots of the current record
+
   Driver(const ssnal_dense_problem_t& p, const ssnal_options_t& o, cudaStream_t s, Layout l,
-         Pinned* h)
-      : P(p), O(o), S(s), L(l), H(h) {}
+         Pinned* h, const ssnal_comm_t* c = nullptr)
+      : P(p), O(o), S(s), L(l), H(h), C(c) {}
+
+  bool sh() const { return C != nullptr; }
+
+  // in-place sum over the ranks (enqueued on S; every rank receives the same buffer)
+  void allsum(double* buf, long long count) {
+    if (!C || count <= 0) return;
+    ++collectives;
+    if (C->allreduce_sum(C->ctx, buf, (int64_t)count, S) != 0)
+      throw DriverError{SSNAL_E_DEVICE, "sharded all-reduce failed"};
+  }
+  void allgather(const double* in, double* out, long long count) {
+    ++collectives;
+    if (C->allgather(C->ctx, in, out, (int64_t)count, S) != 0)
+      throw DriverError{SSNAL_E_DEVICE, "sharded all-gather failed"};
+  }
 
   template <class F>
   void timed(int op, double bytes, F&& f) {
@@ -425,6 +462,13 @@ struct Driver {
     ck(launch_csrj_xd_dot(L.cj, p, v, L.cg_zq, L.cg_aJ, L.cgs + 7, L.cg_part,
                           (int)cg_part_doubles(P.n) - 8, reinterpret_cast<unsigned int*>(L.cgs + 8),
                           S));
+    allsum(L.cgs + 7, 1);
+  }
+
+  // X_J^T w over the J-restricted CSC (all-reduced when sharded)
+  void cscj_xt(const double* w, double* out) {
+    ck(launch_cscj_xt(*P.csr, L.cj, w, out, L.csc_part, S));
+    allsum(out, P.q);
   }
 
   // Factor-space Jacobi-preconditioned CG for p >= q (Zipf-hot columns make the
@@ -435,8 +479,9 @@ struct Driver {
     const CsrOp& op = *P.csr;
     const long long q = P.q;
     ck(launch_gather(L.J, p, P.a, L.cg_aJ, S));
-    ck(launch_cscj_xt(op, L.cj, L.cg_aJ, L.cg_u, L.csc_part, S));  // u = X_J^T a_J
+    cscj_xt(L.cg_aJ, L.cg_u);  // u = X_J^T a_J
     ck(launch_csc_colsq(op, L.fr, L.cg_d, L.csc_part, S));
+    allsum(L.cg_d, q);
     ck(launch_cg_jacobi(q, L.cg_d, L.cg_u, asa, sigma, L.cg_d, S));
     ck(launch_vec(4, q, -1.0, L.gr, nullptr, nullptr, L.cg_b, S));
     ck(launch_cg_init(q, L.cg_b, L.cg_y, L.cg_r, L.cg_pv, L.cg_d, g2_dev,
@@ -445,7 +490,7 @@ struct Driver {
     auto gram_apply = [&](const double* v, double* out) {
       xd_dot(p, v);
       ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
-      ck(launch_cscj_xt(op, L.cj, L.cg_w, out, L.csc_part, S));
+      cscj_xt(L.cg_w, out);
     };
     for (int it = 0; it < max_it;) {
       for (int b = 0; b < cg_batch() && it < max_it; ++b, ++it) {
@@ -457,7 +502,12 @@ struct Driver {
       }
       gram_apply(L.cg_r, L.tq);
       ck(launch_csr_xd(op, nullptr, P.n_phys, L.tq, L.tmp, S));
-      ck(launch_cg_check(P.n, L.tmp, sigma, L.cgs, L.cg_part, S));
+      if (sh()) {  // ||X (.)||^2 is a sum over the slots: all-reduced before the test
+        dots({{L.tmp, nullptr}}, L.cgs + 10, P.n);
+        ck(launch_cg_check_final(L.cgs + 10, sigma, L.cgs, S));
+      } else {
+        ck(launch_cg_check(P.n, L.tmp, sigma, L.cgs, L.cg_part, S));
+      }
       ck(cudaMemcpyAsync(H->cg, L.cgs, sizeof(double) * 8, cudaMemcpyDeviceToHost, S));
       ck(cudaStreamSynchronize(S));
       ++syncs;
@@ -519,6 +569,7 @@ struct Driver {
     if (col_spread < 0.0) {
       ck(cudaMemsetAsync(L.tfree, 1, P.n, S));
       ck(launch_csc_colsq(*P.csr, L.tfree, L.cg_d, L.csc_part, S));
+      allsum(L.cg_d, P.q);
       std::vector<double> cs(P.q);
       ck(cudaMemcpyAsync(cs.data(), L.cg_d, sizeof(double) * P.q, cudaMemcpyDeviceToHost, S));
       ck(cudaStreamSynchronize(S));
@@ -532,15 +583,18 @@ struct Driver {
 
   // matrix-free reduced Newton solve; on CG failure fall back to the direct system
   // when it fits (ref solver.py:251-255), else keep iterating up to 4x the budget
-  void sparse_iterative(long long p, double asa, const double* g2_dev) {
-    const bool can_direct = std::min<long long>(p, P.q) <= SPARSE_DIRECT_MAX;
+  // (p: global free count for the routing; pl: this rank's, the size of its J)
+  // sharded: always the factor-space CG (the sample-space system couples the ranks' J)
+  void sparse_iterative(long long p, long long pl, double asa, const double* g2_dev) {
+    const bool can_direct = sh() ? P.q <= SPARSE_DIRECT_MAX
+                                 : std::min<long long>(p, P.q) <= SPARSE_DIRECT_MAX;
     const int max_it = can_direct ? O.cg_max_iters : 4 * O.cg_max_iters;
-    ck(launch_cscj_build(*P.csr, L.fr, L.J, p, L.cj, S));  // X_J's CSC for every CG product
-    const bool ok = (p < P.q && !hot_columns()) ? cg_direction(p, asa, g2_dev, max_it)
-                                                : cg_direction_q(p, asa, g2_dev, max_it);
+    ck(launch_cscj_build(*P.csr, L.fr, L.J, pl, L.cj, S));  // X_J's CSC for every CG product
+    const bool ok = (!sh() && p < P.q && !hot_columns()) ? cg_direction(p, asa, g2_dev, max_it)
+                                                         : cg_direction_q(pl, asa, g2_dev, max_it);
     if (!ok && can_direct) {
       ++cg_fallbacks;
-      sparse_direct(p, asa);
+      sparse_direct(p, pl, asa);
     }
   }
 
@@ -560,9 +614,9 @@ struct Driver {
   // direct reduced systems for the sparse operator (ref solver.py:238-246):
   //   p < q : Q_JJ by sparse row merges, (I + sigma P Q_JJ P) y = P g_J, t from y;
   //   p >= q: X_J^T X_J by masked column merges, (I + sigma X_J^T P X_J) t = -X^T s.
-  void sparse_direct(long long p, double asa) {
+  void sparse_direct(long long p, long long pl, double asa) {
     const CsrOp& op = *P.csr;
-    if (p < P.q) {
+    if (p < P.q && !sh()) {
       ck(launch_sparse_gram_rows(op, L.J, p, L.M, S));
       double* y = (double*)L.ws_ps + 3 * p;
       ck(launch_pspace_solve(L.J, p, L.grad, P.a, sigma, asa, L.M, (double*)L.ws_ps, y, L.info,
@@ -571,11 +625,13 @@ struct Driver {
       return;
     }
     ck(launch_sparse_gram_cols(op, L.fr, L.M, S));
+    allsum(L.M, P.q * P.q);
     // u = X_J^T a_J (the rank-one correction's factor vector)
-    ck(launch_gather(L.J, p, P.a, L.cg_aJ, S));
-    ck(launch_scatter(L.J, p, L.cg_aJ, L.ys, S));
+    ck(launch_gather(L.J, pl, P.a, L.cg_aJ, S));
+    ck(launch_scatter(L.J, pl, L.cg_aJ, L.ys, S));
     ck(launch_csc_xt(op, L.ys, L.tq, L.csc_part, S));
-    ck(launch_scatter_zero(L.J, p, L.ys, S));
+    ck(launch_scatter_zero(L.J, pl, L.ys, S));
+    allsum(L.tq, P.q);
     ck(launch_qspace_assemble(P.q, L.tq, asa, sigma, L.M, S));
     ck(launch_chol_solve(L.M, P.q, L.gr, -1.0, L.t, L.info, S));
   }
@@ -640,6 +696,11 @@ struct Driver {
   void project(const double* A, ProjState* st, int T, const double* B, const double* coefs,
                double* xo, uint8_t* fo, const double* ref, double hint, int newton_passes = 3,
                int passes = 0, int phases = 4, const double* hints = nullptr) {
+    if (sh()) {  // continuation (finish) when called without Newton passes
+      project_sharded(A, st, T, B, coefs, xo, fo, ref, hint, hints, newton_passes == 0,
+                      newton_passes == 0 ? 8 : std::max(newton_passes, 1));
+      return;
+    }
     ProjLaunch pl;
     pl.hints = hints;
     pl.A = A; pl.B = B; pl.coef = coefs; pl.a = P.a; pl.l = P.l; pl.u = P.u;
@@ -669,6 +730,49 @@ struct Driver {
     ++projections;
   }
 
+  // Row-sharded projection (dist.cu): unless continuing, the search state starts at the
+  // warm start; `passes` passes of eval -> all-gather of the 5-double records ->
+  // rank-ordered fold + Newton step, then apply (x / mask rank-locally) -> all-gather ->
+  // global records.  A trial still searching comes back with status != APPLIED and
+  // finish() continues it.
+  void project_sharded(const double* A, ProjState* st, int T, const double* B,
+                       const double* coefs, double* xo, uint8_t* fo, const double* ref,
+                       double hint, const double* hints, bool cont, int passes) {
+    ShardProj sp{};
+    sp.A = A; sp.B = B; sp.a = P.a; sp.l = P.l; sp.u = P.u;
+    sp.lc = P.l_const; sp.uc = P.u_const; sp.d = P.d; sp.n = P.n; sp.T = T;
+    for (int t = 0; t < T; ++t) {
+      sp.coef[t] = B ? coefs[t] : 0.0;
+      sp.hints[t] = hints ? hints[t] : hint;
+    }
+    sp.has_hints = hints != nullptr;
+    sp.hint = hint;
+    if (B && xo == L.tx && qgrad() && slope_ok && !hints) {
+      sp.slope_num = reinterpret_cast<const double*>(static_cast<const char*>(L.ws_grad) + 128);
+      sp.slope_den = &L.st_cur->sum_a2_free;
+    }
+    sp.x_out = xo; sp.free_out = fo; sp.ref = ref;
+    if (B && O.psi_stable == 2) {
+      sp.base = L.xp;
+      sp.base_lam = lam_cur;
+    }
+    trial_deferred = false;
+    const double per = 8.0 * P.n * (2 + (B != nullptr) + (P.l != nullptr) + (P.u != nullptr));
+    const double bytes = T * (per * (passes + 1) + (xo ? 8.0 * P.n : 0.0) + (fo ? 1.0 * P.n : 0.0));
+    timed(SSNAL_OP_PROJ, bytes, [&] {
+      if (!cont) ck(launch_sproj_init(sp, L.sp, S));
+      for (int k = 0; k < passes; ++k) {
+        ck(launch_sproj_eval(sp, L.sp, (double*)L.ws_plocal, L.rec_loc, S));
+        allgather(L.rec_loc, L.rec_all, 8LL * T);
+        ck(launch_sproj_update(C->world, T, L.rec_all, P.d, L.sp, S));
+      }
+      ck(launch_sproj_apply(sp, L.sp, (double*)L.ws_plocal, L.rec_loc, S));
+      allgather(L.rec_loc, L.rec_all, 8LL * T);
+      ck(launch_sproj_finish(C->world, T, L.rec_all, L.rec_loc, L.sp, sp.base != nullptr, st, S));
+    });
+    ++projections;
+  }
+
   static void raise_status(int s) {
     if (s == PROJ_INFEASIBLE_LOW || s == PROJ_INFEASIBLE_HIGH)
       throw DriverError{SSNAL_E_ARG, "projection bracket failed: constraint set infeasible"};
@@ -680,8 +784,9 @@ struct Driver {
     static const bool dbg_proj = std::getenv("SSNAL_DEBUG_PROJ") != nullptr;
     if (dbg_proj)
       for (int t = 0; t < T; ++t)
-        std::fprintf(stderr, "proj T=%d t=%d passes=%d status=%d nfree=%lld lam=%.6g\n", T, t,
-                     H->st[t].passes, H->st[t].status, (long long)H->st[t].nfree, H->st[t].lam);
+        std::fprintf(stderr, "proj T=%d t=%d passes=%d status=%d nfree=%lld lam=%.17g lo=%.17g hi=%.17g\n",
+                     T, t, H->st[t].passes, H->st[t].status, (long long)H->st[t].nfree,
+                     H->st[t].lam, H->st[t].lo, H->st[t].hi);
     bool extra = false;
     for (int round = 0;; ++round) {
       bool pending = false;
@@ -693,13 +798,20 @@ struct Driver {
       if (round > 20) throw DriverError{SSNAL_E_ARG, "projection failed to bracket the multiplier"};
       if (!extra) ++proj_fallbacks;
       extra = true;
+      if (dbg_proj)
+        for (int t = 0; t < T; ++t)
+          std::fprintf(stderr, "  round %d t=%d passes=%d status=%d lam=%.17g lo=%.17g hi=%.17g\n",
+                       round, t, H->st[t].passes, H->st[t].status, H->st[t].lam, H->st[t].lo,
+                       H->st[t].hi);
       project(A, st_dev, T, B, coefs, xo, fo, ref, 0.0, 0, 8, PHASE_EXACT | PHASE_APPLY);
       fetch(st_dev, T, false);
     }
   }
 
+  // sums over the dual slots are rank-local partials until all-reduced; sums over
+  // q-vectors (replicated on every rank) are not
   void dots(std::initializer_list<std::pair<const double*, const double*>> pairs, double* out,
-            long long len) {
+            long long len, bool replicated = false) {
     const double* xs[8];
     const double* ys[8];
     int k = 0;
@@ -710,6 +822,7 @@ struct Driver {
     }
     timed(SSNAL_OP_VEC, 8.0 * len * 2 * k,
           [&] { ck(launch_dots(k, xs, ys, nullptr, len, out, L.ws_red, S)); });
+    if (!replicated) allsum(out, k);
   }
 
   void vec(int op, double alpha, const double* x, const double* y, const double* z, double* out) {
@@ -731,6 +844,7 @@ struct Driver {
                            L.ws_xt, S));
       }
     });
+    allsum(out, (long long)k * P.q);
   }
 
   void xd(const double* d, double* out, int k) {
@@ -805,6 +919,7 @@ struct Driver {
       ck(launch_gradient_factor(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.w, L.xp,
                                 L.s, L.r, L.ws_grad, S));
     });
+    allsum(L.r, P.q);
     ck(launch_vec(3, P.q, 0.0, L.xw, L.r, nullptr, L.xpi, S));
   }
 
@@ -819,6 +934,7 @@ struct Driver {
           ck(launch_grad_from_factor(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.r,
                                      L.grad, L.scal + 4, L.ws_grad, S));
         });
+        allsum(L.scal + 4, 1);
         ck(launch_vec(4, P.q, -1.0, L.r, nullptr, nullptr, L.t, S));
       }
       vec(4, -1.0, L.s, nullptr, nullptr, L.dir);
@@ -828,30 +944,45 @@ struct Driver {
     }
     if (P.csr) {  // direct when min(p, q) is small, else matrix-free sample-space CG
       const long long lim = std::min<long long>(O.direct_solve_threshold, SPARSE_DIRECT_MAX);
+      // sharded: only the q x q direct system (the p x p one couples the ranks' J)
+      const bool direct = sh() ? P.q <= lim : std::min<long long>(p, P.q) <= lim;
+      const long long pl = sh() ? cur_local : p;
       timed(SSNAL_OP_NEWTON, 0.0, [&] {
         ck(launch_compact(L.fr, P.n, L.J, L.pcount, L.ws_cmp, S));
-        if (std::min<long long>(p, P.q) <= lim) sparse_direct(p, asa);
-        else sparse_iterative(p, asa, g2_dev);
+        if (direct) sparse_direct(p, pl, asa);
+        else sparse_iterative(p, pl, asa, g2_dev);
       });
       xd(L.t, L.qdir, 1);
       timed(SSNAL_OP_VEC, 8.0 * P.n * 5, [&] {
-        ck(launch_hs_apply(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.ws_red, S));
+        if (sh()) {  // {a_J'(Qd)_J, a_J'a_J} summed over the ranks first
+          const double* xs[2] = {P.a, P.a};
+          const double* ys[2] = {L.qdir, nullptr};
+          ck(launch_dots(2, xs, ys, L.fr, P.n, L.hsum, L.ws_red, S));
+          allsum(L.hsum, 2);
+          ck(launch_hs_finish(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.hsum, S));
+        } else {
+          ck(launch_hs_apply(L.fr, P.a, L.qdir, P.n, -sigma, L.s, -1.0, L.dir, L.ws_red, S));
+        }
       });
-      if (std::min<long long>(p, P.q) > lim) {
+      if (!direct) {
         // inexact y: X t is not Q d.  Recompute the exact image (t = X^T d, Qd = X t)
         // so Qw stays Q w along the iterates and psi / the Armijo test are exact.
         xt({L.dir}, L.t);
         xd(L.t, L.qdir, 1);
       }
       dots({{L.grad, L.dir}, {L.w, L.qw}, {L.w, L.qdir}}, L.scal, P.n);
-      dots({{L.t, nullptr}}, L.scal + 3, P.q);
+      dots({{L.t, nullptr}}, L.scal + 3, P.q, true);
       return;
     }
-    if (p < P.q && p > O.direct_solve_threshold)
+    // sharded: always the q x q system (the p x p one couples the ranks' free rows)
+    const bool qroute = p >= P.q || sh();
+    if (sh() && (P.q > O.direct_solve_threshold || P.q > DENSE_QSYS_MAX))
+      throw DriverError{SSNAL_E_ARG, "sharded dense solve: q x q system above the direct limit"};
+    if (!qroute && p > O.direct_solve_threshold)
       throw DriverError{SSNAL_E_ARG, "p x p system above direct_solve_threshold (no CG path)"};
     if (p >= P.q && P.q > O.direct_solve_threshold)
       throw DriverError{SSNAL_E_ARG, "q x q system above direct_solve_threshold (no CG path)"};
-    if (p < P.q && p > DENSE_PSYS_MAX)
+    if (!qroute && p > DENSE_PSYS_MAX)
       throw DriverError{SSNAL_E_ARG, "p x p system above the dense workspace cap (4096)"};
     if (p >= P.q && P.q > DENSE_QSYS_MAX)
       throw DriverError{SSNAL_E_ARG, "q x q system above the dense workspace cap (4096)"};
@@ -860,7 +991,7 @@ struct Driver {
     const double* g_r = qgrad() ? L.r : L.gr;
     timed(SSNAL_OP_NEWTON, p < P.q ? 8.0 * p * P.q + 16.0 * m * m : 1.0 * P.n + 4.0 * p, [&] {
       ck(launch_compact(L.fr, P.n, L.J, L.pcount, L.ws_cmp, S));
-      if (p < P.q) {
+      if (!qroute) {
         // factor-space gradient: the right-hand side needs grad_J = X_J r only
         if (qgrad())
           ck(launch_rows_grad(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.J, p, L.r,
@@ -869,14 +1000,24 @@ struct Driver {
                                    L.grad, P.a, sigma, asa, g_r, L.t, L.info, L.ws_ps, S));
       }
     });
-    if (p >= P.q) {
+    if (qroute) {
       const double* asa_dev = &L.st_cur->sum_a2_free;
       // gathered rows: bytes and flops added once the row count is known (gram_rows)
       timed(SSNAL_OP_GRAM, 0.0, [&] { gram(); });
+      const double* G = L.G;
+      const double* m1 = L.m1;
+      if (sh()) {  // the kept Gram is this rank's rows; [G ; m1] summed over the ranks
+        const size_t qq = (size_t)P.q * P.q;
+        ck(cudaMemcpyAsync(L.Gg, L.G, sizeof(double) * qq, cudaMemcpyDeviceToDevice, S));
+        ck(cudaMemcpyAsync(L.Gg + qq, L.m1, sizeof(double) * P.q, cudaMemcpyDeviceToDevice, S));
+        allsum(L.Gg, (long long)qq + P.q);
+        G = L.Gg;
+        m1 = L.Gg + qq;
+      }
       const double qd = (double)P.q;
       op_flops[SSNAL_OP_CHOL] += qd * qd * qd / 3.0 + 2.0 * qd * qd;
       timed(SSNAL_OP_CHOL, 24.0 * qd * qd, [&] {
-        ck(launch_gram_assemble(L.G, P.q, L.m1, sigma, asa_dev, L.M, S));
+        ck(launch_gram_assemble(G, P.q, m1, sigma, asa_dev, L.M, S));
         ck(launch_chol_solve(L.M, P.q, g_r, -1.0, L.t, L.info, S));
       });
     }
@@ -890,11 +1031,16 @@ struct Driver {
                                        L.qdir, L.fr, P.a, &L.st_cur->sum_a2_free, L.s, sigma,
                                        L.w, L.qw, L.dir, L.scal, L.scal + 4, L.ws_grad, S, 1));
       });
+      if (sh()) {  // a_J'(Qd)_J (P_J's coefficient, the ray slope) and ||grad||^2
+        allsum(reinterpret_cast<double*>(static_cast<char*>(L.ws_grad) + 128), 1);
+        allsum(L.scal + 4, 1);
+      }
       timed(SSNAL_OP_VEC, 8.0 * P.n * 7 + 1.0 * P.n, [&] {
         ck(launch_direction_epilogue_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, L.t,
                                        L.qdir, L.fr, P.a, &L.st_cur->sum_a2_free, L.s, sigma,
                                        L.w, L.qw, L.dir, L.scal, L.scal + 4, L.ws_grad, S, 2));
       });
+      allsum(L.scal, 3);  // {g'd, w'Qw, w'Qd}; t't is a q-space (replicated) sum
       return;
     }
     // Qd = X t (a_J'(Qd)_J folded in the sweep), d = -s - sigma P(Qd), and
@@ -1049,8 +1195,13 @@ struct Driver {
         ck(launch_accept_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, P.n, alpha,
                            -(sigma * alpha), L.w, L.dir, L.qw, L.qdir, L.u, L.xp,
                            L.tx + (size_t)j * P.n, L.fr, L.tfree + (size_t)j * P.n, L.s, tdir,
-                           L.xw, L.xpi, L.r, L.qpart, L.st_trial + j, L.st_cur, S));
+                           L.xw, L.xpi, L.r, L.qpart, L.st_trial + j, L.st_cur, S,
+                           sh() ? L.dsum : nullptr));
       });
+      if (sh()) {  // X^T (Pi_new - Pi_old) summed over the ranks, then the factor update
+        allsum(L.dsum, P.q);
+        ck(launch_factor_update(P.q, alpha, tdir, L.dsum, L.xw, L.xpi, L.r, S));
+      }
       return;
     }
     timed(SSNAL_OP_VEC, 8.0 * P.n * 8 + 2.0 * P.n, [&] {
@@ -1094,6 +1245,7 @@ struct Driver {
       gnorm2 = H->scal[0];
     }
     cur = H->st[0];
+    cur_local = cur.in_count;
     lam_cur = cur.lam;
     double dv[4];
     ProjState trial0;
@@ -1166,6 +1318,7 @@ struct Driver {
                      (long long)cur.nfree);
       accept(alpha, j);
       cur = rec;
+      cur_local = rec.in_count;
       ++its;
       advance(cur.nfree, cur.sum_a2_free, true, gnorm2, dv, trial0);
     }
@@ -1183,6 +1336,8 @@ struct Driver {
     if (w0) ck(cudaMemcpyAsync(L.w, w0, nb, cudaMemcpyDeviceToDevice, S));
     else ck(cudaMemsetAsync(L.w, 0, nb, S));
     cold_zero = x0 == nullptr && w0 == nullptr;
+    if (sh() && !P.csr && !qgrad())
+      throw DriverError{SSNAL_E_ARG, "sharded dense solve needs q <= 2048 (factor-space gradient)"};
     if (P.csr) ck(cudaMemsetAsync(L.cj.ticket, 0, sizeof(unsigned int), S));
     else {
       if (L.qpart) ck(cudaMemsetAsync(L.qpart, 0, 256, S));  // accept_q ticket
@@ -1294,25 +1449,28 @@ struct Driver {
 
 }  // namespace
 
-size_t alm_ws_bytes(long long n_phys, long long q, int svr) {
+size_t alm_ws_bytes(long long n_phys, long long q, int svr, int world) {
   size_t total = 0;
   const long long n = svr ? 2 * n_phys : n_phys;
-  carve(nullptr, n, n_phys, q, &total);
+  carve(nullptr, n, n_phys, q, &total, nullptr, world);
   return total;
 }
 
-size_t alm_ws_bytes_csr(const ssnal_csr_operator_t* op) {
+size_t alm_ws_bytes_csr(const ssnal_csr_operator_t* op, int world) {
   size_t total = 0;
-  carve(nullptr, op->n, op->n, op->q, &total, op);
+  carve(nullptr, op->n, op->n, op->q, &total, op, world);
   return total;
 }
 
+// comm == nullptr: one GPU; else the row-sharded driver over comm's ranks (the problem is
+// this rank's slice, d the global right-hand side)
 int alm_solve_dense(const ssnal_dense_problem_t* pb, const ssnal_options_t* opt, const double* x0,
                     const double* w0, double* x_out, ssnal_report_t* rep, void* ws,
                     size_t ws_bytes, ssnal_progress_fn cb, void* ctx, cudaStream_t stream,
-                    const char** err) {
+                    const char** err, const ssnal_comm_t* comm) {
   size_t need = 0;
-  Layout L = carve((char*)ws, pb->n, pb->n_phys, pb->q, &need, pb->csr);
+  const int world = comm ? comm->world : 0;
+  Layout L = carve((char*)ws, pb->n, pb->n_phys, pb->q, &need, pb->csr, world);
   if (ws_bytes < need) {
     *err = "workspace smaller than ssnal_alm_ws_bytes()";
     return SSNAL_E_ARG;
@@ -1329,7 +1487,7 @@ int alm_solve_dense(const ssnal_dense_problem_t* pb, const ssnal_options_t* opt,
     *err = "cudaMemsetAsync of the workspace failed";
     return SSNAL_E_DEVICE;
   }
-  Driver d(*pb, *opt, stream, L, H);
+  Driver d(*pb, *opt, stream, L, H, comm);
   try {
     d.alm_solve(x0, w0, x_out, rep, cb, ctx);
   } catch (const DriverError& e) {

@@ -329,6 +329,7 @@ struct AcceptQArgs {
   // last-CTA fold: xpi += sum_b part[b] (block order), xw += alpha t, r = xw - xpi
   const double* t;
   double *xw, *xpi, *r;
+  double* dsum;  // sharded driver: the fold goes here (all-reduced, then launch_factor_update)
   // accepted trial's projection record -> current record (replaces a D2D memcpy)
   const ProjState* st_src;
   ProjState* st_dst;
@@ -479,11 +480,15 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
       double sum = 0.0;
 #pragma unroll
       for (int w = 0; w < AQ_NT / 32; ++w) sum += wsum[w][tid];
-      const double pi = a.xpi[c] + sum;
-      const double ww = __dadd_rn(a.xw[c], __dmul_rn(a.alpha, a.t[c]));
-      a.xpi[c] = pi;
-      a.xw[c] = ww;
-      a.r[c] = ww - pi;
+      if (a.dsum) {
+        a.dsum[c] = sum;
+      } else {
+        const double pi = a.xpi[c] + sum;
+        const double ww = __dadd_rn(a.xw[c], __dmul_rn(a.alpha, a.t[c]));
+        a.xpi[c] = pi;
+        a.xw[c] = ww;
+        a.r[c] = ww - pi;
+      }
     }
     __syncthreads();
   }
@@ -504,7 +509,7 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
                             double* xp, const double* txj, uint8_t* fr, const uint8_t* tfj,
                             double* s, const double* t, double* xw, double* xpi, double* r,
                             double* part, const ProjState* st_src, ProjState* st_dst,
-                            cudaStream_t stream) {
+                            cudaStream_t stream, double* dsum) {
   if (q > (long long)AQ_NT * AQ_MAXC) return cudaErrorInvalidValue;
   AcceptQArgs a;
   a.g = RowsArgs{A, n_phys, q, lda, rs, svr, nullptr, 0};
@@ -514,7 +519,7 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
   a.ticket = (unsigned int*)part;  // zeroed workspace; reset by the last CTA
   a.touched = (int*)((char*)part + 256);
   a.part = (double*)((char*)part + 256 + 148 * 8 * sizeof(int));
-  a.t = t; a.xw = xw; a.xpi = xpi; a.r = r;
+  a.t = t; a.xw = xw; a.xpi = xpi; a.r = r; a.dsum = dsum;
   a.st_src = st_src; a.st_dst = st_dst;
   const int grid = accept_q_grid(n);
   const int nc = (int)ceil_div(q, (long long)AQ_NT);
@@ -523,6 +528,26 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
   else if (nc <= 2) accept_q_kernel<2><<<grid, AQ_NT, 0, stream>>>(a);
   else if (nc <= 4) accept_q_kernel<4><<<grid, AQ_NT, 0, stream>>>(a);
   else accept_q_kernel<8><<<grid, AQ_NT, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+// sharded: xpi += dsum (the all-reduced X^T (Pi_new - Pi_old)), xw += alpha t, r = xw - xpi
+__global__ void factor_update_kernel(long long q, double alpha, const double* __restrict__ t,
+                                     const double* __restrict__ dsum, double* __restrict__ xw,
+                                     double* __restrict__ xpi, double* __restrict__ r) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= q) return;
+  const double pi = xpi[c] + dsum[c];
+  const double ww = __dadd_rn(xw[c], __dmul_rn(alpha, t[c]));
+  xpi[c] = pi;
+  xw[c] = ww;
+  r[c] = ww - pi;
+}
+
+cudaError_t launch_factor_update(long long q, double alpha, const double* t, const double* dsum,
+                                 double* xw, double* xpi, double* r, cudaStream_t s) {
+  note_launch();
+  factor_update_kernel<<<(unsigned)ceil_div(q, 256LL), 256, 0, s>>>(q, alpha, t, dsum, xw, xpi, r);
   return cudaGetLastError();
 }
 

@@ -97,6 +97,55 @@ struct ProjLaunch {
   const double* slope_den = nullptr;
 };
 
+// ---- row-sharded native driver (dist.cu, comm.cu) -----------------------------------
+// Device state of one trial's multiplier search (the safeguarded Newton of the sharded
+// projection, one all-gather of 5-double records per pass)
+enum { SP_SEARCH = 0, SP_DONE = 1, SP_INFEAS_LOW = -1, SP_INFEAS_HIGH = -2 };
+struct SProj {
+  double lam, lo, hi;
+  int status, passes;
+};
+struct ShardProj {  // one sharded projection call (driver.cu project_sharded)
+  const double *A, *B, *a, *l, *u;
+  double lc, uc, d;
+  long long n;
+  int T;
+  double coef[SSNAL_MAX_TRIALS];
+  double hints[SSNAL_MAX_TRIALS];
+  int has_hints;
+  double hint;
+  const double* slope_num;  // device scalars: first-order start along the ray (or null)
+  const double* slope_den;
+  double* x_out;
+  unsigned char* free_out;
+  const double* ref;
+  const double* base;
+  double base_lam;
+};
+size_t proj_local_ws_bytes(long long n, int T);
+cudaError_t launch_sproj_init(const ShardProj& P, SProj* sp, cudaStream_t s);
+cudaError_t launch_sproj_eval(const ShardProj& P, const SProj* sp, double* part, double* rec,
+                              cudaStream_t s);
+cudaError_t launch_sproj_update(int world, int T, const double* rec_all, double d, SProj* sp,
+                                cudaStream_t s);
+cudaError_t launch_sproj_apply(const ShardProj& P, const SProj* sp, double* part, double* rec,
+                               cudaStream_t s);
+cudaError_t launch_sproj_finish(int world, int T, const double* rec_all, const double* rec_loc,
+                                const SProj* sp, int base_mode, ProjState* st, cudaStream_t s);
+cudaError_t launch_hs_finish(const uint8_t* fm, const double* a, const double* y, long long n,
+                             double beta, const double* add, double alpha, double* out,
+                             const double* sums, cudaStream_t s);
+cudaError_t launch_factor_update(long long q, double alpha, const double* t, const double* dsum,
+                                 double* xw, double* xpi, double* r, cudaStream_t s);
+cudaError_t launch_cg_check_final(const double* sq, double scale, double* cgs, cudaStream_t s);
+int nccl_unique_id(unsigned char* id, const char** err);
+int nccl_comm_create(int world, int rank, const unsigned char* id, ssnal_comm_t* out,
+                     const char** err);
+int loop_group_create(int world, void** group);
+int loop_comm_create(void* group, int rank, ssnal_comm_t* out);
+int loop_group_destroy(void* group);
+int comm_destroy(ssnal_comm_t* c);
+
 int proj_blocks(long long n);
 int proj_wave_trials(long long n, bool first = false);
 size_t proj_ws_bytes(long long n, int T);

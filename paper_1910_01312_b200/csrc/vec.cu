@@ -124,6 +124,17 @@ __global__ void hs_finish_kernel(const uint8_t* __restrict__ fm, const double* _
   }
 }
 
+// out = alpha*add + beta*P y with the sums {a_J'y_J, a_J'a_J} supplied (DEVICE): the
+// sharded driver all-reduces them between the dots and this pass
+cudaError_t launch_hs_finish(const uint8_t* fm, const double* a, const double* y, long long n,
+                             double beta, const double* add, double alpha, double* out,
+                             const double* sums, cudaStream_t stream) {
+  note_launch();
+  hs_finish_kernel<<<stream_blocks(n, 4), SSNAL_NT, 0, stream>>>(fm, a, y, n, beta, add, alpha,
+                                                                  out, sums);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_hs_apply(const uint8_t* fm, const double* a, const double* y, long long n,
                             double beta, const double* add, double alpha, double* out,
                             void* ws, cudaStream_t stream) {

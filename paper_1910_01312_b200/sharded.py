@@ -23,13 +23,24 @@ holds the root (the reference's interpolation, ref projection.py:204-208) or
 moves lambda.  The Newton system is always the q x q factor-space one (the
 Woodbury p x p dual would need the free rows of other ranks).
 
-The solver control flow is solver._Engine / ssn_solve / alm_solve unchanged:
-``ShardedBackend`` makes every reduction global and ``ShardedEngine`` replaces
-the direction assembly.  torch.distributed (NCCL on GPUs, gloo in the CPU tests)
-is the transport only.
+Two engines run this partition:
+
+  * the native sharded driver (csrc/driver.cu through ssnal_alm_solve_sharded): the
+    whole ALM/SsN loop in C++ on the rank's stream, its collectives NCCL all-reduces /
+    all-gathers enqueued on that stream (csrc/comm.cu, a communicator of the library's
+    own, bootstrapped through torch.distributed); the projection search runs on the
+    device (one all-gather of 8-double records per pass).  ``alm_solve`` takes it for
+    NCCL groups.  ``solve_loopback`` runs the same driver with the ranks as threads of
+    one process on one GPU (host-ordered collectives, no kernel waits on another rank):
+    the multi-rank tests of the one-GPU boxes.
+  * the Python mirror (solver._Engine / ssn_solve / alm_solve with ``ShardedBackend``
+    making every reduction global and ``ShardedEngine`` replacing the direction
+    assembly): gloo groups (the CPU tests) and ``SsnOptions(engine="python")``.
 """
 
+import ctypes
 import math
+import threading
 
 import numpy as np
 import torch
@@ -55,6 +66,31 @@ class ShardComm:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.nccl = dist.get_backend(group) == "nccl"
+        self._native = None
+
+    def native(self):
+        """The library's own NCCL communicator over this group (ssnal_comm_t for the
+        native sharded driver), created once: rank 0 makes the unique id, the group
+        broadcasts it, every rank joins with its current device."""
+        if self._native is None:
+            if not self.nccl:
+                raise InputError("the native sharded driver needs an NCCL process group")
+            _lib.load()
+            uid = ctypes.create_string_buffer(_lib.COMM_ID_BYTES)
+            if self.rank == 0:
+                _lib.call("ssnal_nccl_unique_id", uid)
+            box = [bytes(uid.raw)]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(self.group, 0)
+                                       if self.group is not None else 0, group=self.group)
+            comm = _lib.Comm()
+            _lib.call("ssnal_nccl_comm_create", self.world, self.rank, box[0], ctypes.byref(comm))
+            self._native = comm
+        return self._native
+
+    def close(self):
+        if self._native is not None:
+            _lib.load().ssnal_comm_destroy(ctypes.byref(self._native))
+            self._native = None
 
     def all_gather(self, t):
         """(world, *t.shape) tensor of every rank's t (same device as t)."""
@@ -410,7 +446,7 @@ def build_csvc_dual_sharded(features, labels, C, comm, backend=None):
         op = CsrKernelOperator(features, labels=y, backend=be)
     else:
         op = LinearKernelOperator(features, labels=y, backend=be)
-    box = BoxLineSet(a=y, d=0.0, l=np.zeros(n_loc), u=np.full(n_loc, float(C)), backend=be)
+    box = BoxLineSet(a=y, d=0.0, l=0.0, u=float(C), backend=be)
     lo = int(sum(sizes[: comm.rank]))
     return ShardedQpProblem(op, -np.ones(n_loc), box, 0.0, comm,
                             ("csvc", int(sum(sizes)), lo, lo + n_loc))
@@ -429,10 +465,61 @@ def build_svr_dual_sharded(features, targets, C, epsilon, comm, backend=None):
     op = LinearKernelOperator(features, svr_block=True, backend=be)
     c = np.concatenate([epsilon - t, epsilon + t])
     a = np.concatenate([np.ones(n_loc), -np.ones(n_loc)])
-    box = BoxLineSet(a=a, d=0.0, l=np.zeros(2 * n_loc), u=np.full(2 * n_loc, float(C)),
-                     backend=be)
+    box = BoxLineSet(a=a, d=0.0, l=0.0, u=float(C), backend=be)
     lo = int(sum(sizes[: comm.rank]))
     return ShardedQpProblem(op, c, box, 0.0, comm, ("svr", int(sum(sizes)), lo, lo + n_loc))
+
+
+def solve_loopback(problems, alm_opts=None, ssn_opts=None, device=None):
+    """Run the native sharded driver over ``len(problems)`` ranks as host threads of
+    this process on ONE GPU (ssnal_loopback_comm_create): ``problems[r]`` is rank r's
+    slice, built with the single-GPU builders (``build_csvc_dual`` / ``build_svr_dual``
+    on its rows; a nonzero global right-hand side goes in ``constraint.d_global``).
+    Each rank runs on its own stream; a collective drains the caller's stream, meets
+    the other ranks at a host barrier and sums their buffers in rank order -- no
+    kernel waits on another rank, the ranks' kernels only share the GPU.  Returns the
+    per-rank SolveReports (x_opt = the rank's slice)."""
+    from .solver import AlmOptions, SsnOptions, _alm_solve_native
+
+    alm_opts = alm_opts or AlmOptions()
+    ssn_opts = ssn_opts or SsnOptions()
+    world = len(problems)
+    _lib.load()
+    group = ctypes.c_void_p()
+    _lib.call("ssnal_loopback_group_create", world, ctypes.byref(group))
+    comms = []
+    try:
+        for r in range(world):
+            c = _lib.Comm()
+            _lib.call("ssnal_loopback_comm_create", group, r, ctypes.byref(c))
+            comms.append(c)
+        dev = torch.cuda.current_device() if device is None else device
+        out, errs = [None] * world, [None] * world
+
+        def run(r):
+            try:
+                torch.cuda.set_device(dev)
+                with torch.cuda.stream(torch.cuda.Stream(dev)):
+                    out[r] = _alm_solve_native(problems[r], alm_opts, ssn_opts, None, None, None,
+                                               False, comm=comms[r])
+                    torch.cuda.current_stream(dev).synchronize()
+            except BaseException as e:  # noqa: BLE001 -- re-raised below
+                errs[r] = e
+
+        threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for e in errs:
+            if e is not None:
+                raise e
+        return out
+    finally:
+        lib = _lib.load()
+        for c in comms:
+            lib.ssnal_comm_destroy(ctypes.byref(c))
+        lib.ssnal_loopback_group_destroy(group)
 
 
 def gather_solution(problem, x_local):
@@ -449,4 +536,5 @@ def gather_solution(problem, x_local):
 
 
 __all__ = ["ShardComm", "ShardedBackend", "ShardedEngine", "ShardedQpProblem", "shard_range",
-           "build_csvc_dual_sharded", "build_svr_dual_sharded", "gather_solution"]
+           "build_csvc_dual_sharded", "build_svr_dual_sharded", "gather_solution",
+           "solve_loopback"]

@@ -544,9 +544,14 @@ def kkt_residual(x, problem):
 def _native_ok(problem, alm_opts, ssn_opts):
     from .operators import CsrKernelOperator, LinearKernelOperator
 
+    comm = getattr(problem, "comm", None)
+    if comm is not None:
+        # row-sharded: the native sharded driver over NCCL (ssnal_alm_solve_sharded); gloo
+        # groups (CPU tests) and engine="python" run sharded.ShardedEngine
+        return (comm.nccl and ssn_opts.engine == "native"
+                and isinstance(problem.q_op, (CsrKernelOperator, LinearKernelOperator))
+                and alm_opts.eps_seq is _half_powers and alm_opts.delta_seq is _half_powers)
     if isinstance(problem.q_op, CsrKernelOperator):
-        if getattr(problem, "comm", None) is not None:  # row-sharded: sharded.ShardedEngine
-            return False
         if not (alm_opts.eps_seq is _half_powers and alm_opts.delta_seq is _half_powers):
             raise InputError("the sparse operator runs only in the native driver, which uses "
                              "the reference's default eps/delta sequences")
@@ -559,15 +564,20 @@ def _native_ok(problem, alm_opts, ssn_opts):
 _PSI_MODES = {"reference": 0, "stable": 1, "delta": 2}
 
 
-def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_device):
-    """The same loop through the C++ driver (csrc/driver.cu): one C-ABI call."""
+def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_device, comm=None):
+    """The same loop through the C++ driver (csrc/driver.cu): one C-ABI call.  With
+    ``comm`` (a _lib.Comm) the problem is one rank's slice and the row-sharded driver
+    (ssnal_alm_solve_sharded) runs it with the other ranks."""
     import ctypes
 
     be, op, box = problem.backend, problem.q_op, problem.constraint
     n = problem.n
     lib = _lib.load()
     sparse = getattr(op, "kind", "dense") == "csr"
-    if sparse:
+    if comm is not None:
+        nbytes = (lib.ssnal_alm_ws_bytes_csr_sharded(op._cref, comm.world) if sparse else
+                  lib.ssnal_alm_ws_bytes_sharded(op.n_phys, op.q, int(op.svr_block), comm.world))
+    elif sparse:
         nbytes = lib.ssnal_alm_ws_bytes_csr(op._cref)
     else:
         nbytes = lib.ssnal_alm_ws_bytes(op.n_phys, op.q, int(op.svr_block))
@@ -580,7 +590,7 @@ def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_devi
         A=None if sparse else ptr(op.A), n_phys=op.n_phys, q=op.q, lda=op.lda,
         row_sign=ptr(op.row_sign), svr_block=int(op.svr_block), n=n, c=ptr(problem.c),
         a=ptr(box.a_dev), l=ptr(box.l_dev), u=ptr(box.u_dev), l_const=box.l_const,
-        u_const=box.u_const, d=box.d, csr=ctypes.pointer(op.c_op) if sparse else None)
+        u_const=box.u_const, d=float(getattr(box, "d_global", box.d)), csr=ctypes.pointer(op.c_op) if sparse else None)
     opts = _lib.Options(
         sigma0=alm_opts.sigma0, sigma_growth=alm_opts.sigma_growth, sigma_max=alm_opts.sigma_max,
         tol_kkt=alm_opts.tol_kkt, lambda_min_surrogate=alm_opts.lambda_min_surrogate,
@@ -601,8 +611,14 @@ def _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_devi
         cb = _lib.PROGRESS_FN(lambda k, r, s, p, inner, ctx: callback(k, r, s, int(p), inner))
     else:
         cb = _lib.PROGRESS_FN()
-    _lib.call("ssnal_alm_solve_dense", ctypes.byref(prob), ctypes.byref(opts), ptr(x0d), ptr(w0d),
-              ptr(x_out), ctypes.byref(rep), ptr(ws), ws.numel(), cb, None, be.stream())
+    if comm is None:
+        _lib.call("ssnal_alm_solve_dense", ctypes.byref(prob), ctypes.byref(opts), ptr(x0d),
+                  ptr(w0d), ptr(x_out), ctypes.byref(rep), ptr(ws), ws.numel(), cb, None,
+                  be.stream())
+    else:
+        _lib.call("ssnal_alm_solve_sharded", ctypes.byref(prob), ctypes.byref(opts),
+                  ctypes.byref(comm), ptr(x0d), ptr(w0d), ptr(x_out), ctypes.byref(rep), ptr(ws),
+                  ws.numel(), cb, None, be.stream())
     notes = [f"inner solver hit max_inner at outer iteration {k}" for k in range(64)
              if rep.hit_max_inner_mask64 >> k & 1]
     if rep.hit_max_inner_count > len(notes):
@@ -641,7 +657,9 @@ def alm_solve(problem, alm_opts=None, ssn_opts=None, x0=None, w0=None, callback=
     alm_opts = alm_opts or AlmOptions()
     ssn_opts = ssn_opts or SsnOptions()
     if _native_ok(problem, alm_opts, ssn_opts):
-        return _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_device)
+        comm = getattr(problem, "comm", None)
+        return _alm_solve_native(problem, alm_opts, ssn_opts, x0, w0, callback, return_device,
+                                 comm=None if comm is None else comm.native())
     t_start = time.perf_counter()
     eng = problem.engine()
     eng._direct_limit = ssn_opts.direct_solve_threshold

@@ -1,8 +1,10 @@
 """Row-sharded path on the GPU: the shard-local kernels of csrc/dist.cu against the
-single-GPU projection, and the sharded solver at world size 1 over NCCL against the
-native driver and the golden reference runs.  (world > 1 needs more than the one
-GPU a gpurun box has; the multi-rank control flow is covered over gloo in
-tests/test_sharded_cpu.py.)"""
+single-GPU projection; the NATIVE sharded driver (ssnal_alm_solve_sharded) with 2 and 3
+ranks as threads on this one GPU (loopback transport: host-ordered collectives, no
+kernel waits on another rank) and with 1 rank over NCCL, against the single-GPU
+driver, the golden reference runs and an independent KKT certificate; the Python
+mirror of the sharded engine over NCCL.  (The gloo multi-rank runs of the Python
+mirror are tests/test_sharded_cpu.py.)"""
 
 import os
 import socket
@@ -124,7 +126,7 @@ def test_sharded_world1_nccl_matches_native(pkg):
         assert rep.objective == pytest.approx(nat.objective, rel=1e-6)
         # sparse operator (config-3 generator, Zipf columns): rank-local CSR products and
         # the sharded factor-space CG vs the single-GPU native driver
-        cfg = datagen.make_config(3, n=6000, q=1500)
+        cfg = datagen.make_config(3, n=6000, q=3000)
         csr = (cfg["indptr"], cfg["indices"], cfg["data"], cfg["shape"])
         pb = sharded.build_csvc_dual_sharded(csr, cfg["y"], cfg["C"], comm)
         ssn = pkg.SsnOptions(max_inner=200)
@@ -132,7 +134,107 @@ def test_sharded_world1_nccl_matches_native(pkg):
         nat = pkg.alm_solve(pkg.build_csvc_dual(csr, cfg["y"], cfg["C"]),
                             pkg.AlmOptions(tol_kkt=1e-6), ssn)
         assert rep.converged and nat.converged and rep.kkt_residual <= 1e-6
-        assert pb.engine().counters.get("cg_iters", 0) > 0
+        assert pb.native_counters["cg_iters"] > 0  # the native sharded factor-space CG
         assert rep.objective == pytest.approx(nat.objective, rel=1e-6)
+        # the Python mirror of the sharded engine on the same group
+        cfg = datagen.config1(seed=4, n=4000, q=60)
+        pb = sharded.build_csvc_dual_sharded(cfg["A"], cfg["y"], cfg["C"], comm)
+        rep = pkg.alm_solve(pb, pkg.AlmOptions(tol_kkt=1e-6), pkg.SsnOptions(engine="python"))
+        nat = pkg.alm_solve(pkg.build_csvc_dual(cfg["A"], cfg["y"], cfg["C"]),
+                            pkg.AlmOptions(tol_kkt=1e-6))
+        assert rep.converged and rep.objective == pytest.approx(nat.objective, rel=1e-6)
+        comm.close()
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ native sharded, loopback
+def _assemble(kind, reps, sizes):
+    """Global dual vector (reference ordering) from the ranks' slices."""
+    parts = [np.asarray(r.x_opt) for r in reps]
+    if kind == "csvc":
+        return np.concatenate(parts)
+    return np.concatenate([np.concatenate([p[:m] for p, m in zip(parts, sizes)]),
+                           np.concatenate([p[m:] for p, m in zip(parts, sizes)])])
+
+
+def _check_ranks_agree(reps):
+    """Every rank holds the same reduced scalars: identical reports."""
+    for r in reps[1:]:
+        assert (r.kkt_residual, r.objective, r.outer_iters, r.total_inner_iters,
+                r.unbounded_support_count) == (reps[0].kkt_residual, reps[0].objective,
+                                               reps[0].outer_iters, reps[0].total_inner_iters,
+                                               reps[0].unbounded_support_count)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_native_sharded_loopback_csvc(pkg, world):
+    from paper_1910_01312_b200 import datagen, sharded
+
+    cfg = datagen.config1(seed=11, n=12000, q=80)
+    A, y, C = cfg["A"], cfg["y"], cfg["C"]
+    single = pkg.build_csvc_dual(A, y, C)
+    nat = pkg.alm_solve(single, pkg.AlmOptions(tol_kkt=1e-6))
+    cuts = [sharded.shard_range(A.shape[0], r, world) for r in range(world)]
+    probs = [pkg.build_csvc_dual(A[lo:hi], y[lo:hi], C) for lo, hi in cuts]
+    reps = sharded.solve_loopback(probs, pkg.AlmOptions(tol_kkt=1e-6))
+    _check_ranks_agree(reps)
+    rep = reps[0]
+    assert rep.converged and rep.kkt_residual <= 1e-6
+    assert rep.objective == pytest.approx(nat.objective, rel=1e-8)
+    x = _assemble("csvc", reps, [hi - lo for lo, hi in cuts])
+    assert pkg.kkt_residual(x, single) <= 1e-6  # certified by the single-GPU operator
+    assert abs(float(np.dot(y, x))) <= 1e-9 * (1 + np.abs(x).sum())
+    assert x.min() >= 0.0 and x.max() <= C
+    np.testing.assert_allclose(x, nat.x_opt, atol=1e-5)
+    assert rep.unbounded_support_count == nat.unbounded_support_count
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_native_sharded_loopback_svr(pkg, world):
+    from paper_1910_01312_b200 import datagen, sharded
+
+    cfg = datagen.make_config(4, n=20000, q=50)
+    A, t = cfg["A"], cfg["t"]
+    single = pkg.build_svr_dual(A, t, cfg["C"], cfg["epsilon"])
+    nat = pkg.alm_solve(single, pkg.AlmOptions(tol_kkt=1e-6))
+    cuts = [sharded.shard_range(A.shape[0], r, world) for r in range(world)]
+    probs = [pkg.build_svr_dual(A[lo:hi], t[lo:hi], cfg["C"], cfg["epsilon"]) for lo, hi in cuts]
+    reps = sharded.solve_loopback(probs, pkg.AlmOptions(tol_kkt=1e-6))
+    _check_ranks_agree(reps)
+    rep = reps[0]
+    assert rep.converged and rep.kkt_residual <= 1e-6
+    assert rep.objective == pytest.approx(nat.objective, rel=1e-8)
+    x = _assemble("svr", reps, [hi - lo for lo, hi in cuts])
+    assert pkg.kkt_residual(x, single) <= 1e-6
+    np.testing.assert_allclose(x, nat.x_opt, atol=1e-5)
+
+
+@pytest.mark.parametrize("q", [1500, 3000])
+def test_native_sharded_loopback_csr(pkg, q):
+    """Config-3 generator (Zipf columns): q <= 2048 runs the all-reduced q x q direct
+    system, q > 2048 the sharded factor-space Jacobi CG."""
+    from paper_1910_01312_b200 import datagen, sharded
+
+    cfg = datagen.make_config(3, n=8000, q=q)
+    indptr, indices, data = cfg["indptr"], cfg["indices"], cfg["data"]
+    y, C = cfg["y"], cfg["C"]
+    single = pkg.build_csvc_dual((indptr, indices, data, cfg["shape"]), y, C)
+    ssn = pkg.SsnOptions(max_inner=200)
+    nat = pkg.alm_solve(single, pkg.AlmOptions(tol_kkt=1e-6), ssn)
+    world = 2
+    cuts = [sharded.shard_range(len(y), r, world) for r in range(world)]
+    probs = []
+    for lo, hi in cuts:
+        ip = np.asarray(indptr[lo:hi + 1]) - indptr[lo]
+        sl = slice(int(indptr[lo]), int(indptr[hi]))
+        probs.append(pkg.build_csvc_dual((ip, indices[sl], data[sl], (hi - lo, q)), y[lo:hi], C))
+    reps = sharded.solve_loopback(probs, pkg.AlmOptions(tol_kkt=1e-6), ssn)
+    _check_ranks_agree(reps)
+    rep = reps[0]
+    assert rep.converged and rep.kkt_residual <= 1e-6
+    assert rep.objective == pytest.approx(nat.objective, rel=1e-6)
+    x = _assemble("csvc", reps, [hi - lo for lo, hi in cuts])
+    assert pkg.kkt_residual(x, single) <= 1e-6
+    if q > 2048:
+        assert probs[0].native_counters["cg_iters"] > 0
