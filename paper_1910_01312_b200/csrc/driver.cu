@@ -154,6 +154,14 @@ static double cg_eta_cap() {
                                                           : SPARSE_CG_ETA;
   return v;
 }
+// CG stopping rule.  0: the TRUE Newton residual of Algorithm 3 Step 1 (an n-row product
+// per check).  1: the reference's rule (solver.py:151-172, 253: absolute residual of its
+// (I/sigma + Q_JJ + ..) v = g_J system <= target), which in factor space is
+// ||P_J X_J r_t|| <= target -- the true residual is sigma X X_J^T of that vector.
+static int cg_rule() {
+  static const int v = std::getenv("SSNAL_CG_RULE") ? std::atoi(std::getenv("SSNAL_CG_RULE")) : 0;
+  return v;
+}
 // max / mean column sum of squares above which the factor-space Jacobi PCG is used
 constexpr double HOT_COLUMN_SPREAD = 50.0;
 
@@ -500,13 +508,20 @@ struct Driver {
                           S));
         ck(launch_cg_dir(q, L.cg_z, L.cg_pv, L.cgs, S));
       }
-      gram_apply(L.cg_r, L.tq);
-      ck(launch_csr_xd(op, nullptr, P.n_phys, L.tq, L.tmp, S));
-      if (sh()) {  // ||X (.)||^2 is a sum over the slots: all-reduced before the test
-        dots({{L.tmp, nullptr}}, L.cgs + 10, P.n);
-        ck(launch_cg_check_final(L.cgs + 10, sigma, L.cgs, S));
+      if (cg_rule() == 1) {
+        xd_dot(p, L.cg_r);
+        ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
+        dots({{L.cg_w, L.cg_w}}, L.cgs + 10, p);
+        ck(launch_cg_check_final(L.cgs + 10, 1.0, L.cgs, S));
       } else {
-        ck(launch_cg_check(P.n, L.tmp, sigma, L.cgs, L.cg_part, S));
+        gram_apply(L.cg_r, L.tq);
+        ck(launch_csr_xd(op, nullptr, P.n_phys, L.tq, L.tmp, S));
+        if (sh()) {  // ||X (.)||^2 is a sum over the slots: all-reduced before the test
+          dots({{L.tmp, nullptr}}, L.cgs + 10, P.n);
+          ck(launch_cg_check_final(L.cgs + 10, sigma, L.cgs, S));
+        } else {
+          ck(launch_cg_check(P.n, L.tmp, sigma, L.cgs, L.cg_part, S));
+        }
       }
       ck(cudaMemcpyAsync(H->cg, L.cgs, sizeof(double) * 8, cudaMemcpyDeviceToHost, S));
       ck(cudaStreamSynchronize(S));
@@ -541,6 +556,14 @@ struct Driver {
       }
       // Newton residual of the direction built from y (Algorithm 3 Step 1 test):
       // (Q + sigma Q P~ Q) d + Q s = sigma^2 X X_J^T P Q_JJ P r
+      if (cg_rule() == 1) {
+        ck(launch_cg_check_final(L.cgs + 3, 1.0, L.cgs, S));
+        ck(cudaMemcpyAsync(H->cg, L.cgs, sizeof(double) * 8, cudaMemcpyDeviceToHost, S));
+        ck(cudaStreamSynchronize(S));
+        ++syncs;
+        if (H->cg[5] != 0.0) break;
+        continue;
+      }
       dots({{L.cg_aJ, L.cg_r}}, L.cgs + 7, p);
       ck(launch_cg_project(p, L.cg_r, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
       ck(launch_cscj_xt(op, L.cj, L.cg_w, L.tq, L.csc_part, S));
