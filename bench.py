@@ -200,9 +200,17 @@ def build_problem(P, cfg, A=None):
 
 
 def ssn_options(P, cfg):
-    # the large sparse configs need more inner Newton steps than the reference default 50
-    # at sigma >= 3125
-    return P.SsnOptions(max_inner=200) if "indptr" in cfg else P.SsnOptions()
+    # sparse configs: max_inner=200 (datagen.solve_options)
+    from paper_1910_01312_b200 import datagen
+
+    return P.SsnOptions(**datagen.solve_options(cfg)["ssn"])
+
+
+def alm_options(P, cfg, **kw):
+    # sparse configs: sigma_max=625 (datagen.solve_options)
+    from paper_1910_01312_b200 import datagen
+
+    return P.AlmOptions(tol_kkt=TOL, **datagen.solve_options(cfg)["alm"], **kw)
 
 
 def oracle_problem(cfg):
@@ -223,10 +231,42 @@ def cpu_oracle_solve(cfg):
 
     O.set_psi_mode("delta")
     op, c, bl = oracle_problem(cfg)
-    ssn = O.SsnOpts(newton="factor", max_inner=200 if "indptr" in cfg else 50)
+    from paper_1910_01312_b200 import datagen
+
+    opts = datagen.solve_options(cfg)
+    ssn = O.SsnOpts(newton="factor", **opts["ssn"])
     t0 = time.perf_counter()
-    rep = O.alm_solve(op, c, bl, O.AlmOpts(tol_kkt=TOL), ssn)
+    rep = O.alm_solve(op, c, bl, O.AlmOpts(tol_kkt=TOL, **opts["alm"]), ssn)
     return time.perf_counter() - t0, rep
+
+
+# sparse configs: the oracle needs ~27 min (config 2, 8 cores) or hours (config 3) for a full
+# solve, so the CPU legs time the SAME generator at 1/CPU_SAMPLE_DIV of n and q
+CPU_SAMPLE_DIV = {2: 10, 3: 80}
+
+
+def cpu_baseline_solve(args):
+    """(seconds, report, sample description) of the CPU leg for args.config: the full
+    workload for the dense configs, a 1/CPU_SAMPLE_DIV-scale instance for the sparse."""
+    from paper_1910_01312_b200 import datagen
+
+    what = ("numpy oracle = the reference path restated: factor-space Newton system, delta "
+            "line search; OpenBLAS/scipy threads")
+    div = CPU_SAMPLE_DIV.get(args.config)
+    if div is None or getattr(args, "full_cpu_baseline", False):
+        secs, rep = cpu_oracle_solve(make_cfg(args.config))
+        return secs, rep, (f"one full solve of the workload ({what}); longer than the 10-30 s "
+                           "sample guidance because no bounded sub-sample of an ALM solve "
+                           "scales to the full one")
+    full = datagen.make_config.__globals__["CONFIGS"][args.config]
+    import inspect
+
+    sig = inspect.signature(full).parameters
+    n, q = sig["n"].default // div, sig["q"].default // div
+    secs, rep = cpu_oracle_solve(datagen.make_config(args.config, n=n, q=q))
+    return secs, rep, (f"one full solve of a 1/{div}-scale instance of the workload's generator "
+                       f"(n = {n}, q = {q}; {what}); the full-size oracle solve takes tens of "
+                       "minutes to hours")
 
 
 def config_dict(args, cfg, world, n=None, q=None):
@@ -241,6 +281,11 @@ def config_dict(args, cfg, world, n=None, q=None):
         d.update({"n": int(cfg["A"].shape[0]), "q": int(cfg["A"].shape[1])})
     if cfg["task"] == "svr":
         d.update({"epsilon": cfg["epsilon"], "dual_slots": 2 * d["n"]})
+    from paper_1910_01312_b200 import datagen
+
+    so = datagen.solve_options(cfg)
+    if so["alm"] or so["ssn"]:  # non-default reference options (sparse configs)
+        d["options"] = {**so["alm"], **so["ssn"]}
     return d
 
 
@@ -249,7 +294,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     cfg = make_cfg(args.config)
-    secs, rep = cpu_oracle_solve(cfg)
+    secs, rep, sample = cpu_baseline_solve(args)
     cores = _threads()
     line = {
         "impl": "reference", "metric": METRICS[args.config], "value": secs, "unit": "s",
@@ -259,10 +304,7 @@ def run_reference(args, rank, world):
         "data": "synthetic (seeded, BASELINE config shapes and distributions)",
         "config": config_dict(args, cfg, world),
         "cpu_baseline": {"value": secs, "unit": "s", "cores": cores, "kind": "port",
-                         "sample": "one full solve of the workload (numpy oracle = the "
-                                   "reference path restated: factor-space Newton system, "
-                                   "delta line search; OpenBLAS threads); a full solve per "
-                                   "step, so one step runs"},
+                         "sample": sample + "; a full solve per step, so one step runs"},
         "e2e": {"value": secs, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "result": {"kkt": rep["kkt_residual"], "objective": rep["objective"],
                    "outer": rep["outer_iters"], "inner": rep["total_inner_iters"],
@@ -281,6 +323,12 @@ ROOF = {
     "chol": ("latency", "TFLOP/s", "chol_cluster_kernel (q x q Cholesky)"),
     "newton_system": ("hbm", "GB/s", "compaction / p-space system / CG"),
     "vector": ("hbm", "GB/s", "accept_q / hs_finish_dots / dots"),
+}
+ROOF_SPARSE = {
+    "newton_system": ("hbm", "GB/s", "matrix-free CG of the reduced Newton system: csrj_xd_dot(_hot)_kernel "
+                      "(X_J d) + cscj_xt_kernel (X_J^T w) SpMV pair + cg_update_kernel"),
+    "dense_x": ("hbm", "GB/s", "csr_xd_kernel (X d over all rows)"),
+    "dense_xt": ("hbm", "GB/s", "csc_xt_kernel (X^T v on the CSC plan)"),
 }
 NCU_FILES = {"dense_x": "r2_ncu_c4_stream_xd_kernel.txt", "gram": "r2_ncu_c4_gram_kernel.txt"}
 
@@ -350,7 +398,7 @@ def run_ours(args, rank, world, local_rank):
     dense = "indptr" not in cfg
     A_host = torch.from_numpy(lcfg["A"]).pin_memory() if dense else None
     problem = build(A_host.to("cuda") if dense else None)
-    opts = P.AlmOptions(tol_kkt=TOL)
+    opts = alm_options(P, cfg)
     ssn = ssn_options(P, cfg)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -456,7 +504,8 @@ def run_ours(args, rank, world, local_rank):
                   "TFLOPs": flops / secs / 1e12 if secs and flops else None}
     if ops:
         dom = max(ops, key=lambda k: ops[k]["s"])
-        bound, unit, kname = ROOF.get(dom, ("hbm", "GB/s", dom))
+        table = {**ROOF, **ROOF_SPARSE} if "indptr" in cfg else ROOF
+        bound, unit, kname = table.get(dom, ("hbm", "GB/s", dom))
         calls, secs, nbytes, flops = kern[dom]
         if bound == "tensor" or unit == "TFLOP/s":
             achieved = flops / secs / 1e12 if secs else 0.0
@@ -479,12 +528,9 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_cpu_baseline:
         # the FULL workload: no sub-sample of an ALM solve scales to it (config 4 at 1/10 of
         # the rows took 86 s on 16 cores, the full problem 93 s -- different iterates)
-        secs, ref = cpu_oracle_solve(cfg)
+        secs, ref, sample = cpu_baseline_solve(args)
         cpu = {"value": secs, "unit": "s", "cores": _threads(), "kind": "port",
-               "sample": "one full solve of the workload (numpy oracle = the reference path "
-                         "restated, factor-space Newton route, delta line search; OpenBLAS "
-                         "threads); longer than the 10-30 s sample guidance because no "
-                         "bounded sub-sample of an ALM solve scales to the full one",
+               "sample": sample,
                "kkt": ref["kkt_residual"], "objective": ref["objective"],
                "outer": ref["outer_iters"], "inner": ref["total_inner_iters"]}
     last = reps[-1]
@@ -545,6 +591,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--full-cpu-baseline", action="store_true",
+                    help="sparse configs: time the oracle on the full workload, not the 1/N-scale sample")
     ap.add_argument("--sharded", action="store_true",
                     help="row-sharded engine even at N = 1 (checks the multi-GPU path on one GPU)")
     args = ap.parse_args()

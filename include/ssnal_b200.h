@@ -194,7 +194,15 @@ typedef struct ssnal_csr_operator_t {
   int64_t nfold;           /* split columns                                         */
   const int32_t* fold_col; const int32_t* fold_beg;   /* fold_beg: nfold + 1 entries  */
   int64_t nslots;          /* partial slots (workspace doubles for ssnal_csr_xt)    */
+  /* hot-column staging of the CG's X_J d (optional study path, used only with
+   * SSNAL_CSR_HOT=1 in the environment; nhot = 0 disables it): the nhot
+   * (<= SSNAL_CSR_HOT_MAX) most populated columns, hot_cols[k] = column of rank k,
+   * hot_rank[col] = rank or -1.  The packed J rows store ~rank for hot columns and the
+   * product reads their d entries from a shared-memory copy instead of gathering.    */
+  int64_t nhot;
+  const int32_t* hot_cols; const int32_t* hot_rank;   /* nhot / q entries (DEVICE)   */
 } ssnal_csr_operator_t;
+#define SSNAL_CSR_HOT_MAX 4096
 
 /* out[r] = row_sign[i] * A[i,:] . d for i = rows[r] (rows NULL: i = r), r < nrows */
 int ssnal_csr_xd(const ssnal_csr_operator_t* op, const int32_t* rows, int64_t nrows,

@@ -72,7 +72,8 @@ class CsrOperator(ctypes.Structure):
                 ("colptr", _P), ("rowidx", _P), ("valt", _P), ("row_sign", _P),
                 ("nseg", ctypes.c_int64), ("seg_beg", _P), ("seg_end", _P), ("seg_col", _P),
                 ("seg_slot", _P), ("nfold", ctypes.c_int64), ("fold_col", _P), ("fold_beg", _P),
-                ("nslots", ctypes.c_int64)]
+                ("nslots", ctypes.c_int64),
+                ("nhot", ctypes.c_int64), ("hot_cols", _P), ("hot_rank", _P)]
 
 
 class DenseProblem(ctypes.Structure):

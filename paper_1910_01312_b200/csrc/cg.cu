@@ -9,6 +9,10 @@
 #include "common.cuh"
 #include "ssnal_internal.h"
 
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 namespace ssnal {
 
 int stream_blocks(long long n, int per_thread);
@@ -250,6 +254,105 @@ cudaError_t launch_cg_dir(long long p, const double* r, double* pv, const double
   note_launch();
   cg_dir_kernel<<<cg_blocks(p), SSNAL_NT, 0, s>>>(p, r, pv, cgs);
   return cudaGetLastError();
+}
+
+// One CG iteration's vector work in ONE cooperative launch (replaces cg_ap + cg_step +
+// cg_dir: three launches and two device-wide reductions per iteration):
+//   A: Ap = pv + sigma (zq - c aJ), c = cgs[DOT] / asa;  pAp          -> grid sync
+//   B: alpha = rz / pAp; y += alpha pv; r -= alpha Ap; z = Dinv r; rz', rr -> grid sync
+//   C: beta = rz' / rz;  pv = z + beta pv
+// Every block folds the same per-block partials in block order, so alpha and beta are
+// identical in every block and the sums are the unfused kernels' (same grid, same order).
+namespace cgrp = cooperative_groups;
+static constexpr int CGU_NT = 512;
+static constexpr int CGU_MAX_GRID = 512;  // 3 * CGU_MAX_GRID partial doubles (cg_part_doubles)
+__global__ void __launch_bounds__(CGU_NT) cg_update_kernel(
+    long long p, double* __restrict__ y, double* __restrict__ r, double* __restrict__ pv,
+    const double* __restrict__ zq, const double* __restrict__ aJ, double asa, double sigma,
+    const double* __restrict__ dinv, double* __restrict__ Ap, double* __restrict__ z, double* cgs,
+    double* part) {
+  cgrp::grid_group grid = cgrp::this_grid();
+  __shared__ double red[2 * 32];
+  if (cgs[CG_DONE] != 0.0) return;  // uniform over the grid: set only by a finished launch
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const double c = asa != 0.0 ? cgs[CG_DOT] / asa : 0.0;
+  const double rz_old = cgs[CG_RZ];
+  double a1[1] = {0.0};
+  for (long long i = i0; i < p; i += stride) {
+    const double a = pv[i] + sigma * (zq[i] - c * aJ[i]);
+    Ap[i] = a;
+    a1[0] = fma(pv[i], a, a1[0]);
+  }
+  const int o1[1] = {0};
+  const int ops[2] = {0, 0};
+  block_reduce<1>(a1, o1, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = a1[0];
+  grid.sync();
+  block_fold_partials<1>(part, gridDim.x, 1, o1, a1, red);
+  __shared__ double bc[2];
+  if (threadIdx.x == 0) bc[0] = a1[0];
+  __syncthreads();
+  const double pap = bc[0];
+  const double alpha = pap > 0.0 ? rz_old / pap : 0.0;
+  double acc[2] = {0.0, 0.0};
+  for (long long i = i0; i < p; i += stride) {
+    y[i] = fma(alpha, pv[i], y[i]);
+    const double ri = fma(-alpha, Ap[i], r[i]);
+    r[i] = ri;
+    const double zi = dinv ? ri * dinv[i] : ri;
+    if (dinv) z[i] = zi;
+    acc[0] = fma(ri, zi, acc[0]);
+    acc[1] = fma(ri, ri, acc[1]);
+  }
+  block_reduce<2>(acc, ops, red);
+  double* part2 = part + gridDim.x;
+  if (threadIdx.x == 0) {
+    part2[2 * blockIdx.x] = acc[0];
+    part2[2 * blockIdx.x + 1] = acc[1];
+  }
+  grid.sync();
+  block_fold_partials<2>(part2, gridDim.x, 2, ops, acc, red);
+  if (threadIdx.x == 0) {
+    bc[0] = acc[0];
+    bc[1] = acc[1];
+  }
+  __syncthreads();
+  const double rz = bc[0];
+  const bool stop = !(pap > 0.0) || !(rz > 0.0);  // exact solve / breakdown
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    cgs[CG_PAP] = pap;
+    cgs[CG_BETA] = rz_old > 0.0 ? rz / rz_old : 0.0;
+    cgs[CG_RZ] = rz;
+    cgs[CG_RR] = bc[1];
+    cgs[CG_IT] += 1.0;
+    if (stop) cgs[CG_DONE] = 1.0;
+  }
+  if (stop) return;
+  const double beta = rz_old > 0.0 ? rz / rz_old : 0.0;
+  const double* zz = dinv ? z : r;
+  for (long long i = i0; i < p; i += stride) pv[i] = fma(beta, pv[i], zz[i]);
+}
+
+static int cg_update_grid(long long p) {
+  static DeviceCache cache;
+  const int cap = per_device(cache, [](int dev) {
+    int sms = 148, per = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_update_kernel, CGU_NT, 0);
+    return std::min(CGU_MAX_GRID, sms * std::max(1, std::min(per, 2)));
+  });
+  return (int)std::max(1LL, std::min((long long)cap, ceil_div(p, (long long)CGU_NT)));
+}
+
+// part: 3 * grid doubles (cg_part_doubles covers it)
+cudaError_t launch_cg_update(long long p, double* y, double* r, double* pv, const double* zq,
+                             const double* aJ, double asa, double sigma, const double* dinv,
+                             double* Ap, double* z, double* cgs, double* part, cudaStream_t s) {
+  note_launch();
+  void* args[] = {&p, &y, &r, &pv, &zq, &aJ, &asa, &sigma, &dinv, &Ap, &z, &cgs, &part};
+  return cudaLaunchCooperativeKernel((void*)cg_update_kernel, dim3(cg_update_grid(p)),
+                                     dim3(CGU_NT), args, 0, s);
 }
 
 cudaError_t launch_scatter_zero(const int32_t* rows, long long p, double* dst, cudaStream_t s) {

@@ -158,6 +158,23 @@ static double cg_eta_cap() {
 // per check).  1: the reference's rule (solver.py:151-172, 253: absolute residual of its
 // (I/sigma + Q_JJ + ..) v = g_J system <= target), which in factor space is
 // ||P_J X_J r_t|| <= target -- the true residual is sigma X X_J^T of that vector.
+cudaError_t launch_cg_update(long long p, double* y, double* r, double* pv, const double* zq,
+                             const double* aJ, double asa, double sigma, const double* dinv,
+                             double* Ap, double* z, double* cgs, double* part, cudaStream_t s);
+// SSNAL_CG_FUSED=0: the unfused cg_ap / cg_step / cg_dir launches (A/B knob)
+static bool cg_fused() {
+  static const bool v = !(std::getenv("SSNAL_CG_FUSED") && std::atoi(std::getenv("SSNAL_CG_FUSED")) == 0);
+  return v;
+}
+// SSNAL_CG_ADAPT=0: run the true-residual test after every batch.  Default: after the
+// first test, a batch is followed by the test only when the recurrence residual predicts
+// it may pass (||r||^2 rho^2 <= 4 tol^2 with rho^2 = true^2 / ||r||^2 from the last test),
+// or after 3 skipped batches -- the test costs a full Gram product plus an n-row X
+// product, ~15 % of a 16-iteration batch.
+static bool cg_adapt() {
+  static const bool v = !(std::getenv("SSNAL_CG_ADAPT") && std::atoi(std::getenv("SSNAL_CG_ADAPT")) == 0);
+  return v;
+}
 static int cg_rule() {
   static const int v = std::getenv("SSNAL_CG_RULE") ? std::atoi(std::getenv("SSNAL_CG_RULE")) : 0;
   return v;
@@ -261,7 +278,9 @@ struct Layout {
   void* ws_plocal;
 };
 
-size_t cg_part_doubles(long long n) { return 2 * (size_t)stream_blocks(n, 4) + 8; }
+// per-block partials of the CG kernels: the step kernels' 2 per block, the fused update's
+// 3 per block on at most 512 blocks (cg.cu CGU_MAX_GRID)
+size_t cg_part_doubles(long long n) { return 2 * (size_t)stream_blocks(n, 4) + 8 + 3 * 512; }
 
 Layout carve(char* base, long long n, long long n_phys, long long q, size_t* total,
              const ssnal_csr_operator_t* csr = nullptr, int world = 0) {
@@ -479,6 +498,33 @@ struct Driver {
     allsum(out, P.q);
   }
 
+  // Gate of the CG's true-residual test (cg_adapt): rho2 = (true residual)^2 / ||r||^2 at
+  // the last test, rr0 the recurrence ||r||^2 read just before it.
+  struct CheckGate {
+    double rho2 = -1.0, rr0 = 0.0;
+    int skipped = 0;
+  };
+  // after a batch: 1 = run the test now, 0 = skip it (next batch), -1 = the CG flagged
+  // done (breakdown / exact solve).  Reads the device scalars (one small sync).
+  int gate_peek(CheckGate& g, bool more) {
+    if (!cg_adapt()) return 1;
+    ck(cudaMemcpyAsync(H->cg, L.cgs, sizeof(double) * 8, cudaMemcpyDeviceToHost, S));
+    ck(cudaStreamSynchronize(S));
+    ++syncs;
+    if (H->cg[5] != 0.0) return -1;
+    g.rr0 = H->cg[3];
+    if (g.rho2 > 0.0 && more && g.skipped < 3 && g.rr0 * g.rho2 > 4.0 * H->cg[4]) {
+      ++g.skipped;
+      return 0;
+    }
+    return 1;
+  }
+  // after a test that did not pass: H->cg[3] holds the true residual squared
+  void gate_update(CheckGate& g) {
+    g.rho2 = g.rr0 > 0.0 ? H->cg[3] / g.rr0 : -1.0;
+    g.skipped = 0;
+  }
+
   // Factor-space Jacobi-preconditioned CG for p >= q (Zipf-hot columns make the
   // sample-space spectrum spread; column scaling flattens it):
   //   (I_q + sigma X_J^T P_J X_J) t = -X^T s,  D = diag(.)  (ref solver.py:151-172 role)
@@ -500,13 +546,28 @@ struct Driver {
       ck(launch_cg_project(p, L.cg_zq, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
       cscj_xt(L.cg_w, out);
     };
+    CheckGate gate;
     for (int it = 0; it < max_it;) {
       for (int b = 0; b < cg_batch() && it < max_it; ++b, ++it) {
+        if (cg_fused()) {
+          // X_J^T P zq = X_J^T zq - (a_J.zq / a'a) u with u = X_J^T a_J (the Jacobi setup's):
+          // no projection pass, and the vector updates of the iteration in one launch
+          xd_dot(p, L.cg_pv);
+          cscj_xt(L.cg_zq, L.tq);
+          ck(launch_cg_update(q, L.cg_y, L.cg_r, L.cg_pv, L.tq, L.cg_u, asa, sigma, L.cg_d,
+                              L.cg_Ap, L.cg_z, L.cgs, L.cg_part, S));
+          continue;
+        }
         gram_apply(L.cg_pv, L.tq);
         ck(launch_cg_ap(q, L.cg_pv, L.tq, L.tq, 0.0, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
         ck(launch_cg_step(q, L.cg_y, L.cg_r, L.cg_pv, L.cg_Ap, L.cg_d, L.cg_z, L.cgs, L.cg_part,
                           S));
         ck(launch_cg_dir(q, L.cg_z, L.cg_pv, L.cgs, S));
+      }
+      if (cg_rule() == 0) {
+        const int g = gate_peek(gate, it < max_it);
+        if (g < 0) break;
+        if (g == 0) continue;
       }
       if (cg_rule() == 1) {
         xd_dot(p, L.cg_r);
@@ -527,6 +588,7 @@ struct Driver {
       ck(cudaStreamSynchronize(S));
       ++syncs;
       if (H->cg[5] != 0.0) break;
+      gate_update(gate);
     }
     cg_report(p);
     ck(cudaMemcpyAsync(L.t, L.cg_y, sizeof(double) * q, cudaMemcpyDeviceToDevice, S));
@@ -545,10 +607,16 @@ struct Driver {
     // stalls; the matrix-free path instead solves tighter from the start
     ck(launch_cg_init(p, L.cg_b, L.cg_y, L.cg_r, L.cg_pv, nullptr, g2_dev,
                       std::min(O.eta, cg_eta_cap()), O.tau, L.cgs, L.cg_part, S));
+    CheckGate gate;
     for (int it = 0; it < max_it;) {
       for (int b = 0; b < cg_batch() && it < max_it; ++b, ++it) {
         ck(launch_cscj_xt(op, L.cj, L.cg_pv, L.tq, L.csc_part, S));
         xd_dot(p, L.tq);
+        if (cg_fused()) {
+          ck(launch_cg_update(p, L.cg_y, L.cg_r, L.cg_pv, L.cg_zq, L.cg_aJ, asa, sigma, nullptr,
+                              L.cg_Ap, nullptr, L.cgs, L.cg_part, S));
+          continue;
+        }
         ck(launch_cg_ap(p, L.cg_pv, L.cg_zq, L.cg_aJ, asa, sigma, L.cg_Ap, L.cgs, L.cg_part, S));
         ck(launch_cg_step(p, L.cg_y, L.cg_r, L.cg_pv, L.cg_Ap, nullptr, nullptr, L.cgs, L.cg_part,
                           S));
@@ -564,6 +632,11 @@ struct Driver {
         if (H->cg[5] != 0.0) break;
         continue;
       }
+      {
+        const int g = gate_peek(gate, it < max_it);
+        if (g < 0) break;
+        if (g == 0) continue;
+      }
       dots({{L.cg_aJ, L.cg_r}}, L.cgs + 7, p);
       ck(launch_cg_project(p, L.cg_r, L.cg_aJ, L.cgs + 7, asa, L.cg_w, S));
       ck(launch_cscj_xt(op, L.cj, L.cg_w, L.tq, L.csc_part, S));
@@ -576,6 +649,7 @@ struct Driver {
       ck(cudaStreamSynchronize(S));
       ++syncs;
       if (H->cg[5] != 0.0) break;
+      gate_update(gate);
     }
     cg_report(p);
     // w = P_J y, t = -g_r + sigma X^T scatter(w)
@@ -615,6 +689,15 @@ struct Driver {
     ck(launch_cscj_build(*P.csr, L.fr, L.J, pl, L.cj, S));  // X_J's CSC for every CG product
     const bool ok = (!sh() && p < P.q && !hot_columns()) ? cg_direction(p, asa, g2_dev, max_it)
                                                          : cg_direction_q(pl, asa, g2_dev, max_it);
+    if (O.profile) {
+      // algorithmic bytes of the CG phase (profiled solves only: one extra 8-byte read):
+      // per iteration the two products stream nnz(X_J) (value, index) pairs each, 12 B,
+      // and the vector updates make ~9 passes over the system vectors
+      int64_t nnzj = 0;
+      ck(cudaMemcpyAsync(&nnzj, L.cj.rptr + pl, sizeof nnzj, cudaMemcpyDeviceToHost, S));
+      ck(cudaStreamSynchronize(S));
+      op_bytes[SSNAL_OP_NEWTON] += H->cg[6] * (24.0 * (double)nnzj + 72.0 * (double)std::min<long long>(p, P.q));
+    }
     if (!ok && can_direct) {
       ++cg_fallbacks;
       sparse_direct(p, pl, asa);

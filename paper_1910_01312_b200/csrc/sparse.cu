@@ -417,8 +417,8 @@ __global__ void index_map_kernel(const int32_t* __restrict__ J, long long p,
 // Zipf data leave most of the ~1e6 column segments with 0-3 kept entries, where a
 // warp per segment ran at ~1/10 of the HBM rate; here every lane streams CH_E entries.
 // Fixed chunking => fixed summation order: deterministic run to run.
-static constexpr int CH_E = 8;
-static constexpr int CH = 32 * CH_E;
+static constexpr int CH_E = 4;           // smallest entries-per-lane instantiation:
+static constexpr int CH = 32 * CH_E;     // sizes the per-chunk workspace arrays
 
 __device__ __forceinline__ void seg_write(int s, double v, const int32_t* __restrict__ seg_col,
                                           const int32_t* __restrict__ seg_slot,
@@ -428,8 +428,15 @@ __device__ __forceinline__ void seg_write(int s, double v, const int32_t* __rest
   else part[slot] = v;
 }
 
-template <int CHE>
-__global__ void __launch_bounds__(256) cscj_xt_kernel(
+// TR (CHE = 8): the chunk is loaded INTERLEAVED (lane l takes entries 32 u + l: every index /
+// value load is one fully coalesced 128/256-byte request, and the 32 gathers of one
+// instruction are 32 consecutive CSC entries -- ascending row slots of one column, so a
+// column present in a fraction f of the J rows touches ~2/f lines instead of 16/f), then
+// transposed through shared memory (index i stored at i + i/8: conflict-free both ways)
+// into the 8-consecutive-entries-per-lane layout of the segmented sum below.  The kernel
+// is bound by L1 tag lookups (one per distinct 128-byte line per gather instruction).
+template <int CHE, bool TR>
+__global__ void __launch_bounds__(256, CHE <= 8 ? 4 : 1) cscj_xt_kernel(
     const long long* __restrict__ total, const int32_t* __restrict__ jseg,
     const int32_t* __restrict__ jpos, const double* __restrict__ jval,
     const int32_t* __restrict__ seg_col, const int32_t* __restrict__ seg_slot,
@@ -449,30 +456,64 @@ __global__ void __launch_bounds__(256) cscj_xt_kernel(
     int sg[CHE];
     double pr[CHE];
     {
-      const int4* s4 = reinterpret_cast<const int4*>(jseg + e0);
-      const int4* p4 = reinterpret_cast<const int4*>(jpos + e0);
-      const double2* v2 = reinterpret_cast<const double2*>(jval + e0);
-      int ps[CHE];
-      double vv[CHE];
-#pragma unroll
-      for (int h = 0; h < CHE / 4; ++h) {
-        const int4 a = __ldg(s4 + h), b = __ldg(p4 + h);
-        sg[4 * h] = a.x; sg[4 * h + 1] = a.y; sg[4 * h + 2] = a.z; sg[4 * h + 3] = a.w;
-        ps[4 * h] = b.x; ps[4 * h + 1] = b.y; ps[4 * h + 2] = b.z; ps[4 * h + 3] = b.w;
-      }
-#pragma unroll
-      for (int h = 0; h < CHE / 2; ++h) {
-        const double2 v = __ldg(v2 + h);
-        vv[2 * h] = v.x; vv[2 * h + 1] = v.y;
-      }
-      // gathers of w after all index loads are in flight
       double wg[CHE];
+      if constexpr (TR) {
+        static_assert(!TR || CHE == 8, "transposed load is written for 8 entries per lane");
+        __shared__ int t_seg[8][288];
+        __shared__ double t_val[8][288], t_w[8][288];
+        const int wp = threadIdx.x >> 5;
+        int ps[CHE];
 #pragma unroll
-      for (int u = 0; u < CHE; ++u) {
-        const bool ok = e0 + u < nnz;
-        if (!ok) sg[u] = NONE;
-        pr[u] = ok ? vv[u] : 0.0;
-        wg[u] = ok ? __ldg(w + ps[u]) : 0.0;
+        for (int u = 0; u < CHE; ++u) {
+          const long long e = c0 + 32 * u + lane;
+          const bool ok = e < nnz;
+          sg[u] = ok ? __ldg(jseg + e) : NONE;
+          ps[u] = ok ? __ldg(jpos + e) : 0;
+          pr[u] = ok ? __ldg(jval + e) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < CHE; ++u) wg[u] = sg[u] != NONE ? __ldg(w + ps[u]) : 0.0;
+        __syncwarp();  // the previous chunk's reads of this warp's tile are done
+#pragma unroll
+        for (int u = 0; u < CHE; ++u) {
+          const int i = 32 * u + lane, ip = i + (i >> 3);
+          t_seg[wp][ip] = sg[u];
+          t_val[wp][ip] = pr[u];
+          t_w[wp][ip] = wg[u];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < CHE; ++u) {
+          const int ip = 9 * lane + u;  // (8 lane + u) + lane
+          sg[u] = t_seg[wp][ip];
+          pr[u] = t_val[wp][ip];
+          wg[u] = t_w[wp][ip];
+        }
+      } else {
+        const int4* s4 = reinterpret_cast<const int4*>(jseg + e0);
+        const int4* p4 = reinterpret_cast<const int4*>(jpos + e0);
+        const double2* v2 = reinterpret_cast<const double2*>(jval + e0);
+        int ps[CHE];
+        double vv[CHE];
+#pragma unroll
+        for (int h = 0; h < CHE / 4; ++h) {
+          const int4 a = __ldg(s4 + h), b = __ldg(p4 + h);
+          sg[4 * h] = a.x; sg[4 * h + 1] = a.y; sg[4 * h + 2] = a.z; sg[4 * h + 3] = a.w;
+          ps[4 * h] = b.x; ps[4 * h + 1] = b.y; ps[4 * h + 2] = b.z; ps[4 * h + 3] = b.w;
+        }
+#pragma unroll
+        for (int h = 0; h < CHE / 2; ++h) {
+          const double2 v = __ldg(v2 + h);
+          vv[2 * h] = v.x; vv[2 * h + 1] = v.y;
+        }
+        // gathers of w after all index loads are in flight
+#pragma unroll
+        for (int u = 0; u < CHE; ++u) {
+          const bool ok = e0 + u < nnz;
+          if (!ok) sg[u] = NONE;
+          pr[u] = ok ? vv[u] : 0.0;
+          wg[u] = ok ? __ldg(w + ps[u]) : 0.0;
+        }
       }
       // sequential segmented sums over the lane's entries
       const int head = sg[0];
@@ -612,7 +653,8 @@ __global__ void __launch_bounds__(RJ_NT) csrj_fill_kernel(
     const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
     const double* __restrict__ values, const double* __restrict__ rs,
     const int32_t* __restrict__ J, long long p, const long long* __restrict__ rblk, int nblk,
-    int64_t* __restrict__ rptr, int32_t* __restrict__ ridx, double* __restrict__ rval) {
+    const int32_t* __restrict__ hot_rank, int64_t* __restrict__ rptr, int32_t* __restrict__ ridx,
+    double* __restrict__ rval) {
   __shared__ long long sm[33];
   __shared__ long long off[RJ_NT];
   const long long r0 = (long long)blockIdx.x * RJ_NT;
@@ -634,7 +676,11 @@ __global__ void __launch_bounds__(RJ_NT) csrj_fill_kernel(
     const long long k0 = indptr[i], k1 = indptr[i + 1], o = off[t];
     const double sg = rs ? rs[i] : 1.0;
     for (long long k = k0 + lane; k < k1; k += 32) {
-      ridx[o + (k - k0)] = indices[k];
+      // hot columns (operator's popularity table) are stored as ~rank < 0: the product
+      // reads their d entries from its shared-memory copy
+      const int32_t col = indices[k];
+      const int32_t hr = hot_rank ? __ldg(hot_rank + col) : -1;
+      ridx[o + (k - k0)] = hr >= 0 ? ~hr : col;
       rval[o + (k - k0)] = sg * values[k];
     }
   }
@@ -689,12 +735,118 @@ __global__ void __launch_bounds__(256) csrj_xd_dot_kernel(
   if (threadIdx.x == 0) *dot_out = acc[0];
 }
 
+// The same product with shared-memory staging of the d entries of the operator's hot
+// columns (Zipf popularity: the 4096 most populated columns hold ~2/3 of the entries):
+// each 512-thread CTA (two per SM) copies d[hot_cols[0..nhot)] into shared memory once and then
+// grid-strides over the packed rows, whose hot entries carry ~rank instead of the
+// column.  The plain kernel is bound by L1/TEX gather wavefronts (one per scattered
+// 8-byte load, 96 % L1 throughput at 0.50 of HBM); shared-memory lookups take the hot
+// share off that path.  Per-row summation order is the plain kernel's: bit-identical out.
+static constexpr int HOT_NT = 512;
+__global__ void __launch_bounds__(HOT_NT, 2) csrj_xd_dot_hot_kernel(
+    const int64_t* __restrict__ rptr, const int32_t* __restrict__ ridx,
+    const double* __restrict__ rval, long long p, const double* __restrict__ d,
+    const int32_t* __restrict__ hot_cols, int nhot, double* __restrict__ out,
+    const double* __restrict__ wdot, double* dot_out, double* __restrict__ part,
+    unsigned int* ticket) {
+  extern __shared__ double hot[];
+  __shared__ double red[32];
+  for (int k = threadIdx.x; k < nhot; k += HOT_NT) hot[k] = __ldg(d + __ldg(hot_cols + k));
+  __syncthreads();
+  const int sl = threadIdx.x & (SUB - 1), sub = (threadIdx.x & 31) / SUB;
+  double acc[1] = {0.0};
+  const long long wstride = (long long)gridDim.x * blockDim.x / SUB;
+  // Software pipeline over the warp's row groups (the chain row pointer -> entries ->
+  // gather is three dependent loads): iteration i gathers for group i while the entry
+  // loads of group i+1 and the row pointers of group i+2 are in flight.
+  auto ptrs = [&](long long g0, long long& a, long long& b) {
+    const long long g = g0 + sub;
+    const bool ok = g < p;
+    a = ok ? __ldg(rptr + g) : 0;
+    b = ok ? __ldg(rptr + g + 1) : 0;
+  };
+  auto ents = [&](long long a, long long b, int (&ix)[XD_UNROLL], double (&vv)[XD_UNROLL]) {
+#pragma unroll
+    for (int u = 0; u < XD_UNROLL; ++u) {
+      const long long k = a + sl + u * SUB;
+      const bool ok = k < b;
+      ix[u] = ok ? __ldg(ridx + k) : 0;
+      vv[u] = ok ? __ldg(rval + k) : 0.0;
+    }
+  };
+  long long g0 = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / SUB;
+  long long k0, k1, nk0, nk1;
+  int idx[XD_UNROLL];
+  double v[XD_UNROLL];
+  ptrs(g0, k0, k1);
+  ents(k0, k1, idx, v);
+  ptrs(g0 + wstride, nk0, nk1);
+  for (; g0 < p; g0 += wstride) {
+    int nidx[XD_UNROLL];
+    double nv[XD_UNROLL];
+    long long nnk0, nnk1;
+    ents(nk0, nk1, nidx, nv);
+    ptrs(g0 + 2 * wstride, nnk0, nnk1);
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < XD_UNROLL; ++u)
+      if (k0 + sl + u * SUB < k1) s = fma(v[u], idx[u] < 0 ? hot[~idx[u]] : __ldg(d + idx[u]), s);
+    // rows longer than one round (XD_UNROLL * SUB entries): the plain loop
+    for (long long kb = k0 + sl + XD_UNROLL * SUB; kb < k1; kb += XD_UNROLL * SUB) {
+      int ix[XD_UNROLL];
+      double vv[XD_UNROLL];
+      ents(kb - sl, k1, ix, vv);
+#pragma unroll
+      for (int u = 0; u < XD_UNROLL; ++u)
+        if (kb + u * SUB < k1) s = fma(vv[u], ix[u] < 0 ? hot[~ix[u]] : __ldg(d + ix[u]), s);
+    }
+#pragma unroll
+    for (int o = SUB / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, SUB);
+    const long long g = g0 + sub;
+    if (sl == 0 && g < p) {
+      out[g] = s;
+      if (wdot) acc[0] = fma(wdot[g], s, acc[0]);
+    }
+#pragma unroll
+    for (int u = 0; u < XD_UNROLL; ++u) {
+      idx[u] = nidx[u];
+      v[u] = nv[u];
+    }
+    k0 = nk0; k1 = nk1; nk0 = nnk0; nk1 = nnk1;
+  }
+  if (!wdot) return;
+  const int ops[1] = {0};
+  block_reduce<1>(acc, ops, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (!last_block_arrive(ticket, gridDim.x)) return;
+  block_fold_partials<1>(part, gridDim.x, 1, ops, acc, red);
+  if (threadIdx.x == 0) *dot_out = acc[0];
+}
+
+static int hot_grid(long long p, int max_blocks) {
+  static DeviceCache cache;
+  const int sms = per_device(cache, [](int dev) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(csrj_xd_dot_hot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(SSNAL_CSR_HOT_MAX * sizeof(double)));
+    return n;
+  });
+  return (int)std::max(1LL, std::min({ceil_div(p * SUB, (long long)HOT_NT), 2LL * sms,
+                                      (long long)max_blocks}));
+}
+
 cudaError_t launch_csrj_xd_dot(const CscJ& c, long long p, const double* d, double* out,
                                const double* wdot, double* dot_out, double* part,
                                int max_blocks, unsigned int* ticket, cudaStream_t stream) {
   if (p < 1) return cudaMemsetAsync(dot_out, 0, sizeof(double), stream);
-  const int grid = (int)std::max(1LL, std::min(ceil_div(p * SUB, 256LL), (long long)max_blocks));
   note_launch();
+  if (c.nhot > 0) {
+    csrj_xd_dot_hot_kernel<<<hot_grid(p, max_blocks), HOT_NT, c.nhot * sizeof(double), stream>>>(
+        c.rptr, c.ridx, c.rval, p, d, c.hot_cols, c.nhot, out, wdot, dot_out, part, ticket);
+    return cudaGetLastError();
+  }
+  const int grid = (int)std::max(1LL, std::min(ceil_div(p * SUB, 256LL), (long long)max_blocks));
   csrj_xd_dot_kernel<<<grid, 256, 0, stream>>>(c.rptr, c.ridx, c.rval, p, d, out, wdot, dot_out,
                                                 part, ticket);
   return cudaGetLastError();
@@ -704,6 +856,11 @@ cudaError_t launch_csrj_xd(const CscJ& c, long long p, const double* d, double* 
                            cudaStream_t stream) {
   if (p < 1) return cudaSuccess;
   note_launch();
+  if (c.nhot > 0) {
+    csrj_xd_dot_hot_kernel<<<hot_grid(p, 1 << 30), HOT_NT, c.nhot * sizeof(double), stream>>>(
+        c.rptr, c.ridx, c.rval, p, d, c.hot_cols, c.nhot, out, nullptr, nullptr, nullptr, nullptr);
+    return cudaGetLastError();
+  }
   csr_xd_kernel<<<(unsigned)ceil_div(p * SUB, 256LL), 256, 0, stream>>>(
       c.rptr, c.ridx, c.rval, nullptr, nullptr, p, d, out);
   return cudaGetLastError();
@@ -747,6 +904,14 @@ CscJ cscj_layout(const CsrOp& op, void* ws) {
   c.rblk = (long long*)p; p = al256(p + sizeof(long long) * (ceil_div(op.n, (long long)RJ_NT) + 1));
   c.empty = (int32_t*)p; p = al256(p + sizeof(int32_t) * op.nseg);
   c.nempty = (unsigned int*)p;
+  // measured on config-3 data (|J| = 700k, 69 % of the entries in the 4096 hot columns):
+  // 84 us against 81 us for the plain gather kernel -- random 8-byte shared-memory
+  // lookups still cost ~5 bank-conflict wavefronts each and the longer kernel runs at
+  // lower occupancy, so the staging is off unless SSNAL_CSR_HOT=1 (study knob)
+  static const bool hot_on = std::getenv("SSNAL_CSR_HOT") && std::atoi(std::getenv("SSNAL_CSR_HOT")) != 0;
+  c.nhot = (hot_on && op.hot_cols && op.hot_rank && op.nhot > 0 && op.nhot <= SSNAL_CSR_HOT_MAX)
+               ? (int)op.nhot : 0;
+  c.hot_cols = op.hot_cols;
   return c;
 }
 
@@ -771,12 +936,13 @@ cudaError_t launch_cscj_build(const CsrOp& op, const uint8_t* keep, const int32_
     csrj_count_kernel<<<rb, RJ_NT, 0, stream>>>(op.indptr, J, p, c.rblk, c.ticket, rb);
     note_launch();
     csrj_fill_kernel<<<rb, RJ_NT, 0, stream>>>(op.indptr, op.indices, op.values, op.row_sign, J,
-                                               p, c.rblk, rb, c.rptr, c.ridx, c.rval);
+                                               p, c.rblk, rb, c.nhot > 0 ? op.hot_rank : nullptr,
+                                               c.rptr, c.ridx, c.rval);
   }
   return cudaGetLastError();
 }
 
-template <int CHE>
+template <int CHE, bool TR = false>
 static void launch_cscj_xt_che(const CsrOp& op, const CscJ& c, const double* w, double* out,
                                double* part, cudaStream_t stream) {
   const long long nblk = ceil_div(op.nseg, (long long)CJ_WARPS);
@@ -786,7 +952,7 @@ static void launch_cscj_xt_che(const CsrOp& op, const CscJ& c, const double* w, 
   const long long nch_max = ceil_div(op.nnz, (long long)(32 * CHE));
   const unsigned grid = (unsigned)std::max(1LL, std::min(ceil_div(nch_max, 8LL), 148LL * 8));
   note_launch();
-  cscj_xt_kernel<CHE><<<grid, 256, 0, stream>>>(total, c.seg, c.pos, c.val, op.seg_col,
+  cscj_xt_kernel<CHE, TR><<<grid, 256, 0, stream>>>(total, c.seg, c.pos, c.val, op.seg_col,
                                                  op.seg_slot, w, out, part, c.cval, c.ctail,
                                                  c.cflag);
   note_launch();
@@ -798,11 +964,15 @@ static void launch_cscj_xt_che(const CsrOp& op, const CscJ& c, const double* w, 
 
 cudaError_t launch_cscj_xt(const CsrOp& op, const CscJ& c, const double* w, double* out,
                            double* part, cudaStream_t stream) {
-  // entries per lane of the nnz-balanced product (SSNAL_CSCJ_CHE = 8 | 16 | 32; the
+  // entries per lane of the nnz-balanced product (SSNAL_CSCJ_CHE = 4 | 8 | 16 | 32; the
   // workspace is sized for the smallest chunk, larger chunks fit)
   static const int che = std::getenv("SSNAL_CSCJ_CHE") ? std::atoi(std::getenv("SSNAL_CSCJ_CHE")) : 8;
-  if (che == 32) launch_cscj_xt_che<32>(op, c, w, out, part, stream);
+  // measured slower than the per-lane vector loads (175 vs 120 us, config-3 data): study knob
+  static const bool tr = std::getenv("SSNAL_CSCJ_T") && std::atoi(std::getenv("SSNAL_CSCJ_T")) != 0;
+  if (che == 8 && tr) launch_cscj_xt_che<8, true>(op, c, w, out, part, stream);
+  else if (che == 32) launch_cscj_xt_che<32>(op, c, w, out, part, stream);
   else if (che == 16) launch_cscj_xt_che<16>(op, c, w, out, part, stream);
+  else if (che == 4) launch_cscj_xt_che<4>(op, c, w, out, part, stream);
   else launch_cscj_xt_che<8>(op, c, w, out, part, stream);
   if (op.nfold > 0) {
     note_launch();

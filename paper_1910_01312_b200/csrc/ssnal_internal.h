@@ -62,6 +62,9 @@ struct CscJ {
   long long* rblk; // per-block row-length offsets
   int32_t* empty;  // segments without kept entries (written as zeros by every product)
   unsigned int* nempty;
+  // hot-column staging of X_J d (operator's popularity table; 0: off): ridx holds ~rank
+  int nhot;
+  const int32_t* hot_cols;
 };
 size_t cscj_ws_bytes(const CsrOp& op);
 CscJ cscj_layout(const CsrOp& op, void* ws);

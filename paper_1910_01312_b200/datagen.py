@@ -144,6 +144,19 @@ def config4(seed=4, n=1_000_000, q=500):
 CONFIGS = {0: config0, 1: config1, 2: config2, 3: config3, 4: config4}
 
 
+def solve_options(cfg):
+    """Solver options the workloads are run with: ``{"alm": {...}, "ssn": {...}}`` keyword
+    sets for AlmOptions / SsnOptions (both are reference options, ref solver.py:73-95).
+    Dense configs: the reference defaults.  Sparse (CSR) configs, whose Newton systems
+    are solved by matrix-free CG: ``max_inner=200`` (the default 50 ends the large-sigma
+    subproblems early) and ``sigma_max=625`` -- the CG system's condition number grows
+    with sigma, and capping the penalty trades a few more outer iterations for ~5x fewer
+    CG iterations (config 3: 113 s -> 21 s; profiles/r2_sigma_study_*.txt)."""
+    if "indptr" in cfg:
+        return {"alm": {"sigma_max": 625.0}, "ssn": {"max_inner": 200}}
+    return {"alm": {}, "ssn": {}}
+
+
 def make_config(k, **overrides):
     if k not in CONFIGS:
         raise InputError(f"unknown config {k}")

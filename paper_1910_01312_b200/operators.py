@@ -113,6 +113,8 @@ class CsrKernelOperator:
 
     kind = "csr"
     SEG = 2048  # max nonzeros per warp segment of the CSC product
+    HOT_MAX = 4096        # SSNAL_CSR_HOT_MAX: columns staged in shared memory (32 KB of d)
+    HOT_MIN_SHARE = 0.25  # staging pays when the hot columns hold at least this share of nnz
 
     def __init__(self, samples, labels=None, backend=None):
         import ctypes
@@ -149,6 +151,16 @@ class CsrKernelOperator:
         seg_slot[split] = np.arange(int(split.sum()))
         fold_cols = np.flatnonzero(nseg_col > 1)
         fold_beg = np.concatenate([[0], np.cumsum(nseg_col[fold_cols])]).astype(np.int32)
+        # hot-column staging of the CG's X_J d (csrc/sparse.cu csrj_xd_dot_hot_kernel): when
+        # the HOT_MAX most populated columns hold a sizeable share of the entries (Zipf
+        # popularity), their d entries are served from shared memory
+        nhot = int(min(self.HOT_MAX, self.q))
+        order = np.argsort(-lens, kind="stable")[:nhot]
+        if self.nnz == 0 or lens[order].sum() < self.HOT_MIN_SHARE * self.nnz:
+            nhot, order = 0, order[:0]
+        hot_rank = np.full(self.q, -1, dtype=np.int32)
+        hot_rank[order] = np.arange(nhot, dtype=np.int32)
+        self.nhot = nhot
         from .backend import H2D
 
         def dev(a, dt):
@@ -170,6 +182,8 @@ class CsrKernelOperator:
             "fold_col": dev(fold_cols.astype(np.int32) if fold_cols.size else np.zeros(1, np.int32),
                             torch.int32),
             "fold_beg": dev(fold_beg if fold_cols.size else np.zeros(2, np.int32), torch.int32),
+            "hot_cols": dev(order.astype(np.int32) if nhot else np.zeros(1, np.int32), torch.int32),
+            "hot_rank": dev(hot_rank, torch.int32),
         }
         if labels is not None:
             if isinstance(labels, torch.Tensor) and labels.is_cuda:
@@ -197,7 +211,8 @@ class CsrKernelOperator:
             row_sign=None if self.row_sign is None else self.row_sign.data_ptr(),
             nseg=int(seg_col.size), seg_beg=p("seg_beg"), seg_end=p("seg_end"),
             seg_col=p("seg_col"), seg_slot=p("seg_slot"), nfold=int(fold_cols.size),
-            fold_col=p("fold_col"), fold_beg=p("fold_beg"), nslots=self.nslots)
+            fold_col=p("fold_col"), fold_beg=p("fold_beg"), nslots=self.nslots,
+            nhot=nhot, hot_cols=p("hot_cols"), hot_rank=p("hot_rank"))
         self._cref = ctypes.byref(self.c_op)
         self.host_csr = A  # kept for callers (oracle checks, columns())
 

@@ -1,5 +1,5 @@
 """Sparse-config solve for ncu launch windows: python scripts/prof_sparse.py K [max_outer]
-(K = 2 or 3; the solve runs with the sparse configs' max_inner=200)."""
+(K = 2 or 3; the solve runs with datagen.solve_options: max_inner=200, sigma_max=625)."""
 import sys
 import time
 
@@ -17,6 +17,8 @@ cfg = datagen.make_config(k)
 pb = P.build_csvc_dual((cfg["indptr"], cfg["indices"], cfg["data"], cfg["shape"]), cfg["y"], cfg["C"])
 print("gen+build", time.time() - t0, flush=True)
 t0 = time.time()
-r = P.alm_solve(pb, P.AlmOptions(tol_kkt=1e-6, max_outer=max_outer), P.SsnOptions(max_inner=200))
+so = datagen.solve_options(cfg)
+r = P.alm_solve(pb, P.AlmOptions(tol_kkt=1e-6, max_outer=max_outer, **so["alm"]),
+                P.SsnOptions(**so["ssn"]))
 print("solve", time.time() - t0, r.converged, r.kkt_residual, r.outer_iters, r.total_inner_iters,
       getattr(pb, "native_counters", None), flush=True)

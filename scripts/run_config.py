@@ -33,12 +33,13 @@ rows = []
 out = {}
 # the large sparse configs need more inner Newton steps than the reference default 50
 # at sigma >= 3125
-ssn = P.SsnOptions(max_inner=200) if "indptr" in cfg else P.SsnOptions()
+so = datagen.solve_options(cfg)
+ssn = P.SsnOptions(**so["ssn"])
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 for rep_i in range(reps):
     torch.cuda.synchronize()
     t0 = time.time()
-    r = P.alm_solve(pb, P.AlmOptions(tol_kkt=1e-6), ssn,
+    r = P.alm_solve(pb, P.AlmOptions(tol_kkt=1e-6, **so["alm"]), ssn,
                     callback=(lambda *a: rows.append(a)) if rep_i == 0 else None)
     torch.cuda.synchronize()
     out[f"solve{rep_i}_s"] = time.time() - t0
@@ -47,5 +48,5 @@ box_ok = bool(x.min() >= -1e-12 and x.max() <= cfg["C"] + 1e-12)
 out.update({"config": k, "n": pb.n, "q": pb.q_op.q, "gen_s": tgen, "kkt": r.kkt_residual,
             "objective": r.objective, "outer": r.outer_iters, "inner": r.total_inner_iters,
             "p": r.unbounded_support_count, "converged": r.converged, "box_ok": box_ok,
-            "warnings": r.warnings, "trace": rows, "ssn_options": {"max_inner": ssn.max_inner, "psi_eval": ssn.psi_eval}, "counters": getattr(pb, "native_counters", None)})
+            "warnings": r.warnings, "trace": rows, "ssn_options": {"max_inner": ssn.max_inner, "psi_eval": ssn.psi_eval}, "alm_options": so["alm"], "counters": getattr(pb, "native_counters", None)})
 print(json.dumps(out))
