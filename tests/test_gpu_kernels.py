@@ -357,6 +357,25 @@ def test_csr_restricted_products(pkg, keep_frac):
         assert torch.equal(z2, zo[:p])
 
 
+def test_csr_study_knob_kernels():
+    """The measured-and-left-off variants of the CG products stay
+    correct: SSNAL_CSR_HOT=1 (shared-memory staging of the hot columns' d entries in X_J d,
+    bit-identical to the plain kernel) and SSNAL_CSCJ_T=1 (interleaved loads transposed
+    through shared memory in X_J^T w).  The knobs are read once per process, so the
+    restricted-product tests run again in a child process with both set."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SSNAL_CSR_HOT="1", SSNAL_CSCJ_T="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_kernels.py"),
+                        "-q", "-x", "-m", "gpu", "-k", "test_csr_restricted_products"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "5 passed" in r.stdout, r.stdout[-1000:]
+
+
 @pytest.mark.parametrize("shape,svr,aligned", [((3001, 300), False, True), ((2000, 51), False, False),
                                                 ((1500, 64), True, True)])
 def test_fused_gradient_and_direction_epilogue(pkg, shape, svr, aligned):
