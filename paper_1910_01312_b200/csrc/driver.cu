@@ -133,7 +133,10 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
                             double* xp, const double* txj, uint8_t* fr, const uint8_t* tfj,
                             double* s, const double* t, double* xw, double* xpi, double* r,
                             double* part, const ProjState* st_src, ProjState* st_dst,
-                            cudaStream_t stream, double* dsum = nullptr);
+                            cudaStream_t stream, double* dsum = nullptr, const double* gt = nullptr,
+                            const double* m1 = nullptr, const double* avec = nullptr);
+cudaError_t launch_gram_tvec(const double* G, long long q, const double* t, double* out,
+                             cudaStream_t stream);
 
 // direct reduced systems of the sparse operator: min(p, q) up to this size (M buffer)
 constexpr long long SPARSE_DIRECT_MAX = 2048;
@@ -161,6 +164,11 @@ static double cg_eta_cap() {
 cudaError_t launch_cg_update(long long p, double* y, double* r, double* pv, const double* zq,
                              const double* aJ, double asa, double sigma, const double* dinv,
                              double* Ap, double* z, double* cgs, double* part, cudaStream_t s);
+// SSNAL_ACCEPT_LIN=0: the accept pass gathers the rows of every changed slot (A/B knob)
+static bool accept_lin() {
+  static const bool v = !(std::getenv("SSNAL_ACCEPT_LIN") && std::atoi(std::getenv("SSNAL_ACCEPT_LIN")) == 0);
+  return v;
+}
 // SSNAL_CG_FUSED=0: the unfused cg_ap / cg_step / cg_dir launches (A/B knob)
 static bool cg_fused() {
   static const bool v = !(std::getenv("SSNAL_CG_FUSED") && std::atoi(std::getenv("SSNAL_CG_FUSED")) == 0);
@@ -252,7 +260,7 @@ struct Layout {
   double *gr, *t, *M, *m1, *scal;
   // dense operator, factor-space gradient: r = t + q (t2 = [t ; r]), X^T w, X^T Pi(u),
   // accept partials; qdir and grad are adjacent ([Qd ; grad] from one X sweep)
-  double *r, *xw, *xpi, *qpart;
+  double *r, *xw, *xpi, *qpart, *gt;
   uint8_t *fr, *tfree;
   int32_t* J;
   long long* pcount;
@@ -320,6 +328,7 @@ Layout carve(char* base, long long n, long long n_phys, long long q, size_t* tot
     L.gctl = cv.take<GramCtl>(1);
   }
   L.m1 = cv.take<double>(q);
+  L.gt = cv.take<double>(q);
   {  // contiguous read-back blob (see BLOB_ST)
     char* blob = cv.take<char>(BLOB_BYTES);
     L.scal = reinterpret_cast<double*>(blob);
@@ -1030,10 +1039,14 @@ struct Driver {
   }
 
   bool slope_ok = false;  // ws_grad + 128 holds a_J'(Qd)_J of the current direction
+  // the kept Gram G / m1 describe the CURRENT free set and the direction is the Newton
+  // one (Qd = X t): the accept pass may use the linear update over the staying free slots
+  bool lin_ok = false;
 
   void direction(long long p, double asa, const double* g2_dev) {
     tdir = L.t;
     slope_ok = false;
+    lin_ok = false;
     if (p == 0) {  // Sigma = 0: d = -s, Qd = -grad (ref solver.py:221-222)
       if (qgrad()) {  // grad = X r (one sweep, ||grad||^2 folded); t = X^T d = -r
         timed(SSNAL_OP_XD, a_bytes() + 8.0 * (P.n + P.q), [&] {
@@ -1110,6 +1123,7 @@ struct Driver {
       const double* asa_dev = &L.st_cur->sum_a2_free;
       // gathered rows: bytes and flops added once the row count is known (gram_rows)
       timed(SSNAL_OP_GRAM, 0.0, [&] { gram(); });
+      lin_ok = accept_lin();
       const double* G = L.G;
       const double* m1 = L.m1;
       if (sh()) {  // the kept Gram is this rank's rows; [G ; m1] summed over the ranks
@@ -1179,6 +1193,7 @@ struct Driver {
 
   void steepest(double out[4]) {
     slope_ok = false;
+    lin_ok = false;
     vec(4, -1.0, L.grad, nullptr, nullptr, L.dir);
     tdir = L.gr + P.q;
     xt({L.dir}, L.gr + P.q);
@@ -1297,13 +1312,16 @@ struct Driver {
     trace_resume();
     materialize(alpha, j);
     if (qgrad()) {  // + s, and X^T w, X^T Pi(u), r = X^T s updated from the changed slots
+      const bool lin = lin_ok && tdir == L.t && L.G != nullptr;
       timed(SSNAL_OP_VEC, 8.0 * P.n * 9 + 2.0 * P.n, [&] {
+        if (lin) ck(launch_gram_tvec(L.G, P.q, L.t, L.gt, S));
         ck(launch_accept_q(P.A, P.n_phys, P.q, P.lda, P.row_sign, P.svr_block, P.n, alpha,
                            -(sigma * alpha), L.w, L.dir, L.qw, L.qdir, L.u, L.xp,
                            L.tx + (size_t)j * P.n, L.fr, L.tfree + (size_t)j * P.n, L.s, tdir,
                            L.xw, L.xpi, L.r, L.qpart, L.st_trial + j, L.st_cur, S,
-                           sh() ? L.dsum : nullptr));
+                           sh() ? L.dsum : nullptr, lin ? L.gt : nullptr, L.m1, P.a));
       });
+      lin_ok = false;
       if (sh()) {  // X^T (Pi_new - Pi_old) summed over the ranks, then the factor update
         allsum(L.dsum, P.q);
         ck(launch_factor_update(P.q, alpha, tdir, L.dsum, L.xw, L.xpi, L.r, S));

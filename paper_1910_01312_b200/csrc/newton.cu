@@ -333,6 +333,13 @@ struct AcceptQArgs {
   // accepted trial's projection record -> current record (replaces a D2D memcpy)
   const ProjState* st_src;
   ProjState* st_dst;
+  // linear update over the slots free before AND after the step:
+  // there Pi_new - Pi_old = cu (Qd)_i - dlam a_i exactly, and their rows sum to
+  // cu G t - dlam m1 minus the leaving rows' share -- no row gathers for them.
+  // gt = G t (kept q-space Gram of the CURRENT free set times t), m1 = X_J^T a_J; NULL: off
+  const double* gt;
+  const double* m1;
+  const double* avec;
 };
 
 template <int NC>
@@ -341,9 +348,10 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
   __shared__ double dval[AQ_NT];
   __shared__ int wcnt[AQ_NT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (blockIdx.x == 0 && a.st_dst && tid < (int)(sizeof(ProjState) / sizeof(unsigned int)))
-    reinterpret_cast<unsigned int*>(a.st_dst)[tid] =
-        reinterpret_cast<const unsigned int*>(a.st_src)[tid];
+  // multiplier change of the accepted trial (st_dst still holds the old record: it is
+  // overwritten by the last CTA, after every CTA has read it)
+  const bool lin = a.gt != nullptr;
+  const double dlam = lin ? a.st_src->lam - a.st_dst->lam : 0.0;
   const long long chunk = ceil_div(ceil_div(a.n, (long long)gridDim.x), (long long)AQ_NT) * AQ_NT;
   const long long b0 = (long long)blockIdx.x * chunk, b1 = min(a.n, b0 + chunk);
   double acc[NC];
@@ -362,8 +370,14 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
       const double xn = a.txj[i];
       dpi = xn - a.xp[i];
       a.xp[i] = xn;
-      a.fr[i] = a.tfj[i];
+      const uint8_t f_old = a.fr[i], f_new = a.tfj[i];
+      a.fr[i] = f_new;
       a.s[i] = __dsub_rn(wn, xn);
+      if (lin && f_old) {
+        // free before: its linear share is inside cu G t - dlam m1; free after too:
+        // nothing left to gather, leaving: the difference to the actual change
+        dpi = f_new ? 0.0 : dpi - (a.cu * qdi - dlam * a.avec[i]);
+      }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, dpi != 0.0);
     if (lane == 0) wcnt[warp] = __popc(bal);
@@ -424,6 +438,9 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
   }
   if (tid == 0) a.touched[blockIdx.x] = any ? 1 : 0;
   if (!last_block_arrive(a.ticket, gridDim.x)) return;
+  if (a.st_dst && tid < (int)(sizeof(ProjState) / sizeof(unsigned int)))
+    reinterpret_cast<unsigned int*>(a.st_dst)[tid] =
+        reinterpret_cast<const unsigned int*>(a.st_src)[tid];
   // fold only the CTAs that saw a change (typically a handful), in block order
   // touched CTAs listed in block order: all flags loaded at once, ballot + warp prefix
   __shared__ int blist[148 * 8];
@@ -480,6 +497,7 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
       double sum = 0.0;
 #pragma unroll
       for (int w = 0; w < AQ_NT / 32; ++w) sum += wsum[w][tid];
+      if (lin) sum += a.cu * a.gt[c] - dlam * a.m1[c];
       if (a.dsum) {
         a.dsum[c] = sum;
       } else {
@@ -492,6 +510,33 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
     }
     __syncthreads();
   }
+}
+
+// out = G t for the kept q-space Gram (tile-symmetric storage of gram_kernel: the tile
+// (I, J) with I > J is stored transposed at (J, I); GT = 128), a warp per row, lanes stride
+// the columns, fixed shuffle tree
+static constexpr int GTV_TILE = 128;
+__global__ void __launch_bounds__(256) gram_tvec_kernel(const double* __restrict__ G, long long q,
+                                                        const double* __restrict__ t,
+                                                        double* __restrict__ out) {
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= q) return;
+  const long long ti = i / GTV_TILE;
+  double acc = 0.0;
+  for (long long j = lane; j < q; j += 32) {
+    const double g = (ti > j / GTV_TILE) ? __ldg(G + j * q + i) : __ldg(G + i * q + j);
+    acc = fma(g, __ldg(t + j), acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) out[i] = acc;
+}
+
+cudaError_t launch_gram_tvec(const double* G, long long q, const double* t, double* out,
+                             cudaStream_t stream) {
+  note_launch();
+  gram_tvec_kernel<<<(unsigned)ceil_div(q * 32, 256LL), 256, 0, stream>>>(G, q, t, out);
+  return cudaGetLastError();
 }
 
 int accept_q_grid(long long n) {
@@ -509,7 +554,8 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
                             double* xp, const double* txj, uint8_t* fr, const uint8_t* tfj,
                             double* s, const double* t, double* xw, double* xpi, double* r,
                             double* part, const ProjState* st_src, ProjState* st_dst,
-                            cudaStream_t stream, double* dsum) {
+                            cudaStream_t stream, double* dsum, const double* gt,
+                            const double* m1, const double* avec) {
   if (q > (long long)AQ_NT * AQ_MAXC) return cudaErrorInvalidValue;
   AcceptQArgs a;
   a.g = RowsArgs{A, n_phys, q, lda, rs, svr, nullptr, 0};
@@ -521,6 +567,8 @@ cudaError_t launch_accept_q(const double* A, long long n_phys, long long q, long
   a.part = (double*)((char*)part + 256 + 148 * 8 * sizeof(int));
   a.t = t; a.xw = xw; a.xpi = xpi; a.r = r; a.dsum = dsum;
   a.st_src = st_src; a.st_dst = st_dst;
+  a.gt = (gt && m1 && avec && st_src && st_dst) ? gt : nullptr;
+  a.m1 = m1; a.avec = avec;
   const int grid = accept_q_grid(n);
   const int nc = (int)ceil_div(q, (long long)AQ_NT);
   note_launch();
