@@ -344,9 +344,13 @@ struct AcceptQArgs {
 
 template <int NC>
 __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
-  __shared__ int list[AQ_NT];
-  __shared__ double dval[AQ_NT];
-  __shared__ int wcnt[AQ_NT / 32];
+  // changed slots of the CTA's chunk are collected over several 256-slot tiles (ascending
+  // slot order) and their rows gathered in one batch of 4-row rounds: one barrier per
+  // tile in the streaming part, and few single-row rounds when a tile has 1-3 changes
+  constexpr int LCAP = 1024;
+  __shared__ int list[LCAP];
+  __shared__ double dval[LCAP];
+  __shared__ int wcnt[2][AQ_NT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // multiplier change of the accepted trial (st_dst still holds the old record: it is
   // overwritten by the last CTA, after every CTA has read it)
@@ -357,7 +361,45 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
   double acc[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) acc[k] = 0.0;
-  int any = 0;
+  int any = 0, cnt = 0, par = 0;
+  // rows of list[0, cnt) added to acc in list order (the order of the sums is the slot
+  // order whatever the batching: results do not depend on LCAP)
+  auto flush = [&]() {
+    __syncthreads();
+    int k = 0;
+    for (; k + 4 <= cnt; k += 4) {
+      double sg[4], f[4], v[4][NC];
+      const double* row[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        row[u] = logical_row(a.g, b0 + list[k + u], sg[u]);
+        f[u] = dval[k + u] * sg[u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const long long col = tid + (long long)c * AQ_NT;
+          v[u][c] = col < a.g.q ? __ldg(row[u] + col) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = fma(f[u], v[u][c], acc[c]);
+    }
+    for (; k < cnt; ++k) {
+      double sg;
+      const double* row = logical_row(a.g, b0 + list[k], sg);
+      const double f = dval[k] * sg;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const long long col = tid + (long long)c * AQ_NT;
+        if (col < a.g.q) acc[c] = fma(f, __ldg(row + col), acc[c]);
+      }
+    }
+    __syncthreads();
+    cnt = 0;
+  };
   for (long long base = b0; base < b1; base += AQ_NT) {
     const long long i = base + tid;
     double dpi = 0.0;
@@ -380,55 +422,25 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
       }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, dpi != 0.0);
-    if (lane == 0) wcnt[warp] = __popc(bal);
+    if (lane == 0) wcnt[par][warp] = __popc(bal);
     __syncthreads();
     int off = 0, tot = 0;
 #pragma unroll
     for (int w = 0; w < AQ_NT / 32; ++w) {
-      off += w < warp ? wcnt[w] : 0;
-      tot += wcnt[w];
+      off += w < warp ? wcnt[par][w] : 0;
+      tot += wcnt[par][w];
     }
     if (dpi != 0.0) {
-      const int o = off + __popc(bal & ((1u << lane) - 1u));
+      const int o = cnt + off + __popc(bal & ((1u << lane) - 1u));
       list[o] = (int)(i - b0);
       dval[o] = dpi;
     }
-    __syncthreads();
+    cnt += tot;
     any |= tot;
-    // changed rows four at a time: their loads are in flight together
-    int k = 0;
-    for (; k + 4 <= tot; k += 4) {
-      double sg[4], f[4], v[4][NC];
-      const double* row[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        row[u] = logical_row(a.g, b0 + list[k + u], sg[u]);
-        f[u] = dval[k + u] * sg[u];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const long long col = tid + (long long)c * AQ_NT;
-          v[u][c] = col < a.g.q ? __ldg(row[u] + col) : 0.0;
-        }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) acc[c] = fma(f[u], v[u][c], acc[c]);
-    }
-    for (; k < tot; ++k) {
-      double sg;
-      const double* row = logical_row(a.g, b0 + list[k], sg);
-      const double f = dval[k] * sg;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const long long col = tid + (long long)c * AQ_NT;
-        if (col < a.g.q) acc[c] = fma(f, __ldg(row + col), acc[c]);
-      }
-    }
-    __syncthreads();
+    par ^= 1;
+    if (cnt + AQ_NT > LCAP) flush();
   }
+  if (__syncthreads_or(cnt)) flush();
   if (any) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -449,13 +461,13 @@ __global__ void __launch_bounds__(AQ_NT) accept_q_kernel(AcceptQArgs a) {
     const unsigned b = c0 + tid;
     const bool f = b < gridDim.x && __ldcg(a.touched + b) != 0;
     const unsigned bal = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) wcnt[warp] = __popc(bal);
+    if (lane == 0) wcnt[0][warp] = __popc(bal);
     __syncthreads();
     int off = m, tot = 0;
 #pragma unroll
     for (int w = 0; w < AQ_NT / 32; ++w) {
-      off += w < warp ? wcnt[w] : 0;
-      tot += wcnt[w];
+      off += w < warp ? wcnt[0][w] : 0;
+      tot += wcnt[0][w];
     }
     if (f) blist[off + __popc(bal & ((1u << lane) - 1u))] = (int)b;
     m += tot;
