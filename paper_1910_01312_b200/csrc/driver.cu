@@ -1287,8 +1287,6 @@ struct Driver {
           alpha_out = a;
           j_out = k;
           rec = H->st[k];
-          static const bool dbg_ls = std::getenv("SSNAL_DEBUG_LS") != nullptr;
-          if (dbg_ls) std::fprintf(stderr, "ls sigma=%g alpha=%g trials=%d\n", sigma, a, tried + k + 1);
           return true;
         }
       }
