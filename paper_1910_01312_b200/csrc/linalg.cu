@@ -453,15 +453,21 @@ __device__ __forceinline__ void bg_diag_step(double (&r)[BG_NB], int lane, doubl
   // 32 x 32 block); the buffer alternates by J parity, so one __syncwarp per column
   colbuf[J & 1][lane] = r[J];
   __syncwarp();
-#pragma unroll
-  for (int c = J + 1; c < BG_NB; ++c) {
-    const double lcj = colbuf[J & 1][c];
-    if (lane >= c) r[c] = fma(-r[J], lcj, r[c]);
-  }
-  // next pivot: lane J+1's updated diagonal entry
   if constexpr (J + 1 < BG_NB) {
-    bg_diag_step<J + 1>(r, lane, rd, k0, fail, __shfl_sync(0xffffffffu, r[J + 1], J + 1),
-                        colbuf);
+    // column J+1 first and the next pivot fetched right away: the pivot chain (shuffle ->
+    // rsqrt -> scale -> store -> broadcast) is the critical path, the updates of the
+    // columns past J+1 are independent of it and fill its latency
+    {
+      const double lcj = colbuf[J & 1][J + 1];
+      if (lane >= J + 1) r[J + 1] = fma(-r[J], lcj, r[J + 1]);
+    }
+    const double dnext = __shfl_sync(0xffffffffu, r[J + 1], J + 1);
+#pragma unroll
+    for (int c = J + 2; c < BG_NB; ++c) {
+      const double lcj = colbuf[J & 1][c];
+      if (lane >= c) r[c] = fma(-r[J], lcj, r[c]);
+    }
+    bg_diag_step<J + 1>(r, lane, rd, k0, fail, dnext, colbuf);
   }
 }
 
@@ -533,19 +539,17 @@ __global__ void __launch_bounds__(BG_NT) chol_big_kernel(double* __restrict__ M,
       // block's (unused) strict upper triangle of M: the panel TRSM becomes a DMMA
       // product and both substitutions become matrix-vector products -- no 32-step
       // shuffle chains outside the factorization itself
+      // right-looking order: as soon as col[t] is known every later partial sum takes its
+      // term (independent FMAs), so the dependent chain is one FMA + one multiply per row
+      // instead of the whole row sum; each sum still adds its terms in ascending t
       double col[BG_NB];
 #pragma unroll
-      for (int i = 0; i < BG_NB; ++i) {
-        if (i < lane) {
-          col[i] = 0.0;
-        } else if (i == lane) {
-          col[i] = rd[i];
-        } else {
-          double sacc = 0.0;
+      for (int i = 0; i < BG_NB; ++i) col[i] = 0.0;
 #pragma unroll
-          for (int t = 0; t < i; ++t) sacc = fma(D[i][t], col[t], sacc);
-          col[i] = -sacc * rd[i];
-        }
+      for (int t = 0; t < BG_NB; ++t) {
+        col[t] = t < lane ? 0.0 : (t == lane ? rd[t] : -col[t] * rd[t]);
+#pragma unroll
+        for (int i = t + 1; i < BG_NB; ++i) col[i] = fma(D[i][t], col[t], col[i]);
       }
       __syncwarp();
 #pragma unroll
