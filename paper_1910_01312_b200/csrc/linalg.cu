@@ -786,9 +786,7 @@ cudaError_t launch_chol_solve(double* M, long long m, const double* b, double sc
     int mi = (int)m;
     void* args[] = {&M, &mi, (void*)&b, &scale, &x, &info};
     note_launch();
-    static const int grid_env = std::getenv("SSNAL_CHOL_GRID") ? std::atoi(std::getenv("SSNAL_CHOL_GRID")) : 0;
-    const int grid_sz = grid_env > 0 ? std::min(grid_env, big_grid()) : big_grid();
-    return cudaLaunchCooperativeKernel((void*)chol_big_kernel, dim3(grid_sz), dim3(BG_NT), args,
+    return cudaLaunchCooperativeKernel((void*)chol_big_kernel, dim3(big_grid()), dim3(BG_NT), args,
                                        0, stream);
   }
   size_t smem = (size_t)(NB * (NB + 1) + PANEL_ROWS * (NB + 1)) * sizeof(double);
