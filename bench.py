@@ -431,6 +431,34 @@ def run_ours(args, rank, world, local_rank):
         sampler.sample()
     launches = (be.launch_count() - launches0) // max(args.steps, 1)
     barrier()
+    # informational: the same workload with a tuned penalty schedule (reference options
+    # sigma0 / sigma_max, datagen.tuned_alm_options); the headline keeps the defaults
+    tuned = None
+    from paper_1910_01312_b200 import datagen as _dg
+
+    topt = _dg.tuned_alm_options(cfg) if not sharded else None
+    if topt:
+        t_opts = P.AlmOptions(tol_kkt=TOL, **topt)
+        for _ in range(2):
+            P.alm_solve(problem, t_opts, ssn, return_device=True)
+        ts = []
+        for _ in range(min(args.steps, 5)):
+            flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            trep = P.alm_solve(problem, t_opts, ssn, return_device=True)
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        tuned = {"options": topt, "value": float(np.mean(ts)), "unit": "s", "steps": len(ts),
+                 "result": {"kkt": trep.kkt_residual, "objective": trep.objective,
+                            "outer": trep.outer_iters, "inner": trep.total_inner_iters,
+                            "converged": trep.converged},
+                 "note": "not the headline: AlmOptions(sigma0, sigma_max) tuned for this workload; "
+                         "value / e2e / cpu_baseline / reference arm all run the reference defaults"}
+        del trep
+        barrier()
     t = torch.tensor([float(np.sum(step_s))], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -561,6 +589,7 @@ def run_ours(args, rank, world, local_rank):
                    "outer": last.outer_iters, "inner": last.total_inner_iters,
                    "p": last.unbounded_support_count, "converged": last.converged},
         "counters": counters,
+        "tuned_schedule": tuned,
         "step_ms": [round(t_ * 1e3, 3) for t_ in step_s],
         "median_ms": round(float(np.median(step_s)) * 1e3, 3),
     }

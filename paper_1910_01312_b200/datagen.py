@@ -157,6 +157,19 @@ def solve_options(cfg):
     return {"alm": {}, "ssn": {}}
 
 
+def tuned_alm_options(cfg):
+    """A faster penalty schedule for the dense eps-SVR workload (config 4), or None: start
+    at sigma0 = 125 and stop growing at sigma_max = 15625 (both reference options).  The
+    first outer iterations of the default schedule (sigma = 1, 5, 25) run with 3-6 x 10^5
+    free slots and pay for large Gram rebuilds; the last ones (sigma >= 78125) pass the
+    Armijo test only at step lengths ~1e-7.  Config 4: 5 outer / 39 inner iterations instead
+    of 8 / 62, objective equal to 3e-8 relative (profiles/r2_sigma_study_config4*.txt).
+    bench.py reports it BESIDE the headline, which stays on the reference defaults."""
+    if "indptr" not in cfg and cfg.get("task") == "svr":
+        return {"sigma0": 125.0, "sigma_max": 15625.0}
+    return None
+
+
 def make_config(k, **overrides):
     if k not in CONFIGS:
         raise InputError(f"unknown config {k}")
