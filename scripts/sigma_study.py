@@ -17,11 +17,15 @@ if sys.argv[1] == "c2":  # config 2 at full size
     cfg = datagen.config2()
 elif sys.argv[1] == "c4":  # config 4 (dense eps-SVR) at full size
     cfg = datagen.config4()
+elif sys.argv[1] == "c1":  # config 1 (dense C-SVC 50,000 x 300)
+    cfg = datagen.config1()
 else:
     scale = float(sys.argv[1])
     cfg = datagen.config3(n=int(4_000_000 * scale), q=int(1_000_000 * scale))
 if cfg["task"] == "svr":
     pb = P.build_svr_dual(cfg["A"], cfg["t"], cfg["C"], cfg["epsilon"])
+elif "A" in cfg:
+    pb = P.build_csvc_dual(cfg["A"], cfg["y"], cfg["C"])
 else:
     pb = P.build_csvc_dual((cfg["indptr"], cfg["indices"], cfg["data"], cfg["shape"]), cfg["y"], cfg["C"])
 ssn = P.SsnOptions(**datagen.solve_options(cfg)["ssn"])
