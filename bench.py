@@ -258,7 +258,7 @@ def cpu_baseline_solve(args):
         return secs, rep, (f"one full solve of the workload ({what}); longer than the 10-30 s "
                            "sample guidance because no bounded sub-sample of an ALM solve "
                            "scales to the full one")
-    full = datagen.make_config.__globals__["CONFIGS"][args.config]
+    full = datagen.CONFIGS[args.config]
     import inspect
 
     sig = inspect.signature(full).parameters
