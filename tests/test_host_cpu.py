@@ -69,3 +69,48 @@ def test_batched_line_search_picks_reference_alpha(mods):
         rep = solver.alm_solve(pb, solver.AlmOptions(tol_kkt=c["tol"]),
                                solver.SsnOptions(line_search_batch=batch))
         assert (rep.outer_iters, rep.total_inner_iters) == (c["outer"], c["inner"])
+
+
+def test_workload_solve_options_are_reference_options():
+    """datagen.solve_options / tuned_alm_options only name fields of the reference-shaped
+    AlmOptions / SsnOptions (ref solver.py:73-95) and leave the dense configs on the
+    defaults; the oracle's option classes accept the same keywords (bench.py feeds both
+    arms from one table)."""
+    import dataclasses
+
+    import oracle as O
+    from paper_1910_01312_b200 import datagen, solver
+
+    alm_fields = {f.name for f in dataclasses.fields(solver.AlmOptions)}
+    ssn_fields = {f.name for f in dataclasses.fields(solver.SsnOptions)}
+    sparse = datagen.solve_options({"indptr": None})
+    assert set(sparse["alm"]) <= alm_fields and set(sparse["ssn"]) <= ssn_fields
+    assert sparse["alm"]["sigma_max"] == 625.0 and sparse["ssn"]["max_inner"] == 200
+    O.AlmOpts(tol_kkt=1e-6, **sparse["alm"])
+    O.SsnOpts(newton="factor", **sparse["ssn"])
+    for cfg in ({"A": None, "task": "csvc"}, {"A": None, "task": "svr"}):
+        assert datagen.solve_options(cfg) == {"alm": {}, "ssn": {}}
+    assert datagen.tuned_alm_options({"A": None, "task": "csvc"}) is None
+    assert datagen.tuned_alm_options({"indptr": None, "task": "csvc"}) is None
+    tuned = datagen.tuned_alm_options({"A": None, "task": "svr"})
+    assert set(tuned) <= alm_fields
+    solver.AlmOptions(tol_kkt=1e-6, **tuned)
+
+
+def test_bench_cpu_sample_shapes():
+    """bench.py's bounded CPU sample of the sparse configs scales n and q of the SAME
+    generator (no oracle solve here)."""
+    import inspect
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_1910_01312_b200 import datagen
+
+    for k, div in bench.CPU_SAMPLE_DIV.items():
+        sig = inspect.signature(datagen.CONFIGS[k]).parameters
+        n, q = sig["n"].default // div, sig["q"].default // div
+        assert n >= 10_000 and q >= 1_000
+    small = datagen.make_config(3, n=2000, q=500)
+    assert small["shape"] == (2000, 500) and small["indptr"][-1] == small["indices"].size
